@@ -1,0 +1,170 @@
+/*
+ * stmg_b200 — C ABI of the B200-native hp space-time multigrid hot path
+ * (arXiv 2502.09159): matrix-free space-time operator, additive Vanka
+ * smoothers, hp transfers, V-cycle, right-preconditioned GMRES and time
+ * marching for 2D instationary Stokes, Q_{r+1}/P_r^disc x DG(k), FP64.
+ *
+ * Every entry point replaces one interface of the reference C++ library
+ * (/root/reference/proj, cited per function). The reference binds these as
+ * std::function callbacks (ApplyFn / PrecondFn, include/stmg/solver.hpp:70-71)
+ * consumed by gmres() and time_march(); INTEGRATION.md shows the adapter.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Functions without a `_host` suffix take
+ *    DEVICE pointers and are ordered on the context's CUDA stream
+ *    (stmg_ctx_set_stream); `_host` variants take host pointers and block.
+ *  - Vectors use the reference BlockVector layout (block_vector.hpp:13-45):
+ *    one interval = [V^1..V^{k+1}, P^1..P^{k+1}], V^a = [comp 0 | comp 1] on
+ *    the global GLL grid (node id iy*grid_x + ix), P^a cell-blocked
+ *    (cell*n_p + mode). N intervals are stored interval-major.
+ *  - Status codes (no exceptions cross the ABI):
+ *      0 STMG_OK, 1 STMG_EINVAL  (reference: std::invalid_argument),
+ *      2 STMG_ERUNTIME (reference: std::runtime_error — singular matrix,
+ *        caps, GMRES non-convergence), 3 STMG_ECUDA.
+ *    stmg_last_error() returns the message of the calling thread's last
+ *    failure.
+ */
+#ifndef STMG_B200_H
+#define STMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STMG_OK 0
+#define STMG_EINVAL 1
+#define STMG_ERUNTIME 2
+#define STMG_ECUDA 3
+
+#define STMG_SMOOTHER_NONE (-1)
+#define STMG_SMOOTHER_CELL 0        /* SmootherKind::cell        (vanka.hpp:15-19) */
+#define STMG_SMOOTHER_VERTEX_STAR 1 /* SmootherKind::vertex_star (vanka.hpp:15-19) */
+
+typedef struct stmg_ctx stmg_ctx;
+typedef struct stmg_level stmg_level;
+typedef struct stmg_solver stmg_solver;
+
+const char *stmg_last_error(void);
+/* Library version string, e.g. "stmg_b200 0.1 sm_100a". */
+const char *stmg_version(void);
+
+/* ------------------------------------------------------------ context */
+int stmg_ctx_create(int device, stmg_ctx **out);
+int stmg_ctx_destroy(stmg_ctx *ctx);
+/* cudaStream_t passed as void*; NULL selects the legacy default stream. */
+int stmg_ctx_set_stream(stmg_ctx *ctx, void *cuda_stream);
+int stmg_ctx_synchronize(stmg_ctx *ctx);
+/* Number of kernels this context has launched so far (evidence counter). */
+int64_t stmg_ctx_launch_count(const stmg_ctx *ctx);
+
+/* ------------------------------------------------------------ one level
+ * SpaceTimeBlockOperator (st_operator.hpp:94-165) + VankaSmoother
+ * (vanka.hpp:45-89) on an nx x ny Cartesian mesh of the unit square, with
+ * Q_{r+1}/P_r^disc in space, DG(k) on intervals of length tau, viscosity nu
+ * and grad-div coefficient gamma. smoother_kind: STMG_SMOOTHER_*.
+ * r in 1..4, k in 0..4. */
+int stmg_level_create(stmg_ctx *ctx, int nx, int ny, int r, int k, double tau, double nu, double gamma,
+                      int smoother_kind, stmg_level **out);
+int stmg_level_destroy(stmg_level *level);
+/* out[0..7] = n_slots, M^v, M^p, interval size, n_scalar, grid_x,
+ * n_patch_classes, sum over patches of n_T^2 (total_matrix_elements,
+ * vanka.cpp:235-243). */
+int stmg_level_sizes(const stmg_level *level, int64_t *out);
+
+/* y_n = D x_n for each of n_intervals independent intervals
+ * (apply_block, raw=0: Dirichlet elimination, st_operator.cpp:397-401;
+ *  apply_block_raw, raw=1: st_operator.cpp:403-407). */
+int stmg_apply_block(stmg_level *level, const double *x, double *y, int n_intervals, int raw);
+
+/* All-at-once operator of Eq. GloSys:
+ *   y_n = D x_n - Z C x_{n-1}[slot k]        n = 0..n_intervals-1
+ * with C the DG jump coupling (coupling_rhs, st_operator.cpp:409-421) and Z
+ * zeroing constrained rows. x_prev_slot (M^v doubles, may be NULL) is the
+ * velocity of slot k of the interval preceding x (the time-slab halo). */
+int stmg_vmult(stmg_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);
+
+/* r = b - A x with A = stmg_vmult's operator (coupled=1) or the per-interval
+ * apply_block (coupled=0). */
+int stmg_residual(stmg_level *level, const double *b, const double *x, double *r, int n_intervals,
+                  const double *x_prev_slot, int coupled);
+
+/* out = coupling_rhs(v_prev) for one interval (st_operator.cpp:409-421). */
+int stmg_coupling_rhs(stmg_level *level, const double *v_prev, double *out);
+
+/* out = sum_T R_T^T w_T (R_T S R_T^T)^{-1} R_T r per interval
+ * (VankaSmoother::apply_additive, vanka.cpp:196-215). */
+int stmg_apply_additive(stmg_level *level, const double *r, double *out, int n_intervals);
+
+/* u <- u + omega * apply_additive(b - A u) (VankaSmoother::smooth_step,
+ * vanka.cpp:217-233); A as in stmg_residual. omega must lie in (0, 1]
+ * (else STMG_EINVAL, vanka.cpp:223-224). `work` is a caller buffer of
+ * n_intervals interval sizes (may be NULL: the level allocates one). */
+int stmg_smooth_step(stmg_level *level, const double *b, double *u, double omega, int n_intervals,
+                     const double *x_prev_slot, int coupled, double *work);
+
+/* Host-buffer variants of stmg_vmult / stmg_smooth_step: copy in, run,
+ * copy out, synchronise (the end-to-end path a CPU caller binds). */
+int stmg_vmult_host(stmg_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);
+int stmg_smooth_step_host(stmg_level *level, const double *b, double *u, double omega, int n_intervals,
+                          const double *x_prev_slot, int coupled);
+
+/* ------------------------------------------------------------ solver
+ * build_setup + VCycle + gmres + time_march (harness.cpp:26-70,
+ * solver.cpp:56-325) on the 2^refinements x 2^refinements unit-square mesh:
+ * hp hierarchy (spatial p-halving then h-doubling to 1x1; temporal k -> 1),
+ * or h-only when h_only != 0. k < 0 selects k = r; n_steps <= 0 selects
+ * tau = t_end / 2^(refinements+1) (harness.cpp:16-24). The coarse level is
+ * solved on the GPU with a dense inverse of the pinned operator. */
+int stmg_solver_create(stmg_ctx *ctx, int refinements, int r, int k, int n_steps, double t_end, double nu,
+                       double gamma, int smoother_kind, int nu1, int nu2, double omega, int h_only, double rtol,
+                       double atol, int max_iterations, stmg_solver **out);
+int stmg_solver_destroy(stmg_solver *solver);
+/* out[0] = n_levels, out[1] = n_steps, then per level l (coarse first):
+ * out[2+5l..] = nx, r, k, kind_to_coarser (TransferKind, transfer.hpp:15-23),
+ * interval size. */
+int stmg_solver_info(const stmg_solver *solver, int64_t *out);
+/* Borrowed handle of level l (0 = coarsest); owned by the solver. */
+stmg_level *stmg_solver_level(stmg_solver *solver, int l);
+
+/* TransferPair::restrict_residual / prolongate_correction between level l
+ * and l-1 (transfer.cpp:102-132), one interval. prolongate writes
+ * (accumulate=0) or adds (accumulate=1) into fine. */
+int stmg_restrict_residual(stmg_solver *solver, int l, const double *fine, double *coarse, int project_pressure);
+int stmg_prolongate_correction(stmg_solver *solver, int l, const double *coarse, double *fine,
+                               int project_pressure, int accumulate);
+/* CoarseSolver::solve (solver.cpp:43-54) on level 0. */
+int stmg_coarse_solve(stmg_solver *solver, const double *b, double *x);
+/* x = VCycle::apply(b) (solver.cpp:63-93), finest level, one interval. */
+int stmg_vcycle(stmg_solver *solver, const double *b, double *x);
+/* Right-preconditioned GMRES (solver.cpp:95-202) of apply_block x = b with
+ * the V-cycle, x0 = 0. iterations/converged/residual history as GmresResult.
+ * Returns STMG_ERUNTIME if not converged. */
+int stmg_gmres(stmg_solver *solver, const double *b, double *x, int *iterations, double *residual_history,
+               int history_cap);
+/* time_march (solver.cpp:204-325) with zero initial velocity, homogeneous
+ * Dirichlet data and a per-step load vector F_n (n_steps intervals,
+ * interval-major) added to the right-hand side; writes the trajectory X
+ * (n_steps intervals, pressure projected mean-zero per slot) and the GMRES
+ * iterations of each step. */
+int stmg_time_march(stmg_solver *solver, const double *F, double *X, int *iterations);
+int stmg_time_march_host(stmg_solver *solver, const double *F, double *X, int *iterations);
+
+/* ------------------------------------------------------------ host-only
+ * Setup queries that need no GPU (used by the CPU test tier).
+ * stmg_plan_levels: the level table of plan_hierarchy/combine_hierarchies
+ * (harness.cpp:26-42, hierarchy.cpp:9-97) in the stmg_solver_info layout.
+ * stmg_patch_info: Vanka patches of one level: out[0] n_patches, out[1]
+ * n_classes, out[2] sum n_T^2, out[3] n_colours, out[4+c] n_T of class c
+ * (c < 60). If inverse_out is non-NULL, the dense (pseudo-)inverse of class
+ * `class_index` (n_T x n_T, row-major) is written there. */
+int stmg_plan_levels(int refinements, int r, int k, int n_steps, double t_end, int h_only, int64_t *out);
+int stmg_patch_info(int nx, int ny, int r, int k, double tau, double nu, double gamma, int smoother_kind,
+                    int64_t *out, double *inverse_out, int class_index);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STMG_B200_H */

@@ -1,0 +1,317 @@
+"""stmg_b200 — B200-native hot path of the hp space-time multigrid Stokes
+solver of arXiv 2502.09159 (matrix-free space-time operator, additive Vanka
+smoothers, hp transfers, V-cycle, GMRES, time marching; FP64, sm_100a).
+
+This module is a thin ctypes binding of the C ABI in ``include/stmg_b200.h``
+(``_build/libstmg_b200.so``). The names mirror the reference interfaces
+(/root/reference/proj/include/stmg/st_operator.hpp, vanka.hpp, transfer.hpp,
+solver.hpp). Device vectors are torch float64 CUDA tensors (plumbing only);
+every computation runs in the library's CUDA kernels. There is no CPU
+fallback: if the library is missing or the device is not a CUDA GPU, calls
+raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+from typing import Optional, Sequence
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_build" / "libstmg_b200.so"
+HEADER_PATH = _PKG.parent / "include" / "stmg_b200.h"
+
+SMOOTHER_NONE = -1
+SMOOTHER_CELL = 0
+SMOOTHER_VERTEX_STAR = 1
+
+TRANSFER_KINDS = ["identity", "h_space", "p_space", "p_time", "h_space+p_time", "p_space+p_time"]
+
+
+class StmgError(RuntimeError):
+    """Raised for non-zero status codes (1 invalid argument, 2 runtime, 3 CUDA)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"stmg_b200 error {code}: {msg}")
+        self.code = code
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+_c_int, _c_double, _c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_SIGNATURES = {
+    "stmg_last_error": ([], ctypes.c_char_p),
+    "stmg_version": ([], ctypes.c_char_p),
+    "stmg_ctx_create": ([_c_int, ctypes.POINTER(_c_void_p)], _c_int),
+    "stmg_ctx_destroy": ([_c_void_p], _c_int),
+    "stmg_ctx_set_stream": ([_c_void_p, _c_void_p], _c_int),
+    "stmg_ctx_synchronize": ([_c_void_p], _c_int),
+    "stmg_ctx_launch_count": ([_c_void_p], ctypes.c_int64),
+    "stmg_level_create": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
+                           ctypes.POINTER(_c_void_p)], _c_int),
+    "stmg_level_destroy": ([_c_void_p], _c_int),
+    "stmg_level_sizes": ([_c_void_p, _c_i64p], _c_int),
+    "stmg_apply_block": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int], _c_int),
+    "stmg_vmult": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
+    "stmg_residual": ([_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, _c_int], _c_int),
+    "stmg_coupling_rhs": ([_c_void_p, _c_void_p, _c_void_p], _c_int),
+    "stmg_apply_additive": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
+    "stmg_smooth_step": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int, _c_void_p], _c_int),
+    "stmg_vmult_host": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
+    "stmg_smooth_step_host": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int], _c_int),
+    "stmg_solver_create": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
+                            _c_int, _c_int, _c_double, _c_int, _c_double, _c_double, _c_int,
+                            ctypes.POINTER(_c_void_p)], _c_int),
+    "stmg_solver_destroy": ([_c_void_p], _c_int),
+    "stmg_solver_info": ([_c_void_p, _c_i64p], _c_int),
+    "stmg_solver_level": ([_c_void_p, _c_int], _c_void_p),
+    "stmg_restrict_residual": ([_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int], _c_int),
+    "stmg_prolongate_correction": ([_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int], _c_int),
+    "stmg_coarse_solve": ([_c_void_p, _c_void_p, _c_void_p], _c_int),
+    "stmg_vcycle": ([_c_void_p, _c_void_p, _c_void_p], _c_int),
+    "stmg_gmres": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_double), _c_int],
+                   _c_int),
+    "stmg_time_march": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
+    "stmg_time_march_host": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
+    "stmg_plan_levels": ([_c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _c_i64p], _c_int),
+    "stmg_patch_info": ([_c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int, _c_i64p,
+                         ctypes.POINTER(_c_double), _c_int], _c_int),
+}
+
+
+def load_library(path: Optional[os.PathLike] = None) -> ctypes.CDLL:
+    """Load (once) the in-tree CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(f"stmg_b200: CUDA library {p} missing — run __graft_entry__.build() "
+                           "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(code: int) -> None:
+    if code != 0:
+        raise StmgError(code, load_library().stmg_last_error().decode())
+
+
+def _ptr(t) -> Optional[int]:
+    """Device pointer of a contiguous float64 CUDA tensor (None passes NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda or t.dtype.itemsize != 8 or not t.is_contiguous():
+        raise ValueError("stmg_b200 expects contiguous float64 CUDA tensors")
+    return t.data_ptr()
+
+
+def _hptr(a) -> Optional[int]:
+    """Host pointer of a C-contiguous float64 numpy array (None passes NULL)."""
+    if a is None:
+        return None
+    if a.dtype.itemsize != 8 or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("stmg_b200 expects C-contiguous float64 host arrays")
+    return a.ctypes.data
+
+
+class Context:
+    """CUDA device + stream the library launches on (torch's current stream by default)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+
+        lib = load_library()
+        h = _c_void_p()
+        _check(lib.stmg_ctx_create(device, ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        _check(lib.stmg_ctx_set_stream(h, _c_void_p(s.cuda_stream)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def synchronize(self) -> None:
+        _check(load_library().stmg_ctx_synchronize(self._h))
+
+    def launch_count(self) -> int:
+        return int(load_library().stmg_ctx_launch_count(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.stmg_ctx_destroy(self._h)
+            self._h = None
+
+
+class Level:
+    """SpaceTimeBlockOperator + VankaSmoother of one Cartesian level
+    (st_operator.hpp:94-165, vanka.hpp:45-89)."""
+
+    def __init__(self, ctx: Context, nx: int, ny: int, r: int, k: int, tau: float, nu: float,
+                 gamma: float = 0.0, smoother: int = SMOOTHER_CELL, _borrowed=None):
+        self.ctx = ctx
+        lib = load_library()
+        if _borrowed is not None:
+            self._h = _borrowed
+            self._owned = False
+        else:
+            h = _c_void_p()
+            _check(lib.stmg_level_create(ctx.handle, nx, ny, r, k, tau, nu, gamma, smoother, ctypes.byref(h)))
+            self._h = h
+            self._owned = True
+        out = (ctypes.c_int64 * 8)()
+        _check(lib.stmg_level_sizes(self._h, out))
+        (self.n_slots, self.n_velocity, self.n_pressure, self.size, self.n_scalar, self.grid_x,
+         self.n_patch_classes, self.total_matrix_elements) = [int(v) for v in out]
+
+    # -- operator
+    def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
+        _check(load_library().stmg_apply_block(self._h, _ptr(x), _ptr(y), n_intervals, int(raw)))
+        return y
+
+    def apply_block_raw(self, x, y, n_intervals: int = 1):
+        return self.apply_block(x, y, n_intervals, raw=True)
+
+    def vmult(self, x, y, n_intervals: int = 1, x_prev_slot=None):
+        _check(load_library().stmg_vmult(self._h, _ptr(x), _ptr(y), n_intervals, _ptr(x_prev_slot)))
+        return y
+
+    def residual(self, b, x, r, n_intervals: int = 1, x_prev_slot=None, coupled: bool = True):
+        _check(load_library().stmg_residual(self._h, _ptr(b), _ptr(x), _ptr(r), n_intervals, _ptr(x_prev_slot),
+                                            int(coupled)))
+        return r
+
+    def coupling_rhs(self, v_prev, out):
+        _check(load_library().stmg_coupling_rhs(self._h, _ptr(v_prev), _ptr(out)))
+        return out
+
+    # -- smoother
+    def apply_additive(self, residual, out, n_intervals: int = 1):
+        _check(load_library().stmg_apply_additive(self._h, _ptr(residual), _ptr(out), n_intervals))
+        return out
+
+    def smooth_step(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False,
+                    work=None):
+        _check(load_library().stmg_smooth_step(self._h, _ptr(b), _ptr(u), omega, n_intervals, _ptr(x_prev_slot),
+                                               int(coupled), _ptr(work)))
+        return u
+
+    # -- host-buffer (end-to-end) variants
+    def vmult_host(self, x, y, n_intervals: int = 1, x_prev_slot=None):
+        _check(load_library().stmg_vmult_host(self._h, _hptr(x), _hptr(y), n_intervals, _hptr(x_prev_slot)))
+        return y
+
+    def smooth_step_host(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False):
+        _check(load_library().stmg_smooth_step_host(self._h, _hptr(b), _hptr(u), omega, n_intervals,
+                                                    _hptr(x_prev_slot), int(coupled)))
+        return u
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and getattr(self, "_h", None) and _lib is not None:
+            _lib.stmg_level_destroy(self._h)
+            self._h = None
+
+
+class Solver:
+    """build_setup + VCycle + gmres + time_march (harness.cpp:26-70, solver.cpp:56-325)."""
+
+    def __init__(self, ctx: Context, refinements: int, r: int, k: int = -1, n_steps: int = 0, t_end: float = 1.0,
+                 nu: float = 0.1, gamma: float = 1.0, smoother: int = SMOOTHER_CELL, nu1: int = 1, nu2: int = 1,
+                 omega: float = 0.8, h_only: bool = False, rtol: float = 1e-8, atol: float = 1e-14,
+                 max_iterations: int = 200):
+        self.ctx = ctx
+        lib = load_library()
+        h = _c_void_p()
+        _check(lib.stmg_solver_create(ctx.handle, refinements, r, k, n_steps, t_end, nu, gamma, smoother, nu1, nu2,
+                                      omega, int(h_only), rtol, atol, max_iterations, ctypes.byref(h)))
+        self._h = h
+        out = (ctypes.c_int64 * (2 + 5 * 64))()
+        _check(lib.stmg_solver_info(h, out))
+        self.n_levels, self.n_steps = int(out[0]), int(out[1])
+        self.level_info = [dict(nx=int(out[2 + 5 * l]), r=int(out[3 + 5 * l]), k=int(out[4 + 5 * l]),
+                                kind=TRANSFER_KINDS[int(out[5 + 5 * l])], size=int(out[6 + 5 * l]))
+                           for l in range(self.n_levels)]
+        self.levels = [Level(ctx, 0, 0, 0, 0, 0, 0, _borrowed=lib.stmg_solver_level(h, l))
+                       for l in range(self.n_levels)]
+        self.finest = self.levels[-1]
+
+    def restrict_residual(self, l: int, fine, coarse, project_pressure: bool = True):
+        _check(load_library().stmg_restrict_residual(self._h, l, _ptr(fine), _ptr(coarse), int(project_pressure)))
+        return coarse
+
+    def prolongate_correction(self, l: int, coarse, fine, project_pressure: bool = True, accumulate: bool = False):
+        _check(load_library().stmg_prolongate_correction(self._h, l, _ptr(coarse), _ptr(fine),
+                                                         int(project_pressure), int(accumulate)))
+        return fine
+
+    def coarse_solve(self, b, x):
+        _check(load_library().stmg_coarse_solve(self._h, _ptr(b), _ptr(x)))
+        return x
+
+    def vcycle(self, b, x):
+        _check(load_library().stmg_vcycle(self._h, _ptr(b), _ptr(x)))
+        return x
+
+    def gmres(self, b, x, history_cap: int = 256):
+        it = _c_int(0)
+        hist = (ctypes.c_double * history_cap)()
+        code = load_library().stmg_gmres(self._h, _ptr(b), _ptr(x), ctypes.byref(it), hist, history_cap)
+        _check(code)
+        return int(it.value), [hist[i] for i in range(min(history_cap, it.value + 1))]
+
+    def time_march(self, F, X):
+        iters = (ctypes.c_int * self.n_steps)()
+        _check(load_library().stmg_time_march(self._h, _ptr(F), _ptr(X), iters))
+        return [int(v) for v in iters]
+
+    def time_march_host(self, F, X):
+        iters = (ctypes.c_int * self.n_steps)()
+        _check(load_library().stmg_time_march_host(self._h, _hptr(F), _hptr(X), iters))
+        return [int(v) for v in iters]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.stmg_solver_destroy(self._h)
+            self._h = None
+
+
+def plan_levels(refinements: int, r: int, k: int = -1, n_steps: int = 0, t_end: float = 1.0,
+                h_only: bool = False) -> dict:
+    """Host-only hierarchy plan (plan_hierarchy + combine_hierarchies)."""
+    out = (ctypes.c_int64 * (2 + 5 * 64))()
+    _check(load_library().stmg_plan_levels(refinements, r, k, n_steps, t_end, int(h_only), out))
+    n = int(out[0])
+    return dict(n_steps=int(out[1]),
+                levels=[dict(nx=int(out[2 + 5 * l]), r=int(out[3 + 5 * l]), k=int(out[4 + 5 * l]),
+                             kind=TRANSFER_KINDS[int(out[5 + 5 * l])], size=int(out[6 + 5 * l]))
+                        for l in range(n)])
+
+
+def patch_info(nx: int, ny: int, r: int, k: int, tau: float, nu: float, gamma: float, smoother: int):
+    """Host-only Vanka patch statistics: dict(n_patches, n_classes, sum_nt2, n_t per class, inverses...)."""
+    out = (ctypes.c_int64 * 64)()
+    _check(load_library().stmg_patch_info(nx, ny, r, k, tau, nu, gamma, smoother, out, None, 0))
+    n_classes = int(out[1])
+    return dict(n_patches=int(out[0]), n_classes=n_classes, sum_nt2=int(out[2]), n_colours=int(out[3]),
+                class_sizes=[int(out[4 + i]) for i in range(min(n_classes, 60))])
+
+
+def exported_symbols() -> Sequence[str]:
+    """Function names declared in include/stmg_b200.h."""
+    import re
+
+    text = HEADER_PATH.read_text()
+    return sorted(set(re.findall(r"\b(stmg_[a-z_0-9]+)\s*\(", text)))
+
+
+__all__ = ["Context", "Level", "Solver", "StmgError", "load_library", "plan_levels", "patch_info",
+           "exported_symbols", "SMOOTHER_CELL", "SMOOTHER_VERTEX_STAR", "SMOOTHER_NONE"]

@@ -1,0 +1,76 @@
+// Device-side data views and kernel launchers of the B200 hp-STMG path.
+#pragma once
+
+#include "level_consts.cuh"
+
+#include <algorithm>
+#include <cuda_runtime.h>
+
+namespace stmg_b200
+{
+
+/// Geometry of one level as the auxiliary kernels see it.
+struct DevGeom
+{
+  int nx, ny, gx, gy, S, np;
+  long long nsc, mv, mp, isz;
+  double hx, hy;
+};
+
+struct DevCsr
+{
+  const int *ptr;
+  const int *col;
+  const double *val;
+};
+
+/// One TransferPair on the device (transfer.hpp:33-96).
+struct DevTransfer
+{
+  int spatial, temporal, pmode, zero_constrained;
+  DevCsr px, py, rx, ry;
+  const double *child; // pmode 1: 4 blocks np x np
+  const int *embed;    // pmode 2
+  double E[kMaxS * kMaxS]; // E[a*kMaxS+b], fine slot a, coarse slot b
+  DevGeom f, c;
+};
+
+/// Device view of one Vanka patch class (setup.hpp PatchClass).
+struct DevPatchClass
+{
+  int n_t, n_vel;
+  const long long *rel;  // n_t offsets from the velocity / pressure anchor
+  const double *weight;  // n_t valence weights
+  const double *inverse; // n_t x n_t row-major
+};
+
+/// One Vanka block's work item: a run of same-class patches of one colour.
+struct VankaBatch
+{
+  int cls;   // class index
+  int first; // index into the anchor arrays
+  int count; // <= vanka_cols_per_batch()
+};
+
+cudaError_t launch_vmult(int r, int S, const LevelConsts &P, const double *x, const double *b, double *y,
+                         int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t stream);
+cudaError_t launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, int n_batches, int max_nt,
+                                const long long *vel_anchor, const long long *pre_anchor, const double *r, double *u,
+                                long long isz, int n_intervals, double omega, cudaStream_t stream);
+int vanka_cols_per_batch();
+cudaError_t launch_prolongate(const DevTransfer &T, const double *coarse, double *fine, int n_intervals,
+                              int accumulate, cudaStream_t st);
+cudaError_t launch_restrict(const DevTransfer &T, const double *fine, double *coarse, int n_intervals,
+                            cudaStream_t st);
+cudaError_t launch_project_mean_zero(const DevGeom &G, double *x, int n_intervals, cudaStream_t st);
+cudaError_t launch_zero_constrained(const DevGeom &G, double *x, int n_intervals, cudaStream_t st);
+cudaError_t launch_coarse_solve(const double *inv, const long long *pinned, int n_pinned, int nrows, const double *b,
+                                double *x, cudaStream_t st);
+int dot_partials();
+cudaError_t launch_dot(const double *x, const double *y, long long n, double *part, double *out, cudaStream_t st);
+cudaError_t launch_axpy(long long n, double alpha, const double *alpha_dev, double sign, const double *x, double *y,
+                        cudaStream_t st);
+cudaError_t launch_scale(long long n, double alpha, double *y, cudaStream_t st);
+cudaError_t launch_xpby(long long n, const double *x, double beta, double *y, cudaStream_t st);
+
+} // namespace stmg_b200

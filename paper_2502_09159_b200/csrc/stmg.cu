@@ -1,0 +1,995 @@
+// C ABI (include/stmg_b200.h) and host orchestration of the B200 hp-STMG
+// path: levels, smoother colour sweeps, V-cycle, FGMRES and time marching.
+// Mirrors the reference's operator/smoother/transfer/solver interfaces
+// (st_operator.hpp, vanka.hpp, transfer.hpp, solver.hpp) on device vectors.
+#include "../../include/stmg_b200.h"
+#include "kernels.hpp"
+#include "setup.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace stmg_b200;
+
+namespace
+{
+thread_local std::string g_error;
+
+struct CudaError : std::runtime_error
+{
+  using std::runtime_error::runtime_error;
+};
+
+void
+check(cudaError_t e, const char *what)
+{
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int
+guarded(F &&f)
+{
+  try
+    {
+      f();
+      return STMG_OK;
+    }
+  catch (const std::invalid_argument &e)
+    {
+      g_error = e.what();
+      return STMG_EINVAL;
+    }
+  catch (const CudaError &e)
+    {
+      g_error = e.what();
+      return STMG_ECUDA;
+    }
+  catch (const std::exception &e)
+    {
+      g_error = e.what();
+      return STMG_ERUNTIME;
+    }
+}
+
+/// Owning device array.
+template <class T>
+struct DevArray
+{
+  T *p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  DevArray(const DevArray &) = delete;
+  DevArray &operator=(const DevArray &) = delete;
+  DevArray(DevArray &&o) noexcept : p(o.p), n(o.n)
+  {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  ~DevArray()
+  {
+    if (p)
+      cudaFree(p);
+  }
+  void
+  resize(size_t count)
+  {
+    if (count <= n)
+      return;
+    if (p)
+      cudaFree(p);
+    p = nullptr;
+    n = 0;
+    check(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)), "cudaMalloc");
+    n = count;
+  }
+  void
+  upload(const std::vector<T> &h)
+  {
+    resize(h.size());
+    if (!h.empty())
+      check(cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice), "upload");
+  }
+};
+} // namespace
+
+// ================================================================ context
+struct stmg_ctx
+{
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  void
+  count(int k = 1)
+  {
+    launches += k;
+  }
+};
+
+// ================================================================ level
+struct stmg_level
+{
+  stmg_ctx *ctx = nullptr;
+  LevelSpec spec;
+  LevelConsts consts{};
+  DevGeom geom{};
+  int smoother_kind = STMG_SMOOTHER_NONE;
+  // Vanka
+  std::vector<DevArray<long long>> cls_rel;
+  std::vector<DevArray<double>> cls_weight, cls_inverse;
+  DevArray<DevPatchClass> classes;
+  DevArray<VankaBatch> batches;
+  DevArray<long long> vel_anchor, pre_anchor;
+  std::vector<int> colour_first, colour_count;
+  int max_nt = 0;
+  int n_classes = 0;
+  std::uint64_t total_matrix_elements = 0;
+  // scratch
+  DevArray<double> work, zeros, host_in, host_out, host_prev;
+
+  void
+  vmult(const double *x, const double *b, double *y, int n, const double *xprev0, int coupled, int mode)
+  {
+    check(launch_vmult(spec.r, spec.S(), consts, x, b, y, n, xprev0, coupled, mode, ctx->stream), "vmult");
+    ctx->count();
+  }
+
+  /// u += omega * sum over colours of the patch corrections of residual r.
+  void
+  vanka(const double *r, double *u, int n, double omega)
+  {
+    if (smoother_kind == STMG_SMOOTHER_NONE)
+      throw std::invalid_argument("level has no smoother");
+    for (size_t c = 0; c < colour_first.size(); ++c)
+      if (colour_count[c] > 0)
+        {
+          check(launch_vanka_colour(classes.p, batches.p + colour_first[c], colour_count[c], max_nt, vel_anchor.p,
+                                    pre_anchor.p, r, u, spec.isz(), n, omega, ctx->stream),
+                "vanka");
+          ctx->count();
+        }
+  }
+
+  double *
+  scratch(int n)
+  {
+    work.resize(static_cast<size_t>(spec.isz()) * n);
+    return work.p;
+  }
+
+  const double *
+  zero_vector(int n)
+  {
+    const size_t need = static_cast<size_t>(spec.isz()) * n;
+    if (zeros.n < need)
+      {
+        zeros.resize(need);
+        check(cudaMemsetAsync(zeros.p, 0, sizeof(double) * zeros.n, ctx->stream), "memset");
+      }
+    return zeros.p;
+  }
+
+  void
+  smooth_step(const double *b, double *u, double omega, int n, const double *xprev, int coupled, double *work_buf,
+              bool u_is_zero = false)
+  {
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("smooth_step: omega must be in (0, 1]");
+    double *r = work_buf ? work_buf : scratch(n);
+    if (u_is_zero && !coupled)
+      check(cudaMemcpyAsync(r, b, sizeof(double) * spec.isz() * n, cudaMemcpyDeviceToDevice, ctx->stream),
+            "copy"); // b - D*0 == b exactly
+    else
+      vmult(u, b, r, n, xprev, coupled, 1);
+    vanka(r, u, n, omega);
+  }
+};
+
+namespace
+{
+void
+build_level(stmg_level &L)
+{
+  const LevelSpec &s = L.spec;
+  if (s.r < 1 || s.r > 4)
+    throw std::invalid_argument("stmg_level: r must be in 1..4");
+  if (s.k < 0 || s.k > 4)
+    throw std::invalid_argument("stmg_level: k must be in 0..4");
+  if (s.nx < 1 || s.ny < 1)
+    throw std::invalid_argument("stmg_level: need at least one cell per direction");
+  if (!(s.tau > 0.0))
+    throw std::invalid_argument("stmg_level: tau must be positive");
+  L.consts = make_level_consts(s);
+  L.geom = DevGeom{s.nx, s.ny, s.gx(), s.gy(), s.S(), s.np(), s.nsc(), s.mv(), s.mp(), s.isz(), s.hx, s.hy};
+  if (L.smoother_kind == STMG_SMOOTHER_NONE)
+    return;
+  const PatchSet ps = build_patches(s, L.smoother_kind == STMG_SMOOTHER_CELL ? PatchKind::cell : PatchKind::vertex_star);
+  L.n_classes = static_cast<int>(ps.classes.size());
+  L.total_matrix_elements = ps.total_matrix_elements;
+  std::vector<DevPatchClass> dc(ps.classes.size());
+  L.cls_rel.resize(ps.classes.size());
+  L.cls_weight.resize(ps.classes.size());
+  L.cls_inverse.resize(ps.classes.size());
+  for (size_t i = 0; i < ps.classes.size(); ++i)
+    {
+      const PatchClass &pc = ps.classes[i];
+      L.cls_rel[i].upload(pc.rel);
+      L.cls_weight[i].upload(pc.weight);
+      L.cls_inverse[i].upload(pc.inverse);
+      dc[i] = DevPatchClass{pc.n_t, pc.n_vel, L.cls_rel[i].p, L.cls_weight[i].p, L.cls_inverse[i].p};
+      L.max_nt = std::max(L.max_nt, pc.n_t);
+    }
+  L.classes.upload(dc);
+  std::vector<VankaBatch> batches;
+  std::vector<long long> va, pa;
+  const int cols = vanka_cols_per_batch();
+  for (const auto &col : ps.colours)
+    {
+      L.colour_first.push_back(static_cast<int>(batches.size()));
+      size_t i = 0;
+      while (i < col.size())
+        {
+          VankaBatch b{col[i].cls, static_cast<int>(va.size()), 0};
+          while (i < col.size() && col[i].cls == b.cls && b.count < cols)
+            {
+              va.push_back(patch_vel_anchor(s, ps.kind, col[i].ax, col[i].ay));
+              pa.push_back(patch_pre_anchor(s, ps.kind, col[i].ax, col[i].ay));
+              ++b.count;
+              ++i;
+            }
+          batches.push_back(b);
+        }
+      L.colour_count.push_back(static_cast<int>(batches.size()) - L.colour_first.back());
+    }
+  L.batches.upload(batches);
+  L.vel_anchor.upload(va);
+  L.pre_anchor.upload(pa);
+}
+} // namespace
+
+// ================================================================ solver
+namespace
+{
+struct SolverLevel
+{
+  std::unique_ptr<stmg_level> level;
+  TransferKind kind = TransferKind::identity;
+  // transfer to the next coarser level (absent on level 0)
+  DevArray<int> px_ptr, px_col, py_ptr, py_col, rx_ptr, rx_col, ry_ptr, ry_col, embed;
+  DevArray<double> px_val, py_val, rx_val, ry_val, child;
+  DevTransfer dt{};
+  // V-cycle buffers (one interval)
+  DevArray<double> x, b, r, t;
+};
+} // namespace
+
+struct stmg_solver
+{
+  stmg_ctx *ctx = nullptr;
+  HierarchyConfig cfg;
+  int n_steps = 0;
+  int nu1 = 1, nu2 = 1;
+  double omega = 0.8;
+  bool project_pressure = true;
+  double rtol = 1e-8, atol = 1e-14;
+  int max_iterations = 200;
+  std::vector<std::unique_ptr<SolverLevel>> levels;
+  DevArray<double> coarse_inv;
+  DevArray<long long> coarse_pinned;
+  int n_pinned = 0, coarse_n = 0;
+  // Krylov workspace
+  std::vector<std::unique_ptr<DevArray<double>>> V, Z;
+  DevArray<double> w, scal, part, rhs, vprev;
+  std::vector<double> hist;
+
+  stmg_level &fine() { return *levels.back()->level; }
+
+  void
+  restrict_residual(int l, const double *fine_v, double *coarse_v, bool project)
+  {
+    SolverLevel &F = *levels[l];
+    check(launch_restrict(F.dt, fine_v, coarse_v, 1, ctx->stream), "restrict");
+    ctx->count(2);
+    if (F.kind != TransferKind::identity && project)
+      {
+        check(launch_project_mean_zero(levels[l - 1]->level->geom, coarse_v, 1, ctx->stream), "project");
+        ctx->count();
+      }
+  }
+
+  void
+  prolongate_correction(int l, const double *coarse_v, double *fine_v, bool project, bool accumulate)
+  {
+    SolverLevel &F = *levels[l];
+    if (F.kind != TransferKind::identity && project)
+      {
+        // out = P c, zero constrained, project mean-zero, then (x +=) out
+        F.t.resize(F.level->spec.isz());
+        check(launch_prolongate(F.dt, coarse_v, F.t.p, 1, 0, ctx->stream), "prolongate");
+        ctx->count(2);
+        check(launch_project_mean_zero(F.level->geom, F.t.p, 1, ctx->stream), "project");
+        ctx->count();
+        if (accumulate)
+          {
+            check(launch_axpy(F.level->spec.isz(), 1.0, nullptr, 1.0, F.t.p, fine_v, ctx->stream), "axpy");
+            ctx->count();
+          }
+        else
+          check(cudaMemcpyAsync(fine_v, F.t.p, sizeof(double) * F.level->spec.isz(), cudaMemcpyDeviceToDevice,
+                                ctx->stream),
+                "copy");
+      }
+    else
+      {
+        check(launch_prolongate(F.dt, coarse_v, fine_v, 1, accumulate ? 1 : 0, ctx->stream), "prolongate");
+        ctx->count(2);
+      }
+  }
+
+  void
+  coarse_solve(const double *b_v, double *x_v)
+  {
+    check(launch_coarse_solve(coarse_inv.p, coarse_pinned.p, n_pinned, coarse_n, b_v, x_v, ctx->stream), "coarse");
+    ctx->count();
+    check(launch_project_mean_zero(levels[0]->level->geom, x_v, 1, ctx->stream), "project");
+    ctx->count();
+  }
+
+  // VCycle::cycle (solver.cpp:69-93); writes the result into x_v.
+  void
+  cycle(int l, const double *b_v, double *x_v)
+  {
+    if (l == 0)
+      {
+        coarse_solve(b_v, x_v);
+        return;
+      }
+    SolverLevel &S = *levels[l];
+    stmg_level &L = *S.level;
+    const long long isz = L.spec.isz();
+    S.r.resize(isz);
+    check(cudaMemsetAsync(x_v, 0, sizeof(double) * isz, ctx->stream), "memset");
+    for (int s = 0; s < nu1; ++s)
+      L.smooth_step(b_v, x_v, omega, 1, nullptr, 0, S.r.p, s == 0);
+    L.vmult(x_v, b_v, S.r.p, 1, nullptr, 0, 1);
+    SolverLevel &C = *levels[l - 1];
+    const long long csz = C.level->spec.isz();
+    C.b.resize(csz);
+    C.x.resize(csz);
+    restrict_residual(l, S.r.p, C.b.p, project_pressure);
+    cycle(l - 1, C.b.p, C.x.p);
+    prolongate_correction(l, C.x.p, x_v, project_pressure, true);
+    for (int s = 0; s < nu2; ++s)
+      L.smooth_step(b_v, x_v, omega, 1, nullptr, 0, S.r.p);
+  }
+
+  void
+  vcycle(const double *b_v, double *x_v)
+  {
+    cycle(static_cast<int>(levels.size()) - 1, b_v, x_v);
+  }
+
+  double
+  dot(const double *a, const double *b, long long n, int slot)
+  {
+    check(launch_dot(a, b, n, part.p, scal.p + slot, ctx->stream), "dot");
+    ctx->count(2);
+    double h = 0.0;
+    check(cudaMemcpyAsync(&h, scal.p + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    check(cudaStreamSynchronize(ctx->stream), "sync");
+    return h;
+  }
+
+  DevArray<double> &
+  basis(std::vector<std::unique_ptr<DevArray<double>>> &B, int j, long long n)
+  {
+    while (static_cast<int>(B.size()) <= j)
+      B.push_back(std::make_unique<DevArray<double>>());
+    B[j]->resize(n);
+    return *B[j];
+  }
+
+  // gmres (solver.cpp:95-202), x0 = 0, preconditioner = V-cycle.
+  int
+  gmres(const double *b_v, double *x_v, int *iterations, double *history, int history_cap)
+  {
+    stmg_level &L = fine();
+    const long long n = L.spec.isz();
+    w.resize(n);
+    part.resize(dot_partials());
+    scal.resize(2 * (max_iterations + 2));
+    hist.clear();
+    const double norm_b = std::sqrt(dot(b_v, b_v, n, 0));
+    const double tol = std::max(rtol * norm_b, atol);
+    // r = b - A*0 = b
+    const double beta = norm_b;
+    hist.push_back(beta);
+    check(cudaMemsetAsync(x_v, 0, sizeof(double) * n, ctx->stream), "memset");
+    int iters = 0;
+    bool converged = false;
+    if (beta <= tol)
+      converged = true;
+    else
+      {
+        const int m = max_iterations;
+        std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0), g(m + 1, 0.0), cs(m), sn(m);
+        g[0] = beta;
+        DevArray<double> &v0 = basis(V, 0, n);
+        check(cudaMemcpyAsync(v0.p, b_v, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+        check(launch_scale(n, 1.0 / beta, v0.p, ctx->stream), "scale");
+        ctx->count();
+        int j = 0;
+        std::vector<double> hcol(m + 2);
+        for (; j < m; ++j)
+          {
+            DevArray<double> &zj = basis(Z, j, n);
+            vcycle(V[j]->p, zj.p);
+            L.vmult(zj.p, nullptr, w.p, 1, nullptr, 0, 0);
+            // modified Gram-Schmidt with device-resident coefficients
+            for (int i = 0; i <= j; ++i)
+              {
+                check(launch_dot(w.p, V[i]->p, n, part.p, scal.p + i, ctx->stream), "dot");
+                check(launch_axpy(n, 0.0, scal.p + i, -1.0, V[i]->p, w.p, ctx->stream), "axpy");
+                ctx->count(3);
+              }
+            check(launch_dot(w.p, w.p, n, part.p, scal.p + j + 1, ctx->stream), "dot");
+            ctx->count(2);
+            check(cudaMemcpyAsync(hcol.data(), scal.p, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->stream),
+                  "d2h");
+            check(cudaStreamSynchronize(ctx->stream), "sync");
+            const double h_next = std::sqrt(hcol[j + 1]);
+            const bool breakdown = !(h_next > 1e-300);
+            for (int i = 0; i <= j; ++i)
+              H[static_cast<size_t>(j) * (m + 1) + i] = hcol[i];
+            auto Hc = [&](int i) -> double & { return H[static_cast<size_t>(j) * (m + 1) + i]; };
+            for (int i = 0; i < j; ++i)
+              {
+                const double t = cs[i] * Hc(i) + sn[i] * Hc(i + 1);
+                Hc(i + 1) = -sn[i] * Hc(i) + cs[i] * Hc(i + 1);
+                Hc(i) = t;
+              }
+            const double denom = std::hypot(Hc(j), h_next);
+            cs[j] = Hc(j) / denom;
+            sn[j] = h_next / denom;
+            Hc(j) = denom;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            const double res = std::abs(g[j + 1]);
+            hist.push_back(res);
+            if (res <= tol || breakdown)
+              {
+                ++j;
+                converged = true;
+                break;
+              }
+            DevArray<double> &vn = basis(V, j + 1, n);
+            check(cudaMemcpyAsync(vn.p, w.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+            check(launch_scale(n, 1.0 / h_next, vn.p, ctx->stream), "scale");
+            ctx->count();
+          }
+        iters = std::min(j, m);
+        if (iters > 0)
+          {
+            std::vector<double> y(iters);
+            for (int i = iters - 1; i >= 0; --i)
+              {
+                double s = g[i];
+                for (int c = i + 1; c < iters; ++c)
+                  s -= H[static_cast<size_t>(c) * (m + 1) + i] * y[c];
+                y[i] = s / H[static_cast<size_t>(i) * (m + 1) + i];
+              }
+            for (int i = 0; i < iters; ++i)
+              {
+                check(launch_axpy(n, y[i], nullptr, 1.0, Z[i]->p, x_v, ctx->stream), "axpy");
+                ctx->count();
+              }
+          }
+      }
+    if (iterations)
+      *iterations = iters;
+    for (int i = 0; history && i < history_cap && i < static_cast<int>(hist.size()); ++i)
+      history[i] = hist[i];
+    if (!converged)
+      throw std::runtime_error("gmres: not converged within max_iterations");
+    return iters;
+  }
+
+  // time_march (solver.cpp:204-325) with per-step load vectors F.
+  void
+  time_march(const double *F, double *X, int *iterations)
+  {
+    stmg_level &L = fine();
+    const long long n = L.spec.isz();
+    rhs.resize(n);
+    vprev.resize(L.spec.mv());
+    check(cudaMemsetAsync(vprev.p, 0, sizeof(double) * L.spec.mv(), ctx->stream), "memset");
+    const double *zero = L.zero_vector(1);
+    for (int step = 0; step < n_steps; ++step)
+      {
+        // rhs = F_n + C v_prev (coupling_rhs), constrained rows zeroed
+        L.vmult(zero, F + step * n, rhs.p, 1, vprev.p, 1, 1);
+        check(launch_zero_constrained(L.geom, rhs.p, 1, ctx->stream), "zero");
+        ctx->count();
+        double *x = X + step * n;
+        int it = 0;
+        gmres(rhs.p, x, &it, nullptr, 0);
+        check(launch_project_mean_zero(L.geom, x, 1, ctx->stream), "project");
+        ctx->count();
+        if (iterations)
+          iterations[step] = it;
+        check(cudaMemcpyAsync(vprev.p, x + (L.spec.S() - 1) * L.spec.mv(), sizeof(double) * L.spec.mv(),
+                              cudaMemcpyDeviceToDevice, ctx->stream),
+              "copy");
+      }
+  }
+};
+
+namespace
+{
+void
+upload_transfer(SolverLevel &F, const LevelSpec &coarse, const LevelSpec &fine, TransferKind kind)
+{
+  const TransferTables t = build_transfer(coarse, fine, kind);
+  DevTransfer &d = F.dt;
+  d = DevTransfer{};
+  d.spatial = t.spatial;
+  d.temporal = t.temporal;
+  d.pmode = t.pmode;
+  d.zero_constrained = kind != TransferKind::identity;
+  if (t.spatial)
+    {
+      F.px_ptr.upload(t.px.ptr);
+      F.px_col.upload(t.px.col);
+      F.px_val.upload(t.px.val);
+      F.py_ptr.upload(t.py.ptr);
+      F.py_col.upload(t.py.col);
+      F.py_val.upload(t.py.val);
+      F.rx_ptr.upload(t.rx.ptr);
+      F.rx_col.upload(t.rx.col);
+      F.rx_val.upload(t.rx.val);
+      F.ry_ptr.upload(t.ry.ptr);
+      F.ry_col.upload(t.ry.col);
+      F.ry_val.upload(t.ry.val);
+      d.px = DevCsr{F.px_ptr.p, F.px_col.p, F.px_val.p};
+      d.py = DevCsr{F.py_ptr.p, F.py_col.p, F.py_val.p};
+      d.rx = DevCsr{F.rx_ptr.p, F.rx_col.p, F.rx_val.p};
+      d.ry = DevCsr{F.ry_ptr.p, F.ry_col.p, F.ry_val.p};
+    }
+  if (t.pmode == 1)
+    {
+      F.child.upload(t.child);
+      d.child = F.child.p;
+    }
+  if (t.pmode == 2)
+    {
+      F.embed.upload(t.embed);
+      d.embed = F.embed.p;
+    }
+  if (t.temporal)
+    for (int a = 0; a <= fine.k; ++a)
+      for (int b = 0; b <= coarse.k; ++b)
+        d.E[a * kMaxS + b] = t.e_time[a * (coarse.k + 1) + b];
+  const auto geom = [](const LevelSpec &s) {
+    return DevGeom{s.nx, s.ny, s.gx(), s.gy(), s.S(), s.np(), s.nsc(), s.mv(), s.mp(), s.isz(), s.hx, s.hy};
+  };
+  d.f = geom(fine);
+  d.c = geom(coarse);
+}
+} // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char *
+stmg_last_error(void)
+{
+  return g_error.c_str();
+}
+
+const char *
+stmg_version(void)
+{
+  return "stmg_b200 0.1 sm_100a fp64";
+}
+
+int
+stmg_ctx_create(int device, stmg_ctx **out)
+{
+  return guarded([&] {
+    if (!out)
+      throw std::invalid_argument("stmg_ctx_create: null out");
+    check(cudaSetDevice(device), "cudaSetDevice");
+    auto c = std::make_unique<stmg_ctx>();
+    c->device = device;
+    *out = c.release();
+  });
+}
+
+int
+stmg_ctx_destroy(stmg_ctx *ctx)
+{
+  delete ctx;
+  return STMG_OK;
+}
+
+int
+stmg_ctx_set_stream(stmg_ctx *ctx, void *stream)
+{
+  return guarded([&] {
+    if (!ctx)
+      throw std::invalid_argument("null ctx");
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+int
+stmg_ctx_synchronize(stmg_ctx *ctx)
+{
+  return guarded([&] { check(cudaStreamSynchronize(ctx->stream), "sync"); });
+}
+
+int64_t
+stmg_ctx_launch_count(const stmg_ctx *ctx)
+{
+  return ctx ? ctx->launches : 0;
+}
+
+int
+stmg_level_create(stmg_ctx *ctx, int nx, int ny, int r, int k, double tau, double nu, double gamma, int smoother_kind,
+                  stmg_level **out)
+{
+  return guarded([&] {
+    if (!ctx || !out)
+      throw std::invalid_argument("stmg_level_create: null argument");
+    if (smoother_kind < -1 || smoother_kind > 1)
+      throw std::invalid_argument("stmg_level_create: unknown smoother kind");
+    auto L = std::make_unique<stmg_level>();
+    L->ctx = ctx;
+    L->spec.nx = nx;
+    L->spec.ny = ny;
+    L->spec.r = r;
+    L->spec.k = k;
+    L->spec.hx = 1.0 / nx;
+    L->spec.hy = 1.0 / ny;
+    L->spec.tau = tau;
+    L->spec.nu = nu;
+    L->spec.gamma = gamma;
+    L->smoother_kind = smoother_kind;
+    build_level(*L);
+    *out = L.release();
+  });
+}
+
+int
+stmg_level_destroy(stmg_level *level)
+{
+  delete level;
+  return STMG_OK;
+}
+
+int
+stmg_level_sizes(const stmg_level *L, int64_t *out)
+{
+  return guarded([&] {
+    out[0] = L->spec.S();
+    out[1] = L->spec.mv();
+    out[2] = L->spec.mp();
+    out[3] = L->spec.isz();
+    out[4] = L->spec.nsc();
+    out[5] = L->spec.gx();
+    out[6] = L->n_classes;
+    out[7] = static_cast<int64_t>(L->total_matrix_elements);
+  });
+}
+
+int
+stmg_apply_block(stmg_level *L, const double *x, double *y, int n, int raw)
+{
+  return guarded([&] { L->vmult(x, nullptr, y, n, nullptr, 0, raw ? 2 : 0); });
+}
+
+int
+stmg_vmult(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot)
+{
+  return guarded([&] { L->vmult(x, nullptr, y, n, x_prev_slot, 1, 0); });
+}
+
+int
+stmg_residual(stmg_level *L, const double *b, const double *x, double *r, int n, const double *x_prev_slot,
+              int coupled)
+{
+  return guarded([&] { L->vmult(x, b, r, n, x_prev_slot, coupled ? 1 : 0, 1); });
+}
+
+int
+stmg_coupling_rhs(stmg_level *L, const double *v_prev, double *out)
+{
+  return guarded([&] {
+    // raw apply of D*0 - C v_prev on every row, negated: out = C v_prev
+    L->vmult(L->zero_vector(1), nullptr, out, 1, v_prev, 1, 2);
+    check(launch_scale(L->spec.isz(), -1.0, out, L->ctx->stream), "scale");
+    L->ctx->count();
+  });
+}
+
+int
+stmg_apply_additive(stmg_level *L, const double *r, double *out, int n)
+{
+  return guarded([&] {
+    check(cudaMemsetAsync(out, 0, sizeof(double) * L->spec.isz() * n, L->ctx->stream), "memset");
+    L->vanka(r, out, n, 1.0);
+  });
+}
+
+int
+stmg_smooth_step(stmg_level *L, const double *b, double *u, double omega, int n, const double *x_prev_slot,
+                 int coupled, double *work)
+{
+  return guarded([&] { L->smooth_step(b, u, omega, n, x_prev_slot, coupled ? 1 : 0, work); });
+}
+
+int
+stmg_vmult_host(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot)
+{
+  return guarded([&] {
+    const size_t sz = static_cast<size_t>(L->spec.isz()) * n;
+    L->host_in.resize(sz);
+    L->host_out.resize(sz);
+    cudaStream_t st = L->ctx->stream;
+    check(cudaMemcpyAsync(L->host_in.p, x, sizeof(double) * sz, cudaMemcpyHostToDevice, st), "h2d");
+    const double *prev = nullptr;
+    if (x_prev_slot)
+      {
+        L->host_prev.resize(L->spec.mv());
+        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * L->spec.mv(), cudaMemcpyHostToDevice, st),
+              "h2d");
+        prev = L->host_prev.p;
+      }
+    L->vmult(L->host_in.p, nullptr, L->host_out.p, n, prev, 1, 0);
+    check(cudaMemcpyAsync(y, L->host_out.p, sizeof(double) * sz, cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int
+stmg_smooth_step_host(stmg_level *L, const double *b, double *u, double omega, int n, const double *x_prev_slot,
+                      int coupled)
+{
+  return guarded([&] {
+    const size_t sz = static_cast<size_t>(L->spec.isz()) * n;
+    L->host_in.resize(sz);
+    L->host_out.resize(sz);
+    cudaStream_t st = L->ctx->stream;
+    check(cudaMemcpyAsync(L->host_in.p, b, sizeof(double) * sz, cudaMemcpyHostToDevice, st), "h2d");
+    check(cudaMemcpyAsync(L->host_out.p, u, sizeof(double) * sz, cudaMemcpyHostToDevice, st), "h2d");
+    const double *prev = nullptr;
+    if (x_prev_slot)
+      {
+        L->host_prev.resize(L->spec.mv());
+        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * L->spec.mv(), cudaMemcpyHostToDevice, st),
+              "h2d");
+        prev = L->host_prev.p;
+      }
+    L->smooth_step(L->host_in.p, L->host_out.p, omega, n, prev, coupled ? 1 : 0, nullptr);
+    check(cudaMemcpyAsync(u, L->host_out.p, sizeof(double) * sz, cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int
+stmg_solver_create(stmg_ctx *ctx, int refinements, int r, int k, int n_steps, double t_end, double nu, double gamma,
+                   int smoother_kind, int nu1, int nu2, double omega, int h_only, double rtol, double atol,
+                   int max_iterations, stmg_solver **out)
+{
+  return guarded([&] {
+    if (!ctx || !out)
+      throw std::invalid_argument("stmg_solver_create: null argument");
+    if (smoother_kind != STMG_SMOOTHER_CELL && smoother_kind != STMG_SMOOTHER_VERTEX_STAR)
+      throw std::invalid_argument("stmg_solver_create: smoother must be cell or vertex_star");
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("stmg_solver_create: omega must be in (0, 1]");
+    if (refinements < 0 || max_iterations < 1 || nu1 < 0 || nu2 < 0)
+      throw std::invalid_argument("stmg_solver_create: invalid configuration");
+    auto S = std::make_unique<stmg_solver>();
+    S->ctx = ctx;
+    S->cfg.refinements = refinements;
+    S->cfg.r = r;
+    S->cfg.k = k;
+    S->cfg.n_steps = n_steps;
+    S->cfg.t_end = t_end;
+    S->cfg.nu = nu;
+    S->cfg.gamma = gamma;
+    S->cfg.h_only = h_only;
+    S->cfg.smoother = smoother_kind == STMG_SMOOTHER_CELL ? PatchKind::cell : PatchKind::vertex_star;
+    S->nu1 = nu1;
+    S->nu2 = nu2;
+    S->omega = omega;
+    S->rtol = rtol;
+    S->atol = atol;
+    S->max_iterations = max_iterations;
+    const std::vector<LevelPlan> plan = plan_levels(S->cfg, &S->n_steps);
+    for (size_t l = 0; l < plan.size(); ++l)
+      {
+        auto SL = std::make_unique<SolverLevel>();
+        SL->kind = plan[l].kind_to_coarser;
+        SL->level = std::make_unique<stmg_level>();
+        SL->level->ctx = ctx;
+        SL->level->spec = plan[l].spec;
+        SL->level->smoother_kind = l == 0 ? STMG_SMOOTHER_NONE : smoother_kind;
+        build_level(*SL->level);
+        if (l > 0)
+          upload_transfer(*SL, plan[l - 1].spec, plan[l].spec, SL->kind);
+        S->levels.push_back(std::move(SL));
+      }
+    std::vector<long long> pinned;
+    const std::vector<double> inv = coarse_inverse(plan[0].spec, pinned);
+    S->coarse_inv.upload(inv);
+    S->coarse_pinned.upload(pinned);
+    S->n_pinned = static_cast<int>(pinned.size());
+    S->coarse_n = static_cast<int>(plan[0].spec.isz());
+    *out = S.release();
+  });
+}
+
+int
+stmg_solver_destroy(stmg_solver *s)
+{
+  delete s;
+  return STMG_OK;
+}
+
+int
+stmg_solver_info(const stmg_solver *s, int64_t *out)
+{
+  return guarded([&] {
+    out[0] = static_cast<int64_t>(s->levels.size());
+    out[1] = s->n_steps;
+    for (size_t l = 0; l < s->levels.size(); ++l)
+      {
+        const LevelSpec &sp = s->levels[l]->level->spec;
+        out[2 + 5 * l + 0] = sp.nx;
+        out[2 + 5 * l + 1] = sp.r;
+        out[2 + 5 * l + 2] = sp.k;
+        out[2 + 5 * l + 3] = static_cast<int64_t>(s->levels[l]->kind);
+        out[2 + 5 * l + 4] = sp.isz();
+      }
+  });
+}
+
+stmg_level *
+stmg_solver_level(stmg_solver *s, int l)
+{
+  if (!s || l < 0 || l >= static_cast<int>(s->levels.size()))
+    return nullptr;
+  return s->levels[l]->level.get();
+}
+
+int
+stmg_restrict_residual(stmg_solver *s, int l, const double *fine, double *coarse, int project_pressure)
+{
+  return guarded([&] {
+    if (l < 1 || l >= static_cast<int>(s->levels.size()))
+      throw std::invalid_argument("stmg_restrict_residual: level out of range");
+    s->restrict_residual(l, fine, coarse, project_pressure != 0);
+  });
+}
+
+int
+stmg_prolongate_correction(stmg_solver *s, int l, const double *coarse, double *fine, int project_pressure,
+                           int accumulate)
+{
+  return guarded([&] {
+    if (l < 1 || l >= static_cast<int>(s->levels.size()))
+      throw std::invalid_argument("stmg_prolongate_correction: level out of range");
+    s->prolongate_correction(l, coarse, fine, project_pressure != 0, accumulate != 0);
+  });
+}
+
+int
+stmg_coarse_solve(stmg_solver *s, const double *b, double *x)
+{
+  return guarded([&] { s->coarse_solve(b, x); });
+}
+
+int
+stmg_vcycle(stmg_solver *s, const double *b, double *x)
+{
+  return guarded([&] { s->vcycle(b, x); });
+}
+
+int
+stmg_gmres(stmg_solver *s, const double *b, double *x, int *iterations, double *history, int history_cap)
+{
+  return guarded([&] { s->gmres(b, x, iterations, history, history_cap); });
+}
+
+int
+stmg_time_march(stmg_solver *s, const double *F, double *X, int *iterations)
+{
+  return guarded([&] { s->time_march(F, X, iterations); });
+}
+
+int
+stmg_time_march_host(stmg_solver *s, const double *F, double *X, int *iterations)
+{
+  return guarded([&] {
+    stmg_level &L = s->fine();
+    const size_t sz = static_cast<size_t>(L.spec.isz()) * s->n_steps;
+    L.host_in.resize(sz);
+    L.host_out.resize(sz);
+    cudaStream_t st = s->ctx->stream;
+    check(cudaMemcpyAsync(L.host_in.p, F, sizeof(double) * sz, cudaMemcpyHostToDevice, st), "h2d");
+    s->time_march(L.host_in.p, L.host_out.p, iterations);
+    check(cudaMemcpyAsync(X, L.host_out.p, sizeof(double) * sz, cudaMemcpyDeviceToHost, st), "d2h");
+    check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int
+stmg_plan_levels(int refinements, int r, int k, int n_steps, double t_end, int h_only, int64_t *out)
+{
+  return guarded([&] {
+    HierarchyConfig cfg;
+    cfg.refinements = refinements;
+    cfg.r = r;
+    cfg.k = k;
+    cfg.n_steps = n_steps;
+    cfg.t_end = t_end;
+    cfg.h_only = h_only;
+    int ns = 0;
+    const std::vector<LevelPlan> plan = plan_levels(cfg, &ns);
+    out[0] = static_cast<int64_t>(plan.size());
+    out[1] = ns;
+    for (size_t l = 0; l < plan.size(); ++l)
+      {
+        out[2 + 5 * l + 0] = plan[l].spec.nx;
+        out[2 + 5 * l + 1] = plan[l].spec.r;
+        out[2 + 5 * l + 2] = plan[l].spec.k;
+        out[2 + 5 * l + 3] = static_cast<int64_t>(plan[l].kind_to_coarser);
+        out[2 + 5 * l + 4] = plan[l].spec.isz();
+      }
+  });
+}
+
+int
+stmg_patch_info(int nx, int ny, int r, int k, double tau, double nu, double gamma, int smoother_kind, int64_t *out,
+                double *inverse_out, int class_index)
+{
+  return guarded([&] {
+    LevelSpec s;
+    s.nx = nx;
+    s.ny = ny;
+    s.r = r;
+    s.k = k;
+    s.hx = 1.0 / nx;
+    s.hy = 1.0 / ny;
+    s.tau = tau;
+    s.nu = nu;
+    s.gamma = gamma;
+    const PatchSet ps = build_patches(s, smoother_kind == STMG_SMOOTHER_VERTEX_STAR ? PatchKind::vertex_star
+                                                                                   : PatchKind::cell);
+    long long n = 0;
+    for (const auto &c : ps.colours)
+      n += static_cast<long long>(c.size());
+    out[0] = n;
+    out[1] = static_cast<int64_t>(ps.classes.size());
+    out[2] = static_cast<int64_t>(ps.total_matrix_elements);
+    out[3] = static_cast<int64_t>(ps.colours.size());
+    for (size_t c = 0; c < ps.classes.size() && c < 60; ++c)
+      out[4 + c] = ps.classes[c].n_t;
+    if (inverse_out)
+      {
+        if (class_index < 0 || class_index >= static_cast<int>(ps.classes.size()))
+          throw std::invalid_argument("stmg_patch_info: class index out of range");
+        const auto &inv = ps.classes[class_index].inverse;
+        std::memcpy(inverse_out, inv.data(), sizeof(double) * inv.size());
+      }
+  });
+}
+
+} // extern "C"

@@ -1,0 +1,335 @@
+// Fused matrix-free space-time operator on B200 (sm_100a), FP64.
+//
+// Replaces SpaceTimeBlockOperator::apply_block / apply_block_raw /
+// coupling_rhs (st_operator.cpp:321-421) and the residual b - D x of
+// VankaSmoother::smooth_step (vanka.cpp:225-228), for one interval or the
+// all-at-once system of N intervals with the DG jump coupling
+//   y_n = D x_n - Z C x_{n-1}[slot k]      (Eq. GloSys).
+//
+// Design:
+//  * One pass over memory: all k+1 temporal slots and all five spatial
+//    operators (mass, Laplacian, grad-div, B, B^T) of a cell are evaluated in
+//    registers. The temporal Kronecker combination is done on nodal values
+//    (UK = sum_b K_ab u^b - lv_a v_prev, UM = sum_b M_ab u^b), so each output
+//    slot costs one spatial Stokes cell operator.
+//  * Cartesian cells are congruent: the element operator factorises into 1D
+//    matrices (M1, K1, C1, Legendre moments) that sit in the kernel parameter
+//    constant bank (LevelConsts) and feed DFMA directly.
+//  * Thread mapping: warp = one output slot a, lane = one cell of a strip of
+//    31 owned cells (+1 halo cell on the left). A block marches upward through
+//    a segment of cell rows. Contributions to shared nodes are summed with
+//    __shfl_up_sync across the strip (x) and a register carry (y): no atomics,
+//    no zero-fill pass, every output written exactly once. Halo work: 1/31 in
+//    x, 1/rows_per_seg in y.
+#pragma once
+#include "level_consts.cuh"
+
+#include <cuda_runtime.h>
+
+namespace stmg_b200
+{
+
+namespace vmult_detail
+{
+constexpr int kStrip = 31; // owned cells per warp strip
+
+template <int R, int S, bool RESID, bool RAW>
+__global__ void __launch_bounds__(32 * S)
+vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
+             double *__restrict__ y, const double *__restrict__ xprev0, int rows_per_seg, int coupled)
+{
+  constexpr int N1 = R + 2, p = R + 1, NPM = (R + 1) * (R + 2) / 2, PL = R + 1;
+  const int lane = threadIdx.x & 31;
+  const int a = threadIdx.x >> 5; // output slot
+  const int n = blockIdx.z;       // interval
+  const int cx = blockIdx.x * kStrip - 1 + lane;
+  const bool active = cx >= 0 && cx < P.nx;
+  const bool owner = lane >= 1 && active;
+
+  const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
+  const int gx = P.gx, gy = P.gy;
+  const double *__restrict__ xn = x + n * isz;
+  const double *__restrict__ vprev = nullptr;
+  if (coupled)
+    vprev = n > 0 ? x + (n - 1) * isz + (S - 1) * mv : xprev0;
+
+  // Temporal coefficients of this warp's output slot, selected with
+  // compile-time indices so the parameter bank is never indexed dynamically.
+  double kt[S], mt[S], lva = 0.0;
+#pragma unroll
+  for (int bs = 0; bs < S; ++bs)
+    kt[bs] = mt[bs] = 0.0;
+#pragma unroll
+  for (int aa = 0; aa < S; ++aa)
+    if (a == aa)
+      {
+#pragma unroll
+        for (int bs = 0; bs < S; ++bs)
+          {
+            kt[bs] = P.Kt[aa * S + bs];
+            mt[bs] = P.Mt[aa * S + bs];
+          }
+        lva = P.lv[aa];
+      }
+
+  const int cy_begin = blockIdx.y * rows_per_seg;
+  const int cy_end = min(P.ny, cy_begin + rows_per_seg);
+  const int cy_first = max(cy_begin - 1, 0);
+
+  double carx[N1], cary[N1];
+#pragma unroll
+  for (int i = 0; i < N1; ++i)
+    carx[i] = cary[i] = 0.0;
+
+  for (int cy = cy_first; cy < cy_end; ++cy)
+    {
+      double Yx[N1][N1], Yy[N1][N1], Yp[NPM];
+#pragma unroll
+      for (int i = 0; i < N1; ++i)
+#pragma unroll
+        for (int j = 0; j < N1; ++j)
+          Yx[i][j] = Yy[i][j] = 0.0;
+#pragma unroll
+      for (int m = 0; m < NPM; ++m)
+        Yp[m] = 0.0;
+
+      if (active)
+        {
+          const long long cell = static_cast<long long>(cy) * P.nx + cx;
+          // ---- pressure: PM = sum_b Mt(a,b) p^b; B^T init of Yx, Yy
+          {
+            double PM[NPM];
+#pragma unroll
+            for (int m = 0; m < NPM; ++m)
+              PM[m] = 0.0;
+#pragma unroll
+            for (int bs = 0; bs < S; ++bs)
+              {
+                const double c = mt[bs];
+                const double *pp = xn + S * mv + bs * mp + cell * NPM;
+#pragma unroll
+                for (int m = 0; m < NPM; ++m)
+                  PM[m] = fma(c, __ldg(pp + m), PM[m]);
+              }
+            // Yx(i,j) -= sum_b Qx(i,b) yLm(b,j),  Qx(i,b) = sum_{m: ay=b} xLc(ax,i) PM_m
+            // Yy(i,j) -= sum_b Qy(i,b) yLc(b,j),  Qy(i,b) = sum_{m: ay=b} xLm(ax,i) PM_m
+#pragma unroll
+            for (int bb = 0; bb < PL; ++bb)
+              {
+                double Qx[N1], Qy[N1];
+#pragma unroll
+                for (int i = 0; i < N1; ++i)
+                  Qx[i] = Qy[i] = 0.0;
+#pragma unroll
+                for (int m = 0; m < NPM; ++m)
+                  {
+                    if (pdisc_mode_ay(R, m) != bb)
+                      continue;
+                    const int am = pdisc_mode_ax(R, m);
+#pragma unroll
+                    for (int i = 0; i < N1; ++i)
+                      {
+                        Qx[i] = fma(P.xLc[am * N1 + i], PM[m], Qx[i]);
+                        Qy[i] = fma(P.xLm[am * N1 + i], PM[m], Qy[i]);
+                      }
+                  }
+#pragma unroll
+                for (int i = 0; i < N1; ++i)
+#pragma unroll
+                  for (int j = 0; j < N1; ++j)
+                    {
+                      Yx[i][j] = fma(-Qx[i], P.yLm[bb * N1 + j], Yx[i][j]);
+                      Yy[i][j] = fma(-Qy[i], P.yLc[bb * N1 + j], Yy[i][j]);
+                    }
+              }
+          }
+
+          // ---- velocity rows of the cell
+#pragma unroll
+          for (int l = 0; l < N1; ++l)
+            {
+              const int Y = cy * p + l;
+              const bool yb = (Y == 0) || (Y == gy - 1);
+              const long long rowbase = static_cast<long long>(Y) * gx + cx * p;
+              double UKx[N1], UMx[N1], UKy[N1], UMy[N1];
+#pragma unroll
+              for (int k = 0; k < N1; ++k)
+                {
+                  const int X = cx * p + k;
+                  const bool bnd = !RAW && (yb || X == 0 || X == gx - 1);
+                  const long long node = rowbase + k;
+                  double ukx = 0.0, umx = 0.0, uky = 0.0, umy = 0.0;
+#pragma unroll
+                  for (int bs = 0; bs < S; ++bs)
+                    {
+                      const double vx = bnd ? 0.0 : __ldg(xn + bs * mv + node);
+                      const double vy = bnd ? 0.0 : __ldg(xn + bs * mv + nsc + node);
+                      ukx = fma(kt[bs], vx, ukx);
+                      umx = fma(mt[bs], vx, umx);
+                      uky = fma(kt[bs], vy, uky);
+                      umy = fma(mt[bs], vy, umy);
+                    }
+                  if (vprev != nullptr)
+                    {
+                      ukx = fma(-lva, __ldg(vprev + node), ukx);
+                      uky = fma(-lva, __ldg(vprev + nsc + node), uky);
+                    }
+                  UKx[k] = ukx;
+                  UMx[k] = umx;
+                  UKy[k] = uky;
+                  UMy[k] = umy;
+                }
+              // x-contraction for output column i, immediately folded into the
+              // y-accumulation (keeps only the running Yx/Yy tiles live)
+#pragma unroll
+              for (int i = 0; i < N1; ++i)
+                {
+                  double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0;
+#pragma unroll
+                  for (int k = 0; k < N1; ++k)
+                    {
+                      const int o = i * N1 + k;
+                      s0 = fma(P.xM[o], UKx[k], s0);
+                      s0 = fma(P.xKa[o], UMx[k], s0);
+                      s1 = fma(P.xM[o], UMx[k], s1);
+                      s2 = fma(P.xC[o], UMy[k], s2);
+                      s3 = fma(P.xM[o], UKy[k], s3);
+                      s3 = fma(P.xKb[o], UMy[k], s3);
+                      s4 = fma(P.xM[o], UMy[k], s4);
+                      s5 = fma(P.xCt[o], UMx[k], s5);
+                    }
+#pragma unroll
+                  for (int j = 0; j < N1; ++j)
+                    {
+                      const int o = j * N1 + l;
+                      double vx = Yx[i][j], vy = Yy[i][j];
+                      vx = fma(P.yM[o], s0, vx);
+                      vx = fma(P.yKa[o], s1, vx);
+                      vx = fma(P.yCx[o], s2, vx);
+                      vy = fma(P.yM[o], s3, vy);
+                      vy = fma(P.yKb[o], s4, vy);
+                      vy = fma(P.yCy[o], s5, vy);
+                      Yx[i][j] = vx;
+                      Yy[i][j] = vy;
+                    }
+                }
+              double dp[PL], ep[PL];
+#pragma unroll
+              for (int aa = 0; aa < PL; ++aa)
+                {
+                  double s0 = 0, s1 = 0;
+#pragma unroll
+                  for (int k = 0; k < N1; ++k)
+                    {
+                      s0 = fma(P.xLc[aa * N1 + k], UMx[k], s0);
+                      s1 = fma(P.xLm[aa * N1 + k], UMy[k], s1);
+                    }
+                  dp[aa] = s0;
+                  ep[aa] = s1;
+                }
+#pragma unroll
+              for (int m = 0; m < NPM; ++m)
+                {
+                  const int am = pdisc_mode_ax(R, m), bm = pdisc_mode_ay(R, m);
+                  Yp[m] = fma(P.yLm[bm * N1 + l], dp[am], Yp[m]);
+                  Yp[m] = fma(P.yLc[bm * N1 + l], ep[am], Yp[m]);
+                }
+            }
+        }
+
+      // ---- assemble shared nodes: x across lanes, y through the carry
+#pragma unroll
+      for (int j = 0; j < N1; ++j)
+        {
+          const double lx = __shfl_up_sync(0xffffffffu, Yx[N1 - 1][j], 1);
+          const double ly = __shfl_up_sync(0xffffffffu, Yy[N1 - 1][j], 1);
+          if (lane > 0)
+            {
+              Yx[0][j] += lx;
+              Yy[0][j] += ly;
+            }
+        }
+      if (cy > cy_first)
+#pragma unroll
+        for (int i = 0; i < N1; ++i)
+          {
+            Yx[i][0] += carx[i];
+            Yy[i][0] += cary[i];
+          }
+#pragma unroll
+      for (int i = 0; i < N1; ++i)
+        {
+          carx[i] = Yx[i][N1 - 1];
+          cary[i] = Yy[i][N1 - 1];
+        }
+
+      // ---- write owned outputs
+      if (owner && cy >= cy_begin)
+        {
+          const int ixmax = (cx == P.nx - 1) ? p : p - 1;
+          const int iymax = (cy == P.ny - 1) ? p : p - 1;
+          const long long obase = n * isz + a * mv;
+#pragma unroll
+          for (int j = 0; j < N1; ++j)
+            {
+              if (j > iymax)
+                continue;
+              const int Y = cy * p + j;
+              const bool yb = (Y == 0) || (Y == gy - 1);
+#pragma unroll
+              for (int i = 0; i < N1; ++i)
+                {
+                  if (i > ixmax)
+                    continue;
+                  const int X = cx * p + i;
+                  const long long node = static_cast<long long>(Y) * gx + X;
+                  double vx = Yx[i][j], vy = Yy[i][j];
+                  if (!RAW && (yb || X == 0 || X == gx - 1))
+                    {
+                      // identity rows on constrained velocity dofs (st_operator.cpp:383-394)
+                      vx = __ldg(x + obase + node);
+                      vy = __ldg(x + obase + nsc + node);
+                    }
+                  if (RESID)
+                    {
+                      vx = __ldg(b + obase + node) - vx;
+                      vy = __ldg(b + obase + nsc + node) - vy;
+                    }
+                  y[obase + node] = vx;
+                  y[obase + nsc + node] = vy;
+                }
+            }
+          const long long pbase = n * isz + S * mv + a * mp + (static_cast<long long>(cy) * P.nx + cx) * NPM;
+#pragma unroll
+          for (int m = 0; m < NPM; ++m)
+            y[pbase + m] = RESID ? __ldg(b + pbase + m) - Yp[m] : Yp[m];
+        }
+    }
+}
+
+template <int R, int S>
+cudaError_t
+launch_rs(const LevelConsts &P, const double *x, const double *b, double *y, int n_intervals, const double *xprev0,
+          int coupled, int mode, cudaStream_t stream)
+{
+  const int strips = (P.nx + kStrip - 1) / kStrip;
+  // Row segments: enough blocks to fill 148 SMs several times, >= 8 rows
+  // each so the recomputed halo row stays small.
+  int segs = 1;
+  const long long base_blocks = static_cast<long long>(strips) * n_intervals;
+  while (base_blocks * segs < 148 * 8 && P.ny / (segs * 2) >= 8)
+    segs *= 2;
+  const int rows = (P.ny + segs - 1) / segs;
+  dim3 grid(strips, (P.ny + rows - 1) / rows, n_intervals);
+  dim3 block(32 * S);
+  switch (mode)
+    {
+      case 0: vmult_kernel<R, S, false, false><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
+      case 1: vmult_kernel<R, S, true, false><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
+      default: vmult_kernel<R, S, false, true><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
+    }
+  return cudaGetLastError();
+}
+
+} // namespace vmult_detail
+} // namespace stmg_b200

@@ -1,0 +1,214 @@
+"""GPU tier: the sm_100a kernels through the C ABI against the oracle on the
+same seeded inputs. Tolerances are the north star's: vmult relative
+max-norm <= 1e-12, smoother step <= 1e-10, solve iterations within +-1 and
+solution relative L2 <= 1e-8."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_ctypes as oc
+
+pytestmark = pytest.mark.gpu
+
+VMULT_TOL = 1e-12
+SMOOTH_TOL = 1e-10
+
+
+def rel_max(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+LEVEL_CASES = [
+    # nc, r, k, tau, nu, gamma
+    (1, 1, 1, 0.25, 0.1, 1.0),
+    (2, 1, 1, 0.25, 0.1, 0.0),
+    (4, 2, 2, 0.25, 0.1, 1.0),
+    (4, 3, 1, 0.5, 0.1, 0.7),
+    (8, 1, 0, 0.125, 1.0, 1.0),
+    (16, 1, 1, 0.125, 1.0, 1.0),   # C1 discretisation
+    (32, 2, 2, 1 / 64, 1.0, 1.0),  # C2 discretisation, 2 strips
+    (64, 1, 1, 1 / 64, 1.0, 1.0),  # 3 strips, row segments
+    (4, 4, 4, 0.25, 0.1, 1.0),
+    (8, 2, 3, 0.3, 0.5, 0.0),
+]
+
+
+@pytest.mark.parametrize("nc,r,k,tau,nu,gamma", LEVEL_CASES)
+def test_apply_block_matches_oracle(ctx, stmg, nc, r, k, tau, nu, gamma):
+    lvl = stmg.Level(ctx, nc, nc, r, k, tau, nu, gamma, stmg.SMOOTHER_NONE)
+    ref = oc.OracleLevel(nc, r, k, tau, nu, gamma, build_smoother=False)
+    assert lvl.size == ref.size
+    for seed, raw in ((1, False), (2, True)):
+        x = oc.seeded(ref.size, seed)
+        y = torch.zeros(lvl.size, dtype=torch.float64, device="cuda")
+        lvl.apply_block(dev(x), y, raw=raw)
+        err = rel_max(host(y), ref.apply_block(x, raw=raw))
+        assert err <= VMULT_TOL, err
+
+
+@pytest.mark.parametrize("nc,r,k,tau,nu,gamma", [c for c in LEVEL_CASES if c[0] >= 2])
+def test_all_at_once_vmult_with_coupling(ctx, stmg, nc, r, k, tau, nu, gamma):
+    """y_n = D x_n - Z C x_{n-1}[slot k] over N intervals plus the halo slot."""
+    N = 5
+    lvl = stmg.Level(ctx, nc, nc, r, k, tau, nu, gamma, stmg.SMOOTHER_NONE)
+    ref = oc.OracleLevel(nc, r, k, tau, nu, gamma, build_smoother=False)
+    x = oc.seeded(N * ref.size, 11)
+    halo = oc.seeded(ref.n_velocity, 12)
+    y = torch.zeros(N * lvl.size, dtype=torch.float64, device="cuda")
+    lvl.vmult(dev(x), y, N, dev(halo))
+    err = rel_max(host(y), ref.vmult_all(x, N, halo))
+    assert err <= VMULT_TOL, err
+    # residual form b - A x
+    b = oc.seeded(N * ref.size, 13)
+    r_ = torch.zeros_like(y)
+    lvl.residual(dev(b), dev(x), r_, N, dev(halo), coupled=True)
+    err = rel_max(host(r_), b - ref.vmult_all(x, N, halo))
+    assert err <= VMULT_TOL, err
+
+
+def test_coupling_rhs_matches_oracle(ctx, stmg):
+    lvl = stmg.Level(ctx, 8, 8, 2, 2, 0.25, 0.1, 1.0, stmg.SMOOTHER_NONE)
+    ref = oc.OracleLevel(8, 2, 2, 0.25, 0.1, 1.0, build_smoother=False)
+    v = oc.seeded(ref.n_velocity, 5)
+    out = torch.zeros(lvl.size, dtype=torch.float64, device="cuda")
+    lvl.coupling_rhs(dev(v), out)
+    assert rel_max(host(out), ref.coupling_rhs(v)) <= VMULT_TOL
+
+
+SMOOTH_CASES = [
+    (4, 1, 1, 0),
+    (4, 2, 2, 0),
+    (8, 1, 1, 1),
+    (4, 2, 1, 1),
+    (16, 1, 1, 0),
+    (32, 2, 2, 0),
+    (1, 2, 1, 0),   # whole-domain patch: pseudo-inverse (min-norm, vanka.cpp:167-176)
+    (2, 3, 2, 0),
+]
+
+
+@pytest.mark.parametrize("nc,r,k,kind", SMOOTH_CASES)
+def test_apply_additive_matches_oracle(ctx, stmg, nc, r, k, kind):
+    tau, nu, gamma = 0.25, 0.1, 1.0
+    lvl = stmg.Level(ctx, nc, nc, r, k, tau, nu, gamma, kind)
+    ref = oc.OracleLevel(nc, r, k, tau, nu, gamma, kind)
+    res = oc.seeded(ref.size, 21)
+    out = torch.zeros(lvl.size, dtype=torch.float64, device="cuda")
+    lvl.apply_additive(dev(res), out)
+    err = rel_max(host(out), ref.apply_additive(res))
+    assert err <= SMOOTH_TOL, err
+
+
+@pytest.mark.parametrize("nc,r,k,kind", [c for c in SMOOTH_CASES if c[0] >= 2])
+def test_smooth_step_all_at_once_matches_oracle(ctx, stmg, nc, r, k, kind):
+    N, tau, nu, gamma, omega = 3, 0.25, 0.1, 1.0, 0.8
+    lvl = stmg.Level(ctx, nc, nc, r, k, tau, nu, gamma, kind)
+    ref = oc.OracleLevel(nc, r, k, tau, nu, gamma, kind)
+    b = oc.seeded(N * ref.size, 31)
+    u = oc.seeded(N * ref.size, 32)
+    halo = oc.seeded(ref.n_velocity, 33)
+    ud = dev(u)
+    lvl.smooth_step(dev(b), ud, omega, N, dev(halo), coupled=True)
+    err = rel_max(host(ud), ref.smooth_step_all(b, u, omega, N, halo))
+    assert err <= SMOOTH_TOL, err
+
+
+def test_smooth_step_rejects_bad_omega(ctx, stmg):
+    lvl = stmg.Level(ctx, 4, 4, 1, 1, 0.25, 0.1, 1.0, stmg.SMOOTHER_CELL)
+    v = torch.zeros(lvl.size, dtype=torch.float64, device="cuda")
+    for omega in (0.0, 1.5):
+        with pytest.raises(stmg.StmgError) as e:
+            lvl.smooth_step(v, v.clone(), omega)
+        assert e.value.code == 1
+
+
+SOLVER_CASES = [
+    # refinements, r, k, nu, gamma, smoother, nu1, nu2, h_only
+    (2, 1, 1, 0.1, 1.0, 0, 1, 1, False),
+    (2, 2, 2, 0.1, 1.0, 0, 1, 1, False),
+    (3, 2, 2, 1.0, 1.0, 0, 2, 2, False),
+    (2, 2, -1, 0.1, 1.0, 0, 1, 1, True),
+    (2, 1, 1, 0.1, 1.0, 1, 1, 1, False),
+    (4, 1, 1, 1.0, 1.0, 0, 2, 2, False),   # C1: 16x16, Q2/P1, DG(1), V(2,2)
+]
+
+
+def _consistent(sol, ref, seed, n_intervals=1):
+    lv = sol.finest
+    ncell = lv.n_pressure // ((ref.levels[-1]["r"] + 1) * (ref.levels[-1]["r"] + 2) // 2)
+    npc = lv.n_pressure // ncell
+    v = oc.seeded(n_intervals * lv.size, seed)
+    return oc.make_consistent(v, lv.n_slots, lv.n_scalar, lv.grid_x, lv.n_pressure, ncell, npc, n_intervals)
+
+
+@pytest.mark.parametrize("c,r,k,nu,gamma,kind,nu1,nu2,h_only", SOLVER_CASES)
+def test_transfers_and_coarse_solve_match_oracle(ctx, stmg, c, r, k, nu, gamma, kind, nu1, nu2, h_only):
+    sol = stmg.Solver(ctx, c, r, k, nu=nu, gamma=gamma, smoother=kind, nu1=nu1, nu2=nu2, h_only=h_only)
+    ref = oc.OracleSolver(c, r, k, nu=nu, gamma=gamma, smoother=kind, nu1=nu1, nu2=nu2, h_only=h_only)
+    assert sol.n_levels == ref.n_levels
+    for l in range(1, sol.n_levels):
+        fine = oc.seeded(ref.levels[l]["size"], 40 + l)
+        coarse = oc.seeded(ref.levels[l - 1]["size"], 60 + l)
+        cd = torch.zeros(ref.levels[l - 1]["size"], dtype=torch.float64, device="cuda")
+        sol.restrict_residual(l, dev(fine), cd, True)
+        assert rel_max(host(cd), ref.restrict_residual(l, fine)) <= 1e-12
+        fd = torch.zeros(ref.levels[l]["size"], dtype=torch.float64, device="cuda")
+        sol.prolongate_correction(l, dev(coarse), fd, True)
+        assert rel_max(host(fd), ref.prolongate_correction(l, coarse)) <= 1e-12
+
+
+@pytest.mark.parametrize("c,r,k,nu,gamma,kind,nu1,nu2,h_only", SOLVER_CASES)
+def test_vcycle_and_gmres_match_oracle(ctx, stmg, c, r, k, nu, gamma, kind, nu1, nu2, h_only):
+    sol = stmg.Solver(ctx, c, r, k, nu=nu, gamma=gamma, smoother=kind, nu1=nu1, nu2=nu2, h_only=h_only)
+    ref = oc.OracleSolver(c, r, k, nu=nu, gamma=gamma, smoother=kind, nu1=nu1, nu2=nu2, h_only=h_only)
+    b = _consistent(sol, ref, 77)
+    x = torch.zeros(sol.finest.size, dtype=torch.float64, device="cuda")
+    sol.vcycle(dev(b), x)
+    assert rel_max(host(x), ref.vcycle(b)) <= SMOOTH_TOL
+    it, hist = sol.gmres(dev(b), x)
+    xr, itr, histr = ref.gmres(b)
+    assert abs(it - itr) <= 1, (it, itr)
+    xs = host(x)
+    assert np.linalg.norm(xs - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+@pytest.mark.parametrize("c,r,k,nu,gamma,kind,nu1,nu2,h_only", [SOLVER_CASES[0], SOLVER_CASES[5]])
+def test_time_march_matches_oracle(ctx, stmg, c, r, k, nu, gamma, kind, nu1, nu2, h_only):
+    """Seeded time marching (C1 = last case): per-step iterations within +-1,
+    trajectory relative L2 <= 1e-8 after the per-slot mean-zero projection."""
+    n_steps = 8
+    sol = stmg.Solver(ctx, c, r, k, n_steps=n_steps, nu=nu, gamma=gamma, smoother=kind, nu1=nu1, nu2=nu2,
+                      h_only=h_only)
+    ref = oc.OracleSolver(c, r, k, n_steps=n_steps, nu=nu, gamma=gamma, smoother=kind, nu1=nu1, nu2=nu2,
+                          h_only=h_only)
+    F = _consistent(sol, ref, 99, n_steps)
+    X = torch.zeros(n_steps * sol.finest.size, dtype=torch.float64, device="cuda")
+    iters = sol.time_march(dev(F), X)
+    Xr, itr, _ = ref.time_march(F)
+    assert all(abs(a - b) <= 1 for a, b in zip(iters, itr)), (iters, itr)
+    Xs = host(X)
+    assert np.linalg.norm(Xs - Xr) <= 1e-8 * np.linalg.norm(Xr)
+    # host-buffer entry point gives the same trajectory
+    Xh = np.zeros_like(F)
+    iters_h = sol.time_march_host(F, Xh)
+    assert iters_h == iters
+    assert np.linalg.norm(Xh - Xs) <= 1e-12 * np.linalg.norm(Xs)
+
+
+def test_kernels_really_launch(ctx, stmg):
+    before = ctx.launch_count()
+    lvl = stmg.Level(ctx, 16, 16, 1, 1, 0.125, 1.0, 1.0, stmg.SMOOTHER_CELL)
+    x = torch.rand(lvl.size, dtype=torch.float64, device="cuda")
+    y = torch.zeros_like(x)
+    lvl.vmult(x, y)
+    lvl.smooth_step(x, y, 0.8)
+    assert ctx.launch_count() - before >= 1 + 1 + 4
