@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hp-STMG hot path (BASELINE.json configs[1], "C2").
+
+Workload (one step): the all-at-once space-time operator vmult plus one cell
+Vanka smoother step, over the full C2 system: 2D Stokes, Q3/P2disc (r=2),
+DG(2), Cartesian 256x256 mesh, 64 intervals on [0,1], nu=1, gamma=1, FP64,
+3.03e8 space-time dofs per GPU, seeded uniform[-1,1] inputs resident in HBM.
+Local Vanka inverses are precomputed once and shared by all intervals.
+
+  value   = space-time dofs processed per second by the whole job
+            (n_gpus * dofs_per_gpu / ms_per_step), step = vmult + smoother step
+  e2e     = the same step through the host-buffer C-ABI entry points
+            (stmg_vmult_host + stmg_smooth_step_host), H2D/D2H inside
+  --gpus N: one process per GPU (torchrun), time slabs of 64 intervals per
+            rank (weak scaling); the DG jump couples rank p to p-1 through the
+            slot-k velocity halo, exchanged with NCCL send/recv every vmult
+            and smoother residual.
+  --impl reference: the CPU restatement of the reference (oracle/, OpenMP over
+            intervals on all host cores) on a bounded sample of the same
+            discretisation; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG = dict(workload="C2: all-at-once vmult + cell-Vanka smoother step", mesh="256x256", r=2, k=2,
+              intervals_per_gpu=64, nu=1.0, gamma=1.0, omega=0.8, domain="unit square x (0,1]")
+METRIC = "space-time DoF/s: matrix-free vmult, Vanka step, full hp-STMG solve"
+UNIT = "DoF/s"
+
+
+def peaks():
+    hbm, fp64, src = 6443.2, 36.77, []
+    try:
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        hbm = float(mp["hbm_gbs"])
+        src.append("MEASURED_PEAKS.json hbm_gbs")
+    except Exception:
+        src.append("fallback hbm 6443")
+    for f in sorted((ROOT / "profiles").glob("fp64_peaks_r*.json")):
+        try:
+            line = f.read_text().strip().splitlines()[0]
+            fp64 = float(json.loads(line)["dfma_tflops"])
+            src.append(f"{f.name} dfma_tflops")
+        except Exception:
+            pass
+    return hbm, fp64, ", ".join(src)
+
+
+def vmult_fma_per_cell(r, k, coupled=True):
+    """FMAs of the fused vmult kernel per cell and interval (all output slots),
+    excluding the 1/31 + 1/rows halo recompute (see vmult_impl.cuh)."""
+    N1, NP, PL, S = r + 2, (r + 1) * (r + 2) // 2, r + 1, k + 1
+    per_slot = S * NP + 2 * N1 * NP + 2 * PL * N1 * N1 + N1 * (
+        4 * S * N1 + (2 * N1 if coupled else 0) + 8 * N1 * N1 + 6 * N1 * N1 + 2 * PL * N1 + 2 * NP)
+    return per_slot * S
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "power_w_max": max(float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()),
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_ctypes as oc
+
+    threads = os.cpu_count() or 1
+    nc, n_int = 64, 8  # bounded sample of the C2 discretisation
+    lvl = oc.OracleLevel(nc, CONFIG["r"], CONFIG["k"], 1.0 / 64, CONFIG["nu"], CONFIG["gamma"], 0)
+    dofs = n_int * lvl.size
+    x = oc.seeded(dofs, 1)
+    b = oc.seeded(dofs, 2)
+    halo = oc.seeded(lvl.n_velocity, 3)
+    u = x.copy()
+    for _ in range(args.warmup):
+        lvl.vmult_all(x, n_int, halo, threads)
+        u = lvl.smooth_step_all(b, u, CONFIG["omega"], n_int, halo, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        lvl.vmult_all(x, n_int, halo, threads)
+        u = lvl.smooth_step_all(b, u, CONFIG["omega"], n_int, halo, threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = dofs / dt
+    sample = (f"oracle port of the reference (C++ restatement, OpenMP over intervals) on {nc}x{nc} cells, "
+              f"r=2, k=2, {n_int} intervals ({dofs} dofs) per step; per-dof rate of the C2 workload")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1])",
+            "config": dict(CONFIG, workload=CONFIG["workload"] + " (CPU sample)"),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_quick():
+    """Bounded oracle sample for the cpu_baseline field of our own line."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_ctypes as oc
+
+    threads = os.cpu_count() or 1
+    nc, n_int = 32, 8
+    lvl = oc.OracleLevel(nc, CONFIG["r"], CONFIG["k"], 1.0 / 64, CONFIG["nu"], CONFIG["gamma"], 0)
+    dofs = n_int * lvl.size
+    x, b = oc.seeded(dofs, 1), oc.seeded(dofs, 2)
+    halo = oc.seeded(lvl.n_velocity, 3)
+    lvl.vmult_all(x, n_int, halo, threads)
+    t0 = time.perf_counter()
+    reps = 2
+    u = x
+    for _ in range(reps):
+        lvl.vmult_all(x, n_int, halo, threads)
+        u = lvl.smooth_step_all(b, u, CONFIG["omega"], n_int, halo, threads)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": dofs / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle (C++ restatement of the reference) on {nc}x{nc} cells, r=2, k=2, {n_int} intervals, "
+                      f"vmult + Vanka step, OpenMP over intervals, {reps} steps"}
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=256)
+    ap.add_argument("--intervals", type=int, default=64)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_09159_b200 as stmg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = stmg.Context(local)
+    nx, N, r, k = args.nx, args.intervals, CONFIG["r"], CONFIG["k"]
+    tau = 1.0 / (N * world)
+    lvl = stmg.Level(ctx, nx, nx, r, k, tau, CONFIG["nu"], CONFIG["gamma"], stmg.SMOOTHER_CELL)
+    isz, mv, S = lvl.size, lvl.n_velocity, lvl.n_slots
+    dofs = N * isz
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1234 + rank)
+    x = torch.rand(dofs, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    b = torch.rand(dofs, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    u = torch.rand(dofs, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    y = torch.empty_like(x)
+    res = torch.empty_like(x)
+    halo_x = torch.zeros(mv, dtype=torch.float64, device="cuda")
+    halo_u = torch.zeros(mv, dtype=torch.float64, device="cuda")
+    last_slot = slice((N - 1) * isz + (S - 1) * mv, (N - 1) * isz + S * mv)
+
+    def exchange(src, dst):
+        """time-slab halo: slot-k velocity of my last interval -> rank+1."""
+        if world == 1:
+            return
+        ops = []
+        if rank + 1 < world:
+            ops.append(dist.P2POp(dist.isend, src[last_slot].contiguous(), rank + 1))
+        if rank > 0:
+            ops.append(dist.P2POp(dist.irecv, dst, rank - 1))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+    first = rank == 0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    t_vmult, t_resid, t_vanka = [], [], []
+
+    def step(record):
+        exchange(x, halo_x)
+        if record:
+            ev[0].record()
+        lvl.vmult(x, y, N, None if first and world == 1 else halo_x)
+        if record:
+            ev[1].record()
+        exchange(u, halo_u)
+        lvl.residual(b, u, res, N, None if first and world == 1 else halo_u, coupled=True)
+        if record:
+            ev[2].record()
+        lvl.vanka_update(res, u, CONFIG["omega"], N)
+        if record:
+            ev[3].record()
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record()
+        for _ in range(args.steps):
+            step(True)
+            torch.cuda.synchronize()  # per-step event readout (kernel shares below)
+            t_vmult.append(ev[0].elapsed_time(ev[1]))
+            t_resid.append(ev[1].elapsed_time(ev[2]))
+            t_vanka.append(ev[2].elapsed_time(ev[3]))
+        stop.record()
+        torch.cuda.synchronize()
+    gpu_launches = ctx.launch_count() - launches0
+    ms = start.elapsed_time(stop) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = world * dofs / (ms * 1e-3)
+
+    # ---- end to end through the host-buffer C ABI (pinned host memory)
+    e2e = None
+    if args.e2e_steps > 0:
+        hx = torch.empty(dofs, dtype=torch.float64, pin_memory=True)
+        hb = torch.empty(dofs, dtype=torch.float64, pin_memory=True)
+        hu = torch.empty(dofs, dtype=torch.float64, pin_memory=True)
+        hy = torch.empty(dofs, dtype=torch.float64, pin_memory=True)
+        hh = torch.empty(mv, dtype=torch.float64, pin_memory=True)
+        hx.copy_(x)
+        hb.copy_(b)
+        hu.copy_(u)
+        hh.zero_()
+        nx_, nb_, nu_, ny_, nh_ = hx.numpy(), hb.numpy(), hu.numpy(), hy.numpy(), hh.numpy()
+        halo_arg = None if first and world == 1 else nh_
+        lvl.vmult_host(nx_, ny_, N, halo_arg)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            lvl.vmult_host(nx_, ny_, N, halo_arg)
+            lvl.smooth_step_host(nb_, nu_, CONFIG["omega"], N, halo_arg, True)
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * (3 * dofs + 2 * mv),
+               "d2h_bytes_per_step": 8 * 2 * dofs}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    hbm, fp64, peak_src = peaks()
+    ncell = nx * nx
+    vm_ms = statistics.mean(t_vmult)
+    rs_ms = statistics.mean(t_resid)
+    vk_ms = statistics.mean(t_vanka)
+    vm_flops = 2.0 * vmult_fma_per_cell(r, k) * ncell * N
+    vm_bytes = 16.0 * dofs
+    sum_nt2 = lvl.total_matrix_elements
+    vk_flops = 2.0 * sum_nt2 * N
+    vk_bytes = 24.0 * dofs
+    kernels = {
+        "vmult": {"ms": vm_ms, "GB/s": vm_bytes / vm_ms / 1e6, "TFLOP/s": vm_flops / vm_ms / 1e9,
+                  "algorithmic_bytes": vm_bytes, "algorithmic_flops": vm_flops},
+        "residual": {"ms": rs_ms, "GB/s": 24.0 * dofs / rs_ms / 1e6, "TFLOP/s": vm_flops / rs_ms / 1e9},
+        "vanka_update": {"ms": vk_ms, "GB/s": vk_bytes / vk_ms / 1e6, "TFLOP/s": vk_flops / vk_ms / 1e9,
+                         "algorithmic_bytes": vk_bytes, "algorithmic_flops": vk_flops, "launches": 4},
+    }
+    dom = "vanka_update" if vk_ms >= vm_ms else "vmult"
+    kd = kernels[dom]
+    # both candidate roofs; the binding one is the larger time bound
+    t_hbm = kd["algorithmic_bytes"] / (hbm * 1e9)
+    t_fp = kd["algorithmic_flops"] / (fp64 * 1e12)
+    if t_fp >= t_hbm:
+        roof = {"bound": "fp64", "achieved": kd["TFLOP/s"], "peak": fp64, "unit": "TFLOP/s",
+                "frac": kd["TFLOP/s"] / fp64}
+    else:
+        roof = {"bound": "hbm", "achieved": kd["GB/s"], "peak": hbm, "unit": "GB/s", "frac": kd["GB/s"] / hbm}
+    roof.update({"kernel": dom, "traffic": None, "peak_source": peak_src,
+                 "hbm_frac": kd["GB/s"] / hbm, "fp64_frac": kd["TFLOP/s"] / fp64})
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1], torch Philox on device)",
+            "config": dict(CONFIG, mesh=f"{nx}x{nx}", intervals_per_gpu=N, dofs_per_gpu=dofs,
+                           parallelism=f"time-slab dp{world}" if world > 1 else "single GPU",
+                           l2="inputs 2.4 GB per vector >> 126 MB L2 (no flush needed)"),
+            "components": {"vmult_dofs_per_s": world * dofs / (vm_ms * 1e-3),
+                           "vanka_step_dofs_per_s": world * dofs / ((rs_ms + vk_ms) * 1e-3)},
+            "kernels": kernels, "roofline": roof, "gpu_launches": gpu_launches,
+            "clocks": clk.summary(), "e2e": e2e}
+    if not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_quick()
+        except Exception as exc:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"failed: {exc}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

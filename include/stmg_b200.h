@@ -104,6 +104,10 @@ int stmg_apply_additive(stmg_level *level, const double *r, double *out, int n_i
 int stmg_smooth_step(stmg_level *level, const double *b, double *u, double omega, int n_intervals,
                      const double *x_prev_slot, int coupled, double *work);
 
+/* u += omega * apply_additive(r): the patch-solve half of smooth_step
+ * (vanka.cpp:229-232) for a precomputed residual r. */
+int stmg_vanka_update(stmg_level *level, const double *r, double *u, double omega, int n_intervals);
+
 /* Host-buffer variants of stmg_vmult / stmg_smooth_step: copy in, run,
  * copy out, synchronise (the end-to-end path a CPU caller binds). */
 int stmg_vmult_host(stmg_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);

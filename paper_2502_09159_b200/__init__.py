@@ -58,6 +58,7 @@ _SIGNATURES = {
     "stmg_coupling_rhs": ([_c_void_p, _c_void_p, _c_void_p], _c_int),
     "stmg_apply_additive": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
     "stmg_smooth_step": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int, _c_void_p], _c_int),
+    "stmg_vanka_update": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int], _c_int),
     "stmg_vmult_host": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
     "stmg_smooth_step_host": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int], _c_int),
     "stmg_solver_create": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
@@ -203,6 +204,10 @@ class Level:
                     work=None):
         _check(load_library().stmg_smooth_step(self._h, _ptr(b), _ptr(u), omega, n_intervals, _ptr(x_prev_slot),
                                                int(coupled), _ptr(work)))
+        return u
+
+    def vanka_update(self, residual, u, omega: float, n_intervals: int = 1):
+        _check(load_library().stmg_vanka_update(self._h, _ptr(residual), _ptr(u), omega, n_intervals))
         return u
 
     # -- host-buffer (end-to-end) variants

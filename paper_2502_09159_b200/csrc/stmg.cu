@@ -734,6 +734,16 @@ stmg_smooth_step(stmg_level *L, const double *b, double *u, double omega, int n,
 }
 
 int
+stmg_vanka_update(stmg_level *L, const double *r, double *u, double omega, int n)
+{
+  return guarded([&] {
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("vanka_update: omega must be in (0, 1]");
+    L->vanka(r, u, n, omega);
+  });
+}
+
+int
 stmg_vmult_host(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot)
 {
   return guarded([&] {

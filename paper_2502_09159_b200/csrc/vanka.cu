@@ -113,6 +113,163 @@ vanka_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__rest
         }
     }
 }
+
+// ---------------------------------------------------------------------------
+// DMMA path (n_T <= 128): the class inverse lives in registers as FP64 tensor
+// core A-fragments (warp w owns rows 8w..8w+7), residual columns are staged
+// in shared memory as B-fragments, Z = A^{-1} R runs on mma.m8n8k4.f64.
+// Gather of tile t+1 and the read half of the scatter of tile t are issued
+// before the MMAs of tile t (register prefetch), so their latency overlaps
+// the tensor-core work.
+constexpr int kDThreads = 512;            // 16 warps
+constexpr int kDRows = 128;               // max n_T
+constexpr int kDK = 32;                   // max k-steps (K <= 128)
+constexpr int kDCols = 32;                // columns per tile
+constexpr int kDRLd = 40;                 // R tile pitch (doubles): conflict-free B-fragment loads
+constexpr int kDZLd = 33;                 // Z tile pitch
+constexpr int kDPer = kDRows * kDCols / kDThreads; // elements per thread per tile (8)
+constexpr int kDGroup = 16;               // intervals per block
+
+__device__ __forceinline__ void
+dmma_8x8x4(double (&d)[2], double a, double b)
+{
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kDThreads, 1)
+vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
+                  const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
+                  const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals, double omega)
+{
+  extern __shared__ __align__(16) double dsm[];
+  double *Rs = dsm;                                   // kDRows x kDRLd
+  double *Zs = Rs + kDRows * kDRLd;                   // kDRows x kDZLd
+  double *w_s = Zs + kDRows * kDZLd;                  // kDRows
+  long long *rel_s = reinterpret_cast<long long *>(w_s + kDRows); // kDRows
+
+  const VankaBatch bt = batches[blockIdx.x];
+  const DevPatchClass pc = classes[bt.cls];
+  const int nt = pc.n_t, nvel = pc.n_vel;
+  const int n0 = blockIdx.y * kDGroup;
+  const int ng = min(kDGroup, n_intervals - n0);
+  const int ncols = bt.count * ng;
+  const int ntiles = (ncols + kDCols - 1) / kDCols;
+  const int ksteps = (nt + 3) >> 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (int i = tid; i < kDRows; i += kDThreads)
+    {
+      rel_s[i] = i < nt ? pc.rel[i] : 0;
+      w_s[i] = i < nt ? omega * pc.weight[i] : 0.0;
+    }
+  // A fragments of this warp's row tile (m8n8k4 .row: row = lane/4, col = lane%4)
+  double afr[kDK];
+  {
+    const int arow = 8 * warp + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < kDK; ++kk)
+      {
+        const int col = 4 * kk + (lane & 3);
+        afr[kk] = (arow < nt && col < nt) ? __ldg(pc.inverse + arow * nt + col) : 0.0;
+      }
+  }
+  __syncthreads();
+
+  // element q of this thread: row i = (tid + q*kDThreads) / kDCols, column c = tid % kDCols
+  const int c = tid & (kDCols - 1);
+  const int i0 = tid >> 5; // kDCols == 32
+  auto addr_of = [&](int i, int j) -> long long {
+    const int patch = j / ng, n = n0 + j - patch * ng;
+    const long long anchor = i < nvel ? __ldg(vel_anchor + bt.first + patch) : __ldg(pre_anchor + bt.first + patch);
+    return n * isz + anchor + rel_s[i];
+  };
+
+  double g[kDPer];
+  {
+    const int j = c;
+#pragma unroll
+    for (int q = 0; q < kDPer; ++q)
+      {
+        const int i = i0 + q * (kDThreads / kDCols);
+        g[q] = (i < nt && j < ncols) ? __ldg(r + addr_of(i, j)) : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < kDPer; ++q)
+      Rs[(i0 + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
+  }
+  __syncthreads();
+
+  for (int t = 0; t < ntiles; ++t)
+    {
+      // prefetch: old u of this tile and the residual of the next tile
+      double uo[kDPer];
+      {
+        const int j = t * kDCols + c;
+#pragma unroll
+        for (int q = 0; q < kDPer; ++q)
+          {
+            const int i = i0 + q * (kDThreads / kDCols);
+            uo[q] = (i < nt && j < ncols) ? u[addr_of(i, j)] : 0.0;
+          }
+      }
+      if (t + 1 < ntiles)
+        {
+          const int j = (t + 1) * kDCols + c;
+#pragma unroll
+          for (int q = 0; q < kDPer; ++q)
+            {
+              const int i = i0 + q * (kDThreads / kDCols);
+              g[q] = (i < nt && j < ncols) ? __ldg(r + addr_of(i, j)) : 0.0;
+            }
+        }
+      // Z = A^{-1} R on the FP64 tensor path
+      if (8 * warp < nt)
+        {
+          double acc[kDCols / 8][2];
+#pragma unroll
+          for (int ct = 0; ct < kDCols / 8; ++ct)
+            acc[ct][0] = acc[ct][1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < kDK; ++kk)
+            {
+              if (kk < ksteps)
+                {
+                  const double *brow = Rs + (4 * kk + (lane & 3)) * kDRLd + (lane >> 2);
+#pragma unroll
+                  for (int ct = 0; ct < kDCols / 8; ++ct)
+                    dmma_8x8x4(acc[ct], afr[kk], brow[8 * ct]);
+                }
+            }
+          const int row = 8 * warp + (lane >> 2);
+          const double wr = w_s[row];
+#pragma unroll
+          for (int ct = 0; ct < kDCols / 8; ++ct)
+            {
+              const int col = 8 * ct + 2 * (lane & 3);
+              Zs[row * kDZLd + col] = acc[ct][0] * wr;
+              Zs[row * kDZLd + col + 1] = acc[ct][1] * wr;
+            }
+        }
+      __syncthreads();
+      {
+        const int j = t * kDCols + c;
+#pragma unroll
+        for (int q = 0; q < kDPer; ++q)
+          {
+            const int i = i0 + q * (kDThreads / kDCols);
+            if (i < nt && j < ncols)
+              u[addr_of(i, j)] = uo[q] + Zs[i * kDZLd + c];
+          }
+      }
+      if (t + 1 < ntiles)
+#pragma unroll
+        for (int q = 0; q < kDPer; ++q)
+          Rs[(i0 + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
+      __syncthreads();
+    }
+}
 } // namespace
 
 /// Launch one colour: `n_batches` batches over `n_intervals` intervals.
@@ -123,6 +280,20 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, int
 {
   if (n_batches == 0 || n_intervals == 0)
     return cudaSuccess;
+  if (max_nt <= kDRows)
+    {
+      static bool dattr = false;
+      const size_t dsmem = sizeof(double) * (kDRows * kDRLd + kDRows * kDZLd + 2 * kDRows);
+      if (!dattr)
+        {
+          cudaFuncSetAttribute(vanka_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
+          dattr = true;
+        }
+      dim3 grid(n_batches, (n_intervals + kDGroup - 1) / kDGroup);
+      vanka_dmma_kernel<<<grid, kDThreads, dsmem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz,
+                                                            n_intervals, omega);
+      return cudaGetLastError();
+    }
   const int ntp = (max_nt + 1) & ~1;
   size_t smem = sizeof(double) * (static_cast<size_t>(max_nt) * ntp + static_cast<size_t>(ntp) * kVankaCols);
   int in_smem = 1;
