@@ -86,7 +86,7 @@ def load_library(path: Optional[os.PathLike] = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("STMG_LIB", str(LIB_PATH)))
     if not p.exists():
         raise RuntimeError(f"stmg_b200: CUDA library {p} missing — run __graft_entry__.build() "
                            "(there is no CPU fallback)")

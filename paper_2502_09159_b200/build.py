@@ -50,12 +50,13 @@ def _stale(obj: Path, src: Path) -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
+    extra = os.environ.get("STMG_DEFS", "").split()  # experiment switches, e.g. -DSTMG_VMULT_SPLIT=1
     jobs = []
     for name in SOURCES:
         src = CSRC / name
         obj = BUILD / (name + ".o")
         if force or _stale(obj, src):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *_host_cxx(), "-c", str(src), "-o", str(obj)]
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, *_host_cxx(), "-c", str(src), "-o", str(obj)]
             if name.endswith(".cpp"):
                 cmd[1:1] = ["-x", "cu"]
             jobs.append((name, cmd))

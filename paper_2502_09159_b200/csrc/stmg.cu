@@ -202,6 +202,8 @@ build_level(stmg_level &L)
     throw std::invalid_argument("stmg_level: k must be in 0..4");
   if (s.nx < 1 || s.ny < 1)
     throw std::invalid_argument("stmg_level: need at least one cell per direction");
+  if (s.isz() >= (1ll << 31))
+    throw std::invalid_argument("stmg_level: one interval must hold fewer than 2^31 dofs (int32 patch offsets)");
   if (!(s.tau > 0.0))
     throw std::invalid_argument("stmg_level: tau must be positive");
   L.consts = make_level_consts(s);

@@ -123,12 +123,15 @@ vanka_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__rest
 // the tensor-core work.
 constexpr int kDThreads = 512;            // 16 warps
 constexpr int kDRows = 128;               // max n_T
-constexpr int kDK = 32;                   // max k-steps (K <= 128)
-constexpr int kDCols = 32;                // columns per tile
-constexpr int kDRLd = 40;                 // R tile pitch (doubles): conflict-free B-fragment loads
+#ifndef STMG_VANKA_COLS
+#define STMG_VANKA_COLS 16
+#endif
+constexpr int kDCols = STMG_VANKA_COLS;   // columns per tile
+constexpr int kDRLd = 36;                 // R tile pitch (doubles): conflict-free B-fragment loads
 constexpr int kDZLd = 33;                 // Z tile pitch
 constexpr int kDPer = kDRows * kDCols / kDThreads; // elements per thread per tile (8)
 constexpr int kDGroup = 16;               // intervals per block
+constexpr long long kNoCol = -(1ll << 62); // column-base sentinel (anchors may be negative)
 
 __device__ __forceinline__ void
 dmma_8x8x4(double (&d)[2], double a, double b)
@@ -138,16 +141,17 @@ dmma_8x8x4(double (&d)[2], double a, double b)
                : "d"(a), "d"(b));
 }
 
+template <int KS>
 __global__ void __launch_bounds__(kDThreads, 1)
 vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
                   const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
                   const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals, double omega)
 {
   extern __shared__ __align__(16) double dsm[];
-  double *Rs = dsm;                                   // kDRows x kDRLd
-  double *Zs = Rs + kDRows * kDRLd;                   // kDRows x kDZLd
-  double *w_s = Zs + kDRows * kDZLd;                  // kDRows
-  long long *rel_s = reinterpret_cast<long long *>(w_s + kDRows); // kDRows
+  double *Rs = dsm;                                                 // kDRows x kDRLd
+  double *Zs = Rs + kDRows * kDRLd;                                 // kDRows x kDZLd
+  double *w_s = Zs + kDRows * kDZLd;                                // kDRows
+  long long *cb = reinterpret_cast<long long *>(w_s + kDRows);     // [3][2][kDCols] column bases
 
   const VankaBatch bt = batches[blockIdx.x];
   const DevPatchClass pc = classes[bt.cls];
@@ -156,72 +160,91 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
   const int ng = min(kDGroup, n_intervals - n0);
   const int ncols = bt.count * ng;
   const int ntiles = (ncols + kDCols - 1) / kDCols;
-  const int ksteps = (nt + 3) >> 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = tid % kDCols;        // column of this thread in every tile
+  const int ibase = tid / kDCols;    // first row of this thread (rows ibase + q * kDThreads / kDCols)
+
+  // column bases of tile t: interval base + velocity / pressure anchor
+  auto column_bases = [&](int t) {
+    if (tid < kDCols && t < ntiles)
+      {
+        const int j = t * kDCols + tid;
+        long long vb = kNoCol, pb = kNoCol;
+        if (j < ncols)
+          {
+            const int patch = j / ng, n = n0 + j - patch * ng;
+            vb = n * isz + __ldg(vel_anchor + bt.first + patch);
+            pb = n * isz + __ldg(pre_anchor + bt.first + patch);
+          }
+        cb[(t % 3) * 2 * kDCols + tid] = vb;
+        cb[(t % 3) * 2 * kDCols + kDCols + tid] = pb;
+      }
+  };
 
   for (int i = tid; i < kDRows; i += kDThreads)
-    {
-      rel_s[i] = i < nt ? pc.rel[i] : 0;
-      w_s[i] = i < nt ? omega * pc.weight[i] : 0.0;
-    }
+    w_s[i] = i < nt ? omega * pc.weight[i] : 0.0;
+  column_bases(0);
+  column_bases(1);
   // A fragments of this warp's row tile (m8n8k4 .row: row = lane/4, col = lane%4)
-  double afr[kDK];
+  double afr[KS];
   {
     const int arow = 8 * warp + (lane >> 2);
 #pragma unroll
-    for (int kk = 0; kk < kDK; ++kk)
+    for (int kk = 0; kk < KS; ++kk)
       {
         const int col = 4 * kk + (lane & 3);
         afr[kk] = (arow < nt && col < nt) ? __ldg(pc.inverse + arow * nt + col) : 0.0;
       }
   }
+  // rows handled by this thread in gather/scatter: i = warp + 16 q
+  long long relq[kDPer]; // offsets within one interval (< 2^31, checked at setup)
+  bool velq[kDPer], validq[kDPer];
+#pragma unroll
+  for (int q = 0; q < kDPer; ++q)
+    {
+      const int i = ibase + q * (kDThreads / kDCols);
+      validq[q] = i < nt;
+      velq[q] = i < nvel;
+      relq[q] = i < nt ? pc.rel[i] : 0;
+    }
   __syncthreads();
-
-  // element q of this thread: row i = (tid + q*kDThreads) / kDCols, column c = tid % kDCols
-  const int c = tid & (kDCols - 1);
-  const int i0 = tid >> 5; // kDCols == 32
-  auto addr_of = [&](int i, int j) -> long long {
-    const int patch = j / ng, n = n0 + j - patch * ng;
-    const long long anchor = i < nvel ? __ldg(vel_anchor + bt.first + patch) : __ldg(pre_anchor + bt.first + patch);
-    return n * isz + anchor + rel_s[i];
-  };
 
   double g[kDPer];
   {
-    const int j = c;
+    const long long vb = cb[c], pb = cb[kDCols + c];
 #pragma unroll
     for (int q = 0; q < kDPer; ++q)
       {
-        const int i = i0 + q * (kDThreads / kDCols);
-        g[q] = (i < nt && j < ncols) ? __ldg(r + addr_of(i, j)) : 0.0;
+        const long long base = velq[q] ? vb : pb;
+        g[q] = (validq[q] && base != kNoCol) ? __ldg(r + base + relq[q]) : 0.0;
       }
 #pragma unroll
     for (int q = 0; q < kDPer; ++q)
-      Rs[(i0 + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
+      Rs[(ibase + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
   }
   __syncthreads();
 
   for (int t = 0; t < ntiles; ++t)
     {
+      const long long *cbt = cb + (t % 3) * 2 * kDCols;
+      const long long vb = cbt[c], pb = cbt[kDCols + c];
       // prefetch: old u of this tile and the residual of the next tile
       double uo[kDPer];
-      {
-        const int j = t * kDCols + c;
 #pragma unroll
-        for (int q = 0; q < kDPer; ++q)
-          {
-            const int i = i0 + q * (kDThreads / kDCols);
-            uo[q] = (i < nt && j < ncols) ? u[addr_of(i, j)] : 0.0;
-          }
-      }
+      for (int q = 0; q < kDPer; ++q)
+        {
+          const long long base = velq[q] ? vb : pb;
+          uo[q] = (validq[q] && base != kNoCol) ? u[base + relq[q]] : 0.0;
+        }
       if (t + 1 < ntiles)
         {
-          const int j = (t + 1) * kDCols + c;
+          const long long *cbn = cb + ((t + 1) % 3) * 2 * kDCols;
+          const long long nvb = cbn[c], npb = cbn[kDCols + c];
 #pragma unroll
           for (int q = 0; q < kDPer; ++q)
             {
-              const int i = i0 + q * (kDThreads / kDCols);
-              g[q] = (i < nt && j < ncols) ? __ldg(r + addr_of(i, j)) : 0.0;
+              const long long base = velq[q] ? nvb : npb;
+              g[q] = (validq[q] && base != kNoCol) ? __ldg(r + base + relq[q]) : 0.0;
             }
         }
       // Z = A^{-1} R on the FP64 tensor path
@@ -231,16 +254,14 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
 #pragma unroll
           for (int ct = 0; ct < kDCols / 8; ++ct)
             acc[ct][0] = acc[ct][1] = 0.0;
+          const double *bbase = Rs + (lane & 3) * kDRLd + (lane >> 2);
 #pragma unroll
-          for (int kk = 0; kk < kDK; ++kk)
+          for (int kk = 0; kk < KS; ++kk)
             {
-              if (kk < ksteps)
-                {
-                  const double *brow = Rs + (4 * kk + (lane & 3)) * kDRLd + (lane >> 2);
+              const double *brow = bbase + 4 * kk * kDRLd;
 #pragma unroll
-                  for (int ct = 0; ct < kDCols / 8; ++ct)
-                    dmma_8x8x4(acc[ct], afr[kk], brow[8 * ct]);
-                }
+              for (int ct = 0; ct < kDCols / 8; ++ct)
+                dmma_8x8x4(acc[ct], afr[kk], brow[8 * ct]);
             }
           const int row = 8 * warp + (lane >> 2);
           const double wr = w_s[row];
@@ -252,21 +273,19 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
               Zs[row * kDZLd + col + 1] = acc[ct][1] * wr;
             }
         }
+      column_bases(t + 2);
       __syncthreads();
-      {
-        const int j = t * kDCols + c;
 #pragma unroll
-        for (int q = 0; q < kDPer; ++q)
-          {
-            const int i = i0 + q * (kDThreads / kDCols);
-            if (i < nt && j < ncols)
-              u[addr_of(i, j)] = uo[q] + Zs[i * kDZLd + c];
-          }
-      }
+      for (int q = 0; q < kDPer; ++q)
+        {
+          const long long base = velq[q] ? vb : pb;
+          if (validq[q] && base != kNoCol)
+            u[base + relq[q]] = uo[q] + Zs[(ibase + q * (kDThreads / kDCols)) * kDZLd + c];
+        }
       if (t + 1 < ntiles)
 #pragma unroll
         for (int q = 0; q < kDPer; ++q)
-          Rs[(i0 + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
+          Rs[(ibase + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
       __syncthreads();
     }
 }
@@ -282,16 +301,30 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, int
     return cudaSuccess;
   if (max_nt <= kDRows)
     {
-      static bool dattr = false;
-      const size_t dsmem = sizeof(double) * (kDRows * kDRLd + kDRows * kDZLd + 2 * kDRows);
-      if (!dattr)
-        {
-          cudaFuncSetAttribute(vanka_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
-          dattr = true;
-        }
+      const size_t dsmem = sizeof(double) * (kDRows * kDRLd + kDRows * kDZLd + kDRows) + sizeof(long long) * 6 * kDCols;
       dim3 grid(n_batches, (n_intervals + kDGroup - 1) / kDGroup);
-      vanka_dmma_kernel<<<grid, kDThreads, dsmem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz,
-                                                            n_intervals, omega);
+      const int ks = (max_nt + 3) / 4;
+      auto go = [&](auto kern) {
+        static bool set = false;
+        (void)set;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
+        kern<<<grid, kDThreads, dsmem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz, n_intervals,
+                                                 omega);
+      };
+      if (ks <= 8)
+        go(vanka_dmma_kernel<8>);
+      else if (ks <= 12)
+        go(vanka_dmma_kernel<12>);
+      else if (ks <= 16)
+        go(vanka_dmma_kernel<16>);
+      else if (ks <= 20)
+        go(vanka_dmma_kernel<20>);
+      else if (ks <= 24)
+        go(vanka_dmma_kernel<24>);
+      else if (ks <= 28)
+        go(vanka_dmma_kernel<28>);
+      else
+        go(vanka_dmma_kernel<32>);
       return cudaGetLastError();
     }
   const int ntp = (max_nt + 1) & ~1;
