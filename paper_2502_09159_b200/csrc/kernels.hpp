@@ -54,9 +54,14 @@ struct VankaBatch
 
 cudaError_t launch_vmult(int r, int S, const LevelConsts &P, const double *x, const double *b, double *y,
                          int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t stream);
-cudaError_t launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, int n_batches, int max_nt,
-                                const long long *vel_anchor, const long long *pre_anchor, const double *r, double *u,
-                                long long isz, int n_intervals, double omega, cudaStream_t stream);
+/// One Vanka launch. item_ptr == nullptr: block b runs item b (one colour
+/// batch); otherwise block b runs items [item_ptr[b], item_ptr[b+1]) in
+/// order (super-cell sub-phases). The non-DMMA fallback (n_T > 128) requires
+/// item_ptr == nullptr.
+cudaError_t launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, const int *item_ptr,
+                                int n_batches, int max_nt, const long long *vel_anchor, const long long *pre_anchor,
+                                const double *r, double *u, long long isz, int n_intervals, double omega,
+                                cudaStream_t stream);
 int vanka_cols_per_batch();
 cudaError_t launch_prolongate(const DevTransfer &T, const double *coarse, double *fine, int n_intervals,
                               int accumulate, cudaStream_t st);

@@ -126,6 +126,13 @@ struct stmg_level
   DevArray<VankaBatch> batches;
   DevArray<long long> vel_anchor, pre_anchor;
   std::vector<int> colour_first, colour_count;
+  // super-cell sweeps (DMMA path): 4 passes, block b of pass s runs items
+  // [pass_ptr[s][b], pass_ptr[s][b+1])
+  bool super = false;
+  std::vector<DevArray<int>> pass_ptr;
+  std::vector<int> pass_blocks;
+  DevArray<VankaBatch> sitems;
+  DevArray<long long> sva, spa;
   int max_nt = 0;
   int n_classes = 0;
   std::uint64_t total_matrix_elements = 0;
@@ -145,11 +152,23 @@ struct stmg_level
   {
     if (smoother_kind == STMG_SMOOTHER_NONE)
       throw std::invalid_argument("level has no smoother");
+    if (super)
+      {
+        for (size_t sc = 0; sc < pass_ptr.size(); ++sc)
+          if (pass_blocks[sc] > 0)
+            {
+              check(launch_vanka_colour(classes.p, sitems.p, pass_ptr[sc].p, pass_blocks[sc], max_nt, sva.p, spa.p, r,
+                                        u, spec.isz(), n, omega, ctx->stream),
+                    "vanka");
+              ctx->count();
+            }
+        return;
+      }
     for (size_t c = 0; c < colour_first.size(); ++c)
       if (colour_count[c] > 0)
         {
-          check(launch_vanka_colour(classes.p, batches.p + colour_first[c], colour_count[c], max_nt, vel_anchor.p,
-                                    pre_anchor.p, r, u, spec.isz(), n, omega, ctx->stream),
+          check(launch_vanka_colour(classes.p, batches.p + colour_first[c], nullptr, colour_count[c], max_nt,
+                                    vel_anchor.p, pre_anchor.p, r, u, spec.isz(), n, omega, ctx->stream),
                 "vanka");
           ctx->count();
         }
@@ -251,6 +270,77 @@ build_level(stmg_level &L)
   L.batches.upload(batches);
   L.vel_anchor.upload(va);
   L.pre_anchor.upload(pa);
+
+  // Super-cell sweeps for the DMMA path: a super-cell holds P x P patch
+  // anchors (one of each colour, P = colour period); a block processes the
+  // P^2 colours of a row of super-cells one after the other, separated by
+  // block barriers, so its data stays cache-resident across colours.
+  // Super-cells are 2x2-coloured over 4 launches: same-launch super-cells
+  // are a full super-cell apart and never share a dof.
+  if (L.max_nt <= 128)
+    {
+      const int P = ps.kind == PatchKind::cell ? 2 : 3;
+      const int nax = ps.kind == PatchKind::cell ? s.nx : s.nx + 1;
+      const int nay = ps.kind == PatchKind::cell ? s.ny : s.ny + 1;
+      std::vector<int> cls_of(static_cast<size_t>(nax) * nay, -1);
+      for (const auto &col : ps.colours)
+        for (const auto &e : col)
+          cls_of[static_cast<size_t>(e.ay) * nax + e.ax] = e.cls;
+      const int nsx = (nax + P - 1) / P, nsy = (nay + P - 1) / P;
+      const int B = P == 2 ? 4 : 2; // super-cells per block
+      std::vector<VankaBatch> items;
+      std::vector<long long> sva, spa;
+      L.pass_ptr.resize(4);
+      L.pass_blocks.assign(4, 0);
+      for (int sc = 0; sc < 4; ++sc)
+        {
+          std::vector<int> ptr{static_cast<int>(items.size())};
+          for (int SY = sc / 2; SY < nsy; SY += 2)
+            {
+              std::vector<int> sxs;
+              for (int SX = sc % 2; SX < nsx; SX += 2)
+                sxs.push_back(SX);
+              for (size_t c0 = 0; c0 < sxs.size(); c0 += B)
+                {
+                  for (int qy = 0; qy < P; ++qy)
+                    for (int qx = 0; qx < P; ++qx)
+                      {
+                        std::vector<std::pair<int, std::pair<int, int>>> anchors; // (cls, (ax, ay))
+                        for (size_t c1 = c0; c1 < std::min(sxs.size(), c0 + B); ++c1)
+                          {
+                            const int ax = P * sxs[c1] + qx, ay = P * SY + qy;
+                            if (ax < nax && ay < nay)
+                              anchors.push_back({cls_of[static_cast<size_t>(ay) * nax + ax], {ax, ay}});
+                          }
+                        std::stable_sort(anchors.begin(), anchors.end(),
+                                         [](const auto &a, const auto &b) { return a.first < b.first; });
+                        size_t i = 0;
+                        while (i < anchors.size())
+                          {
+                            VankaBatch it{anchors[i].first, static_cast<int>(sva.size()), 0};
+                            while (i < anchors.size() && anchors[i].first == it.cls)
+                              {
+                                sva.push_back(patch_vel_anchor(s, ps.kind, anchors[i].second.first,
+                                                               anchors[i].second.second));
+                                spa.push_back(patch_pre_anchor(s, ps.kind, anchors[i].second.first,
+                                                               anchors[i].second.second));
+                                ++it.count;
+                                ++i;
+                              }
+                            items.push_back(it);
+                          }
+                      }
+                  ptr.push_back(static_cast<int>(items.size()));
+                }
+            }
+          L.pass_blocks[sc] = static_cast<int>(ptr.size()) - 1;
+          L.pass_ptr[sc].upload(ptr);
+        }
+      L.sitems.upload(items);
+      L.sva.upload(sva);
+      L.spa.upload(spa);
+      L.super = true;
+    }
 }
 } // namespace
 

@@ -143,9 +143,10 @@ dmma_8x8x4(double (&d)[2], double a, double b)
 
 template <int KS>
 __global__ void __launch_bounds__(kDThreads, 1)
-vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
-                  const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
-                  const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals, double omega)
+vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ items,
+                  const int *__restrict__ item_ptr, const long long *__restrict__ vel_anchor,
+                  const long long *__restrict__ pre_anchor, const double *__restrict__ r, double *__restrict__ u,
+                  long long isz, int n_intervals, double omega)
 {
   extern __shared__ __align__(16) double dsm[];
   double *Rs = dsm;                                                 // kDRows x kDRLd
@@ -153,148 +154,159 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
   double *w_s = Zs + kDRows * kDZLd;                                // kDRows
   long long *cb = reinterpret_cast<long long *>(w_s + kDRows);     // [3][2][kDCols] column bases
 
-  const VankaBatch bt = batches[blockIdx.x];
-  const DevPatchClass pc = classes[bt.cls];
-  const int nt = pc.n_t, nvel = pc.n_vel;
   const int n0 = blockIdx.y * kDGroup;
   const int ng = min(kDGroup, n_intervals - n0);
-  const int ncols = bt.count * ng;
-  const int ntiles = (ncols + kDCols - 1) / kDCols;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = tid % kDCols;        // column of this thread in every tile
   const int ibase = tid / kDCols;    // first row of this thread (rows ibase + q * kDThreads / kDCols)
+  const int it0 = item_ptr ? item_ptr[blockIdx.x] : blockIdx.x;
+  const int it1 = item_ptr ? item_ptr[blockIdx.x + 1] : blockIdx.x + 1;
 
-  // column bases of tile t: interval base + velocity / pressure anchor
-  auto column_bases = [&](int t) {
-    if (tid < kDCols && t < ntiles)
-      {
-        const int j = t * kDCols + tid;
-        long long vb = kNoCol, pb = kNoCol;
-        if (j < ncols)
-          {
-            const int patch = j / ng, n = n0 + j - patch * ng;
-            vb = n * isz + __ldg(vel_anchor + bt.first + patch);
-            pb = n * isz + __ldg(pre_anchor + bt.first + patch);
-          }
-        cb[(t % 3) * 2 * kDCols + tid] = vb;
-        cb[(t % 3) * 2 * kDCols + kDCols + tid] = pb;
-      }
-  };
-
-  for (int i = tid; i < kDRows; i += kDThreads)
-    w_s[i] = i < nt ? omega * pc.weight[i] : 0.0;
-  column_bases(0);
-  column_bases(1);
-  // A fragments of this warp's row tile (m8n8k4 .row: row = lane/4, col = lane%4)
+  int loaded = -1, nt = 0, nvel = 0;
   double afr[KS];
-  {
-    const int arow = 8 * warp + (lane >> 2);
-#pragma unroll
-    for (int kk = 0; kk < KS; ++kk)
-      {
-        const int col = 4 * kk + (lane & 3);
-        afr[kk] = (arow < nt && col < nt) ? __ldg(pc.inverse + arow * nt + col) : 0.0;
-      }
-  }
-  // rows handled by this thread in gather/scatter: i = warp + 16 q
-  long long relq[kDPer]; // offsets within one interval (< 2^31, checked at setup)
+  long long relq[kDPer];
   bool velq[kDPer], validq[kDPer];
-#pragma unroll
-  for (int q = 0; q < kDPer; ++q)
-    {
-      const int i = ibase + q * (kDThreads / kDCols);
-      validq[q] = i < nt;
-      velq[q] = i < nvel;
-      relq[q] = i < nt ? pc.rel[i] : 0;
-    }
-  __syncthreads();
 
-  double g[kDPer];
-  {
-    const long long vb = cb[c], pb = cb[kDCols + c];
-#pragma unroll
-    for (int q = 0; q < kDPer; ++q)
-      {
-        const long long base = velq[q] ? vb : pb;
-        g[q] = (validq[q] && base != kNoCol) ? __ldg(r + base + relq[q]) : 0.0;
-      }
-#pragma unroll
-    for (int q = 0; q < kDPer; ++q)
-      Rs[(ibase + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
-  }
-  __syncthreads();
-
-  for (int t = 0; t < ntiles; ++t)
+  // Items run in order; consecutive items of one block are separated by
+  // block barriers (every tile ends with one), which is what makes the
+  // super-cell sub-phases conflict-free.
+  for (int it = it0; it < it1; ++it)
     {
-      const long long *cbt = cb + (t % 3) * 2 * kDCols;
-      const long long vb = cbt[c], pb = cbt[kDCols + c];
-      // prefetch: old u of this tile and the residual of the next tile
-      double uo[kDPer];
-#pragma unroll
-      for (int q = 0; q < kDPer; ++q)
+      const VankaBatch bt = items[it];
+      if (bt.cls != loaded)
         {
-          const long long base = velq[q] ? vb : pb;
-          uo[q] = (validq[q] && base != kNoCol) ? u[base + relq[q]] : 0.0;
-        }
-      if (t + 1 < ntiles)
-        {
-          const long long *cbn = cb + ((t + 1) % 3) * 2 * kDCols;
-          const long long nvb = cbn[c], npb = cbn[kDCols + c];
-#pragma unroll
-          for (int q = 0; q < kDPer; ++q)
-            {
-              const long long base = velq[q] ? nvb : npb;
-              g[q] = (validq[q] && base != kNoCol) ? __ldg(r + base + relq[q]) : 0.0;
-            }
-        }
-      // Z = A^{-1} R on the FP64 tensor path
-      if (8 * warp < nt)
-        {
-          double acc[kDCols / 8][2];
-#pragma unroll
-          for (int ct = 0; ct < kDCols / 8; ++ct)
-            acc[ct][0] = acc[ct][1] = 0.0;
-          const double *bbase = Rs + (lane & 3) * kDRLd + (lane >> 2);
+          const DevPatchClass pc = classes[bt.cls];
+          nt = pc.n_t;
+          nvel = pc.n_vel;
+          for (int i = tid; i < kDRows; i += kDThreads)
+            w_s[i] = i < nt ? omega * pc.weight[i] : 0.0;
+          const int arow = 8 * warp + (lane >> 2);
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk)
             {
-              const double *brow = bbase + 4 * kk * kDRLd;
-#pragma unroll
-              for (int ct = 0; ct < kDCols / 8; ++ct)
-                dmma_8x8x4(acc[ct], afr[kk], brow[8 * ct]);
+              const int col = 4 * kk + (lane & 3);
+              afr[kk] = (arow < nt && col < nt) ? __ldg(pc.inverse + arow * nt + col) : 0.0;
             }
-          const int row = 8 * warp + (lane >> 2);
-          const double wr = w_s[row];
 #pragma unroll
-          for (int ct = 0; ct < kDCols / 8; ++ct)
+          for (int q = 0; q < kDPer; ++q)
             {
-              const int col = 8 * ct + 2 * (lane & 3);
-              Zs[row * kDZLd + col] = acc[ct][0] * wr;
-              Zs[row * kDZLd + col + 1] = acc[ct][1] * wr;
+              const int i = ibase + q * (kDThreads / kDCols);
+              validq[q] = i < nt;
+              velq[q] = i < nvel;
+              relq[q] = i < nt ? pc.rel[i] : 0;
             }
+          loaded = bt.cls;
         }
-      column_bases(t + 2);
+      const int ncols = bt.count * ng;
+      const int ntiles = (ncols + kDCols - 1) / kDCols;
+
+      // column bases of tile t: interval base + velocity / pressure anchor
+      auto column_bases = [&](int t) {
+        if (tid < kDCols && t < ntiles)
+          {
+            const int j = t * kDCols + tid;
+            long long vb = kNoCol, pb = kNoCol;
+            if (j < ncols)
+              {
+                const int patch = j / ng, n = n0 + j - patch * ng;
+                vb = n * isz + __ldg(vel_anchor + bt.first + patch);
+                pb = n * isz + __ldg(pre_anchor + bt.first + patch);
+              }
+            cb[(t % 3) * 2 * kDCols + tid] = vb;
+            cb[(t % 3) * 2 * kDCols + kDCols + tid] = pb;
+          }
+      };
+      column_bases(0);
+      column_bases(1);
       __syncthreads();
+
+      double g[kDPer];
+      {
+        const long long vb = cb[c], pb = cb[kDCols + c];
 #pragma unroll
-      for (int q = 0; q < kDPer; ++q)
-        {
-          const long long base = velq[q] ? vb : pb;
-          if (validq[q] && base != kNoCol)
-            u[base + relq[q]] = uo[q] + Zs[(ibase + q * (kDThreads / kDCols)) * kDZLd + c];
-        }
-      if (t + 1 < ntiles)
+        for (int q = 0; q < kDPer; ++q)
+          {
+            const long long base = velq[q] ? vb : pb;
+            g[q] = (validq[q] && base != kNoCol) ? __ldg(r + base + relq[q]) : 0.0;
+          }
 #pragma unroll
         for (int q = 0; q < kDPer; ++q)
           Rs[(ibase + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
+      }
       __syncthreads();
+
+      for (int t = 0; t < ntiles; ++t)
+        {
+          const long long *cbt = cb + (t % 3) * 2 * kDCols;
+          const long long vb = cbt[c], pb = cbt[kDCols + c];
+          // prefetch: old u of this tile and the residual of the next tile
+          double uo[kDPer];
+#pragma unroll
+          for (int q = 0; q < kDPer; ++q)
+            {
+              const long long base = velq[q] ? vb : pb;
+              uo[q] = (validq[q] && base != kNoCol) ? u[base + relq[q]] : 0.0;
+            }
+          if (t + 1 < ntiles)
+            {
+              const long long *cbn = cb + ((t + 1) % 3) * 2 * kDCols;
+              const long long nvb = cbn[c], npb = cbn[kDCols + c];
+#pragma unroll
+              for (int q = 0; q < kDPer; ++q)
+                {
+                  const long long base = velq[q] ? nvb : npb;
+                  g[q] = (validq[q] && base != kNoCol) ? __ldg(r + base + relq[q]) : 0.0;
+                }
+            }
+          // Z = A^{-1} R on the FP64 tensor path
+          if (8 * warp < nt)
+            {
+              double acc[kDCols / 8][2];
+#pragma unroll
+              for (int ct = 0; ct < kDCols / 8; ++ct)
+                acc[ct][0] = acc[ct][1] = 0.0;
+              const double *bbase = Rs + (lane & 3) * kDRLd + (lane >> 2);
+#pragma unroll
+              for (int kk = 0; kk < KS; ++kk)
+                {
+                  const double *brow = bbase + 4 * kk * kDRLd;
+#pragma unroll
+                  for (int ct = 0; ct < kDCols / 8; ++ct)
+                    dmma_8x8x4(acc[ct], afr[kk], brow[8 * ct]);
+                }
+              const int row = 8 * warp + (lane >> 2);
+              const double wr = w_s[row];
+#pragma unroll
+              for (int ct = 0; ct < kDCols / 8; ++ct)
+                {
+                  const int col = 8 * ct + 2 * (lane & 3);
+                  Zs[row * kDZLd + col] = acc[ct][0] * wr;
+                  Zs[row * kDZLd + col + 1] = acc[ct][1] * wr;
+                }
+            }
+          column_bases(t + 2);
+          __syncthreads();
+#pragma unroll
+          for (int q = 0; q < kDPer; ++q)
+            {
+              const long long base = velq[q] ? vb : pb;
+              if (validq[q] && base != kNoCol)
+                u[base + relq[q]] = uo[q] + Zs[(ibase + q * (kDThreads / kDCols)) * kDZLd + c];
+            }
+          if (t + 1 < ntiles)
+#pragma unroll
+            for (int q = 0; q < kDPer; ++q)
+              Rs[(ibase + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
+          __syncthreads();
+        }
     }
 }
 } // namespace
 
 /// Launch one colour: `n_batches` batches over `n_intervals` intervals.
 cudaError_t
-launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, int n_batches, int max_nt,
-                    const long long *vel_anchor, const long long *pre_anchor, const double *r, double *u,
+launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, const int *item_ptr, int n_batches,
+                    int max_nt, const long long *vel_anchor, const long long *pre_anchor, const double *r, double *u,
                     long long isz, int n_intervals, double omega, cudaStream_t stream)
 {
   if (n_batches == 0 || n_intervals == 0)
@@ -308,8 +320,8 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, int
         static bool set = false;
         (void)set;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
-        kern<<<grid, kDThreads, dsmem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz, n_intervals,
-                                                 omega);
+        kern<<<grid, kDThreads, dsmem, stream>>>(classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz,
+                                                 n_intervals, omega);
       };
       if (ks <= 8)
         go(vanka_dmma_kernel<8>);
