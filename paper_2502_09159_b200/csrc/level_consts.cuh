@@ -57,6 +57,12 @@ struct LevelConsts
   double yCy[kMaxN1 * kMaxN1]; // J gamma cx cy C1(j,l)
   double yLm[kMaxP * kMaxN1];  // J cx Lm(b,l)
   double yLc[kMaxP * kMaxN1];  // J cy Lc(b,l)
+  // compact form used by the fused kernel: exactly symmetrised reference
+  // factors, scalar coefficients, and temporal matrices scaled by J
+  double cM1[kMaxN1 * kMaxN1], cK1[kMaxN1 * kMaxN1], cC1[kMaxN1 * kMaxN1];
+  double cLm[kMaxP * kMaxN1], cLc[kMaxP * kMaxN1];
+  double sax, say, sbx, sby, sg, scx, scy; // (nu+g)cx^2, nu cx^2, nu cy^2, (nu+g)cy^2, g cx cy, cx, cy
+  double KtJ[kMaxS * kMaxS], MtJ[kMaxS * kMaxS], lvJ[kMaxS];
   // DG(k) temporal matrices (time_basis.cpp:8-59)
   double Kt[kMaxS * kMaxS]; // dt_plus_jump(a,b)
   double Mt[kMaxS * kMaxS]; // mass(a,b)

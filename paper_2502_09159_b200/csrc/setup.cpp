@@ -309,7 +309,41 @@ make_level_consts(const LevelSpec &L)
         c.yLm[o] = J * cx * f.Lm[o];
         c.yLc[o] = J * cy * f.Lc[o];
       }
+  // compact, exactly symmetrised factors (canonical representative wins)
+  const auto csym = [n](int i, int k) {
+    const int a = i * n + k, b = k * n + i, cc = (n - 1 - i) * n + (n - 1 - k), d = (n - 1 - k) * n + (n - 1 - i);
+    return std::min(std::min(a, b), std::min(cc, d));
+  };
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k)
+      {
+        c.cM1[i * n + k] = f.M1[csym(i, k)];
+        c.cK1[i * n + k] = f.K1[csym(i, k)];
+        c.cC1[i * n + k] = f.C1[i * n + k];
+      }
+  for (int a = 0; a < f.P; ++a)
+    for (int k = 0; k < n; ++k)
+      {
+        c.cLm[a * n + k] = f.Lm[a * n + k];
+        c.cLc[a * n + k] = f.Lc[a * n + k];
+      }
+  c.sax = (nu + gm) * cx * cx;
+  c.say = nu * cx * cx;
+  c.sbx = nu * cy * cy;
+  c.sby = (nu + gm) * cy * cy;
+  c.sg = gm * cx * cy;
+  c.scx = cx;
+  c.scy = cy;
   const int s = L.S();
+  for (int a = 0; a < s; ++a)
+    {
+      c.lvJ[a] = J * t.lv[a];
+      for (int b = 0; b < s; ++b)
+        {
+          c.KtJ[a * s + b] = J * t.Kt[a * s + b];
+          c.MtJ[a * s + b] = J * t.Mt[a * s + b];
+        }
+    }
   for (int a = 0; a < s; ++a)
     {
       c.lv[a] = t.lv[a];
