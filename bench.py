@@ -196,6 +196,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2502_09159_b200 as stmg
+    from paper_2502_09159_b200 import timeslab
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -218,33 +219,24 @@ def main():
     res = torch.empty_like(x)
     halo_x = torch.zeros(mv, dtype=torch.float64, device="cuda")
     halo_u = torch.zeros(mv, dtype=torch.float64, device="cuda")
-    last_slot = slice((N - 1) * isz + (S - 1) * mv, (N - 1) * isz + S * mv)
 
     def exchange(src, dst):
         """time-slab halo: slot-k velocity of my last interval -> rank+1."""
-        if world == 1:
-            return
-        ops = []
-        if rank + 1 < world:
-            ops.append(dist.P2POp(dist.isend, src[last_slot].contiguous(), rank + 1))
-        if rank > 0:
-            ops.append(dist.P2POp(dist.irecv, dst, rank - 1))
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+        return timeslab.exchange_halo(src, dst, N, isz, mv, S, rank, world)
 
     first = rank == 0
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t_vmult, t_resid, t_vanka = [], [], []
 
     def step(record):
-        exchange(x, halo_x)
+        hx = exchange(x, halo_x)
         if record:
             ev[0].record()
-        lvl.vmult(x, y, N, None if first and world == 1 else halo_x)
+        lvl.vmult(x, y, N, hx)
         if record:
             ev[1].record()
-        exchange(u, halo_u)
-        lvl.residual(b, u, res, N, None if first and world == 1 else halo_u, coupled=True)
+        hu = exchange(u, halo_u)
+        lvl.residual(b, u, res, N, hu, coupled=True)
         if record:
             ev[2].record()
         lvl.vanka_update(res, u, CONFIG["omega"], N)
@@ -291,7 +283,7 @@ def main():
         hu.copy_(u)
         hh.zero_()
         nx_, nb_, nu_, ny_, nh_ = hx.numpy(), hb.numpy(), hu.numpy(), hy.numpy(), hh.numpy()
-        halo_arg = None if first and world == 1 else nh_
+        halo_arg = nh_ if rank > 0 else None
         lvl.vmult_host(nx_, ny_, N, halo_arg)
         torch.cuda.synchronize()
         if world > 1:
