@@ -6,8 +6,8 @@
 //    transfer is the tensor product of two 1D stencils (CSR, <= n1 or 2 n1
 //    entries per row), evaluated matrix-free per output node; the temporal
 //    node-evaluation matrix (transfer.cpp:363-386) is applied in registers.
-//  * project_mean_zero (dof_space.cpp:110-119): one block per (slot,
-//    interval), deterministic tree reduction.
+//  * project_mean_zero (dof_space.cpp:110-119): chunked partial sums per
+//    (slot, interval), re-reduced in fixed order by every block (deterministic).
 //  * coarse solve (solver.cpp:43-54): dense inverse of the pinned coarse
 //    operator, one warp per row.
 //  * dot / axpy for FGMRES (solver.cpp:139-199): fixed-grid two-stage
@@ -272,24 +272,53 @@ restrict_pressure_kernel(const DevTransfer T, const double *__restrict__ fine, d
 
 // ---------------------------------------------------------------- projection
 constexpr int kProjThreads = 256;
+constexpr int kProjChunkCells = 8192;
 
-__global__ void __launch_bounds__(kProjThreads)
-project_mean_zero_kernel(const DevGeom G, double *__restrict__ x, double scale)
+__host__ __device__ inline int
+proj_chunks(long long ncell)
 {
-  const int a = blockIdx.x; // slot
+  const long long c = (ncell + kProjChunkCells - 1) / kProjChunkCells;
+  return static_cast<int>(c < 1 ? 1 : (c > 64 ? 64 : c));
+}
+
+// Partial sums of the mode-0 pressure coefficients: block (slot, interval, chunk).
+__global__ void __launch_bounds__(kProjThreads)
+pmz_partial_kernel(const DevGeom G, const double *__restrict__ x, double *__restrict__ part)
+{
+  const int a = blockIdx.x, chunk = blockIdx.z, nch = gridDim.z;
   const long long n = blockIdx.y;
-  double *p = x + n * G.isz + G.S * G.mv + a * G.mp;
+  const double *p = x + n * G.isz + G.S * G.mv + a * G.mp;
   const long long ncell = static_cast<long long>(G.nx) * G.ny;
+  const long long c0 = ncell * chunk / nch, c1 = ncell * (chunk + 1) / nch;
   double s = 0.0;
-  for (long long c = threadIdx.x; c < ncell; c += blockDim.x)
+  for (long long c = c0 + threadIdx.x; c < c1; c += blockDim.x)
     s += p[c * G.np];
   s = block_sum<kProjThreads>(s);
+  if (threadIdx.x == 0)
+    part[(n * G.S + a) * nch + chunk] = s;
+}
+
+// Every block re-reduces its (slot, interval) partials in a fixed order and
+// subtracts the mean from its chunk (deterministic).
+__global__ void __launch_bounds__(kProjThreads)
+pmz_apply_kernel(const DevGeom G, double *__restrict__ x, const double *__restrict__ part, double scale)
+{
+  const int a = blockIdx.x, chunk = blockIdx.z, nch = gridDim.z;
+  const long long n = blockIdx.y;
   __shared__ double mean;
   if (threadIdx.x == 0)
-    mean = s * scale;
+    {
+      double s = 0.0;
+      for (int k = 0; k < nch; ++k)
+        s += part[(n * G.S + a) * nch + k];
+      mean = s * scale;
+    }
   __syncthreads();
+  double *p = x + n * G.isz + G.S * G.mv + a * G.mp;
+  const long long ncell = static_cast<long long>(G.nx) * G.ny;
+  const long long c0 = ncell * chunk / nch, c1 = ncell * (chunk + 1) / nch;
   const double m = mean;
-  for (long long c = threadIdx.x; c < ncell; c += blockDim.x)
+  for (long long c = c0 + threadIdx.x; c < c1; c += blockDim.x)
     p[c * G.np] -= m;
 }
 
@@ -431,16 +460,23 @@ launch_restrict(const DevTransfer &T, const double *fine, double *coarse, int n_
   return cudaGetLastError();
 }
 
+int
+project_scratch_doubles(const DevGeom &G, int n_intervals)
+{
+  return G.S * n_intervals * proj_chunks(static_cast<long long>(G.nx) * G.ny);
+}
+
 cudaError_t
-launch_project_mean_zero(const DevGeom &G, double *x, int n_intervals, cudaStream_t st)
+launch_project_mean_zero(const DevGeom &G, double *x, int n_intervals, double *scratch, cudaStream_t st)
 {
   if (n_intervals <= 0)
     return cudaSuccess;
   // mean = <m, p> / |Omega| with m = |K| on mode 0 (dof_space.cpp:96-119)
   const double cell_area = G.hx * G.hy;
   const double volume = (G.nx * G.hx) * (G.ny * G.hy);
-  dim3 grid(G.S, n_intervals);
-  project_mean_zero_kernel<<<grid, kProjThreads, 0, st>>>(G, x, cell_area / volume);
+  dim3 grid(G.S, n_intervals, proj_chunks(static_cast<long long>(G.nx) * G.ny));
+  pmz_partial_kernel<<<grid, kProjThreads, 0, st>>>(G, x, scratch);
+  pmz_apply_kernel<<<grid, kProjThreads, 0, st>>>(G, x, scratch, cell_area / volume);
   return cudaGetLastError();
 }
 

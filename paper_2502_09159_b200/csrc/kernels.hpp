@@ -67,7 +67,10 @@ cudaError_t launch_prolongate(const DevTransfer &T, const double *coarse, double
                               int accumulate, cudaStream_t st);
 cudaError_t launch_restrict(const DevTransfer &T, const double *fine, double *coarse, int n_intervals,
                             cudaStream_t st);
-cudaError_t launch_project_mean_zero(const DevGeom &G, double *x, int n_intervals, cudaStream_t st);
+/// Per-slot mean-zero projection of the pressure (two deterministic passes);
+/// `scratch` holds project_scratch_doubles(G, n_intervals) doubles.
+int project_scratch_doubles(const DevGeom &G, int n_intervals);
+cudaError_t launch_project_mean_zero(const DevGeom &G, double *x, int n_intervals, double *scratch, cudaStream_t st);
 cudaError_t launch_zero_constrained(const DevGeom &G, double *x, int n_intervals, cudaStream_t st);
 cudaError_t launch_coarse_solve(const double *inv, const long long *pinned, int n_pinned, int nrows, const double *b,
                                 double *x, cudaStream_t st);

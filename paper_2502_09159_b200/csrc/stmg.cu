@@ -128,16 +128,29 @@ struct stmg_level
   std::vector<int> colour_first, colour_count;
   // super-cell sweeps (DMMA path): 4 passes, block b of pass s runs items
   // [pass_ptr[s][b], pass_ptr[s][b+1])
+  struct SuperSet
+  {
+    std::vector<DevArray<int>> pass_ptr;
+    std::vector<int> pass_blocks;
+    DevArray<VankaBatch> items;
+    DevArray<long long> va, pa;
+  };
   bool super = false;
-  std::vector<DevArray<int>> pass_ptr;
-  std::vector<int> pass_blocks;
-  DevArray<VankaBatch> sitems;
-  DevArray<long long> sva, spa;
+  SuperSet sup[2]; // [0]: many intervals per launch, [1]: few (time marching)
   int max_nt = 0;
   int n_classes = 0;
   std::uint64_t total_matrix_elements = 0;
   // scratch
-  DevArray<double> work, zeros, host_in, host_out, host_prev;
+  DevArray<double> work, zeros, host_in, host_out, host_prev, proj;
+
+  /// u_p <- u_p - mean per slot (PressureSpace::project_mean_zero)
+  void
+  project(double *x, int n)
+  {
+    proj.resize(project_scratch_doubles(geom, n));
+    check(launch_project_mean_zero(geom, x, n, proj.p, ctx->stream), "project");
+    ctx->count(2);
+  }
 
   void
   vmult(const double *x, const double *b, double *y, int n, const double *xprev0, int coupled, int mode)
@@ -154,11 +167,12 @@ struct stmg_level
       throw std::invalid_argument("level has no smoother");
     if (super)
       {
-        for (size_t sc = 0; sc < pass_ptr.size(); ++sc)
-          if (pass_blocks[sc] > 0)
+        const SuperSet &ss = sup[n < 8 ? 1 : 0];
+        for (size_t sc = 0; sc < ss.pass_ptr.size(); ++sc)
+          if (ss.pass_blocks[sc] > 0)
             {
-              check(launch_vanka_colour(classes.p, sitems.p, pass_ptr[sc].p, pass_blocks[sc], max_nt, sva.p, spa.p, r,
-                                        u, spec.isz(), n, omega, ctx->stream),
+              check(launch_vanka_colour(classes.p, ss.items.p, ss.pass_ptr[sc].p, ss.pass_blocks[sc], max_nt, ss.va.p,
+                                        ss.pa.p, r, u, spec.isz(), n, omega, ctx->stream),
                     "vanka");
               ctx->count();
             }
@@ -287,58 +301,64 @@ build_level(stmg_level &L)
         for (const auto &e : col)
           cls_of[static_cast<size_t>(e.ay) * nax + e.ax] = e.cls;
       const int nsx = (nax + P - 1) / P, nsy = (nay + P - 1) / P;
-      const int B = P == 2 ? 4 : 2; // super-cells per block
-      std::vector<VankaBatch> items;
-      std::vector<long long> sva, spa;
-      L.pass_ptr.resize(4);
-      L.pass_blocks.assign(4, 0);
-      for (int sc = 0; sc < 4; ++sc)
+      // B super-cells per block: few for many intervals (columns = B * 16
+      // intervals), many for time marching (one interval, 16 columns).
+      for (int set = 0; set < 2; ++set)
         {
-          std::vector<int> ptr{static_cast<int>(items.size())};
-          for (int SY = sc / 2; SY < nsy; SY += 2)
+          const int B = set == 0 ? (P == 2 ? 4 : 2) : 16;
+          stmg_level::SuperSet &ss = L.sup[set];
+          std::vector<VankaBatch> items;
+          std::vector<long long> sva, spa;
+          ss.pass_ptr.resize(4);
+          ss.pass_blocks.assign(4, 0);
+          for (int sc = 0; sc < 4; ++sc)
             {
-              std::vector<int> sxs;
-              for (int SX = sc % 2; SX < nsx; SX += 2)
-                sxs.push_back(SX);
-              for (size_t c0 = 0; c0 < sxs.size(); c0 += B)
+              std::vector<int> ptr{static_cast<int>(items.size())};
+              for (int SY = sc / 2; SY < nsy; SY += 2)
                 {
-                  for (int qy = 0; qy < P; ++qy)
-                    for (int qx = 0; qx < P; ++qx)
-                      {
-                        std::vector<std::pair<int, std::pair<int, int>>> anchors; // (cls, (ax, ay))
-                        for (size_t c1 = c0; c1 < std::min(sxs.size(), c0 + B); ++c1)
+                  std::vector<int> sxs;
+                  for (int SX = sc % 2; SX < nsx; SX += 2)
+                    sxs.push_back(SX);
+                  for (size_t c0 = 0; c0 < sxs.size(); c0 += B)
+                    {
+                      for (int qy = 0; qy < P; ++qy)
+                        for (int qx = 0; qx < P; ++qx)
                           {
-                            const int ax = P * sxs[c1] + qx, ay = P * SY + qy;
-                            if (ax < nax && ay < nay)
-                              anchors.push_back({cls_of[static_cast<size_t>(ay) * nax + ax], {ax, ay}});
-                          }
-                        std::stable_sort(anchors.begin(), anchors.end(),
-                                         [](const auto &a, const auto &b) { return a.first < b.first; });
-                        size_t i = 0;
-                        while (i < anchors.size())
-                          {
-                            VankaBatch it{anchors[i].first, static_cast<int>(sva.size()), 0};
-                            while (i < anchors.size() && anchors[i].first == it.cls)
+                            std::vector<std::pair<int, std::pair<int, int>>> anchors; // (cls, (ax, ay))
+                            for (size_t c1 = c0; c1 < std::min(sxs.size(), c0 + B); ++c1)
                               {
-                                sva.push_back(patch_vel_anchor(s, ps.kind, anchors[i].second.first,
-                                                               anchors[i].second.second));
-                                spa.push_back(patch_pre_anchor(s, ps.kind, anchors[i].second.first,
-                                                               anchors[i].second.second));
-                                ++it.count;
-                                ++i;
+                                const int ax = P * sxs[c1] + qx, ay = P * SY + qy;
+                                if (ax < nax && ay < nay)
+                                  anchors.push_back({cls_of[static_cast<size_t>(ay) * nax + ax], {ax, ay}});
                               }
-                            items.push_back(it);
+                            std::stable_sort(anchors.begin(), anchors.end(),
+                                             [](const auto &x, const auto &y) { return x.first < y.first; });
+                            size_t i = 0;
+                            while (i < anchors.size())
+                              {
+                                VankaBatch it{anchors[i].first, static_cast<int>(sva.size()), 0};
+                                while (i < anchors.size() && anchors[i].first == it.cls)
+                                  {
+                                    sva.push_back(patch_vel_anchor(s, ps.kind, anchors[i].second.first,
+                                                                   anchors[i].second.second));
+                                    spa.push_back(patch_pre_anchor(s, ps.kind, anchors[i].second.first,
+                                                                   anchors[i].second.second));
+                                    ++it.count;
+                                    ++i;
+                                  }
+                                items.push_back(it);
+                              }
                           }
-                      }
-                  ptr.push_back(static_cast<int>(items.size()));
+                      ptr.push_back(static_cast<int>(items.size()));
+                    }
                 }
+              ss.pass_blocks[sc] = static_cast<int>(ptr.size()) - 1;
+              ss.pass_ptr[sc].upload(ptr);
             }
-          L.pass_blocks[sc] = static_cast<int>(ptr.size()) - 1;
-          L.pass_ptr[sc].upload(ptr);
+          ss.items.upload(items);
+          ss.va.upload(sva);
+          ss.pa.upload(spa);
         }
-      L.sitems.upload(items);
-      L.sva.upload(sva);
-      L.spa.upload(spa);
       L.super = true;
     }
 }
@@ -389,8 +409,7 @@ struct stmg_solver
     ctx->count(2);
     if (F.kind != TransferKind::identity && project)
       {
-        check(launch_project_mean_zero(levels[l - 1]->level->geom, coarse_v, 1, ctx->stream), "project");
-        ctx->count();
+        levels[l - 1]->level->project(coarse_v, 1);
       }
   }
 
@@ -404,8 +423,7 @@ struct stmg_solver
         F.t.resize(F.level->spec.isz());
         check(launch_prolongate(F.dt, coarse_v, F.t.p, 1, 0, ctx->stream), "prolongate");
         ctx->count(2);
-        check(launch_project_mean_zero(F.level->geom, F.t.p, 1, ctx->stream), "project");
-        ctx->count();
+        F.level->project(F.t.p, 1);
         if (accumulate)
           {
             check(launch_axpy(F.level->spec.isz(), 1.0, nullptr, 1.0, F.t.p, fine_v, ctx->stream), "axpy");
@@ -428,8 +446,7 @@ struct stmg_solver
   {
     check(launch_coarse_solve(coarse_inv.p, coarse_pinned.p, n_pinned, coarse_n, b_v, x_v, ctx->stream), "coarse");
     ctx->count();
-    check(launch_project_mean_zero(levels[0]->level->geom, x_v, 1, ctx->stream), "project");
-    ctx->count();
+    levels[0]->level->project(x_v, 1);
   }
 
   // VCycle::cycle (solver.cpp:69-93); writes the result into x_v.
@@ -610,8 +627,7 @@ struct stmg_solver
         double *x = X + step * n;
         int it = 0;
         gmres(rhs.p, x, &it, nullptr, 0);
-        check(launch_project_mean_zero(L.geom, x, 1, ctx->stream), "project");
-        ctx->count();
+        L.project(x, 1);
         if (iterations)
           iterations[step] = it;
         check(cudaMemcpyAsync(vprev.p, x + (L.spec.S() - 1) * L.spec.mv(), sizeof(double) * L.spec.mv(),
