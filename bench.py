@@ -175,17 +175,69 @@ def cpu_baseline_quick():
                       f"vmult + Vanka step, OpenMP over intervals, {reps} steps"}
 
 
+def _consistent_rhs(torch, sol, n_steps, seed):
+    """Seeded uniform[-1,1] load vectors made consistent: constrained velocity
+    rows zero, per-slot pressure mean zero."""
+    lv = sol.finest
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    F = torch.rand(n_steps * lv.size, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+    gx, gy = lv.grid_x, lv.n_scalar // lv.grid_x
+    Fv = F.view(n_steps, lv.size)
+    npc = (sol.level_info[-1]["r"] + 1) * (sol.level_info[-1]["r"] + 2) // 2
+    for a in range(lv.n_slots):
+        for c in range(2):
+            base = a * lv.n_velocity + c * lv.n_scalar
+            g = Fv[:, base: base + lv.n_scalar].view(n_steps, gy, gx)
+            g[:, 0, :] = 0
+            g[:, -1, :] = 0
+            g[:, :, 0] = 0
+            g[:, :, -1] = 0
+        pb = lv.n_slots * lv.n_velocity + a * lv.n_pressure
+        p = Fv[:, pb: pb + lv.n_pressure].view(n_steps, -1, npc)
+        p[:, :, 0] -= p[:, :, 0].mean(dim=1, keepdim=True)
+    return F
+
+
+def solve_legs(stmg, ctx, torch):
+    """Full FGMRES + hp-STMG V(2,2) time-marching solves to rtol 1e-8 on
+    seeded consistent load vectors: C1 exactly (16^2, Q2/P1, DG(1), 8
+    intervals, cell Vanka) and the C4 discretisation (1024^2, Q2/P1, DG(1),
+    tau = 1/64, vertex-star Vanka) over its first 2 intervals."""
+    out = {}
+    for name, kw in [("C1", dict(refinements=4, r=1, k=1, n_steps=8, t_end=1.0, smoother=stmg.SMOOTHER_CELL)),
+                     ("C4_first2", dict(refinements=10, r=1, k=1, n_steps=2, t_end=2.0 / 64,
+                                        smoother=stmg.SMOOTHER_VERTEX_STAR))]:
+        sol = stmg.Solver(ctx, nu=1.0, gamma=1.0, nu1=2, nu2=2, omega=0.8, rtol=1e-8, **kw)
+        F = _consistent_rhs(torch, sol, sol.n_steps, 11)
+        X = torch.zeros_like(F)
+        sol.time_march(F, X)  # warm-up: Krylov workspace
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        iters = sol.time_march(F, X)
+        e.record()
+        torch.cuda.synchronize()
+        sec = s.elapsed_time(e) / 1e3
+        out[name] = {"dofs": F.numel(), "seconds": sec, "dofs_per_s": F.numel() / sec,
+                     "avg_gmres_iterations": sum(iters) / len(iters), "levels": sol.n_levels,
+                     "smoother": "cell" if kw["smoother"] == stmg.SMOOTHER_CELL else "vertex_star"}
+        del sol, F, X
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nx", type=int, default=256)
     ap.add_argument("--intervals", type=int, default=64)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -332,7 +384,14 @@ def main():
                 "frac": kd["TFLOP/s"] / fp64}
     else:
         roof = {"bound": "hbm", "achieved": kd["GB/s"], "peak": hbm, "unit": "GB/s", "frac": kd["GB/s"] / hbm}
-    roof.update({"kernel": dom, "traffic": None, "peak_source": peak_src,
+    traffic = None
+    try:  # dram__bytes_read+write per launch of this kernel from the committed ncu capture
+        tr = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+        per = tr["per_launch_dram_bytes"]
+        traffic = per["vmult"] if dom == "vmult" else per["vanka_update_pass"] * tr["launches_per_step"]["vanka_update_pass"]
+    except Exception:
+        pass
+    roof.update({"kernel": dom, "traffic": traffic, "algorithmic_bytes": kd["algorithmic_bytes"], "peak_source": peak_src,
                  "hbm_frac": kd["GB/s"] / hbm, "fp64_frac": kd["TFLOP/s"] / fp64})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -344,6 +403,8 @@ def main():
                            "vanka_step_dofs_per_s": world * dofs / ((rs_ms + vk_ms) * 1e-3)},
             "kernels": kernels, "roofline": roof, "gpu_launches": gpu_launches,
             "clocks": clk.summary(), "e2e": e2e}
+    if not args.no_solve:
+        line["solve"] = solve_legs(stmg, ctx, torch)
     if not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_quick()
