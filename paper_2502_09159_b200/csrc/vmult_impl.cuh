@@ -70,7 +70,7 @@ sign_refl(int i, int k) // C1(N-1-i, N-1-k) = -C1(i, k)
                                                            : P.cLc[(a) * N1 + ((k) > N1 - 1 - (k) ? N1 - 1 - (k) : (k))])
 
 template <int R, int S, bool RESID, bool RAW>
-__global__ void __launch_bounds__(32 * S)
+__global__ void __launch_bounds__(32 * S, R == 2 ? 3 : 1)
 vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
              double *__restrict__ y, const double *__restrict__ xprev0, int rows_per_seg, int coupled)
 {
