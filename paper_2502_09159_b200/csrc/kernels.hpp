@@ -52,6 +52,20 @@ struct VankaBatch
   int count; // <= vanka_cols_per_batch()
 };
 
+/// One tile of the pipelined tensor-core Vanka: <= 32 columns (patch,
+/// interval) of one class; column data in parallel arrays at tile*32 + c.
+struct VankaTile
+{
+  int cls;
+  int ncols;
+};
+cudaError_t launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *colv,
+                            const long long *colp, const int *coln, const int *tile_ptr, int n_blocks, int ng_full,
+                            int max_nt, const double *r, double *u, long long isz, int n_intervals, double omega,
+                            cudaStream_t stream);
+int vanka_tc_cols();
+int vanka_tc_max_tiles();
+
 cudaError_t launch_vmult(int r, int S, const LevelConsts &P, const double *x, const double *b, double *y,
                          int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t stream);
 /// One Vanka launch. item_ptr == nullptr: block b runs item b (one colour

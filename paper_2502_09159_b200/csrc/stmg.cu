@@ -134,6 +134,15 @@ struct stmg_level
     std::vector<int> pass_blocks;
     DevArray<VankaBatch> items;
     DevArray<long long> va, pa;
+    // pipelined tensor-core tiles (vanka_tc.cu): per pass, block b runs
+    // tiles [tile_ptr[b], tile_ptr[b+1]); each tile <= 32 (patch, interval)
+    // columns of one class and one colour sub-phase
+    int ng_full = 1;
+    std::vector<DevArray<int>> tile_ptr;
+    std::vector<int> tile_blocks;
+    DevArray<VankaTile> tiles;
+    DevArray<long long> colv, colp;
+    DevArray<int> coln;
   };
   bool super = false;
   SuperSet sup[2]; // [0]: many intervals per launch, [1]: few (time marching)
@@ -168,6 +177,19 @@ struct stmg_level
     if (super)
       {
         const SuperSet &ss = sup[n < 8 ? 1 : 0];
+        if (!ss.tile_ptr.empty())
+          {
+            for (size_t sc = 0; sc < ss.tile_ptr.size(); ++sc)
+              if (ss.tile_blocks[sc] > 0)
+                {
+                  check(launch_vanka_tc(classes.p, ss.tiles.p, ss.colv.p, ss.colp.p, ss.coln.p, ss.tile_ptr[sc].p,
+                                        ss.tile_blocks[sc], ss.ng_full, max_nt, r, u, spec.isz(), n, omega,
+                                        ctx->stream),
+                        "vanka_tc");
+                  ctx->count();
+                }
+            return;
+          }
         for (size_t sc = 0; sc < ss.pass_ptr.size(); ++sc)
           if (ss.pass_blocks[sc] > 0)
             {
@@ -305,7 +327,7 @@ build_level(stmg_level &L)
       // intervals), many for time marching (one interval, 16 columns).
       for (int set = 0; set < 2; ++set)
         {
-          const int B = set == 0 ? (P == 2 ? 4 : 2) : 16;
+          const int B = set == 0 ? (P == 2 ? 4 : 2) : 32;
           stmg_level::SuperSet &ss = L.sup[set];
           std::vector<VankaBatch> items;
           std::vector<long long> sva, spa;
@@ -358,6 +380,64 @@ build_level(stmg_level &L)
           ss.items.upload(items);
           ss.va.upload(sva);
           ss.pa.upload(spa);
+
+          // expand the items into tensor-core tiles of <= 32 columns
+          // (patch-major, interval-minor; ng_full intervals per block)
+          ss.ng_full = set == 0 ? 16 : 1;
+          const int tc = vanka_tc_cols();
+          bool tc_ok = true;
+          std::vector<VankaTile> tiles;
+          std::vector<long long> colv, colp;
+          std::vector<int> coln;
+          ss.tile_ptr.resize(4);
+          ss.tile_blocks.assign(4, 0);
+          for (int sc = 0; sc < 4; ++sc)
+            {
+              std::vector<int> hptr(ss.pass_blocks[sc] + 1);
+              cudaMemcpy(hptr.data(), ss.pass_ptr[sc].p, sizeof(int) * hptr.size(), cudaMemcpyDeviceToHost);
+              std::vector<int> tptr{static_cast<int>(tiles.size())};
+              for (int blk = 0; blk < ss.pass_blocks[sc]; ++blk)
+                {
+                  for (int it = hptr[blk]; it < hptr[blk + 1]; ++it)
+                    {
+                      const VankaBatch &item = items[it];
+                      const int ncols = item.count * ss.ng_full;
+                      for (int c0 = 0; c0 < ncols; c0 += tc)
+                        {
+                          VankaTile tl{item.cls, std::min(tc, ncols - c0)};
+                          for (int c = 0; c < tc; ++c)
+                            {
+                              const int j = c0 + c;
+                              if (j < ncols)
+                                {
+                                  const int patch = j / ss.ng_full, nl = j % ss.ng_full;
+                                  colv.push_back(nl * s.isz() + sva[item.first + patch]);
+                                  colp.push_back(nl * s.isz() + spa[item.first + patch]);
+                                  coln.push_back(nl);
+                                }
+                              else
+                                {
+                                  colv.push_back(0);
+                                  colp.push_back(0);
+                                  coln.push_back(1 << 30);
+                                }
+                            }
+                          tiles.push_back(tl);
+                        }
+                    }
+                  tptr.push_back(static_cast<int>(tiles.size()));
+                  if (tptr.back() - tptr[tptr.size() - 2] > vanka_tc_max_tiles())
+                    tc_ok = false; // block too long for the staged tile data
+                }
+              ss.tile_blocks[sc] = ss.pass_blocks[sc];
+              ss.tile_ptr[sc].upload(tptr);
+            }
+          ss.tiles.upload(tiles);
+          ss.colv.upload(colv);
+          ss.colp.upload(colp);
+          ss.coln.upload(coln);
+          if (!tc_ok)
+            ss.tile_ptr.clear(); // use the item-based DMMA kernel instead
         }
       L.super = true;
     }

@@ -1,0 +1,238 @@
+// Additive Vanka patch solves on the FP64 tensor path, pipelined (sm_100a).
+//
+// Replaces the patch loop of VankaSmoother::apply_additive / smooth_step
+// (vanka.cpp:196-233): u += omega * sum_T R_T^T w_T A_T^{-1} R_T r.
+//
+// Per block: a host-built list of tiles, each <= 32 columns (patch, interval)
+// of one congruence class inside one super-cell colour sub-phase.
+//  * gather: R tiles are copied global -> shared with cp.async two tiles
+//    ahead (3-slot ring), so residual loads never hold registers and their
+//    latency overlaps the tensor work of earlier tiles;
+//  * Z = A^{-1} R with mma.sync.m8n8k4.f64 (DMMA); the class inverse lives in
+//    registers as A-fragments, warp w owns rows 8w..8w+7;
+//  * scatter straight from the accumulator fragments with red.global.add.f64:
+//    no read-back of u, no Z staging. The super-cell colouring guarantees that
+//    no two concurrently running tiles touch the same dof, and tiles of one
+//    block are ordered by the per-tile barrier, so results are deterministic.
+#include "kernels.hpp"
+
+#include <cuda_runtime.h>
+
+namespace stmg_b200
+{
+
+namespace
+{
+constexpr int kTThreads = 512;
+constexpr int kTRows = 128;
+constexpr int kTCols = 32;
+constexpr int kTLd = 36; // == 4 mod 16 doubles: conflict-free B-fragment loads
+constexpr int kTSlot = kTRows * kTLd;
+constexpr int kTMaxTiles = 64; // tiles per block (host falls back beyond)
+constexpr size_t kTSmem = sizeof(double) * 3 * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4));
+
+__device__ __forceinline__ void
+cp_async8(double *dst, const double *src)
+{
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(src));
+}
+__device__ __forceinline__ void
+cp_async_commit()
+{
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void
+cp_async_wait1()
+{
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void
+dmma(double (&d)[2], double a, double b)
+{
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int KS>
+__global__ void __launch_bounds__(kTThreads, 1)
+vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__restrict__ tiles,
+                const long long *__restrict__ colv, const long long *__restrict__ colp, const int *__restrict__ coln,
+                const int *__restrict__ tile_ptr, int ng_full, const double *__restrict__ r, double *__restrict__ u,
+                long long isz, int n_intervals, double omega)
+{
+  extern __shared__ __align__(16) double ring[]; // 3 slots of kTRows x kTLd, then the block's tile data
+  long long *s_colv = reinterpret_cast<long long *>(ring + 3 * kTSlot);
+  long long *s_colp = s_colv + kTMaxTiles * kTCols;
+  int *s_coln = reinterpret_cast<int *>(s_colp + kTMaxTiles * kTCols);
+  VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_coln + kTMaxTiles * kTCols);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = tile_ptr[blockIdx.x], t1 = tile_ptr[blockIdx.x + 1];
+  const int nb = t1 - t0;
+  const int n0 = blockIdx.y * ng_full;
+  const long long base0 = n0 * isz;
+
+  // stage this block's tile headers and column data (<= kTMaxTiles tiles)
+  for (int e = tid; e < nb * kTCols; e += kTThreads)
+    {
+      s_colv[e] = colv[t0 * kTCols + e];
+      s_colp[e] = colp[t0 * kTCols + e];
+      s_coln[e] = coln[t0 * kTCols + e];
+    }
+  for (int e = tid; e < nb; e += kTThreads)
+    s_tile[e] = tiles[t0 + e];
+  __syncthreads();
+
+  // gather rows of this thread: row = tid/32 + 16 q (fixed across tiles)
+  constexpr int QN = kTRows * kTCols / kTThreads;
+  int cls_issue = -1, nt_issue = 0, nvel_issue = 0;
+  long long relq[QN];
+  const int col_g = tid & 31;
+
+  // gather of local tile lt into ring slot s
+  auto issue = [&](int lt, int s) {
+    if (lt < nb)
+      {
+        const VankaTile tl = s_tile[lt];
+        if (tl.cls != cls_issue)
+          {
+            const DevPatchClass pc = classes[tl.cls];
+            nt_issue = pc.n_t;
+            nvel_issue = pc.n_vel;
+#pragma unroll
+            for (int q = 0; q < QN; ++q)
+              {
+                const int row = (tid >> 5) + q * (kTThreads / kTCols);
+                relq[q] = row < nt_issue ? pc.rel[row] : 0;
+              }
+            cls_issue = tl.cls;
+          }
+        double *slot = ring + s * kTSlot;
+        const int ci = lt * kTCols + col_g;
+        const bool colok = col_g < tl.ncols && n0 + s_coln[ci] < n_intervals;
+        const long long cv = base0 + s_colv[ci], cp = base0 + s_colp[ci];
+#pragma unroll
+        for (int q = 0; q < QN; ++q)
+          {
+            const int row = (tid >> 5) + q * (kTThreads / kTCols);
+            double *dst = slot + row * kTLd + col_g;
+            if (colok && row < nt_issue)
+              cp_async8(dst, r + (row < nvel_issue ? cv : cp) + relq[q]);
+            else
+              *dst = 0.0;
+          }
+      }
+    cp_async_commit(); // possibly empty group: keeps the group count uniform
+  };
+
+  issue(0, 0);
+  issue(1, 1);
+
+  int loaded = -1, nt_loaded = 0;
+  double afr[KS];
+  long long rel_row = 0;
+  bool vel_row = false, ok_row = false;
+  double w_row = 0.0;
+  const int row = 8 * warp + (lane >> 2);
+
+  for (int lt = 0; lt < nb; ++lt)
+    {
+      cp_async_wait1(); // own copies of tile lt done (tile lt+1 may be in flight)
+      __syncthreads();  // everyone's copies of tile lt visible; slot of tile lt-1 free
+      issue(lt + 2, (lt + 2) % 3);
+      const VankaTile tl = s_tile[lt];
+      if (tl.cls != loaded)
+        {
+          const DevPatchClass pc = classes[tl.cls];
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk)
+            {
+              const int col = 4 * kk + (lane & 3);
+              afr[kk] = (row < pc.n_t && col < pc.n_t) ? __ldg(pc.inverse + row * pc.n_t + col) : 0.0;
+            }
+          ok_row = row < pc.n_t;
+          vel_row = row < pc.n_vel;
+          rel_row = ok_row ? pc.rel[row] : 0;
+          w_row = ok_row ? omega * pc.weight[row] : 0.0;
+          nt_loaded = pc.n_t;
+          loaded = tl.cls;
+        }
+      double acc[kTCols / 8][2];
+#pragma unroll
+      for (int ct = 0; ct < kTCols / 8; ++ct)
+        acc[ct][0] = acc[ct][1] = 0.0;
+      const double *bbase = ring + (lt % 3) * kTSlot + (lane & 3) * kTLd + (lane >> 2);
+      if (8 * warp < nt_loaded) // warps past n_T only join the barriers
+        {
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk)
+            {
+              const double *brow = bbase + 4 * kk * kTLd;
+#pragma unroll
+              for (int ct = 0; ct < kTCols / 8; ++ct)
+                dmma(acc[ct], afr[kk], brow[8 * ct]);
+            }
+        }
+      if (ok_row)
+        {
+#pragma unroll
+          for (int ct = 0; ct < kTCols / 8; ++ct)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+              {
+                const int col = 8 * ct + 2 * (lane & 3) + b;
+                const int ci = lt * kTCols + col;
+                if (col < tl.ncols && n0 + s_coln[ci] < n_intervals)
+                  atomicAdd(u + base0 + (vel_row ? s_colv[ci] : s_colp[ci]) + rel_row, acc[ct][b] * w_row);
+              }
+        }
+    }
+}
+} // namespace
+
+cudaError_t
+launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *colv, const long long *colp,
+                const int *coln, const int *tile_ptr, int n_blocks, int ng_full, int max_nt, const double *r,
+                double *u, long long isz, int n_intervals, double omega, cudaStream_t stream)
+{
+  if (n_blocks == 0 || n_intervals == 0)
+    return cudaSuccess;
+  dim3 grid(n_blocks, (n_intervals + ng_full - 1) / ng_full);
+  const int ks = (max_nt + 3) / 4;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTSmem));
+    kern<<<grid, kTThreads, kTSmem, stream>>>(classes, tiles, colv, colp, coln, tile_ptr, ng_full, r, u, isz,
+                                              n_intervals, omega);
+  };
+  if (ks <= 8)
+    go(vanka_tc_kernel<8>);
+  else if (ks <= 12)
+    go(vanka_tc_kernel<12>);
+  else if (ks <= 16)
+    go(vanka_tc_kernel<16>);
+  else if (ks <= 20)
+    go(vanka_tc_kernel<20>);
+  else if (ks <= 24)
+    go(vanka_tc_kernel<24>);
+  else if (ks <= 29)
+    go(vanka_tc_kernel<29>);
+  else
+    go(vanka_tc_kernel<32>);
+  return cudaGetLastError();
+}
+
+int
+vanka_tc_cols()
+{
+  return kTCols;
+}
+
+int
+vanka_tc_max_tiles()
+{
+  return kTMaxTiles;
+}
+
+} // namespace stmg_b200
