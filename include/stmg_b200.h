@@ -155,6 +155,50 @@ int stmg_gmres(stmg_solver *solver, const double *b, double *x, int *iterations,
 int stmg_time_march(stmg_solver *solver, const double *F, double *X, int *iterations);
 int stmg_time_march_host(stmg_solver *solver, const double *F, double *X, int *iterations);
 
+/* ------------------------------------------------------------ all-at-once
+ * The global space-time system of Eq. GloSys: the block
+ * lower-bidiagonal operator (A X)_n = D X_n - C X_{n-1} over a slab of
+ * n_intervals intervals. It is solved by right-preconditioned FGMRES (the
+ * reference's gmres, solver.cpp:95-202) with an all-at-once V-cycle:
+ *  - Vanka smoothing of all intervals at once, residuals carrying the jump
+ *    coupling;
+ *  - the reference's spatial / temporal-p transfers per interval;
+ *  - an exact coarse solve by block forward substitution in time.
+ * The reference only time-marches (solver.cpp:204-325), so this path is
+ * pinned by the identity "all-at-once solution = time-marched solution"
+ * (SURVEY §8c).
+ *
+ * Time-slab partition: with a communicator installed, rank p owns
+ * intervals [p*n_intervals, (p+1)*n_intervals) of a world*n_intervals system
+ * (equal slabs). The library calls back for the only three exchanges the path
+ * has. Every buffer is device memory, and every call is stream-ordered on
+ * `stream` (the context's stream):
+ *  - exchange_halo: send n doubles (slot-k velocity of this rank's last
+ *    interval) to rank+1 and receive rank-1's into recv. The first rank
+ *    receives nothing; the last rank sends nothing.
+ *  - allreduce_sum: in-place sum over ranks of n doubles (Krylov dots).
+ *  - allgather: recv[r*n .. (r+1)*n) = send of rank r (coarse right-hand sides).
+ * Callbacks return 0 on success. */
+typedef struct stmg_comm_ops {
+    void *user;
+    int rank;
+    int world;
+    int (*exchange_halo)(void *user, const double *send, double *recv, int64_t n, void *stream);
+    int (*allreduce_sum)(void *user, double *buf, int64_t n, void *stream);
+    int (*allgather)(void *user, const double *send, double *recv, int64_t n, void *stream);
+} stmg_comm_ops;
+/* Install (ops != NULL, copied) or remove (NULL) the communicator. */
+int stmg_solver_set_comm(stmg_solver *solver, const stmg_comm_ops *ops);
+/* One all-at-once V-cycle x = V(b) on the finest level, n_intervals intervals. */
+int stmg_vcycle_all_at_once(stmg_solver *solver, const double *b, double *x, int n_intervals);
+/* Solve A X = F on the slab. v_init (nullable, M^v doubles) is the slot-k
+ * velocity entering the slab's first interval: the hand-off between
+ * consecutive macro steps. Only the first rank reads it.
+ * X is projected mean-zero per slot. iterations receives the FGMRES
+ * iteration count. */
+int stmg_solve_all_at_once(stmg_solver *solver, const double *F, double *X, int n_intervals, const double *v_init,
+                           int *iterations, double *residual_history, int history_cap);
+
 /* ------------------------------------------------------------ host-only
  * Setup queries that need no GPU (used by the CPU test tier).
  * stmg_plan_levels: the level table of plan_hierarchy/combine_hierarchies

@@ -75,6 +75,10 @@ _SIGNATURES = {
                    _c_int),
     "stmg_time_march": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_time_march_host": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
+    "stmg_solver_set_comm": ([_c_void_p, _c_void_p], _c_int),
+    "stmg_vcycle_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
+    "stmg_solve_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, ctypes.POINTER(_c_int),
+                                ctypes.POINTER(_c_double), _c_int], _c_int),
     "stmg_plan_levels": ([_c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _c_i64p], _c_int),
     "stmg_patch_info": ([_c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int, _c_i64p,
                          ctypes.POINTER(_c_double), _c_int], _c_int),
@@ -121,6 +125,30 @@ def _hptr(a) -> Optional[int]:
     if a.dtype.itemsize != 8 or not a.flags["C_CONTIGUOUS"]:
         raise ValueError("stmg_b200 expects C-contiguous float64 host arrays")
     return a.ctypes.data
+
+
+_HALO_FN = ctypes.CFUNCTYPE(_c_int, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int64, _c_void_p)
+_REDUCE_FN = ctypes.CFUNCTYPE(_c_int, _c_void_p, _c_void_p, ctypes.c_int64, _c_void_p)
+
+
+class _CommOps(ctypes.Structure):
+    """struct stmg_comm_ops (include/stmg_b200.h)."""
+    _fields_ = [("user", _c_void_p), ("rank", _c_int), ("world", _c_int), ("exchange_halo", _HALO_FN),
+                ("allreduce_sum", _REDUCE_FN), ("allgather", _HALO_FN)]
+
+
+def _guard(fn):
+    """Callbacks must not raise into C: map exceptions to a non-zero status."""
+    def wrapped(*args):
+        try:
+            fn(*args)
+            return 0
+        except BaseException as exc:  # noqa: BLE001 - reported through the status code
+            import traceback
+
+            traceback.print_exception(exc)
+            return 1
+    return wrapped
 
 
 class Context:
@@ -282,6 +310,37 @@ class Solver:
         iters = (ctypes.c_int * self.n_steps)()
         _check(load_library().stmg_time_march_host(self._h, _hptr(F), _hptr(X), iters))
         return [int(v) for v in iters]
+
+    def set_comm(self, comm) -> None:
+        """Install a time-slab communicator (``timeslab.TorchComm`` /
+        ``timeslab.LoopbackComm``: attributes ``rank``, ``world`` and methods
+        ``exchange_halo(send, recv, n, stream)``, ``allreduce_sum(buf, n,
+        stream)``, ``allgather(send, recv, n, stream)`` taking raw device
+        pointers), or remove it with None."""
+        lib = load_library()
+        if comm is None:
+            self._comm = None
+            _check(lib.stmg_solver_set_comm(self._h, None))
+            return
+        ops = _CommOps(None, comm.rank, comm.world,
+                       _HALO_FN(_guard(lambda u, s, r, n, st: comm.exchange_halo(s, r, n, st))),
+                       _REDUCE_FN(_guard(lambda u, b, n, st: comm.allreduce_sum(b, n, st))),
+                       _HALO_FN(_guard(lambda u, s, r, n, st: comm.allgather(s, r, n, st))))
+        self._comm = ops  # the C side keeps the function pointers: keep them alive
+        _check(lib.stmg_solver_set_comm(self._h, ctypes.byref(ops)))
+
+    def vcycle_all_at_once(self, b, x, n_intervals: int):
+        """One all-at-once V-cycle over n_intervals intervals (Eq. GloSys)."""
+        _check(load_library().stmg_vcycle_all_at_once(self._h, _ptr(b), _ptr(x), n_intervals))
+        return x
+
+    def solve_all_at_once(self, F, X, n_intervals: int, v_init=None, history_cap: int = 256):
+        """FGMRES + all-at-once hp-STMG on a slab; returns (iterations, residual history)."""
+        it = _c_int(0)
+        hist = (ctypes.c_double * history_cap)()
+        _check(load_library().stmg_solve_all_at_once(self._h, _ptr(F), _ptr(X), n_intervals, _ptr(v_init),
+                                                      ctypes.byref(it), hist, history_cap))
+        return int(it.value), [hist[i] for i in range(min(history_cap, it.value + 1))]
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

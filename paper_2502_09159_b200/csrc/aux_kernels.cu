@@ -371,6 +371,44 @@ coarse_solve_kernel(const double *__restrict__ inv, const long long *__restrict_
     x[warp] = s;
 }
 
+// One block walks the time axis of the coarse all-at-once system (lower block
+// bidiagonal): the exact coarse solve of the all-at-once
+// V-cycle. One warp per row for the two small dense matvecs of each step.
+__global__ void __launch_bounds__(1024)
+coarse_forward_kernel(const double *__restrict__ G, const double *__restrict__ H, int n, int mv, long long v_off,
+                      const double *__restrict__ B, int n_all, int n_begin, int n_own, double *__restrict__ X)
+{
+  extern __shared__ double sh[]; // v[mv], then x_t[n]
+  double *v = sh, *xt = sh + mv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int i = tid; i < mv; i += blockDim.x)
+    v[i] = 0.0;
+  __syncthreads();
+  for (int t = 0; t < n_all; ++t)
+    {
+      const double *b = B + static_cast<long long>(t) * n;
+      for (int i = warp; i < n; i += nw)
+        {
+          const double *g = G + static_cast<long long>(i) * n, *h = H + static_cast<long long>(i) * mv;
+          double s = 0.0;
+          for (int j = lane; j < n; j += 32)
+            s = fma(g[j], b[j], s);
+          for (int j = lane; j < mv; j += 32)
+            s = fma(h[j], v[j], s);
+          s = warp_sum(s);
+          if (lane == 0)
+            xt[i] = s;
+        }
+      __syncthreads();
+      if (t >= n_begin && t < n_begin + n_own)
+        for (int i = tid; i < n; i += blockDim.x)
+          X[static_cast<long long>(t - n_begin) * n + i] = xt[i];
+      for (int i = tid; i < mv; i += blockDim.x)
+        v[i] = xt[v_off + i];
+      __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- BLAS-1
 constexpr int kDotThreads = 256;
 
@@ -535,6 +573,17 @@ cudaError_t
 launch_xpby(long long n, const double *x, double beta, double *y, cudaStream_t st)
 {
   xpby_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, x, beta, y);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_coarse_forward(const double *G, const double *H, int n, int mv, long long v_off, const double *B, int n_all,
+                      int n_begin, int n_own, double *X, cudaStream_t st)
+{
+  const size_t smem = sizeof(double) * (n + mv);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(coarse_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  coarse_forward_kernel<<<1, 1024, smem, st>>>(G, H, n, mv, v_off, B, n_all, n_begin, n_own, X);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,11 @@ cudaError_t launch_project_mean_zero(const DevGeom &G, double *x, int n_interval
 cudaError_t launch_zero_constrained(const DevGeom &G, double *x, int n_intervals, cudaStream_t st);
 cudaError_t launch_coarse_solve(const double *inv, const long long *pinned, int n_pinned, int nrows, const double *b,
                                 double *x, cudaStream_t st);
+// All-at-once coarse solve by block forward substitution in time:
+// x_t = G b_t + H v_{t-1}, v_{t-1} = slot-k velocity of x_{t-1}, v_{-1} = 0.
+// B holds n_all intervals; intervals [n_begin, n_begin + n_own) go to X.
+cudaError_t launch_coarse_forward(const double *G, const double *H, int n, int mv, long long v_off, const double *B,
+                                  int n_all, int n_begin, int n_own, double *X, cudaStream_t st);
 int dot_partials();
 cudaError_t launch_dot(const double *x, const double *y, long long n, double *part, double *out, cudaStream_t st);
 cudaError_t launch_axpy(long long n, double alpha, const double *alpha_dev, double sign, const double *x, double *y,

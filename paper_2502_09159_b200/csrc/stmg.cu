@@ -455,8 +455,8 @@ struct SolverLevel
   DevArray<int> px_ptr, px_col, py_ptr, py_col, rx_ptr, rx_col, ry_ptr, ry_col, embed;
   DevArray<double> px_val, py_val, rx_val, ry_val, child;
   DevTransfer dt{};
-  // V-cycle buffers (one interval)
-  DevArray<double> x, b, r, t;
+  // V-cycle buffers (one interval, or a slab in all-at-once mode)
+  DevArray<double> x, b, r, t, halo;
 };
 } // namespace
 
@@ -481,42 +481,78 @@ struct stmg_solver
 
   stmg_level &fine() { return *levels.back()->level; }
 
+  // ---- time-slab communicator (all-at-once mode only; see stmg_comm_ops)
+  stmg_comm_ops comm{};
+  bool has_comm = false;
+  int
+  rank() const
+  {
+    return has_comm ? comm.rank : 0;
+  }
+  int
+  world() const
+  {
+    return has_comm ? comm.world : 1;
+  }
+
+  /// Slot-k velocity of the previous rank's last interval of x at level l
+  /// (nullptr on the first rank: zero initial data / folded into the RHS).
+  const double *
+  halo(int l, const double *x, int nI)
+  {
+    if (world() == 1)
+      return nullptr;
+    stmg_level &L = *levels[l]->level;
+    DevArray<double> &h = levels[l]->halo;
+    h.resize(L.spec.mv());
+    const double *send = x + static_cast<long long>(nI - 1) * L.spec.isz() + static_cast<long long>(L.spec.S() - 1) * L.spec.mv();
+    if (comm.exchange_halo(comm.user, send, h.p, L.spec.mv(), ctx->stream) != 0)
+      throw std::runtime_error("comm: exchange_halo failed");
+    return rank() == 0 ? nullptr : h.p;
+  }
+
   void
-  restrict_residual(int l, const double *fine_v, double *coarse_v, bool project)
+  allreduce(double *buf, int n)
+  {
+    if (world() > 1 && comm.allreduce_sum(comm.user, buf, n, ctx->stream) != 0)
+      throw std::runtime_error("comm: allreduce_sum failed");
+  }
+
+  void
+  restrict_residual(int l, const double *fine_v, double *coarse_v, bool project, int nI = 1)
   {
     SolverLevel &F = *levels[l];
-    check(launch_restrict(F.dt, fine_v, coarse_v, 1, ctx->stream), "restrict");
+    check(launch_restrict(F.dt, fine_v, coarse_v, nI, ctx->stream), "restrict");
     ctx->count(2);
     if (F.kind != TransferKind::identity && project)
       {
-        levels[l - 1]->level->project(coarse_v, 1);
+        levels[l - 1]->level->project(coarse_v, nI);
       }
   }
 
   void
-  prolongate_correction(int l, const double *coarse_v, double *fine_v, bool project, bool accumulate)
+  prolongate_correction(int l, const double *coarse_v, double *fine_v, bool project, bool accumulate, int nI = 1)
   {
     SolverLevel &F = *levels[l];
+    const long long n = F.level->spec.isz() * nI;
     if (F.kind != TransferKind::identity && project)
       {
         // out = P c, zero constrained, project mean-zero, then (x +=) out
-        F.t.resize(F.level->spec.isz());
-        check(launch_prolongate(F.dt, coarse_v, F.t.p, 1, 0, ctx->stream), "prolongate");
+        F.t.resize(n);
+        check(launch_prolongate(F.dt, coarse_v, F.t.p, nI, 0, ctx->stream), "prolongate");
         ctx->count(2);
-        F.level->project(F.t.p, 1);
+        F.level->project(F.t.p, nI);
         if (accumulate)
           {
-            check(launch_axpy(F.level->spec.isz(), 1.0, nullptr, 1.0, F.t.p, fine_v, ctx->stream), "axpy");
+            check(launch_axpy(n, 1.0, nullptr, 1.0, F.t.p, fine_v, ctx->stream), "axpy");
             ctx->count();
           }
         else
-          check(cudaMemcpyAsync(fine_v, F.t.p, sizeof(double) * F.level->spec.isz(), cudaMemcpyDeviceToDevice,
-                                ctx->stream),
-                "copy");
+          check(cudaMemcpyAsync(fine_v, F.t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
       }
     else
       {
-        check(launch_prolongate(F.dt, coarse_v, fine_v, 1, accumulate ? 1 : 0, ctx->stream), "prolongate");
+        check(launch_prolongate(F.dt, coarse_v, fine_v, nI, accumulate ? 1 : 0, ctx->stream), "prolongate");
         ctx->count(2);
       }
   }
@@ -529,32 +565,135 @@ struct stmg_solver
     levels[0]->level->project(x_v, 1);
   }
 
-  // VCycle::cycle (solver.cpp:69-93); writes the result into x_v.
+  // ---- all-at-once coarse solve: x_t = G b_t + H v_{t-1} with
+  // G = P A^+ (pinned solve then mean-zero projection, solver.cpp:43-54) and
+  // H = G C_c (the jump coupling of level 0, st_operator.cpp:409-421).
+  DevArray<double> cf_G, cf_H, cf_B;
+  int cf_mv = 0;
+  bool cf_ready = false;
+
   void
-  cycle(int l, const double *b_v, double *x_v)
+  prepare_coarse_forward()
+  {
+    if (cf_ready)
+      return;
+    stmg_level &L0 = *levels[0]->level;
+    const LevelSpec &sp = L0.spec;
+    const int n = coarse_n, mv = static_cast<int>(sp.mv());
+    std::vector<double> inv(static_cast<size_t>(n) * n);
+    std::vector<long long> pin(n_pinned);
+    check(cudaMemcpy(inv.data(), coarse_inv.p, sizeof(double) * inv.size(), cudaMemcpyDeviceToHost), "d2h");
+    check(cudaMemcpy(pin.data(), coarse_pinned.p, sizeof(long long) * pin.size(), cudaMemcpyDeviceToHost), "d2h");
+    for (long long q : pin) // pinned right-hand-side entries are ignored
+      for (int i = 0; i < n; ++i)
+        inv[static_cast<size_t>(i) * n + q] = 0.0;
+    // mean-zero projection per slot: mode-0 pressure entries minus their
+    // cell-area-weighted mean (dof_space.cpp:110-119; uniform cells)
+    const int ncell = sp.nx * sp.ny;
+    std::vector<double> G(inv);
+    for (int a = 0; a < sp.S(); ++a)
+      {
+        const long long base = sp.S() * sp.mv() + a * sp.mp();
+        for (int j = 0; j < n; ++j)
+          {
+            double mean = 0.0;
+            for (int c = 0; c < ncell; ++c)
+              mean += inv[static_cast<size_t>(base + static_cast<long long>(c) * sp.np()) * n + j];
+            mean /= ncell;
+            for (int c = 0; c < ncell; ++c)
+              G[static_cast<size_t>(base + static_cast<long long>(c) * sp.np()) * n + j] -= mean;
+          }
+      }
+    // C_c column by column: residual of x = 0 with unit previous velocity
+    DevArray<double> e, out;
+    e.resize(mv);
+    out.resize(n);
+    const double *zero = L0.zero_vector(1);
+    std::vector<double> Cc(static_cast<size_t>(n) * mv);
+    std::vector<double> col(n);
+    const double one = 1.0;
+    for (int j = 0; j < mv; ++j)
+      {
+        check(cudaMemsetAsync(e.p, 0, sizeof(double) * mv, ctx->stream), "memset");
+        check(cudaMemcpyAsync(e.p + j, &one, sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "h2d");
+        L0.vmult(zero, zero, out.p, 1, e.p, 1, 1);
+        check(launch_zero_constrained(L0.geom, out.p, 1, ctx->stream), "zero");
+        check(cudaMemcpyAsync(col.data(), out.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        check(cudaStreamSynchronize(ctx->stream), "sync");
+        for (int i = 0; i < n; ++i)
+          Cc[static_cast<size_t>(i) * mv + j] = col[i];
+      }
+    std::vector<double> H(static_cast<size_t>(n) * mv, 0.0);
+    for (int i = 0; i < n; ++i)
+      for (int q = 0; q < n; ++q)
+        {
+          const double g = G[static_cast<size_t>(i) * n + q];
+          if (g != 0.0)
+            for (int j = 0; j < mv; ++j)
+              H[static_cast<size_t>(i) * mv + j] += g * Cc[static_cast<size_t>(q) * mv + j];
+        }
+    cf_G.upload(G);
+    cf_H.upload(H);
+    cf_mv = mv;
+    cf_ready = true;
+  }
+
+  void
+  coarse_forward(const double *b_v, double *x_v, int nI)
+  {
+    prepare_coarse_forward();
+    const LevelSpec &sp = levels[0]->level->spec;
+    const long long per = static_cast<long long>(coarse_n) * nI;
+    const double *B = b_v;
+    if (world() > 1)
+      {
+        cf_B.resize(per * world());
+        if (comm.allgather(comm.user, b_v, cf_B.p, per, ctx->stream) != 0)
+          throw std::runtime_error("comm: allgather failed");
+        B = cf_B.p;
+      }
+    check(launch_coarse_forward(cf_G.p, cf_H.p, coarse_n, cf_mv, (sp.S() - 1) * sp.mv(), B, nI * world(),
+                                nI * rank(), nI, x_v, ctx->stream),
+          "coarse_forward");
+    ctx->count();
+  }
+
+  // VCycle::cycle (solver.cpp:69-93); writes the result into x_v. With aao,
+  // the cycle acts on nI intervals of the all-at-once system: residuals carry
+  // the jump coupling (halo from the previous rank), the coarse solve is the
+  // block forward substitution.
+  void
+  cycle(int l, const double *b_v, double *x_v, int nI = 1, bool aao = false)
   {
     if (l == 0)
       {
-        coarse_solve(b_v, x_v);
+        if (aao)
+          coarse_forward(b_v, x_v, nI);
+        else
+          coarse_solve(b_v, x_v);
         return;
       }
     SolverLevel &S = *levels[l];
     stmg_level &L = *S.level;
-    const long long isz = L.spec.isz();
+    const long long isz = L.spec.isz() * nI;
     S.r.resize(isz);
     check(cudaMemsetAsync(x_v, 0, sizeof(double) * isz, ctx->stream), "memset");
     for (int s = 0; s < nu1; ++s)
-      L.smooth_step(b_v, x_v, omega, 1, nullptr, 0, S.r.p, s == 0);
-    L.vmult(x_v, b_v, S.r.p, 1, nullptr, 0, 1);
+      {
+        // x = 0 on every rank before the first sweep: b - A 0 = b exactly
+        const bool coupled = aao && s > 0;
+        L.smooth_step(b_v, x_v, omega, nI, coupled ? halo(l, x_v, nI) : nullptr, coupled ? 1 : 0, S.r.p, s == 0);
+      }
+    L.vmult(x_v, b_v, S.r.p, nI, aao ? halo(l, x_v, nI) : nullptr, aao ? 1 : 0, 1);
     SolverLevel &C = *levels[l - 1];
-    const long long csz = C.level->spec.isz();
+    const long long csz = C.level->spec.isz() * nI;
     C.b.resize(csz);
     C.x.resize(csz);
-    restrict_residual(l, S.r.p, C.b.p, project_pressure);
-    cycle(l - 1, C.b.p, C.x.p);
-    prolongate_correction(l, C.x.p, x_v, project_pressure, true);
+    restrict_residual(l, S.r.p, C.b.p, project_pressure, nI);
+    cycle(l - 1, C.b.p, C.x.p, nI, aao);
+    prolongate_correction(l, C.x.p, x_v, project_pressure, true, nI);
     for (int s = 0; s < nu2; ++s)
-      L.smooth_step(b_v, x_v, omega, 1, nullptr, 0, S.r.p);
+      L.smooth_step(b_v, x_v, omega, nI, aao ? halo(l, x_v, nI) : nullptr, aao ? 1 : 0, S.r.p);
   }
 
   void
@@ -568,6 +707,7 @@ struct stmg_solver
   {
     check(launch_dot(a, b, n, part.p, scal.p + slot, ctx->stream), "dot");
     ctx->count(2);
+    allreduce(scal.p + slot, 1);
     double h = 0.0;
     check(cudaMemcpyAsync(&h, scal.p + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
     check(cudaStreamSynchronize(ctx->stream), "sync");
@@ -583,12 +723,16 @@ struct stmg_solver
     return *B[j];
   }
 
-  // gmres (solver.cpp:95-202), x0 = 0, preconditioner = V-cycle.
+  // gmres (solver.cpp:95-202), x0 = 0, preconditioner = V-cycle. With aao,
+  // the operator and V-cycle are the all-at-once ones over nI intervals and
+  // every inner product is summed over the ranks of the time-slab partition.
   int
-  gmres(const double *b_v, double *x_v, int *iterations, double *history, int history_cap)
+  gmres(const double *b_v, double *x_v, int *iterations, double *history, int history_cap, int nI = 1,
+        bool aao = false)
   {
     stmg_level &L = fine();
-    const long long n = L.spec.isz();
+    const int top = static_cast<int>(levels.size()) - 1;
+    const long long n = L.spec.isz() * nI;
     w.resize(n);
     part.resize(dot_partials());
     scal.resize(2 * (max_iterations + 2));
@@ -617,16 +761,18 @@ struct stmg_solver
         for (; j < m; ++j)
           {
             DevArray<double> &zj = basis(Z, j, n);
-            vcycle(V[j]->p, zj.p);
-            L.vmult(zj.p, nullptr, w.p, 1, nullptr, 0, 0);
+            cycle(top, V[j]->p, zj.p, nI, aao);
+            L.vmult(zj.p, nullptr, w.p, nI, aao ? halo(top, zj.p, nI) : nullptr, aao ? 1 : 0, 0);
             // modified Gram-Schmidt with device-resident coefficients
             for (int i = 0; i <= j; ++i)
               {
                 check(launch_dot(w.p, V[i]->p, n, part.p, scal.p + i, ctx->stream), "dot");
+                allreduce(scal.p + i, 1);
                 check(launch_axpy(n, 0.0, scal.p + i, -1.0, V[i]->p, w.p, ctx->stream), "axpy");
                 ctx->count(3);
               }
             check(launch_dot(w.p, w.p, n, part.p, scal.p + j + 1, ctx->stream), "dot");
+            allreduce(scal.p + j + 1, 1);
             ctx->count(2);
             check(cudaMemcpyAsync(hcol.data(), scal.p, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->stream),
                   "d2h");
@@ -686,6 +832,30 @@ struct stmg_solver
     if (!converged)
       throw std::runtime_error("gmres: not converged within max_iterations");
     return iters;
+  }
+
+  // All-at-once solve of A X = F on a slab (Eq. GloSys).
+  // v_init enters the slab's first interval like time_march's v_prev
+  // (solver.cpp:251-268): F_0 += C v_init, constrained rows zeroed.
+  int
+  solve_all_at_once(const double *F, double *X, int nI, const double *v_init, int *iterations, double *history,
+                    int history_cap)
+  {
+    if (nI < 1)
+      throw std::invalid_argument("solve_all_at_once: need at least one interval");
+    stmg_level &L = fine();
+    const long long n = L.spec.isz() * nI;
+    rhs.resize(n);
+    check(cudaMemcpyAsync(rhs.p, F, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    if (v_init && rank() == 0)
+      {
+        L.vmult(L.zero_vector(1), F, rhs.p, 1, v_init, 1, 1);
+        check(launch_zero_constrained(L.geom, rhs.p, 1, ctx->stream), "zero");
+        ctx->count();
+      }
+    const int it = gmres(rhs.p, X, iterations, history, history_cap, nI, true);
+    L.project(X, nI);
+    return it;
   }
 
   // time_march (solver.cpp:204-325) with per-step load vectors F.
@@ -1104,6 +1274,42 @@ int
 stmg_gmres(stmg_solver *s, const double *b, double *x, int *iterations, double *history, int history_cap)
 {
   return guarded([&] { s->gmres(b, x, iterations, history, history_cap); });
+}
+
+int
+stmg_solver_set_comm(stmg_solver *s, const stmg_comm_ops *ops)
+{
+  return guarded([&] {
+    if (!ops)
+      {
+        s->has_comm = false;
+        s->comm = stmg_comm_ops{};
+        return;
+      }
+    if (ops->world < 1 || ops->rank < 0 || ops->rank >= ops->world)
+      throw std::invalid_argument("stmg_solver_set_comm: invalid rank/world");
+    if (ops->world > 1 && (!ops->exchange_halo || !ops->allreduce_sum || !ops->allgather))
+      throw std::invalid_argument("stmg_solver_set_comm: missing callback");
+    s->comm = *ops;
+    s->has_comm = true;
+  });
+}
+
+int
+stmg_vcycle_all_at_once(stmg_solver *s, const double *b, double *x, int n_intervals)
+{
+  return guarded([&] {
+    if (n_intervals < 1)
+      throw std::invalid_argument("stmg_vcycle_all_at_once: need at least one interval");
+    s->cycle(static_cast<int>(s->levels.size()) - 1, b, x, n_intervals, true);
+  });
+}
+
+int
+stmg_solve_all_at_once(stmg_solver *s, const double *F, double *X, int n_intervals, const double *v_init,
+                       int *iterations, double *history, int history_cap)
+{
+  return guarded([&] { s->solve_all_at_once(F, X, n_intervals, v_init, iterations, history, history_cap); });
 }
 
 int

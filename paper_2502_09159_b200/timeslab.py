@@ -46,3 +46,154 @@ def exchange_halo(x, halo, n_local: int, interval_size: int, n_velocity: int, n_
     for w in dist.batch_isend_irecv(ops):
         w.wait()
     return halo if rank > 0 else None
+
+
+# ---------------------------------------------------------------- communicators
+# Implementations of the library's stmg_comm_ops (include/stmg_b200.h) for the
+# all-at-once solve: Solver.set_comm(comm). The library passes raw pointers
+# and its stream; every exchange is stream-ordered on that stream.
+
+def _view(ptr: int, n: int, device):
+    """Zero-copy float64 tensor over a raw pointer (device or host memory)."""
+    import ctypes
+
+    import torch
+
+    if n == 0:
+        return torch.empty(0, dtype=torch.float64, device=device)
+    if torch.device(device).type == "cuda":
+        class _Iface:
+            __cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                        "version": 3, "strides": None}
+        return torch.as_tensor(_Iface(), device=device)
+    return torch.frombuffer((ctypes.c_double * int(n)).from_address(int(ptr)), dtype=torch.float64)
+
+
+def _on_stream(stream, device):
+    import contextlib
+
+    import torch
+
+    if stream and torch.device(device).type == "cuda":
+        return torch.cuda.stream(torch.cuda.ExternalStream(int(stream), device=device))
+    return contextlib.nullcontext()
+
+
+class TorchComm:
+    """Time-slab communicator over torch.distributed (NCCL over NVLink on
+    the GPU box; gloo for CPU tests): point-to-point halo, all-reduce of the
+    Krylov dots, all-gather of the coarse right-hand sides."""
+
+    def __init__(self, device="cuda", group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device
+
+    def exchange_halo(self, send, recv, n, stream=None):
+        import torch.distributed as dist
+
+        with _on_stream(stream, self.device):
+            ops = []
+            if self.rank + 1 < self.world:
+                ops.append(dist.P2POp(dist.isend, _view(send, n, self.device), self.rank + 1, group=self.group))
+            if self.rank > 0:
+                ops.append(dist.P2POp(dist.irecv, _view(recv, n, self.device), self.rank - 1, group=self.group))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+
+    def allreduce_sum(self, buf, n, stream=None):
+        import torch.distributed as dist
+
+        with _on_stream(stream, self.device):
+            dist.all_reduce(_view(buf, n, self.device), group=self.group)
+
+    def allgather(self, send, recv, n, stream=None):
+        import torch.distributed as dist
+
+        with _on_stream(stream, self.device):
+            out = _view(recv, n * self.world, self.device)
+            src = _view(send, n, self.device)
+            if hasattr(dist, "all_gather_into_tensor") and out.is_cuda:
+                dist.all_gather_into_tensor(out, src, group=self.group)
+            else:
+                dist.all_gather(list(out.split(n)), src, group=self.group)
+
+
+class LoopbackHub:
+    """Shared state of `world` in-process ranks (one thread each). Every
+    exchange is host-synchronised: a rank finishes its stream, hands over a
+    copy, and the receiver copies it in. No kernel ever waits on another
+    rank's kernel, so several ranks can share one GPU safely. This is how the
+    partitioned solve is tested on a single B200."""
+
+    def __init__(self, world: int, timeout: float = 120.0):
+        import queue
+        import threading
+
+        self.world = world
+        self.timeout = timeout
+        self.barrier = threading.Barrier(world)
+        self.lock = threading.Lock()
+        self.slots = {}
+        self.mail = [queue.Queue() for _ in range(world)]
+
+    def gather(self, rank, t):
+        with self.lock:
+            self.slots[rank] = t
+        self.barrier.wait(self.timeout)
+        parts = [self.slots[r] for r in range(self.world)]
+        self.barrier.wait(self.timeout)  # all read before the next round writes
+        return parts
+
+
+class LoopbackComm:
+    def __init__(self, hub: LoopbackHub, rank: int, device="cuda"):
+        self.hub, self.rank, self.world, self.device = hub, rank, hub.world, device
+
+    def _sync(self, stream):
+        import torch
+
+        if torch.device(self.device).type == "cuda":
+            if stream:
+                torch.cuda.ExternalStream(int(stream), device=self.device).synchronize()
+            else:
+                torch.cuda.synchronize(self.device)
+
+    def _snapshot(self, ptr, n, stream):
+        with _on_stream(stream, self.device):
+            t = _view(ptr, n, self.device).clone()
+        self._sync(stream)
+        return t
+
+    def exchange_halo(self, send, recv, n, stream=None):
+        self._sync(stream)
+        if self.rank + 1 < self.world:
+            self.hub.mail[self.rank + 1].put(self._snapshot(send, n, stream))
+        if self.rank > 0:
+            data = self.hub.mail[self.rank].get(timeout=self.hub.timeout)
+            with _on_stream(stream, self.device):
+                _view(recv, n, self.device).copy_(data)
+            self._sync(stream)
+
+    def allreduce_sum(self, buf, n, stream=None):
+        self._sync(stream)
+        parts = self.hub.gather(self.rank, self._snapshot(buf, n, stream))
+        with _on_stream(stream, self.device):
+            total = parts[0].clone()
+            for p in parts[1:]:  # fixed rank order: identical sums on every rank
+                total += p
+            _view(buf, n, self.device).copy_(total)
+        self._sync(stream)
+
+    def allgather(self, send, recv, n, stream=None):
+        self._sync(stream)
+        parts = self.hub.gather(self.rank, self._snapshot(send, n, stream))
+        with _on_stream(stream, self.device):
+            out = _view(recv, n * self.world, self.device)
+            for r, p in enumerate(parts):
+                out[r * n:(r + 1) * n].copy_(p)
+        self._sync(stream)

@@ -75,3 +75,89 @@ def test_time_slab_partition_matches_single_process(oracle):
     u_ref = lvl.smooth_step_all(b, x, 0.8, N_GLOBAL, None)
     assert np.array_equal(y_part, y_ref)
     assert np.array_equal(u_part, u_ref)
+
+
+# ------------------------------------------------ communicator callbacks
+# The library's stmg_comm_ops receive raw pointers. TorchComm is the
+# implementation bench.py installs over NCCL; here it runs over gloo on host
+# buffers (same code, device "cpu") and LoopbackComm on host threads.
+
+def _comm_worker(rank, world, port, out):
+    import ctypes
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = timeslab.TorchComm(device="cpu")
+    n = 5
+    send = np.arange(n, dtype=np.float64) + 100 * rank
+    recv = np.full(n, -1.0)
+    comm.exchange_halo(send.ctypes.data, recv.ctypes.data, n, None)
+    buf = np.full(3, rank + 1.0)
+    comm.allreduce_sum(buf.ctypes.data, 3, None)
+    gat = np.zeros(n * world)
+    comm.allgather(send.ctypes.data, gat.ctypes.data, n, None)
+    out.put((rank, recv.copy(), buf.copy(), gat.copy()))
+    dist.destroy_process_group()
+    del ctypes
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torch_comm_callbacks_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, recv, buf, gat = q.get(timeout=300)
+        res[rank] = (recv, buf, gat)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 5
+    every = np.concatenate([np.arange(n) + 100.0 * r for r in range(world)])
+    for rank, (recv, buf, gat) in res.items():
+        if rank == 0:
+            assert np.all(recv == -1.0)  # first rank receives nothing
+        else:
+            assert np.array_equal(recv, np.arange(n) + 100.0 * (rank - 1))
+        assert np.all(buf == world * (world + 1) / 2)
+        assert np.array_equal(gat, every)
+
+
+def test_loopback_comm_threads_on_host():
+    import threading
+
+    world, n = 3, 4
+    hub = timeslab.LoopbackHub(world, timeout=30)
+    res, errs = {}, []
+
+    def run(rank):
+        try:
+            c = timeslab.LoopbackComm(hub, rank, device="cpu")
+            send = np.arange(n, dtype=np.float64) + 10 * rank
+            recv = np.full(n, -1.0)
+            c.exchange_halo(send.ctypes.data, recv.ctypes.data, n, None)
+            buf = np.array([rank + 0.5, 1.0])
+            c.allreduce_sum(buf.ctypes.data, 2, None)
+            gat = np.zeros(n * world)
+            c.allgather(send.ctypes.data, gat.ctypes.data, n, None)
+            res[rank] = (recv, buf, gat)
+        except BaseException as exc:
+            errs.append(exc)
+            hub.barrier.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(60)
+    assert not errs, errs
+    every = np.concatenate([np.arange(n) + 10.0 * r for r in range(world)])
+    for rank, (recv, buf, gat) in res.items():
+        assert np.array_equal(recv, np.full(n, -1.0) if rank == 0 else np.arange(n) + 10.0 * (rank - 1))
+        assert np.allclose(buf, [sum(r + 0.5 for r in range(world)), world])
+        assert np.array_equal(gat, every)
