@@ -145,7 +145,7 @@ struct stmg_level
     DevArray<int> coln;
   };
   bool super = false;
-  SuperSet sup[2]; // [0]: many intervals per launch, [1]: few (time marching)
+  SuperSet sup[3]; // intervals per block: [0] 16, [2] 8 (slabs), [1] 1 (time marching)
   int max_nt = 0;
   int n_classes = 0;
   std::uint64_t total_matrix_elements = 0;
@@ -176,7 +176,8 @@ struct stmg_level
       throw std::invalid_argument("level has no smoother");
     if (super)
       {
-        const SuperSet &ss = sup[n < 8 ? 1 : 0];
+        // widest interval group that the launch fills: 16, 8 or 1 per block
+        const SuperSet &ss = sup[n >= 16 ? 0 : (n >= 8 ? 2 : 1)];
         if (!ss.tile_ptr.empty())
           {
             for (size_t sc = 0; sc < ss.tile_ptr.size(); ++sc)
@@ -323,11 +324,13 @@ build_level(stmg_level &L)
         for (const auto &e : col)
           cls_of[static_cast<size_t>(e.ay) * nax + e.ax] = e.cls;
       const int nsx = (nax + P - 1) / P, nsy = (nay + P - 1) / P;
-      // B super-cells per block: few for many intervals (columns = B * 16
-      // intervals), many for time marching (one interval, 16 columns).
-      for (int set = 0; set < 2; ++set)
+      // B super-cells per block: few for many intervals (columns = B x 16
+      // intervals), twice as many for 8-interval slabs, 32 for time marching
+      // (one interval per block).
+      for (int set = 0; set < 3; ++set)
         {
-          const int B = set == 0 ? (P == 2 ? 4 : 2) : 32;
+          const int B0 = P == 2 ? 4 : 2;
+          const int B = set == 0 ? B0 : (set == 2 ? 2 * B0 : 32);
           stmg_level::SuperSet &ss = L.sup[set];
           std::vector<VankaBatch> items;
           std::vector<long long> sva, spa;
@@ -383,7 +386,7 @@ build_level(stmg_level &L)
 
           // expand the items into tensor-core tiles of <= 32 columns
           // (patch-major, interval-minor; ng_full intervals per block)
-          ss.ng_full = set == 0 ? 16 : 1;
+          ss.ng_full = set == 0 ? 16 : (set == 2 ? 8 : 1);
           const int tc = vanka_tc_cols();
           bool tc_ok = true;
           std::vector<VankaTile> tiles;
