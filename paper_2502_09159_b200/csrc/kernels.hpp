@@ -65,6 +65,7 @@ cudaError_t launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles
                             cudaStream_t stream);
 int vanka_tc_cols();
 int vanka_tc_max_tiles();
+int vanka_tc_stage(); // tiles per barrier stage
 
 cudaError_t launch_vmult(int r, int S, const LevelConsts &P, const double *x, const double *b, double *y,
                          int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t stream);

@@ -329,10 +329,11 @@ build_level(stmg_level &L)
       // (one interval per block).
       for (int set = 0; set < 3; ++set)
         {
-          const int B0 = P == 2 ? 4 : 2;
+          const int B0 = 4;
           const int B = set == 0 ? B0 : (set == 2 ? 2 * B0 : 32);
           stmg_level::SuperSet &ss = L.sup[set];
           std::vector<VankaBatch> items;
+          std::vector<int> item_phase; // colour sub-phase (qy, qx) of each item
           std::vector<long long> sva, spa;
           ss.pass_ptr.resize(4);
           ss.pass_blocks.assign(4, 0);
@@ -372,6 +373,7 @@ build_level(stmg_level &L)
                                     ++i;
                                   }
                                 items.push_back(it);
+                                item_phase.push_back(qy * P + qx);
                               }
                           }
                       ptr.push_back(static_cast<int>(items.size()));
@@ -399,10 +401,28 @@ build_level(stmg_level &L)
               std::vector<int> hptr(ss.pass_blocks[sc] + 1);
               cudaMemcpy(hptr.data(), ss.pass_ptr[sc].p, sizeof(int) * hptr.size(), cudaMemcpyDeviceToHost);
               std::vector<int> tptr{static_cast<int>(tiles.size())};
+              const int stage = vanka_tc_stage();
               for (int blk = 0; blk < ss.pass_blocks[sc]; ++blk)
                 {
+                  int phase_first = static_cast<int>(tiles.size());
+                  // close a colour sub-phase: pad with empty tiles to whole stages
+                  const auto pad = [&](int cls) {
+                    while ((static_cast<int>(tiles.size()) - phase_first) % stage != 0)
+                      {
+                        tiles.push_back(VankaTile{cls, 0});
+                        for (int c = 0; c < tc; ++c)
+                          {
+                            colv.push_back(0);
+                            colp.push_back(0);
+                            coln.push_back(1 << 30);
+                          }
+                      }
+                    phase_first = static_cast<int>(tiles.size());
+                  };
                   for (int it = hptr[blk]; it < hptr[blk + 1]; ++it)
                     {
+                      if (it > hptr[blk] && item_phase[it] != item_phase[it - 1])
+                        pad(items[it - 1].cls);
                       const VankaBatch &item = items[it];
                       const int ncols = item.count * ss.ng_full;
                       for (int c0 = 0; c0 < ncols; c0 += tc)
@@ -428,6 +448,8 @@ build_level(stmg_level &L)
                           tiles.push_back(tl);
                         }
                     }
+                  if (hptr[blk + 1] > hptr[blk])
+                    pad(items[hptr[blk + 1] - 1].cls);
                   tptr.push_back(static_cast<int>(tiles.size()));
                   if (tptr.back() - tptr[tptr.size() - 2] > vanka_tc_max_tiles())
                     tc_ok = false; // block too long for the staged tile data

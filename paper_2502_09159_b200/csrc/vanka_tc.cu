@@ -4,16 +4,19 @@
 // (vanka.cpp:196-233): u += omega * sum_T R_T^T w_T A_T^{-1} R_T r.
 //
 // Per block: a host-built list of tiles, each <= 32 columns (patch, interval)
-// of one congruence class inside one super-cell colour sub-phase.
-//  * gather: R tiles are copied global -> shared with cp.async two tiles
-//    ahead (3-slot ring), so residual loads never hold registers and their
-//    latency overlaps the tensor work of earlier tiles;
+// of one congruence class inside one super-cell colour sub-phase, grouped in
+// stages of kTStage tiles (one barrier per stage; the host pads every colour
+// sub-phase to whole stages, so a stage never mixes colours).
+//  * gather: R tiles are copied global -> shared with cp.async one stage
+//    ahead (double-buffered stages), so residual loads never hold registers
+//    and their latency overlaps the tensor work of the previous stage;
 //  * Z = A^{-1} R with mma.sync.m8n8k4.f64 (DMMA); the class inverse lives in
 //    registers as A-fragments, warp w owns rows 8w..8w+7;
 //  * scatter straight from the accumulator fragments with red.global.add.f64:
 //    no read-back of u, no Z staging. The super-cell colouring guarantees that
-//    no two concurrently running tiles touch the same dof, and tiles of one
-//    block are ordered by the per-tile barrier, so results are deterministic.
+//    no two concurrently running tiles touch the same dof (tiles of one stage
+//    share a colour; stages are ordered by the barrier), so results are
+//    deterministic.
 #include "kernels.hpp"
 
 #include <cuda_runtime.h>
@@ -26,10 +29,31 @@ namespace
 constexpr int kTThreads = 512;
 constexpr int kTRows = 128;
 constexpr int kTCols = 32;
-constexpr int kTLd = 36; // == 4 mod 16 doubles: conflict-free B-fragment loads
+// Diagnostic build switches (wrong results, timing only; DESIGN.md §3.2 cost
+// breakdown): STMG_VT_NO_GATHER, STMG_VT_NO_SCATTER. STMG_VT_ROWMAJOR selects
+// the previous row-major R tile layout.
+#ifndef STMG_VT_ROWMAJOR
+// R tiles column-major in shared memory: element (row k, column n) at
+// n * kTLd + k. The gather walks rows with the lanes of a warp (rows of a
+// patch come in contiguous runs of 4-6 dofs: few sectors per instruction);
+// pitch 132 == 4 mod 16 doubles keeps the DMMA B-fragment loads
+// (k = lane % 4, n = lane / 4) conflict-free.
+constexpr int kTLd = kTRows + 4;
+constexpr int kTSlot = kTCols * kTLd;
+#else
+constexpr int kTLd = 36; // row-major, == 4 mod 16 doubles: conflict-free B-fragment loads
 constexpr int kTSlot = kTRows * kTLd;
-constexpr int kTMaxTiles = 64; // tiles per block (host falls back beyond)
-constexpr size_t kTSmem = sizeof(double) * 3 * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4));
+#endif
+#ifndef STMG_VANKA_STAGE
+#define STMG_VANKA_STAGE 1
+#endif
+constexpr int kTStage = STMG_VANKA_STAGE; // tiles per barrier stage
+constexpr int kTSlots = 2 * kTStage;      // double-buffered stages
+#ifndef STMG_VANKA_MAXTILES
+#define STMG_VANKA_MAXTILES 32
+#endif
+constexpr int kTMaxTiles = STMG_VANKA_MAXTILES; // tiles per block (host falls back beyond)
+constexpr size_t kTSmem = sizeof(double) * kTSlots * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4));
 
 __device__ __forceinline__ void
 cp_async8(double *dst, const double *src)
@@ -43,9 +67,9 @@ cp_async_commit()
   asm volatile("cp.async.commit_group;\n" ::);
 }
 __device__ __forceinline__ void
-cp_async_wait1()
+cp_async_wait0()
 {
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void
@@ -63,8 +87,8 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
                 const int *__restrict__ tile_ptr, int ng_full, const double *__restrict__ r, double *__restrict__ u,
                 long long isz, int n_intervals, double omega)
 {
-  extern __shared__ __align__(16) double ring[]; // 3 slots of kTRows x kTLd, then the block's tile data
-  long long *s_colv = reinterpret_cast<long long *>(ring + 3 * kTSlot);
+  extern __shared__ __align__(16) double ring[]; // kTSlots slots of kTRows x kTLd, then the block's tile data
+  long long *s_colv = reinterpret_cast<long long *>(ring + kTSlots * kTSlot);
   long long *s_colp = s_colv + kTMaxTiles * kTCols;
   int *s_coln = reinterpret_cast<int *>(s_colp + kTMaxTiles * kTCols);
   VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_coln + kTMaxTiles * kTCols);
@@ -85,17 +109,28 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
     s_tile[e] = tiles[t0 + e];
   __syncthreads();
 
+#ifndef STMG_VT_ROWMAJOR
+  // gather: warp w fills columns w and w + 16, lane l rows l + 32 q
+  constexpr int QN = kTRows / 32;
+  constexpr int CN = kTCols / (kTThreads / 32);
+  const int lane_g = tid & 31, warp_g = tid >> 5;
+  auto row_of = [&](int q) { return lane_g + 32 * q; };
+#else
   // gather rows of this thread: row = tid/32 + 16 q (fixed across tiles)
   constexpr int QN = kTRows * kTCols / kTThreads;
+  const int col_g = tid & 31;
+  auto row_of = [&](int q) { return (tid >> 5) + q * (kTThreads / kTCols); };
+#endif
   int cls_issue = -1, nt_issue = 0, nvel_issue = 0;
   long long relq[QN];
-  const int col_g = tid & 31;
 
   // gather of local tile lt into ring slot s
   auto issue = [&](int lt, int s) {
     if (lt < nb)
       {
         const VankaTile tl = s_tile[lt];
+        if (tl.ncols == 0)
+          return; // stage padding: nothing to gather
         if (tl.cls != cls_issue)
           {
             const DevPatchClass pc = classes[tl.cls];
@@ -103,32 +138,63 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
             nvel_issue = pc.n_vel;
 #pragma unroll
             for (int q = 0; q < QN; ++q)
-              {
-                const int row = (tid >> 5) + q * (kTThreads / kTCols);
-                relq[q] = row < nt_issue ? pc.rel[row] : 0;
-              }
+              relq[q] = row_of(q) < nt_issue ? pc.rel[row_of(q)] : 0;
             cls_issue = tl.cls;
           }
         double *slot = ring + s * kTSlot;
+#ifndef STMG_VT_ROWMAJOR
+#pragma unroll
+        for (int cc = 0; cc < CN; ++cc)
+          {
+            const int col = warp_g + cc * (kTThreads / 32);
+            const int ci = lt * kTCols + col;
+            const bool colok = col < tl.ncols && n0 + s_coln[ci] < n_intervals;
+            const long long cv = base0 + s_colv[ci], cp = base0 + s_colp[ci];
+#pragma unroll
+            for (int q = 0; q < QN; ++q)
+              {
+                const int row = row_of(q);
+                double *dst = slot + col * kTLd + row;
+#ifdef STMG_VT_NO_GATHER
+                if (false)
+#else
+                if (colok && row < nt_issue)
+#endif
+                  cp_async8(dst, r + (row < nvel_issue ? cv : cp) + relq[q]);
+                else
+                  *dst = 0.0;
+              }
+          }
+#else
         const int ci = lt * kTCols + col_g;
         const bool colok = col_g < tl.ncols && n0 + s_coln[ci] < n_intervals;
         const long long cv = base0 + s_colv[ci], cp = base0 + s_colp[ci];
 #pragma unroll
         for (int q = 0; q < QN; ++q)
           {
-            const int row = (tid >> 5) + q * (kTThreads / kTCols);
+            const int row = row_of(q);
             double *dst = slot + row * kTLd + col_g;
+#ifdef STMG_VT_NO_GATHER
+            if (false)
+#else
             if (colok && row < nt_issue)
+#endif
               cp_async8(dst, r + (row < nvel_issue ? cv : cp) + relq[q]);
             else
               *dst = 0.0;
           }
+#endif
       }
-    cp_async_commit(); // possibly empty group: keeps the group count uniform
+  };
+  // gather of stage g (tiles kTStage*g ..) into its half of the ring
+  auto issue_stage = [&](int g) {
+#pragma unroll
+    for (int h = 0; h < kTStage; ++h)
+      issue(kTStage * g + h, (g & 1) * kTStage + h);
+    cp_async_commit(); // possibly empty group
   };
 
-  issue(0, 0);
-  issue(1, 1);
+  issue_stage(0);
 
   int loaded = -1, nt_loaded = 0;
   double afr[KS];
@@ -137,12 +203,29 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
   double w_row = 0.0;
   const int row = 8 * warp + (lane >> 2);
 
-  for (int lt = 0; lt < nb; ++lt)
+  // Stage g: wait for its gather, barrier (its slots are visible to all, the
+  // slots of stage g-1 are free), gather stage g+1 into them, then compute
+  // the stage's tiles. Within a stage the warps drift apart, so one warp's
+  // scatter overlaps the DMMAs of another.
+  const int n_stages = (nb + kTStage - 1) / kTStage;
+  for (int g = 0; g < n_stages; ++g)
+  {
+    cp_async_wait0();
+    __syncthreads();
+    issue_stage(g + 1);
+#ifdef STMG_VANKA_UNROLL_H
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+    for (int h = 0; h < kTStage; ++h)
     {
-      cp_async_wait1(); // own copies of tile lt done (tile lt+1 may be in flight)
-      __syncthreads();  // everyone's copies of tile lt visible; slot of tile lt-1 free
-      issue(lt + 2, (lt + 2) % 3);
+      const int lt = kTStage * g + h;
+      if (lt >= nb)
+        break;
       const VankaTile tl = s_tile[lt];
+      if (tl.ncols == 0)
+        continue; // stage padding (keeps colour sub-phases in separate stages)
       if (tl.cls != loaded)
         {
           const DevPatchClass pc = classes[tl.cls];
@@ -163,16 +246,26 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
 #pragma unroll
       for (int ct = 0; ct < kTCols / 8; ++ct)
         acc[ct][0] = acc[ct][1] = 0.0;
-      const double *bbase = ring + (lt % 3) * kTSlot + (lane & 3) * kTLd + (lane >> 2);
+#ifndef STMG_VT_ROWMAJOR
+      const double *bbase = ring + ((g & 1) * kTStage + h) * kTSlot + (lane >> 2) * kTLd + (lane & 3);
+#else
+      const double *bbase = ring + ((g & 1) * kTStage + h) * kTSlot + (lane & 3) * kTLd + (lane >> 2);
+#endif
       if (8 * warp < nt_loaded) // warps past n_T only join the barriers
         {
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk)
             {
+#ifndef STMG_VT_ROWMAJOR
+              const double *brow = bbase + 4 * kk;
+              constexpr int kNStep = 8 * kTLd; // next 8 columns
+#else
               const double *brow = bbase + 4 * kk * kTLd;
+              constexpr int kNStep = 8;
+#endif
 #pragma unroll
               for (int ct = 0; ct < kTCols / 8; ++ct)
-                dmma(acc[ct], afr[kk], brow[8 * ct]);
+                dmma(acc[ct], afr[kk], brow[kNStep * ct]);
             }
         }
       if (ok_row)
@@ -184,11 +277,16 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
               {
                 const int col = 8 * ct + 2 * (lane & 3) + b;
                 const int ci = lt * kTCols + col;
+#ifdef STMG_VT_NO_SCATTER
+                if (acc[ct][b] == 123.456)
+#else
                 if (col < tl.ncols && n0 + s_coln[ci] < n_intervals)
+#endif
                   atomicAdd(u + base0 + (vel_row ? s_colv[ci] : s_colp[ci]) + rel_row, acc[ct][b] * w_row);
               }
         }
     }
+  }
 }
 } // namespace
 
@@ -227,6 +325,12 @@ int
 vanka_tc_cols()
 {
   return kTCols;
+}
+
+int
+vanka_tc_stage()
+{
+  return kTStage;
 }
 
 int

@@ -212,3 +212,22 @@ def test_kernels_really_launch(ctx, stmg):
     lvl.vmult(x, y)
     lvl.smooth_step(x, y, 0.8)
     assert ctx.launch_count() - before >= 1 + 1 + 4
+
+
+@pytest.mark.parametrize("nc,r,k,kind,n", [(32, 2, 2, 0, 16), (24, 1, 1, 1, 16), (20, 1, 1, 0, 8), (18, 1, 1, 1, 1),
+                                          (33, 2, 2, 0, 20)])
+def test_vanka_update_is_bitwise_deterministic(ctx, stmg, nc, r, k, kind, n):
+    """Colour-separated stages: no two concurrently running tiles add into the
+    same dof, so repeated smoother updates are bitwise identical."""
+    lvl = stmg.Level(ctx, nc, nc, r, k, 1.0 / 64, 1.0, 1.0, kind)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    res = torch.rand(n * lvl.size, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    u0 = torch.rand(n * lvl.size, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    outs = []
+    for _ in range(3):
+        u = u0.clone()
+        lvl.vanka_update(res, u, 0.8, n)
+        outs.append(u)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
