@@ -6,6 +6,7 @@
 #include "kernels.hpp"
 #include "setup.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -104,10 +105,41 @@ struct stmg_ctx
   int device = 0;
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
+  // copy streams + events of the pipelined host-buffer entry points
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> events;
   void
   count(int k = 1)
   {
     launches += k;
+  }
+  void
+  copy_streams()
+  {
+    if (!h2d)
+      check(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "stream");
+    if (!d2h)
+      check(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "stream");
+  }
+  cudaEvent_t
+  event(size_t i)
+  {
+    while (events.size() <= i)
+      {
+        cudaEvent_t e;
+        check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        events.push_back(e);
+      }
+    return events[i];
+  }
+  ~stmg_ctx()
+  {
+    for (cudaEvent_t e : events)
+      cudaEventDestroy(e);
+    if (h2d)
+      cudaStreamDestroy(h2d);
+    if (d2h)
+      cudaStreamDestroy(d2h);
   }
 };
 
@@ -1126,26 +1158,47 @@ stmg_vanka_update(stmg_level *L, const double *r, double *u, double omega, int n
   });
 }
 
+// Host-buffer entry points, pipelined over chunks of kHostChunk intervals:
+// the H2D copy of chunk c+1, the kernels of chunk c and the D2H copy of
+// chunk c-1 run concurrently (two copy engines + SMs), so one call costs
+// about max(H2D, D2H) bytes over PCIe instead of their sum.
+namespace
+{
+constexpr int kHostChunk = 8;
+}
+
 int
 stmg_vmult_host(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot)
 {
   return guarded([&] {
-    const size_t sz = static_cast<size_t>(L->spec.isz()) * n;
+    stmg_ctx &C = *L->ctx;
+    C.copy_streams();
+    const long long isz = L->spec.isz(), mv = L->spec.mv();
+    const size_t sz = static_cast<size_t>(isz) * n;
     L->host_in.resize(sz);
     L->host_out.resize(sz);
-    cudaStream_t st = L->ctx->stream;
-    check(cudaMemcpyAsync(L->host_in.p, x, sizeof(double) * sz, cudaMemcpyHostToDevice, st), "h2d");
     const double *prev = nullptr;
     if (x_prev_slot)
       {
-        L->host_prev.resize(L->spec.mv());
-        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * L->spec.mv(), cudaMemcpyHostToDevice, st),
-              "h2d");
+        L->host_prev.resize(mv);
+        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * mv, cudaMemcpyHostToDevice, C.h2d), "h2d");
         prev = L->host_prev.p;
       }
-    L->vmult(L->host_in.p, nullptr, L->host_out.p, n, prev, 1, 0);
-    check(cudaMemcpyAsync(y, L->host_out.p, sizeof(double) * sz, cudaMemcpyDeviceToHost, st), "d2h");
-    check(cudaStreamSynchronize(st), "sync");
+    const int nch = (n + kHostChunk - 1) / kHostChunk;
+    for (int c = 0; c < nch; ++c)
+      {
+        const int i0 = c * kHostChunk, m = std::min(kHostChunk, n - i0);
+        const size_t off = static_cast<size_t>(i0) * isz, len = static_cast<size_t>(m) * isz;
+        check(cudaMemcpyAsync(L->host_in.p + off, x + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
+        check(cudaEventRecord(C.event(2 * c), C.h2d), "event");
+        check(cudaStreamWaitEvent(C.stream, C.event(2 * c), 0), "wait");
+        const double *pc = c == 0 ? prev : L->host_in.p + off - isz + (L->spec.S() - 1) * mv;
+        L->vmult(L->host_in.p + off, nullptr, L->host_out.p + off, m, pc, 1, 0);
+        check(cudaEventRecord(C.event(2 * c + 1), C.stream), "event");
+        check(cudaStreamWaitEvent(C.d2h, C.event(2 * c + 1), 0), "wait");
+        check(cudaMemcpyAsync(y + off, L->host_out.p + off, sizeof(double) * len, cudaMemcpyDeviceToHost, C.d2h), "d2h");
+      }
+    check(cudaStreamSynchronize(C.d2h), "sync");
   });
 }
 
@@ -1154,23 +1207,46 @@ stmg_smooth_step_host(stmg_level *L, const double *b, double *u, double omega, i
                       int coupled)
 {
   return guarded([&] {
-    const size_t sz = static_cast<size_t>(L->spec.isz()) * n;
-    L->host_in.resize(sz);
-    L->host_out.resize(sz);
-    cudaStream_t st = L->ctx->stream;
-    check(cudaMemcpyAsync(L->host_in.p, b, sizeof(double) * sz, cudaMemcpyHostToDevice, st), "h2d");
-    check(cudaMemcpyAsync(L->host_out.p, u, sizeof(double) * sz, cudaMemcpyHostToDevice, st), "h2d");
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("smooth_step: omega must be in (0, 1]");
+    stmg_ctx &C = *L->ctx;
+    C.copy_streams();
+    const long long isz = L->spec.isz(), mv = L->spec.mv();
+    const size_t sz = static_cast<size_t>(isz) * n;
+    L->host_in.resize(sz);   // b
+    L->host_out.resize(sz);  // u
+    L->host_prev.resize(3 * mv); // [0]: x_prev_slot, [1], [2]: ring of pre-update chunk halos
     const double *prev = nullptr;
-    if (x_prev_slot)
+    if (x_prev_slot && coupled)
       {
-        L->host_prev.resize(L->spec.mv());
-        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * L->spec.mv(), cudaMemcpyHostToDevice, st),
-              "h2d");
+        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * mv, cudaMemcpyHostToDevice, C.h2d), "h2d");
         prev = L->host_prev.p;
       }
-    L->smooth_step(L->host_in.p, L->host_out.p, omega, n, prev, coupled ? 1 : 0, nullptr);
-    check(cudaMemcpyAsync(u, L->host_out.p, sizeof(double) * sz, cudaMemcpyDeviceToHost, st), "d2h");
-    check(cudaStreamSynchronize(st), "sync");
+    double *r = L->scratch(std::min(n, kHostChunk));
+    const int nch = (n + kHostChunk - 1) / kHostChunk;
+    for (int c = 0; c < nch; ++c)
+      {
+        const int i0 = c * kHostChunk, m = std::min(kHostChunk, n - i0);
+        const size_t off = static_cast<size_t>(i0) * isz, len = static_cast<size_t>(m) * isz;
+        check(cudaMemcpyAsync(L->host_in.p + off, b + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
+        check(cudaMemcpyAsync(L->host_out.p + off, u + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
+        check(cudaEventRecord(C.event(2 * c), C.h2d), "event");
+        check(cudaStreamWaitEvent(C.stream, C.event(2 * c), 0), "wait");
+        // residual with the pre-update halo of the previous chunk (Jacobi: the
+        // whole step sees the old u, as in VankaSmoother::smooth_step)
+        const double *halo = c == 0 ? prev : L->host_prev.p + (1 + ((c - 1) & 1)) * mv;
+        double *uc = L->host_out.p + off;
+        L->vmult(uc, L->host_in.p + off, r, m, coupled ? halo : nullptr, coupled ? 1 : 0, 1);
+        if (coupled && c + 1 < nch)
+          check(cudaMemcpyAsync(L->host_prev.p + (1 + (c & 1)) * mv, uc + (m - 1) * isz + (L->spec.S() - 1) * mv,
+                                sizeof(double) * mv, cudaMemcpyDeviceToDevice, C.stream),
+                "halo");
+        L->vanka(r, uc, m, omega);
+        check(cudaEventRecord(C.event(2 * c + 1), C.stream), "event");
+        check(cudaStreamWaitEvent(C.d2h, C.event(2 * c + 1), 0), "wait");
+        check(cudaMemcpyAsync(u + off, uc, sizeof(double) * len, cudaMemcpyDeviceToHost, C.d2h), "d2h");
+      }
+    check(cudaStreamSynchronize(C.d2h), "sync");
   });
 }
 

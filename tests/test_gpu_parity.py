@@ -231,3 +231,30 @@ def test_vanka_update_is_bitwise_deterministic(ctx, stmg, nc, r, k, kind, n):
         outs.append(u)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("nc,r,k,kind,n", [(16, 2, 2, 0, 20), (32, 1, 1, 1, 17), (8, 1, 1, 0, 3)])
+@pytest.mark.parametrize("with_prev", [False, True])
+def test_host_buffer_entry_points_match_device_path(ctx, stmg, oracle, nc, r, k, kind, n, with_prev):
+    """stmg_vmult_host / stmg_smooth_step_host (pipelined over 8-interval
+    chunks) equal the device-resident calls and the oracle."""
+    tau = 1.0 / 64
+    lvl = stmg.Level(ctx, nc, nc, r, k, tau, 1.0, 1.0, kind)
+    ref = oc.OracleLevel(nc, r, k, tau, 1.0, 1.0, kind)
+    x = oc.seeded(n * lvl.size, 71)
+    bb = oc.seeded(n * lvl.size, 72)
+    prev = oc.seeded(lvl.n_velocity, 73) if with_prev else None
+    # vmult through host buffers vs oracle
+    y = np.zeros_like(x)
+    lvl.vmult_host(np.ascontiguousarray(x), y, n, prev)
+    y_ref = ref.vmult_all(x, n, prev)
+    assert rel_max(y, y_ref) <= VMULT_TOL
+    # smoother step through host buffers vs the device path (bitwise up to
+    # the patch grouping of the chunked launch) and vs the oracle
+    u = x.copy()
+    lvl.smooth_step_host(bb, u, 0.8, n, prev, True)
+    ud = dev(x)
+    lvl.smooth_step(dev(bb), ud, 0.8, n, None if prev is None else dev(prev), coupled=True)
+    assert rel_max(u, host(ud)) <= 1e-13
+    u_ref = ref.smooth_step_all(bb, x.copy(), 0.8, n, prev)
+    assert rel_max(u, u_ref) <= SMOOTH_TOL
