@@ -7,6 +7,7 @@
 #include "setup.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -58,6 +59,10 @@ guarded(F &&f)
     }
 }
 
+/// Reallocations of any DevArray: captured CUDA graphs hold raw pointers and
+/// are re-captured when this changes.
+std::atomic<uint64_t> g_reallocs{0};
+
 /// Owning device array.
 template <class T>
 struct DevArray
@@ -88,6 +93,7 @@ struct DevArray
     n = 0;
     check(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)), "cudaMalloc");
     n = count;
+    g_reallocs.fetch_add(1, std::memory_order_relaxed);
   }
   void
   upload(const std::vector<T> &h)
@@ -362,7 +368,11 @@ build_level(stmg_level &L)
       for (int set = 0; set < 3; ++set)
         {
           const int B0 = 4;
-          const int B = set == 0 ? B0 : (set == 2 ? 2 * B0 : 32);
+          // time-marching set: 32 super-cells per block, fewer on small levels
+          // so that a pass still spreads over ~2 blocks per SM (latency)
+          const long long per_pass = std::max(1LL, static_cast<long long>(nsx) * nsy / 4);
+          const int B1 = static_cast<int>(std::min(32LL, std::max(1LL, per_pass / 296)));
+          const int B = set == 0 ? B0 : (set == 2 ? 2 * B0 : B1);
           stmg_level::SuperSet &ss = L.sup[set];
           std::vector<VankaBatch> items;
           std::vector<int> item_phase; // colour sub-phase (qy, qx) of each item
@@ -759,6 +769,96 @@ struct stmg_solver
     cycle(static_cast<int>(levels.size()) - 1, b_v, x_v);
   }
 
+  // ---- CUDA graph of the whole V-cycle for launch-bound (small) problems:
+  // replayed on fixed in/out buffers; captured on the second call with a
+  // given shape, after an uncaptured call has allocated every workspace.
+  cudaGraphExec_t vc_exec = nullptr;
+  int vc_nI = -1, vc_calls = 0;
+  bool vc_aao = false;
+  int64_t vc_launches = 0;
+  uint64_t vc_gen = 0;
+  cudaStream_t vc_stream = nullptr;
+  DevArray<double> vc_in, vc_out;
+  static constexpr long long kGraphMaxDofs = 2'000'000;
+
+  void
+  drop_graph()
+  {
+    if (vc_exec)
+      cudaGraphExecDestroy(vc_exec);
+    vc_exec = nullptr;
+    vc_calls = 0;
+  }
+
+  void
+  precondition(const double *b_v, double *x_v, int nI, bool aao)
+  {
+    const int top = static_cast<int>(levels.size()) - 1;
+    const long long n = fine().spec.isz() * nI;
+    if (n > kGraphMaxDofs || world() > 1)
+      {
+        cycle(top, b_v, x_v, nI, aao);
+        return;
+      }
+    vc_in.resize(n);
+    vc_out.resize(n);
+    if (nI != vc_nI || aao != vc_aao || (vc_exec && vc_gen != g_reallocs.load()))
+      {
+        drop_graph();
+        vc_nI = nI;
+        vc_aao = aao;
+      }
+    if (!vc_exec && vc_calls++ == 0)
+      {
+        cycle(top, b_v, x_v, nI, aao); // first call: allocates the workspaces
+        return;
+      }
+    if (!vc_exec)
+      {
+        const int64_t before = ctx->launches;
+        cudaGraph_t g = nullptr;
+        // the context stream may be the legacy default stream, which cannot
+        // be captured: record on a private stream (the replay goes to ctx->stream)
+        if (!vc_stream)
+          check(cudaStreamCreateWithFlags(&vc_stream, cudaStreamNonBlocking), "stream");
+        cudaStream_t user = ctx->stream;
+        check(cudaStreamSynchronize(user), "sync");
+        ctx->stream = vc_stream;
+        check(cudaStreamBeginCapture(vc_stream, cudaStreamCaptureModeRelaxed), "capture");
+        try
+          {
+            cycle(top, vc_in.p, vc_out.p, nI, aao);
+          }
+        catch (...)
+          {
+            cudaStreamEndCapture(vc_stream, &g);
+            ctx->stream = user;
+            if (g)
+              cudaGraphDestroy(g);
+            throw;
+          }
+        ctx->stream = user;
+        check(cudaStreamEndCapture(vc_stream, &g), "capture");
+        const cudaError_t e = cudaGraphInstantiate(&vc_exec, g, 0);
+        cudaGraphDestroy(g);
+        check(e, "graph instantiate");
+        vc_launches = ctx->launches - before;
+        ctx->launches = before;
+        vc_gen = g_reallocs.load();
+      }
+    check(cudaMemcpyAsync(vc_in.p, b_v, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    check(cudaGraphLaunch(vc_exec, ctx->stream), "graph launch");
+    ctx->count(static_cast<int>(vc_launches));
+    check(cudaMemcpyAsync(x_v, vc_out.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+  }
+
+  ~stmg_solver()
+  {
+    drop_graph();
+    if (vc_stream)
+      cudaStreamDestroy(vc_stream);
+  }
+
   double
   dot(const double *a, const double *b, long long n, int slot)
   {
@@ -818,7 +918,7 @@ struct stmg_solver
         for (; j < m; ++j)
           {
             DevArray<double> &zj = basis(Z, j, n);
-            cycle(top, V[j]->p, zj.p, nI, aao);
+            precondition(V[j]->p, zj.p, nI, aao);
             L.vmult(zj.p, nullptr, w.p, nI, aao ? halo(top, zj.p, nI) : nullptr, aao ? 1 : 0, 0);
             // modified Gram-Schmidt with device-resident coefficients
             for (int i = 0; i <= j; ++i)

@@ -367,10 +367,12 @@ launch_rs(const LevelConsts &P, const double *x, const double *b, double *y, int
 {
   const int strips = (P.nx + kStrip - 1) / kStrip;
   // Row segments: enough blocks to fill 148 SMs several times, >= 8 rows
-  // each so the recomputed halo row stays small.
+  // each so the recomputed halo row stays small -- down to 2 rows on small
+  // grids, where the march length (latency) matters more than the halo row.
   int segs = 1;
   const long long base_blocks = static_cast<long long>(strips) * n_intervals;
-  while (base_blocks * segs < 148 * 8 && P.ny / (segs * 2) >= 8)
+  const int min_rows = base_blocks * P.ny >= 148 * 64 ? 8 : 2;
+  while (base_blocks * segs < 148 * 8 && P.ny / (segs * 2) >= min_rows)
     segs *= 2;
   const int rows = (P.ny + segs - 1) / segs;
   dim3 grid(strips, (P.ny + rows - 1) / rows, n_intervals);
