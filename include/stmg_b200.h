@@ -109,10 +109,27 @@ int stmg_smooth_step(stmg_level *level, const double *b, double *u, double omega
 int stmg_vanka_update(stmg_level *level, const double *r, double *u, double omega, int n_intervals);
 
 /* Host-buffer variants of stmg_vmult / stmg_smooth_step: copy in, run,
- * copy out, synchronise (the end-to-end path a CPU caller binds). */
+ * copy out, synchronise (the end-to-end path a CPU caller binds). Pipelined
+ * over 8-interval chunks on separate H2D / D2H streams; pinned host memory
+ * lets the copies overlap the kernels. */
 int stmg_vmult_host(stmg_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);
 int stmg_smooth_step_host(stmg_level *level, const double *b, double *u, double omega, int n_intervals,
                           const double *x_prev_slot, int coupled);
+
+/* ------------------------------------------------------------ built-in problems
+ * The reference's manufactured problem (problems.cpp:13-62): its load vector
+ * via SpaceTimeBlockOperator::assemble_rhs (st_operator.cpp:423-467) and its
+ * space-time error norms via compute_errors (harness.cpp:72-183), on the
+ * device. F / X hold n_intervals consecutive intervals of this level, interval
+ * i covering [t_start + i tau, t_start + (i+1) tau]. The force uses the
+ * level's nu (the reference problem has nu = 0.1). assemble_rhs writes the
+ * velocity rows (pressure rows 0, constrained rows 0). compute_errors writes
+ * out[0..4] = e_v L2(L2), e_p L2(L2), e_v L2(H1-seminorm), ||div v|| L2(L2),
+ * e_v max over quadrature points (host array). r <= 4, k <= 4. */
+#define STMG_PROBLEM_MANUFACTURED 0
+int stmg_assemble_rhs(stmg_level *level, int problem, double t_start, double *F, int n_intervals);
+int stmg_compute_errors(stmg_level *level, int problem, double t_start, const double *X, int n_intervals,
+                        double *out);
 
 /* ------------------------------------------------------------ solver
  * build_setup + VCycle + gmres + time_march (harness.cpp:26-70,

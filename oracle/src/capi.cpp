@@ -462,4 +462,56 @@ oracle_time_march_seeded(void *hp, const double *F, double *X, int *iterations, 
   });
 }
 
+/// Manufactured problem (problems.cpp:13-62; its force uses nu = 0.1):
+/// assemble_rhs (st_operator.cpp:423-467) on the finest level at t_start.
+int
+oracle_assemble_rhs_manufactured(void *hp, double t_start, double *out)
+{
+  return guard([&] {
+    auto *h = static_cast<SolverHandle *>(hp);
+    const StokesProblem mp = manufactured_problem();
+    const BlockVector v = h->setup.levels.finest().op->assemble_rhs(mp.data.force, t_start);
+    std::memcpy(out, v.data.data(), sizeof(double) * v.data.size());
+  });
+}
+
+/// time_march (solver.cpp:204-325) of the manufactured problem: trajectory X
+/// (n_steps intervals) and GMRES iterations per step.
+int
+oracle_time_march_manufactured(void *hp, double *X, int *iterations)
+{
+  return guard([&] {
+    auto *h = static_cast<SolverHandle *>(hp);
+    const StokesProblem mp = manufactured_problem();
+    const TimeMarchResult res = time_march(h->setup.levels, mp.data, h->n_steps, h->config.mg, h->config.krylov, true);
+    const size_t sz = res.trajectory.empty() ? 0 : res.trajectory[0].data.size();
+    for (int n = 0; n < h->n_steps; ++n)
+      {
+        std::memcpy(X + n * sz, res.trajectory[n].data.data(), sizeof(double) * sz);
+        iterations[n] = res.steps[n].iterations;
+      }
+  });
+}
+
+/// compute_errors (harness.cpp:72-183) of a trajectory X (n_steps intervals)
+/// against the manufactured exact solution: out = e_v, e_p, e_h1, e_div, linf.
+int
+oracle_manufactured_errors(void *hp, const double *X, double *out)
+{
+  return guard([&] {
+    auto *h = static_cast<SolverHandle *>(hp);
+    const auto &op = *h->setup.levels.finest().op;
+    const size_t sz = op.make_vector().data.size();
+    TimeMarchResult m;
+    for (int n = 0; n < h->n_steps; ++n)
+      m.trajectory.push_back(view_copy(op, X + n * sz));
+    const ErrorReport e = compute_errors(h->setup, m, manufactured_problem().exact);
+    out[0] = e.e_v_l2;
+    out[1] = e.e_p_l2;
+    out[2] = e.e_v_h1;
+    out[3] = e.e_div;
+    out[4] = e.e_v_linf;
+  });
+}
+
 } // extern "C"

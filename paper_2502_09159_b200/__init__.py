@@ -21,6 +21,8 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "_build" / "libstmg_b200.so"
 HEADER_PATH = _PKG.parent / "include" / "stmg_b200.h"
 
+PROBLEM_MANUFACTURED = 0
+
 SMOOTHER_NONE = -1
 SMOOTHER_CELL = 0
 SMOOTHER_VERTEX_STAR = 1
@@ -75,6 +77,8 @@ _SIGNATURES = {
                    _c_int),
     "stmg_time_march": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_time_march_host": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
+    "stmg_assemble_rhs": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int], _c_int),
+    "stmg_compute_errors": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int, ctypes.POINTER(_c_double)], _c_int),
     "stmg_solver_set_comm": ([_c_void_p, _c_void_p], _c_int),
     "stmg_vcycle_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
     "stmg_solve_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, ctypes.POINTER(_c_int),
@@ -239,6 +243,18 @@ class Level:
         return u
 
     # -- host-buffer (end-to-end) variants
+    def assemble_rhs(self, F, t_start: float = 0.0, n_intervals: int = 1, problem: int = PROBLEM_MANUFACTURED):
+        """SpaceTimeBlockOperator::assemble_rhs of a built-in force for n_intervals intervals from t_start."""
+        _check(load_library().stmg_assemble_rhs(self._h, problem, t_start, _ptr(F), n_intervals))
+        return F
+
+    def compute_errors(self, X, t_start: float = 0.0, n_intervals: int = 1,
+                       problem: int = PROBLEM_MANUFACTURED) -> dict:
+        """compute_errors (harness.cpp:72-183) of a trajectory against the built-in exact solution."""
+        out = (ctypes.c_double * 5)()
+        _check(load_library().stmg_compute_errors(self._h, problem, t_start, _ptr(X), n_intervals, out))
+        return dict(e_v_l2=out[0], e_p_l2=out[1], e_v_h1=out[2], e_div=out[3], e_v_linf=out[4])
+
     def vmult_host(self, x, y, n_intervals: int = 1, x_prev_slot=None):
         _check(load_library().stmg_vmult_host(self._h, _hptr(x), _hptr(y), n_intervals, _hptr(x_prev_slot)))
         return y
@@ -378,4 +394,4 @@ def exported_symbols() -> Sequence[str]:
 
 
 __all__ = ["Context", "Level", "Solver", "StmgError", "load_library", "plan_levels", "patch_info",
-           "exported_symbols", "SMOOTHER_CELL", "SMOOTHER_VERTEX_STAR", "SMOOTHER_NONE"]
+           "exported_symbols", "SMOOTHER_CELL", "SMOOTHER_VERTEX_STAR", "SMOOTHER_NONE", "PROBLEM_MANUFACTURED"]

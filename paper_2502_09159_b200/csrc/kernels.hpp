@@ -94,6 +94,12 @@ cudaError_t launch_coarse_solve(const double *inv, const long long *pinned, int 
 // B holds n_all intervals; intervals [n_begin, n_begin + n_own) go to X.
 cudaError_t launch_coarse_forward(const double *G, const double *H, int n, int mv, long long v_off, const double *B,
                                   int n_all, int n_begin, int n_own, double *X, cudaStream_t st);
+// Built-in problems (problems.cu): manufactured force load vector and error norms.
+cudaError_t launch_assemble_manufactured(const DevGeom &G, int r, const ProblemTables &T, double nu, double t_start,
+                                         double tau, double *F, int n_intervals, cudaStream_t st);
+long long errors_partials(const DevGeom &G, int n_intervals);
+cudaError_t launch_errors_manufactured(const DevGeom &G, int r, const ProblemTables &T, double t_start, double tau,
+                                       const double *X, int n_intervals, double *part, double *out, cudaStream_t st);
 int dot_partials();
 cudaError_t launch_dot(const double *x, const double *y, long long n, double *part, double *out, cudaStream_t st);
 cudaError_t launch_axpy(long long n, double alpha, const double *alpha_dev, double sign, const double *x, double *y,

@@ -69,6 +69,21 @@ struct LevelConsts
   double lv[kMaxS];         // left_values(a)
 };
 
+/// 1D tables of the built-in problem kernels (problems.cu), r <= 4, k <= 4:
+/// assemble_rhs quadrature (st_operator.cpp:423-467) and compute_errors
+/// quadrature (harness.cpp:72-183). Passed by value as a kernel parameter.
+struct ProblemTables
+{
+  // assemble: Gauss(r+2) points/weights, GLL Lagrange basis phi(q, i)
+  double ax[8], aw[8], aphi[8 * 8];
+  // temporal right-Radau nodes / weights (time_basis.cpp:8-59)
+  double tn[6], tw[6];
+  // errors: Gauss(r+3) in space, phi / dphi(q, i), Legendre P_a(x_q)
+  double ex[9], ew[9], ephi[9 * 8], edphi[9 * 8], eleg[9 * 6];
+  // errors: Gauss(k+2) in time, Radau-node Lagrange values tval(q, a)
+  double tq[8], tqw[8], tval[8 * 6];
+};
+
 /// Degree-major P_r^disc mode list (pdisc.cpp:41-55): mode m has Legendre
 /// degrees (ax(m), ay(m)).
 __host__ __device__ constexpr int

@@ -1023,6 +1023,53 @@ coarse_inverse(const LevelSpec &L, std::vector<long long> &pinned)
   return A;
 }
 
+// ================================================================ problem tables
+ProblemTables
+problem_tables(const LevelSpec &L)
+{
+  if (L.r > 4 || L.k > 4)
+    throw std::invalid_argument("problem_tables: r and k must be <= 4");
+  ProblemTables T{};
+  const int n1 = L.n1();
+  const std::vector<double> gll = gauss_lobatto(n1);
+  const Rule1D ga = gauss_legendre(L.r + 2); // st_operator.cpp:167
+  for (int q = 0; q < L.r + 2; ++q)
+    {
+      T.ax[q] = ga.x[q];
+      T.aw[q] = ga.w[q];
+      for (int i = 0; i < n1; ++i)
+        T.aphi[q * n1 + i] = lagrange(gll, i, ga.x[q]);
+    }
+  const TimeTables tt = time_tables(L.k, L.tau);
+  for (int a = 0; a <= L.k; ++a)
+    {
+      T.tn[a] = tt.nodes[a];
+      T.tw[a] = tt.weights[a];
+    }
+  const Rule1D ge = gauss_legendre(L.r + 3); // harness.cpp:85 (CellKernels eval(vs, ps, r + 3))
+  for (int q = 0; q < L.r + 3; ++q)
+    {
+      T.ex[q] = ge.x[q];
+      T.ew[q] = ge.w[q];
+      for (int i = 0; i < n1; ++i)
+        {
+          T.ephi[q * n1 + i] = lagrange(gll, i, ge.x[q]);
+          T.edphi[q * n1 + i] = lagrange_deriv(gll, i, ge.x[q]);
+        }
+      for (int a = 0; a <= L.r; ++a)
+        T.eleg[q * (L.r + 1) + a] = legendre(a, ge.x[q]);
+    }
+  const Rule1D gt = gauss_legendre(L.k + 2); // harness.cpp:81
+  for (int q = 0; q < L.k + 2; ++q)
+    {
+      T.tq[q] = gt.x[q];
+      T.tqw[q] = gt.w[q];
+      for (int a = 0; a <= L.k; ++a)
+        T.tval[q * (L.k + 1) + a] = lagrange(tt.nodes, a, gt.x[q]);
+    }
+  return T;
+}
+
 // ================================================================ hierarchy plan
 std::vector<LevelPlan>
 plan_levels(const HierarchyConfig &cfg, int *n_steps_out)

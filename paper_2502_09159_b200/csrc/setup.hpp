@@ -169,6 +169,9 @@ TransferTables build_transfer(const LevelSpec &coarse, const LevelSpec &fine, Tr
 /// of every slot pinned (solver.cpp:10-41), inverted. Row-major.
 std::vector<double> coarse_inverse(const LevelSpec &L, std::vector<long long> &pinned);
 
+/// Quadrature and basis tables of the built-in problem kernels (problems.cu).
+ProblemTables problem_tables(const LevelSpec &L);
+
 // ---------------------------------------------------------------- hierarchy
 struct HierarchyConfig
 {

@@ -188,7 +188,20 @@ struct stmg_level
   int n_classes = 0;
   std::uint64_t total_matrix_elements = 0;
   // scratch
-  DevArray<double> work, zeros, host_in, host_out, host_prev, proj;
+  DevArray<double> work, zeros, host_in, host_out, host_prev, proj, err_part, err_out;
+  // built-in problem tables (problems.cu), built on first use
+  ProblemTables ptab{};
+  bool ptab_ready = false;
+  const ProblemTables &
+  problem_tab()
+  {
+    if (!ptab_ready)
+      {
+        ptab = problem_tables(spec);
+        ptab_ready = true;
+      }
+    return ptab;
+  }
 
   /// u_p <- u_p - mean per slot (PressureSpace::project_mean_zero)
   void
@@ -1475,6 +1488,40 @@ int
 stmg_gmres(stmg_solver *s, const double *b, double *x, int *iterations, double *history, int history_cap)
 {
   return guarded([&] { s->gmres(b, x, iterations, history, history_cap); });
+}
+
+int
+stmg_assemble_rhs(stmg_level *L, int problem, double t_start, double *F, int n)
+{
+  return guarded([&] {
+    if (problem != STMG_PROBLEM_MANUFACTURED)
+      throw std::invalid_argument("stmg_assemble_rhs: unknown problem");
+    if (n < 0 || !F)
+      throw std::invalid_argument("stmg_assemble_rhs: invalid arguments");
+    check(launch_assemble_manufactured(L->geom, L->spec.r, L->problem_tab(), L->spec.nu, t_start, L->spec.tau, F, n,
+                                       L->ctx->stream),
+          "assemble_rhs");
+    L->ctx->count(5);
+  });
+}
+
+int
+stmg_compute_errors(stmg_level *L, int problem, double t_start, const double *X, int n, double *out)
+{
+  return guarded([&] {
+    if (problem != STMG_PROBLEM_MANUFACTURED)
+      throw std::invalid_argument("stmg_compute_errors: unknown problem");
+    if (n < 1 || !X || !out)
+      throw std::invalid_argument("stmg_compute_errors: invalid arguments");
+    L->err_part.resize(errors_partials(L->geom, n));
+    L->err_out.resize(5);
+    check(launch_errors_manufactured(L->geom, L->spec.r, L->problem_tab(), t_start, L->spec.tau, X, n,
+                                     L->err_part.p, L->err_out.p, L->ctx->stream),
+          "compute_errors");
+    L->ctx->count(2);
+    check(cudaMemcpyAsync(out, L->err_out.p, sizeof(double) * 5, cudaMemcpyDeviceToHost, L->ctx->stream), "d2h");
+    check(cudaStreamSynchronize(L->ctx->stream), "sync");
+  });
 }
 
 int

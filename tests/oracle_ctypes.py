@@ -63,6 +63,9 @@ def lib():
         L.oracle_vcycle.argtypes = [_P, _D, _D]
         L.oracle_gmres.argtypes = [_P, _D, _D, ctypes.POINTER(ctypes.c_int), _D, ctypes.c_int]
         L.oracle_time_march_seeded.argtypes = [_P, _D, _D, ctypes.POINTER(ctypes.c_int), _D]
+        L.oracle_assemble_rhs_manufactured.argtypes = [_P, ctypes.c_double, _D]
+        L.oracle_time_march_manufactured.argtypes = [_P, _D, ctypes.POINTER(ctypes.c_int)]
+        L.oracle_manufactured_errors.argtypes = [_P, _D, _D]
     return _lib
 
 
@@ -181,6 +184,22 @@ class OracleSolver:
         thr = np.zeros(1)
         _chk(lib().oracle_time_march_seeded(self.h, _d(F), _d(X), it, _d(thr)))
         return X, list(it), float(thr[0])
+
+    def assemble_rhs_manufactured(self, t_start):
+        out = np.zeros(self.size)
+        _chk(lib().oracle_assemble_rhs_manufactured(self.h, t_start, _d(out)))
+        return out
+
+    def time_march_manufactured(self):
+        X = np.zeros(self.n_steps * self.size)
+        it = (ctypes.c_int * self.n_steps)()
+        _chk(lib().oracle_time_march_manufactured(self.h, _d(X), it))
+        return X, list(it)
+
+    def manufactured_errors(self, X):
+        out = np.zeros(5)
+        _chk(lib().oracle_manufactured_errors(self.h, _d(np.ascontiguousarray(X)), _d(out)))
+        return out
 
     def __del__(self):
         if getattr(self, "h", None):

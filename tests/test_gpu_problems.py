@@ -1,0 +1,96 @@
+"""GPU tier: the built-in manufactured problem (problems.cpp:13-62) on the
+device -- assemble_rhs (st_operator.cpp:423-467) and compute_errors
+(harness.cpp:72-183) against the oracle, and acceptance Table 1
+(tests/acceptance.cpp:383-420) end to end on the GPU:
+assemble -> time_march -> errors."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_ctypes as oc
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("c,r,k", [(2, 1, 1), (2, 2, 2), (1, 4, 4), (3, 3, 1)])
+def test_assemble_rhs_matches_oracle(ctx, stmg, c, r, k):
+    sol = stmg.Solver(ctx, c, r, k, nu=0.1)
+    ref = oc.OracleSolver(c, r, k, nu=0.1)
+    lv = sol.finest
+    tau = 1.0 / sol.n_steps
+    n = 3
+    F = torch.zeros(n * lv.size, dtype=torch.float64, device="cuda")
+    lv.assemble_rhs(F, 0.25, n)
+    Fh = host(F)
+    for i in range(n):
+        Fr = ref.assemble_rhs_manufactured(0.25 + i * tau)
+        got = Fh[i * lv.size:(i + 1) * lv.size]
+        assert np.abs(got - Fr).max() <= 1e-12 * np.abs(Fr).max(), i
+
+
+@pytest.mark.parametrize("c,r,k", [(2, 1, 1), (2, 2, 2), (1, 4, 4)])
+def test_compute_errors_match_oracle(ctx, stmg, c, r, k):
+    sol = stmg.Solver(ctx, c, r, k, nu=0.1)
+    ref = oc.OracleSolver(c, r, k, nu=0.1)
+    lv = sol.finest
+    X = oc.seeded(sol.n_steps * lv.size, 5) * 0.1
+    got = lv.compute_errors(dev(X), 0.0, sol.n_steps)
+    want = ref.manufactured_errors(X)
+    for key, w in zip(["e_v_l2", "e_p_l2", "e_v_h1", "e_div", "e_v_linf"], want):
+        assert abs(got[key] - w) <= 1e-11 * abs(w), (key, got[key], w)
+
+
+def _gpu_manufactured_run(stmg, ctx, c, r):
+    sol = stmg.Solver(ctx, c, r, -1, nu=0.1, gamma=1.0, rtol=1e-10, max_iterations=400)
+    lv = sol.finest
+    n = sol.n_steps
+    F = torch.zeros(n * lv.size, dtype=torch.float64, device="cuda")
+    lv.assemble_rhs(F, 0.0, n)
+    X = torch.zeros_like(F)
+    iters = sol.time_march(F, X)
+    return sol, X, iters, lv.compute_errors(X, 0.0, n)
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_manufactured_solve_matches_oracle(ctx, stmg, c):
+    """Seeded-free end-to-end check: the GPU trajectory and its error norms
+    equal the oracle's time_march of the manufactured problem (r = 2)."""
+    sol, X, iters, err = _gpu_manufactured_run(stmg, ctx, c, 2)
+    ref = oc.OracleSolver(c, 2, -1, nu=0.1, gamma=1.0, rtol=1e-10, maxit=400)
+    Xr, itr = ref.time_march_manufactured()
+    assert all(abs(a - b) <= 1 for a, b in zip(iters, itr)), (iters, itr)
+    assert np.linalg.norm(host(X) - Xr) <= 1e-8 * np.linalg.norm(Xr)
+    er = ref.manufactured_errors(Xr)
+    assert abs(err["e_v_l2"] - er[0]) <= 1e-6 * er[0]
+    assert abs(err["e_p_l2"] - er[1]) <= 1e-6 * er[1]
+
+
+def test_table1_r4_on_gpu(ctx, stmg):
+    """PAPER.md Table 1 (r = 4, c = 1..3): velocity and pressure L2(L2)
+    errors within a factor 2 of the published values and velocity EOC within
+    +-0.3 (acceptance.cpp:383-420), computed entirely on the GPU."""
+    ref_v = [1.00279e-04, 2.32706e-06, 3.98114e-08]
+    ref_p = [1.14907e-03, 1.11534e-04, 3.58645e-06]
+    ref_eoc = [5.43, 5.87]
+    ev, ep = [], []
+    for c in (1, 2, 3):
+        _, _, iters, err = _gpu_manufactured_run(stmg, ctx, c, 4)
+        ev.append(err["e_v_l2"])
+        ep.append(err["e_p_l2"])
+        print(f"Table 1 GPU c={c}: e_v={err['e_v_l2']:.4e} e_p={err['e_p_l2']:.4e} "
+              f"avg iters={sum(iters) / len(iters):.2f}")
+        assert 0.5 < ev[-1] / ref_v[c - 1] < 2.0
+        assert 0.5 < ep[-1] / ref_p[c - 1] < 2.0
+    for i in (1, 2):
+        assert abs(math.log2(ev[i - 1] / ev[i]) - ref_eoc[i - 1]) <= 0.3
