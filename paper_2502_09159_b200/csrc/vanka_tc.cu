@@ -30,9 +30,8 @@ constexpr int kTThreads = 512;
 constexpr int kTRows = 128;
 constexpr int kTCols = 32;
 // Diagnostic build switches (wrong results, timing only; DESIGN.md §3.2 cost
-// breakdown): STMG_VT_NO_GATHER, STMG_VT_NO_SCATTER. STMG_VT_ROWMAJOR selects
-// the previous row-major R tile layout.
-#ifndef STMG_VT_ROWMAJOR
+// breakdown): STMG_VT_NO_GATHER, STMG_VT_NO_SCATTER.
+//
 // R tiles column-major in shared memory: element (row k, column n) at
 // n * kTLd + k. The gather walks rows with the lanes of a warp (rows of a
 // patch come in contiguous runs of 4-6 dofs: few sectors per instruction);
@@ -40,10 +39,6 @@ constexpr int kTCols = 32;
 // (k = lane % 4, n = lane / 4) conflict-free.
 constexpr int kTLd = kTRows + 4;
 constexpr int kTSlot = kTCols * kTLd;
-#else
-constexpr int kTLd = 36; // row-major, == 4 mod 16 doubles: conflict-free B-fragment loads
-constexpr int kTSlot = kTRows * kTLd;
-#endif
 #ifndef STMG_VANKA_STAGE
 #define STMG_VANKA_STAGE 1
 #endif
@@ -109,18 +104,11 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
     s_tile[e] = tiles[t0 + e];
   __syncthreads();
 
-#ifndef STMG_VT_ROWMAJOR
   // gather: warp w fills columns w and w + 16, lane l rows l + 32 q
   constexpr int QN = kTRows / 32;
   constexpr int CN = kTCols / (kTThreads / 32);
   const int lane_g = tid & 31, warp_g = tid >> 5;
   auto row_of = [&](int q) { return lane_g + 32 * q; };
-#else
-  // gather rows of this thread: row = tid/32 + 16 q (fixed across tiles)
-  constexpr int QN = kTRows * kTCols / kTThreads;
-  const int col_g = tid & 31;
-  auto row_of = [&](int q) { return (tid >> 5) + q * (kTThreads / kTCols); };
-#endif
   int cls_issue = -1, nt_issue = 0, nvel_issue = 0;
   long long relq[QN];
 
@@ -142,7 +130,6 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
             cls_issue = tl.cls;
           }
         double *slot = ring + s * kTSlot;
-#ifndef STMG_VT_ROWMAJOR
 #pragma unroll
         for (int cc = 0; cc < CN; ++cc)
           {
@@ -165,25 +152,6 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
                   *dst = 0.0;
               }
           }
-#else
-        const int ci = lt * kTCols + col_g;
-        const bool colok = col_g < tl.ncols && n0 + s_coln[ci] < n_intervals;
-        const long long cv = base0 + s_colv[ci], cp = base0 + s_colp[ci];
-#pragma unroll
-        for (int q = 0; q < QN; ++q)
-          {
-            const int row = row_of(q);
-            double *dst = slot + row * kTLd + col_g;
-#ifdef STMG_VT_NO_GATHER
-            if (false)
-#else
-            if (colok && row < nt_issue)
-#endif
-              cp_async8(dst, r + (row < nvel_issue ? cv : cp) + relq[q]);
-            else
-              *dst = 0.0;
-          }
-#endif
       }
   };
   // gather of stage g (tiles kTStage*g ..) into its half of the ring
@@ -213,11 +181,7 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
     cp_async_wait0();
     __syncthreads();
     issue_stage(g + 1);
-#ifdef STMG_VANKA_UNROLL_H
-#pragma unroll
-#else
 #pragma unroll 1
-#endif
     for (int h = 0; h < kTStage; ++h)
     {
       const int lt = kTStage * g + h;
@@ -246,23 +210,14 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
 #pragma unroll
       for (int ct = 0; ct < kTCols / 8; ++ct)
         acc[ct][0] = acc[ct][1] = 0.0;
-#ifndef STMG_VT_ROWMAJOR
       const double *bbase = ring + ((g & 1) * kTStage + h) * kTSlot + (lane >> 2) * kTLd + (lane & 3);
-#else
-      const double *bbase = ring + ((g & 1) * kTStage + h) * kTSlot + (lane & 3) * kTLd + (lane >> 2);
-#endif
       if (8 * warp < nt_loaded) // warps past n_T only join the barriers
         {
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk)
             {
-#ifndef STMG_VT_ROWMAJOR
               const double *brow = bbase + 4 * kk;
               constexpr int kNStep = 8 * kTLd; // next 8 columns
-#else
-              const double *brow = bbase + 4 * kk * kTLd;
-              constexpr int kNStep = 8;
-#endif
 #pragma unroll
               for (int ct = 0; ct < kTCols / 8; ++ct)
                 dmma(acc[ct], afr[kk], brow[kNStep * ct]);
