@@ -226,6 +226,42 @@ def solve_legs(stmg, ctx, torch):
     return out
 
 
+def c4_step_leg(stmg, ctx, torch, n_int=8, reps=5):
+    """C4 discretisation (1024^2, Q2/P1, DG(1), tau = 1/64, vertex-star Vanka)
+    over one 8-interval slab (1.85e8 space-time dofs): all-at-once vmult and
+    one smoother step (residual + Vanka update), CUDA-event timed."""
+    lvl = stmg.Level(ctx, 1024, 1024, 1, 1, 1.0 / 64, 1.0, 1.0, stmg.SMOOTHER_VERTEX_STAR)
+    n = n_int * lvl.size
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    u = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    y, res = torch.empty_like(x), torch.empty_like(x)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    tv, tr, tk = [], [], []
+    for it in range(reps + 2):
+        ev[0].record()
+        lvl.vmult(x, y, n_int)
+        ev[1].record()
+        lvl.residual(b, u, res, n_int, None, coupled=True)
+        ev[2].record()
+        lvl.vanka_update(res, u, 0.8, n_int)
+        ev[3].record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            tv.append(ev[0].elapsed_time(ev[1]))
+            tr.append(ev[1].elapsed_time(ev[2]))
+            tk.append(ev[2].elapsed_time(ev[3]))
+    vm, rs, vk = (statistics.mean(t) for t in (tv, tr, tk))
+    flops_vk = 2.0 * lvl.total_matrix_elements * n_int
+    out = {"dofs": n, "vmult_ms": vm, "residual_ms": rs, "vanka_update_ms": vk,
+           "vmult_dofs_per_s": n / (vm * 1e-3), "smoother_step_dofs_per_s": n / ((rs + vk) * 1e-3),
+           "vanka_TFLOP/s": flops_vk / vk / 1e9, "smoother": "vertex_star (n_T = 124)"}
+    del lvl, x, b, u, y, res
+    return out
+
+
 def slab_solve_leg(stmg, ctx, torch, dist, world, rank, n_local=8):
     """All-at-once FGMRES + hp-STMG V(2,2) solve of the C4 discretisation
     (1024^2, Q2/P1, DG(1), tau = 1/64, vertex-star Vanka) partitioned by time
@@ -447,6 +483,7 @@ def main():
     if not args.no_solve:
         line["solve"] = solve_legs(stmg, ctx, torch)
         line["solve"]["C4_all_at_once"] = slab
+        line["C4_step"] = c4_step_leg(stmg, ctx, torch)
     if not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_quick()

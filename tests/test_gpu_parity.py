@@ -258,3 +258,34 @@ def test_host_buffer_entry_points_match_device_path(ctx, stmg, oracle, nc, r, k,
     assert rel_max(u, host(ud)) <= 1e-13
     u_ref = ref.smooth_step_all(bb, x.copy(), 0.8, n, prev)
     assert rel_max(u, u_ref) <= SMOOTH_TOL
+
+
+def test_error_codes_mirror_reference_exceptions(ctx, stmg):
+    """Status codes at the C ABI follow the reference's exceptions:
+    invalid_argument -> STMG_EINVAL (1), runtime_error -> STMG_ERUNTIME (2)."""
+    lvl = stmg.Level(ctx, 4, 4, 1, 1, 0.25, 0.1, 1.0, stmg.SMOOTHER_CELL)
+    x = torch.zeros(lvl.size, dtype=torch.float64, device="cuda")
+    for bad in (0.0, -0.5, 1.5):  # vanka.cpp:223-224
+        with pytest.raises(stmg.StmgError) as ei:
+            lvl.smooth_step(x, x.clone(), bad)
+        assert ei.value.code == 1
+    for r, k in [(0, 1), (5, 1), (1, 5), (1, -1)]:  # degree range
+        with pytest.raises(stmg.StmgError) as ei:
+            stmg.Level(ctx, 4, 4, r, k, 0.25, 0.1, 1.0, stmg.SMOOTHER_CELL)
+        assert ei.value.code == 1
+    with pytest.raises(stmg.StmgError) as ei:
+        lvl.assemble_rhs(x, 0.0, 1, problem=7)
+    assert ei.value.code == 1
+    # zero intervals: a no-op, not an error
+    y = torch.full_like(x, 3.0)
+    lvl.vmult(x, y, 0)
+    lvl.vanka_update(x, y, 0.8, 0)
+    torch.cuda.synchronize()
+    assert bool((y == 3.0).all())
+    # GMRES non-convergence -> runtime_error (solver.cpp:275)
+    sol = stmg.Solver(ctx, 2, 1, 1, nu=0.1, rtol=1e-14, atol=0.0, max_iterations=1)
+    b = torch.from_numpy(oc.make_consistent(oc.seeded(sol.finest.size, 3), sol.finest.n_slots, sol.finest.n_scalar,
+                                            sol.finest.grid_x, sol.finest.n_pressure, 16, 3)).cuda()
+    with pytest.raises(stmg.StmgError) as ei:
+        sol.gmres(b, torch.zeros_like(b))
+    assert ei.value.code == 2
