@@ -375,9 +375,9 @@ build_level(stmg_level &L)
         for (const auto &e : col)
           cls_of[static_cast<size_t>(e.ay) * nax + e.ax] = e.cls;
       const int nsx = (nax + P - 1) / P, nsy = (nay + P - 1) / P;
-      // B super-cells per block: few for many intervals (columns = B x 16
-      // intervals), twice as many for 8-interval slabs, 32 for time marching
-      // (one interval per block).
+      // B super-cells (one contiguous strip) per block: few for many
+      // intervals (columns = B x 16 intervals), twice as many for 8-interval
+      // slabs, up to 32 for time marching (one interval per block).
       for (int set = 0; set < 3; ++set)
         {
           const int B0 = 4;
@@ -395,20 +395,22 @@ build_level(stmg_level &L)
           for (int sc = 0; sc < 4; ++sc)
             {
               std::vector<int> ptr{static_cast<int>(items.size())};
+              // A block owns one contiguous strip of B super-cells (P*B anchors
+              // wide, P high); strips are 2x2-coloured over the 4 passes, so
+              // same-pass strips are a full strip apart (no shared dof) and
+              // each block reads contiguous node runs (DRAM bursts fully used).
+              const int nwx = (nax + P * B - 1) / (P * B);
               for (int SY = sc / 2; SY < nsy; SY += 2)
                 {
-                  std::vector<int> sxs;
-                  for (int SX = sc % 2; SX < nsx; SX += 2)
-                    sxs.push_back(SX);
-                  for (size_t c0 = 0; c0 < sxs.size(); c0 += B)
+                  for (int WX = sc % 2; WX < nwx; WX += 2)
                     {
                       for (int qy = 0; qy < P; ++qy)
                         for (int qx = 0; qx < P; ++qx)
                           {
                             std::vector<std::pair<int, std::pair<int, int>>> anchors; // (cls, (ax, ay))
-                            for (size_t c1 = c0; c1 < std::min(sxs.size(), c0 + B); ++c1)
+                            for (int w = 0; w < B; ++w)
                               {
-                                const int ax = P * sxs[c1] + qx, ay = P * SY + qy;
+                                const int ax = P * B * WX + P * w + qx, ay = P * SY + qy;
                                 if (ax < nax && ay < nay)
                                   anchors.push_back({cls_of[static_cast<size_t>(ay) * nax + ax], {ax, ay}});
                               }
