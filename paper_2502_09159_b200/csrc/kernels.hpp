@@ -54,13 +54,19 @@ struct VankaBatch
 
 /// One tile of the pipelined tensor-core Vanka: <= 32 columns (patch,
 /// interval) of one class; column data in parallel arrays at tile*32 + c.
+/// <= 32 columns (patch, interval) of one class: column j is entry c0 + j
+/// of the patch-major / interval-minor enumeration of the item whose patches
+/// start at pfirst in the velocity / pressure anchor arrays (ncols == 0:
+/// stage padding).
 struct VankaTile
 {
   int cls;
   int ncols;
+  int pfirst;
+  int c0;
 };
-cudaError_t launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *colv,
-                            const long long *colp, const int *coln, const int *tile_ptr, int n_blocks, int ng_full,
+cudaError_t launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *va,
+                            const long long *pa, const int *tile_ptr, int n_blocks, int ng_full,
                             int max_nt, const double *r, double *u, long long isz, int n_intervals, double omega,
                             cudaStream_t stream);
 int vanka_tc_cols();

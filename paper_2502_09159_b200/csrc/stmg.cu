@@ -179,8 +179,6 @@ struct stmg_level
     std::vector<DevArray<int>> tile_ptr;
     std::vector<int> tile_blocks;
     DevArray<VankaTile> tiles;
-    DevArray<long long> colv, colp;
-    DevArray<int> coln;
   };
   bool super = false;
   SuperSet sup[3]; // intervals per block: [0] 16, [2] 8 (slabs), [1] 1 (time marching)
@@ -234,7 +232,7 @@ struct stmg_level
             for (size_t sc = 0; sc < ss.tile_ptr.size(); ++sc)
               if (ss.tile_blocks[sc] > 0)
                 {
-                  check(launch_vanka_tc(classes.p, ss.tiles.p, ss.colv.p, ss.colp.p, ss.coln.p, ss.tile_ptr[sc].p,
+                  check(launch_vanka_tc(classes.p, ss.tiles.p, ss.va.p, ss.pa.p, ss.tile_ptr[sc].p,
                                         ss.tile_blocks[sc], ss.ng_full, max_nt, r, u, spec.isz(), n, omega,
                                         ctx->stream),
                         "vanka_tc");
@@ -392,6 +390,7 @@ build_level(stmg_level &L)
           std::vector<long long> sva, spa;
           ss.pass_ptr.resize(4);
           ss.pass_blocks.assign(4, 0);
+          std::vector<std::vector<int>> host_ptr(4);
           for (int sc = 0; sc < 4; ++sc)
             {
               std::vector<int> ptr{static_cast<int>(items.size())};
@@ -438,6 +437,7 @@ build_level(stmg_level &L)
                 }
               ss.pass_blocks[sc] = static_cast<int>(ptr.size()) - 1;
               ss.pass_ptr[sc].upload(ptr);
+              host_ptr[sc] = std::move(ptr);
             }
           ss.items.upload(items);
           ss.va.upload(sva);
@@ -449,14 +449,11 @@ build_level(stmg_level &L)
           const int tc = vanka_tc_cols();
           bool tc_ok = true;
           std::vector<VankaTile> tiles;
-          std::vector<long long> colv, colp;
-          std::vector<int> coln;
           ss.tile_ptr.resize(4);
           ss.tile_blocks.assign(4, 0);
           for (int sc = 0; sc < 4; ++sc)
             {
-              std::vector<int> hptr(ss.pass_blocks[sc] + 1);
-              cudaMemcpy(hptr.data(), ss.pass_ptr[sc].p, sizeof(int) * hptr.size(), cudaMemcpyDeviceToHost);
+              const std::vector<int> &hptr = host_ptr[sc];
               std::vector<int> tptr{static_cast<int>(tiles.size())};
               const int stage = vanka_tc_stage();
               for (int blk = 0; blk < ss.pass_blocks[sc]; ++blk)
@@ -465,15 +462,7 @@ build_level(stmg_level &L)
                   // close a colour sub-phase: pad with empty tiles to whole stages
                   const auto pad = [&](int cls) {
                     while ((static_cast<int>(tiles.size()) - phase_first) % stage != 0)
-                      {
-                        tiles.push_back(VankaTile{cls, 0});
-                        for (int c = 0; c < tc; ++c)
-                          {
-                            colv.push_back(0);
-                            colp.push_back(0);
-                            coln.push_back(1 << 30);
-                          }
-                      }
+                      tiles.push_back(VankaTile{cls, 0, 0, 0});
                     phase_first = static_cast<int>(tiles.size());
                   };
                   for (int it = hptr[blk]; it < hptr[blk + 1]; ++it)
@@ -483,27 +472,7 @@ build_level(stmg_level &L)
                       const VankaBatch &item = items[it];
                       const int ncols = item.count * ss.ng_full;
                       for (int c0 = 0; c0 < ncols; c0 += tc)
-                        {
-                          VankaTile tl{item.cls, std::min(tc, ncols - c0)};
-                          for (int c = 0; c < tc; ++c)
-                            {
-                              const int j = c0 + c;
-                              if (j < ncols)
-                                {
-                                  const int patch = j / ss.ng_full, nl = j % ss.ng_full;
-                                  colv.push_back(nl * s.isz() + sva[item.first + patch]);
-                                  colp.push_back(nl * s.isz() + spa[item.first + patch]);
-                                  coln.push_back(nl);
-                                }
-                              else
-                                {
-                                  colv.push_back(0);
-                                  colp.push_back(0);
-                                  coln.push_back(1 << 30);
-                                }
-                            }
-                          tiles.push_back(tl);
-                        }
+                        tiles.push_back(VankaTile{item.cls, std::min(tc, ncols - c0), item.first, c0});
                     }
                   if (hptr[blk + 1] > hptr[blk])
                     pad(items[hptr[blk + 1] - 1].cls);
@@ -515,9 +484,6 @@ build_level(stmg_level &L)
               ss.tile_ptr[sc].upload(tptr);
             }
           ss.tiles.upload(tiles);
-          ss.colv.upload(colv);
-          ss.colp.upload(colp);
-          ss.coln.upload(coln);
           if (!tc_ok)
             ss.tile_ptr.clear(); // use the item-based DMMA kernel instead
         }

@@ -78,9 +78,9 @@ dmma(double (&d)[2], double a, double b)
 template <int KS>
 __global__ void __launch_bounds__(kTThreads, 1)
 vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__restrict__ tiles,
-                const long long *__restrict__ colv, const long long *__restrict__ colp, const int *__restrict__ coln,
-                const int *__restrict__ tile_ptr, int ng_full, const double *__restrict__ r, double *__restrict__ u,
-                long long isz, int n_intervals, double omega)
+                const long long *__restrict__ va, const long long *__restrict__ pa, const int *__restrict__ tile_ptr,
+                int ng_full, const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals,
+                double omega)
 {
   extern __shared__ __align__(16) double ring[]; // kTSlots slots of kTRows x kTLd, then the block's tile data
   long long *s_colv = reinterpret_cast<long long *>(ring + kTSlots * kTSlot);
@@ -93,15 +93,28 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
   const int n0 = blockIdx.y * ng_full;
   const long long base0 = n0 * isz;
 
-  // stage this block's tile headers and column data (<= kTMaxTiles tiles)
-  for (int e = tid; e < nb * kTCols; e += kTThreads)
-    {
-      s_colv[e] = colv[t0 * kTCols + e];
-      s_colp[e] = colp[t0 * kTCols + e];
-      s_coln[e] = coln[t0 * kTCols + e];
-    }
+  // stage this block's tile headers and expand their column data
+  // (<= kTMaxTiles tiles): column j of tile t = (patch, interval) entry
+  // c0 + j of its item, patch-major, interval-minor
   for (int e = tid; e < nb; e += kTThreads)
     s_tile[e] = tiles[t0 + e];
+  for (int e = tid; e < nb * kTCols; e += kTThreads)
+    {
+      const VankaTile tl = tiles[t0 + e / kTCols];
+      const int j = e % kTCols;
+      if (j < tl.ncols)
+        {
+          const int q = tl.c0 + j, patch = tl.pfirst + q / ng_full, nl = q % ng_full;
+          s_colv[e] = nl * isz + va[patch];
+          s_colp[e] = nl * isz + pa[patch];
+          s_coln[e] = nl;
+        }
+      else
+        {
+          s_colv[e] = s_colp[e] = 0;
+          s_coln[e] = 1 << 30; // masked column
+        }
+    }
   __syncthreads();
 
   // gather: warp w fills columns w and w + 16, lane l rows l + 32 q
@@ -246,9 +259,9 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
 } // namespace
 
 cudaError_t
-launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *colv, const long long *colp,
-                const int *coln, const int *tile_ptr, int n_blocks, int ng_full, int max_nt, const double *r,
-                double *u, long long isz, int n_intervals, double omega, cudaStream_t stream)
+launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *va, const long long *pa,
+                const int *tile_ptr, int n_blocks, int ng_full, int max_nt, const double *r, double *u, long long isz,
+                int n_intervals, double omega, cudaStream_t stream)
 {
   if (n_blocks == 0 || n_intervals == 0)
     return cudaSuccess;
@@ -256,8 +269,8 @@ launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long
   const int ks = (max_nt + 3) / 4;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTSmem));
-    kern<<<grid, kTThreads, kTSmem, stream>>>(classes, tiles, colv, colp, coln, tile_ptr, ng_full, r, u, isz,
-                                              n_intervals, omega);
+    kern<<<grid, kTThreads, kTSmem, stream>>>(classes, tiles, va, pa, tile_ptr, ng_full, r, u, isz, n_intervals,
+                                              omega);
   };
   if (ks <= 8)
     go(vanka_tc_kernel<8>);
