@@ -130,6 +130,10 @@ int stmg_smooth_step_host(stmg_level *level, const double *b, double *u, double 
 int stmg_assemble_rhs(stmg_level *level, int problem, double t_start, double *F, int n_intervals);
 int stmg_compute_errors(stmg_level *level, int problem, double t_start, const double *X, int n_intervals,
                         double *out);
+/* interpolate_exact (harness.cpp:185-239): the built-in exact solution as a
+ * trajectory X (nodal velocity at the GLL grid, per-cell L2-projected
+ * pressure), n_intervals intervals from t_start. */
+int stmg_interpolate_exact(stmg_level *level, int problem, double t_start, double *X, int n_intervals);
 
 /* ------------------------------------------------------------ solver
  * build_setup + VCycle + gmres + time_march (harness.cpp:26-70,

@@ -615,6 +615,7 @@ std::vector<LevelDescriptor> plan_hierarchy(const RunConfig &config, double t_en
 Setup build_setup(const StokesProblem &problem, const RunConfig &config);          // harness.cpp:51-70
 int step_count(const StokesProblem &problem, const RunConfig &config);
 ErrorReport compute_errors(const Setup &setup, const TimeMarchResult &march, const ExactSolution &exact);
+TimeMarchResult interpolate_exact(const Setup &setup, const ExactSolution &exact, int n_steps); // harness.cpp:185-239
 double evaluate_pressure(const PressureSpace &ps, const double *coeffs, double x, double y);
 double evaluate_velocity(const VelocitySpace &vs, const double *coeffs, double x, double y, int comp);
 

@@ -514,4 +514,18 @@ oracle_manufactured_errors(void *hp, const double *X, double *out)
   });
 }
 
+/// interpolate_exact (harness.cpp:185-239) of the manufactured solution on
+/// the finest level: X (n_steps intervals).
+int
+oracle_interpolate_manufactured(void *hp, double *X)
+{
+  return guard([&] {
+    auto *h = static_cast<SolverHandle *>(hp);
+    const TimeMarchResult m = interpolate_exact(h->setup, manufactured_problem().exact, h->n_steps);
+    const size_t sz = m.trajectory[0].data.size();
+    for (int n = 0; n < h->n_steps; ++n)
+      std::memcpy(X + n * sz, m.trajectory[n].data.data(), sizeof(double) * sz);
+  });
+}
+
 } // extern "C"

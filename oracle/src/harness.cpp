@@ -218,6 +218,54 @@ compute_errors(const Setup &setup, const TimeMarchResult &march, const ExactSolu
   return rep;
 }
 
+// harness.cpp:185-239: nodal velocity at the GLL grid, pressure by the
+// per-cell L2 projection onto the orthogonal P_r^disc basis (Gauss(r+3)).
+TimeMarchResult
+interpolate_exact(const Setup &setup, const ExactSolution &exact, int n_steps)
+{
+  const MultigridLevel &fine = setup.levels.finest();
+  const VelocitySpace &vs = *fine.vspace;
+  const PressureSpace &ps = *fine.pspace;
+  const TemporalMatrices &tm = *fine.tmat;
+  const int ns = tm.n_dofs();
+  const int np = ps.dofs_per_cell();
+  const CellKernels eval(vs, ps, vs.r() + 3);
+  const int nq = eval.n_q_1d();
+  const Mesh &mesh = vs.mesh();
+  TimeMarchResult result;
+  for (int n = 1; n <= n_steps; ++n)
+    {
+      BlockVector x = fine.op->make_vector();
+      for (int a = 0; a < ns; ++a)
+        {
+          const double t = (n - 1) * tm.tau + 0.5 * tm.tau * (tm.nodes[a] + 1.0);
+          double *v = x.velocity(a);
+          for (int s = 0; s < vs.n_scalar_dofs(); ++s)
+            for (int comp = 0; comp < 2; ++comp)
+              v[vs.global_dof(comp, s)] = exact.velocity(vs.node_x(s), vs.node_y(s), t, comp);
+          double *p = x.pressure(a);
+          for (int cell = 0; cell < mesh.n_cells(vs.level()); ++cell)
+            {
+              const Box box = mesh.cell_box(vs.level(), cell);
+              std::vector<double> rhs(np, 0.0);
+              for (int qy = 0; qy < nq; ++qy)
+                for (int qx = 0; qx < nq; ++qx)
+                  {
+                    const double xp = box.x0 + 0.5 * box.width() * (eval.qpoints()[qx] + 1.0);
+                    const double yp = box.y0 + 0.5 * box.height() * (eval.qpoints()[qy] + 1.0);
+                    const double wq = eval.qweights()[qx] * eval.qweights()[qy] * eval.jdet() * exact.pressure(xp, yp, t);
+                    for (int l = 0; l < np; ++l)
+                      rhs[l] += wq * eval.psi()(qy * nq + qx, l);
+                  }
+              for (int l = 0; l < np; ++l)
+                p[ps.cell_dof(cell, l)] = rhs[l] / (eval.jdet() * ps.basis().gram_diagonal(l));
+            }
+        }
+      result.trajectory.push_back(std::move(x));
+    }
+  return result;
+}
+
 // harness.cpp:325-346
 double
 evaluate_pressure(const PressureSpace &ps, const double *coeffs, double x, double y)

@@ -78,6 +78,7 @@ _SIGNATURES = {
     "stmg_time_march": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_time_march_host": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_assemble_rhs": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int], _c_int),
+    "stmg_interpolate_exact": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int], _c_int),
     "stmg_compute_errors": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int, ctypes.POINTER(_c_double)], _c_int),
     "stmg_solver_set_comm": ([_c_void_p, _c_void_p], _c_int),
     "stmg_vcycle_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
@@ -247,6 +248,11 @@ class Level:
         """SpaceTimeBlockOperator::assemble_rhs of a built-in force for n_intervals intervals from t_start."""
         _check(load_library().stmg_assemble_rhs(self._h, problem, t_start, _ptr(F), n_intervals))
         return F
+
+    def interpolate_exact(self, X, t_start: float = 0.0, n_intervals: int = 1, problem: int = PROBLEM_MANUFACTURED):
+        """interpolate_exact (harness.cpp:185-239) of the built-in exact solution into X."""
+        _check(load_library().stmg_interpolate_exact(self._h, problem, t_start, _ptr(X), n_intervals))
+        return X
 
     def compute_errors(self, X, t_start: float = 0.0, n_intervals: int = 1,
                        problem: int = PROBLEM_MANUFACTURED) -> dict:

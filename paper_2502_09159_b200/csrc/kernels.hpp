@@ -104,6 +104,8 @@ cudaError_t launch_coarse_forward(const double *G, const double *H, int n, int m
 cudaError_t launch_assemble_manufactured(const DevGeom &G, int r, const ProblemTables &T, double nu, double t_start,
                                          double tau, double *F, int n_intervals, cudaStream_t st);
 long long errors_partials(const DevGeom &G, int n_intervals);
+cudaError_t launch_interpolate_manufactured(const DevGeom &G, int r, const ProblemTables &T, double t_start,
+                                            double tau, double *X, int n_intervals, cudaStream_t st);
 cudaError_t launch_errors_manufactured(const DevGeom &G, int r, const ProblemTables &T, double t_start, double tau,
                                        const double *X, int n_intervals, double *part, double *out, cudaStream_t st);
 int dot_partials();

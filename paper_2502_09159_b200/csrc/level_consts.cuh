@@ -82,6 +82,8 @@ struct ProblemTables
   double ex[9], ew[9], ephi[9 * 8], edphi[9 * 8], eleg[9 * 6];
   // errors: Gauss(k+2) in time, Radau-node Lagrange values tval(q, a)
   double tq[8], tqw[8], tval[8 * 6];
+  // GLL nodes of the velocity basis (interpolate_exact)
+  double gll[8];
 };
 
 /// Degree-major P_r^disc mode list (pdisc.cpp:41-55): mode m has Legendre

@@ -1,9 +1,10 @@
 // Built-in problem data on the GPU: the load vector of SpaceTimeBlockOperator::
 // assemble_rhs (st_operator.cpp:423-467) for the reference's manufactured
-// problem (problems.cpp:13-62), and the space-time error norms of
-// compute_errors (harness.cpp:72-183). These close the loop of acceptance
-// Table 1 on the device: assemble -> time_march ->
-// errors, with no host round trip of the trajectory.
+// problem (problems.cpp:13-62), its interpolant (interpolate_exact,
+// harness.cpp:185-239) and the space-time error norms of compute_errors
+// (harness.cpp:72-183). These close the loop of acceptance Table 1
+// on the device: assemble -> time_march -> errors, with
+// no host round trip of the trajectory.
 #include "kernels.hpp"
 
 #include <cuda_runtime.h>
@@ -106,6 +107,70 @@ mf_exact(double xp, double yp, double t, double &u0, double &u1, double g[4], do
   g[2] = -sg * cx * (1.0 - cy);  // d u1 / dx
   g[3] = -sg * sx * sy;          // d u1 / dy
   pr = 0.25 * stt * sx * sy;
+}
+
+// interpolate_exact (harness.cpp:185-239), velocity: nodal values at the GLL
+// grid, one thread per (scalar node, interval).
+__global__ void
+interp_velocity_kernel(DevGeom G, int p, ProblemTables T, double t_start, double tau, double *X)
+{
+  const long long s = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (s >= G.nsc)
+    return;
+  const int n = blockIdx.y;
+  const int ix = static_cast<int>(s % G.gx), iy = static_cast<int>(s / G.gx);
+  const int cx = min(ix / p, G.nx - 1), cy = min(iy / p, G.ny - 1);
+  const double xp = cx * G.hx + 0.5 * G.hx * (T.gll[ix - cx * p] + 1.0);
+  const double yp = cy * G.hy + 0.5 * G.hy * (T.gll[iy - cy * p] + 1.0);
+  for (int a = 0; a < G.S; ++a)
+    {
+      const double t = t_start + n * tau + 0.5 * tau * (T.tn[a] + 1.0);
+      double u0, u1, g[4], pr;
+      mf_exact(xp, yp, t, u0, u1, g, pr);
+      X[n * G.isz + a * G.mv + s] = u0;
+      X[n * G.isz + a * G.mv + G.nsc + s] = u1;
+    }
+}
+
+// pressure: per-cell L2 projection onto the orthogonal tensor-Legendre
+// P_r^disc basis with Gauss(r+3), one thread per (cell, interval)
+template <int R>
+__global__ void
+interp_pressure_kernel(DevGeom G, ProblemTables T, double t_start, double tau, double *X)
+{
+  constexpr int NQ = R + 3, NP = (R + 1) * (R + 2) / 2;
+  const long long cell = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (cell >= static_cast<long long>(G.nx) * G.ny)
+    return;
+  const int n = blockIdx.y;
+  const int cx = static_cast<int>(cell % G.nx), cy = static_cast<int>(cell / G.nx);
+  const double x0 = cx * G.hx, y0 = cy * G.hy;
+  for (int a = 0; a < G.S; ++a)
+    {
+      const double t = t_start + n * tau + 0.5 * tau * (T.tn[a] + 1.0);
+      double rhs[NP];
+#pragma unroll
+      for (int l = 0; l < NP; ++l)
+        rhs[l] = 0.0;
+      for (int qy = 0; qy < NQ; ++qy)
+        for (int qx = 0; qx < NQ; ++qx)
+          {
+            double u0, u1, g[4], pr;
+            mf_exact(x0 + 0.5 * G.hx * (T.ex[qx] + 1.0), y0 + 0.5 * G.hy * (T.ex[qy] + 1.0), t, u0, u1, g, pr);
+            const double wq = T.ew[qx] * T.ew[qy] * pr; // jdet cancels against the Gram scaling
+#pragma unroll
+            for (int l = 0; l < NP; ++l)
+              rhs[l] = fma(wq, T.eleg[qx * (R + 1) + pdisc_mode_ax(R, l)] * T.eleg[qy * (R + 1) + pdisc_mode_ay(R, l)],
+                           rhs[l]);
+          }
+#pragma unroll
+      for (int l = 0; l < NP; ++l)
+        {
+          const int ax = pdisc_mode_ax(R, l), ay = pdisc_mode_ay(R, l);
+          const double gram = (2.0 / (2 * ax + 1)) * (2.0 / (2 * ay + 1)); // pdisc.cpp gram_diagonal
+          X[n * G.isz + G.S * G.mv + a * G.mp + cell * NP + l] = rhs[l] / gram;
+        }
+    }
 }
 
 constexpr int kErrThreads = 128;
@@ -302,6 +367,26 @@ launch_assemble_manufactured(const DevGeom &G, int r, const ProblemTables &T, do
         }
     }
   return launch_zero_constrained(G, F, n_intervals, st); // st_operator.cpp:465
+}
+
+cudaError_t
+launch_interpolate_manufactured(const DevGeom &G, int r, const ProblemTables &T, double t_start, double tau,
+                                double *X, int n_intervals, cudaStream_t st)
+{
+  if (n_intervals <= 0)
+    return cudaSuccess;
+  dim3 gv(static_cast<unsigned>((G.nsc + 127) / 128), n_intervals);
+  interp_velocity_kernel<<<gv, 128, 0, st>>>(G, r + 1, T, t_start, tau, X);
+  const long long ncell = static_cast<long long>(G.nx) * G.ny;
+  dim3 gp(static_cast<unsigned>((ncell + 127) / 128), n_intervals);
+  switch (r)
+    {
+      case 1: interp_pressure_kernel<1><<<gp, 128, 0, st>>>(G, T, t_start, tau, X); break;
+      case 2: interp_pressure_kernel<2><<<gp, 128, 0, st>>>(G, T, t_start, tau, X); break;
+      case 3: interp_pressure_kernel<3><<<gp, 128, 0, st>>>(G, T, t_start, tau, X); break;
+      default: interp_pressure_kernel<4><<<gp, 128, 0, st>>>(G, T, t_start, tau, X); break;
+    }
+  return cudaGetLastError();
 }
 
 cudaError_t

@@ -1032,6 +1032,8 @@ problem_tables(const LevelSpec &L)
   ProblemTables T{};
   const int n1 = L.n1();
   const std::vector<double> gll = gauss_lobatto(n1);
+  for (int i = 0; i < n1; ++i)
+    T.gll[i] = gll[i];
   const Rule1D ga = gauss_legendre(L.r + 2); // st_operator.cpp:167
   for (int q = 0; q < L.r + 2; ++q)
     {

@@ -1474,6 +1474,21 @@ stmg_assemble_rhs(stmg_level *L, int problem, double t_start, double *F, int n)
 }
 
 int
+stmg_interpolate_exact(stmg_level *L, int problem, double t_start, double *X, int n)
+{
+  return guarded([&] {
+    if (problem != STMG_PROBLEM_MANUFACTURED)
+      throw std::invalid_argument("stmg_interpolate_exact: unknown problem");
+    if (n < 0 || !X)
+      throw std::invalid_argument("stmg_interpolate_exact: invalid arguments");
+    check(launch_interpolate_manufactured(L->geom, L->spec.r, L->problem_tab(), t_start, L->spec.tau, X, n,
+                                          L->ctx->stream),
+          "interpolate_exact");
+    L->ctx->count(2);
+  });
+}
+
+int
 stmg_compute_errors(stmg_level *L, int problem, double t_start, const double *X, int n, double *out)
 {
   return guarded([&] {

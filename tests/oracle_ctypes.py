@@ -66,6 +66,7 @@ def lib():
         L.oracle_assemble_rhs_manufactured.argtypes = [_P, ctypes.c_double, _D]
         L.oracle_time_march_manufactured.argtypes = [_P, _D, ctypes.POINTER(ctypes.c_int)]
         L.oracle_manufactured_errors.argtypes = [_P, _D, _D]
+        L.oracle_interpolate_manufactured.argtypes = [_P, _D]
     return _lib
 
 
@@ -195,6 +196,11 @@ class OracleSolver:
         it = (ctypes.c_int * self.n_steps)()
         _chk(lib().oracle_time_march_manufactured(self.h, _d(X), it))
         return X, list(it)
+
+    def interpolate_manufactured(self):
+        X = np.zeros(self.n_steps * self.size)
+        _chk(lib().oracle_interpolate_manufactured(self.h, _d(X)))
+        return X
 
     def manufactured_errors(self, X):
         out = np.zeros(5)

@@ -94,3 +94,22 @@ def test_table1_r4_on_gpu(ctx, stmg):
         assert 0.5 < ep[-1] / ref_p[c - 1] < 2.0
     for i in (1, 2):
         assert abs(math.log2(ev[i - 1] / ev[i]) - ref_eoc[i - 1]) <= 0.3
+
+
+@pytest.mark.parametrize("c,r,k", [(2, 1, 1), (2, 2, 2), (1, 4, 4)])
+def test_interpolate_exact_matches_oracle(ctx, stmg, c, r, k):
+    """interpolate_exact (harness.cpp:185-239) on the GPU equals the oracle's,
+    and its error norms are the interpolation errors the oracle reports."""
+    sol = stmg.Solver(ctx, c, r, k, nu=0.1)
+    ref = oc.OracleSolver(c, r, k, nu=0.1)
+    lv = sol.finest
+    n = sol.n_steps
+    X = torch.zeros(n * lv.size, dtype=torch.float64, device="cuda")
+    lv.interpolate_exact(X, 0.0, n)
+    Xr = ref.interpolate_manufactured()
+    Xh = host(X)
+    assert np.abs(Xh - Xr).max() <= 1e-13 * np.abs(Xr).max()
+    got = lv.compute_errors(X, 0.0, n)
+    want = ref.manufactured_errors(Xr)
+    assert abs(got["e_v_l2"] - want[0]) <= 1e-9 * want[0]
+    assert abs(got["e_p_l2"] - want[1]) <= 1e-9 * want[1]
