@@ -127,6 +127,7 @@ int stmg_smooth_step_host(stmg_level *level, const double *b, double *u, double 
  * out[0..4] = e_v L2(L2), e_p L2(L2), e_v L2(H1-seminorm), ||div v|| L2(L2),
  * e_v max over quadrature points (host array). r <= 4, k <= 4. */
 #define STMG_PROBLEM_MANUFACTURED 0
+#define STMG_PROBLEM_CAVITY 1 /* lid-driven cavity (problems.cpp:64-78): boundary data only */
 int stmg_assemble_rhs(stmg_level *level, int problem, double t_start, double *F, int n_intervals);
 int stmg_compute_errors(stmg_level *level, int problem, double t_start, const double *X, int n_intervals,
                         double *out);
@@ -175,6 +176,12 @@ int stmg_gmres(stmg_solver *solver, const double *b, double *x, int *iterations,
  * iterations of each step. */
 int stmg_time_march(stmg_solver *solver, const double *F, double *X, int *iterations);
 int stmg_time_march_host(stmg_solver *solver, const double *F, double *X, int *iterations);
+/* time_march (solver.cpp:204-325) of a built-in problem with the solver's nu:
+ * STMG_PROBLEM_MANUFACTURED assembles its force every step (assemble_rhs);
+ * STMG_PROBLEM_CAVITY has no force and inhomogeneous Dirichlet data, applied
+ * by the reference's lift: rhs -= A_raw lift, solve, x += lift
+ * (solver.cpp:251-283). Zero initial velocity. */
+int stmg_time_march_problem(stmg_solver *solver, int problem, double *X, int *iterations);
 
 /* ------------------------------------------------------------ all-at-once
  * The global space-time system of Eq. GloSys: the block

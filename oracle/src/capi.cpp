@@ -528,4 +528,22 @@ oracle_interpolate_manufactured(void *hp, double *X)
   });
 }
 
+/// time_march of the lid-driven cavity (problems.cpp:64-78) with the
+/// solver's nu: inhomogeneous Dirichlet data by lifting (solver.cpp:251-283).
+int
+oracle_time_march_cavity(void *hp, double *X, int *iterations)
+{
+  return guard([&] {
+    auto *h = static_cast<SolverHandle *>(hp);
+    const StokesProblem cp = cavity_problem(h->config.nu);
+    const TimeMarchResult res = time_march(h->setup.levels, cp.data, h->n_steps, h->config.mg, h->config.krylov, true);
+    const size_t sz = res.trajectory[0].data.size();
+    for (int n = 0; n < h->n_steps; ++n)
+      {
+        std::memcpy(X + n * sz, res.trajectory[n].data.data(), sizeof(double) * sz);
+        iterations[n] = res.steps[n].iterations;
+      }
+  });
+}
+
 } // extern "C"

@@ -22,6 +22,7 @@ LIB_PATH = _PKG / "_build" / "libstmg_b200.so"
 HEADER_PATH = _PKG.parent / "include" / "stmg_b200.h"
 
 PROBLEM_MANUFACTURED = 0
+PROBLEM_CAVITY = 1
 
 SMOOTHER_NONE = -1
 SMOOTHER_CELL = 0
@@ -76,6 +77,7 @@ _SIGNATURES = {
     "stmg_gmres": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_double), _c_int],
                    _c_int),
     "stmg_time_march": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
+    "stmg_time_march_problem": ([_c_void_p, _c_int, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_time_march_host": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_assemble_rhs": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int], _c_int),
     "stmg_interpolate_exact": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int], _c_int),
@@ -328,6 +330,12 @@ class Solver:
         _check(load_library().stmg_time_march(self._h, _ptr(F), _ptr(X), iters))
         return [int(v) for v in iters]
 
+    def time_march_problem(self, problem: int, X):
+        """time_march of a built-in problem (PROBLEM_MANUFACTURED: force; PROBLEM_CAVITY: lifted lid data)."""
+        iters = (ctypes.c_int * self.n_steps)()
+        _check(load_library().stmg_time_march_problem(self._h, problem, _ptr(X), iters))
+        return [int(v) for v in iters]
+
     def time_march_host(self, F, X):
         iters = (ctypes.c_int * self.n_steps)()
         _check(load_library().stmg_time_march_host(self._h, _hptr(F), _hptr(X), iters))
@@ -400,4 +408,5 @@ def exported_symbols() -> Sequence[str]:
 
 
 __all__ = ["Context", "Level", "Solver", "StmgError", "load_library", "plan_levels", "patch_info",
-           "exported_symbols", "SMOOTHER_CELL", "SMOOTHER_VERTEX_STAR", "SMOOTHER_NONE", "PROBLEM_MANUFACTURED"]
+           "exported_symbols", "SMOOTHER_CELL", "SMOOTHER_VERTEX_STAR", "SMOOTHER_NONE", "PROBLEM_MANUFACTURED",
+           "PROBLEM_CAVITY"]

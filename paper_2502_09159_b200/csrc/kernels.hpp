@@ -104,12 +104,16 @@ cudaError_t launch_coarse_forward(const double *G, const double *H, int n, int m
 cudaError_t launch_assemble_manufactured(const DevGeom &G, int r, const ProblemTables &T, double nu, double t_start,
                                          double tau, double *F, int n_intervals, cudaStream_t st);
 long long errors_partials(const DevGeom &G, int n_intervals);
+cudaError_t launch_lift_cavity(const DevGeom &G, int r, const ProblemTables &T, double t_start, double tau,
+                               double *L, int n_intervals, cudaStream_t st);
 cudaError_t launch_interpolate_manufactured(const DevGeom &G, int r, const ProblemTables &T, double t_start,
                                             double tau, double *X, int n_intervals, cudaStream_t st);
 cudaError_t launch_errors_manufactured(const DevGeom &G, int r, const ProblemTables &T, double t_start, double tau,
                                        const double *X, int n_intervals, double *part, double *out, cudaStream_t st);
 int dot_partials();
 cudaError_t launch_dot(const double *x, const double *y, long long n, double *part, double *out, cudaStream_t st);
+/// y += a x with a = alpha_dev ? sign * (*alpha_dev) : alpha (sign applies to
+/// the device-resident coefficient only).
 cudaError_t launch_axpy(long long n, double alpha, const double *alpha_dev, double sign, const double *x, double *y,
                         cudaStream_t st);
 cudaError_t launch_scale(long long n, double alpha, double *y, cudaStream_t st);

@@ -173,6 +173,37 @@ interp_pressure_kernel(DevGeom G, ProblemTables T, double t_start, double tau, d
     }
 }
 
+// Lid-driven cavity boundary data (problems.cpp:64-78): u_x = sin(pi t / 4)
+// on the open lid y = 1, 0 < x < 1; zero elsewhere. Writes the lift vector of
+// time_march (solver.cpp:251-262): boundary values on the constrained nodes
+// at the slot times (VelocitySpace::set_boundary_values, dof_space.cpp:71-81),
+// zero everywhere else. Node coordinates follow dof_space.cpp:40-50 exactly
+// (last grid line forced to the domain edge), so the y >= 1 test matches.
+__global__ void
+lift_cavity_kernel(DevGeom G, int p, ProblemTables T, double t_start, double tau, double *L)
+{
+  const long long s = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (s >= G.nsc)
+    return;
+  const int n = blockIdx.y;
+  const int ix = static_cast<int>(s % G.gx), iy = static_cast<int>(s / G.gx);
+  const bool bnd = ix == 0 || ix == G.gx - 1 || iy == 0 || iy == G.gy - 1;
+  const auto coord = [&](int i, int g, double h) {
+    if (i == g - 1)
+      return 1.0;
+    const int c = i / p;
+    return h * (c + 0.5 * (T.gll[i - c * p] + 1.0));
+  };
+  const double xp = coord(ix, G.gx, G.hx), yp = coord(iy, G.gy, G.hy);
+  for (int a = 0; a < G.S; ++a)
+    {
+      const double t = t_start + n * tau + 0.5 * tau * (T.tn[a] + 1.0);
+      const double ux = (bnd && yp >= 1.0 && xp > 0.0 && xp < 1.0) ? sin(0.25 * kPi * t) : 0.0;
+      L[n * G.isz + a * G.mv + s] = ux;
+      L[n * G.isz + a * G.mv + G.nsc + s] = 0.0;
+    }
+}
+
 constexpr int kErrThreads = 128;
 
 // compute_errors (harness.cpp:72-183): one thread per (cell, interval);
@@ -386,6 +417,18 @@ launch_interpolate_manufactured(const DevGeom &G, int r, const ProblemTables &T,
       case 3: interp_pressure_kernel<3><<<gp, 128, 0, st>>>(G, T, t_start, tau, X); break;
       default: interp_pressure_kernel<4><<<gp, 128, 0, st>>>(G, T, t_start, tau, X); break;
     }
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_lift_cavity(const DevGeom &G, int r, const ProblemTables &T, double t_start, double tau, double *L,
+                   int n_intervals, cudaStream_t st)
+{
+  if (n_intervals <= 0)
+    return cudaSuccess;
+  cudaMemsetAsync(L, 0, sizeof(double) * G.isz * n_intervals, st);
+  dim3 g(static_cast<unsigned>((G.nsc + 127) / 128), n_intervals);
+  lift_cavity_kernel<<<g, 128, 0, st>>>(G, r + 1, T, t_start, tau, L);
   return cudaGetLastError();
 }
 

@@ -996,9 +996,11 @@ struct stmg_solver
     return it;
   }
 
-  // time_march (solver.cpp:204-325) with per-step load vectors F.
+  // time_march (solver.cpp:204-325) with per-step load vectors F, or a
+  // built-in problem (force assembled per step; boundary data by lifting).
+  DevArray<double> fstep, lift, lifted;
   void
-  time_march(const double *F, double *X, int *iterations)
+  time_march(const double *F, double *X, int *iterations, int problem = -1)
   {
     stmg_level &L = fine();
     const long long n = L.spec.isz();
@@ -1006,15 +1008,49 @@ struct stmg_solver
     vprev.resize(L.spec.mv());
     check(cudaMemsetAsync(vprev.p, 0, sizeof(double) * L.spec.mv(), ctx->stream), "memset");
     const double *zero = L.zero_vector(1);
+    const double tau = L.spec.tau;
+    const bool inhomogeneous = problem == STMG_PROBLEM_CAVITY;
+    if (problem >= 0)
+      fstep.resize(n);
+    if (inhomogeneous)
+      {
+        lift.resize(n);
+        lifted.resize(n);
+      }
     for (int step = 0; step < n_steps; ++step)
       {
-        // rhs = F_n + C v_prev (coupling_rhs), constrained rows zeroed
-        L.vmult(zero, F + step * n, rhs.p, 1, vprev.p, 1, 1);
+        const double t_start = step * tau;
+        const double *Fn = F ? F + step * n : zero;
+        if (problem == STMG_PROBLEM_MANUFACTURED)
+          {
+            check(launch_assemble_manufactured(L.geom, L.spec.r, L.problem_tab(), L.spec.nu, t_start, tau, fstep.p, 1,
+                                               ctx->stream),
+                  "assemble_rhs");
+            ctx->count(5);
+            Fn = fstep.p;
+          }
+        // rhs = F_n + C v_prev (coupling_rhs)
+        L.vmult(zero, Fn, rhs.p, 1, vprev.p, 1, 1);
+        if (inhomogeneous)
+          {
+            // rhs -= A_raw lift (solver.cpp:251-262)
+            check(launch_lift_cavity(L.geom, L.spec.r, L.problem_tab(), t_start, tau, lift.p, 1, ctx->stream),
+                  "lift");
+            ctx->count();
+            L.vmult(lift.p, nullptr, lifted.p, 1, nullptr, 0, 2);
+            check(launch_axpy(n, -1.0, nullptr, 1.0, lifted.p, rhs.p, ctx->stream), "axpy");
+            ctx->count();
+          }
         check(launch_zero_constrained(L.geom, rhs.p, 1, ctx->stream), "zero");
         ctx->count();
         double *x = X + step * n;
         int it = 0;
         gmres(rhs.p, x, &it, nullptr, 0);
+        if (inhomogeneous)
+          {
+            check(launch_axpy(n, 1.0, nullptr, 1.0, lift.p, x, ctx->stream), "axpy"); // x += lift
+            ctx->count();
+          }
         L.project(x, 1);
         if (iterations)
           iterations[step] = it;
@@ -1547,6 +1583,16 @@ int
 stmg_time_march(stmg_solver *s, const double *F, double *X, int *iterations)
 {
   return guarded([&] { s->time_march(F, X, iterations); });
+}
+
+int
+stmg_time_march_problem(stmg_solver *s, int problem, double *X, int *iterations)
+{
+  return guarded([&] {
+    if (problem != STMG_PROBLEM_MANUFACTURED && problem != STMG_PROBLEM_CAVITY)
+      throw std::invalid_argument("stmg_time_march_problem: unknown problem");
+    s->time_march(nullptr, X, iterations, problem);
+  });
 }
 
 int

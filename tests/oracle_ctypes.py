@@ -67,6 +67,7 @@ def lib():
         L.oracle_time_march_manufactured.argtypes = [_P, _D, ctypes.POINTER(ctypes.c_int)]
         L.oracle_manufactured_errors.argtypes = [_P, _D, _D]
         L.oracle_interpolate_manufactured.argtypes = [_P, _D]
+        L.oracle_time_march_cavity.argtypes = [_P, _D, ctypes.POINTER(ctypes.c_int)]
     return _lib
 
 
@@ -195,6 +196,12 @@ class OracleSolver:
         X = np.zeros(self.n_steps * self.size)
         it = (ctypes.c_int * self.n_steps)()
         _chk(lib().oracle_time_march_manufactured(self.h, _d(X), it))
+        return X, list(it)
+
+    def time_march_cavity(self):
+        X = np.zeros(self.n_steps * self.size)
+        it = (ctypes.c_int * self.n_steps)()
+        _chk(lib().oracle_time_march_cavity(self.h, _d(X), it))
         return X, list(it)
 
     def interpolate_manufactured(self):

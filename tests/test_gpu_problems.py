@@ -113,3 +113,33 @@ def test_interpolate_exact_matches_oracle(ctx, stmg, c, r, k):
     want = ref.manufactured_errors(Xr)
     assert abs(got["e_v_l2"] - want[0]) <= 1e-9 * want[0]
     assert abs(got["e_p_l2"] - want[1]) <= 1e-9 * want[1]
+
+
+@pytest.mark.parametrize("c,r,k,nu", [(2, 2, 2, 0.1), (3, 1, 1, 0.05)])
+def test_cavity_time_march_with_lift_matches_oracle(ctx, stmg, c, r, k, nu):
+    """time_march with inhomogeneous Dirichlet data (solver.cpp:251-283): the
+    lid-driven cavity (problems.cpp:64-78) lifted on the GPU reproduces the
+    oracle's trajectory; iterations within +-1."""
+    n_steps = 4
+    sol = stmg.Solver(ctx, c, r, k, n_steps=n_steps, t_end=8.0 * n_steps / 32, nu=nu, rtol=1e-10)
+    ref = oc.OracleSolver(c, r, k, n_steps=n_steps, t_end=8.0 * n_steps / 32, nu=nu, rtol=1e-10)
+    X = torch.zeros(n_steps * sol.finest.size, dtype=torch.float64, device="cuda")
+    iters = sol.time_march_problem(stmg.PROBLEM_CAVITY, X)
+    Xr, itr = ref.time_march_cavity()
+    assert all(abs(a - b) <= 1 for a, b in zip(iters, itr)), (iters, itr)
+    assert np.linalg.norm(Xr) > 0
+    assert np.linalg.norm(host(X) - Xr) <= 1e-8 * np.linalg.norm(Xr)
+
+
+def test_time_march_problem_manufactured_equals_assembled_path(ctx, stmg):
+    sol = stmg.Solver(ctx, 2, 2, 2, nu=0.1, rtol=1e-10)
+    lv = sol.finest
+    n = sol.n_steps
+    F = torch.zeros(n * lv.size, dtype=torch.float64, device="cuda")
+    lv.assemble_rhs(F, 0.0, n)
+    X1 = torch.zeros_like(F)
+    it1 = sol.time_march(F, X1)
+    X2 = torch.zeros_like(F)
+    it2 = sol.time_march_problem(stmg.PROBLEM_MANUFACTURED, X2)
+    assert it1 == it2
+    assert float((X1 - X2).abs().max()) <= 1e-12 * float(X1.abs().max())
