@@ -18,6 +18,14 @@ Local Vanka inverses are precomputed once and shared by all intervals.
   --impl reference: the CPU restatement of the reference (oracle/, OpenMP over
             intervals on all host cores) on a bounded sample of the same
             discretisation; rank 0 only.
+
+Extra fields of the JSON line (not the headline; skipped with --no-solve):
+  solve.C1             FGMRES + V(2,2) time marching of C1 (16^2, Q2/P1, DG(1))
+  solve.C4_first2      time marching of the C4 discretisation, first 2 intervals
+  solve.C4_all_at_once all-at-once slab solve of C4, 8 intervals per rank,
+                       partitioned over all ranks (NCCL time slabs)
+  solve.C4_full        (1 GPU) the whole 64-interval C4 system as 8 macro steps
+  C4_step              C4 vmult + vertex-star smoother step over 8 intervals
 """
 from __future__ import annotations
 
