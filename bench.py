@@ -469,7 +469,10 @@ def main():
 
     slab = None
     if not args.no_solve:
-        slab = slab_solve_leg(stmg, ctx, torch, dist, world, rank)
+        try:  # a side leg: a failure is reported in the line, never fatal for the headline
+            slab = slab_solve_leg(stmg, ctx, torch, dist, world, rank)
+        except Exception as exc:
+            slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank != 0:
         if world > 1:
@@ -523,11 +526,16 @@ def main():
             "kernels": kernels, "roofline": roof, "gpu_launches": gpu_launches,
             "clocks": clk.summary(), "e2e": e2e}
     if not args.no_solve:
-        line["solve"] = solve_legs(stmg, ctx, torch)
+        def side(fn):
+            try:
+                return fn()
+            except Exception as exc:  # reported, never fatal for the headline
+                return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        line["solve"] = side(lambda: solve_legs(stmg, ctx, torch))
         line["solve"]["C4_all_at_once"] = slab
-        line["C4_step"] = c4_step_leg(stmg, ctx, torch)
+        line["C4_step"] = side(lambda: c4_step_leg(stmg, ctx, torch))
         if world == 1:
-            line["solve"]["C4_full"] = c4_full_leg(stmg, ctx, torch)
+            line["solve"]["C4_full"] = side(lambda: c4_full_leg(stmg, ctx, torch))
     if not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_quick()

@@ -28,7 +28,10 @@ namespace
 {
 constexpr int kTThreads = 512;
 constexpr int kTRows = 128;
-constexpr int kTCols = 32;
+#ifndef STMG_VANKA_COLS
+#define STMG_VANKA_COLS 32
+#endif
+constexpr int kTCols = STMG_VANKA_COLS; // columns (patch, interval) per tile
 // Diagnostic build switches (wrong results, timing only; DESIGN.md §3.2 cost
 // breakdown): STMG_VT_NO_GATHER, STMG_VT_NO_SCATTER.
 //
