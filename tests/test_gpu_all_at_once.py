@@ -158,3 +158,52 @@ def test_time_slab_partition_loopback(stmg, world):
     assert abs(results[0] - it1) <= 1, (results, it1)
     torch.cuda.synchronize()
     assert float((Xp - X1).norm() / X1.norm()) <= 1e-9
+
+
+def test_torch_comm_over_nccl_single_rank(stmg):
+    """The NCCL flavour of the communicator on real device memory (one rank:
+    NCCL cannot pair two ranks on one GPU): raw-pointer views, the library's
+    stream, all-reduce and all-gather through torch.distributed/NCCL, and a
+    partitioned solve object with the communicator installed."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2502_09159_b200 import timeslab
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comm = timeslab.TorchComm(device="cuda:0")
+        stream = torch.cuda.Stream()
+        buf = torch.arange(6, dtype=torch.float64, device="cuda")
+        recv = torch.full((4,), -1.0, dtype=torch.float64, device="cuda")
+        out = torch.zeros(3, dtype=torch.float64, device="cuda")
+        src = torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        comm.allreduce_sum(buf.data_ptr(), 6, stream.cuda_stream)
+        comm.allgather(src.data_ptr(), out.data_ptr(), 3, stream.cuda_stream)
+        comm.exchange_halo(src.data_ptr(), recv.data_ptr(), 3, stream.cuda_stream)  # single rank: no-op
+        stream.synchronize()
+        assert torch.equal(buf, torch.arange(6, dtype=torch.float64, device="cuda"))
+        assert torch.equal(out, src)
+        assert bool((recv == -1.0).all())
+        # the solver accepts it and solves exactly as without a communicator
+        ctx = stmg.Context(0)
+        sol = stmg.Solver(ctx, 3, 1, 1, n_steps=4, nu=1.0, nu1=2, nu2=2, rtol=1e-10)
+        lv = sol.finest
+        F = torch.from_numpy(oc.make_consistent(oc.seeded(4 * lv.size, 9), lv.n_slots, lv.n_scalar, lv.grid_x,
+                                                lv.n_pressure, 64, 3, 4)).cuda()
+        X0 = torch.zeros_like(F)
+        it0, _ = sol.solve_all_at_once(F, X0, 4)
+        sol.set_comm(comm)
+        X1 = torch.zeros_like(F)
+        it1, _ = sol.solve_all_at_once(F, X1, 4)
+        assert it0 == it1 and torch.equal(X0, X1)
+    finally:
+        dist.destroy_process_group()
