@@ -69,6 +69,42 @@ sign_refl(int i, int k) // C1(N-1-i, N-1-k) = -C1(i, k)
 #define VM_LC(a, k) (((k) > N1 - 1 - (k) && !((a) & 1)) ? -P.cLc[(a) * N1 + N1 - 1 - (k)] \
                                                            : P.cLc[(a) * N1 + ((k) > N1 - 1 - (k) ? N1 - 1 - (k) : (k))])
 
+// Shared-memory staging, one NODE ROW of the strip at a time (all input
+// slots, both components, the previous interval's slot-k velocity; with node
+// row 0 of a cell row also the cell row's pressure), double-buffered with
+// cp.async one node row ahead. Warp b stages input slot b with a fixed
+// lane -> node mapping (one address add per copy), so the contractions read
+// shared memory instead of waiting on global loads.
+template <int R, int S>
+struct RowStage
+{
+  static constexpr int p = R + 1, NPM = (R + 1) * (R + 2) / 2;
+  static constexpr int VW = 32 * p + 1;          // nodes of one strip row
+  static constexpr int NBUF = (2 * S + 2) * VW;  // one node row: S slots x 2 comps + v_prev x 2 comps
+  static constexpr int NPRE = S * 32 * NPM;      // pressure of one cell row
+  static constexpr size_t kBytes = sizeof(double) * (2 * NBUF + NPRE);
+  // Measured per instantiation (C2 r = 2 and C4 r = 1 on the B200): staging
+  // wins for r = 1 plain applications (C4 vmult 1.66 -> 1.26 ms) and loses
+  // for r = 2 (2.63 -> 2.80 ms) and for residuals (their late b loads stall
+  // in lockstep behind the per-row barriers), which keep direct loads.
+  template <bool RESID>
+  static constexpr bool on()
+  {
+#ifdef STMG_VM_NOSTAGE
+    return false;
+#else
+    return R == 1 && !RESID;
+#endif
+  }
+};
+
+__device__ __forceinline__ void
+vm_cp_async8(double *dst, const double *src)
+{
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(src));
+}
+
 template <int R, int S, bool RESID, bool RAW>
 __global__ void __launch_bounds__(32 * S, R == 2 ? 3 : 1)
 vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
@@ -117,9 +153,65 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
   for (int i = 0; i < N1; ++i)
     carx[i] = cary[i] = 0.0;
 
+  using RS = RowStage<R, S>;
+  constexpr bool kStaged = RS::template on<RESID>();
+  extern __shared__ __align__(16) double vm_smem[];
+  double *const pre_s = vm_smem + 2 * RS::NBUF;
+  const int X0 = (blockIdx.x * kStrip - 1) * p; // first node column of the strip
+  const int cx0 = blockIdx.x * kStrip - 1;
+  // gather node row l of cell row cyy (and, for l == 0, its pressure) into buffer buf
+  auto stage_row = [&](int cyy, int l, int buf) {
+    double *dst = vm_smem + buf * RS::NBUF;
+    const long long rowoff = static_cast<long long>(cyy * p + l) * gx + X0;
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp)
+#pragma unroll
+      for (int q = 0; q < (RS::VW + 31) / 32; ++q)
+        {
+          const int j = lane + 32 * q;
+          if (j < RS::VW && X0 + j >= 0 && X0 + j < gx)
+            {
+              vm_cp_async8(dst + (a * 2 + comp) * RS::VW + j, xn + a * mv + comp * nsc + rowoff + j);
+              if (a == 0 && vprev != nullptr)
+                vm_cp_async8(dst + (2 * S + comp) * RS::VW + j, vprev + comp * nsc + rowoff + j);
+            }
+        }
+    if (l == 0)
+      {
+        const double *src = xn + S * mv + a * mp + (static_cast<long long>(cyy) * P.nx + cx0) * NPM;
+#pragma unroll
+        for (int q = 0; q < NPM; ++q)
+          {
+            const int e = lane + 32 * q, c = e / NPM;
+            if (cx0 + c >= 0 && cx0 + c < P.nx)
+              vm_cp_async8(pre_s + a * 32 * NPM + e, src + e);
+          }
+      }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  // wait for node row (cy, l), then prefetch the next node row of the march
+  auto stage_sync = [&](int cy, int l) {
+    if constexpr (kStaged)
+      {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        const int s = (cy - cy_first) * N1 + l + 1;
+        if (l + 1 < N1)
+          stage_row(cy, l + 1, s & 1);
+        else if (cy + 1 < cy_end)
+          stage_row(cy + 1, 0, s & 1);
+      }
+  };
+  if constexpr (kStaged)
+    {
+      if (cy_first < cy_end)
+        stage_row(cy_first, 0, 0);
+    }
+
   for (int cy = cy_first; cy < cy_end; ++cy)
     {
       double Yx[N1][N1], Yy[N1][N1], Yp[NPM];
+      stage_sync(cy, 0);
 #pragma unroll
       for (int i = 0; i < N1; ++i)
 #pragma unroll
@@ -143,9 +235,10 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
               {
                 const double c = mt[bs];
                 const double *pp = xn + S * mv + bs * mp + cell * NPM;
+                const double *ps = pre_s + (bs * 32 + lane) * NPM;
 #pragma unroll
                 for (int m = 0; m < NPM; ++m)
-                  PM[m] = fma(c, __ldg(pp + m), PM[m]);
+                  PM[m] = fma(c, kStaged ? ps[m] : __ldg(pp + m), PM[m]);
               }
             // Yx(i,j) -= sum_b Qx(i,b) yLm(b,j),  Qx(i,b) = sum_{m: ay=b} xLc(ax,i) PM_m
             // Yy(i,j) -= sum_b Qy(i,b) yLc(b,j),  Qy(i,b) = sum_{m: ay=b} xLm(ax,i) PM_m
@@ -186,9 +279,16 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
               }
           }
 
-          // ---- velocity rows of the cell
+        }
+
+      // ---- velocity rows of the cell
 #pragma unroll
-          for (int l = 0; l < N1; ++l)
+      for (int l = 0; l < N1; ++l)
+        {
+          if (l > 0)
+            stage_sync(cy, l);
+          const double *sb = vm_smem + (((cy - cy_first) * N1 + l) & 1) * RS::NBUF;
+          if (active)
             {
               const int Y = cy * p + l;
               const bool yb = (Y == 0) || (Y == gy - 1);
@@ -201,11 +301,14 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
                   const bool bnd = !RAW && (yb || X == 0 || X == gx - 1);
                   const long long node = rowbase + k;
                   double ukx = 0.0, umx = 0.0, uky = 0.0, umy = 0.0;
+                  const int js = lane * p + k; // node column within the staged strip row
 #pragma unroll
                   for (int bs = 0; bs < S; ++bs)
                     {
-                      const double vx = bnd ? 0.0 : __ldg(xn + bs * mv + node);
-                      const double vy = bnd ? 0.0 : __ldg(xn + bs * mv + nsc + node);
+                      const double vx =
+                        bnd ? 0.0 : (kStaged ? sb[(bs * 2 + 0) * RS::VW + js] : __ldg(xn + bs * mv + node));
+                      const double vy =
+                        bnd ? 0.0 : (kStaged ? sb[(bs * 2 + 1) * RS::VW + js] : __ldg(xn + bs * mv + nsc + node));
                       ukx = fma(kt[bs], vx, ukx);
                       umx = fma(mt[bs], vx, umx);
                       uky = fma(kt[bs], vy, uky);
@@ -213,8 +316,8 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
                     }
                   if (vprev != nullptr)
                     {
-                      ukx = fma(-lva, __ldg(vprev + node), ukx);
-                      uky = fma(-lva, __ldg(vprev + nsc + node), uky);
+                      ukx = fma(-lva, kStaged ? sb[(2 * S + 0) * RS::VW + js] : __ldg(vprev + node), ukx);
+                      uky = fma(-lva, kStaged ? sb[(2 * S + 1) * RS::VW + js] : __ldg(vprev + nsc + node), uky);
                     }
                   UKx[k] = ukx;
                   UMx[k] = umx;
@@ -377,11 +480,18 @@ launch_rs(const LevelConsts &P, const double *x, const double *b, double *y, int
   const int rows = (P.ny + segs - 1) / segs;
   dim3 grid(strips, (P.ny + rows - 1) / rows, n_intervals);
   dim3 block(32 * S);
+  auto go = [&](auto kern, bool staged) {
+    const size_t smem = staged ? RowStage<R, S>::kBytes : 0;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, block, smem, stream>>>(P, x, b, y, xprev0, rows, coupled);
+  };
+  constexpr bool st_plain = RowStage<R, S>::template on<false>(), st_resid = RowStage<R, S>::template on<true>();
   switch (mode)
     {
-      case 0: vmult_kernel<R, S, false, false><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
-      case 1: vmult_kernel<R, S, true, false><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
-      default: vmult_kernel<R, S, false, true><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
+      case 0: go(vmult_kernel<R, S, false, false>, st_plain); break;
+      case 1: go(vmult_kernel<R, S, true, false>, st_resid); break;
+      default: go(vmult_kernel<R, S, false, true>, st_plain); break;
     }
   return cudaGetLastError();
 }
