@@ -15,9 +15,10 @@ ap.add_argument("--intervals", type=int, default=64)
 ap.add_argument("--r", type=int, default=2)
 ap.add_argument("--k", type=int, default=2)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--kind", type=int, default=0, help="0 cell Vanka, 1 vertex-star Vanka")
 a = ap.parse_args()
 ctx = stmg.Context(0)
-lvl = stmg.Level(ctx, a.nx, a.nx, a.r, a.k, 1.0 / a.intervals, 1.0, 1.0, stmg.SMOOTHER_CELL)
+lvl = stmg.Level(ctx, a.nx, a.nx, a.r, a.k, 1.0 / 64, 1.0, 1.0, a.kind)
 n = a.intervals * lvl.size
 x = torch.rand(n, dtype=torch.float64, device="cuda")
 b = torch.rand_like(x)
