@@ -105,8 +105,11 @@ vm_cp_async8(double *dst, const double *src)
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(src));
 }
 
+#ifndef STMG_VM_MINB1
+#define STMG_VM_MINB1 8 // r = 1: 128 registers (C4 residual 1.96 -> 1.50 ms; 96 and 80 registers spill)
+#endif
 template <int R, int S, bool RESID, bool RAW>
-__global__ void __launch_bounds__(32 * S, R == 2 ? 3 : 1)
+__global__ void __launch_bounds__(32 * S, R == 2 ? 3 : (R == 1 ? STMG_VM_MINB1 : 1))
 vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
              double *__restrict__ y, const double *__restrict__ xprev0, int rows_per_seg, int coupled)
 {
