@@ -1000,7 +1000,7 @@ struct stmg_solver
   // built-in problem (force assembled per step; boundary data by lifting).
   DevArray<double> fstep, lift, lifted;
   void
-  time_march(const double *F, double *X, int *iterations, int problem = -1)
+  time_march(const double *F, double *X, int *iterations, int problem = -1, const double *Lifts = nullptr)
   {
     stmg_level &L = fine();
     const long long n = L.spec.isz();
@@ -1009,7 +1009,7 @@ struct stmg_solver
     check(cudaMemsetAsync(vprev.p, 0, sizeof(double) * L.spec.mv(), ctx->stream), "memset");
     const double *zero = L.zero_vector(1);
     const double tau = L.spec.tau;
-    const bool inhomogeneous = problem == STMG_PROBLEM_CAVITY;
+    const bool inhomogeneous = problem == STMG_PROBLEM_CAVITY || Lifts != nullptr;
     if (problem >= 0)
       fstep.resize(n);
     if (inhomogeneous)
@@ -1034,9 +1034,16 @@ struct stmg_solver
         if (inhomogeneous)
           {
             // rhs -= A_raw lift (solver.cpp:251-262)
-            check(launch_lift_cavity(L.geom, L.spec.r, L.problem_tab(), t_start, tau, lift.p, 1, ctx->stream),
-                  "lift");
-            ctx->count();
+            if (Lifts)
+              check(cudaMemcpyAsync(lift.p, Lifts + step * n, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                    ctx->stream),
+                    "copy");
+            else
+              {
+                check(launch_lift_cavity(L.geom, L.spec.r, L.problem_tab(), t_start, tau, lift.p, 1, ctx->stream),
+                      "lift");
+                ctx->count();
+              }
             L.vmult(lift.p, nullptr, lifted.p, 1, nullptr, 0, 2);
             check(launch_axpy(n, -1.0, nullptr, 1.0, lifted.p, rhs.p, ctx->stream), "axpy");
             ctx->count();
@@ -1592,6 +1599,16 @@ stmg_time_march_problem(stmg_solver *s, int problem, double *X, int *iterations)
     if (problem != STMG_PROBLEM_MANUFACTURED && problem != STMG_PROBLEM_CAVITY)
       throw std::invalid_argument("stmg_time_march_problem: unknown problem");
     s->time_march(nullptr, X, iterations, problem);
+  });
+}
+
+int
+stmg_time_march_lifted(stmg_solver *s, const double *F, const double *lifts, double *X, int *iterations)
+{
+  return guarded([&] {
+    if (!lifts)
+      throw std::invalid_argument("stmg_time_march_lifted: lifts must not be NULL");
+    s->time_march(F, X, iterations, -1, lifts);
   });
 }
 

@@ -143,3 +143,35 @@ def test_time_march_problem_manufactured_equals_assembled_path(ctx, stmg):
     it2 = sol.time_march_problem(stmg.PROBLEM_MANUFACTURED, X2)
     assert it1 == it2
     assert float((X1 - X2).abs().max()) <= 1e-12 * float(X1.abs().max())
+
+
+def _radau_right(n):
+    """Right Gauss-Radau points on [-1, 1] (n points, +1 included): the
+    mirror of the left rule, whose points are the roots of P_{n-1} + P_n."""
+    c = np.zeros(n + 1)
+    c[n - 1] = 1.0
+    c[n] = 1.0
+    return np.sort(-np.real(np.polynomial.legendre.legroots(c)))
+
+
+def test_time_march_lifted_general_boundary_data(ctx, stmg):
+    """General Dirichlet data through per-step lift vectors: the cavity lid
+    written by the caller (set_boundary_values semantics, dof_space.cpp:71-81)
+    reproduces the built-in cavity time march."""
+    n_steps, k = 3, 2
+    sol = stmg.Solver(ctx, 2, 2, k, n_steps=n_steps, t_end=0.75, nu=0.1, rtol=1e-10)
+    lv = sol.finest
+    X_ref = torch.zeros(n_steps * lv.size, dtype=torch.float64, device="cuda")
+    it_ref = sol.time_march_problem(stmg.PROBLEM_CAVITY, X_ref)
+    gx, gy, mv = lv.grid_x, lv.n_scalar // lv.grid_x, lv.n_velocity
+    tau = 0.75 / n_steps
+    lifts = np.zeros(n_steps * lv.size)
+    for n in range(n_steps):
+        for a, xi in enumerate(_radau_right(k + 1)):
+            t = n * tau + 0.5 * tau * (xi + 1.0)
+            base = n * lv.size + a * mv + (gy - 1) * gx  # top grid row, component 0
+            lifts[base + 1: base + gx - 1] = math.sin(0.25 * math.pi * t)
+    X = torch.zeros_like(X_ref)
+    it = sol.time_march_lifted(None, dev(lifts), X)
+    assert it == it_ref
+    assert float((X - X_ref).abs().max()) <= 1e-12 * float(X_ref.abs().max())
