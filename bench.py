@@ -387,23 +387,41 @@ def main():
     halo_x = torch.zeros(mv, dtype=torch.float64, device="cuda")
     halo_u = torch.zeros(mv, dtype=torch.float64, device="cuda")
 
-    def exchange(src, dst):
-        """time-slab halo: slot-k velocity of my last interval -> rank+1."""
-        return timeslab.exchange_halo(src, dst, N, isz, mv, S, rank, world)
+    comm_stream = torch.cuda.Stream() if world > 1 else None
 
-    first = rank == 0
+    def coupled(apply, src, halo, dst, *extra):
+        """Time-slab application with the halo exchange overlapped: the NCCL
+        send/recv of the slot-k velocity runs on a side stream while
+        intervals 1..N-1 (local predecessor) are computed; interval 0 then
+        waits for the halo."""
+        if world == 1:
+            apply(src, dst, N, None, *extra)
+            return
+        main = torch.cuda.current_stream()
+        comm_stream.wait_stream(main)
+        with torch.cuda.stream(comm_stream):
+            h = timeslab.exchange_halo(src, halo, N, isz, mv, S, rank, world)
+        if N > 1:
+            apply(src[isz:], dst[isz:], N - 1, src[(S - 1) * mv:S * mv], *[e[isz:] for e in extra])
+        main.wait_stream(comm_stream)
+        apply(src[:isz], dst[:isz], 1, h, *[e[:isz] for e in extra])
+
+    def vmult(src, dst, n, prev):
+        lvl.vmult(src, dst, n, prev)
+
+    def residual(src, dst, n, prev, bb):
+        lvl.residual(bb, src, dst, n, prev, coupled=True)
+
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t_vmult, t_resid, t_vanka = [], [], []
 
     def step(record):
-        hx = exchange(x, halo_x)
         if record:
             ev[0].record()
-        lvl.vmult(x, y, N, hx)
+        coupled(vmult, x, halo_x, y)
         if record:
             ev[1].record()
-        hu = exchange(u, halo_u)
-        lvl.residual(b, u, res, N, hu, coupled=True)
+        coupled(residual, u, halo_u, res, b)
         if record:
             ev[2].record()
         lvl.vanka_update(res, u, CONFIG["omega"], N)

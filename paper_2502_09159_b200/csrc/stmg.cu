@@ -543,20 +543,41 @@ struct stmg_solver
     return has_comm ? comm.world : 1;
   }
 
-  /// Slot-k velocity of the previous rank's last interval of x at level l
-  /// (nullptr on the first rank: zero initial data / folded into the RHS).
-  const double *
-  halo(int l, const double *x, int nI)
+  // Coupled application on the slab at level l: y = A x (mode 0) or
+  // y = b - A x (mode 1), A with the jump coupling (Eq. GloSys). With a
+  // communicator the halo (slot-k velocity of the previous rank's last
+  // interval) travels on a side stream while intervals 1..nI-1, whose
+  // predecessor is local, are computed; interval 0 waits for the halo.
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_h = nullptr;
+  void
+  coupled_vmult(int l, const double *x, const double *b, double *y, int nI, int mode)
   {
-    if (world() == 1)
-      return nullptr;
     stmg_level &L = *levels[l]->level;
+    if (world() == 1)
+      {
+        L.vmult(x, b, y, nI, nullptr, 1, mode);
+        return;
+      }
+    if (!comm_stream)
+      {
+        check(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking), "stream");
+        check(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming), "event");
+      }
+    const long long isz = L.spec.isz(), mv = L.spec.mv();
     DevArray<double> &h = levels[l]->halo;
-    h.resize(L.spec.mv());
-    const double *send = x + static_cast<long long>(nI - 1) * L.spec.isz() + static_cast<long long>(L.spec.S() - 1) * L.spec.mv();
-    if (comm.exchange_halo(comm.user, send, h.p, L.spec.mv(), ctx->stream) != 0)
+    h.resize(mv);
+    check(cudaEventRecord(ev_x, ctx->stream), "event"); // x final, previous use of h done
+    check(cudaStreamWaitEvent(comm_stream, ev_x, 0), "wait");
+    const double *send = x + (nI - 1) * isz + (L.spec.S() - 1) * mv;
+    if (comm.exchange_halo(comm.user, send, h.p, mv, comm_stream) != 0)
       throw std::runtime_error("comm: exchange_halo failed");
-    return rank() == 0 ? nullptr : h.p;
+    check(cudaEventRecord(ev_h, comm_stream), "event");
+    if (nI > 1) // interior intervals: predecessor is interval 0 of this slab
+      L.vmult(x + isz, b ? b + isz : nullptr, y + isz, nI - 1, x + (L.spec.S() - 1) * mv, 1, mode);
+    check(cudaStreamWaitEvent(ctx->stream, ev_h, 0), "wait");
+    L.vmult(x, b, y, 1, rank() == 0 ? nullptr : h.p, 1, mode);
   }
 
   void
@@ -726,13 +747,24 @@ struct stmg_solver
     const long long isz = L.spec.isz() * nI;
     S.r.resize(isz);
     check(cudaMemsetAsync(x_v, 0, sizeof(double) * isz, ctx->stream), "memset");
+    // smoothing step: residual (coupled in all-at-once mode), then Vanka
+    const auto smooth = [&](bool first) {
+      if (first) // x = 0 on every rank before the first sweep: b - A 0 = b exactly
+        L.smooth_step(b_v, x_v, omega, nI, nullptr, 0, S.r.p, true);
+      else if (aao)
+        {
+          coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
+          L.vanka(S.r.p, x_v, nI, omega);
+        }
+      else
+        L.smooth_step(b_v, x_v, omega, nI, nullptr, 0, S.r.p);
+    };
     for (int s = 0; s < nu1; ++s)
-      {
-        // x = 0 on every rank before the first sweep: b - A 0 = b exactly
-        const bool coupled = aao && s > 0;
-        L.smooth_step(b_v, x_v, omega, nI, coupled ? halo(l, x_v, nI) : nullptr, coupled ? 1 : 0, S.r.p, s == 0);
-      }
-    L.vmult(x_v, b_v, S.r.p, nI, aao ? halo(l, x_v, nI) : nullptr, aao ? 1 : 0, 1);
+      smooth(s == 0);
+    if (aao)
+      coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
+    else
+      L.vmult(x_v, b_v, S.r.p, nI, nullptr, 0, 1);
     SolverLevel &C = *levels[l - 1];
     const long long csz = C.level->spec.isz() * nI;
     C.b.resize(csz);
@@ -741,7 +773,7 @@ struct stmg_solver
     cycle(l - 1, C.b.p, C.x.p, nI, aao);
     prolongate_correction(l, C.x.p, x_v, project_pressure, true, nI);
     for (int s = 0; s < nu2; ++s)
-      L.smooth_step(b_v, x_v, omega, nI, aao ? halo(l, x_v, nI) : nullptr, aao ? 1 : 0, S.r.p);
+      smooth(false);
   }
 
   void
@@ -838,6 +870,12 @@ struct stmg_solver
     drop_graph();
     if (vc_stream)
       cudaStreamDestroy(vc_stream);
+    if (comm_stream)
+      cudaStreamDestroy(comm_stream);
+    if (ev_x)
+      cudaEventDestroy(ev_x);
+    if (ev_h)
+      cudaEventDestroy(ev_h);
   }
 
   double
@@ -900,7 +938,10 @@ struct stmg_solver
           {
             DevArray<double> &zj = basis(Z, j, n);
             precondition(V[j]->p, zj.p, nI, aao);
-            L.vmult(zj.p, nullptr, w.p, nI, aao ? halo(top, zj.p, nI) : nullptr, aao ? 1 : 0, 0);
+            if (aao)
+              coupled_vmult(top, zj.p, nullptr, w.p, nI, 0);
+            else
+              L.vmult(zj.p, nullptr, w.p, nI, nullptr, 0, 0);
             // modified Gram-Schmidt with device-resident coefficients
             for (int i = 0; i <= j; ++i)
               {
