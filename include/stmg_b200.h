@@ -110,7 +110,7 @@ int stmg_vanka_update(stmg_level *level, const double *r, double *u, double omeg
 
 /* Host-buffer variants of stmg_vmult / stmg_smooth_step: copy in, run,
  * copy out, synchronise (the end-to-end path a CPU caller binds). Pipelined
- * over 8-interval chunks on separate H2D / D2H streams; pinned host memory
+ * over 4-interval chunks on separate H2D / D2H streams; pinned host memory
  * lets the copies overlap the kernels. */
 int stmg_vmult_host(stmg_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);
 int stmg_smooth_step_host(stmg_level *level, const double *b, double *u, double omega, int n_intervals,
