@@ -182,12 +182,18 @@ int stmg_time_march_host(stmg_solver *solver, const double *F, double *X, int *i
  * by the reference's lift: rhs -= A_raw lift, solve, x += lift
  * (solver.cpp:251-283). Zero initial velocity. */
 int stmg_time_march_problem(stmg_solver *solver, int problem, double *X, int *iterations);
-/* time_march with general inhomogeneous Dirichlet data: lifts holds n_steps
- * interval vectors with the boundary values g(x, y, t_a) of every slot on the
- * constrained velocity nodes and zero elsewhere (set_boundary_values,
- * dof_space.cpp:71-81). Step n solves with rhs -= A_raw lift_n and returns
- * x + lift_n (solver.cpp:251-283). F (load vectors) may be NULL. */
-int stmg_time_march_lifted(stmg_solver *solver, const double *F, const double *lifts, double *X, int *iterations);
+/* time_march with all of the reference's problem data as vectors; every
+ * pointer may be NULL:
+ *  - F: per-step load vectors (n_steps intervals);
+ *  - lifts: general inhomogeneous Dirichlet data. n_steps interval vectors
+ *    hold the boundary values g(x, y, t_a) of every slot on the constrained
+ *    velocity nodes and zero elsewhere (set_boundary_values,
+ *    dof_space.cpp:71-81). Step n solves with rhs -= A_raw lift_n and
+ *    returns x + lift_n (solver.cpp:251-283);
+ *  - v_init: the initial velocity at the nodes (M^v doubles,
+ *    solver.cpp:229-236). */
+int stmg_time_march_ex(stmg_solver *solver, const double *F, const double *lifts, const double *v_init, double *X,
+                       int *iterations);
 
 /* ------------------------------------------------------------ all-at-once
  * The global space-time system of Eq. GloSys: the block

@@ -77,7 +77,7 @@ _SIGNATURES = {
     "stmg_gmres": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_double), _c_int],
                    _c_int),
     "stmg_time_march": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
-    "stmg_time_march_lifted": ([_c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
+    "stmg_time_march_ex": ([_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_time_march_problem": ([_c_void_p, _c_int, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_time_march_host": ([_c_void_p, _c_void_p, _c_void_p, ctypes.POINTER(_c_int)], _c_int),
     "stmg_assemble_rhs": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int], _c_int),
@@ -337,10 +337,10 @@ class Solver:
         _check(load_library().stmg_time_march_problem(self._h, problem, _ptr(X), iters))
         return [int(v) for v in iters]
 
-    def time_march_lifted(self, F, lifts, X):
-        """time_march with inhomogeneous Dirichlet data given as per-step lift vectors (F may be None)."""
+    def time_march_ex(self, X, F=None, lifts=None, v_init=None):
+        """time_march with load vectors, per-step Dirichlet lift vectors and an initial velocity (all optional)."""
         iters = (ctypes.c_int * self.n_steps)()
-        _check(load_library().stmg_time_march_lifted(self._h, _ptr(F), _ptr(lifts), _ptr(X), iters))
+        _check(load_library().stmg_time_march_ex(self._h, _ptr(F), _ptr(lifts), _ptr(v_init), _ptr(X), iters))
         return [int(v) for v in iters]
 
     def time_march_host(self, F, X):

@@ -1041,13 +1041,18 @@ struct stmg_solver
   // built-in problem (force assembled per step; boundary data by lifting).
   DevArray<double> fstep, lift, lifted;
   void
-  time_march(const double *F, double *X, int *iterations, int problem = -1, const double *Lifts = nullptr)
+  time_march(const double *F, double *X, int *iterations, int problem = -1, const double *Lifts = nullptr,
+             const double *v_init = nullptr)
   {
     stmg_level &L = fine();
     const long long n = L.spec.isz();
     rhs.resize(n);
     vprev.resize(L.spec.mv());
-    check(cudaMemsetAsync(vprev.p, 0, sizeof(double) * L.spec.mv(), ctx->stream), "memset");
+    if (v_init) // initial velocity at the nodes (solver.cpp:229-236)
+      check(cudaMemcpyAsync(vprev.p, v_init, sizeof(double) * L.spec.mv(), cudaMemcpyDeviceToDevice, ctx->stream),
+            "copy");
+    else
+      check(cudaMemsetAsync(vprev.p, 0, sizeof(double) * L.spec.mv(), ctx->stream), "memset");
     const double *zero = L.zero_vector(1);
     const double tau = L.spec.tau;
     const bool inhomogeneous = problem == STMG_PROBLEM_CAVITY || Lifts != nullptr;
@@ -1647,13 +1652,10 @@ stmg_time_march_problem(stmg_solver *s, int problem, double *X, int *iterations)
 }
 
 int
-stmg_time_march_lifted(stmg_solver *s, const double *F, const double *lifts, double *X, int *iterations)
+stmg_time_march_ex(stmg_solver *s, const double *F, const double *lifts, const double *v_init, double *X,
+                   int *iterations)
 {
-  return guarded([&] {
-    if (!lifts)
-      throw std::invalid_argument("stmg_time_march_lifted: lifts must not be NULL");
-    s->time_march(F, X, iterations, -1, lifts);
-  });
+  return guarded([&] { s->time_march(F, X, iterations, -1, lifts, v_init); });
 }
 
 int

@@ -172,6 +172,26 @@ def test_time_march_lifted_general_boundary_data(ctx, stmg):
             base = n * lv.size + a * mv + (gy - 1) * gx  # top grid row, component 0
             lifts[base + 1: base + gx - 1] = math.sin(0.25 * math.pi * t)
     X = torch.zeros_like(X_ref)
-    it = sol.time_march_lifted(None, dev(lifts), X)
+    it = sol.time_march_ex(X, lifts=dev(lifts))
     assert it == it_ref
     assert float((X - X_ref).abs().max()) <= 1e-12 * float(X_ref.abs().max())
+
+
+def test_time_march_initial_velocity_is_the_first_coupling(ctx, stmg):
+    """An initial velocity v0 (solver.cpp:229-236) enters step 1 through the
+    coupling: time_march_ex(v_init = v0) equals time_march with the load
+    F_1 += coupling_rhs(v0) and zero initial data."""
+    n_steps = 3
+    sol = stmg.Solver(ctx, 3, 1, 1, n_steps=n_steps, nu=0.5, rtol=1e-11)
+    lv = sol.finest
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    v0 = torch.rand(lv.n_velocity, dtype=torch.float64, device="cuda", generator=g)
+    X1 = torch.zeros(n_steps * lv.size, dtype=torch.float64, device="cuda")
+    it1 = sol.time_march_ex(X1, v_init=v0)
+    F = torch.zeros_like(X1)
+    lv.coupling_rhs(v0, F[:lv.size])
+    X2 = torch.zeros_like(X1)
+    it2 = sol.time_march(F, X2)
+    assert it1 == it2
+    assert float((X1 - X2).abs().max()) <= 1e-12 * float(X2.abs().max())
