@@ -68,9 +68,10 @@ int64_t stmg_ctx_launch_count(const stmg_ctx *ctx);
 int stmg_level_create(stmg_ctx *ctx, int nx, int ny, int r, int k, double tau, double nu, double gamma,
                       int smoother_kind, stmg_level **out);
 int stmg_level_destroy(stmg_level *level);
-/* out[0..7] = n_slots, M^v, M^p, interval size, n_scalar, grid_x,
+/* out[0..9] = n_slots, M^v, M^p, interval size, n_scalar, grid_x,
  * n_patch_classes, sum over patches of n_T^2 (total_matrix_elements,
- * vanka.cpp:235-243). */
+ * vanka.cpp:235-243), 1 if the smoother applies the time-diagonalised
+ * (factored) patch inverses, and their multiply-adds per interval. */
 int stmg_level_sizes(const stmg_level *level, int64_t *out);
 
 /* y_n = D x_n for each of n_intervals independent intervals
@@ -245,8 +246,11 @@ int stmg_solve_all_at_once(stmg_solver *solver, const double *F, double *X, int 
  * (harness.cpp:26-42, hierarchy.cpp:9-97) in the stmg_solver_info layout.
  * stmg_patch_info: Vanka patches of one level: out[0] n_patches, out[1]
  * n_classes, out[2] sum n_T^2, out[3] n_colours, out[4+c] n_T of class c
- * (c < 60). If inverse_out is non-NULL, the dense (pseudo-)inverse of class
- * `class_index` (n_T x n_T, row-major) is written there. */
+ * (c < 56), out[60] 1 if the level uses the factored (time-diagonalised)
+ * patch inverses, out[61] their padded spatial size, out[62] their
+ * multiply-adds per interval (middle blocks + temporal transforms). out must
+ * hold 64 entries. If inverse_out is non-NULL, the dense (pseudo-)inverse of
+ * class `class_index` (n_T x n_T, row-major) is written there. */
 int stmg_plan_levels(int refinements, int r, int k, int n_steps, double t_end, int h_only, int64_t *out);
 int stmg_patch_info(int nx, int ny, int r, int k, double tau, double nu, double gamma, int smoother_kind,
                     int64_t *out, double *inverse_out, int class_index);

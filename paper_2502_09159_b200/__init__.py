@@ -205,10 +205,12 @@ class Level:
             _check(lib.stmg_level_create(ctx.handle, nx, ny, r, k, tau, nu, gamma, smoother, ctypes.byref(h)))
             self._h = h
             self._owned = True
-        out = (ctypes.c_int64 * 8)()
+        out = (ctypes.c_int64 * 10)()
         _check(lib.stmg_level_sizes(self._h, out))
         (self.n_slots, self.n_velocity, self.n_pressure, self.size, self.n_scalar, self.grid_x,
-         self.n_patch_classes, self.total_matrix_elements) = [int(v) for v in out]
+         self.n_patch_classes, self.total_matrix_elements) = [int(v) for v in out[:8]]
+        self.factored = bool(out[8])           # time-diagonalised Vanka inverses in use
+        self.factored_matrix_elements = int(out[9])
 
     # -- operator
     def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
@@ -403,7 +405,8 @@ def patch_info(nx: int, ny: int, r: int, k: int, tau: float, nu: float, gamma: f
     _check(load_library().stmg_patch_info(nx, ny, r, k, tau, nu, gamma, smoother, out, None, 0))
     n_classes = int(out[1])
     return dict(n_patches=int(out[0]), n_classes=n_classes, sum_nt2=int(out[2]), n_colours=int(out[3]),
-                class_sizes=[int(out[4 + i]) for i in range(min(n_classes, 60))])
+                class_sizes=[int(out[4 + i]) for i in range(min(n_classes, 56))], factored=bool(out[60]),
+                n_sp=int(out[61]), factored_macs=int(out[62]))
 
 
 def exported_symbols() -> Sequence[str]:

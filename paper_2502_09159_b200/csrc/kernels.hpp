@@ -42,6 +42,18 @@ struct DevPatchClass
   const long long *rel;  // n_t offsets from the velocity / pressure anchor
   const double *weight;  // n_t valence weights
   const double *inverse; // n_t x n_t row-major
+  // factored form (vanka_fac_kernel): spatial dofs n_s (n_vs velocity) and
+  // the middle-block inverses, (S * n_sp) x (2 * n_sp) block-local columns
+  int n_s, n_vs;
+  const double *fac_inv;
+};
+
+/// Time-diagonalised Vanka (setup.hpp TemporalEigen): per level.
+struct FacParams
+{
+  int S, nsp;
+  double V[kMaxS * kMaxS], W[kMaxS * kMaxS]; // row-major
+  int kbase[16], ksteps[16];                 // per warp (8-row tile): K range of its block
 };
 
 /// One Vanka block's work item: a run of same-class patches of one colour.
@@ -69,9 +81,14 @@ cudaError_t launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles
                             const long long *pa, const int *tile_ptr, int n_blocks, int ng_full,
                             int max_nt, const double *r, double *u, long long isz, int n_intervals, double omega,
                             cudaStream_t stream);
+cudaError_t launch_vanka_fac(const DevPatchClass *classes, const VankaTile *tiles, const long long *va,
+                             const long long *pa, const int *tile_ptr, int n_blocks, int ng_full, const FacParams &F,
+                             const double *r, double *u, long long isz, int n_intervals, double omega,
+                             cudaStream_t stream);
 int vanka_tc_cols();
 int vanka_tc_max_tiles();
 int vanka_tc_stage(); // tiles per barrier stage
+bool vanka_fac_supported(int S, int nsp); // instantiated (S, n_sp) shapes of vanka_fac_kernel
 
 cudaError_t launch_vmult(int r, int S, const LevelConsts &P, const double *x, const double *b, double *y,
                          int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t stream);

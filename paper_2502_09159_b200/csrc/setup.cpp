@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <limits>
 #include <map>
 #include <stdexcept>
@@ -218,6 +219,241 @@ time_tables(int k, double tau)
         t.Kt[a * s + b] = kd + t.lv[b] * t.lv[a];
       }
   return t;
+}
+
+// ---------------------------------------------------------------- temporal eigen
+namespace
+{
+  using cplx = std::complex<double>;
+
+  // null vector of the complex S x S matrix A (rank S-1), full pivoting
+  std::vector<cplx>
+  null_vector(std::vector<cplx> A, int n)
+  {
+    std::vector<int> colp(n);
+    for (int j = 0; j < n; ++j)
+      colp[j] = j;
+    int rank = 0;
+    for (int k = 0; k < n; ++k)
+      {
+        int pi = -1, pj = -1;
+        double best = 0.0;
+        for (int i = k; i < n; ++i)
+          for (int j = k; j < n; ++j)
+            if (std::abs(A[i * n + j]) > best)
+              {
+                best = std::abs(A[i * n + j]);
+                pi = i;
+                pj = j;
+              }
+        if (best < 1e-11)
+          break;
+        for (int j = 0; j < n; ++j)
+          std::swap(A[k * n + j], A[pi * n + j]);
+        for (int i = 0; i < n; ++i)
+          std::swap(A[i * n + k], A[i * n + pj]);
+        std::swap(colp[k], colp[pj]);
+        for (int i = k + 1; i < n; ++i)
+          {
+            const cplx f = A[i * n + k] / A[k * n + k];
+            for (int j = k; j < n; ++j)
+              A[i * n + j] -= f * A[k * n + j];
+          }
+        ++rank;
+      }
+    // back substitution with the free variables rank..n-1 = (1, 0, ...)
+    std::vector<cplx> y(n, 0.0);
+    if (rank < n)
+      y[rank] = 1.0;
+    for (int k = rank - 1; k >= 0; --k)
+      {
+        cplx t = 0.0;
+        for (int j = k + 1; j < n; ++j)
+          t += A[k * n + j] * y[j];
+        y[k] = -t / A[k * n + k];
+      }
+    std::vector<cplx> v(n);
+    for (int j = 0; j < n; ++j)
+      v[colp[j]] = y[j];
+    return v;
+  }
+} // namespace
+
+TemporalEigen
+temporal_eigen(const TimeTables &T)
+{
+  TemporalEigen e;
+  const int S = T.k + 1;
+  e.S = S;
+  // Q = M_t^{-1} K_t
+  std::vector<double> Minv = T.Mt;
+  double rc = 0.0;
+  if (!invert_dense(Minv, S, &rc))
+    return e;
+  std::vector<double> Q(S * S, 0.0);
+  for (int i = 0; i < S; ++i)
+    for (int j = 0; j < S; ++j)
+      for (int l = 0; l < S; ++l)
+        Q[i * S + j] += Minv[i * S + l] * T.Kt[l * S + j];
+  // characteristic polynomial (Faddeev-LeVerrier): p(x) = sum_j c[j] x^j
+  std::vector<double> c(S + 1, 0.0), Mk(S * S, 0.0), QM(S * S);
+  c[S] = 1.0;
+  for (int k = 1; k <= S; ++k)
+    {
+      for (int i = 0; i < S; ++i)
+        for (int j = 0; j < S; ++j)
+          {
+            double t = 0.0;
+            for (int l = 0; l < S; ++l)
+              t += Q[i * S + l] * Mk[l * S + j];
+            QM[i * S + j] = t;
+          }
+      for (int i = 0; i < S; ++i)
+        for (int j = 0; j < S; ++j)
+          Mk[i * S + j] = QM[i * S + j] + (i == j ? c[S - k + 1] : 0.0);
+      double tr = 0.0;
+      for (int i = 0; i < S; ++i)
+        for (int l = 0; l < S; ++l)
+          tr += Q[i * S + l] * Mk[l * S + i];
+      c[S - k] = -tr / k;
+    }
+  const auto poly = [&](cplx x) {
+    cplx r = c[S];
+    for (int j = S - 1; j >= 0; --j)
+      r = r * x + c[j];
+    return r;
+  };
+  const auto dpoly = [&](cplx x) {
+    cplx r = S * c[S];
+    for (int j = S - 1; j >= 1; --j)
+      r = r * x + static_cast<double>(j) * c[j];
+    return r;
+  };
+  // roots: Durand-Kerner, then Newton polishing
+  double scale = 0.0;
+  for (int j = 0; j < S; ++j)
+    scale = std::max(scale, std::abs(c[j]));
+  std::vector<cplx> z(S);
+  for (int i = 0; i < S; ++i)
+    z[i] = std::pow(cplx(0.4, 0.9), i) * (1.0 + scale);
+  for (int it = 0; it < 2000; ++it)
+    {
+      double moved = 0.0;
+      for (int i = 0; i < S; ++i)
+        {
+          cplx den = 1.0;
+          for (int j = 0; j < S; ++j)
+            if (j != i)
+              den *= z[i] - z[j];
+          const cplx dz = poly(z[i]) / den;
+          z[i] -= dz;
+          moved = std::max(moved, std::abs(dz));
+        }
+      if (moved < 1e-15 * (1.0 + scale))
+        break;
+    }
+  for (auto &x : z)
+    for (int it = 0; it < 3; ++it)
+      {
+        const cplx d = dpoly(x);
+        if (std::abs(d) > 0.0)
+          x -= poly(x) / d;
+      }
+  // group: real roots, and pairs (one representative with Im > 0)
+  std::vector<cplx> reps;
+  std::vector<bool> used(S, false);
+  for (int i = 0; i < S; ++i)
+    {
+      if (used[i])
+        continue;
+      used[i] = true;
+      if (std::abs(z[i].imag()) <= 1e-9 * (1.0 + std::abs(z[i])))
+        {
+          reps.push_back(cplx(z[i].real(), 0.0));
+          continue;
+        }
+      int partner = -1;
+      for (int j = 0; j < S; ++j)
+        if (!used[j] && std::abs(z[j] - std::conj(z[i])) <= 1e-7 * (1.0 + std::abs(z[i])))
+          partner = j;
+      if (partner < 0)
+        return e; // not a real matrix spectrum: leave e.ok = false
+      used[partner] = true;
+      reps.push_back(z[i].imag() > 0 ? z[i] : std::conj(z[i]));
+    }
+  e.V.assign(S * S, 0.0);
+  int col = 0;
+  for (const cplx lam : reps)
+    {
+      std::vector<cplx> A(S * S);
+      for (int i = 0; i < S; ++i)
+        for (int j = 0; j < S; ++j)
+          A[i * S + j] = Q[i * S + j] - (i == j ? lam : cplx(0.0));
+      std::vector<cplx> v = null_vector(A, S);
+      double nrm = 0.0;
+      for (const auto &x : v)
+        nrm = std::max(nrm, std::abs(x));
+      for (auto &x : v)
+        x /= nrm;
+      e.blk_c0.push_back(col);
+      e.alpha.push_back(lam.real());
+      if (lam.imag() == 0.0)
+        {
+          e.blk_sz.push_back(1);
+          e.beta.push_back(0.0);
+          for (int i = 0; i < S; ++i)
+            e.V[i * S + col] = v[i].real();
+          col += 1;
+        }
+      else
+        {
+          e.blk_sz.push_back(2);
+          e.beta.push_back(lam.imag());
+          for (int i = 0; i < S; ++i)
+            {
+              e.V[i * S + col] = v[i].real();
+              e.V[i * S + col + 1] = v[i].imag();
+            }
+          col += 2;
+        }
+    }
+  if (col != S)
+    return e;
+  // verify Q V = V Lambda, then W = V^{-1} M_t^{-1}
+  double res = 0.0, qn = 0.0;
+  for (int i = 0; i < S * S; ++i)
+    qn = std::max(qn, std::abs(Q[i]));
+  for (size_t b = 0; b < e.blk_c0.size(); ++b)
+    {
+      const int c0 = e.blk_c0[b];
+      for (int i = 0; i < S; ++i)
+        for (int cc = 0; cc < e.blk_sz[b]; ++cc)
+          {
+            double qv = 0.0;
+            for (int l = 0; l < S; ++l)
+              qv += Q[i * S + l] * e.V[l * S + c0 + cc];
+            double vl;
+            if (e.blk_sz[b] == 1)
+              vl = e.V[i * S + c0] * e.alpha[b];
+            else if (cc == 0) // Q x = alpha x - beta y
+              vl = e.alpha[b] * e.V[i * S + c0] - e.beta[b] * e.V[i * S + c0 + 1];
+            else // Q y = beta x + alpha y
+              vl = e.beta[b] * e.V[i * S + c0] + e.alpha[b] * e.V[i * S + c0 + 1];
+            res = std::max(res, std::abs(qv - vl));
+          }
+    }
+  if (res > 1e-10 * (1.0 + qn))
+    return e;
+  std::vector<double> Vinv = e.V;
+  if (!invert_dense(Vinv, S, &rc) || rc < 1e-10)
+    return e;
+  e.W.assign(S * S, 0.0);
+  for (int i = 0; i < S; ++i)
+    for (int j = 0; j < S; ++j)
+      for (int l = 0; l < S; ++l)
+        e.W[i * S + j] += Vinv[i * S + l] * Minv[l * S + j];
+  e.ok = true;
+  return e;
 }
 
 Factors1D
@@ -634,7 +870,8 @@ namespace
   }
 
   PatchClass
-  build_class(const LevelSpec &L, PatchKind kind, int ax, int ay, const CellMatrices &E, const TimeTables &T)
+  build_class(const LevelSpec &L, PatchKind kind, int ax, int ay, const CellMatrices &E, const TimeTables &T,
+              bool invert = true)
   {
     const PatchGeom g = patch_geometry(L, kind, ax, ay);
     PatchClass pc;
@@ -736,6 +973,52 @@ namespace
                 }
             }
       }
+    if (!invert)
+      {
+        pc.inverse = std::move(A); // the assembled matrix itself
+        return pc;
+      }
+    if (L.k >= 2)
+      {
+        // spatial factors: the same assembly on a single-slot copy with unit
+        // temporal coefficients, (K, M) = (1, 0) -> M_s and (0, 1) -> A_s
+        LevelSpec L0 = L;
+        L0.k = 0;
+        TimeTables t0;
+        t0.k = 0;
+        t0.tau = L.tau;
+        t0.Kt = {1.0};
+        t0.Mt = {0.0};
+        PatchClass ms = build_class(L0, kind, ax, ay, E, t0, false);
+        t0.Kt = {0.0};
+        t0.Mt = {1.0};
+        PatchClass as = build_class(L0, kind, ax, ay, E, t0, false);
+        pc.n_s = ms.n_t;
+        pc.n_vs = ms.n_vel;
+        pc.Ms = std::move(ms.inverse);
+        pc.As = std::move(as.inverse);
+        // A_T must equal K_t (x) M_s + M_t (x) A_s in the patch ordering
+        // (velocity of all slots, then pressure of all slots)
+        const int ns = pc.n_s, nvs = pc.n_vs, nps = ns - nvs;
+        const auto prow = [&](int a, int j) { return j < nvs ? a * nvs + j : S * nvs + a * nps + (j - nvs); };
+        double err = 0.0, amax = 0.0;
+        for (int a = 0; a < S; ++a)
+          for (int b = 0; b < S; ++b)
+            for (int i = 0; i < ns; ++i)
+              for (int j = 0; j < ns; ++j)
+                {
+                  const double want = T.Kt[a * S + b] * pc.Ms[i * ns + j] + T.Mt[a * S + b] * pc.As[i * ns + j];
+                  const double got = A[static_cast<size_t>(prow(a, i)) * pc.n_t + prow(b, j)];
+                  err = std::max(err, std::abs(want - got));
+                  amax = std::max(amax, std::abs(got));
+                }
+        if (pc.n_t != S * ns || err > 1e-12 * amax)
+          {
+            pc.n_s = 0; // no Kronecker structure: dense path only
+            pc.Ms.clear();
+            pc.As.clear();
+          }
+      }
     std::vector<double> inv = A;
     double rc = 0.0;
     const bool ok = invert_dense(inv, pc.n_t, &rc);
@@ -782,6 +1065,120 @@ build_patches(const LevelSpec &L, PatchKind kind)
       }
   for (auto &col : ps.colours)
     std::stable_sort(col.begin(), col.end(), [](const auto &a, const auto &b) { return a.cls < b.cls; });
+
+  // Factored inverses (k >= 2, every class regular with Kronecker structure):
+  // A_T^{-1} = (V (x) I) blockdiag(B_b^{-1}) (W (x) I), middle blocks
+  //   real eigenvalue:  B = alpha M_s + A_s                      (n_s)
+  //   pair:             B = [[alpha M_s + A_s, beta M_s],
+  //                          [-beta M_s, alpha M_s + A_s]]      (2 n_s)
+  bool all_ok = L.k >= 2 && !ps.classes.empty();
+  int max_ns = 0;
+  for (const auto &pc : ps.classes)
+    {
+      all_ok = all_ok && !pc.singular && pc.n_s > 0;
+      max_ns = std::max(max_ns, pc.n_s);
+    }
+  if (all_ok)
+    {
+      ps.eig = temporal_eigen(T);
+      const int S = L.S(), nsp = (max_ns + 7) / 8 * 8;
+      if (ps.eig.ok && S * nsp <= 128)
+        {
+          ps.n_sp = nsp;
+          bool inv_ok = true;
+          for (auto &pc : ps.classes)
+            {
+              const int ns = pc.n_s;
+              pc.fac_inv.assign(static_cast<size_t>(S * nsp) * 2 * nsp, 0.0);
+              for (size_t b = 0; b < ps.eig.blk_c0.size() && inv_ok; ++b)
+                {
+                  const int c0 = ps.eig.blk_c0[b], sz = ps.eig.blk_sz[b], m = sz * ns;
+                  const double al = ps.eig.alpha[b], be = ps.eig.beta[b];
+                  std::vector<double> B(static_cast<size_t>(m) * m, 0.0);
+                  for (int bi = 0; bi < sz; ++bi)
+                    for (int bj = 0; bj < sz; ++bj)
+                      {
+                        // block (bi, bj): diagonal alpha Ms + As; off-diagonal +-beta Ms
+                        const double cm = bi == bj ? al : (bi == 0 ? be : -be), ca = bi == bj ? 1.0 : 0.0;
+                        for (int i = 0; i < ns; ++i)
+                          for (int j = 0; j < ns; ++j)
+                            B[static_cast<size_t>(bi * ns + i) * m + bj * ns + j] =
+                              cm * pc.Ms[i * ns + j] + ca * pc.As[i * ns + j];
+                      }
+                  double rc = 0.0;
+                  if (!invert_dense(B, m, &rc) || rc < 1e-14)
+                    {
+                      inv_ok = false;
+                      break;
+                    }
+                  for (int bi = 0; bi < sz; ++bi)
+                    for (int i = 0; i < ns; ++i)
+                      for (int bj = 0; bj < sz; ++bj)
+                        for (int j = 0; j < ns; ++j)
+                          pc.fac_inv[static_cast<size_t>((c0 + bi) * nsp + i) * 2 * nsp + bj * nsp + j] =
+                            B[static_cast<size_t>(bi * ns + i) * m + bj * ns + j];
+                }
+              pc.fac_ok = inv_ok;
+            }
+          ps.factored = inv_ok;
+          // safety net: the factored inverse must reproduce the dense one
+          for (size_t ci = 0; ci < ps.classes.size() && ps.factored; ++ci)
+            {
+              const PatchClass &pc = ps.classes[ci];
+              const int ns = pc.n_s, nvs = pc.n_vs, nps = ns - nvs, nt = pc.n_t;
+              const auto prow = [&](int a, int j) { return j < nvs ? a * nvs + j : S * nvs + a * nps + (j - nvs); };
+              std::vector<double> r(nt), t(S * nsp, 0.0), y(S * nsp, 0.0), z(nt, 0.0), zd(nt, 0.0);
+              for (int i = 0; i < nt; ++i)
+                r[i] = std::sin(1.0 + 3.7 * i) + 0.3 * std::cos(0.9 * i * i);
+              for (int i = 0; i < S; ++i)
+                for (int j = 0; j < ns; ++j)
+                  for (int b = 0; b < S; ++b)
+                    t[i * nsp + j] += ps.eig.W[i * S + b] * r[prow(b, j)];
+              for (size_t b = 0; b < ps.eig.blk_c0.size(); ++b)
+                {
+                  const int c0 = ps.eig.blk_c0[b], sz = ps.eig.blk_sz[b];
+                  for (int bi = 0; bi < sz; ++bi)
+                    for (int i = 0; i < ns; ++i)
+                      for (int bj = 0; bj < sz; ++bj)
+                        for (int j = 0; j < ns; ++j)
+                          y[(c0 + bi) * nsp + i] +=
+                            pc.fac_inv[static_cast<size_t>((c0 + bi) * nsp + i) * 2 * nsp + bj * nsp + j] *
+                            t[(c0 + bj) * nsp + j];
+                }
+              for (int a = 0; a < S; ++a)
+                for (int j = 0; j < ns; ++j)
+                  for (int i = 0; i < S; ++i)
+                    z[prow(a, j)] += ps.eig.V[a * S + i] * y[i * nsp + j];
+              double err = 0.0, zmax = 0.0;
+              for (int i = 0; i < nt; ++i)
+                {
+                  for (int j = 0; j < nt; ++j)
+                    zd[i] += pc.inverse[static_cast<size_t>(i) * nt + j] * r[j];
+                  zmax = std::max(zmax, std::abs(zd[i]));
+                }
+              for (int i = 0; i < nt; ++i)
+                err = std::max(err, std::abs(z[i] - zd[i]));
+              if (!(err <= 1e-10 * zmax))
+                ps.factored = false;
+            }
+        }
+    }
+  if (ps.factored)
+    for (int ay = 0; ay < nay; ++ay)
+      for (int ax = 0; ax < nax; ++ax)
+        {
+          const int cls = key_to_class[class_key(L, kind, ax, ay)];
+          std::uint64_t e = 0;
+          for (size_t b = 0; b < ps.eig.blk_sz.size(); ++b)
+            e += static_cast<std::uint64_t>(ps.eig.blk_sz[b] * ps.classes[cls].n_s) * ps.eig.blk_sz[b] *
+                 ps.classes[cls].n_s;
+          ps.factored_matrix_elements += e + 2ull * L.S() * L.S() * ps.classes[cls].n_s;
+        }
+  for (auto &pc : ps.classes)
+    {
+      pc.Ms.clear();
+      pc.As.clear();
+    }
   return ps;
 }
 

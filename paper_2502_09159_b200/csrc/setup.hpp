@@ -40,6 +40,22 @@ struct TimeTables
 };
 TimeTables time_tables(int k, double tau);
 
+/// Real block-diagonalisation of the DG(k) time step, M_t^{-1} K_t =
+/// V Lambda V^{-1}: Lambda has 1x1 blocks (real eigenvalue alpha) and 2x2
+/// blocks [[alpha, beta], [-beta, alpha]] (pair alpha +- i beta, columns
+/// Re v, Im v of V). With it, a space-time patch matrix K_t (x) M_s +
+/// M_t (x) A_s factors as (M_t V (x) I) (Lambda (x) M_s + I (x) A_s)
+/// (V^{-1} (x) I): the middle is block diagonal in time (Vanka factored form).
+struct TemporalEigen
+{
+  int S = 0;
+  std::vector<double> V, W;         // S x S row-major; W = V^{-1} M_t^{-1}
+  std::vector<int> blk_c0, blk_sz;  // per block: first coordinate, size (1 or 2)
+  std::vector<double> alpha, beta;  // per block (beta = 0 for a real eigenvalue)
+  bool ok = false;
+};
+TemporalEigen temporal_eigen(const TimeTables &T);
+
 /// Reference-cell 1D factors for Q_{r+1} (GLL nodes) / Legendre pressure.
 struct Factors1D
 {
@@ -99,6 +115,14 @@ struct PatchClass
   std::vector<double> weight;         // 1/valence (vanka.cpp:182-192)
   std::vector<double> inverse;        // n_t x n_t row-major (pseudo-inverse if singular)
   bool singular = false;
+  // spatial factors of the patch matrix (k = 0 copy of the patch: velocity
+  // mass M_s and Stokes block A_s on the n_s spatial dofs, n_vs velocity)
+  int n_s = 0, n_vs = 0;
+  std::vector<double> Ms, As;
+  // factored inverse (fac_ok): the middle block inverses of TemporalEigen,
+  // (S * n_sp) rows x (2 * n_sp) block-local columns, row = coord * n_sp + j
+  bool fac_ok = false;
+  std::vector<double> fac_inv;
 };
 
 struct PatchSet
@@ -113,6 +137,11 @@ struct PatchSet
   };
   std::vector<std::vector<Entry>> colours;
   std::uint64_t total_matrix_elements = 0; // sum n_T^2 over all patches
+  // factored form (all classes non-singular, k >= 2): padded spatial size
+  bool factored = false;
+  int n_sp = 0;
+  TemporalEigen eig;
+  std::uint64_t factored_matrix_elements = 0; // sum over patches of the middle-block MACs
 };
 PatchSet build_patches(const LevelSpec &L, PatchKind kind);
 

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -183,6 +184,11 @@ struct stmg_level
   bool super = false;
   SuperSet sup[3]; // intervals per block: [0] 16, [2] 8 (slabs), [1] 1 (time marching)
   int max_nt = 0;
+  // time-diagonalised patch inverses (vanka_fac_kernel), DG(k >= 2) levels
+  bool factored = false;
+  FacParams fac{};
+  std::vector<DevArray<double>> cls_fac;
+  std::uint64_t factored_matrix_elements = 0;
   int n_classes = 0;
   std::uint64_t total_matrix_elements = 0;
   // scratch
@@ -227,6 +233,19 @@ struct stmg_level
       {
         // widest interval group that the launch fills: 16, 8 or 1 per block
         const SuperSet &ss = sup[n >= 16 ? 0 : (n >= 8 ? 2 : 1)];
+        if (!ss.tile_ptr.empty() && factored)
+          {
+            for (size_t sc = 0; sc < ss.tile_ptr.size(); ++sc)
+              if (ss.tile_blocks[sc] > 0)
+                {
+                  check(launch_vanka_fac(classes.p, ss.tiles.p, ss.va.p, ss.pa.p, ss.tile_ptr[sc].p,
+                                         ss.tile_blocks[sc], ss.ng_full, fac, r, u, spec.isz(), n, omega,
+                                         ctx->stream),
+                        "vanka_fac");
+                  ctx->count();
+                }
+            return;
+          }
         if (!ss.tile_ptr.empty())
           {
             for (size_t sc = 0; sc < ss.tile_ptr.size(); ++sc)
@@ -322,16 +341,54 @@ build_level(stmg_level &L)
   L.cls_rel.resize(ps.classes.size());
   L.cls_weight.resize(ps.classes.size());
   L.cls_inverse.resize(ps.classes.size());
+  L.cls_fac.resize(ps.classes.size());
   for (size_t i = 0; i < ps.classes.size(); ++i)
     {
       const PatchClass &pc = ps.classes[i];
       L.cls_rel[i].upload(pc.rel);
+      if (ps.factored)
+        L.cls_fac[i].upload(pc.fac_inv);
       L.cls_weight[i].upload(pc.weight);
       L.cls_inverse[i].upload(pc.inverse);
-      dc[i] = DevPatchClass{pc.n_t, pc.n_vel, L.cls_rel[i].p, L.cls_weight[i].p, L.cls_inverse[i].p};
+      dc[i] = DevPatchClass{pc.n_t, pc.n_vel, L.cls_rel[i].p, L.cls_weight[i].p, L.cls_inverse[i].p,
+                            pc.n_s, pc.n_vs, ps.factored ? L.cls_fac[i].p : nullptr};
       L.max_nt = std::max(L.max_nt, pc.n_t);
     }
   L.classes.upload(dc);
+  // Time-diagonalised inverses are opt-in (STMG_VANKA_FACTORED=1): for DG(2)
+  // they cut the DMMA work to 0.61x but the slot-mixing stages add 38% more
+  // instructions, so the C2 update measured 5.85 ms against 5.69 ms dense
+  // (DESIGN.md 3.2). The dense kernel is the default.
+  const char *fac_env = std::getenv("STMG_VANKA_FACTORED");
+  if (ps.factored && vanka_fac_supported(s.S(), ps.n_sp) && fac_env && fac_env[0] == '1')
+    {
+      L.factored = true;
+      L.factored_matrix_elements = ps.factored_matrix_elements;
+      FacParams &F = L.fac;
+      F.S = s.S();
+      F.nsp = ps.n_sp;
+      for (int a = 0; a < F.S; ++a)
+        for (int b = 0; b < F.S; ++b)
+          {
+            F.V[a * kMaxS + b] = ps.eig.V[a * F.S + b];
+            F.W[a * kMaxS + b] = ps.eig.W[a * F.S + b];
+          }
+      for (int w = 0; w < 16; ++w)
+        {
+          const int row0 = 8 * w;
+          F.kbase[w] = 0;
+          F.ksteps[w] = 0;
+          if (row0 >= F.S * F.nsp)
+            continue;
+          const int coord = row0 / F.nsp;
+          for (size_t b = 0; b < ps.eig.blk_c0.size(); ++b)
+            if (coord >= ps.eig.blk_c0[b] && coord < ps.eig.blk_c0[b] + ps.eig.blk_sz[b])
+              {
+                F.kbase[w] = ps.eig.blk_c0[b] * F.nsp;
+                F.ksteps[w] = ps.eig.blk_sz[b] * F.nsp / 4;
+              }
+        }
+    }
   std::vector<VankaBatch> batches;
   std::vector<long long> va, pa;
   const int cols = vanka_cols_per_batch();
@@ -1269,6 +1326,8 @@ stmg_level_sizes(const stmg_level *L, int64_t *out)
     out[5] = L->spec.gx();
     out[6] = L->n_classes;
     out[7] = static_cast<int64_t>(L->total_matrix_elements);
+    out[8] = L->factored ? 1 : 0;
+    out[9] = static_cast<int64_t>(L->factored_matrix_elements);
   });
 }
 
@@ -1724,8 +1783,11 @@ stmg_patch_info(int nx, int ny, int r, int k, double tau, double nu, double gamm
     out[1] = static_cast<int64_t>(ps.classes.size());
     out[2] = static_cast<int64_t>(ps.total_matrix_elements);
     out[3] = static_cast<int64_t>(ps.colours.size());
-    for (size_t c = 0; c < ps.classes.size() && c < 60; ++c)
+    for (size_t c = 0; c < ps.classes.size() && c < 56; ++c)
       out[4 + c] = ps.classes[c].n_t;
+    out[60] = ps.factored ? 1 : 0;
+    out[61] = ps.n_sp;
+    out[62] = static_cast<int64_t>(ps.factored_matrix_elements);
     if (inverse_out)
       {
         if (class_index < 0 || class_index >= static_cast<int>(ps.classes.size()))

@@ -259,7 +259,254 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
     }
   }
 }
+// ---------------------------------------------------------------- factored
+// Time-diagonalised patch solves: A_T^{-1} = (V (x) I) blockdiag(B_b^{-1})
+// (W (x) I) (setup.hpp TemporalEigen). Per tile: stage 1 mixes the slots of
+// the gathered R by W into T1 (rows coord * n_sp + j), the DMMA applies the
+// block-diagonal middle (each warp's K range is its own block: ~40% fewer
+// MACs than the dense inverse for DG(2)), Z goes to shared memory, and stage
+// 3 mixes by V and scatters with the valence weights.
+constexpr size_t kFSmem = sizeof(double) * 4 * kTSlot + kTRows * 16 + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4));
+
+template <int S, int NSP>
+__global__ void __launch_bounds__(kTThreads, 1)
+vanka_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__restrict__ tiles,
+                 const long long *__restrict__ va, const long long *__restrict__ pa, const int *__restrict__ tile_ptr,
+                 int ng_full, const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals,
+                 double omega, const FacParams F)
+{
+  // 2 R slots, T1, Z, class rows (rel, omega * weight), then the block's tile data
+  extern __shared__ __align__(16) double ring[];
+  double *t1 = ring + 2 * kTSlot, *zb = ring + 3 * kTSlot;
+  long long *s_rel = reinterpret_cast<long long *>(ring + 4 * kTSlot);
+  double *s_w = reinterpret_cast<double *>(s_rel + kTRows);
+  long long *s_colv = reinterpret_cast<long long *>(s_w + kTRows);
+  long long *s_colp = s_colv + kTMaxTiles * kTCols;
+  int *s_coln = reinterpret_cast<int *>(s_colp + kTMaxTiles * kTCols);
+  VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_coln + kTMaxTiles * kTCols);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = tile_ptr[blockIdx.x], t1i = tile_ptr[blockIdx.x + 1];
+  const int nb = t1i - t0;
+  const int n0 = blockIdx.y * ng_full;
+  const long long base0 = n0 * isz;
+  constexpr int KB = NSP / 2, nsp = NSP; // widest block: 2 NSP columns
+
+  for (int e = tid; e < nb; e += kTThreads)
+    s_tile[e] = tiles[t0 + e];
+  for (int e = tid; e < nb * kTCols; e += kTThreads)
+    {
+      const VankaTile tl = tiles[t0 + e / kTCols];
+      const int j = e % kTCols;
+      if (j < tl.ncols)
+        {
+          const int q = tl.c0 + j, patch = tl.pfirst + q / ng_full, nl = q % ng_full;
+          s_colv[e] = nl * isz + va[patch];
+          s_colp[e] = nl * isz + pa[patch];
+          s_coln[e] = nl;
+        }
+      else
+        {
+          s_colv[e] = s_colp[e] = 0;
+          s_coln[e] = 1 << 30;
+        }
+    }
+  __syncthreads();
+
+  // gather (as vanka_tc_kernel): warp w fills columns w and w + 16
+  constexpr int QN = kTRows / 32;
+  constexpr int CN = kTCols / (kTThreads / 32);
+  int cls_issue = -1, nt_issue = 0, nvel_issue = 0;
+  long long relq[QN];
+  auto issue = [&](int lt, int slot) {
+    if (lt < nb)
+      {
+        const VankaTile tl = s_tile[lt];
+        if (tl.ncols == 0)
+          return;
+        if (tl.cls != cls_issue)
+          {
+            const DevPatchClass pc = classes[tl.cls];
+            nt_issue = pc.n_t;
+            nvel_issue = pc.n_vel;
+#pragma unroll
+            for (int q = 0; q < QN; ++q)
+              relq[q] = lane + 32 * q < nt_issue ? pc.rel[lane + 32 * q] : 0;
+            cls_issue = tl.cls;
+          }
+        double *dst0 = ring + slot * kTSlot;
+#pragma unroll
+        for (int cc = 0; cc < CN; ++cc)
+          {
+            const int col = warp + cc * (kTThreads / 32);
+            const int ci = lt * kTCols + col;
+            const bool colok = col < tl.ncols && n0 + s_coln[ci] < n_intervals;
+            const long long cv = base0 + s_colv[ci], cp = base0 + s_colp[ci];
+#pragma unroll
+            for (int q = 0; q < QN; ++q)
+              {
+                const int row = lane + 32 * q;
+                double *dst = dst0 + col * kTLd + row;
+                if (colok && row < nt_issue)
+                  cp_async8(dst, r + (row < nvel_issue ? cv : cp) + relq[q]);
+                else
+                  *dst = 0.0;
+              }
+          }
+      }
+  };
+  issue(0, 0);
+  cp_async_commit();
+
+  int loaded = -1, ns = 0, nvs = 0, nvel = 0; // class of the tile being computed
+  int p_lt = -1, p_ns = 0, p_nvs = 0, p_nvel = 0, p_ncols = 0; // tile whose Z awaits stage 3
+  double afr[KB];
+  const int row = 8 * warp + (lane >> 2);
+  const int kbase = F.kbase[warp], ksteps = F.ksteps[warp];
+
+  // stage 3 of the pending tile: out(a, j) = sum_i V(a, i) Z(i, j), weights, scatter
+  auto stage3 = [&]() {
+    if (p_lt < 0)
+      return;
+    const int nps = p_ns - p_nvs;
+    for (int e = tid; e < nsp * kTCols; e += kTThreads)
+      {
+        const int j = e % nsp, c = e / nsp;
+        const int ci = p_lt * kTCols + c;
+        if (j >= p_ns || c >= p_ncols || n0 + s_coln[ci] >= n_intervals)
+          continue;
+        double z[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+          z[i] = zb[c * kTLd + i * nsp + j];
+#pragma unroll
+        for (int a = 0; a < S; ++a)
+            {
+              double o = 0.0;
+#pragma unroll
+              for (int i = 0; i < S; ++i)
+                o = fma(F.V[a * kMaxS + i], z[i], o);
+              const int pr = j < p_nvs ? a * p_nvs + j : S * p_nvs + a * nps + (j - p_nvs);
+              atomicAdd(u + base0 + (pr < p_nvel ? s_colv[ci] : s_colp[ci]) + s_rel[pr], o * s_w[pr]);
+            }
+      }
+    p_lt = -1;
+  };
+
+  for (int lt = 0; lt < nb; ++lt)
+    {
+      cp_async_wait0();
+      __syncthreads(); // R of tile lt visible; Z of the pending tile complete; T1 free
+      issue(lt + 1, (lt + 1) & 1);
+      cp_async_commit();
+      const VankaTile tl = s_tile[lt];
+      stage3(); // overlaps nothing but saves a barrier: Z and T1 are separate buffers
+      if (tl.ncols == 0)
+        continue;
+      if (tl.cls != loaded)
+        {
+          // the class rows are read by stage 3 of this tile only after the
+          // next barrier; the previous class's stage 3 is done (just above)
+          __syncthreads();
+          const DevPatchClass pc = classes[tl.cls];
+          ns = pc.n_s;
+          nvs = pc.n_vs;
+          nvel = pc.n_vel;
+          for (int e = tid; e < pc.n_t; e += kTThreads)
+            {
+              s_rel[e] = pc.rel[e];
+              s_w[e] = omega * pc.weight[e];
+            }
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk)
+            afr[kk] = kk < ksteps ? __ldg(pc.fac_inv + static_cast<long long>(row) * 2 * nsp + 4 * kk + (lane & 3))
+                                  : 0.0;
+          loaded = tl.cls;
+        }
+      const int nps = ns - nvs;
+      // stage 1: T1(i, j) = sum_b W(i, b) R(b, j), padding rows zero
+      const double *R = ring + (lt & 1) * kTSlot;
+      for (int e = tid; e < nsp * kTCols; e += kTThreads)
+        {
+          const int j = e % nsp, c = e / nsp;
+          double rb[S];
+#pragma unroll
+          for (int b = 0; b < S; ++b)
+            rb[b] = j < ns ? R[c * kTLd + (j < nvs ? b * nvs + j : S * nvs + b * nps + (j - nvs))] : 0.0;
+#pragma unroll
+          for (int i = 0; i < S; ++i)
+            {
+              double t = 0.0;
+#pragma unroll
+              for (int b = 0; b < S; ++b)
+                t = fma(F.W[i * kMaxS + b], rb[b], t);
+              t1[c * kTLd + i * nsp + j] = t;
+            }
+        }
+      __syncthreads(); // T1 complete; stage 3 of the previous tile done (Z free)
+      double acc[kTCols / 8][2];
+#pragma unroll
+      for (int ct = 0; ct < kTCols / 8; ++ct)
+        acc[ct][0] = acc[ct][1] = 0.0;
+      const double *bbase = t1 + (lane >> 2) * kTLd + kbase + (lane & 3);
+#pragma unroll
+      for (int kk = 0; kk < KB; ++kk)
+        if (kk < ksteps)
+          {
+            const double *brow = bbase + 4 * kk;
+#pragma unroll
+            for (int ct = 0; ct < kTCols / 8; ++ct)
+              dmma(acc[ct], afr[kk], brow[ct * 8 * kTLd]);
+          }
+      if (ksteps > 0)
+#pragma unroll
+        for (int ct = 0; ct < kTCols / 8; ++ct)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            zb[(8 * ct + 2 * (lane & 3) + b) * kTLd + row] = acc[ct][b];
+      p_lt = lt;
+      p_ns = ns;
+      p_nvs = nvs;
+      p_nvel = nvel;
+      p_ncols = tl.ncols;
+    }
+  __syncthreads(); // Z of the last tile complete
+  stage3();
+}
 } // namespace
+
+cudaError_t
+launch_vanka_fac(const DevPatchClass *classes, const VankaTile *tiles, const long long *va, const long long *pa,
+                 const int *tile_ptr, int n_blocks, int ng_full, const FacParams &F, const double *r, double *u,
+                 long long isz, int n_intervals, double omega, cudaStream_t stream)
+{
+  if (n_blocks == 0 || n_intervals == 0)
+    return cudaSuccess;
+  dim3 grid(n_blocks, (n_intervals + ng_full - 1) / ng_full);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFSmem));
+    kern<<<grid, kTThreads, kFSmem, stream>>>(classes, tiles, va, pa, tile_ptr, ng_full, r, u, isz, n_intervals,
+                                              omega, F);
+  };
+  // instantiations with S * NSP <= kTRows (host: setup.cpp factored form)
+#define STMG_FAC_CASE(SS, NN)                                                                                          \
+  if (F.S == SS && F.nsp == NN)                                                                                        \
+    {                                                                                                                  \
+      go(vanka_fac_kernel<SS, NN>);                                                                                    \
+      return cudaGetLastError();                                                                                       \
+    }
+  STMG_FAC_CASE(3, 16)
+  STMG_FAC_CASE(3, 24)
+  STMG_FAC_CASE(3, 32)
+  STMG_FAC_CASE(3, 40)
+  STMG_FAC_CASE(4, 16)
+  STMG_FAC_CASE(4, 24)
+  STMG_FAC_CASE(4, 32)
+  STMG_FAC_CASE(5, 16)
+  STMG_FAC_CASE(5, 24)
+#undef STMG_FAC_CASE
+  return cudaErrorInvalidValue; // host only enables the factored form for these shapes
+  return cudaGetLastError();
+}
 
 cudaError_t
 launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *va, const long long *pa,
@@ -296,6 +543,13 @@ int
 vanka_tc_cols()
 {
   return kTCols;
+}
+
+bool
+vanka_fac_supported(int S, int nsp)
+{
+  return (S == 3 && (nsp == 16 || nsp == 24 || nsp == 32 || nsp == 40)) ||
+         (S == 4 && (nsp == 16 || nsp == 24 || nsp == 32)) || (S == 5 && (nsp == 16 || nsp == 24));
 }
 
 int
