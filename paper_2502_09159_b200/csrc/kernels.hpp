@@ -76,6 +76,7 @@ struct VankaTile
   int ncols;
   int pfirst;
   int c0;
+  int phase; // colour sub-phase within the block (same-phase tiles share no dof)
 };
 cudaError_t launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long long *va,
                             const long long *pa, const int *tile_ptr, int n_blocks, int ng_full,

@@ -435,7 +435,15 @@ build_level(stmg_level &L)
       // slabs, up to 32 for time marching (one interval per block).
       for (int set = 0; set < 3; ++set)
         {
-          const int B0 = 4;
+#ifndef STMG_STRIP_CELL
+#define STMG_STRIP_CELL 8 // measured: C2 Vanka 5.60 (4) -> 5.33 ms (8); 16 overflows the staged tile table
+#endif
+#ifndef STMG_STRIP_VSP
+#define STMG_STRIP_VSP 4 // 6 overflows the 32-tile staging for 8-interval slabs
+#endif
+          // super-cells per strip with 16 intervals per block; 8-interval
+          // slabs use twice as many (same columns per colour sub-phase)
+          const int B0 = P == 2 ? STMG_STRIP_CELL : STMG_STRIP_VSP;
           // time-marching set: 32 super-cells per block, fewer on small levels
           // so that a pass still spreads over ~2 blocks per SM (latency)
           const long long per_pass = std::max(1LL, static_cast<long long>(nsx) * nsy / 4);
@@ -519,7 +527,7 @@ build_level(stmg_level &L)
                   // close a colour sub-phase: pad with empty tiles to whole stages
                   const auto pad = [&](int cls) {
                     while ((static_cast<int>(tiles.size()) - phase_first) % stage != 0)
-                      tiles.push_back(VankaTile{cls, 0, 0, 0});
+                      tiles.push_back(VankaTile{cls, 0, 0, 0, tiles.empty() ? 0 : tiles.back().phase});
                     phase_first = static_cast<int>(tiles.size());
                   };
                   for (int it = hptr[blk]; it < hptr[blk + 1]; ++it)
@@ -529,7 +537,7 @@ build_level(stmg_level &L)
                       const VankaBatch &item = items[it];
                       const int ncols = item.count * ss.ng_full;
                       for (int c0 = 0; c0 < ncols; c0 += tc)
-                        tiles.push_back(VankaTile{item.cls, std::min(tc, ncols - c0), item.first, c0});
+                        tiles.push_back(VankaTile{item.cls, std::min(tc, ncols - c0), item.first, c0, item_phase[it]});
                     }
                   if (hptr[blk + 1] > hptr[blk])
                     pad(items[hptr[blk + 1] - 1].cls);

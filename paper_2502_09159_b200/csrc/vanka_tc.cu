@@ -51,7 +51,15 @@ constexpr int kTSlots = 2 * kTStage;      // double-buffered stages
 #define STMG_VANKA_MAXTILES 32
 #endif
 constexpr int kTMaxTiles = STMG_VANKA_MAXTILES; // tiles per block (host falls back beyond)
-constexpr size_t kTSmem = sizeof(double) * kTSlots * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4));
+#ifndef STMG_VT_BARRIER
+// full/empty mbarrier pipeline over 3 ring slots (see vanka_tc_kernel)
+#define STMG_VT_MBAR 1
+constexpr int kTRing = 3;
+#else
+constexpr int kTRing = kTSlots;
+#endif
+constexpr size_t kTSmem =
+  sizeof(double) * kTRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4)) + 8 * sizeof(unsigned long long);
 
 __device__ __forceinline__ void
 cp_async8(double *dst, const double *src)
@@ -70,6 +78,46 @@ cp_async_wait0()
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+#ifndef STMG_VT_BARRIER
+// zero-filling copy: src_bytes = 0 writes 0.0 (the slot write stays async,
+// so the mbarrier pipeline tracks every write of a gather)
+__device__ __forceinline__ void
+cp_async8z(double *dst, const double *src, bool valid)
+{
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ unsigned
+smem_u32(const void *p)
+{
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void
+mbar_init(unsigned long long *bar, unsigned count)
+{
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void
+mbar_arrive(unsigned long long *bar)
+{
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrive once all prior cp.async of this thread have completed
+__device__ __forceinline__ void
+cp_async_mbar_arrive(unsigned long long *bar)
+{
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void
+mbar_wait(unsigned long long *bar, unsigned parity)
+{
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+                 smem_u32(bar)),
+               "r"(parity)
+               : "memory");
+}
+#endif
+
 __device__ __forceinline__ void
 dmma(double (&d)[2], double a, double b)
 {
@@ -86,10 +134,14 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
                 double omega)
 {
   extern __shared__ __align__(16) double ring[]; // kTSlots slots of kTRows x kTLd, then the block's tile data
-  long long *s_colv = reinterpret_cast<long long *>(ring + kTSlots * kTSlot);
+  long long *s_colv = reinterpret_cast<long long *>(ring + kTRing * kTSlot);
   long long *s_colp = s_colv + kTMaxTiles * kTCols;
   int *s_coln = reinterpret_cast<int *>(s_colp + kTMaxTiles * kTCols);
   VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_coln + kTMaxTiles * kTCols);
+#ifdef STMG_VT_MBAR
+  // full[3], empty[3], phase-done[2]
+  unsigned long long *s_bar = reinterpret_cast<unsigned long long *>(s_tile + kTMaxTiles);
+#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t0 = tile_ptr[blockIdx.x], t1 = tile_ptr[blockIdx.x + 1];
   const int nb = t1 - t0;
@@ -159,13 +211,18 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
                 const int row = row_of(q);
                 double *dst = slot + col * kTLd + row;
 #ifdef STMG_VT_NO_GATHER
-                if (false)
+                const bool valid = false;
 #else
-                if (colok && row < nt_issue)
+                const bool valid = colok && row < nt_issue;
 #endif
+#ifdef STMG_VT_MBAR
+                cp_async8z(dst, valid ? r + (row < nvel_issue ? cv : cp) + relq[q] : r, valid);
+#else
+                if (valid)
                   cp_async8(dst, r + (row < nvel_issue ? cv : cp) + relq[q]);
                 else
                   *dst = 0.0;
+#endif
               }
           }
       }
@@ -178,7 +235,33 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
     cp_async_commit(); // possibly empty group
   };
 
+#ifdef STMG_VT_MBAR
+  // Full/empty mbarrier pipeline over 3 slots: full[s] completes when every
+  // thread's copies of the slot's tile have landed (cp.async arrive), so a
+  // warp waits only for the tile it computes; empty[s] completes when every
+  // thread has finished its MMAs on the slot. Tile lt+2 is gathered (into the
+  // slot of tile lt-1) right after a thread finishes tile lt, so warps drift
+  // up to a tile apart instead of meeting at a block barrier every tile.
+  unsigned long long *full = s_bar, *empty = s_bar + 3, *pdone = s_bar + 6;
+  if (tid == 0)
+    {
+      for (int i = 0; i < 3; ++i)
+        {
+          mbar_init(full + i, kTThreads);
+          mbar_init(empty + i, kTThreads);
+        }
+      mbar_init(pdone + 0, kTThreads);
+      mbar_init(pdone + 1, kTThreads);
+    }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  issue(0, 0);
+  cp_async_mbar_arrive(full + 0);
+  issue(1, 1);
+  cp_async_mbar_arrive(full + 1);
+#else
   issue_stage(0);
+#endif
 
   int loaded = -1, nt_loaded = 0;
   double afr[KS];
@@ -186,6 +269,95 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
   bool vel_row = false, ok_row = false;
   double w_row = 0.0;
   const int row = 8 * warp + (lane >> 2);
+
+#ifdef STMG_VT_MBAR
+  // Colour sub-phases of a block share dofs: before the first scatter of a
+  // new phase, every thread's scatters of the previous phase must be done
+  // (arrive = release, wait = acquire), so the red.add order -- and the
+  // result -- is the same on every run. MMAs of the next phase may start early.
+  int cur_phase = -1, transitions = 0;
+  for (int lt = 0; lt < nb; ++lt)
+    {
+      const int slot = lt % 3;
+      mbar_wait(full + slot, (lt / 3) & 1);
+      const VankaTile tl = s_tile[lt];
+      double acc[kTCols / 8][2];
+#pragma unroll
+      for (int ct = 0; ct < kTCols / 8; ++ct)
+        acc[ct][0] = acc[ct][1] = 0.0;
+      if (tl.ncols > 0)
+        {
+          if (tl.cls != loaded)
+            {
+              const DevPatchClass pc = classes[tl.cls];
+#pragma unroll
+              for (int kk = 0; kk < KS; ++kk)
+                {
+                  const int col = 4 * kk + (lane & 3);
+                  afr[kk] = (row < pc.n_t && col < pc.n_t) ? __ldg(pc.inverse + row * pc.n_t + col) : 0.0;
+                }
+              ok_row = row < pc.n_t;
+              vel_row = row < pc.n_vel;
+              rel_row = ok_row ? pc.rel[row] : 0;
+              w_row = ok_row ? omega * pc.weight[row] : 0.0;
+              nt_loaded = pc.n_t;
+              loaded = tl.cls;
+            }
+          const double *bbase = ring + slot * kTSlot + (lane >> 2) * kTLd + (lane & 3);
+          if (8 * warp < nt_loaded)
+            {
+#pragma unroll
+              for (int kk = 0; kk < KS; ++kk)
+                {
+                  const double *brow = bbase + 4 * kk;
+                  constexpr int kNStep = 8 * kTLd; // next 8 columns
+#pragma unroll
+                  for (int ct = 0; ct < kTCols / 8; ++ct)
+                    dmma(acc[ct], afr[kk], brow[kNStep * ct]);
+                }
+            }
+        }
+      mbar_arrive(empty + slot); // this thread is done reading the slot
+      if (tl.phase != cur_phase)
+        {
+          if (cur_phase >= 0)
+            {
+              unsigned long long *pd = pdone + (transitions & 1);
+              mbar_arrive(pd);
+              mbar_wait(pd, (transitions >> 1) & 1);
+              ++transitions;
+            }
+          cur_phase = tl.phase;
+        }
+      if (tl.ncols > 0 && ok_row)
+        {
+#pragma unroll
+          for (int ct = 0; ct < kTCols / 8; ++ct)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+              {
+                const int col = 8 * ct + 2 * (lane & 3) + b;
+                const int ci = lt * kTCols + col;
+#ifdef STMG_VT_NO_SCATTER
+                if (acc[ct][b] == 123.456)
+#else
+                if (col < tl.ncols && n0 + s_coln[ci] < n_intervals)
+#endif
+                  atomicAdd(u + base0 + (vel_row ? s_colv[ci] : s_colp[ci]) + rel_row, acc[ct][b] * w_row);
+              }
+        }
+      // gather tile lt+2 into the slot of tile lt-1 once every thread released it
+      if (lt + 2 < nb)
+        {
+          const int ns = (lt + 2) % 3;
+          if (lt >= 1)
+            mbar_wait(empty + ns, ((lt - 1) / 3) & 1);
+          issue(lt + 2, ns);
+          cp_async_mbar_arrive(full + ns);
+        }
+    }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+#else
 
   // Stage g: wait for its gather, barrier (its slots are visible to all, the
   // slots of stage g-1 are free), gather stage g+1 into them, then compute
@@ -258,6 +430,7 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
         }
     }
   }
+#endif
 }
 // ---------------------------------------------------------------- factored
 // Time-diagonalised patch solves: A_T^{-1} = (V (x) I) blockdiag(B_b^{-1})
