@@ -439,11 +439,24 @@ build_level(stmg_level &L)
 #define STMG_STRIP_CELL 8 // measured: C2 Vanka 5.60 (4) -> 5.33 ms (8); 16 overflows the staged tile table
 #endif
 #ifndef STMG_STRIP_VSP
-#define STMG_STRIP_VSP 4 // 6 overflows the 32-tile staging for 8-interval slabs
+#define STMG_STRIP_VSP 8 // with the 48-tile staging: C4 vertex stars 12.03 -> 11.79 ms
 #endif
           // super-cells per strip with 16 intervals per block; 8-interval
           // slabs use twice as many (same columns per colour sub-phase)
-          const int B0 = P == 2 ? STMG_STRIP_CELL : STMG_STRIP_VSP;
+          // narrower strips on mid-size levels so a pass still has ~2 blocks
+          // per SM (strips per pass ~ nwx/2 * nsy/2; 16-interval blocks are
+          // counted with 4 interval groups)
+          int B0 = P == 2 ? STMG_STRIP_CELL : STMG_STRIP_VSP;
+          {
+            const int ngroups = set == 0 ? 4 : 1, mult = set == 2 ? 2 : 1;
+            while (B0 > 1)
+              {
+                const long long wx = (nax + P * B0 * mult - 1) / (P * B0 * mult);
+                if ((wx + 1) / 2 * ((nsy + 1) / 2) * ngroups >= 2 * 148)
+                  break;
+                B0 /= 2;
+              }
+          }
           // time-marching set: 32 super-cells per block, fewer on small levels
           // so that a pass still spreads over ~2 blocks per SM (latency)
           const long long per_pass = std::max(1LL, static_cast<long long>(nsx) * nsy / 4);

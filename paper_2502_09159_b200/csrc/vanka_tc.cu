@@ -46,9 +46,9 @@ constexpr int kTSlot = kTCols * kTLd;
 #define STMG_VANKA_STAGE 1
 #endif
 constexpr int kTStage = STMG_VANKA_STAGE; // tiles per barrier stage
-constexpr int kTSlots = 2 * kTStage;      // double-buffered stages
+[[maybe_unused]] constexpr int kTSlots = 2 * kTStage; // double-buffered stages (block-barrier build)
 #ifndef STMG_VANKA_MAXTILES
-#define STMG_VANKA_MAXTILES 32
+#define STMG_VANKA_MAXTILES 48
 #endif
 constexpr int kTMaxTiles = STMG_VANKA_MAXTILES; // tiles per block (host falls back beyond)
 #ifndef STMG_VT_BARRIER
