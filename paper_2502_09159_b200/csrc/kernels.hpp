@@ -88,7 +88,6 @@ cudaError_t launch_vanka_fac(const DevPatchClass *classes, const VankaTile *tile
                              cudaStream_t stream);
 int vanka_tc_cols();
 int vanka_tc_max_tiles();
-int vanka_tc_stage(); // tiles per barrier stage
 bool vanka_fac_supported(int S, int nsp); // instantiated (S, n_sp) shapes of vanka_fac_kernel
 
 cudaError_t launch_vmult(int r, int S, const LevelConsts &P, const double *x, const double *b, double *y,

@@ -533,27 +533,15 @@ build_level(stmg_level &L)
             {
               const std::vector<int> &hptr = host_ptr[sc];
               std::vector<int> tptr{static_cast<int>(tiles.size())};
-              const int stage = vanka_tc_stage();
               for (int blk = 0; blk < ss.pass_blocks[sc]; ++blk)
                 {
-                  int phase_first = static_cast<int>(tiles.size());
-                  // close a colour sub-phase: pad with empty tiles to whole stages
-                  const auto pad = [&](int cls) {
-                    while ((static_cast<int>(tiles.size()) - phase_first) % stage != 0)
-                      tiles.push_back(VankaTile{cls, 0, 0, 0, tiles.empty() ? 0 : tiles.back().phase});
-                    phase_first = static_cast<int>(tiles.size());
-                  };
                   for (int it = hptr[blk]; it < hptr[blk + 1]; ++it)
                     {
-                      if (it > hptr[blk] && item_phase[it] != item_phase[it - 1])
-                        pad(items[it - 1].cls);
                       const VankaBatch &item = items[it];
                       const int ncols = item.count * ss.ng_full;
                       for (int c0 = 0; c0 < ncols; c0 += tc)
                         tiles.push_back(VankaTile{item.cls, std::min(tc, ncols - c0), item.first, c0, item_phase[it]});
                     }
-                  if (hptr[blk + 1] > hptr[blk])
-                    pad(items[hptr[blk + 1] - 1].cls);
                   tptr.push_back(static_cast<int>(tiles.size()));
                   if (tptr.back() - tptr[tptr.size() - 2] > vanka_tc_max_tiles())
                     tc_ok = false; // block too long for the staged tile data

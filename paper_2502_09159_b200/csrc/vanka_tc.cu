@@ -4,19 +4,20 @@
 // (vanka.cpp:196-233): u += omega * sum_T R_T^T w_T A_T^{-1} R_T r.
 //
 // Per block: a host-built list of tiles, each <= 32 columns (patch, interval)
-// of one congruence class inside one super-cell colour sub-phase, grouped in
-// stages of kTStage tiles (one barrier per stage; the host pads every colour
-// sub-phase to whole stages, so a stage never mixes colours).
-//  * gather: R tiles are copied global -> shared with cp.async one stage
-//    ahead (double-buffered stages), so residual loads never hold registers
-//    and their latency overlaps the tensor work of the previous stage;
+// of one congruence class inside one colour sub-phase of a contiguous strip
+// of super-cells.
+//  * gather: R tiles are copied global -> shared with cp.async two tiles
+//    ahead into a 3-slot ring, so residual loads never hold registers;
 //  * Z = A^{-1} R with mma.sync.m8n8k4.f64 (DMMA); the class inverse lives in
 //    registers as A-fragments, warp w owns rows 8w..8w+7;
 //  * scatter straight from the accumulator fragments with red.global.add.f64:
-//    no read-back of u, no Z staging. The super-cell colouring guarantees that
-//    no two concurrently running tiles touch the same dof (tiles of one stage
-//    share a colour; stages are ordered by the barrier), so results are
-//    deterministic.
+//    no read-back of u, no Z staging;
+//  * no block barrier per tile: full/empty mbarriers hand the ring slots
+//    between the gather and the MMAs, so warps drift up to a tile apart and
+//    one warp's gather/scatter overlaps another's tensor work;
+//  * determinism: strips are 2x2-coloured across launches (no two running
+//    blocks share a dof) and a phase-done mbarrier orders the scatters of a
+//    block's colour sub-phases, so every red.add lands in a fixed order.
 #include "kernels.hpp"
 
 #include <cuda_runtime.h>
@@ -42,22 +43,11 @@ constexpr int kTCols = STMG_VANKA_COLS; // columns (patch, interval) per tile
 // (k = lane % 4, n = lane / 4) conflict-free.
 constexpr int kTLd = kTRows + 4;
 constexpr int kTSlot = kTCols * kTLd;
-#ifndef STMG_VANKA_STAGE
-#define STMG_VANKA_STAGE 1
-#endif
-constexpr int kTStage = STMG_VANKA_STAGE; // tiles per barrier stage
-[[maybe_unused]] constexpr int kTSlots = 2 * kTStage; // double-buffered stages (block-barrier build)
 #ifndef STMG_VANKA_MAXTILES
 #define STMG_VANKA_MAXTILES 48
 #endif
 constexpr int kTMaxTiles = STMG_VANKA_MAXTILES; // tiles per block (host falls back beyond)
-#ifndef STMG_VT_BARRIER
-// full/empty mbarrier pipeline over 3 ring slots (see vanka_tc_kernel)
-#define STMG_VT_MBAR 1
-constexpr int kTRing = 3;
-#else
-constexpr int kTRing = kTSlots;
-#endif
+constexpr int kTRing = 3; // ring slots of the full/empty mbarrier pipeline (vanka_tc_kernel)
 constexpr size_t kTSmem =
   sizeof(double) * kTRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4)) + 8 * sizeof(unsigned long long);
 
@@ -78,7 +68,6 @@ cp_async_wait0()
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-#ifndef STMG_VT_BARRIER
 // zero-filling copy: src_bytes = 0 writes 0.0 (the slot write stays async,
 // so the mbarrier pipeline tracks every write of a gather)
 __device__ __forceinline__ void
@@ -116,7 +105,6 @@ mbar_wait(unsigned long long *bar, unsigned parity)
                "r"(parity)
                : "memory");
 }
-#endif
 
 __device__ __forceinline__ void
 dmma(double (&d)[2], double a, double b)
@@ -138,10 +126,8 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
   long long *s_colp = s_colv + kTMaxTiles * kTCols;
   int *s_coln = reinterpret_cast<int *>(s_colp + kTMaxTiles * kTCols);
   VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_coln + kTMaxTiles * kTCols);
-#ifdef STMG_VT_MBAR
   // full[3], empty[3], phase-done[2]
   unsigned long long *s_bar = reinterpret_cast<unsigned long long *>(s_tile + kTMaxTiles);
-#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int t0 = tile_ptr[blockIdx.x], t1 = tile_ptr[blockIdx.x + 1];
   const int nb = t1 - t0;
@@ -215,27 +201,11 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
 #else
                 const bool valid = colok && row < nt_issue;
 #endif
-#ifdef STMG_VT_MBAR
                 cp_async8z(dst, valid ? r + (row < nvel_issue ? cv : cp) + relq[q] : r, valid);
-#else
-                if (valid)
-                  cp_async8(dst, r + (row < nvel_issue ? cv : cp) + relq[q]);
-                else
-                  *dst = 0.0;
-#endif
               }
           }
       }
   };
-  // gather of stage g (tiles kTStage*g ..) into its half of the ring
-  auto issue_stage = [&](int g) {
-#pragma unroll
-    for (int h = 0; h < kTStage; ++h)
-      issue(kTStage * g + h, (g & 1) * kTStage + h);
-    cp_async_commit(); // possibly empty group
-  };
-
-#ifdef STMG_VT_MBAR
   // Full/empty mbarrier pipeline over 3 slots: full[s] completes when every
   // thread's copies of the slot's tile have landed (cp.async arrive), so a
   // warp waits only for the tile it computes; empty[s] completes when every
@@ -259,9 +229,6 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
   cp_async_mbar_arrive(full + 0);
   issue(1, 1);
   cp_async_mbar_arrive(full + 1);
-#else
-  issue_stage(0);
-#endif
 
   int loaded = -1, nt_loaded = 0;
   double afr[KS];
@@ -270,7 +237,6 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
   double w_row = 0.0;
   const int row = 8 * warp + (lane >> 2);
 
-#ifdef STMG_VT_MBAR
   // Colour sub-phases of a block share dofs: before the first scatter of a
   // new phase, every thread's scatters of the previous phase must be done
   // (arrive = release, wait = acquire), so the red.add order -- and the
@@ -357,80 +323,6 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
         }
     }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
-#else
-
-  // Stage g: wait for its gather, barrier (its slots are visible to all, the
-  // slots of stage g-1 are free), gather stage g+1 into them, then compute
-  // the stage's tiles. Within a stage the warps drift apart, so one warp's
-  // scatter overlaps the DMMAs of another.
-  const int n_stages = (nb + kTStage - 1) / kTStage;
-  for (int g = 0; g < n_stages; ++g)
-  {
-    cp_async_wait0();
-    __syncthreads();
-    issue_stage(g + 1);
-#pragma unroll 1
-    for (int h = 0; h < kTStage; ++h)
-    {
-      const int lt = kTStage * g + h;
-      if (lt >= nb)
-        break;
-      const VankaTile tl = s_tile[lt];
-      if (tl.ncols == 0)
-        continue; // stage padding (keeps colour sub-phases in separate stages)
-      if (tl.cls != loaded)
-        {
-          const DevPatchClass pc = classes[tl.cls];
-#pragma unroll
-          for (int kk = 0; kk < KS; ++kk)
-            {
-              const int col = 4 * kk + (lane & 3);
-              afr[kk] = (row < pc.n_t && col < pc.n_t) ? __ldg(pc.inverse + row * pc.n_t + col) : 0.0;
-            }
-          ok_row = row < pc.n_t;
-          vel_row = row < pc.n_vel;
-          rel_row = ok_row ? pc.rel[row] : 0;
-          w_row = ok_row ? omega * pc.weight[row] : 0.0;
-          nt_loaded = pc.n_t;
-          loaded = tl.cls;
-        }
-      double acc[kTCols / 8][2];
-#pragma unroll
-      for (int ct = 0; ct < kTCols / 8; ++ct)
-        acc[ct][0] = acc[ct][1] = 0.0;
-      const double *bbase = ring + ((g & 1) * kTStage + h) * kTSlot + (lane >> 2) * kTLd + (lane & 3);
-      if (8 * warp < nt_loaded) // warps past n_T only join the barriers
-        {
-#pragma unroll
-          for (int kk = 0; kk < KS; ++kk)
-            {
-              const double *brow = bbase + 4 * kk;
-              constexpr int kNStep = 8 * kTLd; // next 8 columns
-#pragma unroll
-              for (int ct = 0; ct < kTCols / 8; ++ct)
-                dmma(acc[ct], afr[kk], brow[kNStep * ct]);
-            }
-        }
-      if (ok_row)
-        {
-#pragma unroll
-          for (int ct = 0; ct < kTCols / 8; ++ct)
-#pragma unroll
-            for (int b = 0; b < 2; ++b)
-              {
-                const int col = 8 * ct + 2 * (lane & 3) + b;
-                const int ci = lt * kTCols + col;
-#ifdef STMG_VT_NO_SCATTER
-                if (acc[ct][b] == 123.456)
-#else
-                if (col < tl.ncols && n0 + s_coln[ci] < n_intervals)
-#endif
-                  atomicAdd(u + base0 + (vel_row ? s_colv[ci] : s_colp[ci]) + rel_row, acc[ct][b] * w_row);
-              }
-        }
-    }
-  }
-#endif
 }
 // ---------------------------------------------------------------- factored
 // Time-diagonalised patch solves: A_T^{-1} = (V (x) I) blockdiag(B_b^{-1})
@@ -723,12 +615,6 @@ vanka_fac_supported(int S, int nsp)
 {
   return (S == 3 && (nsp == 16 || nsp == 24 || nsp == 32 || nsp == 40)) ||
          (S == 4 && (nsp == 16 || nsp == 24 || nsp == 32)) || (S == 5 && (nsp == 16 || nsp == 24));
-}
-
-int
-vanka_tc_stage()
-{
-  return kTStage;
 }
 
 int
