@@ -255,6 +255,71 @@ int stmg_plan_levels(int refinements, int r, int k, int n_steps, double t_end, i
 int stmg_patch_info(int nx, int ny, int r, int k, double tau, double nu, double gamma, int smoother_kind,
                     int64_t *out, double *inverse_out, int class_index);
 
+
+/* ------------------------------------------------------------ 3D (BASELINE C3 / C5)
+ * The reference is 2D only (dof_space.hpp:30); SURVEY.md §9 extends the same
+ * interfaces to 3D by tensor product: Q_{r+1}^3 / P_r^disc on the unit cube
+ * with a trilinear cell map, DG(k) in time. Layout:
+ * BlockVector (block_vector.hpp:13-45) with three velocity components;
+ * scalar node (Z*gy + Y)*gx + X, pressure cell ((cz*ny + cy)*nx + cx)*np + m.
+ * `vertices` (nullable = Cartesian) is host memory, (nx+1)(ny+1)(nz+1) x 3
+ * coordinates, vertex ((vz*(ny+1) + vy)*(nx+1) + vx). Parity is against the
+ * oracle's 3D restatement (oracle/src/st3d.cpp); the reference does not pin 3D.
+ * Instantiated for r in {1, 2} and k in {0, 1, 2}; cell Vanka only. */
+typedef struct stmg3_level stmg3_level;
+typedef struct stmg3_solver stmg3_solver;
+
+/* SpaceTimeBlockOperator + VankaSmoother::build (st_operator.hpp:94-165,
+ * vanka.cpp:30-194) of a 3D level. smoother_kind: STMG_SMOOTHER_NONE or
+ * STMG_SMOOTHER_CELL. */
+int stmg3_level_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
+                       int smoother_kind, const double *vertices, stmg3_level **out);
+int stmg3_level_destroy(stmg3_level *level);
+/* out[0..11] = n_slots, M^v, M^p, interval size, n_scalar, gx, gy, gz, n_p,
+ * max patch size n_T, patch classes, sum of n_T^2 over the patches. */
+int stmg3_level_sizes(const stmg3_level *level, int64_t *out);
+/* apply_block / apply_block_raw (st_operator.cpp:397-407) per interval. */
+int stmg3_apply_block(stmg3_level *level, const double *x, double *y, int n_intervals, int raw);
+/* All-at-once operator y_n = D x_n - Z C x_{n-1} (Eq. GloSys, st_operator.cpp:321-421). */
+int stmg3_vmult(stmg3_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);
+int stmg3_residual(stmg3_level *level, const double *b, const double *x, double *r, int n_intervals,
+                   const double *x_prev_slot, int coupled);
+/* VankaSmoother::apply_additive / smooth_step (vanka.cpp:196-233), cell patches. */
+int stmg3_apply_additive(stmg3_level *level, const double *r, double *out, int n_intervals);
+int stmg3_smooth_step(stmg3_level *level, const double *b, double *u, double omega, int n_intervals,
+                      const double *x_prev_slot, int coupled, double *work);
+int stmg3_vanka_update(stmg3_level *level, const double *r, double *u, double omega, int n_intervals);
+/* PressureSpace::project_mean_zero (dof_space.cpp:110-119) per slot, mapped basis. */
+int stmg3_project_mean_zero(stmg3_level *level, double *x, int n_intervals);
+
+/* hp-STMG hierarchy for the all-at-once system: p-coarsening k -> k/2 -> ... -> 0,
+ * r -> r/2 -> ... -> 1 (hierarchy.cpp:9-97 extended to k = 0), then n_hcoarse
+ * h-steps in space, each also halving the time grid when time_coarsen != 0
+ * (PAPER.md Eq. DeftPrRe). The coarsest level is solved exactly by forward
+ * substitution in time on the GPU. tau = finest interval length. */
+int stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
+                        int n_hcoarse, int time_coarsen, const double *vertices, int nu1, int nu2, double omega,
+                        double rtol, double atol, int max_iterations, stmg3_solver **out);
+int stmg3_solver_destroy(stmg3_solver *solver);
+/* out[0] = n_levels; per level l (coarse first) out[1+7l..]: nx, ny, nz, r, k,
+ * time shift (log2 of the time coarsening), interval size. */
+int stmg3_solver_info(const stmg3_solver *solver, int64_t *out);
+stmg3_level *stmg3_solver_level(stmg3_solver *solver, int l);
+int stmg3_solver_set_comm(stmg3_solver *solver, const stmg_comm_ops *ops);
+/* TransferPair::restrict_residual / prolongate_correction (transfer.cpp:102-132)
+ * between level l and l-1 on nc coarse intervals (2 nc fine ones when the
+ * pair coarsens time). */
+int stmg3_restrict_residual(stmg3_solver *solver, int l, const double *fine, double *coarse, int nc,
+                            int project_pressure);
+int stmg3_prolongate_correction(stmg3_solver *solver, int l, const double *coarse, double *fine, int nc,
+                                int project_pressure, int accumulate);
+/* Exact all-at-once solve on level 0: x_t = CoarseSolve(b_t + C x_{t-1}) (solver.cpp:43-54). */
+int stmg3_coarse_forward(stmg3_solver *solver, const double *b, double *x, int n_intervals);
+int stmg3_vcycle_all_at_once(stmg3_solver *solver, const double *b, double *x, int n_intervals);
+/* FGMRES (solver.cpp:95-202) + all-at-once V-cycle on the slab (see stmg_solve_all_at_once). */
+int stmg3_solve_all_at_once(stmg3_solver *solver, const double *F, double *X, int n_intervals, const double *v_init,
+                            int *iterations, double *residual_history, int history_cap);
+
 #ifdef __cplusplus
 }
 #endif

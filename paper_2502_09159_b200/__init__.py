@@ -90,6 +90,31 @@ _SIGNATURES = {
     "stmg_plan_levels": ([_c_int, _c_int, _c_int, _c_int, _c_double, _c_int, _c_i64p], _c_int),
     "stmg_patch_info": ([_c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int, _c_i64p,
                          ctypes.POINTER(_c_double), _c_int], _c_int),
+    "stmg3_level_create": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double,
+                            _c_int, _c_void_p, ctypes.POINTER(_c_void_p)], _c_int),
+    "stmg3_level_destroy": ([_c_void_p], _c_int),
+    "stmg3_level_sizes": ([_c_void_p, _c_i64p], _c_int),
+    "stmg3_apply_block": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int], _c_int),
+    "stmg3_vmult": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
+    "stmg3_residual": ([_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, _c_int], _c_int),
+    "stmg3_apply_additive": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
+    "stmg3_smooth_step": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int, _c_void_p],
+                          _c_int),
+    "stmg3_vanka_update": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int], _c_int),
+    "stmg3_project_mean_zero": ([_c_void_p, _c_void_p, _c_int], _c_int),
+    "stmg3_solver_create": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double,
+                             _c_int, _c_int, _c_void_p, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
+                             ctypes.POINTER(_c_void_p)], _c_int),
+    "stmg3_solver_destroy": ([_c_void_p], _c_int),
+    "stmg3_solver_info": ([_c_void_p, _c_i64p], _c_int),
+    "stmg3_solver_level": ([_c_void_p, _c_int], _c_void_p),
+    "stmg3_solver_set_comm": ([_c_void_p, _c_void_p], _c_int),
+    "stmg3_restrict_residual": ([_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int], _c_int),
+    "stmg3_prolongate_correction": ([_c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_int, _c_int], _c_int),
+    "stmg3_coarse_forward": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
+    "stmg3_vcycle_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
+    "stmg3_solve_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, ctypes.POINTER(_c_int),
+                                 ctypes.POINTER(_c_double), _c_int], _c_int),
 }
 
 
@@ -387,6 +412,133 @@ class Solver:
             self._h = None
 
 
+class Level3:
+    """3D SpaceTimeBlockOperator + cell VankaSmoother (BASELINE C3 / C5): Q_{r+1}^3 / P_r^disc on the unit cube,
+    optionally on a deformed (trilinear) mesh given by host vertex coordinates."""
+
+    def __init__(self, ctx: Context, nx: int, ny: int, nz: int, r: int, k: int, tau: float, nu: float,
+                 gamma: float = 0.0, smoother: int = SMOOTHER_CELL, vertices=None, _borrowed=None):
+        self.ctx = ctx
+        lib = load_library()
+        if _borrowed is not None:
+            self._h, self._owned = _borrowed, False
+        else:
+            h = _c_void_p()
+            _check(lib.stmg3_level_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, smoother, _hptr(vertices),
+                                          ctypes.byref(h)))
+            self._h, self._owned = h, True
+        out = (ctypes.c_int64 * 12)()
+        _check(lib.stmg3_level_sizes(self._h, out))
+        (self.n_slots, self.n_velocity, self.n_pressure, self.size, self.n_scalar, self.gx, self.gy, self.gz,
+         self.n_p, self.max_patch, self.n_patch_classes, self.total_matrix_elements) = [int(v) for v in out]
+
+    def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
+        _check(load_library().stmg3_apply_block(self._h, _ptr(x), _ptr(y), n_intervals, int(raw)))
+        return y
+
+    def vmult(self, x, y, n_intervals: int = 1, x_prev_slot=None):
+        _check(load_library().stmg3_vmult(self._h, _ptr(x), _ptr(y), n_intervals, _ptr(x_prev_slot)))
+        return y
+
+    def residual(self, b, x, r, n_intervals: int = 1, x_prev_slot=None, coupled: bool = True):
+        _check(load_library().stmg3_residual(self._h, _ptr(b), _ptr(x), _ptr(r), n_intervals, _ptr(x_prev_slot),
+                                             int(coupled)))
+        return r
+
+    def apply_additive(self, residual, out, n_intervals: int = 1):
+        _check(load_library().stmg3_apply_additive(self._h, _ptr(residual), _ptr(out), n_intervals))
+        return out
+
+    def smooth_step(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False,
+                    work=None):
+        _check(load_library().stmg3_smooth_step(self._h, _ptr(b), _ptr(u), omega, n_intervals, _ptr(x_prev_slot),
+                                                int(coupled), _ptr(work)))
+        return u
+
+    def vanka_update(self, residual, u, omega: float, n_intervals: int = 1):
+        _check(load_library().stmg3_vanka_update(self._h, _ptr(residual), _ptr(u), omega, n_intervals))
+        return u
+
+    def project_mean_zero(self, x, n_intervals: int = 1):
+        _check(load_library().stmg3_project_mean_zero(self._h, _ptr(x), n_intervals))
+        return x
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and getattr(self, "_h", None) and _lib is not None:
+            _lib.stmg3_level_destroy(self._h)
+            self._h = None
+
+
+class Solver3:
+    """3D all-at-once hp-STMG: p-coarsening in k and r, then h-coarsening in space (and time); FGMRES."""
+
+    def __init__(self, ctx: Context, nx: int, ny: int, nz: int, r: int, k: int, tau: float, nu: float = 1.0,
+                 gamma: float = 1.0, n_hcoarse: int = 1, time_coarsen: bool = True, vertices=None, nu1: int = 2,
+                 nu2: int = 2, omega: float = 0.8, rtol: float = 1e-8, atol: float = 1e-14,
+                 max_iterations: int = 200):
+        self.ctx = ctx
+        lib = load_library()
+        h = _c_void_p()
+        _check(lib.stmg3_solver_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse, int(time_coarsen),
+                                       _hptr(vertices), nu1, nu2, omega, rtol, atol, max_iterations,
+                                       ctypes.byref(h)))
+        self._h = h
+        out = (ctypes.c_int64 * (1 + 7 * 64))()
+        _check(lib.stmg3_solver_info(h, out))
+        self.n_levels = int(out[0])
+        self.level_info = [dict(nx=int(out[1 + 7 * l]), ny=int(out[2 + 7 * l]), nz=int(out[3 + 7 * l]),
+                                r=int(out[4 + 7 * l]), k=int(out[5 + 7 * l]), tshift=int(out[6 + 7 * l]),
+                                size=int(out[7 + 7 * l])) for l in range(self.n_levels)]
+        self.levels = [Level3(ctx, 0, 0, 0, 0, 0, 0, 0, _borrowed=lib.stmg3_solver_level(h, l))
+                       for l in range(self.n_levels)]
+        self.finest = self.levels[-1]
+
+    def restrict_residual(self, l: int, fine, coarse, n_coarse: int = 1, project_pressure: bool = True):
+        _check(load_library().stmg3_restrict_residual(self._h, l, _ptr(fine), _ptr(coarse), n_coarse,
+                                                      int(project_pressure)))
+        return coarse
+
+    def prolongate_correction(self, l: int, coarse, fine, n_coarse: int = 1, project_pressure: bool = True,
+                              accumulate: bool = False):
+        _check(load_library().stmg3_prolongate_correction(self._h, l, _ptr(coarse), _ptr(fine), n_coarse,
+                                                          int(project_pressure), int(accumulate)))
+        return fine
+
+    def coarse_forward(self, b, x, n_intervals: int):
+        _check(load_library().stmg3_coarse_forward(self._h, _ptr(b), _ptr(x), n_intervals))
+        return x
+
+    def set_comm(self, comm) -> None:
+        """Time-slab communicator, as Solver.set_comm."""
+        lib = load_library()
+        if comm is None:
+            self._comm = None
+            _check(lib.stmg3_solver_set_comm(self._h, None))
+            return
+        ops = _CommOps(None, comm.rank, comm.world,
+                       _HALO_FN(_guard(lambda u, s, r, n, st: comm.exchange_halo(s, r, n, st))),
+                       _REDUCE_FN(_guard(lambda u, b, n, st: comm.allreduce_sum(b, n, st))),
+                       _HALO_FN(_guard(lambda u, s, r, n, st: comm.allgather(s, r, n, st))))
+        self._comm = ops
+        _check(lib.stmg3_solver_set_comm(self._h, ctypes.byref(ops)))
+
+    def vcycle_all_at_once(self, b, x, n_intervals: int):
+        _check(load_library().stmg3_vcycle_all_at_once(self._h, _ptr(b), _ptr(x), n_intervals))
+        return x
+
+    def solve_all_at_once(self, F, X, n_intervals: int, v_init=None, history_cap: int = 256):
+        it = _c_int(0)
+        hist = (ctypes.c_double * history_cap)()
+        _check(load_library().stmg3_solve_all_at_once(self._h, _ptr(F), _ptr(X), n_intervals, _ptr(v_init),
+                                                       ctypes.byref(it), hist, history_cap))
+        return int(it.value), [hist[i] for i in range(min(history_cap, it.value + 1))]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.stmg3_solver_destroy(self._h)
+            self._h = None
+
+
 def plan_levels(refinements: int, r: int, k: int = -1, n_steps: int = 0, t_end: float = 1.0,
                 h_only: bool = False) -> dict:
     """Host-only hierarchy plan (plan_hierarchy + combine_hierarchies)."""
@@ -414,9 +566,9 @@ def exported_symbols() -> Sequence[str]:
     import re
 
     text = HEADER_PATH.read_text()
-    return sorted(set(re.findall(r"\b(stmg_[a-z_0-9]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(stmg3?_[a-z_0-9]+)\s*\(", text)))
 
 
-__all__ = ["Context", "Level", "Solver", "StmgError", "load_library", "plan_levels", "patch_info",
+__all__ = ["Context", "Level", "Solver", "Level3", "Solver3", "StmgError", "load_library", "plan_levels", "patch_info",
            "exported_symbols", "SMOOTHER_CELL", "SMOOTHER_VERTEX_STAR", "SMOOTHER_NONE", "PROBLEM_MANUFACTURED",
            "PROBLEM_CAVITY"]

@@ -1183,8 +1183,6 @@ build_patches(const LevelSpec &L, PatchKind kind)
 }
 
 // ================================================================ transfers
-namespace
-{
   Csr1D
   transpose_csr(const Csr1D &a)
   {
@@ -1255,7 +1253,6 @@ namespace
   {
     return legendre(pdisc_mode_ax(r, m), x) * legendre(pdisc_mode_ay(r, m), y);
   }
-} // namespace
 
 TransferTables
 build_transfer(const LevelSpec &c, const LevelSpec &f, TransferKind kind)

@@ -192,6 +192,10 @@ struct TransferTables
   std::vector<double> e_time; // (k_f+1) x (k_c+1) row-major
 };
 TransferTables build_transfer(const LevelSpec &coarse, const LevelSpec &fine, TransferKind kind);
+Csr1D transpose_csr(const Csr1D &a);
+/// 1D interpolation from the coarse Q_{rc+1} grid to the fine grid points
+/// (h_step: fine cells are the halves of the coarse cells).
+Csr1D interp_1d(int nc_cells, int rc, int nf_cells, int rf, bool h_step);
 
 // ---------------------------------------------------------------- coarse level
 /// Dense constrained operator of a (small) level with the first pressure dof

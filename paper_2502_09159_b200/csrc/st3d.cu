@@ -1,0 +1,907 @@
+// 3D kernels of the B200 hp-STMG path (BASELINE C3 / C5), sm_100a, FP64.
+//
+// vmult3: the space-time operator of one interval or the all-at-once system
+//   y_n = D x_n - Z C x_{n-1}[slot k]       (Eq. GloSys)
+// composed exactly as SpaceTimeBlockOperator::apply_block_impl
+// (st_operator.cpp:321-407, here with three velocity components) plus
+// coupling_rhs (st_operator.cpp:409-421). Per output slot a the temporal
+// Kronecker combination is done first on nodal values (UK = sum_b Kt(a,b) u^b
+// - lv_a v_prev, UM = sum_b Mt(a,b) u^b, PM = sum_b Mt(a,b) p^b), so each
+// slot costs one spatial Stokes cell operator:
+//   y_v^a = M UK + (nu A + gamma G) UM - B^T PM,   y_p^a = B UM.
+// The cell operator is evaluated by sum factorisation through the Gauss
+// points (r+2 per direction, st_operator.cpp:167) with the trilinear cell map
+// evaluated on the fly: Cartesian cells use the constant Jacobian, deformed
+// cells (C5) read their 8 vertices (24 doubles) instead of precomputed
+// per-point geometry.
+//
+// Mapping: a thread block holds CB cells; each cell is worked by N*N threads,
+// one per 1D line of its N^3 node / quadrature-point tile. Every
+// sum-factorisation pass loads a line into registers, applies the 1D matrix
+// (constant bank, compile-time indices) and writes the line back in place,
+// so passes need no scratch beyond 13 fields per cell in shared memory.
+// Velocity contributions are scattered with red.global.add.f64 into y, which
+// a first kernel initialises (0, b, or the identity rows of constrained
+// dofs); cell-owned pressure rows are written directly.
+#include "st3d.hpp"
+
+#include <cuda_runtime.h>
+
+namespace stmg_b200
+{
+
+namespace
+{
+template <int R>
+struct V3
+{
+  static constexpr int N = R + 2, NN = N * N, NNN = N * N * N, p = R + 1;
+  static constexpr int NP = (R + 1) * (R + 2) * (R + 3) / 6;
+  static constexpr int CB = R == 1 ? 16 : (R == 2 ? 8 : 4); // cells per block
+  static constexpr int NF = 13;                             // fields per cell
+  static constexpr int CELL = NF * NNN + NP + 24;           // doubles per cell
+  // block-wide tables (dynamic indexing): w, xq, leg, ex
+  static constexpr int TAB = 2 * N + (R + 1) * N;
+  static constexpr size_t smem() { return sizeof(double) * (CB * CELL + TAB) + sizeof(int) * 3 * NP; }
+};
+
+// 1D pass over one line: out[o] = sum_m M(o, m) in[m] (forward, M = phi /
+// dphi indexed [q * N + i]) or out[i] = sum_q M(q, i) in[q] (transpose).
+template <int N, bool T>
+__device__ __forceinline__ double
+mat(const double *M, int o, int m)
+{
+  return T ? M[m * N + o] : M[o * N + m];
+}
+
+template <int R, int S, int MODE>
+__global__ void __launch_bounds__(V3<R>::NN *V3<R>::CB)
+vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
+              double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
+{
+  using C = V3<R>;
+  constexpr int N = C::N, NN = C::NN, NNN = C::NNN, p = C::p, NP = C::NP;
+  extern __shared__ __align__(16) double sm3[];
+  double *const tw = sm3 + C::CB * C::CELL; // w[N], xq[N], leg[(R+1) * N]
+  double *const txq = tw + N;
+  double *const tleg = txq + N;
+  int *const tex = reinterpret_cast<int *>(tleg + (R + 1) * N);
+  const int tid = threadIdx.y * NN + threadIdx.x;
+  if (tid < N)
+    {
+      tw[tid] = P.w[0];
+#pragma unroll
+      for (int q = 0; q < N; ++q)
+        if (tid == q)
+          {
+            tw[q] = P.w[q];
+            txq[q] = P.xq[q];
+#pragma unroll
+            for (int a = 0; a <= R; ++a)
+              tleg[a * N + q] = P.leg[a * N + q];
+          }
+    }
+#pragma unroll
+  for (int m = 0; m < NP; ++m)
+    if (tid == m)
+      {
+        tex[3 * m] = P.ex[m][0];
+        tex[3 * m + 1] = P.ex[m][1];
+        tex[3 * m + 2] = P.ex[m][2];
+      }
+
+  const long long gc = static_cast<long long>(blockIdx.x) * C::CB + threadIdx.y;
+  const bool active = gc < n_cells_total;
+  const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
+  const int n = active ? static_cast<int>(gc / ncells) : 0;
+  const long long cell = active ? gc - n * ncells : 0;
+  const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
+            cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
+  double *const F = sm3 + threadIdx.y * C::CELL;
+  double *const PM = F + C::NF * NNN;
+  double *const X8 = PM + NP;
+  const int t = threadIdx.x;
+  const int tA = t % N, tB = t / N; // line coordinates
+  const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
+  const int gx = P.gx, gy = P.gy, gz = P.gz;
+  const bool deformed = P.verts != nullptr;
+  const double *__restrict__ xn = x + n * isz;
+  const double *__restrict__ vprev = nullptr;
+  if (coupled)
+    vprev = n > 0 ? x + (n - 1) * isz + (S - 1) * mv : xprev0;
+  if (active && deformed)
+    for (int q = t; q < 24; q += NN)
+      {
+        const int c = q / 3, d = q % 3;
+        const int vx = cx + (c & 1), vy = cy + ((c >> 1) & 1), vz = cz + (c >> 2);
+        X8[q] = __ldg(P.verts + ((static_cast<long long>(vz) * (P.ny + 1) + vy) * (P.nx + 1) + vx) * 3 + d);
+      }
+  // field indices: VK[c] = c, G[c][e] = 3 + 3c + e, QP = 12
+  auto fld = [&](int f) { return F + f * NNN; };
+
+  for (int a = 0; a < S; ++a)
+    {
+      double kt[S], mt[S], lva = 0.0;
+#pragma unroll
+      for (int aa = 0; aa < S; ++aa)
+        if (a == aa)
+          {
+#pragma unroll
+            for (int bs = 0; bs < S; ++bs)
+              {
+                kt[bs] = P.Kt[aa * S + bs];
+                mt[bs] = P.Mt[aa * S + bs];
+              }
+            lva = P.lv[aa];
+          }
+      __syncthreads(); // tables ready; previous slot's fields consumed
+      // ---- gather: x-line (j = tA, k = tB)
+      if (active)
+        {
+          const int Y = cy * p + tA, Z = cz * p + tB;
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+            {
+              const int X = cx * p + i;
+              const long long node = (static_cast<long long>(Z) * gy + Y) * gx + X;
+              const bool bnd = MODE != 2 && (X == 0 || Y == 0 || Z == 0 || X == gx - 1 || Y == gy - 1 || Z == gz - 1);
+              const int li = (tB * N + tA) * N + i;
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                {
+                  double uk = 0.0, um = 0.0;
+                  if (!bnd)
+#pragma unroll
+                    for (int bs = 0; bs < S; ++bs)
+                      {
+                        const double v = __ldg(xn + bs * mv + c * nsc + node);
+                        uk = fma(kt[bs], v, uk);
+                        um = fma(mt[bs], v, um);
+                      }
+                  if (vprev != nullptr)
+                    uk = fma(-lva, __ldg(vprev + c * nsc + node), uk);
+                  fld(c)[li] = uk;
+                  fld(3 + 3 * c)[li] = um;
+                }
+            }
+          if (t < NP)
+            {
+              double s = 0.0;
+#pragma unroll
+              for (int bs = 0; bs < S; ++bs)
+                s = fma(mt[bs], __ldg(xn + S * mv + bs * mp + cell * NP + t), s);
+              PM[t] = s;
+            }
+        }
+      __syncthreads();
+      // ---- forward passes (nodes -> Gauss points)
+      // x: VK value; UM -> A = phi_x UM (into G[c][2]), D = dphi_x UM (into G[c][0])
+      if (active)
+        {
+          const int base = (tB * N + tA) * N; // x-line
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], o1[N], o2[N];
+              double *vk = fld(c) + base;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = vk[m];
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int m = 0; m < N; ++m)
+                    s = fma(P.phi[q * N + m], in[m], s);
+                  o1[q] = s;
+                }
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                vk[q] = o1[q];
+              double *g0 = fld(3 + 3 * c) + base, *g2 = fld(5 + 3 * c) + base;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = g0[m];
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                {
+                  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                  for (int m = 0; m < N; ++m)
+                    {
+                      s1 = fma(P.phi[q * N + m], in[m], s1);
+                      s2 = fma(P.dphi[q * N + m], in[m], s2);
+                    }
+                  o1[q] = s1;
+                  o2[q] = s2;
+                }
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                {
+                  g2[q] = o1[q];
+                  g0[q] = o2[q];
+                }
+            }
+        }
+      __syncthreads();
+      // y: VK value; A -> AA (phi_y, in G[c][2]), AD (dphi_y, into G[c][1]); D -> DA (phi_y, in G[c][0])
+      if (active)
+        {
+          const int base = tB * NN + tA; // y-line (i = tA, k = tB), stride N
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], o1[N], o2[N];
+              double *vk = fld(c) + base;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = vk[m * N];
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int m = 0; m < N; ++m)
+                    s = fma(P.phi[q * N + m], in[m], s);
+                  o1[q] = s;
+                }
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                vk[q * N] = o1[q];
+              double *g0 = fld(3 + 3 * c) + base, *g1 = fld(4 + 3 * c) + base, *g2 = fld(5 + 3 * c) + base;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = g2[m * N];
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                {
+                  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                  for (int m = 0; m < N; ++m)
+                    {
+                      s1 = fma(P.phi[q * N + m], in[m], s1);
+                      s2 = fma(P.dphi[q * N + m], in[m], s2);
+                    }
+                  o1[q] = s1;
+                  o2[q] = s2;
+                }
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                {
+                  g2[q * N] = o1[q];
+                  g1[q * N] = o2[q];
+                }
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = g0[m * N];
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int m = 0; m < N; ++m)
+                    s = fma(P.phi[q * N + m], in[m], s);
+                  o1[q] = s;
+                }
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                g0[q * N] = o1[q];
+            }
+        }
+      __syncthreads();
+      // z: VK value; DA -> d/dxi (phi_z); AD -> d/deta (phi_z); AA -> d/dzeta (dphi_z)
+      if (active)
+        {
+          const int base = tB * N + tA; // z-line (i = tA, j = tB), stride NN
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+              {
+                double *fp = f == 0 ? fld(c) + base : fld(3 + 3 * c + (f - 1)) + base;
+                const bool der = f == 3;
+                double in[N], o1[N];
+#pragma unroll
+                for (int m = 0; m < N; ++m)
+                  in[m] = fp[m * NN];
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                  {
+                    double s = 0.0;
+#pragma unroll
+                    for (int m = 0; m < N; ++m)
+                      s = fma(der ? P.dphi[q * N + m] : P.phi[q * N + m], in[m], s);
+                    o1[q] = s;
+                  }
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                  fp[q * NN] = o1[q];
+              }
+        }
+      __syncthreads();
+      // ---- quadrature points: x-line (qy = tA, qz = tB)
+      if (active)
+        {
+          const double wyz = tw[tA] * tw[tB];
+#pragma unroll
+          for (int qx = 0; qx < N; ++qx)
+            {
+              const int li = (tB * N + tA) * N + qx;
+              double Ji[3][3], det;
+              if (!deformed)
+                {
+                  Ji[0][0] = 2.0 / P.hx;
+                  Ji[1][1] = 2.0 / P.hy;
+                  Ji[2][2] = 2.0 / P.hz;
+                  Ji[0][1] = Ji[0][2] = Ji[1][0] = Ji[1][2] = Ji[2][0] = Ji[2][1] = 0.0;
+                  det = 0.125 * P.hx * P.hy * P.hz;
+                }
+              else
+                {
+                  const double xi[3] = {P.xq[qx], txq[tA], txq[tB]};
+                  double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+                  for (int v = 0; v < 8; ++v)
+                    {
+                      const double n0 = (v & 1) ? 0.5 * (1 + xi[0]) : 0.5 * (1 - xi[0]);
+                      const double n1 = ((v >> 1) & 1) ? 0.5 * (1 + xi[1]) : 0.5 * (1 - xi[1]);
+                      const double n2 = (v >> 2) ? 0.5 * (1 + xi[2]) : 0.5 * (1 - xi[2]);
+                      const double d0 = (v & 1) ? 0.5 : -0.5, d1 = ((v >> 1) & 1) ? 0.5 : -0.5,
+                                   d2 = (v >> 2) ? 0.5 : -0.5;
+                      const double dN[3] = {d0 * n1 * n2, n0 * d1 * n2, n0 * n1 * d2};
+#pragma unroll
+                      for (int d = 0; d < 3; ++d)
+#pragma unroll
+                        for (int e = 0; e < 3; ++e)
+                          J[d][e] = fma(X8[3 * v + d], dN[e], J[d][e]);
+                    }
+                  det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                        J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                        J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+                  const double id = 1.0 / det;
+                  Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
+                  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+                  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+                  Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
+                  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+                  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+                  Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
+                  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+                  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+                }
+              const double wd = P.w[qx] * wyz * det;
+              // physical gradient G(c, d) = sum_e dUM_c/dxi_e Ji(e, d)
+              double G[3][3];
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                {
+                  const double g0 = fld(3 + 3 * c)[li], g1 = fld(4 + 3 * c)[li], g2 = fld(5 + 3 * c)[li];
+#pragma unroll
+                  for (int d = 0; d < 3; ++d)
+                    G[c][d] = g0 * Ji[0][d] + g1 * Ji[1][d] + g2 * Ji[2][d];
+                }
+              const double div = G[0][0] + G[1][1] + G[2][2];
+              double pq = 0.0;
+              for (int m = 0; m < NP; ++m)
+                pq = fma(tleg[tex[3 * m] * N + qx] * tleg[tex[3 * m + 1] * N + tA] * tleg[tex[3 * m + 2] * N + tB],
+                         PM[m], pq);
+              const double diag = P.gamma * div - pq;
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                {
+                  double Fp[3];
+#pragma unroll
+                  for (int d = 0; d < 3; ++d)
+                    Fp[d] = wd * (P.nu * G[c][d] + (c == d ? diag : 0.0));
+#pragma unroll
+                  for (int e = 0; e < 3; ++e)
+                    fld(3 + 3 * c + e)[li] = Fp[0] * Ji[e][0] + Fp[1] * Ji[e][1] + Fp[2] * Ji[e][2];
+                  fld(c)[li] *= wd;
+                }
+              fld(12)[li] = wd * div;
+            }
+        }
+      __syncthreads();
+      // ---- pressure rows: y_p(l) = sum_q psi_l(q) wd div(q)
+      if (active && t < NP)
+        {
+          const int e0 = tex[3 * t], e1 = tex[3 * t + 1], e2 = tex[3 * t + 2];
+          double s = 0.0;
+          for (int qz = 0; qz < N; ++qz)
+            for (int qy = 0; qy < N; ++qy)
+              {
+                const double lyz = tleg[e1 * N + qy] * tleg[e2 * N + qz];
+#pragma unroll
+                for (int qx = 0; qx < N; ++qx)
+                  s = fma(tleg[e0 * N + qx] * lyz, fld(12)[(qz * N + qy) * N + qx], s);
+              }
+          const long long o = n * isz + S * mv + a * mp + cell * NP + t;
+          y[o] = MODE == 1 ? __ldg(b + o) - s : s;
+        }
+      // ---- transpose passes (Gauss points -> nodes)
+      // z: VK <- phi_z^T VK + dphi_z^T G2; G0 <- phi_z^T G0; G1 <- phi_z^T G1
+      if (active)
+        {
+          const int base = tB * N + tA;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], in2[N], o1[N];
+              double *vk = fld(c) + base, *g2 = fld(5 + 3 * c) + base;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  in[m] = vk[m * NN];
+                  in2[m] = g2[m * NN];
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s = fma(P.phi[q * N + i], in[q], s);
+                      s = fma(P.dphi[q * N + i], in2[q], s);
+                    }
+                  o1[i] = s;
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                vk[i * NN] = o1[i];
+#pragma unroll
+              for (int f = 0; f < 2; ++f)
+                {
+                  double *fp = fld(3 + 3 * c + f) + base;
+#pragma unroll
+                  for (int m = 0; m < N; ++m)
+                    in[m] = fp[m * NN];
+#pragma unroll
+                  for (int i = 0; i < N; ++i)
+                    {
+                      double s = 0.0;
+#pragma unroll
+                      for (int q = 0; q < N; ++q)
+                        s = fma(P.phi[q * N + i], in[q], s);
+                      o1[i] = s;
+                    }
+#pragma unroll
+                  for (int i = 0; i < N; ++i)
+                    fp[i * NN] = o1[i];
+                }
+            }
+        }
+      __syncthreads();
+      // y: VK <- phi_y^T VK + dphi_y^T G1; G0 <- phi_y^T G0
+      if (active)
+        {
+          const int base = tB * NN + tA;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], in2[N], o1[N];
+              double *vk = fld(c) + base, *g1 = fld(4 + 3 * c) + base, *g0 = fld(3 + 3 * c) + base;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  in[m] = vk[m * N];
+                  in2[m] = g1[m * N];
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s = fma(P.phi[q * N + i], in[q], s);
+                      s = fma(P.dphi[q * N + i], in2[q], s);
+                    }
+                  o1[i] = s;
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                vk[i * N] = o1[i];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = g0[m * N];
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    s = fma(P.phi[q * N + i], in[q], s);
+                  o1[i] = s;
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                g0[i * N] = o1[i];
+            }
+        }
+      __syncthreads();
+      // x: y = phi_x^T VK + dphi_x^T G0, scattered straight from registers
+      if (active)
+        {
+          const int base = (tB * N + tA) * N;
+          const int Y = cy * p + tA, Z = cz * p + tB;
+          const bool yzb = Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], in2[N];
+              const double *vk = fld(c) + base, *g0 = fld(3 + 3 * c) + base;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  in[m] = vk[m];
+                  in2[m] = g0[m];
+                }
+              double *yv = y + n * isz + a * mv + c * nsc + (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s = fma(P.phi[q * N + i], in[q], s);
+                      s = fma(P.dphi[q * N + i], in2[q], s);
+                    }
+                  const int X = cx * p + i;
+                  const bool bnd = MODE != 2 && (yzb || X == 0 || X == gx - 1);
+                  if (!bnd)
+                    atomicAdd(yv + i, MODE == 1 ? -s : s);
+                }
+            }
+        }
+    }
+}
+
+/// y's velocity rows before the scatter: 0 (plain / raw), b (residual); the
+/// constrained rows get the identity x (plain) or b - x (residual),
+/// st_operator.cpp:383-394.
+template <int MODE>
+__global__ void
+vmult3_init_kernel(DevGeom3 G, const double *__restrict__ x, const double *__restrict__ b, double *__restrict__ y,
+                   long long total)
+{
+  const long long per = static_cast<long long>(G.S) * G.mv;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x)
+    {
+      const long long n = idx / per, rem = idx - n * per;
+      const long long o = n * G.isz + rem;
+      const long long s = rem % G.nsc;
+      const int X = static_cast<int>(s % G.gx), Y = static_cast<int>((s / G.gx) % G.gy),
+                Z = static_cast<int>(s / (static_cast<long long>(G.gx) * G.gy));
+      const bool bnd = X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1;
+      double v = 0.0;
+      if (MODE != 2 && bnd)
+        v = x[o];
+      if (MODE == 1)
+        v = b[o] - v;
+      y[o] = v;
+    }
+}
+
+template <int R, int S>
+cudaError_t
+launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, int nI, const double *xprev0,
+           int coupled, int mode, cudaStream_t st)
+{
+  using C = V3<R>;
+  DevGeom3 G{};
+  G.nx = P.nx;
+  G.ny = P.ny;
+  G.nz = P.nz;
+  G.gx = P.gx;
+  G.gy = P.gy;
+  G.gz = P.gz;
+  G.S = S;
+  G.np = P.np;
+  G.nsc = P.nsc;
+  G.mv = P.mv;
+  G.mp = P.mp;
+  G.isz = P.isz;
+  const long long total_v = static_cast<long long>(nI) * S * P.mv;
+  const int ib = static_cast<int>(std::min<long long>((total_v + 255) / 256, 148 * 16));
+  const long long cells = static_cast<long long>(nI) * P.nx * P.ny * P.nz;
+  dim3 block(C::NN, C::CB);
+  const unsigned grid = static_cast<unsigned>((cells + C::CB - 1) / C::CB);
+  auto go = [&](auto init, auto kern) {
+    init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::smem()));
+    kern<<<grid, block, C::smem(), st>>>(P, x, b, y, xprev0, coupled, cells);
+  };
+  switch (mode)
+    {
+      case 0: go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0>); break;
+      case 1: go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1>); break;
+      default: go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2>); break;
+    }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- aux
+__global__ void
+zero_constrained3_kernel(DevGeom3 G, double *__restrict__ x, long long total)
+{
+  const long long per = static_cast<long long>(G.S) * G.mv;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x)
+    {
+      const long long n = idx / per, rem = idx - n * per;
+      const long long s = rem % G.nsc;
+      const int X = static_cast<int>(s % G.gx), Y = static_cast<int>((s / G.gx) % G.gy),
+                Z = static_cast<int>(s / (static_cast<long long>(G.gx) * G.gy));
+      if (X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1)
+        x[n * G.isz + rem] = 0.0;
+    }
+}
+
+constexpr int kProjThreads = 512;
+__global__ void __launch_bounds__(kProjThreads)
+project3_kernel(DevGeom3 G, const double *__restrict__ pmean, double inv_vol, double *__restrict__ x)
+{
+  __shared__ double red[kProjThreads];
+  const int n = blockIdx.y, a = blockIdx.x;
+  double *pr = x + n * G.isz + G.S * G.mv + a * G.mp;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < G.mp; i += kProjThreads)
+    s = fma(pmean[i], pr[i], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kProjThreads / 2; w > 0; w >>= 1)
+    {
+      if (threadIdx.x < w)
+        red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+  const double mean = red[0] * inv_vol;
+  const long long ncell = G.mp / G.np;
+  for (long long c = threadIdx.x; c < ncell; c += kProjThreads)
+    pr[c * G.np] -= mean;
+}
+
+__global__ void
+prolongate3_kernel(DevTransfer3 T, const double *__restrict__ coarse, double *__restrict__ fine, long long total)
+{
+  const DevGeom3 &F = T.f, &Cg = T.c;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x)
+    {
+      const int n = static_cast<int>(idx / F.isz);
+      const long long rem = idx - n * F.isz;
+      const int m = T.h_time ? n / 2 : n, half = T.h_time ? (n & 1) : 0;
+      const double *cb = coarse + m * Cg.isz;
+      const double *E = T.E + half * kMaxS * kMaxS;
+      double v = 0.0;
+      if (rem < F.S * F.mv)
+        {
+          const int a = static_cast<int>(rem / F.mv);
+          const long long r2 = rem - a * F.mv;
+          const int comp = static_cast<int>(r2 / F.nsc);
+          const long long s = r2 - comp * F.nsc;
+          const int X = static_cast<int>(s % F.gx), Y = static_cast<int>((s / F.gx) % F.gy),
+                    Z = static_cast<int>(s / (static_cast<long long>(F.gx) * F.gy));
+          for (int bs = 0; bs < Cg.S; ++bs)
+            {
+              const double e = E[a * kMaxS + bs];
+              const double *cv = cb + bs * Cg.mv + comp * Cg.nsc;
+              double sv;
+              if (T.spatial)
+                {
+                  sv = 0.0;
+                  for (int kz = T.pz.ptr[Z]; kz < T.pz.ptr[Z + 1]; ++kz)
+                    for (int ky = T.py.ptr[Y]; ky < T.py.ptr[Y + 1]; ++ky)
+                      {
+                        const double wyz = T.pz.val[kz] * T.py.val[ky];
+                        const long long rowc = (static_cast<long long>(T.pz.col[kz]) * Cg.gy + T.py.col[ky]) * Cg.gx;
+                        for (int kx = T.px.ptr[X]; kx < T.px.ptr[X + 1]; ++kx)
+                          sv = fma(wyz * T.px.val[kx], cv[rowc + T.px.col[kx]], sv);
+                      }
+                }
+              else
+                sv = cv[s];
+              v = fma(e, sv, v);
+            }
+        }
+      else
+        {
+          const long long r2 = rem - F.S * F.mv;
+          const int a = static_cast<int>(r2 / F.mp);
+          const long long r3 = r2 - a * F.mp;
+          const long long cell = r3 / F.np;
+          const int mf = static_cast<int>(r3 - cell * F.np);
+          long long ccell = cell;
+          int ch = 0;
+          if (T.pmode == 1)
+            {
+              const int fx = static_cast<int>(cell % F.nx), fy = static_cast<int>((cell / F.nx) % F.ny),
+                        fz = static_cast<int>(cell / (static_cast<long long>(F.nx) * F.ny));
+              ch = (fz & 1) * 4 + (fy & 1) * 2 + (fx & 1);
+              ccell = (static_cast<long long>(fz >> 1) * Cg.ny + (fy >> 1)) * Cg.nx + (fx >> 1);
+            }
+          for (int bs = 0; bs < Cg.S; ++bs)
+            {
+              const double e = E[a * kMaxS + bs];
+              const double *cp = cb + Cg.S * Cg.mv + bs * Cg.mp + ccell * Cg.np;
+              double sv = 0.0;
+              if (T.spatial)
+                {
+                  const double *blk = T.child + (static_cast<long long>(ch) * F.np + mf) * Cg.np;
+                  for (int l = 0; l < Cg.np; ++l)
+                    sv = fma(blk[l], cp[l], sv);
+                }
+              else
+                sv = cp[mf];
+              v = fma(e, sv, v);
+            }
+        }
+      fine[idx] = v;
+    }
+}
+
+__global__ void
+restrict3_kernel(DevTransfer3 T, const double *__restrict__ fine, double *__restrict__ coarse, long long total)
+{
+  const DevGeom3 &F = T.f, &Cg = T.c;
+  const int nh = T.h_time ? 2 : 1;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x)
+    {
+      const int m = static_cast<int>(idx / Cg.isz);
+      const long long rem = idx - m * Cg.isz;
+      double v = 0.0;
+      if (rem < Cg.S * Cg.mv)
+        {
+          const int bs = static_cast<int>(rem / Cg.mv);
+          const long long r2 = rem - bs * Cg.mv;
+          const int comp = static_cast<int>(r2 / Cg.nsc);
+          const long long s = r2 - comp * Cg.nsc;
+          const int X = static_cast<int>(s % Cg.gx), Y = static_cast<int>((s / Cg.gx) % Cg.gy),
+                    Z = static_cast<int>(s / (static_cast<long long>(Cg.gx) * Cg.gy));
+          for (int h = 0; h < nh; ++h)
+            {
+              const int n = T.h_time ? 2 * m + h : m;
+              const double *E = T.E + h * kMaxS * kMaxS;
+              for (int a = 0; a < F.S; ++a)
+                {
+                  const double e = E[a * kMaxS + bs];
+                  const double *fv = fine + n * F.isz + a * F.mv + comp * F.nsc;
+                  double sv;
+                  if (T.spatial)
+                    {
+                      sv = 0.0;
+                      for (int kz = T.rz.ptr[Z]; kz < T.rz.ptr[Z + 1]; ++kz)
+                        for (int ky = T.ry.ptr[Y]; ky < T.ry.ptr[Y + 1]; ++ky)
+                          {
+                            const double wyz = T.rz.val[kz] * T.ry.val[ky];
+                            const long long rowf = (static_cast<long long>(T.rz.col[kz]) * F.gy + T.ry.col[ky]) * F.gx;
+                            for (int kx = T.rx.ptr[X]; kx < T.rx.ptr[X + 1]; ++kx)
+                              sv = fma(wyz * T.rx.val[kx], fv[rowf + T.rx.col[kx]], sv);
+                          }
+                    }
+                  else
+                    sv = fv[s];
+                  v = fma(e, sv, v);
+                }
+            }
+        }
+      else
+        {
+          const long long r2 = rem - Cg.S * Cg.mv;
+          const int bs = static_cast<int>(r2 / Cg.mp);
+          const long long r3 = r2 - bs * Cg.mp;
+          const long long ccell = r3 / Cg.np;
+          const int l = static_cast<int>(r3 - ccell * Cg.np);
+          const int ccx = static_cast<int>(ccell % Cg.nx), ccy = static_cast<int>((ccell / Cg.nx) % Cg.ny),
+                    ccz = static_cast<int>(ccell / (static_cast<long long>(Cg.nx) * Cg.ny));
+          const int nch = T.pmode == 1 ? 8 : 1;
+          for (int h = 0; h < nh; ++h)
+            {
+              const int n = T.h_time ? 2 * m + h : m;
+              const double *E = T.E + h * kMaxS * kMaxS;
+              for (int a = 0; a < F.S; ++a)
+                {
+                  const double e = E[a * kMaxS + bs];
+                  double sv = 0.0;
+                  for (int ch = 0; ch < nch; ++ch)
+                    {
+                      long long fcell = ccell;
+                      if (T.pmode == 1)
+                        fcell = (static_cast<long long>(2 * ccz + (ch >> 2)) * F.ny + 2 * ccy + ((ch >> 1) & 1)) * F.nx +
+                                2 * ccx + (ch & 1);
+                      const double *fp = fine + n * F.isz + F.S * F.mv + a * F.mp + fcell * F.np;
+                      if (T.spatial)
+                        {
+                          const double *blk = T.child + static_cast<long long>(ch) * F.np * Cg.np;
+                          for (int mf = 0; mf < F.np; ++mf)
+                            sv = fma(blk[mf * Cg.np + l], fp[mf], sv);
+                        }
+                      else
+                        sv += fp[l];
+                    }
+                  v = fma(e, sv, v);
+                }
+            }
+        }
+      coarse[idx] = v;
+    }
+}
+
+int
+grid_for(long long total)
+{
+  return static_cast<int>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 148 * 32)));
+}
+} // namespace
+
+bool
+vmult3_supported(int r, int S)
+{
+  return r >= 1 && r <= 2 && S >= 1 && S <= 3;
+}
+
+cudaError_t
+launch_vmult3(int r, int S, const Level3Consts &P, const double *x, const double *b, double *y, int nI,
+              const double *xprev0, int coupled, int mode, cudaStream_t st)
+{
+  if (nI <= 0)
+    return cudaSuccess;
+#define STMG_V3(RR, SS)                                                                                              \
+  if (r == RR && S == SS)                                                                                            \
+    return launch_rs3<RR, SS>(P, x, b, y, nI, xprev0, coupled, mode, st);
+  STMG_V3(1, 1)
+  STMG_V3(1, 2)
+  STMG_V3(1, 3)
+  STMG_V3(2, 1)
+  STMG_V3(2, 2)
+  STMG_V3(2, 3)
+#undef STMG_V3
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t
+launch_zero_constrained3(const DevGeom3 &G, double *x, int nI, cudaStream_t st)
+{
+  const long long total = static_cast<long long>(nI) * G.S * G.mv;
+  if (total == 0)
+    return cudaSuccess;
+  zero_constrained3_kernel<<<grid_for(total), 256, 0, st>>>(G, x, total);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_project3(const DevGeom3 &G, const double *pmean, double inv_vol, double *x, int nI, cudaStream_t st)
+{
+  if (nI == 0)
+    return cudaSuccess;
+  dim3 grid(G.S, nI);
+  project3_kernel<<<grid, kProjThreads, 0, st>>>(G, pmean, inv_vol, x);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_prolongate3(const DevTransfer3 &T, const double *coarse, double *fine, int nc, cudaStream_t st)
+{
+  const long long total = static_cast<long long>(T.h_time ? 2 * nc : nc) * T.f.isz;
+  if (total == 0)
+    return cudaSuccess;
+  prolongate3_kernel<<<grid_for(total), 256, 0, st>>>(T, coarse, fine, total);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_restrict3(const DevTransfer3 &T, const double *fine, double *coarse, int nc, cudaStream_t st)
+{
+  const long long total = static_cast<long long>(nc) * T.c.isz;
+  if (total == 0)
+    return cudaSuccess;
+  restrict3_kernel<<<grid_for(total), 256, 0, st>>>(T, fine, coarse, total);
+  return cudaGetLastError();
+}
+
+} // namespace stmg_b200

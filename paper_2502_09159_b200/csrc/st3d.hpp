@@ -1,0 +1,146 @@
+// 3D hp-STMG path (BASELINE configs C3 and C5): level description, device
+// constants, host setup and kernel launchers.
+//
+// The reference is 2D only (dof_space.hpp:30); SURVEY.md §9 extends it to 3D
+// by tensor product with the trilinear (Q1) cell map of PAPER.md:205-218
+// (mapped Q_{r+1}^3 velocity, mapped P_r^disc pressure). The data layout is
+// the reference BlockVector (block_vector.hpp:13-45) with three velocity
+// components:
+//   interval n            : base n * isz, isz = S * (mv + mp)
+//   velocity slot a       : a * mv;   component c : + c * nsc, mv = 3 * nsc
+//   scalar node (X, Y, Z) : (Z * gy + Y) * gx + X
+//   pressure slot a       : S * mv + a * mp; cell (cx, cy, cz), mode m :
+//                           ((cz * ny + cy) * nx + cx) * NP + m
+// Vertex coordinates (deformed meshes): ((vz * (ny+1) + vy) * (nx+1) + vx) * 3 + d.
+#pragma once
+
+#include "kernels.hpp"
+#include "setup.hpp"
+
+#include <cstdint>
+#include <vector>
+
+namespace stmg_b200
+{
+
+constexpr int kMaxNP3 = 35; // dim P_r^disc(3D), r <= 4
+
+/// Device constants of one 3D level (kernel parameter, constant bank).
+/// N = r + 2 GLL nodes = Gauss points per direction (st_operator.cpp:167).
+struct Level3Consts
+{
+  int nx, ny, nz, gx, gy, gz, np;
+  long long nsc, mv, mp, isz;
+  double phi[kMaxN1 * kMaxN1];  // phi(q, i) = l_i(x_q), row-major [q * N + i]
+  double dphi[kMaxN1 * kMaxN1]; // l_i'(x_q)
+  double w[kMaxN1];             // Gauss weights
+  double xq[kMaxN1];            // Gauss points on [-1, 1]
+  double leg[kMaxP * kMaxN1];   // Legendre P_a(x_q) [a * N + q]
+  int ex[kMaxNP3][3];           // P_r^disc mode exponents (pdisc.cpp:41-55, dim 3)
+  double Kt[kMaxS * kMaxS], Mt[kMaxS * kMaxS], lv[kMaxS];
+  double nu, gamma, hx, hy, hz;
+  const double *verts; // nullptr: Cartesian unit-cube mesh
+};
+
+struct Level3Spec
+{
+  int nx = 1, ny = 1, nz = 1, r = 1, k = 1;
+  double tau = 1.0, nu = 1.0, gamma = 0.0;
+  int n1() const { return r + 2; }
+  int p() const { return r + 1; }
+  int np() const { return (r + 1) * (r + 2) * (r + 3) / 6; }
+  int S() const { return k + 1; }
+  int gx() const { return nx * p() + 1; }
+  int gy() const { return ny * p() + 1; }
+  int gz() const { return nz * p() + 1; }
+  long long nsc() const { return static_cast<long long>(gx()) * gy() * gz(); }
+  long long mv() const { return 3 * nsc(); }
+  long long ncells() const { return static_cast<long long>(nx) * ny * nz; }
+  long long mp() const { return ncells() * np(); }
+  long long isz() const { return S() * (mv() + mp()); }
+  long long nverts() const { return static_cast<long long>(nx + 1) * (ny + 1) * (nz + 1); }
+};
+
+Level3Consts make_level3_consts(const Level3Spec &L, const double *dev_verts);
+
+/// Cartesian unit-cube vertex coordinates, optionally with the interior
+/// vertices displaced by a seeded uniform perturbation of at most
+/// `amp` * h per coordinate (BASELINE C5).
+std::vector<double> cartesian_vertices(const Level3Spec &L, double amp, unsigned seed);
+
+/// Per-cell dense element matrices (quadrature, trilinear geometry):
+/// local velocity dofs [comp][node (k*N + j)*N + i], pressure modes.
+struct Cell3Matrices
+{
+  int nv = 0, np = 0;
+  std::vector<double> mass; // nv x nv (scalar)
+  std::vector<double> a;    // 3nv x 3nv: nu grad:grad + gamma div div
+  std::vector<double> b;    // np x 3nv: int psi_l div u
+  std::vector<double> pmean; // np: int psi_l
+};
+Cell3Matrices cell3_matrices(const Level3Spec &L, const double X8[8][3]);
+void cell_vertices(const Level3Spec &L, const std::vector<double> &verts, int cx, int cy, int cz, double X8[8][3]);
+
+/// Cell-Vanka patch set of a 3D level: classes (Cartesian: by boundary
+/// status per direction, <= 27) or one class per cell (deformed meshes).
+struct Patch3Set
+{
+  std::vector<PatchClass> classes;
+  std::vector<int> cell_class; // per cell
+  std::uint64_t total_matrix_elements = 0;
+  int max_nt = 0;
+};
+Patch3Set build_patches3(const Level3Spec &L, const std::vector<double> *verts);
+
+/// Transfer between 3D levels: spatial h (1D stencils per direction and
+/// pressure child blocks), spatial p (interpolation + modal embedding), none;
+/// temporal p (E) and/or temporal h (E_left / E_right, PAPER.md Eq. DeftPrRe).
+struct Transfer3Tables
+{
+  int spatial = 0, pmode = 0, h_time = 0;
+  Csr1D px, py, pz, rx, ry, rz;
+  std::vector<double> child; // h: 8 blocks (cz*4+cy*2+cx) of np_f x np_c row-major; p: 1 block
+  std::vector<double> E;     // [half][a][b], (h_time ? 2 : 1) x S_f x S_c
+};
+Transfer3Tables build_transfer3(const Level3Spec &coarse, const Level3Spec &fine, bool h_time);
+
+/// Exact all-at-once coarse solve by forward substitution in time,
+/// x_t = G b_t + H v_{t-1}: G = P A^+ is the pinned inverse (solver.cpp:10-54)
+/// followed by the per-slot mean-zero projection, H = G C with the jump
+/// coupling C (isz x mv). Row-major; `verts` may be null (Cartesian).
+void coarse3_tables(const Level3Spec &L, const std::vector<double> *verts, std::vector<double> &G,
+                    std::vector<double> &H, std::vector<double> &pmean);
+
+/// Pressure mean vector int_K psi_l for every cell (mp doubles) and |Omega|.
+std::vector<double> pressure_mean3(const Level3Spec &L, const std::vector<double> *verts, double *volume);
+
+// ---------------------------------------------------------------- device
+struct DevGeom3
+{
+  int nx, ny, nz, gx, gy, gz, S, np;
+  long long nsc, mv, mp, isz;
+};
+DevGeom3 geom3(const Level3Spec &L);
+
+struct DevTransfer3
+{
+  int spatial, pmode, h_time;
+  DevCsr px, py, pz, rx, ry, rz;
+  const double *child;
+  double E[2 * kMaxS * kMaxS]; // [half][a * kMaxS + b]
+  DevGeom3 f, c;
+};
+
+cudaError_t launch_vmult3(int r, int S, const Level3Consts &P, const double *x, const double *b, double *y,
+                          int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t st);
+bool vmult3_supported(int r, int S);
+cudaError_t launch_zero_constrained3(const DevGeom3 &G, double *x, int n_intervals, cudaStream_t st);
+/// p -= (<pmean, p> / vol) on the constant mode, per (interval, slot);
+/// deterministic single-block reductions.
+cudaError_t launch_project3(const DevGeom3 &G, const double *pmean, double inv_vol, double *x, int n_intervals,
+                            cudaStream_t st);
+/// nc coarse intervals -> (h_time ? 2 nc : nc) fine intervals
+cudaError_t launch_prolongate3(const DevTransfer3 &T, const double *coarse, double *fine, int nc, cudaStream_t st);
+cudaError_t launch_restrict3(const DevTransfer3 &T, const double *fine, double *coarse, int nc, cudaStream_t st);
+
+} // namespace stmg_b200

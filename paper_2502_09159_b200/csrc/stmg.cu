@@ -18,137 +18,9 @@
 
 using namespace stmg_b200;
 
-namespace
-{
-thread_local std::string g_error;
+#include "runtime.hpp"
 
-struct CudaError : std::runtime_error
-{
-  using std::runtime_error::runtime_error;
-};
-
-void
-check(cudaError_t e, const char *what)
-{
-  if (e != cudaSuccess)
-    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-template <class F>
-int
-guarded(F &&f)
-{
-  try
-    {
-      f();
-      return STMG_OK;
-    }
-  catch (const std::invalid_argument &e)
-    {
-      g_error = e.what();
-      return STMG_EINVAL;
-    }
-  catch (const CudaError &e)
-    {
-      g_error = e.what();
-      return STMG_ECUDA;
-    }
-  catch (const std::exception &e)
-    {
-      g_error = e.what();
-      return STMG_ERUNTIME;
-    }
-}
-
-/// Reallocations of any DevArray: captured CUDA graphs hold raw pointers and
-/// are re-captured when this changes.
-std::atomic<uint64_t> g_reallocs{0};
-
-/// Owning device array.
-template <class T>
-struct DevArray
-{
-  T *p = nullptr;
-  size_t n = 0;
-  DevArray() = default;
-  DevArray(const DevArray &) = delete;
-  DevArray &operator=(const DevArray &) = delete;
-  DevArray(DevArray &&o) noexcept : p(o.p), n(o.n)
-  {
-    o.p = nullptr;
-    o.n = 0;
-  }
-  ~DevArray()
-  {
-    if (p)
-      cudaFree(p);
-  }
-  void
-  resize(size_t count)
-  {
-    if (count <= n)
-      return;
-    if (p)
-      cudaFree(p);
-    p = nullptr;
-    n = 0;
-    check(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)), "cudaMalloc");
-    n = count;
-    g_reallocs.fetch_add(1, std::memory_order_relaxed);
-  }
-  void
-  upload(const std::vector<T> &h)
-  {
-    resize(h.size());
-    if (!h.empty())
-      check(cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice), "upload");
-  }
-};
-} // namespace
-
-// ================================================================ context
-struct stmg_ctx
-{
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  int64_t launches = 0;
-  // copy streams + events of the pipelined host-buffer entry points
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  std::vector<cudaEvent_t> events;
-  void
-  count(int k = 1)
-  {
-    launches += k;
-  }
-  void
-  copy_streams()
-  {
-    if (!h2d)
-      check(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "stream");
-    if (!d2h)
-      check(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "stream");
-  }
-  cudaEvent_t
-  event(size_t i)
-  {
-    while (events.size() <= i)
-      {
-        cudaEvent_t e;
-        check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-        events.push_back(e);
-      }
-    return events[i];
-  }
-  ~stmg_ctx()
-  {
-    for (cudaEvent_t e : events)
-      cudaEventDestroy(e);
-    if (h2d)
-      cudaStreamDestroy(h2d);
-    if (d2h)
-      cudaStreamDestroy(d2h);
-  }
-};
+using namespace stmg_rt;
 
 // ================================================================ level
 struct stmg_level

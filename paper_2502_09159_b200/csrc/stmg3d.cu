@@ -1,0 +1,937 @@
+// C ABI (include/stmg_b200.h, "3D") and host orchestration of the 3D
+// hp-STMG path (BASELINE C3 / C5): levels with the fused space-time vmult,
+// cell-Vanka colour sweeps, the hp space-time hierarchy with h-coarsening in
+// space AND time (PAPER.md Eq. DeftPrRe) and p-coarsening in k and r, the
+// all-at-once V-cycle with an exact coarse solve by forward substitution in
+// time, and FGMRES over a time slab (time-slab partition through
+// stmg_comm_ops, as in 2D).
+#include "../../include/stmg_b200.h"
+#include "runtime.hpp"
+#include "st3d.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+using namespace stmg_b200;
+using namespace stmg_rt;
+
+namespace
+{
+__global__ void
+coarse3_step_kernel(const double *__restrict__ G, const double *__restrict__ H, int n, int mv,
+                    const double *__restrict__ b, const double *__restrict__ v, double *__restrict__ x)
+{
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n)
+    return;
+  const double *g = G + static_cast<long long>(row) * n;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32)
+    s = fma(g[j], b[j], s);
+  if (v)
+    {
+      const double *h = H + static_cast<long long>(row) * mv;
+      for (int j = lane; j < mv; j += 32)
+        s = fma(h[j], v[j], s);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0)
+    x[row] = s;
+}
+} // namespace
+
+// ================================================================ level
+struct stmg3_level
+{
+  stmg_ctx *ctx = nullptr;
+  Level3Spec spec;
+  Level3Consts consts{};
+  DevGeom3 geom{};
+  bool deformed = false;
+  std::vector<double> verts_h;
+  DevArray<double> verts, pmean, one_w;
+  double inv_vol = 1.0;
+  int smoother_kind = STMG_SMOOTHER_NONE;
+  // Vanka: classes, colour batches (8 parity colours), anchors
+  std::vector<DevArray<long long>> cls_rel;
+  std::vector<DevArray<double>> cls_weight, cls_inverse;
+  DevArray<DevPatchClass> classes;
+  DevArray<VankaBatch> batches;
+  DevArray<long long> vel_anchor, pre_anchor;
+  std::vector<int> colour_first, colour_count;
+  int max_nt = 0, n_classes = 0;
+  std::uint64_t total_matrix_elements = 0;
+  DevArray<double> work, zeros;
+
+  void
+  vmult(const double *x, const double *b, double *y, int n, const double *xprev, int coupled, int mode)
+  {
+    check(launch_vmult3(spec.r, spec.S(), consts, x, b, y, n, xprev, coupled, mode, ctx->stream), "vmult3");
+    ctx->count(2);
+  }
+  void
+  project(double *x, int n)
+  {
+    check(launch_project3(geom, pmean.p, inv_vol, x, n, ctx->stream), "project3");
+    ctx->count();
+  }
+  /// Residual (dual) vectors: remove the component along the left null
+  /// vector of the pressure rows (the constant-mode coefficients). Equal to
+  /// project() on Cartesian meshes; on deformed meshes the |K|-weighted mean
+  /// would leave restricted residuals inconsistent.
+  void
+  project_residual(double *x, int n)
+  {
+    check(launch_project3(geom, one_w.p, 1.0 / static_cast<double>(spec.ncells()), x, n, ctx->stream),
+          "project3");
+    ctx->count();
+  }
+  void
+  zero_constrained(double *x, int n)
+  {
+    check(launch_zero_constrained3(geom, x, n, ctx->stream), "zero3");
+    ctx->count();
+  }
+  void
+  vanka(const double *r, double *u, int n, double omega)
+  {
+    if (smoother_kind == STMG_SMOOTHER_NONE)
+      throw std::invalid_argument("level has no smoother");
+    for (size_t c = 0; c < colour_first.size(); ++c)
+      if (colour_count[c] > 0)
+        {
+          check(launch_vanka_colour(classes.p, batches.p + colour_first[c], nullptr, colour_count[c], max_nt,
+                                    vel_anchor.p, pre_anchor.p, r, u, spec.isz(), n, omega, ctx->stream),
+                "vanka3");
+          ctx->count();
+        }
+  }
+  double *
+  scratch(int n)
+  {
+    work.resize(static_cast<size_t>(spec.isz()) * n);
+    return work.p;
+  }
+  const double *
+  zero_vector(int n)
+  {
+    const size_t need = static_cast<size_t>(spec.isz()) * n;
+    if (zeros.n < need)
+      {
+        zeros.resize(need);
+        check(cudaMemsetAsync(zeros.p, 0, sizeof(double) * zeros.n, ctx->stream), "memset");
+      }
+    return zeros.p;
+  }
+  void
+  smooth_step(const double *b, double *u, double omega, int n, const double *xprev, int coupled, double *wbuf,
+              bool u_is_zero = false)
+  {
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("smooth_step: omega must be in (0, 1]");
+    double *r = wbuf ? wbuf : scratch(n);
+    if (u_is_zero && !coupled)
+      check(cudaMemcpyAsync(r, b, sizeof(double) * spec.isz() * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    else
+      vmult(u, b, r, n, xprev, coupled, 1);
+    vanka(r, u, n, omega);
+  }
+};
+
+namespace
+{
+void
+build_level3(stmg3_level &L, const std::vector<double> *verts_host)
+{
+  const Level3Spec &s = L.spec;
+  if (s.nx < 1 || s.ny < 1 || s.nz < 1)
+    throw std::invalid_argument("3D level: need at least one cell per direction");
+  if (!vmult3_supported(s.r, s.S()))
+    throw std::invalid_argument("3D level: instantiated for r in {1, 2}, k in {0, 1, 2}");
+  if (!(s.tau > 0.0))
+    throw std::invalid_argument("3D level: tau must be positive");
+  if (verts_host)
+    {
+      if (static_cast<long long>(verts_host->size()) != 3 * s.nverts())
+        throw std::invalid_argument("3D level: vertex array has the wrong size");
+      L.deformed = true;
+      L.verts_h = *verts_host;
+      L.verts.upload(L.verts_h);
+    }
+  L.consts = make_level3_consts(s, L.deformed ? L.verts.p : nullptr);
+  L.geom = geom3(s);
+  double vol = 1.0;
+  L.pmean.upload(pressure_mean3(s, L.deformed ? &L.verts_h : nullptr, &vol));
+  L.inv_vol = 1.0 / vol;
+  {
+    std::vector<double> one(static_cast<size_t>(s.mp()), 0.0);
+    for (long long c = 0; c < s.ncells(); ++c)
+      one[c * s.np()] = 1.0;
+    L.one_w.upload(one);
+  }
+  if (L.smoother_kind == STMG_SMOOTHER_NONE)
+    return;
+  if (L.smoother_kind != STMG_SMOOTHER_CELL)
+    throw std::invalid_argument("3D level: only cell Vanka is available in 3D");
+  const Patch3Set ps = build_patches3(s, L.deformed ? &L.verts_h : nullptr);
+  L.n_classes = static_cast<int>(ps.classes.size());
+  L.max_nt = ps.max_nt;
+  L.total_matrix_elements = ps.total_matrix_elements;
+  std::vector<DevPatchClass> dc(ps.classes.size());
+  L.cls_rel.resize(ps.classes.size());
+  L.cls_weight.resize(ps.classes.size());
+  L.cls_inverse.resize(ps.classes.size());
+  for (size_t i = 0; i < ps.classes.size(); ++i)
+    {
+      const PatchClass &pc = ps.classes[i];
+      L.cls_rel[i].upload(pc.rel);
+      L.cls_weight[i].upload(pc.weight);
+      L.cls_inverse[i].upload(pc.inverse);
+      dc[i] = DevPatchClass{pc.n_t, pc.n_vel, L.cls_rel[i].p, L.cls_weight[i].p, L.cls_inverse[i].p, 0, 0, nullptr};
+    }
+  L.classes.upload(dc);
+  // 8 parity colours: cells of one colour share no node, so a launch writes
+  // every dof at most once (read-modify-write, deterministic)
+  std::vector<VankaBatch> batches;
+  std::vector<long long> va, pa;
+  const int cols = vanka_cols_per_batch();
+  const int p = s.p();
+  for (int col = 0; col < 8; ++col)
+    {
+      L.colour_first.push_back(static_cast<int>(batches.size()));
+      std::vector<std::vector<long long>> by_class(ps.classes.size());
+      for (int cz = col >> 2; cz < s.nz; cz += 2)
+        for (int cy = (col >> 1) & 1; cy < s.ny; cy += 2)
+          for (int cx = col & 1; cx < s.nx; cx += 2)
+            by_class[ps.cell_class[(static_cast<size_t>(cz) * s.ny + cy) * s.nx + cx]].push_back(
+              (static_cast<long long>(cz) * s.ny + cy) * s.nx + cx);
+      for (size_t c = 0; c < by_class.size(); ++c)
+        for (size_t i = 0; i < by_class[c].size(); i += cols)
+          {
+            VankaBatch b{static_cast<int>(c), static_cast<int>(va.size()),
+                         static_cast<int>(std::min<size_t>(cols, by_class[c].size() - i))};
+            for (int j = 0; j < b.count; ++j)
+              {
+                const long long cell = by_class[c][i + j];
+                const int cx = static_cast<int>(cell % s.nx), cy = static_cast<int>((cell / s.nx) % s.ny),
+                          cz = static_cast<int>(cell / (static_cast<long long>(s.nx) * s.ny));
+                va.push_back((static_cast<long long>(cz * p) * s.gy() + cy * p) * s.gx() + cx * p);
+                pa.push_back(s.S() * s.mv() + cell * s.np());
+              }
+            batches.push_back(b);
+          }
+      L.colour_count.push_back(static_cast<int>(batches.size()) - L.colour_first.back());
+    }
+  L.batches.upload(batches);
+  L.vel_anchor.upload(va);
+  L.pre_anchor.upload(pa);
+}
+
+struct Solver3Level
+{
+  std::unique_ptr<stmg3_level> level;
+  int tshift = 0;
+  // transfer to the next coarser level (absent on level 0)
+  DevArray<int> csr_i[6];
+  DevArray<double> csr_v[6], child;
+  DevTransfer3 dt{};
+  DevArray<double> x, b, r, t, halo;
+};
+
+void
+upload_csr(const Csr1D &c, DevArray<int> &ip, DevArray<double> &v, DevCsr &d, std::vector<int> &colbuf)
+{
+  // ptr and col packed in one int array: [ptr (rows+1) | col]
+  colbuf.assign(c.ptr.begin(), c.ptr.end());
+  colbuf.insert(colbuf.end(), c.col.begin(), c.col.end());
+  ip.upload(colbuf);
+  v.upload(c.val);
+  d.ptr = ip.p;
+  d.col = ip.p + c.ptr.size();
+  d.val = v.p;
+}
+} // namespace
+
+// ================================================================ solver
+struct stmg3_solver
+{
+  stmg_ctx *ctx = nullptr;
+  int nu1 = 2, nu2 = 2;
+  double omega = 0.8;
+  bool project_pressure = true;
+  double rtol = 1e-8, atol = 1e-14;
+  int max_iterations = 200;
+  std::vector<std::unique_ptr<Solver3Level>> levels;
+  DevArray<double> cG, cH, cB, cX;
+  int coarse_n = 0;
+  std::vector<std::unique_ptr<DevArray<double>>> V, Z;
+  DevArray<double> w, scal, part, rhs;
+  std::vector<double> hist;
+  stmg_comm_ops comm{};
+  bool has_comm = false;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_h = nullptr;
+
+  stmg3_level &fine() { return *levels.back()->level; }
+  int rank() const { return has_comm ? comm.rank : 0; }
+  int world() const { return has_comm ? comm.world : 1; }
+  int n_at(int l, int nI_fine) const { return nI_fine >> levels[l]->tshift; }
+
+  ~stmg3_solver()
+  {
+    if (comm_stream)
+      cudaStreamDestroy(comm_stream);
+    if (ev_x)
+      cudaEventDestroy(ev_x);
+    if (ev_h)
+      cudaEventDestroy(ev_h);
+  }
+
+  // y = A x (mode 0) or b - A x (mode 1) with the jump coupling; the halo of
+  // the previous rank travels on a side stream while intervals 1..nI-1 run.
+  void
+  coupled_vmult(int l, const double *x, const double *b, double *y, int nI, int mode)
+  {
+    stmg3_level &L = *levels[l]->level;
+    if (world() == 1)
+      {
+        L.vmult(x, b, y, nI, nullptr, 1, mode);
+        return;
+      }
+    if (!comm_stream)
+      {
+        check(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking), "stream");
+        check(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming), "event");
+      }
+    const long long isz = L.spec.isz(), mv = L.spec.mv();
+    DevArray<double> &h = levels[l]->halo;
+    h.resize(mv);
+    check(cudaEventRecord(ev_x, ctx->stream), "event");
+    check(cudaStreamWaitEvent(comm_stream, ev_x, 0), "wait");
+    const double *send = x + (nI - 1) * isz + (L.spec.S() - 1) * mv;
+    if (comm.exchange_halo(comm.user, send, h.p, mv, comm_stream) != 0)
+      throw std::runtime_error("comm: exchange_halo failed");
+    check(cudaEventRecord(ev_h, comm_stream), "event");
+    if (nI > 1)
+      L.vmult(x + isz, b ? b + isz : nullptr, y + isz, nI - 1, x + (L.spec.S() - 1) * mv, 1, mode);
+    check(cudaStreamWaitEvent(ctx->stream, ev_h, 0), "wait");
+    // interval 0 alone: its init kernel must not touch intervals 1..nI-1
+    L.vmult(x, b, y, 1, rank() == 0 ? nullptr : h.p, 1, mode);
+  }
+
+  void
+  allreduce(double *buf, int n)
+  {
+    if (world() > 1 && comm.allreduce_sum(comm.user, buf, n, ctx->stream) != 0)
+      throw std::runtime_error("comm: allreduce_sum failed");
+  }
+
+  /// restrict_residual: R fine, zero constrained, project (transfer.cpp:117-132)
+  void
+  restrict_residual(int l, const double *fine_v, double *coarse_v, int nc, bool project)
+  {
+    Solver3Level &F = *levels[l];
+    stmg3_level &C = *levels[l - 1]->level;
+    check(launch_restrict3(F.dt, fine_v, coarse_v, nc, ctx->stream), "restrict3");
+    ctx->count();
+    C.zero_constrained(coarse_v, nc);
+    if (project)
+      C.project_residual(coarse_v, nc);
+  }
+
+  /// prolongate_correction (transfer.cpp:102-115), then fine (+)= result
+  void
+  prolongate_correction(int l, const double *coarse_v, double *fine_v, int nc, bool project, bool accumulate)
+  {
+    Solver3Level &F = *levels[l];
+    stmg3_level &L = *F.level;
+    const int nf = F.dt.h_time ? 2 * nc : nc;
+    const long long n = L.spec.isz() * nf;
+    F.t.resize(n);
+    check(launch_prolongate3(F.dt, coarse_v, F.t.p, nc, ctx->stream), "prolongate3");
+    ctx->count();
+    L.zero_constrained(F.t.p, nf);
+    if (project)
+      L.project(F.t.p, nf);
+    if (accumulate)
+      {
+        check(launch_axpy(n, 1.0, nullptr, 1.0, F.t.p, fine_v, ctx->stream), "axpy");
+        ctx->count();
+      }
+    else
+      check(cudaMemcpyAsync(fine_v, F.t.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+  }
+
+  /// Exact coarse solve of the all-at-once system on level 0 by forward
+  /// substitution x_t = G b_t + H v_{t-1}; every rank gathers the coarse
+  /// right-hand sides, walks the whole time axis and keeps its slab.
+  void
+  coarse_forward(const double *b_v, double *x_v, int nI)
+  {
+    const Level3Spec &sp = levels[0]->level->spec;
+    const long long per = static_cast<long long>(coarse_n) * nI;
+    const double *B = b_v;
+    if (world() > 1)
+      {
+        cB.resize(per * world());
+        if (comm.allgather(comm.user, b_v, cB.p, per, ctx->stream) != 0)
+          throw std::runtime_error("comm: allgather failed");
+        B = cB.p;
+      }
+    const int n_all = nI * world();
+    cX.resize(static_cast<size_t>(coarse_n) * n_all);
+    const int mv = static_cast<int>(sp.mv());
+    const long long v_off = (sp.S() - 1) * sp.mv();
+    const int rows_per_block = 8;
+    for (int t = 0; t < n_all; ++t)
+      {
+        coarse3_step_kernel<<<(coarse_n + rows_per_block - 1) / rows_per_block, 32 * rows_per_block, 0,
+                              ctx->stream>>>(cG.p, cH.p, coarse_n, mv, B + static_cast<long long>(t) * coarse_n,
+                                             t > 0 ? cX.p + static_cast<long long>(t - 1) * coarse_n + v_off : nullptr,
+                                             cX.p + static_cast<long long>(t) * coarse_n);
+        check(cudaGetLastError(), "coarse3_step");
+        ctx->count();
+      }
+    check(cudaMemcpyAsync(x_v, cX.p + static_cast<long long>(rank()) * per, sizeof(double) * per,
+                          cudaMemcpyDeviceToDevice, ctx->stream),
+          "copy");
+  }
+
+  /// All-at-once VCycle::cycle (solver.cpp:69-93); nI = intervals of level l.
+  void
+  cycle(int l, const double *b_v, double *x_v, int nI)
+  {
+    if (l == 0)
+      {
+        coarse_forward(b_v, x_v, nI);
+        return;
+      }
+    Solver3Level &S = *levels[l];
+    stmg3_level &L = *S.level;
+    const long long isz = L.spec.isz() * nI;
+    S.r.resize(isz);
+    check(cudaMemsetAsync(x_v, 0, sizeof(double) * isz, ctx->stream), "memset");
+    for (int s = 0; s < nu1; ++s)
+      {
+        if (s == 0) // x = 0 on every rank: b - A 0 = b
+          L.smooth_step(b_v, x_v, omega, nI, nullptr, 0, S.r.p, true);
+        else
+          {
+            coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
+            L.vanka(S.r.p, x_v, nI, omega);
+          }
+      }
+    coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
+    Solver3Level &C = *levels[l - 1];
+    const int nc = S.dt.h_time ? nI / 2 : nI;
+    const long long csz = C.level->spec.isz() * nc;
+    C.b.resize(csz);
+    C.x.resize(csz);
+    restrict_residual(l, S.r.p, C.b.p, nc, project_pressure);
+    cycle(l - 1, C.b.p, C.x.p, nc);
+    prolongate_correction(l, C.x.p, x_v, nc, project_pressure, true);
+    for (int s = 0; s < nu2; ++s)
+      {
+        coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
+        L.vanka(S.r.p, x_v, nI, omega);
+      }
+  }
+
+  void
+  check_slab(int nI) const
+  {
+    const int tmax = levels.front()->tshift;
+    if (nI < 1 || (nI % (1 << tmax)) != 0)
+      throw std::invalid_argument("3D all-at-once: the slab's interval count must be divisible by 2^(time coarsenings)");
+  }
+
+  double
+  dot(const double *a, const double *b, long long n, int slot)
+  {
+    check(launch_dot(a, b, n, part.p, scal.p + slot, ctx->stream), "dot");
+    ctx->count(2);
+    allreduce(scal.p + slot, 1);
+    double h = 0.0;
+    check(cudaMemcpyAsync(&h, scal.p + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    check(cudaStreamSynchronize(ctx->stream), "sync");
+    return h;
+  }
+
+  DevArray<double> &
+  basis(std::vector<std::unique_ptr<DevArray<double>>> &B, int j, long long n)
+  {
+    while (static_cast<int>(B.size()) <= j)
+      B.push_back(std::make_unique<DevArray<double>>());
+    B[j]->resize(n);
+    return *B[j];
+  }
+
+  /// gmres (solver.cpp:95-202): right preconditioning with the all-at-once
+  /// V-cycle, modified Gram-Schmidt with device-resident coefficients,
+  /// Givens rotations on the host, Z stored (flexible form).
+  int
+  gmres(const double *b_v, double *x_v, int *iterations, double *history, int history_cap, int nI)
+  {
+    stmg3_level &L = fine();
+    const int top = static_cast<int>(levels.size()) - 1;
+    const long long n = L.spec.isz() * nI;
+    w.resize(n);
+    part.resize(dot_partials());
+    scal.resize(2 * (max_iterations + 2));
+    hist.clear();
+    const double norm_b = std::sqrt(dot(b_v, b_v, n, 0));
+    const double tol = std::max(rtol * norm_b, atol);
+    hist.push_back(norm_b);
+    check(cudaMemsetAsync(x_v, 0, sizeof(double) * n, ctx->stream), "memset");
+    int iters = 0;
+    bool converged = norm_b <= tol;
+    if (!converged)
+      {
+        const int m = max_iterations;
+        std::vector<double> H(static_cast<size_t>(m + 1) * m, 0.0), g(m + 1, 0.0), cs(m), sn(m);
+        g[0] = norm_b;
+        DevArray<double> &v0 = basis(V, 0, n);
+        check(cudaMemcpyAsync(v0.p, b_v, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+        check(launch_scale(n, 1.0 / norm_b, v0.p, ctx->stream), "scale");
+        ctx->count();
+        int j = 0;
+        std::vector<double> hcol(m + 2);
+        for (; j < m; ++j)
+          {
+            DevArray<double> &zj = basis(Z, j, n);
+            cycle(top, V[j]->p, zj.p, nI);
+            coupled_vmult(top, zj.p, nullptr, w.p, nI, 0);
+            for (int i = 0; i <= j; ++i)
+              {
+                check(launch_dot(w.p, V[i]->p, n, part.p, scal.p + i, ctx->stream), "dot");
+                allreduce(scal.p + i, 1);
+                check(launch_axpy(n, 0.0, scal.p + i, -1.0, V[i]->p, w.p, ctx->stream), "axpy");
+                ctx->count(3);
+              }
+            check(launch_dot(w.p, w.p, n, part.p, scal.p + j + 1, ctx->stream), "dot");
+            allreduce(scal.p + j + 1, 1);
+            ctx->count(2);
+            check(cudaMemcpyAsync(hcol.data(), scal.p, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->stream),
+                  "d2h");
+            check(cudaStreamSynchronize(ctx->stream), "sync");
+            const double h_next = std::sqrt(hcol[j + 1]);
+            const bool breakdown = !(h_next > 1e-300);
+            auto Hc = [&](int i) -> double & { return H[static_cast<size_t>(j) * (m + 1) + i]; };
+            for (int i = 0; i <= j; ++i)
+              Hc(i) = hcol[i];
+            for (int i = 0; i < j; ++i)
+              {
+                const double tt = cs[i] * Hc(i) + sn[i] * Hc(i + 1);
+                Hc(i + 1) = -sn[i] * Hc(i) + cs[i] * Hc(i + 1);
+                Hc(i) = tt;
+              }
+            const double denom = std::hypot(Hc(j), h_next);
+            cs[j] = Hc(j) / denom;
+            sn[j] = h_next / denom;
+            Hc(j) = denom;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            const double res = std::abs(g[j + 1]);
+            hist.push_back(res);
+            if (res <= tol || breakdown)
+              {
+                ++j;
+                converged = true;
+                break;
+              }
+            DevArray<double> &vn = basis(V, j + 1, n);
+            check(cudaMemcpyAsync(vn.p, w.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+            check(launch_scale(n, 1.0 / h_next, vn.p, ctx->stream), "scale");
+            ctx->count();
+          }
+        iters = std::min(j, m);
+        std::vector<double> y(iters);
+        for (int i = iters - 1; i >= 0; --i)
+          {
+            double s = g[i];
+            for (int c = i + 1; c < iters; ++c)
+              s -= H[static_cast<size_t>(c) * (m + 1) + i] * y[c];
+            y[i] = s / H[static_cast<size_t>(i) * (m + 1) + i];
+          }
+        for (int i = 0; i < iters; ++i)
+          {
+            check(launch_axpy(n, y[i], nullptr, 1.0, Z[i]->p, x_v, ctx->stream), "axpy");
+            ctx->count();
+          }
+      }
+    if (iterations)
+      *iterations = iters;
+    for (int i = 0; history && i < history_cap && i < static_cast<int>(hist.size()); ++i)
+      history[i] = hist[i];
+    if (!converged)
+      throw std::runtime_error("gmres: not converged within max_iterations");
+    return iters;
+  }
+
+  int
+  solve(const double *F, double *X, int nI, const double *v_init, int *iterations, double *history, int cap)
+  {
+    check_slab(nI);
+    stmg3_level &L = fine();
+    const long long n = L.spec.isz() * nI;
+    rhs.resize(n);
+    check(cudaMemcpyAsync(rhs.p, F, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    if (v_init && rank() == 0)
+      {
+        // F_0 += C v_init (coupling_rhs, constrained rows zero)
+        L.vmult(L.zero_vector(1), F, rhs.p, 1, v_init, 1, 1);
+        L.zero_constrained(rhs.p, 1);
+      }
+    const int it = gmres(rhs.p, X, iterations, history, cap, nI);
+    L.project(X, nI);
+    return it;
+  }
+};
+
+namespace
+{
+stmg3_level *
+make_level3(stmg_ctx *ctx, const Level3Spec &s, int smoother, const std::vector<double> *verts)
+{
+  auto L = std::make_unique<stmg3_level>();
+  L->ctx = ctx;
+  L->spec = s;
+  L->smoother_kind = smoother;
+  build_level3(*L, verts);
+  return L.release();
+}
+} // namespace
+
+extern "C" {
+
+int
+stmg3_level_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
+                   int smoother_kind, const double *vertices, stmg3_level **out)
+{
+  return guarded([&] {
+    if (!ctx || !out)
+      throw std::invalid_argument("null argument");
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    Level3Spec s;
+    s.nx = nx;
+    s.ny = ny;
+    s.nz = nz;
+    s.r = r;
+    s.k = k;
+    s.tau = tau;
+    s.nu = nu;
+    s.gamma = gamma;
+    std::vector<double> v;
+    if (vertices)
+      v.assign(vertices, vertices + 3 * s.nverts());
+    *out = make_level3(ctx, s, smoother_kind, vertices ? &v : nullptr);
+  });
+}
+
+int
+stmg3_level_destroy(stmg3_level *level)
+{
+  delete level;
+  return STMG_OK;
+}
+
+int
+stmg3_level_sizes(const stmg3_level *L, int64_t *out)
+{
+  return guarded([&] {
+    if (!L || !out)
+      throw std::invalid_argument("null argument");
+    const Level3Spec &s = L->spec;
+    const int64_t v[12] = {s.S(), s.mv(), s.mp(), s.isz(), s.nsc(), s.gx(), s.gy(), s.gz(), s.np(), L->max_nt,
+                           L->n_classes, static_cast<int64_t>(L->total_matrix_elements)};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
+int
+stmg3_apply_block(stmg3_level *L, const double *x, double *y, int n, int raw)
+{
+  return guarded([&] { L->vmult(x, nullptr, y, n, nullptr, 0, raw ? 2 : 0); });
+}
+
+int
+stmg3_vmult(stmg3_level *L, const double *x, double *y, int n, const double *x_prev_slot)
+{
+  return guarded([&] { L->vmult(x, nullptr, y, n, x_prev_slot, 1, 0); });
+}
+
+int
+stmg3_residual(stmg3_level *L, const double *b, const double *x, double *r, int n, const double *x_prev_slot,
+               int coupled)
+{
+  return guarded([&] { L->vmult(x, b, r, n, x_prev_slot, coupled ? 1 : 0, 1); });
+}
+
+int
+stmg3_apply_additive(stmg3_level *L, const double *r, double *out, int n)
+{
+  return guarded([&] {
+    check(cudaMemsetAsync(out, 0, sizeof(double) * L->spec.isz() * n, L->ctx->stream), "memset");
+    L->vanka(r, out, n, 1.0);
+  });
+}
+
+int
+stmg3_smooth_step(stmg3_level *L, const double *b, double *u, double omega, int n, const double *x_prev_slot,
+                  int coupled, double *work)
+{
+  return guarded([&] { L->smooth_step(b, u, omega, n, x_prev_slot, coupled ? 1 : 0, work); });
+}
+
+int
+stmg3_vanka_update(stmg3_level *L, const double *r, double *u, double omega, int n)
+{
+  return guarded([&] {
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("vanka_update: omega must be in (0, 1]");
+    L->vanka(r, u, n, omega);
+  });
+}
+
+int
+stmg3_project_mean_zero(stmg3_level *L, double *x, int n)
+{
+  return guarded([&] { L->project(x, n); });
+}
+
+int
+stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
+                    int n_hcoarse, int time_coarsen, const double *vertices, int nu1, int nu2, double omega,
+                    double rtol, double atol, int max_iterations, stmg3_solver **out)
+{
+  return guarded([&] {
+    if (!ctx || !out)
+      throw std::invalid_argument("null argument");
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("omega must be in (0, 1]");
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    auto S = std::make_unique<stmg3_solver>();
+    S->ctx = ctx;
+    S->nu1 = nu1;
+    S->nu2 = nu2;
+    S->omega = omega;
+    S->rtol = rtol;
+    S->atol = atol;
+    S->max_iterations = max_iterations;
+    // plan (fine first): p in time k -> k/2 ... -> 0, p in space r -> r/2
+    // ... -> 1, then n_hcoarse h-steps in space (and time)
+    struct D
+    {
+      Level3Spec s;
+      int tsh;
+    };
+    std::vector<D> d;
+    Level3Spec f;
+    f.nx = nx;
+    f.ny = ny;
+    f.nz = nz;
+    f.r = r;
+    f.k = k;
+    f.tau = tau;
+    f.nu = nu;
+    f.gamma = gamma;
+    d.push_back({f, 0});
+    while (d.back().s.k > 0)
+      {
+        D e = d.back();
+        e.s.k /= 2;
+        d.push_back(e);
+      }
+    while (d.back().s.r > 1)
+      {
+        D e = d.back();
+        e.s.r /= 2;
+        d.push_back(e);
+      }
+    for (int i = 0; i < n_hcoarse; ++i)
+      {
+        D e = d.back();
+        if (e.s.nx % 2 || e.s.ny % 2 || e.s.nz % 2)
+          throw std::invalid_argument("3D solver: mesh not divisible for h-coarsening");
+        e.s.nx /= 2;
+        e.s.ny /= 2;
+        e.s.nz /= 2;
+        if (time_coarsen)
+          {
+            e.tsh += 1;
+            e.s.tau *= 2.0;
+          }
+        d.push_back(e);
+      }
+    // geometry of every level: the finest vertices restricted to the coarse
+    // vertex set (nested index sets; non-nested geometry on deformed meshes)
+    std::vector<std::vector<double>> vv(d.size());
+    if (vertices)
+      {
+        vv[0].assign(vertices, vertices + 3 * f.nverts());
+        for (size_t i = 1; i < d.size(); ++i)
+          {
+            const Level3Spec &c = d[i].s;
+            const Level3Spec &fs = d[0].s;
+            const int ratio = fs.nx / c.nx;
+            vv[i].resize(3 * c.nverts());
+            for (int vz = 0; vz <= c.nz; ++vz)
+              for (int vy = 0; vy <= c.ny; ++vy)
+                for (int vx = 0; vx <= c.nx; ++vx)
+                  for (int q = 0; q < 3; ++q)
+                    vv[i][((static_cast<size_t>(vz) * (c.ny + 1) + vy) * (c.nx + 1) + vx) * 3 + q] =
+                      vv[0][((static_cast<size_t>(vz * ratio) * (fs.ny + 1) + vy * ratio) * (fs.nx + 1) + vx * ratio) *
+                              3 + q];
+          }
+      }
+    for (size_t i = d.size(); i-- > 0;)
+      {
+        auto SL = std::make_unique<Solver3Level>();
+        SL->tshift = d[i].tsh;
+        SL->level.reset(make_level3(ctx, d[i].s, i + 1 == d.size() ? STMG_SMOOTHER_NONE : STMG_SMOOTHER_CELL,
+                                    vertices ? &vv[i] : nullptr));
+        S->levels.push_back(std::move(SL));
+      }
+    for (size_t l = 1; l < S->levels.size(); ++l)
+      {
+        Solver3Level &F = *S->levels[l];
+        const Level3Spec &cs = S->levels[l - 1]->level->spec, &fs = F.level->spec;
+        const bool ht = S->levels[l - 1]->tshift > F.tshift;
+        const Transfer3Tables t = build_transfer3(cs, fs, ht);
+        DevTransfer3 &dt = F.dt;
+        dt = DevTransfer3{};
+        dt.spatial = t.spatial;
+        dt.pmode = t.pmode;
+        dt.h_time = t.h_time;
+        std::vector<int> buf;
+        if (t.spatial)
+          {
+            const Csr1D *cc[6] = {&t.px, &t.py, &t.pz, &t.rx, &t.ry, &t.rz};
+            DevCsr *dd[6] = {&dt.px, &dt.py, &dt.pz, &dt.rx, &dt.ry, &dt.rz};
+            for (int q = 0; q < 6; ++q)
+              upload_csr(*cc[q], F.csr_i[q], F.csr_v[q], *dd[q], buf);
+            F.child.upload(t.child);
+            dt.child = F.child.p;
+          }
+        const int Sf = fs.S(), Sc = cs.S();
+        for (int h = 0; h < 2; ++h)
+          for (int a = 0; a < Sf; ++a)
+            for (int b = 0; b < Sc; ++b)
+              dt.E[h * kMaxS * kMaxS + a * kMaxS + b] = t.E[(static_cast<size_t>(h) * Sf + a) * Sc + b];
+        dt.f = F.level->geom;
+        dt.c = S->levels[l - 1]->level->geom;
+      }
+    // coarse level: G, H of the forward substitution
+    {
+      const stmg3_level &L0 = *S->levels[0]->level;
+      std::vector<double> G, H, pm;
+      coarse3_tables(L0.spec, L0.deformed ? &L0.verts_h : nullptr, G, H, pm);
+      S->cG.upload(G);
+      S->cH.upload(H);
+      S->coarse_n = static_cast<int>(L0.spec.isz());
+    }
+    *out = S.release();
+  });
+}
+
+int
+stmg3_solver_destroy(stmg3_solver *s)
+{
+  delete s;
+  return STMG_OK;
+}
+
+int
+stmg3_solver_info(const stmg3_solver *s, int64_t *out)
+{
+  return guarded([&] {
+    out[0] = static_cast<int64_t>(s->levels.size());
+    for (size_t l = 0; l < s->levels.size(); ++l)
+      {
+        const Level3Spec &sp = s->levels[l]->level->spec;
+        int64_t *o = out + 1 + 7 * l;
+        o[0] = sp.nx;
+        o[1] = sp.ny;
+        o[2] = sp.nz;
+        o[3] = sp.r;
+        o[4] = sp.k;
+        o[5] = s->levels[l]->tshift;
+        o[6] = sp.isz();
+      }
+  });
+}
+
+stmg3_level *
+stmg3_solver_level(stmg3_solver *s, int l)
+{
+  if (!s || l < 0 || l >= static_cast<int>(s->levels.size()))
+    return nullptr;
+  return s->levels[l]->level.get();
+}
+
+int
+stmg3_solver_set_comm(stmg3_solver *s, const stmg_comm_ops *ops)
+{
+  return guarded([&] {
+    if (ops)
+      {
+        if (ops->world < 1 || ops->rank < 0 || ops->rank >= ops->world || !ops->exchange_halo ||
+            !ops->allreduce_sum || !ops->allgather)
+          throw std::invalid_argument("invalid communicator");
+        s->comm = *ops;
+        s->has_comm = true;
+      }
+    else
+      s->has_comm = false;
+  });
+}
+
+int
+stmg3_restrict_residual(stmg3_solver *s, int l, const double *fine, double *coarse, int nc, int project)
+{
+  return guarded([&] {
+    if (l < 1 || l >= static_cast<int>(s->levels.size()))
+      throw std::invalid_argument("level out of range");
+    s->restrict_residual(l, fine, coarse, nc, project != 0);
+  });
+}
+
+int
+stmg3_prolongate_correction(stmg3_solver *s, int l, const double *coarse, double *fine, int nc, int project,
+                            int accumulate)
+{
+  return guarded([&] {
+    if (l < 1 || l >= static_cast<int>(s->levels.size()))
+      throw std::invalid_argument("level out of range");
+    s->prolongate_correction(l, coarse, fine, nc, project != 0, accumulate != 0);
+  });
+}
+
+int
+stmg3_coarse_forward(stmg3_solver *s, const double *b, double *x, int n)
+{
+  return guarded([&] { s->coarse_forward(b, x, n); });
+}
+
+int
+stmg3_vcycle_all_at_once(stmg3_solver *s, const double *b, double *x, int n)
+{
+  return guarded([&] {
+    s->check_slab(n);
+    s->cycle(static_cast<int>(s->levels.size()) - 1, b, x, n);
+  });
+}
+
+int
+stmg3_solve_all_at_once(stmg3_solver *s, const double *F, double *X, int n, const double *v_init, int *iterations,
+                        double *history, int history_cap)
+{
+  return guarded([&] { s->solve(F, X, n, v_init, iterations, history, history_cap); });
+}
+
+} // extern "C"
