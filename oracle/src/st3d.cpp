@@ -894,6 +894,8 @@ struct Hier3
   }
 };
 
+int g_kmin = 0; // lowest temporal degree of the p-coarsening (0: k -> ... -> 0)
+
 /// Default C3-type plan: finest (nx,ny,nz, r, k, N); p-coarsen k -> 0 (via
 /// k/2 steps), then h-coarsen space and time together while the mesh and N
 /// stay even and above (cmin, nmin).
@@ -907,7 +909,7 @@ plan(int nx, int ny, int nz, int r, int k, int N, double t_end, double nu, doubl
   };
   std::vector<Desc> d; // fine first
   d.push_back({nx, ny, nz, r, k, 0});
-  while (d.back().k > 0)
+  while (d.back().k > g_kmin)
     {
       Desc e = d.back();
       e.k = e.k / 2;
@@ -1081,6 +1083,12 @@ int
 o3_project_mean_zero(void *h, double *p)
 {
   return guard3([&] { static_cast<Level3 *>(h)->project_mean_zero(p); });
+}
+
+void
+o3_set_kmin(int kmin)
+{
+  oracle::o3::g_kmin = kmin;
 }
 
 int

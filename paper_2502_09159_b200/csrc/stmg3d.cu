@@ -706,7 +706,7 @@ stmg3_project_mean_zero(stmg3_level *L, double *x, int n)
 
 int
 stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
-                    int n_hcoarse, int time_coarsen, const double *vertices, int nu1, int nu2, double omega,
+                    int n_hcoarse, int time_coarsen, int k_min, const double *vertices, int nu1, int nu2, double omega,
                     double rtol, double atol, int max_iterations, stmg3_solver **out)
 {
   return guarded([&] {
@@ -741,7 +741,9 @@ stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double 
     f.nu = nu;
     f.gamma = gamma;
     d.push_back({f, 0});
-    while (d.back().s.k > 0)
+    if (k_min < 0 || k_min > k)
+      throw std::invalid_argument("3D solver: need 0 <= k_min <= k");
+    while (d.back().s.k > k_min)
       {
         D e = d.back();
         e.s.k /= 2;

@@ -41,6 +41,7 @@ def lib():
         L.o3_hier_vcycle.argtypes = [_P, _D, _D, _I]
         L.o3_hier_fgmres.argtypes = [_P, _D, _D, _I, _F, _I, ctypes.POINTER(_I)]
         L.o3_direct_time_march.argtypes = [_P, _D, _D, _I]
+        L.o3_set_kmin.argtypes = [_I]
         _set = True
     return L
 
@@ -108,7 +109,8 @@ class OracleLevel3:
 
 class OracleHier3:
     def __init__(self, nx, ny, nz, r, k, N, t_end=1.0, nu=1.0, gamma=1.0, n_hcoarse=1, time_coarsen=True,
-                 vertices=None, nu1=2, nu2=2, omega=0.8):
+                 vertices=None, nu1=2, nu2=2, omega=0.8, k_min=0):
+        lib().o3_set_kmin(k_min)
         h = _P()
         _chk(lib().o3_hier_create(nx, ny, nz, r, k, N, t_end, nu, gamma, n_hcoarse, int(time_coarsen), _d(vertices),
                                   nu1, nu2, omega, ctypes.byref(h)))

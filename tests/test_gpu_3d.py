@@ -89,19 +89,21 @@ def test_single_cell_whole_domain_patch3(stmg, ctx, oracle):
     assert _rel(u.cpu().numpy(), ref.smooth_step_all(b, np.zeros(ref.size), 1.0, 1)) <= 1e-10
 
 
-HIER = [  # nx, r, k, N, n_hcoarse, amp
-    (2, 1, 1, 2, 1, 0.0),
-    (4, 1, 1, 4, 2, 0.0),
-    (2, 2, 2, 2, 1, 0.0),
-    (4, 1, 1, 2, 1, 0.1),
+HIER = [  # nx, r, k, N, n_hcoarse, amp, time_coarsen, k_min
+    (2, 1, 1, 2, 1, 0.0, True, 0),
+    (4, 1, 1, 4, 2, 0.0, True, 0),
+    (2, 2, 2, 2, 1, 0.0, True, 0),
+    (4, 1, 1, 2, 1, 0.1, True, 0),
+    (4, 1, 1, 3, 2, 0.0, False, 1),
+    (2, 2, 2, 2, 1, 0.1, False, 2),
 ]
 
 
-def _pair(stmg, ctx, nx, r, k, N, nh, amp, rtol=1e-8):
+def _pair(stmg, ctx, nx, r, k, N, nh, amp, tc, kmin, rtol=1e-8):
     verts = o3.vertices(nx, nx, nx, amp, seed=4) if amp else None
-    H = o3.OracleHier3(nx, nx, nx, r, k, N, t_end=N / 8.0, n_hcoarse=nh, time_coarsen=True, vertices=verts)
-    S = stmg.Solver3(ctx, nx, nx, nx, r, k, 1.0 / 8, 1.0, 1.0, n_hcoarse=nh, time_coarsen=True, vertices=verts,
-                     rtol=rtol)
+    H = o3.OracleHier3(nx, nx, nx, r, k, N, t_end=N / 8.0, n_hcoarse=nh, time_coarsen=tc, vertices=verts, k_min=kmin)
+    S = stmg.Solver3(ctx, nx, nx, nx, r, k, 1.0 / 8, 1.0, 1.0, n_hcoarse=nh, time_coarsen=tc, k_min=kmin,
+                     vertices=verts, rtol=rtol)
     assert [(l["nx"], l["r"], l["k"], l["tshift"], l["size"]) for l in S.level_info] == \
         [(l["nx"], l["r"], l["k"], l["tshift"], l["size"]) for l in H.levels]
     return H, S
@@ -128,9 +130,9 @@ def _zero_bnd(lvl_ref, x, n):
     return x.reshape(-1)
 
 
-@pytest.mark.parametrize("nx,r,k,N,nh,amp", HIER)
-def test_transfers3_match_oracle(stmg, ctx, oracle, nx, r, k, N, nh, amp):
-    H, S = _pair(stmg, ctx, nx, r, k, N, nh, amp)
+@pytest.mark.parametrize("nx,r,k,N,nh,amp,tc,kmin", HIER)
+def test_transfers3_match_oracle(stmg, ctx, oracle, nx, r, k, N, nh, amp, tc, kmin):
+    H, S = _pair(stmg, ctx, nx, r, k, N, nh, amp, tc, kmin)
     rng = np.random.default_rng(5)
     nI = N
     for l in range(H.n_levels - 1, 0, -1):
@@ -151,9 +153,9 @@ def test_transfers3_match_oracle(stmg, ctx, oracle, nx, r, k, N, nh, amp):
         nI = nc
 
 
-@pytest.mark.parametrize("nx,r,k,N,nh,amp", HIER)
-def test_coarse_forward_and_vcycle3_match_oracle(stmg, ctx, oracle, nx, r, k, N, nh, amp):
-    H, S = _pair(stmg, ctx, nx, r, k, N, nh, amp)
+@pytest.mark.parametrize("nx,r,k,N,nh,amp,tc,kmin", HIER)
+def test_coarse_forward_and_vcycle3_match_oracle(stmg, ctx, oracle, nx, r, k, N, nh, amp, tc, kmin):
+    H, S = _pair(stmg, ctx, nx, r, k, N, nh, amp, tc, kmin)
     c0 = H.level[0]
     n0 = N >> H.levels[0]["tshift"]
     bc = o3.make_consistent3(np.random.default_rng(6).uniform(-1, 1, n0 * c0.size), c0, n0)
@@ -167,11 +169,11 @@ def test_coarse_forward_and_vcycle3_match_oracle(stmg, ctx, oracle, nx, r, k, N,
     assert _rel(x.cpu().numpy(), H.vcycle(b, N)) <= 1e-10
 
 
-@pytest.mark.parametrize("nx,r,k,N,nh,amp", HIER)
-def test_fgmres3_solve_matches_time_marched(stmg, ctx, oracle, nx, r, k, N, nh, amp):
+@pytest.mark.parametrize("nx,r,k,N,nh,amp,tc,kmin", HIER)
+def test_fgmres3_solve_matches_time_marched(stmg, ctx, oracle, nx, r, k, N, nh, amp, tc, kmin):
     """All-at-once solve = time-marched solution of the same system (<= 1e-8),
     iterations within +-1 of the oracle's FGMRES."""
-    H, S = _pair(stmg, ctx, nx, r, k, N, nh, amp, rtol=1e-10)
+    H, S = _pair(stmg, ctx, nx, r, k, N, nh, amp, tc, kmin, rtol=1e-10)
     f = H.level[-1]
     b = o3.make_consistent3(np.random.default_rng(9).uniform(-1, 1, N * f.size), f, N)
     X = torch.zeros(N * f.size, dtype=torch.float64, device="cuda")

@@ -1,0 +1,170 @@
+#!/usr/bin/env python
+"""3D workloads of BASELINE.json on one B200 (configs[2] "C3", configs[4] "C5").
+
+  C3: 3D Stokes, Q2/P1disc (r=1), DG(1), 32^3 Cartesian cells, 64 intervals,
+      ~1.2e8 space-time dofs. vmult, cell-Vanka smoother step and the full
+      all-at-once FGMRES + hp-STMG solve (p: k 1 -> 0, then h in space AND time
+      down to 4^3 x 8, exact coarse forward substitution on the GPU).
+  C5: 3D Stokes, Q3/P2disc (r=2), DG(2), 32^3 cells with interior vertices
+      perturbed by <= 0.1 h (seeded), 128 intervals, ~1.2e9 dofs: vmult.
+
+Prints one JSON object. Inputs are seeded uniform[-1,1] on the device;
+timings are CUDA events on the library's stream after warm-up.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def seeded(torch, n, seed):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    return torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+
+
+def consistent(torch, lvl, F, n):
+    """Constrained velocity rows zero, per-slot pressure component along the
+    constant mode removed."""
+    gx, gy, gz = lvl.gx, lvl.gy, lvl.gz
+    bnd = torch.zeros((gz, gy, gx), dtype=torch.bool, device="cuda")
+    bnd[0] = bnd[-1] = True
+    bnd[:, 0] = bnd[:, -1] = True
+    bnd[:, :, 0] = bnd[:, :, -1] = True
+    bnd = bnd.reshape(-1)
+    V = F.view(n, lvl.size)
+    for a in range(lvl.n_slots):
+        for c in range(3):
+            base = a * lvl.n_velocity + c * lvl.n_scalar
+            V[:, base:base + lvl.n_scalar][:, bnd] = 0.0
+        p0 = lvl.n_slots * lvl.n_velocity + a * lvl.n_pressure
+        P = V[:, p0:p0 + lvl.n_pressure].view(n, -1, lvl.n_p)
+        P[:, :, 0] -= P[:, :, 0].mean(dim=1, keepdim=True)
+    return F
+
+
+def timed(torch, fn, reps, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def run_c3(torch, stmg, args):
+    ctx = stmg.Context(0)
+    n, N = args.c3_cells, args.c3_intervals
+    out = {"config": f"C3: {n}^3 Q2/P1disc, DG(1), {N} intervals, nu=1, gamma=1, V(2,2) cell Vanka"}
+    t0 = time.perf_counter()
+    spec = args.c3_variant == "spec"
+    # "spec": BASELINE's hierarchy (k 1 -> 0, then h in space and time);
+    # "robust": k kept at 1, h in space only, exact coarse forward
+    # substitution over all intervals (time coarsening with the
+    # time-block-diagonal Vanka is not h-robust)
+    sol = stmg.Solver3(ctx, n, n, n, 1, 1, 1.0 / N, 1.0, 1.0, n_hcoarse=args.c3_hcoarse if spec else args.c3_hcoarse + 1,
+                       time_coarsen=spec, k_min=0 if spec else 1, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
+    out["variant"] = args.c3_variant
+    torch.cuda.synchronize()
+    out["setup_s"] = time.perf_counter() - t0
+    out["levels"] = sol.level_info
+    f = sol.finest
+    dofs = N * f.size
+    out["dofs"] = dofs
+    x = seeded(torch, dofs, 1)
+    y = torch.empty_like(x)
+    b = seeded(torch, dofs, 2)
+    halo = seeded(torch, f.n_velocity, 3)
+    ms = timed(torch, lambda: f.vmult(x, y, N, halo), args.reps)
+    out["vmult_ms"] = ms
+    out["vmult_dofs_per_s"] = dofs / (ms * 1e-3)
+    ms = timed(torch, lambda: f.residual(b, x, y, N, halo), args.reps)
+    out["residual_ms"] = ms
+    fl = sol.levels[-1]
+    # smoother step on the finest level of the hierarchy (has cell Vanka only
+    # below the finest? the finest carries the smoother too)
+    u = x.clone()
+    work = torch.empty_like(x)
+    ms = timed(torch, lambda: fl.smooth_step(b, u, 0.8, N, halo, coupled=True, work=work), args.reps)
+    out["smooth_step_ms"] = ms
+    out["smooth_step_dofs_per_s"] = dofs / (ms * 1e-3)
+    out["max_patch"] = fl.max_patch
+    out["vanka_flops"] = 2.0 * fl.total_matrix_elements * N
+    out["vanka_update_TFLOPs"] = out["vanka_flops"] / ((ms - out["residual_ms"]) * 1e-3) / 1e12
+    del u, work
+    if not args.no_solve:
+        F = consistent(torch, f, seeded(torch, dofs, 4), N)
+        X = torch.zeros_like(F)
+        sol.solve_all_at_once(F, X, N)  # warm (workspaces)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        it, hist = sol.solve_all_at_once(F, X, N)
+        e1.record()
+        torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) * 1e-3
+        out["solve"] = {"seconds": s, "fgmres_iterations": it, "dofs_per_s": dofs / s,
+                        "relative_residual": hist[-1] / hist[0]}
+    return out
+
+
+def run_c5(torch, stmg, args):
+    import numpy as np
+
+    ctx = stmg.Context(0)
+    n, N = args.c5_cells, args.c5_intervals
+    rng = np.random.default_rng(2025)
+    z, yy, xx = np.meshgrid(np.arange(n + 1) / n, np.arange(n + 1) / n, np.arange(n + 1) / n, indexing="ij")
+    v = np.stack([xx, yy, z], axis=-1)
+    inner = np.zeros(v.shape[:3], dtype=bool)
+    inner[1:-1, 1:-1, 1:-1] = True
+    v[inner] += rng.uniform(-1, 1, v.shape)[inner] * 0.1 / n
+    verts = np.ascontiguousarray(v.reshape(-1))
+    lvl = stmg.Level3(ctx, n, n, n, 2, 2, 1.0 / N, 1.0, 1.0, stmg.SMOOTHER_NONE, vertices=verts)
+    dofs = N * lvl.size
+    out = {"config": f"C5: {n}^3 deformed (<= 0.1 h), Q3/P2disc, DG(2), {N} intervals", "dofs": dofs}
+    x = seeded(torch, dofs, 1)
+    y = torch.empty_like(x)
+    halo = seeded(torch, lvl.n_velocity, 3)
+    ms = timed(torch, lambda: lvl.vmult(x, y, N, halo), args.reps)
+    out["vmult_ms"] = ms
+    out["vmult_dofs_per_s"] = dofs / (ms * 1e-3)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="C3,C5")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--c3-cells", type=int, default=32)
+    ap.add_argument("--c3-intervals", type=int, default=64)
+    ap.add_argument("--c3-hcoarse", type=int, default=3)
+    ap.add_argument("--c5-cells", type=int, default=32)
+    ap.add_argument("--c5-intervals", type=int, default=128)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--c3-variant", default="robust", choices=["robust", "spec"])
+    ap.add_argument("--maxit", type=int, default=200)
+    args = ap.parse_args()
+    import torch
+    import paper_2502_09159_b200 as stmg
+
+    res = {}
+    if "C3" in args.case:
+        res["C3"] = run_c3(torch, stmg, args)
+    if "C5" in args.case:
+        res["C5"] = run_c5(torch, stmg, args)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
