@@ -26,6 +26,9 @@ Extra fields of the JSON line (not the headline; skipped with --no-solve):
                        partitioned over all ranks (NCCL time slabs)
   solve.C4_full        (1 GPU) the whole 64-interval C4 system as 8 macro steps
   C4_step              C4 vmult + vertex-star smoother step over 8 intervals
+  3D.C3                (1 GPU) C3: 32^3 Q2/P1disc, DG(1), 64 intervals: vmult,
+                       cell-Vanka step, full all-at-once solve (tools/bench3d.py)
+  3D.C5                (1 GPU) C5: 32^3 deformed Q3/P2disc, DG(2), 128 intervals: vmult
 """
 from __future__ import annotations
 
@@ -269,6 +272,22 @@ def c4_step_leg(stmg, ctx, torch, n_int=8, reps=5):
            "vmult_dofs_per_s": n / (vm * 1e-3), "smoother_step_dofs_per_s": n / ((rs + vk) * 1e-3),
            "vanka_TFLOP/s": flops_vk / vk / 1e9, "smoother": "vertex_star (n_T = 124)"}
     del lvl, x, b, u, y, res
+    return out
+
+
+def three_d_leg(torch, stmg):
+    """BASELINE configs[2] (C3: 32^3 Q2/P1disc, DG(1), 64 intervals: vmult,
+    cell-Vanka step, full all-at-once FGMRES + hp-STMG solve) and configs[4]
+    (C5: 32^3 deformed Q3/P2disc, DG(2), 128 intervals: vmult) on this GPU."""
+    sys.path.insert(0, str(ROOT / "tools"))
+    import bench3d
+
+    a = argparse.Namespace(reps=5, c3_cells=32, c3_intervals=64, c3_hcoarse=3, c3_variant="robust", maxit=200,
+                           no_solve=False, c5_cells=32, c5_intervals=128)
+    out = {"C3": bench3d.run_c3(torch, stmg, a)}
+    torch.cuda.empty_cache()
+    out["C5"] = bench3d.run_c5(torch, stmg, a)
+    torch.cuda.empty_cache()
     return out
 
 
@@ -562,6 +581,7 @@ def main():
         line["C4_step"] = side(lambda: c4_step_leg(stmg, ctx, torch))
         if world == 1:
             line["solve"]["C4_full"] = side(lambda: c4_full_leg(stmg, ctx, torch))
+            line["3D"] = side(lambda: three_d_leg(torch, stmg))
     if not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_quick()

@@ -37,6 +37,414 @@ struct V3
 {
   static constexpr int N = R + 2, NN = N * N, NNN = N * N * N, p = R + 1;
   static constexpr int NP = (R + 1) * (R + 2) * (R + 3) / 6;
+  // lane = cell: a warp works one line of CW cells (r = 1: 32 cells, one
+  // line per warp; r = 2: 16 cells, two lines per warp), so a warp's shared
+  // accesses hit CW different cells at the same offset (odd cell stride:
+  // conflict-free) and its global gathers walk consecutive cells along x.
+  static constexpr int CW = 16;
+  static constexpr int LPW = 32 / CW;
+  static constexpr int NWARP = (NN + LPW - 1) / LPW;
+  static constexpr int THREADS = 32 * NWARP;
+  static constexpr int NF = 13; // in-place fields per cell
+  static constexpr int CELL = NF * NNN + NP + 24 + 1; // doubles per cell, odd
+  static constexpr size_t smem() { return sizeof(double) * (CW * CELL + NP * NNN + 2 * N); }
+};
+
+// Forward 1D contraction of a line: o[q] = sum_m M(q, m) in[m] (M = phi /
+// dphi, constant bank, compile-time indices).
+#define V3_FWD(M, in, o)                                                                                             \
+  _Pragma("unroll") for (int q_ = 0; q_ < N; ++q_)                                                                   \
+  {                                                                                                                  \
+    double s_ = 0.0;                                                                                                 \
+    _Pragma("unroll") for (int m_ = 0; m_ < N; ++m_) s_ = fma(P.M[q_ * N + m_], in[m_], s_);                         \
+    o[q_] = s_;                                                                                                      \
+  }
+
+template <int R, int S, int MODE>
+__global__ void __launch_bounds__(V3<R>::THREADS, 1)
+vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
+              double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
+{
+  using C = V3<R>;
+  constexpr int N = C::N, NN = C::NN, NNN = C::NNN, p = C::p, NP = C::NP, CW = C::CW;
+  extern __shared__ __align__(16) double sm3[];
+  double *const psi = sm3 + CW * C::CELL; // psi[m * NNN + q]: P_r^disc mode m at Gauss point q
+  double *const tw = psi + NP * NNN;      // Gauss weights, points
+  double *const txq = tw + N;
+  for (int e = threadIdx.x; e < NP * NNN; e += C::THREADS)
+    {
+      const int m = e / NNN, q = e - m * NNN;
+      const int qx = q % N, qy = (q / N) % N, qz = q / NN;
+      double v = 1.0;
+#pragma unroll
+      for (int mm = 0; mm < NP; ++mm)
+        if (mm == m)
+          v = P.leg[P.ex[mm][0] * N + qx] * P.leg[P.ex[mm][1] * N + qy] * P.leg[P.ex[mm][2] * N + qz];
+      psi[e] = v;
+    }
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+    if (threadIdx.x == q)
+      {
+        tw[q] = P.w[q];
+        txq[q] = P.xq[q];
+      }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cl = lane % CW;
+  const int t = warp * C::LPW + lane / CW; // line index
+  const long long gc = static_cast<long long>(blockIdx.x) * CW + cl;
+  const bool active = gc < n_cells_total && t < NN;
+  const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
+  const int n = gc < n_cells_total ? static_cast<int>(gc / ncells) : 0;
+  const long long cell = gc < n_cells_total ? gc - n * ncells : 0;
+  const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
+            cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
+  double *const F = sm3 + cl * C::CELL;
+  double *const PM = F + C::NF * NNN;
+  double *const X8 = PM + NP;
+  const int tA = t % N, tB = t / N; // line coordinates
+  const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
+  const int gx = P.gx, gy = P.gy, gz = P.gz;
+  const bool deformed = P.verts != nullptr;
+  const double *__restrict__ xn = x + n * isz;
+  const double *__restrict__ vprev = nullptr;
+  if (coupled)
+    vprev = n > 0 ? x + (n - 1) * isz + (S - 1) * mv : xprev0;
+  if (active && deformed)
+    for (int q = t; q < 24; q += NN)
+      {
+        const int c = q / 3, d = q % 3;
+        const int vx = cx + (c & 1), vy = cy + ((c >> 1) & 1), vz = cz + (c >> 2);
+        X8[q] = __ldg(P.verts + ((static_cast<long long>(vz) * (P.ny + 1) + vy) * (P.nx + 1) + vx) * 3 + d);
+      }
+  // fields (in place): F[c] VK_c, F[3+c] Ax/AA/T0/Yb, F[6+c] Dx/DA/T1, F[9+c] AD, F[12] QP
+  auto fld = [&](int f) { return F + f * NNN; };
+  // line bases: x-line (j = tA, k = tB), y-line (i = tA, k = tB), z-line (i = tA, j = tB)
+  const int bx = (tB * N + tA) * N, by = tB * NN + tA, bz = tB * N + tA;
+  __syncthreads(); // tables
+
+  for (int a = 0; a < S; ++a)
+    {
+      double kt[S], mt[S], lva = 0.0;
+#pragma unroll
+      for (int aa = 0; aa < S; ++aa)
+        if (a == aa)
+          {
+#pragma unroll
+            for (int bs = 0; bs < S; ++bs)
+              {
+                kt[bs] = P.Kt[aa * S + bs];
+                mt[bs] = P.Mt[aa * S + bs];
+              }
+            lva = P.lv[aa];
+          }
+      // ---- phase 1 (x-lines): gather, temporal combination, x-contraction
+      if (active)
+        {
+          const int Y = cy * p + tA, Z = cz * p + tB;
+          const bool yzb = MODE != 2 && (Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1);
+          const long long row = (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double uk[N], um[N], o[N];
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  const int X = cx * p + i;
+                  const bool bnd = yzb || (MODE != 2 && (X == 0 || X == gx - 1));
+                  double k_ = 0.0, m_ = 0.0;
+                  if (!bnd)
+#pragma unroll
+                    for (int bs = 0; bs < S; ++bs)
+                      {
+                        const double v = __ldg(xn + bs * mv + c * nsc + row + i);
+                        k_ = fma(kt[bs], v, k_);
+                        m_ = fma(mt[bs], v, m_);
+                      }
+                  if (vprev != nullptr)
+                    k_ = fma(-lva, __ldg(vprev + c * nsc + row + i), k_);
+                  uk[i] = k_;
+                  um[i] = m_;
+                }
+              V3_FWD(phi, uk, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(c)[bx + q] = o[q];
+              V3_FWD(phi, um, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(3 + c)[bx + q] = o[q];
+              V3_FWD(dphi, um, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(6 + c)[bx + q] = o[q];
+            }
+          if (t < NP)
+            {
+              double s = 0.0;
+#pragma unroll
+              for (int bs = 0; bs < S; ++bs)
+                s = fma(mt[bs], __ldg(xn + S * mv + bs * mp + cell * NP + t), s);
+              PM[t] = s;
+            }
+        }
+      __syncthreads();
+      // ---- phase 2 (y-lines, in place): VK; Ax -> AA (phi_y), AD (dphi_y, F[9+c]); Dx -> DA
+      if (active)
+        {
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], o[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(c)[by + m * N];
+              V3_FWD(phi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(c)[by + q * N] = o[q];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(3 + c)[by + m * N];
+              V3_FWD(phi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(3 + c)[by + q * N] = o[q];
+              V3_FWD(dphi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(9 + c)[by + q * N] = o[q];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(6 + c)[by + m * N];
+              V3_FWD(phi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(6 + c)[by + q * N] = o[q];
+            }
+        }
+      __syncthreads();
+      // ---- phase 3 (z-lines, in place): z-contraction, fluxes at the Gauss
+      // points, transposed z-contraction, all in registers:
+      // Sv_c = phi_z^T Fval_c + dphi_z^T Fref_c2 (F[c]), T0_c = phi_z^T Fref_c0
+      // (F[3+c]), T1_c = phi_z^T Fref_c1 (F[6+c]); QP = w det div (F[12])
+      if (active)
+        {
+          double vk[3][N], g[3][3][N];
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(c)[bz + m * NN];
+              V3_FWD(phi, in, vk[c])
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(6 + c)[bz + m * NN];
+              V3_FWD(phi, in, g[c][0])
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(9 + c)[bz + m * NN];
+              V3_FWD(phi, in, g[c][1])
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(3 + c)[bz + m * NN];
+              V3_FWD(dphi, in, g[c][2])
+            }
+          double sv[3][N], t0[3][N], t1[3][N];
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+              sv[c][i] = t0[c][i] = t1[c][i] = 0.0;
+          const double wxy = tw[tA] * tw[tB];
+#pragma unroll
+          for (int qz = 0; qz < N; ++qz)
+            {
+              double Ji[3][3], det;
+              if (!deformed)
+                {
+                  Ji[0][0] = 2.0 / P.hx;
+                  Ji[1][1] = 2.0 / P.hy;
+                  Ji[2][2] = 2.0 / P.hz;
+                  Ji[0][1] = Ji[0][2] = Ji[1][0] = Ji[1][2] = Ji[2][0] = Ji[2][1] = 0.0;
+                  det = 0.125 * P.hx * P.hy * P.hz;
+                }
+              else
+                {
+                  const double xi[3] = {txq[tA], txq[tB], P.xq[qz]};
+                  double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+                  for (int v = 0; v < 8; ++v)
+                    {
+                      const double n0 = (v & 1) ? 0.5 * (1 + xi[0]) : 0.5 * (1 - xi[0]);
+                      const double n1 = ((v >> 1) & 1) ? 0.5 * (1 + xi[1]) : 0.5 * (1 - xi[1]);
+                      const double n2 = (v >> 2) ? 0.5 * (1 + xi[2]) : 0.5 * (1 - xi[2]);
+                      const double d0 = (v & 1) ? 0.5 : -0.5, d1 = ((v >> 1) & 1) ? 0.5 : -0.5,
+                                   d2 = (v >> 2) ? 0.5 : -0.5;
+                      const double dN[3] = {d0 * n1 * n2, n0 * d1 * n2, n0 * n1 * d2};
+#pragma unroll
+                      for (int d = 0; d < 3; ++d)
+#pragma unroll
+                        for (int e = 0; e < 3; ++e)
+                          J[d][e] = fma(X8[3 * v + d], dN[e], J[d][e]);
+                    }
+                  det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                        J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                        J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+                  const double id = 1.0 / det;
+                  Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
+                  Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+                  Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+                  Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
+                  Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+                  Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+                  Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
+                  Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+                  Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+                }
+              const double wd = P.w[qz] * wxy * det;
+              double G[3][3];
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                  G[c][d] = g[c][0][qz] * Ji[0][d] + g[c][1][qz] * Ji[1][d] + g[c][2][qz] * Ji[2][d];
+              const double div = G[0][0] + G[1][1] + G[2][2];
+              const int q = qz * NN + bz;
+              double pq = 0.0;
+#pragma unroll
+              for (int m = 0; m < NP; ++m)
+                pq = fma(psi[m * NNN + q], PM[m], pq);
+              const double diag = P.gamma * div - pq;
+              fld(12)[q] = wd * div;
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                {
+                  double Fp[3];
+#pragma unroll
+                  for (int d = 0; d < 3; ++d)
+                    Fp[d] = wd * (P.nu * G[c][d] + (c == d ? diag : 0.0));
+                  double Fr[3];
+#pragma unroll
+                  for (int e = 0; e < 3; ++e)
+                    Fr[e] = Fp[0] * Ji[e][0] + Fp[1] * Ji[e][1] + Fp[2] * Ji[e][2];
+                  const double fv = wd * vk[c][qz];
+#pragma unroll
+                  for (int i = 0; i < N; ++i)
+                    {
+                      sv[c][i] = fma(P.phi[qz * N + i], fv, sv[c][i]);
+                      sv[c][i] = fma(P.dphi[qz * N + i], Fr[2], sv[c][i]);
+                      t0[c][i] = fma(P.phi[qz * N + i], Fr[0], t0[c][i]);
+                      t1[c][i] = fma(P.phi[qz * N + i], Fr[1], t1[c][i]);
+                    }
+                }
+            }
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+              {
+                fld(c)[bz + i * NN] = sv[c][i];
+                fld(3 + c)[bz + i * NN] = t0[c][i];
+                fld(6 + c)[bz + i * NN] = t1[c][i];
+              }
+        }
+      __syncthreads();
+      // ---- phase 4 (y-lines, in place): Ya_c = phi_y^T Sv_c + dphi_y^T T1_c (F[c]),
+      // Yb_c = phi_y^T T0_c (F[3+c]); pressure rows from QP
+      if (active)
+        {
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], in2[N], in3[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  in[m] = fld(c)[by + m * N];
+                  in2[m] = fld(6 + c)[by + m * N];
+                  in3[m] = fld(3 + c)[by + m * N];
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s1 = fma(P.phi[q * N + i], in[q], s1);
+                      s1 = fma(P.dphi[q * N + i], in2[q], s1);
+                      s2 = fma(P.phi[q * N + i], in3[q], s2);
+                    }
+                  fld(c)[by + i * N] = s1;
+                  fld(3 + c)[by + i * N] = s2;
+                }
+            }
+          if (t < NP)
+            {
+              const double *qp = fld(12);
+              const double *ps = psi + t * NNN;
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q < NNN; ++q)
+                s = fma(ps[q], qp[q], s);
+              const long long o = n * isz + S * mv + a * mp + cell * NP + t;
+              y[o] = MODE == 1 ? __ldg(b + o) - s : s;
+            }
+        }
+      __syncthreads();
+      // ---- phase 5 (x-lines): y = phi_x^T Ya + dphi_x^T Yb, scattered from registers
+      if (active)
+        {
+          const int Y = cy * p + tA, Z = cz * p + tB;
+          const bool yzb = Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], in2[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  in[m] = fld(c)[bx + m];
+                  in2[m] = fld(3 + c)[bx + m];
+                }
+              double *yv = y + n * isz + a * mv + c * nsc + (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s = fma(P.phi[q * N + i], in[q], s);
+                      s = fma(P.dphi[q * N + i], in2[q], s);
+                    }
+                  const int X = cx * p + i;
+                  const bool bnd = MODE != 2 && (yzb || X == 0 || X == gx - 1);
+                  if (!bnd)
+                    atomicAdd(yv + i, MODE == 1 ? -s : s);
+                }
+            }
+        }
+      // the next slot's phase 1 rewrites this thread's own x-line (fields
+      // 0..8) and nothing another thread still reads: no barrier here
+    }
+}
+#undef V3_FWD
+
+// ---------------------------------------------------------------------------
+// Line-per-thread variant (r = 1): N*N threads per cell, 16 cells per block,
+// 13 in-place fields; every pass reads / writes shared memory. At r = 1 it
+// keeps more warps resident than the lane-per-cell kernel below
+// (C3 vmult 8.9 ms vs 11.3 ms measured on the B200).
+template <int R>
+struct V3L
+{
+  static constexpr int N = R + 2, NN = N * N, NNN = N * N * N, p = R + 1;
+  static constexpr int NP = (R + 1) * (R + 2) * (R + 3) / 6;
   static constexpr int CB = R == 1 ? 16 : (R == 2 ? 8 : 4); // cells per block
   static constexpr int NF = 13;                             // fields per cell
   static constexpr int CELL = NF * NNN + NP + 24;           // doubles per cell
@@ -45,21 +453,13 @@ struct V3
   static constexpr size_t smem() { return sizeof(double) * (CB * CELL + TAB) + sizeof(int) * 3 * NP; }
 };
 
-// 1D pass over one line: out[o] = sum_m M(o, m) in[m] (forward, M = phi /
-// dphi indexed [q * N + i]) or out[i] = sum_q M(q, i) in[q] (transpose).
-template <int N, bool T>
-__device__ __forceinline__ double
-mat(const double *M, int o, int m)
-{
-  return T ? M[m * N + o] : M[o * N + m];
-}
 
 template <int R, int S, int MODE>
-__global__ void __launch_bounds__(V3<R>::NN *V3<R>::CB)
-vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
+__global__ void __launch_bounds__(V3L<R>::NN *V3L<R>::CB)
+vmult3l_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
               double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
-  using C = V3<R>;
+  using C = V3L<R>;
   constexpr int N = C::N, NN = C::NN, NNN = C::NNN, p = C::p, NP = C::NP;
   extern __shared__ __align__(16) double sm3[];
   double *const tw = sm3 + C::CB * C::CELL; // w[N], xq[N], leg[(R+1) * N]
@@ -591,7 +991,6 @@ cudaError_t
 launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, int nI, const double *xprev0,
            int coupled, int mode, cudaStream_t st)
 {
-  using C = V3<R>;
   DevGeom3 G{};
   G.nx = P.nx;
   G.ny = P.ny;
@@ -608,18 +1007,34 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
   const long long total_v = static_cast<long long>(nI) * S * P.mv;
   const int ib = static_cast<int>(std::min<long long>((total_v + 255) / 256, 148 * 16));
   const long long cells = static_cast<long long>(nI) * P.nx * P.ny * P.nz;
-  dim3 block(C::NN, C::CB);
-  const unsigned grid = static_cast<unsigned>((cells + C::CB - 1) / C::CB);
-  auto go = [&](auto init, auto kern) {
+  auto go = [&](auto init, auto kern, dim3 block, unsigned grid, size_t smem) {
     init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::smem()));
-    kern<<<grid, block, C::smem(), st>>>(P, x, b, y, xprev0, coupled, cells);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, block, smem, st>>>(P, x, b, y, xprev0, coupled, cells);
   };
-  switch (mode)
+  if constexpr (R == 1)
     {
-      case 0: go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0>); break;
-      case 1: go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1>); break;
-      default: go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2>); break;
+      using C = V3L<R>;
+      const dim3 block(C::NN, C::CB);
+      const unsigned grid = static_cast<unsigned>((cells + C::CB - 1) / C::CB);
+      switch (mode)
+        {
+          case 0: go(vmult3_init_kernel<0>, vmult3l_kernel<R, S, 0>, block, grid, C::smem()); break;
+          case 1: go(vmult3_init_kernel<1>, vmult3l_kernel<R, S, 1>, block, grid, C::smem()); break;
+          default: go(vmult3_init_kernel<2>, vmult3l_kernel<R, S, 2>, block, grid, C::smem()); break;
+        }
+    }
+  else
+    {
+      using C = V3<R>;
+      const dim3 block(C::THREADS);
+      const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
+      switch (mode)
+        {
+          case 0: go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0>, block, grid, C::smem()); break;
+          case 1: go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1>, block, grid, C::smem()); break;
+          default: go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2>, block, grid, C::smem()); break;
+        }
     }
   return cudaGetLastError();
 }

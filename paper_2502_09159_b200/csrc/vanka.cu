@@ -141,13 +141,16 @@ dmma_8x8x4(double (&d)[2], double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int KS>
-__global__ void __launch_bounds__(kDThreads, 1)
+template <int KS, int ROWS = kDRows, int TPW = 1>
+__global__ void __launch_bounds__(ROWS * 4 / TPW, 1)
 vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ items,
                   const int *__restrict__ item_ptr, const long long *__restrict__ vel_anchor,
                   const long long *__restrict__ pre_anchor, const double *__restrict__ r, double *__restrict__ u,
                   long long isz, int n_intervals, double omega)
 {
+  // ROWS rows of the patch matrix; warp w owns the TPW 8-row tiles w + j * NW
+  constexpr int kDRows = ROWS, kDThreads = ROWS * 4 / TPW, kDPer = kDRows * kDCols / kDThreads;
+  constexpr int NW = kDThreads / 32;
   extern __shared__ __align__(16) double dsm[];
   double *Rs = dsm;                                                 // kDRows x kDRLd
   double *Zs = Rs + kDRows * kDRLd;                                 // kDRows x kDZLd
@@ -163,7 +166,7 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
   const int it1 = item_ptr ? item_ptr[blockIdx.x + 1] : blockIdx.x + 1;
 
   int loaded = -1, nt = 0, nvel = 0;
-  double afr[KS];
+  double afr[TPW][KS];
   long long relq[kDPer];
   bool velq[kDPer], validq[kDPer];
 
@@ -180,12 +183,16 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           nvel = pc.n_vel;
           for (int i = tid; i < kDRows; i += kDThreads)
             w_s[i] = i < nt ? omega * pc.weight[i] : 0.0;
-          const int arow = 8 * warp + (lane >> 2);
 #pragma unroll
-          for (int kk = 0; kk < KS; ++kk)
+          for (int tw = 0; tw < TPW; ++tw)
             {
-              const int col = 4 * kk + (lane & 3);
-              afr[kk] = (arow < nt && col < nt) ? __ldg(pc.inverse + arow * nt + col) : 0.0;
+              const int arow = 8 * (warp + tw * NW) + (lane >> 2);
+#pragma unroll
+              for (int kk = 0; kk < KS; ++kk)
+                {
+                  const int col = 4 * kk + (lane & 3);
+                  afr[tw][kk] = (arow < nt && col < nt) ? __ldg(pc.inverse + arow * nt + col) : 0.0;
+                }
             }
 #pragma unroll
           for (int q = 0; q < kDPer; ++q)
@@ -259,31 +266,33 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
                 }
             }
           // Z = A^{-1} R on the FP64 tensor path
-          if (8 * warp < nt)
-            {
-              double acc[kDCols / 8][2];
 #pragma unroll
-              for (int ct = 0; ct < kDCols / 8; ++ct)
-                acc[ct][0] = acc[ct][1] = 0.0;
-              const double *bbase = Rs + (lane & 3) * kDRLd + (lane >> 2);
+          for (int tw = 0; tw < TPW; ++tw)
+            if (8 * (warp + tw * NW) < nt)
+              {
+                double acc[kDCols / 8][2];
 #pragma unroll
-              for (int kk = 0; kk < KS; ++kk)
-                {
-                  const double *brow = bbase + 4 * kk * kDRLd;
+                for (int ct = 0; ct < kDCols / 8; ++ct)
+                  acc[ct][0] = acc[ct][1] = 0.0;
+                const double *bbase = Rs + (lane & 3) * kDRLd + (lane >> 2);
 #pragma unroll
-                  for (int ct = 0; ct < kDCols / 8; ++ct)
-                    dmma_8x8x4(acc[ct], afr[kk], brow[8 * ct]);
-                }
-              const int row = 8 * warp + (lane >> 2);
-              const double wr = w_s[row];
+                for (int kk = 0; kk < KS; ++kk)
+                  {
+                    const double *brow = bbase + 4 * kk * kDRLd;
 #pragma unroll
-              for (int ct = 0; ct < kDCols / 8; ++ct)
-                {
-                  const int col = 8 * ct + 2 * (lane & 3);
-                  Zs[row * kDZLd + col] = acc[ct][0] * wr;
-                  Zs[row * kDZLd + col + 1] = acc[ct][1] * wr;
-                }
-            }
+                    for (int ct = 0; ct < kDCols / 8; ++ct)
+                      dmma_8x8x4(acc[ct], afr[tw][kk], brow[8 * ct]);
+                  }
+                const int row = 8 * (warp + tw * NW) + (lane >> 2);
+                const double wr = w_s[row];
+#pragma unroll
+                for (int ct = 0; ct < kDCols / 8; ++ct)
+                  {
+                    const int col = 8 * ct + 2 * (lane & 3);
+                    Zs[row * kDZLd + col] = acc[ct][0] * wr;
+                    Zs[row * kDZLd + col + 1] = acc[ct][1] * wr;
+                  }
+              }
           column_bases(t + 2);
           __syncthreads();
 #pragma unroll
@@ -311,19 +320,21 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
 {
   if (n_batches == 0 || n_intervals == 0)
     return cudaSuccess;
-  if (max_nt <= kDRows)
+  if (max_nt <= 176)
     {
-      const size_t dsmem = sizeof(double) * (kDRows * kDRLd + kDRows * kDZLd + kDRows) + sizeof(long long) * 6 * kDCols;
+      // 128 rows (16 warps) for 2D patches; 176 rows (22 warps) for 3D Q2 cells (n_T = 170)
+      const int rows = max_nt <= kDRows ? kDRows : 176;
+      const size_t dsmem = sizeof(double) * (rows * kDRLd + rows * kDZLd + rows) + sizeof(long long) * 6 * kDCols;
       dim3 grid(n_batches, (n_intervals + kDGroup - 1) / kDGroup);
       const int ks = (max_nt + 3) / 4;
       auto go = [&](auto kern) {
-        static bool set = false;
-        (void)set;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
-        kern<<<grid, kDThreads, dsmem, stream>>>(classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz,
-                                                 n_intervals, omega);
+        kern<<<grid, rows == 176 ? 352 : rows * 4, dsmem, stream>>>(classes, batches, item_ptr, vel_anchor,
+                                                                    pre_anchor, r, u, isz, n_intervals, omega);
       };
-      if (ks <= 8)
+      if (rows == 176)
+        go(vanka_dmma_kernel<44, 176, 2>);
+      else if (ks <= 8)
         go(vanka_dmma_kernel<8>);
       else if (ks <= 12)
         go(vanka_dmma_kernel<12>);
