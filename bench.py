@@ -25,6 +25,8 @@ Extra fields of the JSON line (not the headline; skipped with --no-solve):
   solve.C4_all_at_once all-at-once slab solve of C4, 8 intervals per rank,
                        partitioned over all ranks (NCCL time slabs)
   solve.C4_full        (1 GPU) the whole 64-interval C4 system as 8 macro steps
+  solve.C3_all_at_once the 64-interval C3 system (32^3, Q2/P1disc, DG(1))
+                       split into time slabs over all ranks (NCCL)
   C4_step              C4 vmult + vertex-star smoother step over 8 intervals
   3D.C3                (1 GPU) C3: 32^3 Q2/P1disc, DG(1), 64 intervals: vmult,
                        cell-Vanka step, full all-at-once solve (tools/bench3d.py)
@@ -291,6 +293,49 @@ def three_d_leg(torch, stmg):
     return out
 
 
+def c3_slab_leg(stmg, torch, dist, world, rank, n_total=64):
+    """BASELINE configs[2] (C3) partitioned by time slabs: the 64-interval
+    32^3 Q2/P1disc DG(1) all-at-once system split over the ranks (strong
+    scaling), FGMRES + hp-STMG V(2,2) (k kept at 1, h in space down to 2^3,
+    exact coarse forward substitution in time over all intervals), halo /
+    Krylov dots / coarse right-hand sides over NCCL. Time = max over ranks."""
+    from paper_2502_09159_b200 import timeslab
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    import bench3d
+
+    n_local = n_total // world
+    ctx = stmg.Context(torch.cuda.current_device())
+    sol = stmg.Solver3(ctx, 32, 32, 32, 1, 1, 1.0 / n_total, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=1,
+                       nu1=2, nu2=2, rtol=1e-8)
+    if world > 1:
+        sol.set_comm(timeslab.TorchComm(device=f"cuda:{torch.cuda.current_device()}"))
+    f = sol.finest
+    F = bench3d.consistent(torch, f, bench3d.seeded(torch, n_local * f.size, 301 + rank), n_local)
+    X = torch.zeros_like(F)
+    sol.solve_all_at_once(F, X, n_local)  # warm-up: Krylov workspace
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    it, hist = sol.solve_all_at_once(F, X, n_local)
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) / 1e3
+    if world > 1:
+        t = torch.tensor([sec], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    total = world * F.numel()
+    out = {"dofs": total, "intervals": n_total, "seconds": sec, "dofs_per_s": total / sec, "fgmres_iterations": it,
+           "relative_residual": hist[-1] / hist[0], "levels": sol.n_levels, "smoother": "cell (n_T = 170)",
+           "partition": f"{world} time slabs x {n_local} intervals (strong scaling)"}
+    del sol, F, X
+    torch.cuda.empty_cache()
+    return out
+
+
 def slab_solve_leg(stmg, ctx, torch, dist, world, rank, n_local=8):
     """All-at-once FGMRES + hp-STMG V(2,2) solve of the C4 discretisation
     (1024^2, Q2/P1, DG(1), tau = 1/64, vertex-star Vanka) partitioned by time
@@ -506,12 +551,16 @@ def main():
         e2e = {"value": world * dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * (3 * dofs + 2 * mv),
                "d2h_bytes_per_step": 8 * 2 * dofs}
 
-    slab = None
+    slab = c3slab = None
     if not args.no_solve:
         try:  # a side leg: a failure is reported in the line, never fatal for the headline
             slab = slab_solve_leg(stmg, ctx, torch, dist, world, rank)
         except Exception as exc:
             slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        try:
+            c3slab = c3_slab_leg(stmg, torch, dist, world, rank)
+        except Exception as exc:
+            c3slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank != 0:
         if world > 1:
@@ -578,6 +627,7 @@ def main():
                 return {"error": f"{type(exc).__name__}: {exc}"[:300]}
         line["solve"] = side(lambda: solve_legs(stmg, ctx, torch))
         line["solve"]["C4_all_at_once"] = slab
+        line["solve"]["C3_all_at_once"] = c3slab
         line["C4_step"] = side(lambda: c4_step_leg(stmg, ctx, torch))
         if world == 1:
             line["solve"]["C4_full"] = side(lambda: c4_full_leg(stmg, ctx, torch))
