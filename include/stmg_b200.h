@@ -296,9 +296,13 @@ int stmg3_project_mean_zero(stmg3_level *level, double *x, int n_intervals);
  * r -> r/2 -> ... -> 1 (hierarchy.cpp:9-97 extended to k = 0), then n_hcoarse
  * h-steps in space, each also halving the time grid when time_coarsen != 0
  * (PAPER.md Eq. DeftPrRe). The coarsest level is solved exactly by forward
- * substitution in time on the GPU. tau = finest interval length. */
+ * substitution in time on the GPU. tau = finest interval length. affine_patches != 0
+ * (deformed meshes only): the Vanka patch inverses of the undeformed mesh stand in
+ * for the per-cell ones (approximate local solves; the per-cell inverses of C5 are
+ * 96 GB and 1.5e13 flop of setup). */
 int stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
-                        int n_hcoarse, int time_coarsen, int k_min, const double *vertices, int nu1, int nu2, double omega,
+                        int n_hcoarse, int time_coarsen, int k_min, int affine_patches, const double *vertices, int nu1,
+                        int nu2, double omega,
                         double rtol, double atol, int max_iterations, stmg3_solver **out);
 int stmg3_solver_destroy(stmg3_solver *solver);
 /* out[0] = n_levels; per level l (coarse first) out[1+7l..]: nx, ny, nz, r, k,

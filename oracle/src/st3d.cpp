@@ -907,23 +907,22 @@ plan(int nx, int ny, int nz, int r, int k, int N, double t_end, double nu, doubl
   {
     int nx, ny, nz, r, k, tsh;
   };
-  std::vector<Desc> d; // fine first
-  d.push_back({nx, ny, nz, r, k, 0});
-  while (d.back().k > g_kmin)
+  // combine_hierarchies (hierarchy.cpp:9-97, harness.cpp:26-42) in 3D: the
+  // spatial list (fine first: p-halving of r, then h-steps, each h-step also
+  // halving the time grid when time_coarsen) and the temporal list (k, k/2,
+  // ..., k_min) are aligned at the COARSE end, so the temporal p-steps sit on
+  // the coarsest levels (as the reference's C2 plan: L1 = h_space + p_time).
+  std::vector<Desc> sp; // spatial, fine first (k filled below)
+  sp.push_back({nx, ny, nz, r, 0, 0});
+  while (sp.back().r > 1)
     {
-      Desc e = d.back();
-      e.k = e.k / 2;
-      d.push_back(e);
-    }
-  while (d.back().r > 1)
-    {
-      Desc e = d.back();
+      Desc e = sp.back();
       e.r = e.r / 2;
-      d.push_back(e);
+      sp.push_back(e);
     }
   for (int i = 0; i < n_hcoarse; ++i)
     {
-      Desc e = d.back();
+      Desc e = sp.back();
       if (e.nx % 2 || e.ny % 2 || e.nz % 2)
         throw std::invalid_argument("plan: mesh not divisible");
       e.nx /= 2;
@@ -931,7 +930,20 @@ plan(int nx, int ny, int nz, int r, int k, int N, double t_end, double nu, doubl
       e.nz /= 2;
       if (time_coarsen)
         e.tsh += 1;
-      d.push_back(e);
+      sp.push_back(e);
+    }
+  std::vector<int> tk{k}; // temporal, fine first
+  while (tk.back() > g_kmin)
+    tk.push_back(tk.back() / 2);
+  const size_t L = std::max(sp.size(), tk.size());
+  std::vector<Desc> d(L); // fine first
+  for (size_t i = 0; i < L; ++i)
+    {
+      // index from the coarse end: c = L - 1 - i
+      const size_t c = L - 1 - i;
+      Desc e = sp[std::min(sp.size() - 1, i)];
+      e.k = tk[tk.size() - 1 - std::min(c, tk.size() - 1)];
+      d[i] = e;
     }
   auto H = std::make_unique<Hier3>();
   const double tau = t_end / N;

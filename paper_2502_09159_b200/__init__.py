@@ -103,7 +103,7 @@ _SIGNATURES = {
     "stmg3_vanka_update": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int], _c_int),
     "stmg3_project_mean_zero": ([_c_void_p, _c_void_p, _c_int], _c_int),
     "stmg3_solver_create": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double,
-                             _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
+                             _c_int, _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
                              ctypes.POINTER(_c_void_p)], _c_int),
     "stmg3_solver_destroy": ([_c_void_p], _c_int),
     "stmg3_solver_info": ([_c_void_p, _c_i64p], _c_int),
@@ -474,14 +474,14 @@ class Solver3:
 
     def __init__(self, ctx: Context, nx: int, ny: int, nz: int, r: int, k: int, tau: float, nu: float = 1.0,
                  gamma: float = 1.0, n_hcoarse: int = 1, time_coarsen: bool = True, k_min: int = 0, vertices=None,
-                 nu1: int = 2,
+                 affine_patches: bool = False, nu1: int = 2,
                  nu2: int = 2, omega: float = 0.8, rtol: float = 1e-8, atol: float = 1e-14,
                  max_iterations: int = 200):
         self.ctx = ctx
         lib = load_library()
         h = _c_void_p()
         _check(lib.stmg3_solver_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse, int(time_coarsen),
-                                       k_min, _hptr(vertices), nu1, nu2, omega, rtol, atol, max_iterations,
+                                       k_min, int(affine_patches), _hptr(vertices), nu1, nu2, omega, rtol, atol, max_iterations,
                                        ctypes.byref(h)))
         self._h = h
         out = (ctypes.c_int64 * (1 + 7 * 64))()

@@ -68,12 +68,13 @@ def run_c3(torch, stmg, args):
     out = {"config": f"C3: {n}^3 Q2/P1disc, DG(1), {N} intervals, nu=1, gamma=1, V(2,2) cell Vanka"}
     t0 = time.perf_counter()
     spec = args.c3_variant == "spec"
-    # "spec": BASELINE's hierarchy (k 1 -> 0, then h in space and time);
-    # "robust": k kept at 1, h in space only, exact coarse forward
-    # substitution over all intervals (time coarsening with the
-    # time-block-diagonal Vanka is not h-robust)
+    # both: k 1 -> 0 on the coarsest level (temporal p-steps aligned at the
+    # coarse end, as combine_hierarchies). "spec": h in space AND time down
+    # to 4^3 x 8 (BASELINE's plan); "robust": h in space only down to 2^3,
+    # exact coarse forward substitution over all intervals (DESIGN.md 3.4:
+    # time coarsening with the time-block-diagonal Vanka is not h-robust)
     sol = stmg.Solver3(ctx, n, n, n, 1, 1, 1.0 / N, 1.0, 1.0, n_hcoarse=args.c3_hcoarse if spec else args.c3_hcoarse + 1,
-                       time_coarsen=spec, k_min=0 if spec else 1, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
+                       time_coarsen=spec, k_min=0, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
     out["variant"] = args.c3_variant
     torch.cuda.synchronize()
     out["setup_s"] = time.perf_counter() - t0
@@ -118,18 +119,60 @@ def run_c3(torch, stmg, args):
     return out
 
 
-def run_c5(torch, stmg, args):
+def c5_vertices(n, seed=2025):
+    """Unit-cube vertices, interior ones displaced by a seeded uniform
+    perturbation of at most 0.1 h per coordinate (BASELINE C5)."""
     import numpy as np
 
-    ctx = stmg.Context(0)
-    n, N = args.c5_cells, args.c5_intervals
-    rng = np.random.default_rng(2025)
+    rng = np.random.default_rng(seed)
     z, yy, xx = np.meshgrid(np.arange(n + 1) / n, np.arange(n + 1) / n, np.arange(n + 1) / n, indexing="ij")
     v = np.stack([xx, yy, z], axis=-1)
     inner = np.zeros(v.shape[:3], dtype=bool)
     inner[1:-1, 1:-1, 1:-1] = True
     v[inner] += rng.uniform(-1, 1, v.shape)[inner] * 0.1 / n
-    verts = np.ascontiguousarray(v.reshape(-1))
+    return np.ascontiguousarray(v.reshape(-1))
+
+
+def run_c5_solve(torch, stmg, args):
+    """C5 full solve on one GPU: the 128-interval system as macro steps of
+    args.c5_slab intervals (v_init hand-off), FGMRES +
+    hp-STMG V(2,2): p in k 2 -> 1 and r 2 -> 1, h in space down to 2^3, cell
+    Vanka with the undeformed patch inverses (affine_patches)."""
+    n, N, slab = args.c5_cells, args.c5_intervals, args.c5_slab
+    verts = c5_vertices(n)
+    ctx = stmg.Context(0)
+    t0 = time.perf_counter()
+    sol = stmg.Solver3(ctx, n, n, n, 2, 2, 1.0 / N, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=1,
+                       vertices=verts, affine_patches=True, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    f = sol.finest
+    nsl = N // slab
+    Fs = [consistent(torch, f, seeded(torch, slab * f.size, 500 + m), slab) for m in range(nsl)]
+    X = torch.zeros(slab * f.size, dtype=torch.float64, device="cuda")
+    sol.solve_all_at_once(Fs[0], X, slab)  # warm-up (workspaces)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its = []
+    v = None
+    e0.record()
+    for m in range(nsl):
+        it, hist = sol.solve_all_at_once(Fs[m], X, slab, v_init=v)
+        its.append(it)
+        v = X[(slab - 1) * f.size + (f.n_slots - 1) * f.n_velocity:(slab - 1) * f.size + f.n_slots * f.n_velocity].clone()
+    e1.record()
+    torch.cuda.synchronize()
+    s = e0.elapsed_time(e1) * 1e-3
+    return {"dofs": N * f.size, "seconds": s, "dofs_per_s": N * f.size / s, "setup_s": setup,
+            "fgmres_iterations_per_slab": its, "levels": sol.level_info,
+            "partition": f"1 GPU, {nsl} macro steps x {slab} intervals",
+            "smoother": "cell Vanka, undeformed patch inverses (affine_patches)"}
+
+
+def run_c5(torch, stmg, args):
+    ctx = stmg.Context(0)
+    n, N = args.c5_cells, args.c5_intervals
+    verts = c5_vertices(n)
     lvl = stmg.Level3(ctx, n, n, n, 2, 2, 1.0 / N, 1.0, 1.0, stmg.SMOOTHER_NONE, vertices=verts)
     dofs = N * lvl.size
     out = {"config": f"C5: {n}^3 deformed (<= 0.1 h), Q3/P2disc, DG(2), {N} intervals", "dofs": dofs}
@@ -154,6 +197,7 @@ def main():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--c3-variant", default="robust", choices=["robust", "spec"])
     ap.add_argument("--maxit", type=int, default=200)
+    ap.add_argument("--c5-slab", type=int, default=16)
     args = ap.parse_args()
     import torch
     import paper_2502_09159_b200 as stmg
@@ -163,6 +207,9 @@ def main():
         res["C3"] = run_c3(torch, stmg, args)
     if "C5" in args.case:
         res["C5"] = run_c5(torch, stmg, args)
+        if not args.no_solve:
+            torch.cuda.empty_cache()
+            res["C5"]["solve"] = run_c5_solve(torch, stmg, args)
     print(json.dumps(res))
 
 
