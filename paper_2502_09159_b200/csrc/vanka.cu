@@ -310,6 +310,120 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
         }
     }
 }
+
+// ---------------------------------------------------------------------------
+// Large patches (176 < n_T <= 790, e.g. 3D Q3 cells with DG(2): n_T = 606):
+// Z = A^{-1} R on the FP64 tensor path with the inverse streamed from L2
+// (a class inverse is 2.9 MB; the <= 27 Cartesian classes of a level stay
+// L2-resident) as A-fragments, one 32-column tile of R (patch, interval)
+// staged in shared memory for the whole contraction, and the weighted result
+// scattered straight from the accumulators (patches of one launch share no
+// dof, so the adds never collide).
+constexpr int kBThreads = 512; // 16 warps
+constexpr int kBCols = 32;     // columns per tile
+constexpr int kBLd = 36;       // R pitch: conflict-free B-fragment loads
+constexpr int kBMaxTiles = 7;  // row tiles per warp: 16 * 7 * 8 = 896 rows
+constexpr int kBGroup = 16;    // intervals per block
+
+template <int TPW>
+__global__ void __launch_bounds__(kBThreads, 1)
+vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
+                 const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
+                 const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals, double omega)
+{
+  extern __shared__ __align__(16) double bsm[];
+  const VankaBatch bt = batches[blockIdx.x];
+  const DevPatchClass pc = classes[bt.cls];
+  const int nt = pc.n_t, nvel = pc.n_vel;
+  const int ks = (nt + 3) / 4;
+  double *Rs = bsm;                                   // (4 ks) x kBLd
+  long long *cvb = reinterpret_cast<long long *>(Rs + 4 * ks * kBLd); // velocity column bases
+  long long *cpb = cvb + kBCols;                                      // pressure column bases
+  const int n0 = blockIdx.y * kBGroup;
+  const int ng = min(kBGroup, n_intervals - n0);
+  const int ncols = bt.count * ng;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rtiles = (nt + 7) / 8;
+  for (int c0 = 0; c0 < ncols; c0 += kBCols)
+    {
+      if (tid < kBCols)
+        {
+          const int j = c0 + tid;
+          long long vb = 0, pb = 0;
+          if (j < ncols)
+            {
+              const int patch = j / ng, n = n0 + j - patch * ng;
+              vb = n * isz + __ldg(vel_anchor + bt.first + patch);
+              pb = n * isz + __ldg(pre_anchor + bt.first + patch);
+            }
+          cvb[tid] = vb;
+          cpb[tid] = pb;
+        }
+      __syncthreads();
+      // gather R (rows >= nt and columns >= ncols are zero)
+      for (int e = tid; e < 4 * ks * kBCols; e += kBThreads)
+        {
+          const int row = e / kBCols, c = e - row * kBCols;
+          double v = 0.0;
+          if (row < nt && c0 + c < ncols)
+            v = __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + __ldg(pc.rel + row));
+          Rs[row * kBLd + c] = v;
+        }
+      __syncthreads();
+      double acc[TPW][kBCols / 8][2];
+#pragma unroll
+      for (int t = 0; t < TPW; ++t)
+#pragma unroll
+        for (int ct = 0; ct < kBCols / 8; ++ct)
+          acc[t][ct][0] = acc[t][ct][1] = 0.0;
+      const double *bbase = Rs + (lane & 3) * kBLd + (lane >> 2);
+      for (int kk = 0; kk < ks; ++kk)
+        {
+          double bf[kBCols / 8];
+#pragma unroll
+          for (int ct = 0; ct < kBCols / 8; ++ct)
+            bf[ct] = bbase[4 * kk * kBLd + 8 * ct];
+          const int col = 4 * kk + (lane & 3);
+#pragma unroll
+          for (int t = 0; t < TPW; ++t)
+            {
+              const int rt = warp + 16 * t;
+              if (rt < rtiles)
+                {
+                  const int row = 8 * rt + (lane >> 2);
+                  const double a = (row < nt && col < nt) ? __ldg(pc.inverse + static_cast<long long>(row) * nt + col)
+                                                          : 0.0;
+#pragma unroll
+                  for (int ct = 0; ct < kBCols / 8; ++ct)
+                    dmma_8x8x4(acc[t][ct], a, bf[ct]);
+                }
+            }
+        }
+      // scatter u += omega w Z from the accumulators
+#pragma unroll
+      for (int t = 0; t < TPW; ++t)
+        {
+          const int rt = warp + 16 * t;
+          const int row = 8 * rt + (lane >> 2);
+          if (rt < rtiles && row < nt)
+            {
+              const double wr = omega * __ldg(pc.weight + row);
+              const long long rel = __ldg(pc.rel + row);
+              const bool vel = row < nvel;
+#pragma unroll
+              for (int ct = 0; ct < kBCols / 8; ++ct)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  {
+                    const int c = 8 * ct + 2 * (lane & 3) + h;
+                    if (c0 + c < ncols)
+                      atomicAdd(u + (vel ? cvb[c] : cpb[c]) + rel, wr * acc[t][ct][h]);
+                  }
+            }
+        }
+      __syncthreads();
+    }
+}
 } // namespace
 
 /// Launch one colour: `n_batches` batches over `n_intervals` intervals.
@@ -348,6 +462,27 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
         go(vanka_dmma_kernel<28>);
       else
         go(vanka_dmma_kernel<32>);
+      return cudaGetLastError();
+    }
+  if (!item_ptr && max_nt <= 16 * kBMaxTiles * 8)
+    {
+      const int ks = (max_nt + 3) / 4;
+      const size_t smem = sizeof(double) * (4 * ks * kBLd) + sizeof(long long) * 2 * kBCols;
+      const int tpw = ((max_nt + 7) / 8 + 15) / 16;
+      dim3 grid(n_batches, (n_intervals + kBGroup - 1) / kBGroup);
+      auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, kBThreads, smem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz, n_intervals,
+                                                omega);
+      };
+      if (tpw <= 2)
+        go(vanka_big_kernel<2>);
+      else if (tpw <= 4)
+        go(vanka_big_kernel<4>);
+      else if (tpw <= 5)
+        go(vanka_big_kernel<5>);
+      else
+        go(vanka_big_kernel<7>);
       return cudaGetLastError();
     }
   const int ntp = (max_nt + 1) & ~1;
