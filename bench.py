@@ -31,6 +31,7 @@ Extra fields of the JSON line (not the headline; skipped with --no-solve):
   3D.C3                (1 GPU) C3: 32^3 Q2/P1disc, DG(1), 64 intervals: vmult,
                        cell-Vanka step, full all-at-once solve (tools/bench3d.py)
   3D.C5                (1 GPU) C5: 32^3 deformed Q3/P2disc, DG(2), 128 intervals: vmult
+                       and the full solve as 8 macro steps of 16 intervals
 """
 from __future__ import annotations
 
@@ -285,10 +286,12 @@ def three_d_leg(torch, stmg):
     import bench3d
 
     a = argparse.Namespace(reps=5, c3_cells=32, c3_intervals=64, c3_hcoarse=3, c3_variant="robust", maxit=200,
-                           no_solve=False, c5_cells=32, c5_intervals=128)
+                           no_solve=False, c5_cells=32, c5_intervals=128, c5_slab=16, c5_variant="robust")
     out = {"C3": bench3d.run_c3(torch, stmg, a)}
     torch.cuda.empty_cache()
     out["C5"] = bench3d.run_c5(torch, stmg, a)
+    torch.cuda.empty_cache()
+    out["C5"]["solve"] = bench3d.run_c5_solve(torch, stmg, a)
     torch.cuda.empty_cache()
     return out
 
@@ -296,9 +299,8 @@ def three_d_leg(torch, stmg):
 def c3_slab_leg(stmg, torch, dist, world, rank, n_total=64):
     """BASELINE configs[2] (C3) partitioned by time slabs: the 64-interval
     32^3 Q2/P1disc DG(1) all-at-once system split over the ranks (strong
-    scaling), FGMRES + hp-STMG V(2,2) (h in space down to 2^3 with k 1 -> 0
-    on the coarsest level, exact coarse forward substitution in time over
-    all intervals), halo /
+    scaling), FGMRES + hp-STMG V(2,2) (h in space down to 2^3, k kept at 1,
+    exact coarse forward substitution in time over all intervals), halo /
     Krylov dots / coarse right-hand sides over NCCL. Time = max over ranks."""
     from paper_2502_09159_b200 import timeslab
 
@@ -307,7 +309,7 @@ def c3_slab_leg(stmg, torch, dist, world, rank, n_total=64):
 
     n_local = n_total // world
     ctx = stmg.Context(torch.cuda.current_device())
-    sol = stmg.Solver3(ctx, 32, 32, 32, 1, 1, 1.0 / n_total, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=0,
+    sol = stmg.Solver3(ctx, 32, 32, 32, 1, 1, 1.0 / n_total, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=1,
                        nu1=2, nu2=2, rtol=1e-8)
     if world > 1:
         sol.set_comm(timeslab.TorchComm(device=f"cuda:{torch.cuda.current_device()}"))

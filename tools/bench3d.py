@@ -68,13 +68,13 @@ def run_c3(torch, stmg, args):
     out = {"config": f"C3: {n}^3 Q2/P1disc, DG(1), {N} intervals, nu=1, gamma=1, V(2,2) cell Vanka"}
     t0 = time.perf_counter()
     spec = args.c3_variant == "spec"
-    # both: k 1 -> 0 on the coarsest level (temporal p-steps aligned at the
-    # coarse end, as combine_hierarchies). "spec": h in space AND time down
-    # to 4^3 x 8 (BASELINE's plan); "robust": h in space only down to 2^3,
-    # exact coarse forward substitution over all intervals (DESIGN.md 3.4:
-    # time coarsening with the time-block-diagonal Vanka is not h-robust)
+    # "spec": BASELINE's plan, k 1 -> 0 (temporal p-step on the coarsest
+    # level, as combine_hierarchies) and h in space AND time down to 4^3 x 8;
+    # "robust": k kept at 1, h in space only down to 2^3, exact coarse
+    # forward substitution over all intervals (time
+    # coarsening and k -> 0 cost iterations with the time-block-diagonal Vanka)
     sol = stmg.Solver3(ctx, n, n, n, 1, 1, 1.0 / N, 1.0, 1.0, n_hcoarse=args.c3_hcoarse if spec else args.c3_hcoarse + 1,
-                       time_coarsen=spec, k_min=0, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
+                       time_coarsen=spec, k_min=0 if spec else 1, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
     out["variant"] = args.c3_variant
     torch.cuda.synchronize()
     out["setup_s"] = time.perf_counter() - t0
@@ -136,14 +136,15 @@ def c5_vertices(n, seed=2025):
 def run_c5_solve(torch, stmg, args):
     """C5 full solve on one GPU: the 128-interval system as macro steps of
     args.c5_slab intervals (v_init hand-off), FGMRES +
-    hp-STMG V(2,2): p in k 2 -> 1 and r 2 -> 1, h in space down to 2^3, cell
-    Vanka with the undeformed patch inverses (affine_patches)."""
+    hp-STMG V(2,2): p in r 2 -> 1, h in space down to 2^3 ("robust": k kept
+    at 2; "spec": k 2 -> 1 -> 0 on the coarsest levels), cell Vanka with the
+    undeformed patch inverses (affine_patches)."""
     n, N, slab = args.c5_cells, args.c5_intervals, args.c5_slab
     verts = c5_vertices(n)
     ctx = stmg.Context(0)
     t0 = time.perf_counter()
-    sol = stmg.Solver3(ctx, n, n, n, 2, 2, 1.0 / N, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=1,
-                       vertices=verts, affine_patches=True, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
+    sol = stmg.Solver3(ctx, n, n, n, 2, 2, 1.0 / N, 1.0, 1.0, n_hcoarse=4, time_coarsen=False,
+                       k_min=2 if args.c5_variant == "robust" else 0, vertices=verts, affine_patches=True, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     f = sol.finest
@@ -166,7 +167,7 @@ def run_c5_solve(torch, stmg, args):
     return {"dofs": N * f.size, "seconds": s, "dofs_per_s": N * f.size / s, "setup_s": setup,
             "fgmres_iterations_per_slab": its, "levels": sol.level_info,
             "partition": f"1 GPU, {nsl} macro steps x {slab} intervals",
-            "smoother": "cell Vanka, undeformed patch inverses (affine_patches)"}
+            "smoother": "cell Vanka, undeformed patch inverses (affine_patches)", "variant": args.c5_variant}
 
 
 def run_c5(torch, stmg, args):
@@ -198,6 +199,7 @@ def main():
     ap.add_argument("--c3-variant", default="robust", choices=["robust", "spec"])
     ap.add_argument("--maxit", type=int, default=200)
     ap.add_argument("--c5-slab", type=int, default=16)
+    ap.add_argument("--c5-variant", default="robust", choices=["robust", "spec"])
     args = ap.parse_args()
     import torch
     import paper_2502_09159_b200 as stmg
