@@ -127,6 +127,9 @@ constexpr int kDRows = 128;               // max n_T
 #define STMG_VANKA_COLS 16
 #endif
 constexpr int kDCols = STMG_VANKA_COLS;   // columns per tile
+#ifndef STMG_VANKA176_COLS
+#define STMG_VANKA176_COLS 8 // 176-row variant: 8 columns keep 2 x 44 A-fragments in registers
+#endif
 constexpr int kDRLd = 36;                 // R tile pitch (doubles): conflict-free B-fragment loads
 constexpr int kDZLd = 33;                 // Z tile pitch
 constexpr int kDPer = kDRows * kDCols / kDThreads; // elements per thread per tile (8)
@@ -141,15 +144,16 @@ dmma_8x8x4(double (&d)[2], double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int KS, int ROWS = kDRows, int TPW = 1>
-__global__ void __launch_bounds__(ROWS * 4 / TPW, 1)
+template <int KS, int ROWS = kDRows, int TPW = 1, int COLS = kDCols>
+__global__ void __launch_bounds__(ROWS / 8 / TPW * 32, 1)
 vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ items,
                   const int *__restrict__ item_ptr, const long long *__restrict__ vel_anchor,
                   const long long *__restrict__ pre_anchor, const double *__restrict__ r, double *__restrict__ u,
                   long long isz, int n_intervals, double omega)
 {
   // ROWS rows of the patch matrix; warp w owns the TPW 8-row tiles w + j * NW
-  constexpr int kDRows = ROWS, kDThreads = ROWS * 4 / TPW, kDPer = kDRows * kDCols / kDThreads;
+  constexpr int kDCols = COLS;
+  constexpr int kDRows = ROWS, kDThreads = ROWS / 8 / TPW * 32, kDPer = kDRows * kDCols / kDThreads;
   constexpr int NW = kDThreads / 32;
   extern __shared__ __align__(16) double dsm[];
   double *Rs = dsm;                                                 // kDRows x kDRLd
@@ -443,11 +447,11 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       const int ks = (max_nt + 3) / 4;
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
-        kern<<<grid, rows == 176 ? 352 : rows * 4, dsmem, stream>>>(classes, batches, item_ptr, vel_anchor,
-                                                                    pre_anchor, r, u, isz, n_intervals, omega);
+        kern<<<grid, rows == 176 ? 352 : rows * 4, dsmem, stream>>>(
+          classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega);
       };
       if (rows == 176)
-        go(vanka_dmma_kernel<44, 176, 2>);
+        go(vanka_dmma_kernel<44, 176, 2, STMG_VANKA176_COLS>);
       else if (ks <= 8)
         go(vanka_dmma_kernel<8>);
       else if (ks <= 12)
