@@ -147,6 +147,43 @@ oracle_level_sizes(void *hp, long *out)
   out[6] = h->sm ? static_cast<long>(h->sm->patches().size()) : 0;
 }
 
+/// Saddle-point health of a converged step (solver.cpp:286-299): per slot
+/// ||B v|| / sqrt(v^T M v) and |<mean, p>| / ||p||, maximised over the slots.
+int
+oracle_step_health(void *hp, const double *x, double *out)
+{
+  return guard([&] {
+    const auto *h = static_cast<LevelHandle *>(hp);
+    const BlockVector xv = view_copy(*h->op, x);
+    const Index mv = h->vs->n_dofs(), mp = h->ps->n_dofs();
+    Vec work_p(mp), work_v(mv);
+    double max_div = 0.0, max_mean = 0.0;
+    for (int a = 0; a < xv.ns; ++a)
+      {
+        std::fill(work_p.begin(), work_p.end(), 0.0);
+        std::fill(work_v.begin(), work_v.end(), 0.0);
+        h->op->apply_div(xv.velocity(a), work_p.data());
+        h->op->apply_velocity_mass(xv.velocity(a), work_v.data());
+        double vmv = 0.0, pn = 0.0, bn = 0.0, mdot = 0.0;
+        for (Index i = 0; i < mv; ++i)
+          vmv += xv.velocity(a)[i] * work_v[i];
+        for (Index i = 0; i < mp; ++i)
+          {
+            bn += work_p[i] * work_p[i];
+            pn += xv.pressure(a)[i] * xv.pressure(a)[i];
+            mdot += h->ps->mean_vector()[i] * xv.pressure(a)[i];
+          }
+        const double vnorm = std::sqrt(std::abs(vmv));
+        if (vnorm > 0.0)
+          max_div = std::max(max_div, std::sqrt(bn) / vnorm);
+        if (pn > 0.0)
+          max_mean = std::max(max_mean, std::abs(mdot) / std::sqrt(pn));
+      }
+    out[0] = max_div;
+    out[1] = max_mean;
+  });
+}
+
 int
 oracle_apply_block(void *hp, const double *x, double *y, int raw)
 {

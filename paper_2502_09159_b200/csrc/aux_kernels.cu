@@ -588,3 +588,55 @@ launch_coarse_forward(const double *G, const double *H, int n, int mv, long long
 }
 
 } // namespace stmg_b200
+
+// ---------------------------------------------------------------- step health
+namespace stmg_b200
+{
+namespace
+{
+constexpr int kHealthThreads = 256;
+/// Per (interval, slot): sum (B v)^2, v . M v, <mean, p>, p . p from the
+/// health application y = [M v^a ; B v^a] (solver.cpp:286-299).
+__global__ void __launch_bounds__(kHealthThreads)
+health_kernel(DevGeom G, double cell_area, const double *__restrict__ X, const double *__restrict__ Y,
+              double *__restrict__ out)
+{
+  const int a = blockIdx.x, n = blockIdx.y;
+  const double *xv = X + n * G.isz + a * G.mv, *yv = Y + n * G.isz + a * G.mv;
+  const double *xp = X + n * G.isz + G.S * G.mv + a * G.mp, *yp = Y + n * G.isz + G.S * G.mv + a * G.mp;
+  double s_div = 0.0, s_vmv = 0.0, s_m = 0.0, s_p = 0.0;
+  for (long long i = threadIdx.x; i < G.mv; i += kHealthThreads)
+    s_vmv = fma(xv[i], yv[i], s_vmv);
+  for (long long i = threadIdx.x; i < G.mp; i += kHealthThreads)
+    {
+      s_div = fma(yp[i], yp[i], s_div);
+      s_p = fma(xp[i], xp[i], s_p);
+      if (i % G.np == 0)
+        s_m = fma(cell_area, xp[i], s_m); // mean vector: |K| on the constant mode (dof_space.cpp:99-105)
+    }
+  s_div = block_sum<kHealthThreads>(s_div);
+  s_vmv = block_sum<kHealthThreads>(s_vmv);
+  s_m = block_sum<kHealthThreads>(s_m);
+  s_p = block_sum<kHealthThreads>(s_p);
+  if (threadIdx.x == 0)
+    {
+      double *o = out + 4 * (static_cast<long long>(n) * G.S + a);
+      o[0] = s_div;
+      o[1] = s_vmv;
+      o[2] = s_m;
+      o[3] = s_p;
+    }
+}
+} // namespace
+
+cudaError_t
+launch_health(const DevGeom &G, double cell_area, const double *X, const double *Y, double *out, int n_intervals,
+              cudaStream_t st)
+{
+  if (n_intervals == 0)
+    return cudaSuccess;
+  dim3 grid(G.S, n_intervals);
+  health_kernel<<<grid, kHealthThreads, 0, st>>>(G, cell_area, X, Y, out);
+  return cudaGetLastError();
+}
+} // namespace stmg_b200

@@ -127,6 +127,9 @@ cudaError_t launch_interpolate_manufactured(const DevGeom &G, int r, const Probl
                                             double tau, double *X, int n_intervals, cudaStream_t st);
 cudaError_t launch_errors_manufactured(const DevGeom &G, int r, const ProblemTables &T, double t_start, double tau,
                                        const double *X, int n_intervals, double *part, double *out, cudaStream_t st);
+/// Saddle-point health sums per (interval, slot) of y = [M v ; B v]: 4 doubles each.
+cudaError_t launch_health(const DevGeom &G, double cell_area, const double *X, const double *Y, double *out,
+                          int n_intervals, cudaStream_t st);
 int dot_partials();
 cudaError_t launch_dot(const double *x, const double *y, long long n, double *part, double *out, cudaStream_t st);
 /// y += a x with a = alpha_dev ? sign * (*alpha_dev) : alpha (sign applies to
