@@ -91,6 +91,11 @@ int stmg_vmult(stmg_level *level, const double *x, double *y, int n_intervals, c
 int stmg_residual(stmg_level *level, const double *b, const double *x, double *r, int n_intervals,
                   const double *x_prev_slot, int coupled);
 
+/* Saddle-point health of converged steps (solver.cpp:286-299): per interval
+ * out[2n] = max over slots of ||B v|| / sqrt(v^T M v), out[2n+1] = max over
+ * slots of |<mean, p>| / ||p|| (the StepRecord fields of time_march). */
+int stmg_step_health(stmg_level *level, const double *X, int n_intervals, double *out);
+
 /* out = coupling_rhs(v_prev) for one interval (st_operator.cpp:409-421). */
 int stmg_coupling_rhs(stmg_level *level, const double *v_prev, double *out);
 

@@ -59,6 +59,7 @@ _SIGNATURES = {
     "stmg_vmult": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
     "stmg_residual": ([_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, _c_int], _c_int),
     "stmg_coupling_rhs": ([_c_void_p, _c_void_p, _c_void_p], _c_int),
+    "stmg_step_health": ([_c_void_p, _c_void_p, _c_int, ctypes.POINTER(_c_double)], _c_int),
     "stmg_apply_additive": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
     "stmg_smooth_step": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int, _c_void_p], _c_int),
     "stmg_vanka_update": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int], _c_int),
@@ -253,6 +254,12 @@ class Level:
         _check(load_library().stmg_residual(self._h, _ptr(b), _ptr(x), _ptr(r), n_intervals, _ptr(x_prev_slot),
                                             int(coupled)))
         return r
+
+    def step_health(self, X, n_intervals: int = 1):
+        """Saddle-point health per interval (solver.cpp:286-299): [(max_divergence, max_pressure_mean), ...]."""
+        out = (ctypes.c_double * (2 * n_intervals))()
+        _check(load_library().stmg_step_health(self._h, _ptr(X), n_intervals, out))
+        return [(out[2 * i], out[2 * i + 1]) for i in range(n_intervals)]
 
     def coupling_rhs(self, v_prev, out):
         _check(load_library().stmg_coupling_rhs(self._h, _ptr(v_prev), _ptr(out)))

@@ -1243,6 +1243,63 @@ stmg_coupling_rhs(stmg_level *L, const double *v_prev, double *out)
 }
 
 int
+stmg_step_health(stmg_level *L, const double *X, int n, double *out)
+{
+  return guarded([&] {
+    if (n < 1 || !X || !out)
+      throw std::invalid_argument("step_health: bad arguments");
+    const LevelSpec &s = L->spec;
+    // y = [M v^a ; B v^a] per slot: the fused operator with K_t = M_t = I,
+    // no coupling, nu = gamma = 0 and the pressure input zeroed
+    LevelSpec hs = s;
+    hs.nu = 0.0;
+    hs.gamma = 0.0;
+    LevelConsts hc = make_level_consts(hs);
+    const double J = s.hx * s.hy / 4.0;
+    const int S = s.S();
+    for (int a = 0; a < S; ++a)
+      {
+        hc.lv[a] = hc.lvJ[a] = 0.0;
+        for (int b = 0; b < S; ++b)
+          {
+            hc.Kt[a * S + b] = hc.Mt[a * S + b] = (a == b) ? 1.0 : 0.0;
+            hc.KtJ[a * S + b] = hc.MtJ[a * S + b] = (a == b) ? J : 0.0;
+          }
+      }
+    const long long isz = s.isz(), tot = isz * n;
+    DevArray<double> xv, y, sums;
+    xv.resize(tot);
+    y.resize(tot);
+    sums.resize(4 * static_cast<size_t>(S) * n);
+    check(cudaMemcpyAsync(xv.p, X, sizeof(double) * tot, cudaMemcpyDeviceToDevice, L->ctx->stream), "copy");
+    for (int t = 0; t < n; ++t)
+      check(cudaMemsetAsync(xv.p + t * isz + S * s.mv(), 0, sizeof(double) * S * s.mp(), L->ctx->stream), "memset");
+    check(launch_vmult(s.r, S, hc, xv.p, nullptr, y.p, n, nullptr, 0, 2, L->ctx->stream), "vmult");
+    check(launch_health(L->geom, s.hx * s.hy, X, y.p, sums.p, n, L->ctx->stream), "health");
+    L->ctx->count(2);
+    std::vector<double> h(4 * static_cast<size_t>(S) * n);
+    check(cudaMemcpyAsync(h.data(), sums.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, L->ctx->stream),
+          "d2h");
+    check(cudaStreamSynchronize(L->ctx->stream), "sync");
+    for (int t = 0; t < n; ++t)
+      {
+        double max_div = 0.0, max_mean = 0.0;
+        for (int a = 0; a < S; ++a)
+          {
+            const double *q = &h[4 * (static_cast<size_t>(t) * S + a)];
+            const double vnorm = std::sqrt(std::abs(q[1]));
+            if (vnorm > 0.0)
+              max_div = std::max(max_div, std::sqrt(q[0]) / vnorm);
+            if (q[3] > 0.0)
+              max_mean = std::max(max_mean, std::abs(q[2]) / std::sqrt(q[3]));
+          }
+        out[2 * t] = max_div;
+        out[2 * t + 1] = max_mean;
+      }
+  });
+}
+
+int
 stmg_apply_additive(stmg_level *L, const double *r, double *out, int n)
 {
   return guarded([&] {

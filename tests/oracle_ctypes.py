@@ -40,6 +40,7 @@ def lib():
         L.oracle_level_sizes.argtypes = [_P, ctypes.POINTER(ctypes.c_long)]
         L.oracle_apply_block.argtypes = [_P, _D, _D, ctypes.c_int]
         L.oracle_coupling_rhs.argtypes = [_P, _D, _D]
+        L.oracle_step_health.argtypes = [_P, _D, _D]
         L.oracle_vmult_all.argtypes = [_P, _D, _D, ctypes.c_int, _D, ctypes.c_int]
         L.oracle_apply_additive.argtypes = [_P, _D, _D]
         L.oracle_smooth_step_all.argtypes = [_P, _D, _D, ctypes.c_double, ctypes.c_int, _D, ctypes.c_int]
@@ -98,6 +99,11 @@ class OracleLevel:
         y = np.zeros(self.size)
         _chk(lib().oracle_apply_block(self.h, _d(x), _d(y), int(raw)))
         return y
+
+    def step_health(self, x):
+        out = np.zeros(2)
+        _chk(lib().oracle_step_health(self.h, _d(x), _d(out)))
+        return float(out[0]), float(out[1])
 
     def coupling_rhs(self, v_prev):
         y = np.zeros(self.size)

@@ -314,3 +314,27 @@ def test_factored_vanka_matches_oracle(ctx, stmg, oracle, nc, k, n, monkeypatch)
     assert np.array_equal(outs[0], outs[1])
     want = ref.smooth_step_all(b, u, 0.8, n, prev)
     assert rel_max(outs[0], want) <= SMOOTH_TOL
+
+
+@pytest.mark.parametrize("nc,r,k", [(4, 1, 1), (8, 2, 2), (2, 3, 1)])
+def test_step_health_matches_oracle(ctx, stmg, nc, r, k):
+    """time_march's saddle-point health record (solver.cpp:286-299): max over
+    slots of ||B v|| / sqrt(v^T M v) and |<mean, p>| / ||p||, per interval, on
+    seeded vectors and on a converged time-march trajectory."""
+    lvl = stmg.Level(ctx, nc, nc, r, k, 1.0 / 8, 1.0, 1.0, stmg.SMOOTHER_NONE)
+    ref = oc.OracleLevel(nc, r, k, 1.0 / 8, 1.0, 1.0, 0, build_smoother=False)
+    n = 3
+    X = oc.seeded(n * ref.size, 21)
+    got = lvl.step_health(torch.from_numpy(X).cuda(), n)
+    for t in range(n):
+        want = ref.step_health(np.ascontiguousarray(X[t * ref.size:(t + 1) * ref.size]))
+        assert abs(got[t][0] - want[0]) <= 1e-12 * max(1.0, want[0])
+        assert abs(got[t][1] - want[1]) <= 1e-12 * max(1.0, want[1])
+    sol = stmg.Solver(ctx, 2, 1, 1, n_steps=4, nu=1.0, gamma=1.0, nu1=2, nu2=2)
+    lv = sol.finest
+    F = oc.make_consistent(oc.seeded(4 * lv.size, 5), lv.n_slots, lv.n_scalar, lv.grid_x, lv.n_pressure,
+                           lv.n_pressure // 3, 3, 4)
+    Xs = torch.zeros(4 * lv.size, dtype=torch.float64, device="cuda")
+    sol.time_march(torch.from_numpy(F).cuda(), Xs)
+    health = lv.step_health(Xs, 4)
+    assert all(m <= 1e-10 for _, m in health)  # pressure projected mean-zero every step
