@@ -81,6 +81,7 @@ make_level3_consts(const Level3Spec &L, const double *dev_verts)
   P.hy = 1.0 / L.ny;
   P.hz = 1.0 / L.nz;
   P.verts = dev_verts;
+  P.gemmE = nullptr;
   return P;
 }
 
@@ -205,6 +206,40 @@ cell3_matrices(const Level3Spec &L, const double X8[8][3])
                 M.b[static_cast<size_t>(l) * 3 * nv + c * nv + b] += wd * psi[l] * gp[3 * b + c];
         }
   return M;
+}
+
+std::vector<double>
+gemm_element_operator(const Level3Spec &L)
+{
+  if (L.r != 1)
+    throw std::invalid_argument("gemm_element_operator: r = 1 only");
+  double X8[8][3];
+  for (int c = 0; c < 8; ++c)
+    {
+      X8[c][0] = (c & 1) * (1.0 / L.nx);
+      X8[c][1] = ((c >> 1) & 1) * (1.0 / L.ny);
+      X8[c][2] = (c >> 2) * (1.0 / L.nz);
+    }
+  const Cell3Matrices M = cell3_matrices(L, X8);
+  const int nv = 27, np = 4, R = 88, K = 168;
+  std::vector<double> E(static_cast<size_t>(R) * K, 0.0);
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < nv; ++i)
+      {
+        double *row = &E[static_cast<size_t>(c * nv + i) * K];
+        for (int j = 0; j < nv; ++j)
+          row[c * nv + j] = M.mass[i * nv + j]; // M UK
+        for (int c2 = 0; c2 < 3; ++c2)
+          for (int j = 0; j < nv; ++j)
+            row[81 + c2 * nv + j] = M.a[(static_cast<size_t>(c) * nv + i) * 3 * nv + c2 * nv + j]; // A UM
+        for (int l = 0; l < np; ++l)
+          row[162 + l] = -M.b[static_cast<size_t>(l) * 3 * nv + c * nv + i]; // -B^T PM
+      }
+  for (int l = 0; l < np; ++l)
+    for (int c2 = 0; c2 < 3; ++c2)
+      for (int j = 0; j < nv; ++j)
+        E[static_cast<size_t>(81 + l) * K + 81 + c2 * nv + j] = M.b[static_cast<size_t>(l) * 3 * nv + c2 * nv + j];
+  return E;
 }
 
 std::vector<double>

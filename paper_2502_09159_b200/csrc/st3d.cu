@@ -25,6 +25,7 @@
 // dofs); cell-owned pressure rows are written directly.
 #include "st3d.hpp"
 
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace stmg_b200
@@ -959,6 +960,188 @@ vmult3l_kernel(const Level3Consts P, const double *__restrict__ x, const double 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Cartesian r = 1 (C3): every cell has the same spatial element operator, so
+// one output slot of one cell is a dense product
+//   [y_v ; y_p] (85) = E (85 x 166) [UK ; UM ; PM]  (UK, UM: 81 nodal values,
+//   PM: 4 modes, temporally combined as in vmult3_kernel).
+// Batched over all (cell, slot) columns it is a GEMM with a shared A = E.
+// vmult3_gemm_kernel keeps E in shared memory (88 x 168 padded, loaded once by
+// a persistent block), gathers 32 columns at a time and runs the product on
+// the FP64 tensor path (mma.m8n8k4); the velocity rows are scattered with
+// red.global.add from the accumulators, the cell-owned pressure rows stored.
+// This trades ~2x more flops than sum factorisation for DMMA issue density.
+// Measured on C3 (B200): 9.95 ms against 8.91 ms for the line kernel; ncu:
+// DMMA pipe 36% active, stalls on the accumulator chains (wait), the gather
+// (long scoreboard) and the tile barriers. Opt-in (STMG_V3_GEMM=1) until the
+// gather overlaps the MMA (double-buffered B, more columns per warp).
+constexpr int kGRows = 88, kGK = 168, kGBP = 36, kGCols = 32, kGThreads = 352; // 11 warps = 11 row tiles
+
+__device__ __forceinline__ void
+dmma3(double (&d)[2], double a, double b)
+{
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+#ifndef STMG_GEMM_MINB
+#define STMG_GEMM_MINB 2
+#endif
+template <int S, int MODE>
+__global__ void __launch_bounds__(kGThreads, STMG_GEMM_MINB)
+vmult3_gemm_kernel(const Level3Consts P, const double *__restrict__ E, const double *__restrict__ x,
+                   const double *__restrict__ b, double *__restrict__ y, const double *__restrict__ xprev0,
+                   int coupled, long long n_cols)
+{
+  extern __shared__ __align__(16) double gsm[];
+  double *Bs = gsm;                        // kGK x kGBP
+  long long *cbase = reinterpret_cast<long long *>(Bs + kGK * kGBP); // [kGCols] node base of the column's cell
+  long long *cpre = cbase + kGCols;        // [kGCols] pressure base (interval + cell)
+  long long *cx_ = cpre + kGCols;          // [kGCols] x of the interval base
+  int *cflag = reinterpret_cast<int *>(cx_ + kGCols); // [kGCols] boundary bits | slot << 8 | valid << 16
+  int *roff = cflag + kGCols;              // [27] local node offset per velocity node
+  double *ck = reinterpret_cast<double *>(roff + 32); // [kGCols][S] K_t(a, b) of the column's slot a
+  double *cm = ck + kGCols * S;                       // [kGCols][S] M_t(a, b)
+  double *clv = cm + kGCols * S;                      // [kGCols] lv(a)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long nsc = P.nsc, mv = P.mv, mp = P.mp, isz = P.isz;
+  const int gx = P.gx, gy = P.gy;
+  // warp w owns row tile w of E: its A-fragments stay in registers
+  double afr[kGK / 4];
+#pragma unroll
+  for (int kk = 0; kk < kGK / 4; ++kk)
+    afr[kk] = __ldg(E + (8 * warp + (lane >> 2)) * kGK + 4 * kk + (lane & 3));
+  for (int i = tid; i < 27; i += kGThreads)
+    roff[i] = ((i / 9) * gy + (i / 3) % 3) * gx + i % 3;
+  const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
+  const long long ntiles = (n_cols + kGCols - 1) / kGCols;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+    {
+      if (tid < kGCols)
+        {
+          const long long j = tile * kGCols + tid;
+          int flag = 0;
+          long long nb = 0, pb = 0, xb = 0;
+          if (j < n_cols)
+            {
+              const long long cg = j / S;
+              const int a = static_cast<int>(j - cg * S);
+              const long long n = cg / ncells, cell = cg - n * ncells;
+              const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
+                        cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
+              nb = (static_cast<long long>(2 * cz) * gy + 2 * cy) * gx + 2 * cx;
+              pb = n * isz + S * mv + cell * 4;
+              xb = n * isz;
+              flag = (cx == 0) | ((cx == P.nx - 1) << 1) | ((cy == 0) << 2) | ((cy == P.ny - 1) << 3) |
+                     ((cz == 0) << 4) | ((cz == P.nz - 1) << 5) | (a << 8) | (1 << 16) | (n > 0 ? (1 << 17) : 0);
+            }
+          cbase[tid] = nb;
+          cpre[tid] = pb;
+          cx_[tid] = xb;
+          cflag[tid] = flag;
+          const int a = (flag >> 8) & 0xff;
+#pragma unroll
+          for (int bs = 0; bs < S; ++bs)
+            {
+              ck[tid * S + bs] = P.Kt[a * S + bs];
+              cm[tid * S + bs] = P.Mt[a * S + bs];
+            }
+          clv[tid] = P.lv[a];
+        }
+      __syncthreads();
+      // ---- gather B (kGK x 32): UK (81), UM (81), PM (4), zero padding
+      for (int e = tid; e < kGK * kGCols; e += kGThreads)
+        {
+          const int kr = e / kGCols, c = e - kr * kGCols;
+          const int flag = cflag[c];
+          double v = 0.0;
+          if ((flag >> 16) & 1 && kr < 166)
+            {
+              const long long xb = cx_[c];
+              if (kr < 162)
+                {
+                  const int q = kr < 81 ? kr : kr - 81;
+                  const int comp = q / 27, i = q - comp * 27;
+                  const int lx = i % 3, ly = (i / 3) % 3, lz = i / 9;
+                  const bool bnd = MODE != 2 && (((flag & 1) && lx == 0) || ((flag & 2) && lx == 2) ||
+                                                 ((flag & 4) && ly == 0) || ((flag & 8) && ly == 2) ||
+                                                 ((flag & 16) && lz == 0) || ((flag & 32) && lz == 2));
+                  const long long node = cbase[c] + roff[i] + comp * nsc;
+                  if (kr < 81)
+                    {
+                      if (!bnd)
+#pragma unroll
+                        for (int bs = 0; bs < S; ++bs)
+                          v = fma(ck[c * S + bs], __ldg(x + xb + bs * mv + node), v);
+                      if (coupled)
+                        {
+                          const double *vp = (flag >> 17) & 1 ? x + xb - isz + (S - 1) * mv : xprev0;
+                          if (vp != nullptr)
+                            v = fma(-clv[c], __ldg(vp + node), v);
+                        }
+                    }
+                  else if (!bnd)
+#pragma unroll
+                    for (int bs = 0; bs < S; ++bs)
+                      v = fma(cm[c * S + bs], __ldg(x + xb + bs * mv + node), v);
+                }
+              else
+                {
+                  const int l = kr - 162;
+#pragma unroll
+                  for (int bs = 0; bs < S; ++bs)
+                    v = fma(cm[c * S + bs], __ldg(x + cpre[c] + bs * mp + l), v);
+                }
+            }
+          Bs[kr * kGBP + c] = v;
+        }
+      __syncthreads();
+      // ---- DMMA: warp w = row tile w, all 4 column tiles
+      {
+        double acc[4][2];
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct)
+          acc[ct][0] = acc[ct][1] = 0.0;
+        const double *bp = Bs + (lane & 3) * kGBP + (lane >> 2);
+#pragma unroll
+        for (int kk = 0; kk < kGK / 4; ++kk)
+#pragma unroll
+          for (int ct = 0; ct < 4; ++ct)
+            dmma3(acc[ct], afr[kk], bp[4 * kk * kGBP + 8 * ct]);
+        const int row = 8 * warp + (lane >> 2);
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            {
+              const int c = 8 * ct + 2 * (lane & 3) + h;
+              const int flag = cflag[c];
+              if (!((flag >> 16) & 1) || row >= 85)
+                continue;
+              const double val = acc[ct][h];
+              const int a = (flag >> 8) & 0xff;
+              if (row < 81)
+                {
+                  const int comp = row / 27, i = row - comp * 27;
+                  const int lx = i % 3, ly = (i / 3) % 3, lz = i / 9;
+                  const bool bnd = MODE != 2 && (((flag & 1) && lx == 0) || ((flag & 2) && lx == 2) ||
+                                                 ((flag & 4) && ly == 0) || ((flag & 8) && ly == 2) ||
+                                                 ((flag & 16) && lz == 0) || ((flag & 32) && lz == 2));
+                  if (!bnd)
+                    atomicAdd(y + cx_[c] + a * mv + comp * nsc + cbase[c] + roff[i], MODE == 1 ? -val : val);
+                }
+              else
+                {
+                  const long long o = cpre[c] + a * mp + (row - 81);
+                  y[o] = MODE == 1 ? __ldg(b + o) - val : val;
+                }
+            }
+      }
+      __syncthreads();
+    }
+}
 /// y's velocity rows before the scatter: 0 (plain / raw), b (residual); the
 /// constrained rows get the identity x (plain) or b - x (residual),
 /// st_operator.cpp:383-394.
@@ -1012,6 +1195,26 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<grid, block, smem, st>>>(P, x, b, y, xprev0, coupled, cells);
   };
+  if constexpr (R == 1)
+    if (P.gemmE != nullptr && std::getenv("STMG_V3_GEMM") != nullptr) // opt-in: measured slower
+      {
+        const long long ncols = cells * S;
+        const size_t smem = sizeof(double) * (kGK * kGBP) + sizeof(long long) * 3 * kGCols +
+                            sizeof(int) * (kGCols + 32) + sizeof(double) * (2 * S + 1) * kGCols;
+        const unsigned grid = static_cast<unsigned>(std::min<long long>(2 * 148, (ncols + kGCols - 1) / kGCols));
+        auto gg = [&](auto init, auto kern) {
+          init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+          kern<<<grid, kGThreads, smem, st>>>(P, P.gemmE, x, b, y, xprev0, coupled, ncols);
+        };
+        switch (mode)
+          {
+            case 0: gg(vmult3_init_kernel<0>, vmult3_gemm_kernel<S, 0>); break;
+            case 1: gg(vmult3_init_kernel<1>, vmult3_gemm_kernel<S, 1>); break;
+            default: gg(vmult3_init_kernel<2>, vmult3_gemm_kernel<S, 2>); break;
+          }
+        return cudaGetLastError();
+      }
   if constexpr (R == 1)
     {
       using C = V3L<R>;

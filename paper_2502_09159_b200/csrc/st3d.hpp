@@ -40,6 +40,7 @@ struct Level3Consts
   double Kt[kMaxS * kMaxS], Mt[kMaxS * kMaxS], lv[kMaxS];
   double nu, gamma, hx, hy, hz;
   const double *verts; // nullptr: Cartesian unit-cube mesh
+  const double *gemmE; // Cartesian r = 1: dense element operator (88 x 168), vmult3_gemm_kernel; else nullptr
 };
 
 struct Level3Spec
@@ -79,6 +80,9 @@ struct Cell3Matrices
   std::vector<double> pmean; // np: int psi_l
 };
 Cell3Matrices cell3_matrices(const Level3Spec &L, const double X8[8][3]);
+/// Dense spatial element operator of a Cartesian r = 1 cell for vmult3_gemm_kernel:
+/// rows [y_v (3 x 27) ; y_p (4)], columns [UK (81) ; UM (81) ; PM (4)], padded to 88 x 168.
+std::vector<double> gemm_element_operator(const Level3Spec &L);
 void cell_vertices(const Level3Spec &L, const std::vector<double> &verts, int cx, int cy, int cz, double X8[8][3]);
 
 /// Cell-Vanka patch set of a 3D level: classes (Cartesian: by boundary

@@ -53,7 +53,7 @@ struct stmg3_level
   DevGeom3 geom{};
   bool deformed = false;
   std::vector<double> verts_h;
-  DevArray<double> verts, pmean, one_w;
+  DevArray<double> verts, pmean, one_w, gemmE;
   double inv_vol = 1.0;
   int smoother_kind = STMG_SMOOTHER_NONE;
   // Vanka: classes, colour batches (8 parity colours), anchors
@@ -164,6 +164,11 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
       L.verts.upload(L.verts_h);
     }
   L.consts = make_level3_consts(s, L.deformed ? L.verts.p : nullptr);
+  if (!L.deformed && s.r == 1) // one element operator for every cell: DMMA GEMM kernel
+    {
+      L.gemmE.upload(gemm_element_operator(s));
+      L.consts.gemmE = L.gemmE.p;
+    }
   L.geom = geom3(s);
   double vol = 1.0;
   L.pmean.upload(pressure_mean3(s, L.deformed ? &L.verts_h : nullptr, &vol));
