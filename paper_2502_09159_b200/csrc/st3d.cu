@@ -976,7 +976,7 @@ vmult3l_kernel(const Level3Consts P, const double *__restrict__ x, const double 
 // DMMA pipe 36% active, stalls on the accumulator chains (wait), the gather
 // (long scoreboard) and the tile barriers. Opt-in (STMG_V3_GEMM=1) until the
 // gather overlaps the MMA (double-buffered B, more columns per warp).
-constexpr int kGRows = 88, kGK = 168, kGBP = 36, kGCols = 32, kGThreads = 352; // 11 warps = 11 row tiles
+constexpr int kGK = 168, kGBP = 36, kGCols = 32, kGThreads = 352; // 11 warps = 11 row tiles
 
 __device__ __forceinline__ void
 dmma3(double (&d)[2], double a, double b)
@@ -1283,171 +1283,167 @@ project3_kernel(DevGeom3 G, const double *__restrict__ pmean, double inv_vol, do
     pr[c * G.np] -= mean;
 }
 
-__global__ void
-prolongate3_kernel(DevTransfer3 T, const double *__restrict__ coarse, double *__restrict__ fine, long long total)
+// Transfers: velocity rows on a (X-block, Y*Z, interval*slot*component)
+// grid and pressure rows on a (cell-mode block, interval*slot) grid, so the
+// index math is 32-bit and per block instead of 64-bit divisions per element.
+constexpr int kTrX = 64;
+
+__global__ void __launch_bounds__(kTrX)
+prolongate3_vel_kernel(DevTransfer3 T, const double *__restrict__ coarse, double *__restrict__ fine)
 {
   const DevGeom3 &F = T.f, &Cg = T.c;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x)
+  const int X = blockIdx.x * kTrX + threadIdx.x;
+  if (X >= F.gx)
+    return;
+  const int Y = blockIdx.y % F.gy, Z = blockIdx.y / F.gy;
+  const int q = blockIdx.z; // (n * S_f + a) * 3 + comp
+  const int comp = q % 3, a = (q / 3) % F.S, n = q / (3 * F.S);
+  const int m = T.h_time ? n / 2 : n, half = T.h_time ? (n & 1) : 0;
+  const double *E = T.E + half * kMaxS * kMaxS + a * kMaxS;
+  const long long s = (static_cast<long long>(Z) * F.gy + Y) * F.gx + X;
+  double v = 0.0;
+  for (int bs = 0; bs < Cg.S; ++bs)
     {
-      const int n = static_cast<int>(idx / F.isz);
-      const long long rem = idx - n * F.isz;
-      const int m = T.h_time ? n / 2 : n, half = T.h_time ? (n & 1) : 0;
-      const double *cb = coarse + m * Cg.isz;
-      const double *E = T.E + half * kMaxS * kMaxS;
-      double v = 0.0;
-      if (rem < F.S * F.mv)
+      const double *cv = coarse + m * Cg.isz + bs * Cg.mv + comp * Cg.nsc;
+      double sv;
+      if (T.spatial)
         {
-          const int a = static_cast<int>(rem / F.mv);
-          const long long r2 = rem - a * F.mv;
-          const int comp = static_cast<int>(r2 / F.nsc);
-          const long long s = r2 - comp * F.nsc;
-          const int X = static_cast<int>(s % F.gx), Y = static_cast<int>((s / F.gx) % F.gy),
-                    Z = static_cast<int>(s / (static_cast<long long>(F.gx) * F.gy));
-          for (int bs = 0; bs < Cg.S; ++bs)
-            {
-              const double e = E[a * kMaxS + bs];
-              const double *cv = cb + bs * Cg.mv + comp * Cg.nsc;
-              double sv;
-              if (T.spatial)
-                {
-                  sv = 0.0;
-                  for (int kz = T.pz.ptr[Z]; kz < T.pz.ptr[Z + 1]; ++kz)
-                    for (int ky = T.py.ptr[Y]; ky < T.py.ptr[Y + 1]; ++ky)
-                      {
-                        const double wyz = T.pz.val[kz] * T.py.val[ky];
-                        const long long rowc = (static_cast<long long>(T.pz.col[kz]) * Cg.gy + T.py.col[ky]) * Cg.gx;
-                        for (int kx = T.px.ptr[X]; kx < T.px.ptr[X + 1]; ++kx)
-                          sv = fma(wyz * T.px.val[kx], cv[rowc + T.px.col[kx]], sv);
-                      }
-                }
-              else
-                sv = cv[s];
-              v = fma(e, sv, v);
-            }
+          sv = 0.0;
+          for (int kz = T.pz.ptr[Z]; kz < T.pz.ptr[Z + 1]; ++kz)
+            for (int ky = T.py.ptr[Y]; ky < T.py.ptr[Y + 1]; ++ky)
+              {
+                const double wyz = T.pz.val[kz] * T.py.val[ky];
+                const double *row = cv + (static_cast<long long>(T.pz.col[kz]) * Cg.gy + T.py.col[ky]) * Cg.gx;
+                for (int kx = T.px.ptr[X]; kx < T.px.ptr[X + 1]; ++kx)
+                  sv = fma(wyz * T.px.val[kx], __ldg(row + T.px.col[kx]), sv);
+              }
         }
       else
-        {
-          const long long r2 = rem - F.S * F.mv;
-          const int a = static_cast<int>(r2 / F.mp);
-          const long long r3 = r2 - a * F.mp;
-          const long long cell = r3 / F.np;
-          const int mf = static_cast<int>(r3 - cell * F.np);
-          long long ccell = cell;
-          int ch = 0;
-          if (T.pmode == 1)
-            {
-              const int fx = static_cast<int>(cell % F.nx), fy = static_cast<int>((cell / F.nx) % F.ny),
-                        fz = static_cast<int>(cell / (static_cast<long long>(F.nx) * F.ny));
-              ch = (fz & 1) * 4 + (fy & 1) * 2 + (fx & 1);
-              ccell = (static_cast<long long>(fz >> 1) * Cg.ny + (fy >> 1)) * Cg.nx + (fx >> 1);
-            }
-          for (int bs = 0; bs < Cg.S; ++bs)
-            {
-              const double e = E[a * kMaxS + bs];
-              const double *cp = cb + Cg.S * Cg.mv + bs * Cg.mp + ccell * Cg.np;
-              double sv = 0.0;
-              if (T.spatial)
-                {
-                  const double *blk = T.child + (static_cast<long long>(ch) * F.np + mf) * Cg.np;
-                  for (int l = 0; l < Cg.np; ++l)
-                    sv = fma(blk[l], cp[l], sv);
-                }
-              else
-                sv = cp[mf];
-              v = fma(e, sv, v);
-            }
-        }
-      fine[idx] = v;
+        sv = __ldg(cv + s);
+      v = fma(E[bs], sv, v);
     }
+  fine[n * F.isz + a * F.mv + comp * F.nsc + s] = v;
 }
 
 __global__ void
-restrict3_kernel(DevTransfer3 T, const double *__restrict__ fine, double *__restrict__ coarse, long long total)
+prolongate3_pre_kernel(DevTransfer3 T, const double *__restrict__ coarse, double *__restrict__ fine)
 {
   const DevGeom3 &F = T.f, &Cg = T.c;
-  const int nh = T.h_time ? 2 : 1;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x)
+  const int e = blockIdx.x * blockDim.x + threadIdx.x; // cell * np + mode
+  const int ncm = F.nx * F.ny * F.nz * F.np;
+  if (e >= ncm)
+    return;
+  const int q = blockIdx.y; // n * S_f + a
+  const int a = q % F.S, n = q / F.S;
+  const int m = T.h_time ? n / 2 : n, half = T.h_time ? (n & 1) : 0;
+  const double *E = T.E + half * kMaxS * kMaxS + a * kMaxS;
+  const int cell = e / F.np, mf = e - cell * F.np;
+  int ccell = cell, ch = 0;
+  if (T.pmode == 1)
     {
-      const int m = static_cast<int>(idx / Cg.isz);
-      const long long rem = idx - m * Cg.isz;
-      double v = 0.0;
-      if (rem < Cg.S * Cg.mv)
+      const int fx = cell % F.nx, fy = (cell / F.nx) % F.ny, fz = cell / (F.nx * F.ny);
+      ch = (fz & 1) * 4 + (fy & 1) * 2 + (fx & 1);
+      ccell = ((fz >> 1) * Cg.ny + (fy >> 1)) * Cg.nx + (fx >> 1);
+    }
+  double v = 0.0;
+  for (int bs = 0; bs < Cg.S; ++bs)
+    {
+      const double *cp = coarse + m * Cg.isz + Cg.S * Cg.mv + bs * Cg.mp + static_cast<long long>(ccell) * Cg.np;
+      double sv = 0.0;
+      if (T.spatial)
         {
-          const int bs = static_cast<int>(rem / Cg.mv);
-          const long long r2 = rem - bs * Cg.mv;
-          const int comp = static_cast<int>(r2 / Cg.nsc);
-          const long long s = r2 - comp * Cg.nsc;
-          const int X = static_cast<int>(s % Cg.gx), Y = static_cast<int>((s / Cg.gx) % Cg.gy),
-                    Z = static_cast<int>(s / (static_cast<long long>(Cg.gx) * Cg.gy));
-          for (int h = 0; h < nh; ++h)
-            {
-              const int n = T.h_time ? 2 * m + h : m;
-              const double *E = T.E + h * kMaxS * kMaxS;
-              for (int a = 0; a < F.S; ++a)
-                {
-                  const double e = E[a * kMaxS + bs];
-                  const double *fv = fine + n * F.isz + a * F.mv + comp * F.nsc;
-                  double sv;
-                  if (T.spatial)
-                    {
-                      sv = 0.0;
-                      for (int kz = T.rz.ptr[Z]; kz < T.rz.ptr[Z + 1]; ++kz)
-                        for (int ky = T.ry.ptr[Y]; ky < T.ry.ptr[Y + 1]; ++ky)
-                          {
-                            const double wyz = T.rz.val[kz] * T.ry.val[ky];
-                            const long long rowf = (static_cast<long long>(T.rz.col[kz]) * F.gy + T.ry.col[ky]) * F.gx;
-                            for (int kx = T.rx.ptr[X]; kx < T.rx.ptr[X + 1]; ++kx)
-                              sv = fma(wyz * T.rx.val[kx], fv[rowf + T.rx.col[kx]], sv);
-                          }
-                    }
-                  else
-                    sv = fv[s];
-                  v = fma(e, sv, v);
-                }
-            }
+          const double *blk = T.child + (ch * F.np + mf) * Cg.np;
+          for (int l = 0; l < Cg.np; ++l)
+            sv = fma(blk[l], cp[l], sv);
         }
       else
-        {
-          const long long r2 = rem - Cg.S * Cg.mv;
-          const int bs = static_cast<int>(r2 / Cg.mp);
-          const long long r3 = r2 - bs * Cg.mp;
-          const long long ccell = r3 / Cg.np;
-          const int l = static_cast<int>(r3 - ccell * Cg.np);
-          const int ccx = static_cast<int>(ccell % Cg.nx), ccy = static_cast<int>((ccell / Cg.nx) % Cg.ny),
-                    ccz = static_cast<int>(ccell / (static_cast<long long>(Cg.nx) * Cg.ny));
-          const int nch = T.pmode == 1 ? 8 : 1;
-          for (int h = 0; h < nh; ++h)
-            {
-              const int n = T.h_time ? 2 * m + h : m;
-              const double *E = T.E + h * kMaxS * kMaxS;
-              for (int a = 0; a < F.S; ++a)
-                {
-                  const double e = E[a * kMaxS + bs];
-                  double sv = 0.0;
-                  for (int ch = 0; ch < nch; ++ch)
-                    {
-                      long long fcell = ccell;
-                      if (T.pmode == 1)
-                        fcell = (static_cast<long long>(2 * ccz + (ch >> 2)) * F.ny + 2 * ccy + ((ch >> 1) & 1)) * F.nx +
-                                2 * ccx + (ch & 1);
-                      const double *fp = fine + n * F.isz + F.S * F.mv + a * F.mp + fcell * F.np;
-                      if (T.spatial)
-                        {
-                          const double *blk = T.child + static_cast<long long>(ch) * F.np * Cg.np;
-                          for (int mf = 0; mf < F.np; ++mf)
-                            sv = fma(blk[mf * Cg.np + l], fp[mf], sv);
-                        }
-                      else
-                        sv += fp[l];
-                    }
-                  v = fma(e, sv, v);
-                }
-            }
-        }
-      coarse[idx] = v;
+        sv = cp[mf];
+      v = fma(E[bs], sv, v);
     }
+  fine[n * F.isz + F.S * F.mv + a * F.mp + e] = v;
+}
+
+__global__ void __launch_bounds__(kTrX)
+restrict3_vel_kernel(DevTransfer3 T, const double *__restrict__ fine, double *__restrict__ coarse)
+{
+  const DevGeom3 &F = T.f, &Cg = T.c;
+  const int X = blockIdx.x * kTrX + threadIdx.x;
+  if (X >= Cg.gx)
+    return;
+  const int Y = blockIdx.y % Cg.gy, Z = blockIdx.y / Cg.gy;
+  const int q = blockIdx.z; // (m * S_c + b) * 3 + comp
+  const int comp = q % 3, bs = (q / 3) % Cg.S, m = q / (3 * Cg.S);
+  const long long s = (static_cast<long long>(Z) * Cg.gy + Y) * Cg.gx + X;
+  const int nh = T.h_time ? 2 : 1;
+  double v = 0.0;
+  for (int h = 0; h < nh; ++h)
+    {
+      const int n = T.h_time ? 2 * m + h : m;
+      const double *E = T.E + h * kMaxS * kMaxS;
+      for (int a = 0; a < F.S; ++a)
+        {
+          const double *fv = fine + n * F.isz + a * F.mv + comp * F.nsc;
+          double sv;
+          if (T.spatial)
+            {
+              sv = 0.0;
+              for (int kz = T.rz.ptr[Z]; kz < T.rz.ptr[Z + 1]; ++kz)
+                for (int ky = T.ry.ptr[Y]; ky < T.ry.ptr[Y + 1]; ++ky)
+                  {
+                    const double wyz = T.rz.val[kz] * T.ry.val[ky];
+                    const double *row = fv + (static_cast<long long>(T.rz.col[kz]) * F.gy + T.ry.col[ky]) * F.gx;
+                    for (int kx = T.rx.ptr[X]; kx < T.rx.ptr[X + 1]; ++kx)
+                      sv = fma(wyz * T.rx.val[kx], __ldg(row + T.rx.col[kx]), sv);
+                  }
+            }
+          else
+            sv = __ldg(fv + s);
+          v = fma(E[a * kMaxS + bs], sv, v);
+        }
+    }
+  coarse[m * Cg.isz + bs * Cg.mv + comp * Cg.nsc + s] = v;
+}
+
+__global__ void
+restrict3_pre_kernel(DevTransfer3 T, const double *__restrict__ fine, double *__restrict__ coarse)
+{
+  const DevGeom3 &F = T.f, &Cg = T.c;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x; // coarse cell * np + mode
+  const int ncm = Cg.nx * Cg.ny * Cg.nz * Cg.np;
+  if (e >= ncm)
+    return;
+  const int q = blockIdx.y; // m * S_c + b
+  const int bs = q % Cg.S, m = q / Cg.S;
+  const int ccell = e / Cg.np, l = e - ccell * Cg.np;
+  const int ccx = ccell % Cg.nx, ccy = (ccell / Cg.nx) % Cg.ny, ccz = ccell / (Cg.nx * Cg.ny);
+  const int nch = T.pmode == 1 ? 8 : 1, nh = T.h_time ? 2 : 1;
+  double v = 0.0;
+  for (int h = 0; h < nh; ++h)
+    {
+      const int n = T.h_time ? 2 * m + h : m;
+      const double *E = T.E + h * kMaxS * kMaxS;
+      for (int a = 0; a < F.S; ++a)
+        {
+          double sv = 0.0;
+          for (int ch = 0; ch < nch; ++ch)
+            {
+              int fcell = ccell;
+              if (T.pmode == 1)
+                fcell = ((2 * ccz + (ch >> 2)) * F.ny + 2 * ccy + ((ch >> 1) & 1)) * F.nx + 2 * ccx + (ch & 1);
+              const double *fp = fine + n * F.isz + F.S * F.mv + a * F.mp + static_cast<long long>(fcell) * F.np;
+              if (T.spatial)
+                {
+                  const double *blk = T.child + ch * F.np * Cg.np;
+                  for (int mf = 0; mf < F.np; ++mf)
+                    sv = fma(blk[mf * Cg.np + l], fp[mf], sv);
+                }
+              else
+                sv += fp[l];
+            }
+          v = fma(E[a * kMaxS + bs], sv, v);
+        }
+    }
+  coarse[m * Cg.isz + Cg.S * Cg.mv + bs * Cg.mp + e] = v;
 }
 
 int
@@ -1505,20 +1501,29 @@ launch_project3(const DevGeom3 &G, const double *pmean, double inv_vol, double *
 cudaError_t
 launch_prolongate3(const DevTransfer3 &T, const double *coarse, double *fine, int nc, cudaStream_t st)
 {
-  const long long total = static_cast<long long>(T.h_time ? 2 * nc : nc) * T.f.isz;
-  if (total == 0)
+  const int nf = T.h_time ? 2 * nc : nc;
+  if (nf == 0)
     return cudaSuccess;
-  prolongate3_kernel<<<grid_for(total), 256, 0, st>>>(T, coarse, fine, total);
+  const DevGeom3 &F = T.f;
+  dim3 gv((F.gx + kTrX - 1) / kTrX, F.gy * F.gz, nf * F.S * 3);
+  prolongate3_vel_kernel<<<gv, kTrX, 0, st>>>(T, coarse, fine);
+  const int ncm = F.nx * F.ny * F.nz * F.np;
+  dim3 gp((ncm + 255) / 256, nf * F.S);
+  prolongate3_pre_kernel<<<gp, 256, 0, st>>>(T, coarse, fine);
   return cudaGetLastError();
 }
 
 cudaError_t
 launch_restrict3(const DevTransfer3 &T, const double *fine, double *coarse, int nc, cudaStream_t st)
 {
-  const long long total = static_cast<long long>(nc) * T.c.isz;
-  if (total == 0)
+  if (nc == 0)
     return cudaSuccess;
-  restrict3_kernel<<<grid_for(total), 256, 0, st>>>(T, fine, coarse, total);
+  const DevGeom3 &C = T.c;
+  dim3 gv((C.gx + kTrX - 1) / kTrX, C.gy * C.gz, nc * C.S * 3);
+  restrict3_vel_kernel<<<gv, kTrX, 0, st>>>(T, fine, coarse);
+  const int ncm = C.nx * C.ny * C.nz * C.np;
+  dim3 gp((ncm + 255) / 256, nc * C.S);
+  restrict3_pre_kernel<<<gp, 256, 0, st>>>(T, fine, coarse);
   return cudaGetLastError();
 }
 

@@ -348,7 +348,7 @@ struct stmg3_solver
     Solver3Level &F = *levels[l];
     stmg3_level &C = *levels[l - 1]->level;
     check(launch_restrict3(F.dt, fine_v, coarse_v, nc, ctx->stream), "restrict3");
-    ctx->count();
+    ctx->count(2);
     C.zero_constrained(coarse_v, nc);
     if (project)
       C.project_residual(coarse_v, nc);
@@ -364,7 +364,7 @@ struct stmg3_solver
     const long long n = L.spec.isz() * nf;
     F.t.resize(n);
     check(launch_prolongate3(F.dt, coarse_v, F.t.p, nc, ctx->stream), "prolongate3");
-    ctx->count();
+    ctx->count(2);
     L.zero_constrained(F.t.p, nf);
     if (project)
       L.project(F.t.p, nf);
