@@ -76,6 +76,20 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("link of libstmg_b200.so failed")
+    # the drop-in command line (tools/stmg_cli.cpp: the reference's `stmg` flags on the GPU library)
+    cli = BUILD / "stmg_gpu"
+    src = ROOT / "tools" / "stmg_cli.cpp"
+    if src.exists() and (force or not cli.exists() or cli.stat().st_mtime < max(src.stat().st_mtime,
+                                                                              LIB.stat().st_mtime)):
+        cuda_home = Path(_nvcc()).resolve().parents[1]
+        gxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else "g++"
+        cmd = [gxx, "-O2", "-std=c++17", "-I", str(ROOT / "include"), "-I", str(cuda_home / "include"), str(src),
+               "-o", str(cli), "-L", str(BUILD), "-lstmg_b200", "-L", str(cuda_home / "lib64"), "-lcudart",
+               f"-Wl,-rpath,$ORIGIN:{cuda_home / 'lib64'}"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("build of the stmg_gpu command line failed")
     return LIB
 
 
