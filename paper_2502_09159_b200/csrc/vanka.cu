@@ -381,25 +381,40 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
         for (int ct = 0; ct < kBCols / 8; ++ct)
           acc[t][ct][0] = acc[t][ct][1] = 0.0;
       const double *bbase = Rs + (lane & 3) * kBLd + (lane >> 2);
-      for (int kk = 0; kk < ks; ++kk)
+      // A-fragments come from L2: a 3-deep register ring keeps the loads two
+      // k-steps ahead of the DMMAs that consume them
+      auto load_a = [&](int kk, double (&dst)[TPW]) {
+        const int col = 4 * kk + (lane & 3);
+#pragma unroll
+        for (int t = 0; t < TPW; ++t)
+          {
+            const int row = 8 * (warp + 16 * t) + (lane >> 2);
+            dst[t] = (kk < ks && row < nt && col < nt) ? __ldg(pc.inverse + static_cast<long long>(row) * nt + col)
+                                                       : 0.0;
+          }
+      };
+      double ring[3][TPW];
+      load_a(0, ring[0]);
+      load_a(1, ring[1]);
+      for (int kk0 = 0; kk0 < ks; kk0 += 3)
         {
-          double bf[kBCols / 8];
 #pragma unroll
-          for (int ct = 0; ct < kBCols / 8; ++ct)
-            bf[ct] = bbase[4 * kk * kBLd + 8 * ct];
-          const int col = 4 * kk + (lane & 3);
-#pragma unroll
-          for (int t = 0; t < TPW; ++t)
+          for (int u = 0; u < 3; ++u)
             {
-              const int rt = warp + 16 * t;
-              if (rt < rtiles)
+              const int kk = kk0 + u;
+              load_a(kk + 2, ring[(u + 2) % 3]);
+              if (kk < ks)
                 {
-                  const int row = 8 * rt + (lane >> 2);
-                  const double a = (row < nt && col < nt) ? __ldg(pc.inverse + static_cast<long long>(row) * nt + col)
-                                                          : 0.0;
+                  double bf[kBCols / 8];
 #pragma unroll
                   for (int ct = 0; ct < kBCols / 8; ++ct)
-                    dmma_8x8x4(acc[t][ct], a, bf[ct]);
+                    bf[ct] = bbase[4 * kk * kBLd + 8 * ct];
+#pragma unroll
+                  for (int t = 0; t < TPW; ++t)
+                    if (warp + 16 * t < rtiles)
+#pragma unroll
+                      for (int ct = 0; ct < kBCols / 8; ++ct)
+                        dmma_8x8x4(acc[t][ct], ring[u][t], bf[ct]);
                 }
             }
         }
