@@ -324,13 +324,16 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
 // scattered straight from the accumulators (patches of one launch share no
 // dof, so the adds never collide).
 constexpr int kBThreads = 512; // 16 warps
-constexpr int kBCols = 32;     // columns per tile
+#ifndef STMG_BIG_COLS
+#define STMG_BIG_COLS 32
+#endif
+constexpr int kBCols = STMG_BIG_COLS; // columns per tile
 constexpr int kBLd = 36;       // R pitch: conflict-free B-fragment loads
 constexpr int kBMaxTiles = 7;  // row tiles per warp: 16 * 7 * 8 = 896 rows
 constexpr int kBGroup = 16;    // intervals per block
 
 template <int TPW>
-__global__ void __launch_bounds__(kBThreads, 1)
+__global__ void __launch_bounds__(kBThreads, kBCols == 32 ? 1 : 2)
 vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
                  const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
                  const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals, double omega)
