@@ -144,22 +144,30 @@ dmma_8x8x4(double (&d)[2], double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int KS, int ROWS = kDRows, int TPW = 1, int COLS = kDCols>
-__global__ void __launch_bounds__(ROWS / 8 / TPW * 32, 1)
+#ifndef STMG_SPLIT_MINB
+#define STMG_SPLIT_MINB 1
+#endif
+template <int KS, int ROWS = kDRows, int TPW = 1, int COLS = kDCols, int SPLIT = 1>
+__global__ void __launch_bounds__(ROWS / SPLIT / 8 / TPW * 32, SPLIT == 1 ? 1 : STMG_SPLIT_MINB)
 vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ items,
                   const int *__restrict__ item_ptr, const long long *__restrict__ vel_anchor,
                   const long long *__restrict__ pre_anchor, const double *__restrict__ r, double *__restrict__ u,
                   long long isz, int n_intervals, double omega)
 {
-  // ROWS rows of the patch matrix; warp w owns the TPW 8-row tiles w + j * NW
+  // ROWS rows of the patch matrix, split over SPLIT CTAs (blockIdx.z): a CTA
+  // computes and scatters OROWS rows but gathers all ROWS rows of R (the
+  // contraction dimension); warp w owns the TPW 8-row tiles w + j * NW
   constexpr int kDCols = COLS;
-  constexpr int kDRows = ROWS, kDThreads = ROWS / 8 / TPW * 32, kDPer = kDRows * kDCols / kDThreads;
+  constexpr int OROWS = ROWS / SPLIT;
+  constexpr int kDRows = ROWS, kDThreads = OROWS / 8 / TPW * 32, kDPer = kDRows * kDCols / kDThreads;
+  constexpr int kDPerS = OROWS * kDCols / kDThreads;
   constexpr int NW = kDThreads / 32;
+  const int row0 = SPLIT > 1 ? static_cast<int>(blockIdx.z) * OROWS : 0;
   extern __shared__ __align__(16) double dsm[];
   double *Rs = dsm;                                                 // kDRows x kDRLd
-  double *Zs = Rs + kDRows * kDRLd;                                 // kDRows x kDZLd
-  double *w_s = Zs + kDRows * kDZLd;                                // kDRows
-  long long *cb = reinterpret_cast<long long *>(w_s + kDRows);     // [3][2][kDCols] column bases
+  double *Zs = Rs + kDRows * kDRLd;                                 // OROWS x kDZLd
+  double *w_s = Zs + OROWS * kDZLd;                                 // OROWS
+  long long *cb = reinterpret_cast<long long *>(w_s + OROWS);      // [3][2][kDCols] column bases
 
   const int n0 = blockIdx.y * kDGroup;
   const int ng = min(kDGroup, n_intervals - n0);
@@ -171,8 +179,8 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
 
   int loaded = -1, nt = 0, nvel = 0;
   double afr[TPW][KS];
-  long long relq[kDPer];
-  bool velq[kDPer], validq[kDPer];
+  long long relq[kDPer], relS[kDPerS];
+  bool velq[kDPer], validq[kDPer], velS[kDPerS], validS[kDPerS];
 
   // Items run in order; consecutive items of one block are separated by
   // block barriers (every tile ends with one), which is what makes the
@@ -185,12 +193,12 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           const DevPatchClass pc = classes[bt.cls];
           nt = pc.n_t;
           nvel = pc.n_vel;
-          for (int i = tid; i < kDRows; i += kDThreads)
-            w_s[i] = i < nt ? omega * pc.weight[i] : 0.0;
+          for (int i = tid; i < OROWS; i += kDThreads)
+            w_s[i] = row0 + i < nt ? omega * pc.weight[row0 + i] : 0.0;
 #pragma unroll
           for (int tw = 0; tw < TPW; ++tw)
             {
-              const int arow = 8 * (warp + tw * NW) + (lane >> 2);
+              const int arow = row0 + 8 * (warp + tw * NW) + (lane >> 2);
 #pragma unroll
               for (int kk = 0; kk < KS; ++kk)
                 {
@@ -205,6 +213,14 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
               validq[q] = i < nt;
               velq[q] = i < nvel;
               relq[q] = i < nt ? pc.rel[i] : 0;
+            }
+#pragma unroll
+          for (int q = 0; q < kDPerS; ++q)
+            {
+              const int i = row0 + ibase + q * (kDThreads / kDCols);
+              validS[q] = i < nt;
+              velS[q] = i < nvel;
+              relS[q] = i < nt ? pc.rel[i] : 0;
             }
           loaded = bt.cls;
         }
@@ -251,12 +267,12 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           const long long *cbt = cb + (t % 3) * 2 * kDCols;
           const long long vb = cbt[c], pb = cbt[kDCols + c];
           // prefetch: old u of this tile and the residual of the next tile
-          double uo[kDPer];
+          double uo[kDPerS];
 #pragma unroll
-          for (int q = 0; q < kDPer; ++q)
+          for (int q = 0; q < kDPerS; ++q)
             {
-              const long long base = velq[q] ? vb : pb;
-              uo[q] = (validq[q] && base != kNoCol) ? u[base + relq[q]] : 0.0;
+              const long long base = velS[q] ? vb : pb;
+              uo[q] = (validS[q] && base != kNoCol) ? u[base + relS[q]] : 0.0;
             }
           if (t + 1 < ntiles)
             {
@@ -272,7 +288,7 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           // Z = A^{-1} R on the FP64 tensor path
 #pragma unroll
           for (int tw = 0; tw < TPW; ++tw)
-            if (8 * (warp + tw * NW) < nt)
+            if (row0 + 8 * (warp + tw * NW) < nt)
               {
                 double acc[kDCols / 8][2];
 #pragma unroll
@@ -300,11 +316,11 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           column_bases(t + 2);
           __syncthreads();
 #pragma unroll
-          for (int q = 0; q < kDPer; ++q)
+          for (int q = 0; q < kDPerS; ++q)
             {
-              const long long base = velq[q] ? vb : pb;
-              if (validq[q] && base != kNoCol)
-                u[base + relq[q]] = uo[q] + Zs[(ibase + q * (kDThreads / kDCols)) * kDZLd + c];
+              const long long base = velS[q] ? vb : pb;
+              if (validS[q] && base != kNoCol)
+                u[base + relS[q]] = uo[q] + Zs[(ibase + q * (kDThreads / kDCols)) * kDZLd + c];
             }
           if (t + 1 < ntiles)
 #pragma unroll
@@ -460,8 +476,9 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
     {
       // 128 rows (16 warps) for 2D patches; 176 rows (22 warps) for 3D Q2 cells (n_T = 170)
       const int rows = max_nt <= kDRows ? kDRows : 176;
-      const size_t dsmem = sizeof(double) * (rows * kDRLd + rows * kDZLd + rows) + sizeof(long long) * 6 * kDCols;
-      dim3 grid(n_batches, (n_intervals + kDGroup - 1) / kDGroup);
+      const int split = rows == 176 ? 2 : 1, orows = rows / split;
+      const size_t dsmem = sizeof(double) * (rows * kDRLd + orows * kDZLd + orows) + sizeof(long long) * 6 * kDCols;
+      dim3 grid(n_batches, (n_intervals + kDGroup - 1) / kDGroup, split);
       const int ks = (max_nt + 3) / 4;
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
@@ -469,7 +486,7 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
           classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega);
       };
       if (rows == 176)
-        go(vanka_dmma_kernel<44, 176, 2, STMG_VANKA176_COLS>);
+        go(vanka_dmma_kernel<44, 176, 1, 16, 2>); // 2 CTAs x 88 rows, one 8-row tile per warp
       else if (ks <= 8)
         go(vanka_dmma_kernel<8>);
       else if (ks <= 12)
