@@ -33,24 +33,29 @@ namespace stmg_b200
 
 namespace
 {
-template <int R>
+template <int R, int MAP = 0>
 struct V3
 {
   static constexpr int N = R + 2, NN = N * N, NNN = N * N * N, p = R + 1;
   static constexpr int NP = (R + 1) * (R + 2) * (R + 3) / 6;
-  // lane = cell: a warp works one line of CW cells (r = 1: 32 cells, one
-  // line per warp; r = 2: 16 cells, two lines per warp), so a warp's shared
-  // accesses hit CW different cells at the same offset (odd cell stride:
-  // conflict-free) and its global gathers walk consecutive cells along x.
+  // MAP 0, lane = cell: a warp works one line of CW cells (two lines per
+  // warp), so a warp's shared accesses hit CW different cells at the same
+  // offset (odd cell stride: conflict-free) and its global gathers walk
+  // consecutive cells along x. MAP 1, line = thread: N*N consecutive threads
+  // work the lines of one cell (fewer registers per resident cell; used at
+  // r = 1, where more cells in flight beat conflict-free banks).
   static constexpr int CW = 16;
   static constexpr int LPW = 32 / CW;
   static constexpr int NWARP = (NN + LPW - 1) / LPW;
-  static constexpr int THREADS = 32 * NWARP;
+  static constexpr int THREADS = MAP == 0 ? 32 * NWARP : NN * CW;
   static constexpr int NF = 13; // in-place fields per cell
   static constexpr int CELL = NF * NNN + NP + 24 + 1; // doubles per cell, odd
   static constexpr size_t smem() { return sizeof(double) * (CW * CELL + NP * NNN + 2 * N); }
 };
 
+#ifndef STMG_V3_MAP1_MINB
+#define STMG_V3_MAP1_MINB 3
+#endif
 // Forward 1D contraction of a line: o[q] = sum_m M(q, m) in[m] (M = phi /
 // dphi, constant bank, compile-time indices).
 #define V3_FWD(M, in, o)                                                                                             \
@@ -61,12 +66,12 @@ struct V3
     o[q_] = s_;                                                                                                      \
   }
 
-template <int R, int S, int MODE>
-__global__ void __launch_bounds__(V3<R>::THREADS, 1)
+template <int R, int S, int MODE, int MAP = 0>
+__global__ void __launch_bounds__(V3<R, MAP>::THREADS, MAP == 0 ? 1 : STMG_V3_MAP1_MINB)
 vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
               double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
-  using C = V3<R>;
+  using C = V3<R, MAP>;
   constexpr int N = C::N, NN = C::NN, NNN = C::NNN, p = C::p, NP = C::NP, CW = C::CW;
   extern __shared__ __align__(16) double sm3[];
   double *const psi = sm3 + CW * C::CELL; // psi[m * NNN + q]: P_r^disc mode m at Gauss point q
@@ -91,8 +96,8 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
         txq[q] = P.xq[q];
       }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int cl = lane % CW;
-  const int t = warp * C::LPW + lane / CW; // line index
+  const int cl = MAP == 0 ? lane % CW : static_cast<int>(threadIdx.x) / NN;             // cell in block
+  const int t = MAP == 0 ? warp * C::LPW + lane / CW : static_cast<int>(threadIdx.x) % NN; // line index
   const long long gc = static_cast<long long>(blockIdx.x) * CW + cl;
   const bool active = gc < n_cells_total && t < NN;
   const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
@@ -1212,6 +1217,21 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
             case 0: gg(vmult3_init_kernel<0>, vmult3_gemm_kernel<S, 0>); break;
             case 1: gg(vmult3_init_kernel<1>, vmult3_gemm_kernel<S, 1>); break;
             default: gg(vmult3_init_kernel<2>, vmult3_gemm_kernel<S, 2>); break;
+          }
+        return cudaGetLastError();
+      }
+  if constexpr (R == 1)
+    if (std::getenv("STMG_V3_LINE") == nullptr)
+      {
+        // fused in-place pipeline (4 barriers per slot), N*N threads per cell
+        using C = V3<R, 1>;
+        const dim3 block(C::THREADS);
+        const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
+        switch (mode)
+          {
+            case 0: go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 1>, block, grid, C::smem()); break;
+            case 1: go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 1>, block, grid, C::smem()); break;
+            default: go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 1>, block, grid, C::smem()); break;
           }
         return cudaGetLastError();
       }
