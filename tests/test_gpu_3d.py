@@ -276,3 +276,30 @@ def test_vmult3_gemm_kernel_matches_oracle(stmg, ctx, oracle, monkeypatch):
         r_ = torch.zeros_like(y)
         lvl.residual(_cuda(b), _cuda(x), r_, n, _cuda(halo), coupled=True)
         assert _rel(r_.cpu().numpy(), b - yr) <= 1e-12
+
+
+def test_3d_status_codes(stmg, ctx):
+    """invalid_argument cases of the 3D entry points map to STMG_EINVAL (1),
+    like the reference's exceptions (vanka.cpp:223-224, transfer.cpp:155-158)."""
+    with pytest.raises(stmg.StmgError) as e:
+        stmg.Level3(ctx, 2, 2, 2, 3, 1, 0.1, 1.0, 1.0, stmg.SMOOTHER_CELL)  # r = 3 not instantiated in 3D
+    assert e.value.code == 1
+    with pytest.raises(stmg.StmgError) as e:
+        stmg.Level3(ctx, 2, 2, 2, 1, 1, -0.1, 1.0, 1.0, stmg.SMOOTHER_CELL)  # tau <= 0
+    assert e.value.code == 1
+    with pytest.raises(stmg.StmgError) as e:
+        stmg.Level3(ctx, 2, 2, 2, 1, 1, 0.1, 1.0, 1.0, stmg.SMOOTHER_VERTEX_STAR)  # cell Vanka only in 3D
+    assert e.value.code == 1
+    lvl = stmg.Level3(ctx, 2, 2, 2, 1, 1, 0.1, 1.0, 1.0, stmg.SMOOTHER_CELL)
+    b = torch.zeros(lvl.size, dtype=torch.float64, device="cuda")
+    with pytest.raises(stmg.StmgError) as e:
+        lvl.smooth_step(b, b.clone(), 1.5, 1)  # omega outside (0, 1]
+    assert e.value.code == 1
+    with pytest.raises(stmg.StmgError) as e:
+        stmg.Solver3(ctx, 3, 3, 3, 1, 1, 0.1, n_hcoarse=1)  # mesh not divisible
+    assert e.value.code == 1
+    S = stmg.Solver3(ctx, 2, 2, 2, 1, 1, 0.1, n_hcoarse=1, time_coarsen=True)
+    F = torch.zeros(3 * S.finest.size, dtype=torch.float64, device="cuda")
+    with pytest.raises(stmg.StmgError) as e:
+        S.solve_all_at_once(F, F.clone(), 3)  # 3 intervals cannot halve in time
+    assert e.value.code == 1
