@@ -66,7 +66,7 @@ struct V3
     o[q_] = s_;                                                                                                      \
   }
 
-template <int R, int S, int MODE, int MAP = 0>
+template <int R, int S, int MODE, int MAP = 0, bool DEF = true>
 __global__ void __launch_bounds__(V3<R, MAP>::THREADS, MAP == 0 ? 1 : STMG_V3_MAP1_MINB)
 vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
               double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
@@ -111,7 +111,7 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
   const int tA = t % N, tB = t / N; // line coordinates
   const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
   const int gx = P.gx, gy = P.gy, gz = P.gz;
-  const bool deformed = P.verts != nullptr;
+  constexpr bool deformed = DEF; // Cartesian instantiations use the diagonal Jacobian
   const double *__restrict__ xn = x + n * isz;
   const double *__restrict__ vprev = nullptr;
   if (coupled)
@@ -269,13 +269,12 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
 #pragma unroll
           for (int qz = 0; qz < N; ++qz)
             {
-              double Ji[3][3], det;
-              if (!deformed)
+              double Ji[3][3], det, jd[3];
+              if constexpr (!deformed)
                 {
-                  Ji[0][0] = 2.0 / P.hx;
-                  Ji[1][1] = 2.0 / P.hy;
-                  Ji[2][2] = 2.0 / P.hz;
-                  Ji[0][1] = Ji[0][2] = Ji[1][0] = Ji[1][2] = Ji[2][0] = Ji[2][1] = 0.0;
+                  jd[0] = 2.0 / P.hx;
+                  jd[1] = 2.0 / P.hy;
+                  jd[2] = 2.0 / P.hz;
                   det = 0.125 * P.hx * P.hy * P.hz;
                 }
               else
@@ -317,7 +316,10 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
               for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int d = 0; d < 3; ++d)
-                  G[c][d] = g[c][0][qz] * Ji[0][d] + g[c][1][qz] * Ji[1][d] + g[c][2][qz] * Ji[2][d];
+                  if constexpr (deformed)
+                    G[c][d] = g[c][0][qz] * Ji[0][d] + g[c][1][qz] * Ji[1][d] + g[c][2][qz] * Ji[2][d];
+                  else
+                    G[c][d] = g[c][d][qz] * jd[d];
               const double div = G[0][0] + G[1][1] + G[2][2];
               const int q = qz * NN + bz;
               double pq = 0.0;
@@ -336,7 +338,10 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
                   double Fr[3];
 #pragma unroll
                   for (int e = 0; e < 3; ++e)
-                    Fr[e] = Fp[0] * Ji[e][0] + Fp[1] * Ji[e][1] + Fp[2] * Ji[e][2];
+                    if constexpr (deformed)
+                      Fr[e] = Fp[0] * Ji[e][0] + Fp[1] * Ji[e][1] + Fp[2] * Ji[e][2];
+                    else
+                      Fr[e] = Fp[e] * jd[e];
                   const double fv = wd * vk[c][qz];
 #pragma unroll
                   for (int i = 0; i < N; ++i)
@@ -1227,11 +1232,21 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
         using C = V3<R, 1>;
         const dim3 block(C::THREADS);
         const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
+        const bool def = P.verts != nullptr;
         switch (mode)
           {
-            case 0: go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 1>, block, grid, C::smem()); break;
-            case 1: go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 1>, block, grid, C::smem()); break;
-            default: go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 1>, block, grid, C::smem()); break;
+            case 0:
+              def ? go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 1, true>, block, grid, C::smem())
+                  : go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 1, false>, block, grid, C::smem());
+              break;
+            case 1:
+              def ? go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 1, true>, block, grid, C::smem())
+                  : go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 1, false>, block, grid, C::smem());
+              break;
+            default:
+              def ? go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 1, true>, block, grid, C::smem())
+                  : go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 1, false>, block, grid, C::smem());
+              break;
           }
         return cudaGetLastError();
       }
@@ -1252,11 +1267,21 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
       using C = V3<R>;
       const dim3 block(C::THREADS);
       const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
+      const bool def = P.verts != nullptr;
       switch (mode)
         {
-          case 0: go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0>, block, grid, C::smem()); break;
-          case 1: go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1>, block, grid, C::smem()); break;
-          default: go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2>, block, grid, C::smem()); break;
+          case 0:
+            def ? go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 0, true>, block, grid, C::smem())
+                : go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 0, false>, block, grid, C::smem());
+            break;
+          case 1:
+            def ? go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 0, true>, block, grid, C::smem())
+                : go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 0, false>, block, grid, C::smem());
+            break;
+          default:
+            def ? go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 0, true>, block, grid, C::smem())
+                : go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 0, false>, block, grid, C::smem());
+            break;
         }
     }
   return cudaGetLastError();
