@@ -143,8 +143,12 @@ cudaError_t launch_zero_constrained3(const DevGeom3 &G, double *x, int n_interva
 /// deterministic single-block reductions.
 cudaError_t launch_project3(const DevGeom3 &G, const double *pmean, double inv_vol, double *x, int n_intervals,
                             cudaStream_t st);
-/// nc coarse intervals -> (h_time ? 2 nc : nc) fine intervals
-cudaError_t launch_prolongate3(const DevTransfer3 &T, const double *coarse, double *fine, int nc, cudaStream_t st);
-cudaError_t launch_restrict3(const DevTransfer3 &T, const double *fine, double *coarse, int nc, cudaStream_t st);
+/// nc coarse intervals -> (h_time ? 2 nc : nc) fine intervals. With `work`
+/// (transfer3_work_doubles) spatial transfers run as separable 1D passes.
+long long transfer3_work_doubles(const DevTransfer3 &T, int nc);
+cudaError_t launch_prolongate3(const DevTransfer3 &T, const double *coarse, double *fine, int nc, cudaStream_t st,
+                               double *work = nullptr);
+cudaError_t launch_restrict3(const DevTransfer3 &T, const double *fine, double *coarse, int nc, cudaStream_t st,
+                             double *work = nullptr);
 
 } // namespace stmg_b200

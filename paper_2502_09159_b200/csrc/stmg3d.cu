@@ -249,7 +249,7 @@ struct Solver3Level
   DevArray<int> csr_i[6];
   DevArray<double> csr_v[6], child;
   DevTransfer3 dt{};
-  DevArray<double> x, b, r, t, halo;
+  DevArray<double> x, b, r, t, halo, tw;
 };
 
 void
@@ -347,8 +347,9 @@ struct stmg3_solver
   {
     Solver3Level &F = *levels[l];
     stmg3_level &C = *levels[l - 1]->level;
-    check(launch_restrict3(F.dt, fine_v, coarse_v, nc, ctx->stream), "restrict3");
-    ctx->count(2);
+    F.tw.resize(std::max<long long>(1, transfer3_work_doubles(F.dt, nc)));
+    check(launch_restrict3(F.dt, fine_v, coarse_v, nc, ctx->stream, F.dt.spatial ? F.tw.p : nullptr), "restrict3");
+    ctx->count(F.dt.spatial ? 4 : 2);
     C.zero_constrained(coarse_v, nc);
     if (project)
       C.project_residual(coarse_v, nc);
@@ -363,8 +364,10 @@ struct stmg3_solver
     const int nf = F.dt.h_time ? 2 * nc : nc;
     const long long n = L.spec.isz() * nf;
     F.t.resize(n);
-    check(launch_prolongate3(F.dt, coarse_v, F.t.p, nc, ctx->stream), "prolongate3");
-    ctx->count(2);
+    F.tw.resize(std::max<long long>(1, transfer3_work_doubles(F.dt, nc)));
+    check(launch_prolongate3(F.dt, coarse_v, F.t.p, nc, ctx->stream, F.dt.spatial ? F.tw.p : nullptr),
+          "prolongate3");
+    ctx->count(F.dt.spatial ? 4 : 2);
     L.zero_constrained(F.t.p, nf);
     if (project)
       L.project(F.t.p, nf);
