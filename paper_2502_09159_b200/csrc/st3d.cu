@@ -67,7 +67,7 @@ struct V3
   }
 
 template <int R, int S, int MODE, int MAP = 0, bool DEF = true>
-__global__ void __launch_bounds__(V3<R, MAP>::THREADS, MAP == 0 ? 1 : STMG_V3_MAP1_MINB)
+__global__ void __launch_bounds__(V3<R, MAP>::THREADS, MAP == 0 ? 1 : (DEF ? 2 : STMG_V3_MAP1_MINB))
 vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
               double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
