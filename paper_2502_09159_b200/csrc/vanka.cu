@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(ROWS / SPLIT / 8 / TPW * 32, SPLIT == 1 ? 1 : 
 vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ items,
                   const int *__restrict__ item_ptr, const long long *__restrict__ vel_anchor,
                   const long long *__restrict__ pre_anchor, const double *__restrict__ r, double *__restrict__ u,
-                  long long isz, int n_intervals, double omega)
+                  long long isz, int n_intervals, double omega, int group)
 {
   // ROWS rows of the patch matrix, split over SPLIT CTAs (blockIdx.z): a CTA
   // computes and scatters OROWS rows but gathers all ROWS rows of R (the
@@ -169,8 +169,8 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
   double *w_s = Zs + OROWS * kDZLd;                                 // OROWS
   long long *cb = reinterpret_cast<long long *>(w_s + OROWS);      // [3][2][kDCols] column bases
 
-  const int n0 = blockIdx.y * kDGroup;
-  const int ng = min(kDGroup, n_intervals - n0);
+  const int n0 = blockIdx.y * group;
+  const int ng = min(group, n_intervals - n0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = tid % kDCols;        // column of this thread in every tile
   const int ibase = tid / kDCols;    // first row of this thread (rows ibase + q * kDThreads / kDCols)
@@ -352,7 +352,8 @@ template <int TPW>
 __global__ void __launch_bounds__(kBThreads, kBCols == 32 ? 1 : 2)
 vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
                  const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
-                 const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals, double omega)
+                 const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals, double omega,
+                 int group)
 {
   extern __shared__ __align__(16) double bsm[];
   const VankaBatch bt = batches[blockIdx.x];
@@ -362,8 +363,8 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
   double *Rs = bsm;                                   // (4 ks) x kBLd
   long long *cvb = reinterpret_cast<long long *>(Rs + 4 * ks * kBLd); // velocity column bases
   long long *cpb = cvb + kBCols;                                      // pressure column bases
-  const int n0 = blockIdx.y * kBGroup;
-  const int ng = min(kBGroup, n_intervals - n0);
+  const int n0 = blockIdx.y * group;
+  const int ng = min(group, n_intervals - n0);
   const int ncols = bt.count * ng;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rtiles = (nt + 7) / 8;
@@ -478,12 +479,17 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       const int rows = max_nt <= kDRows ? kDRows : 176;
       const int split = rows == 176 ? 2 : 1, orows = rows / split;
       const size_t dsmem = sizeof(double) * (rows * kDRLd + orows * kDZLd + orows) + sizeof(long long) * 6 * kDCols;
-      dim3 grid(n_batches, (n_intervals + kDGroup - 1) / kDGroup, split);
+      // intervals per block: 16, fewer on small levels so the launch still
+      // fills the GPU (a coarse level has only a few batches per colour)
+      int group = kDGroup;
+      while (group > 1 && static_cast<long long>(n_batches) * split * ((n_intervals + group - 1) / group) < 2 * 148)
+        group /= 2;
+      dim3 grid(n_batches, (n_intervals + group - 1) / group, split);
       const int ks = (max_nt + 3) / 4;
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
         kern<<<grid, rows == 176 ? 352 : rows * 4, dsmem, stream>>>(
-          classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega);
+          classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega, group);
       };
       if (rows == 176)
         go(vanka_dmma_kernel<44, 176, 1, 16, 2>); // 2 CTAs x 88 rows, one 8-row tile per warp
@@ -508,11 +514,14 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       const int ks = (max_nt + 3) / 4;
       const size_t smem = sizeof(double) * (4 * ks * kBLd) + sizeof(long long) * 2 * kBCols;
       const int tpw = ((max_nt + 7) / 8 + 15) / 16;
-      dim3 grid(n_batches, (n_intervals + kBGroup - 1) / kBGroup);
+      int group = kBGroup;
+      while (group > 1 && static_cast<long long>(n_batches) * ((n_intervals + group - 1) / group) < 2 * 148)
+        group /= 2;
+      dim3 grid(n_batches, (n_intervals + group - 1) / group);
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         kern<<<grid, kBThreads, smem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz, n_intervals,
-                                                omega);
+                                                omega, group);
       };
       if (tpw <= 2)
         go(vanka_big_kernel<2>);
