@@ -33,7 +33,7 @@ namespace stmg_b200
 
 namespace
 {
-template <int R, int MAP = 0>
+template <int R, int MAP = 0, bool DEF = false>
 struct V3
 {
   static constexpr int N = R + 2, NN = N * N, NNN = N * N * N, p = R + 1;
@@ -49,7 +49,10 @@ struct V3
   static constexpr int NWARP = (NN + LPW - 1) / LPW;
   static constexpr int THREADS = MAP == 0 ? 32 * NWARP : NN * CW;
   static constexpr int NF = 13; // in-place fields per cell
-  static constexpr int CELL = NF * NNN + NP + 24 + 1; // doubles per cell, odd
+  // deformed cells cache J^{-1} (9) and det (1) per Gauss point: computed in
+  // the first output slot, reused by the others
+  static constexpr int GC = DEF ? 10 * NNN : 0;
+  static constexpr int CELL = NF * NNN + NP + 24 + GC + 1 - (NF * NNN + NP + 24 + GC) % 2; // odd
   static constexpr size_t smem() { return sizeof(double) * (CW * CELL + NP * NNN + 2 * N); }
 };
 
@@ -67,11 +70,11 @@ struct V3
   }
 
 template <int R, int S, int MODE, int MAP = 0, bool DEF = true>
-__global__ void __launch_bounds__(V3<R, MAP>::THREADS, MAP == 0 ? 1 : (DEF ? 2 : STMG_V3_MAP1_MINB))
+__global__ void __launch_bounds__(V3<R, MAP, DEF>::THREADS, MAP == 0 ? 1 : (DEF ? 2 : STMG_V3_MAP1_MINB))
 vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
               double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
-  using C = V3<R, MAP>;
+  using C = V3<R, MAP, DEF>;
   constexpr int N = C::N, NN = C::NN, NNN = C::NNN, p = C::p, NP = C::NP, CW = C::CW;
   extern __shared__ __align__(16) double sm3[];
   double *const psi = sm3 + CW * C::CELL; // psi[m * NNN + q]: P_r^disc mode m at Gauss point q
@@ -108,6 +111,7 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
   double *const F = sm3 + cl * C::CELL;
   double *const PM = F + C::NF * NNN;
   double *const X8 = PM + NP;
+  double *const GCa = X8 + 24; // deformed: [point][10] J^{-1}, det
   const int tA = t % N, tB = t / N; // line coordinates
   const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
   const int gx = P.gx, gy = P.gy, gz = P.gz;
@@ -277,6 +281,14 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
                   jd[2] = 2.0 / P.hz;
                   det = 0.125 * P.hx * P.hy * P.hz;
                 }
+              else if (a > 0)
+                {
+                  const double *gp = GCa + (qz * NN + bz) * 10;
+#pragma unroll
+                  for (int e = 0; e < 9; ++e)
+                    Ji[e / 3][e % 3] = gp[e];
+                  det = gp[9];
+                }
               else
                 {
                   const double xi[3] = {txq[tA], txq[tB], P.xq[qz]};
@@ -309,6 +321,14 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
                   Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
                   Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
                   Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+                  if (S > 1)
+                    {
+                      double *gp = GCa + (qz * NN + bz) * 10;
+#pragma unroll
+                      for (int e = 0; e < 9; ++e)
+                        gp[e] = Ji[e / 3][e % 3];
+                      gp[9] = det;
+                    }
                 }
               const double wd = P.w[qz] * wxy * det;
               double G[3][3];
@@ -1229,22 +1249,23 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
     if (std::getenv("STMG_V3_LINE") == nullptr)
       {
         // fused in-place pipeline (4 barriers per slot), N*N threads per cell
-        using C = V3<R, 1>;
+        using C = V3<R, 1, false>;
+        using CD = V3<R, 1, true>;
         const dim3 block(C::THREADS);
         const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
         const bool def = P.verts != nullptr;
         switch (mode)
           {
             case 0:
-              def ? go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 1, true>, block, grid, C::smem())
+              def ? go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 1, true>, block, grid, CD::smem())
                   : go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 1, false>, block, grid, C::smem());
               break;
             case 1:
-              def ? go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 1, true>, block, grid, C::smem())
+              def ? go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 1, true>, block, grid, CD::smem())
                   : go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 1, false>, block, grid, C::smem());
               break;
             default:
-              def ? go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 1, true>, block, grid, C::smem())
+              def ? go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 1, true>, block, grid, CD::smem())
                   : go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 1, false>, block, grid, C::smem());
               break;
           }
@@ -1264,22 +1285,23 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
     }
   else
     {
-      using C = V3<R>;
+      using C = V3<R, 0, false>;
+      using CD = V3<R, 0, true>;
       const dim3 block(C::THREADS);
       const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
       const bool def = P.verts != nullptr;
       switch (mode)
         {
           case 0:
-            def ? go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 0, true>, block, grid, C::smem())
+            def ? go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 0, true>, block, grid, CD::smem())
                 : go(vmult3_init_kernel<0>, vmult3_kernel<R, S, 0, 0, false>, block, grid, C::smem());
             break;
           case 1:
-            def ? go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 0, true>, block, grid, C::smem())
+            def ? go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 0, true>, block, grid, CD::smem())
                 : go(vmult3_init_kernel<1>, vmult3_kernel<R, S, 1, 0, false>, block, grid, C::smem());
             break;
           default:
-            def ? go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 0, true>, block, grid, C::smem())
+            def ? go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 0, true>, block, grid, CD::smem())
                 : go(vmult3_init_kernel<2>, vmult3_kernel<R, S, 2, 0, false>, block, grid, C::smem());
             break;
         }
