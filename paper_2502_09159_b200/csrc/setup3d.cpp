@@ -82,6 +82,32 @@ make_level3_consts(const Level3Spec &L, const double *dev_verts)
   P.hz = 1.0 / L.nz;
   P.verts = dev_verts;
   P.gemmE = nullptr;
+  for (int i = 0; i < N; ++i)
+    for (int k = 0; k < N; ++k)
+      {
+        double m = 0.0, kk = 0.0, c = 0.0;
+        for (int q = 0; q < N; ++q)
+          {
+            m += g.w[q] * P.phi[q * N + i] * P.phi[q * N + k];
+            kk += g.w[q] * P.dphi[q * N + i] * P.dphi[q * N + k];
+            c += g.w[q] * P.phi[q * N + i] * P.dphi[q * N + k];
+          }
+        P.m1[i * N + k] = m;
+        P.k1[i * N + k] = kk;
+        P.c1[i * N + k] = c;
+      }
+  for (int a = 0; a <= L.r; ++a)
+    for (int i = 0; i < N; ++i)
+      {
+        double sm = 0.0, sc = 0.0;
+        for (int q = 0; q < N; ++q)
+          {
+            sm += g.w[q] * P.leg[a * N + q] * P.phi[q * N + i];
+            sc += g.w[q] * P.leg[a * N + q] * P.dphi[q * N + i];
+          }
+        P.lm[a * N + i] = sm;
+        P.lc[a * N + i] = sc;
+      }
   return P;
 }
 

@@ -1172,6 +1172,276 @@ vmult3_gemm_kernel(const Level3Consts P, const double *__restrict__ E, const dou
       __syncthreads();
     }
 }
+
+// ---------------------------------------------------------------------------
+// Cartesian r = 1 (C3), 1D-factor form: on congruent rectangular cells every
+// term of the spatial Stokes operator is a tensor product of exact 1D node
+// matrices (M1, K1, C1 and the Legendre moments Lm, Lc), as in the 2D
+// kernel, so no Gauss points are visited:
+//   y_c = J M(x)M(x)M UK_c + sum_e nu_e s_e K_e (x) M (x) M UM_c
+//         + gamma sum_{d != c} (2/h_c)(2/h_d) J  Ct_c (x) C_d (x) M  UM_d - B_c^T PM,
+//   y_p = sum_c B_c UM_c.
+// Three phases (x, y, z lines, 2 barriers per slot): the x pass forms the
+// 12 x-contracted fields, the y pass combines them into 3 groups per output
+// component by their z factor (M, K, C or C^T), the z pass finishes and
+// scatters from registers. ~40% fewer line passes and no point fluxes.
+template <int S, int MODE>
+__global__ void __launch_bounds__(144, 3)
+vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
+               double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
+{
+  constexpr int N = 3, NN = 9, NNN = 27, p = 2, NP = 4, CB = 16;
+  constexpr int CELL = 12 * NNN + 9 * NNN + NP * NN + NP; // 607 (odd)
+  extern __shared__ __align__(16) double smc[];
+  double *const tab = smc + CB * CELL; // lm[2][3], lc[2][3]
+  if (threadIdx.x < 6)
+    {
+      tab[threadIdx.x] = P.lm[threadIdx.x];
+      tab[6 + threadIdx.x] = P.lc[threadIdx.x];
+    }
+  const int t = threadIdx.x % NN, cl = threadIdx.x / NN;
+  const long long gc = static_cast<long long>(blockIdx.x) * CB + cl;
+  const bool active = gc < n_cells_total;
+  const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
+  const int n = active ? static_cast<int>(gc / ncells) : 0;
+  const long long cell = active ? gc - n * ncells : 0;
+  const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
+            cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
+  double *const XF = smc + cl * CELL; // 12 fields
+  double *const YF = XF + 12 * NNN;   // 9 fields
+  double *const PP = YF + 9 * NNN;    // [NP][NN] pressure-row partials
+  double *const PM = PP + NP * NN;
+  const int tA = t % N, tB = t / N;
+  const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
+  const int gx = P.gx, gy = P.gy, gz = P.gz;
+  const double *__restrict__ xn = x + n * isz;
+  const double *__restrict__ vprev = nullptr;
+  if (coupled)
+    vprev = n > 0 ? x + (n - 1) * isz + (S - 1) * mv : xprev0;
+  const double ix2[3] = {2.0 / P.hx, 2.0 / P.hy, 2.0 / P.hz};
+  const double Jm = 0.125 * P.hx * P.hy * P.hz;
+  double se[3];
+#pragma unroll
+  for (int e = 0; e < 3; ++e)
+    se[e] = ix2[e] * ix2[e] * Jm;
+  const double nu = P.nu, ga = P.gamma;
+  auto lmv = [&](int a, int i) { return tab[a * N + i]; };
+  auto lcv = [&](int a, int i) { return tab[6 + a * N + i]; };
+  // mode exponents of P_1^disc (pdisc.cpp:41-55): (0,0,0), (1,0,0), (0,1,0), (0,0,1)
+  auto ex = [](int m, int d) { return (m > 0 && m - 1 == d) ? 1 : 0; };
+  __syncthreads();
+
+  for (int a = 0; a < S; ++a)
+    {
+      double kt[S], mt[S], lva = 0.0;
+#pragma unroll
+      for (int aa = 0; aa < S; ++aa)
+        if (a == aa)
+          {
+#pragma unroll
+            for (int bs = 0; bs < S; ++bs)
+              {
+                kt[bs] = P.Kt[aa * S + bs];
+                mt[bs] = P.Mt[aa * S + bs];
+              }
+            lva = P.lv[aa];
+          }
+      // ---- x phase (j = tA, k = tB)
+      if (active)
+        {
+          const int Y = cy * p + tA, Z = cz * p + tB;
+          const bool yzb = MODE != 2 && (Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1);
+          const long long row = (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
+          double uk[3][N], um[3][N];
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+              {
+                const int X = cx * p + i;
+                const bool bnd = yzb || (MODE != 2 && (X == 0 || X == gx - 1));
+                double k_ = 0.0, m_ = 0.0;
+                if (!bnd)
+#pragma unroll
+                  for (int bs = 0; bs < S; ++bs)
+                    {
+                      const double v = __ldg(xn + bs * mv + c * nsc + row + i);
+                      k_ = fma(kt[bs], v, k_);
+                      m_ = fma(mt[bs], v, m_);
+                    }
+                if (vprev != nullptr)
+                  k_ = fma(-lva, __ldg(vprev + c * nsc + row + i), k_);
+                uk[c][i] = k_;
+                um[c][i] = m_;
+              }
+          const int base = (tB * N + tA) * N;
+          // out[o] = sum_i A(o, i) in[i]; C: A(o,i) = C1(o,i); C^T: A(o,i) = C1(i,o)
+#pragma unroll
+          for (int o = 0; o < N; ++o)
+            {
+              double f[12];
+#pragma unroll
+              for (int q = 0; q < 12; ++q)
+                f[q] = 0.0;
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  const double m = P.m1[o * N + i], k = P.k1[o * N + i], c = P.c1[o * N + i], ct = P.c1[i * N + o];
+#pragma unroll
+                  for (int cc = 0; cc < 3; ++cc)
+                    f[cc] = fma(m, uk[cc][i], f[cc]);
+                  f[3] = fma(m, um[0][i], f[3]);
+                  f[4] = fma(k, um[0][i], f[4]);
+                  f[5] = fma(c, um[0][i], f[5]);
+                  f[6] = fma(m, um[1][i], f[6]);
+                  f[7] = fma(k, um[1][i], f[7]);
+                  f[8] = fma(ct, um[1][i], f[8]);
+                  f[9] = fma(m, um[2][i], f[9]);
+                  f[10] = fma(k, um[2][i], f[10]);
+                  f[11] = fma(ct, um[2][i], f[11]);
+                }
+#pragma unroll
+              for (int q = 0; q < 12; ++q)
+                XF[q * NNN + base + o] = f[q];
+            }
+          // pressure rows: partial sums of y_p(l) = sum_c (2/h_c) J [L^c_x (x) L^c_y (x) L^c_z](l) UM_c over this x-line
+#pragma unroll
+          for (int l = 0; l < NP; ++l)
+            {
+              double s = 0.0;
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                {
+                  double sx = 0.0;
+#pragma unroll
+                  for (int i = 0; i < N; ++i)
+                    sx = fma(c == 0 ? lcv(ex(l, 0), i) : lmv(ex(l, 0), i), um[c][i], sx);
+                  const double wy = c == 1 ? lcv(ex(l, 1), tA) : lmv(ex(l, 1), tA);
+                  const double wz = c == 2 ? lcv(ex(l, 2), tB) : lmv(ex(l, 2), tB);
+                  s = fma(ix2[c] * Jm * wy * wz, sx, s);
+                }
+              PP[l * NN + t] = s;
+            }
+          if (t < NP)
+            {
+              double s = 0.0;
+#pragma unroll
+              for (int bs = 0; bs < S; ++bs)
+                s = fma(mt[bs], __ldg(xn + S * mv + bs * mp + cell * NP + t), s);
+              PM[t] = s;
+            }
+        }
+      __syncthreads();
+      // ---- y phase (i = tA, k = tB): groups by z factor
+      if (active)
+        {
+          const int base = tB * NN + tA; // + j * N
+          double in[12][N];
+#pragma unroll
+          for (int q = 0; q < 12; ++q)
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+              in[q][j] = XF[q * NNN + base + j * N];
+          const double gxy = ga * ix2[0] * ix2[1] * Jm, gxz = ga * ix2[0] * ix2[2] * Jm, gyz = ga * ix2[1] * ix2[2] * Jm;
+#pragma unroll
+          for (int o = 0; o < N; ++o)
+            {
+              // only the combinations the three outputs use
+              double My[12], Ky3 = 0.0, Ky6 = 0.0, Ky9 = 0.0, Cy6 = 0.0, Cy8 = 0.0, Cty5 = 0.0, Cty9 = 0.0;
+#pragma unroll
+              for (int q = 0; q < 12; ++q)
+                My[q] = 0.0;
+#pragma unroll
+              for (int j = 0; j < N; ++j)
+                {
+                  const double m = P.m1[o * N + j], k = P.k1[o * N + j], c = P.c1[o * N + j], ct = P.c1[j * N + o];
+#pragma unroll
+                  for (int q = 0; q < 12; ++q)
+                    if (q != 8)
+                      My[q] = fma(m, in[q][j], My[q]);
+                  Ky3 = fma(k, in[3][j], Ky3);
+                  Ky6 = fma(k, in[6][j], Ky6);
+                  Ky9 = fma(k, in[9][j], Ky9);
+                  Cy6 = fma(c, in[6][j], Cy6);
+                  Cy8 = fma(c, in[8][j], Cy8);
+                  Cty5 = fma(ct, in[5][j], Cty5);
+                  Cty9 = fma(ct, in[9][j], Cty9);
+                }
+              const int yo = base + o * N;
+              // output x
+              YF[0 * NNN + yo] = Jm * My[0] + (nu + ga) * se[0] * My[4] + nu * se[1] * Ky3 + gxy * Cy8;
+              YF[1 * NNN + yo] = nu * se[2] * My[3];
+              YF[2 * NNN + yo] = gxz * My[11];
+              // output y
+              YF[3 * NNN + yo] = Jm * My[1] + nu * se[0] * My[7] + (nu + ga) * se[1] * Ky6 + gxy * Cty5;
+              YF[4 * NNN + yo] = nu * se[2] * My[6];
+              YF[5 * NNN + yo] = gyz * Cty9;
+              // output z
+              YF[6 * NNN + yo] = Jm * My[2] + nu * se[0] * My[10] + nu * se[1] * Ky9;
+              YF[7 * NNN + yo] = (nu + ga) * se[2] * My[9];
+              YF[8 * NNN + yo] = gxz * My[5] + gyz * Cy6;
+            }
+          if (t < NP)
+            {
+              double s = 0.0;
+#pragma unroll
+              for (int q = 0; q < NN; ++q)
+                s += PP[t * NN + q];
+              const long long o = n * isz + S * mv + a * mp + cell * NP + t;
+              y[o] = MODE == 1 ? __ldg(b + o) - s : s;
+            }
+        }
+      __syncthreads();
+      // ---- z phase (i = tA, j = tB): finish, subtract B^T PM, scatter
+      if (active)
+        {
+          const int base = tB * N + tA; // + k * NN
+          const int X = cx * p + tA, Y = cy * p + tB;
+          const bool xyb = X == 0 || Y == 0 || X == gx - 1 || Y == gy - 1;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double gm[N], gk[N], g3[N];
+#pragma unroll
+              for (int k = 0; k < N; ++k)
+                {
+                  gm[k] = YF[(3 * c) * NNN + base + k * NN];
+                  gk[k] = YF[(3 * c + 1) * NNN + base + k * NN];
+                  g3[k] = YF[(3 * c + 2) * NNN + base + k * NN];
+                }
+              double *yv = y + n * isz + a * mv + c * nsc + static_cast<long long>(Y) * gx + X;
+#pragma unroll
+              for (int o = 0; o < N; ++o)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int k = 0; k < N; ++k)
+                    {
+                      s = fma(P.m1[o * N + k], gm[k], s);
+                      s = fma(P.k1[o * N + k], gk[k], s);
+                      // z factor of group 3: C (trial derivative in z) for outputs x, y; C^T for output z
+                      s = fma(c == 2 ? P.c1[k * N + o] : P.c1[o * N + k], g3[k], s);
+                    }
+                  // - B_c^T PM: sum_l PM_l (2/h_c) J [L^c_x (x) L^c_y (x) L^c_z](l; tA, tB, o)
+#pragma unroll
+                  for (int l = 0; l < NP; ++l)
+                    {
+                      const double wx = c == 0 ? lcv(ex(l, 0), tA) : lmv(ex(l, 0), tA);
+                      const double wy = c == 1 ? lcv(ex(l, 1), tB) : lmv(ex(l, 1), tB);
+                      const double wz = c == 2 ? lcv(ex(l, 2), o) : lmv(ex(l, 2), o);
+                      s = fma(-ix2[c] * Jm * wx * wy * wz, PM[l], s);
+                    }
+                  const int Z = cz * p + o;
+                  const bool bnd = MODE != 2 && (xyb || Z == 0 || Z == gz - 1);
+                  if (!bnd)
+                    atomicAdd(yv + static_cast<long long>(Z) * gy * gx, MODE == 1 ? -s : s);
+                }
+            }
+        }
+      // next slot: x phase writes XF (read only by the y phase, which every
+      // thread has left), the z phase reads YF (written after the next barrier)
+    }
+}
 /// y's velocity rows before the scatter: 0 (plain / raw), b (residual); the
 /// constrained rows get the identity x (plain) or b - x (residual),
 /// st_operator.cpp:383-394.
@@ -1242,6 +1512,25 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
             case 0: gg(vmult3_init_kernel<0>, vmult3_gemm_kernel<S, 0>); break;
             case 1: gg(vmult3_init_kernel<1>, vmult3_gemm_kernel<S, 1>); break;
             default: gg(vmult3_init_kernel<2>, vmult3_gemm_kernel<S, 2>); break;
+          }
+        return cudaGetLastError();
+      }
+  if constexpr (R == 1)
+    if (P.verts == nullptr && std::getenv("STMG_V3_QUAD") == nullptr)
+      {
+        constexpr int CB = 16;
+        const size_t smem = sizeof(double) * (CB * (21 * 27 + 4 * 9 + 4) + 12);
+        const unsigned grid = static_cast<unsigned>((cells + CB - 1) / CB);
+        auto gc = [&](auto init, auto kern) {
+          init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+          kern<<<grid, 144, smem, st>>>(P, x, b, y, xprev0, coupled, cells);
+        };
+        switch (mode)
+          {
+            case 0: gc(vmult3_init_kernel<0>, vmult3c_kernel<S, 0>); break;
+            case 1: gc(vmult3_init_kernel<1>, vmult3c_kernel<S, 1>); break;
+            default: gc(vmult3_init_kernel<2>, vmult3c_kernel<S, 2>); break;
           }
         return cudaGetLastError();
       }

@@ -41,6 +41,11 @@ struct Level3Consts
   double nu, gamma, hx, hy, hz;
   const double *verts; // nullptr: Cartesian unit-cube mesh
   const double *gemmE; // Cartesian r = 1: dense element operator (88 x 168), vmult3_gemm_kernel; else nullptr
+  // reference-cell 1D node matrices (exact Gauss): M1(i,k) = int phi_i phi_k, K1 = int phi_i' phi_k',
+  // C1(i,k) = int phi_i phi_k' (test i, trial derivative k); Legendre moments Lm(a,i) = int L_a phi_i,
+  // Lc(a,i) = int L_a phi_i' (Cartesian 1D-factor kernel vmult3c_kernel)
+  double m1[kMaxN1 * kMaxN1], k1[kMaxN1 * kMaxN1], c1[kMaxN1 * kMaxN1];
+  double lm[kMaxP * kMaxN1], lc[kMaxP * kMaxN1];
 };
 
 struct Level3Spec
