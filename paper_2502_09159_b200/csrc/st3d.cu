@@ -1191,7 +1191,7 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
                double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
   constexpr int N = 3, NN = 9, NNN = 27, p = 2, NP = 4, CB = 16;
-  constexpr int CELL = 12 * NNN + 9 * NNN + NP * NN + NP; // 607 (odd)
+  constexpr int CELL = 12 * NNN + NP * NN + NP + 1; // 365 (odd): the y groups overwrite x fields 0..8 in place
   extern __shared__ __align__(16) double smc[];
   double *const tab = smc + CB * CELL; // lm[2][3], lc[2][3]
   if (threadIdx.x < 6)
@@ -1208,8 +1208,8 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
   const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
             cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
   double *const XF = smc + cl * CELL; // 12 fields
-  double *const YF = XF + 12 * NNN;   // 9 fields
-  double *const PP = YF + 9 * NNN;    // [NP][NN] pressure-row partials
+  double *const YF = XF;             // 9 fields, written in place over the y-line of XF
+  double *const PP = XF + 12 * NNN;  // [NP][NN] pressure-row partials
   double *const PM = PP + NP * NN;
   const int tA = t % N, tB = t / N;
   const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
@@ -1438,8 +1438,7 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
                 }
             }
         }
-      // next slot: x phase writes XF (read only by the y phase, which every
-      // thread has left), the z phase reads YF (written after the next barrier)
+      __syncthreads(); // the next slot's x phase overwrites the groups the z phase reads
     }
 }
 /// y's velocity rows before the scatter: 0 (plain / raw), b (residual); the
@@ -1519,7 +1518,7 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
     if (P.verts == nullptr && std::getenv("STMG_V3_QUAD") == nullptr)
       {
         constexpr int CB = 16;
-        const size_t smem = sizeof(double) * (CB * (21 * 27 + 4 * 9 + 4) + 12);
+        const size_t smem = sizeof(double) * (CB * (12 * 27 + 4 * 9 + 4 + 1) + 12);
         const unsigned grid = static_cast<unsigned>((cells + CB - 1) / CB);
         auto gc = [&](auto init, auto kern) {
           init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
