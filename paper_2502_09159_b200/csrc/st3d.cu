@@ -1185,8 +1185,11 @@ vmult3_gemm_kernel(const Level3Consts P, const double *__restrict__ E, const dou
 // 12 x-contracted fields, the y pass combines them into 3 groups per output
 // component by their z factor (M, K, C or C^T), the z pass finishes and
 // scatters from registers. ~40% fewer line passes and no point fluxes.
+#ifndef STMG_V3C_MINB
+#define STMG_V3C_MINB 4
+#endif
 template <int S, int MODE>
-__global__ void __launch_bounds__(144, 3)
+__global__ void __launch_bounds__(144, STMG_V3C_MINB)
 vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
                double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
