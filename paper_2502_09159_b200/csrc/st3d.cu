@@ -1448,27 +1448,25 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
 /// constrained rows get the identity x (plain) or b - x (residual),
 /// st_operator.cpp:383-394.
 template <int MODE>
-__global__ void
+__global__ void __launch_bounds__(128)
 vmult3_init_kernel(DevGeom3 G, const double *__restrict__ x, const double *__restrict__ b, double *__restrict__ y,
                    long long total)
 {
-  const long long per = static_cast<long long>(G.S) * G.mv;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x)
-    {
-      const long long n = idx / per, rem = idx - n * per;
-      const long long o = n * G.isz + rem;
-      const long long s = rem % G.nsc;
-      const int X = static_cast<int>(s % G.gx), Y = static_cast<int>((s / G.gx) % G.gy),
-                Z = static_cast<int>(s / (static_cast<long long>(G.gx) * G.gy));
-      const bool bnd = X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1;
-      double v = 0.0;
-      if (MODE != 2 && bnd)
-        v = x[o];
-      if (MODE == 1)
-        v = b[o] - v;
-      y[o] = v;
-    }
+  // grid: (X*Y blocks, Z, interval * slot * component); 32-bit index math
+  const int xy = blockIdx.x * 128 + threadIdx.x;
+  if (xy >= G.gx * G.gy)
+    return;
+  const int X = xy % G.gx, Y = xy / G.gx, Z = blockIdx.y;
+  const int q = blockIdx.z, comp = q % 3, a = (q / 3) % G.S, n = q / (3 * G.S);
+  const long long o = n * G.isz + a * G.mv + comp * G.nsc + (static_cast<long long>(Z) * G.gy + Y) * G.gx + X;
+  const bool bnd = X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1;
+  double v = 0.0;
+  if (MODE != 2 && bnd)
+    v = x[o];
+  if (MODE == 1)
+    v = __ldg(b + o) - v;
+  y[o] = v;
+  (void)total;
 }
 
 template <int R, int S>
@@ -1490,10 +1488,10 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
   G.mp = P.mp;
   G.isz = P.isz;
   const long long total_v = static_cast<long long>(nI) * S * P.mv;
-  const int ib = static_cast<int>(std::min<long long>((total_v + 255) / 256, 148 * 16));
+  const dim3 igrid((P.gx * P.gy + 127) / 128, P.gz, nI * S * 3);
   const long long cells = static_cast<long long>(nI) * P.nx * P.ny * P.nz;
   auto go = [&](auto init, auto kern, dim3 block, unsigned grid, size_t smem) {
-    init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
+    init<<<igrid, 128, 0, st>>>(G, x, b, y, total_v);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<grid, block, smem, st>>>(P, x, b, y, xprev0, coupled, cells);
   };
@@ -1505,7 +1503,7 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
                             sizeof(int) * (kGCols + 32) + sizeof(double) * (2 * S + 1) * kGCols;
         const unsigned grid = static_cast<unsigned>(std::min<long long>(2 * 148, (ncols + kGCols - 1) / kGCols));
         auto gg = [&](auto init, auto kern) {
-          init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
+          init<<<igrid, 128, 0, st>>>(G, x, b, y, total_v);
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
           kern<<<grid, kGThreads, smem, st>>>(P, P.gemmE, x, b, y, xprev0, coupled, ncols);
         };
@@ -1524,7 +1522,7 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
         const size_t smem = sizeof(double) * (CB * (12 * 27 + 4 * 9 + 4 + 1) + 12);
         const unsigned grid = static_cast<unsigned>((cells + CB - 1) / CB);
         auto gc = [&](auto init, auto kern) {
-          init<<<ib, 256, 0, st>>>(G, x, b, y, total_v);
+          init<<<igrid, 128, 0, st>>>(G, x, b, y, total_v);
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
           kern<<<grid, 144, smem, st>>>(P, x, b, y, xprev0, coupled, cells);
         };
