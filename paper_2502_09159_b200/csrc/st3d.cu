@@ -1599,20 +1599,18 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
 }
 
 // ---------------------------------------------------------------- aux
-__global__ void
-zero_constrained3_kernel(DevGeom3 G, double *__restrict__ x, long long total)
+__global__ void __launch_bounds__(128)
+zero_constrained3_kernel(DevGeom3 G, double *__restrict__ x)
 {
-  const long long per = static_cast<long long>(G.S) * G.mv;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x)
-    {
-      const long long n = idx / per, rem = idx - n * per;
-      const long long s = rem % G.nsc;
-      const int X = static_cast<int>(s % G.gx), Y = static_cast<int>((s / G.gx) % G.gy),
-                Z = static_cast<int>(s / (static_cast<long long>(G.gx) * G.gy));
-      if (X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1)
-        x[n * G.isz + rem] = 0.0;
-    }
+  // grid: (X*Y blocks, Z, interval * slot * component); only boundary nodes are written
+  const int xy = blockIdx.x * 128 + threadIdx.x;
+  if (xy >= G.gx * G.gy)
+    return;
+  const int X = xy % G.gx, Y = xy / G.gx, Z = blockIdx.y;
+  if (!(X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1))
+    return;
+  const int q = blockIdx.z, comp = q % 3, a = (q / 3) % G.S, n = q / (3 * G.S);
+  x[n * G.isz + a * G.mv + comp * G.nsc + (static_cast<long long>(Z) * G.gy + Y) * G.gx + X] = 0.0;
 }
 
 constexpr int kProjThreads = 512;
@@ -1817,10 +1815,10 @@ __global__ void __launch_bounds__(kTrX)
 sep1d_kernel(DevCsr A, int axis, const double *__restrict__ in, long long ism, long long isb, long long isc,
              double *__restrict__ out, long long osm, long long osb, long long osc, SepDims D, int S)
 {
-  const int X = blockIdx.x * kTrX + threadIdx.x;
-  if (X >= D.ox)
+  const int xy = blockIdx.x * kTrX + threadIdx.x;
+  if (xy >= D.ox * D.oy)
     return;
-  const int Y = blockIdx.y % D.oy, Z = blockIdx.y / D.oy;
+  const int X = xy % D.ox, Y = xy / D.ox, Z = blockIdx.y;
   const int q = blockIdx.z, comp = q % 3, b = (q / 3) % S, m = q / (3 * S);
   const double *ib = in + m * ism + b * isb + comp * isc;
   const int r = axis == 0 ? X : (axis == 1 ? Y : Z);
@@ -1841,10 +1839,10 @@ __global__ void __launch_bounds__(kTrX)
 sep_prolong_x_kernel(DevTransfer3 T, const double *__restrict__ T2, double *__restrict__ fine, int gxc)
 {
   const DevGeom3 &F = T.f, &Cg = T.c;
-  const int X = blockIdx.x * kTrX + threadIdx.x;
-  if (X >= F.gx)
+  const int xy = blockIdx.x * kTrX + threadIdx.x;
+  if (xy >= F.gx * F.gy)
     return;
-  const int Y = blockIdx.y % F.gy, Z = blockIdx.y / F.gy;
+  const int X = xy % F.gx, Y = xy / F.gx, Z = blockIdx.y;
   const int q = blockIdx.z, comp = q % 3, a = (q / 3) % F.S, n = q / (3 * F.S);
   const int m = T.h_time ? n / 2 : n, half = T.h_time ? (n & 1) : 0;
   const double *E = T.E + half * kMaxS * kMaxS + a * kMaxS;
@@ -1867,10 +1865,10 @@ __global__ void __launch_bounds__(kTrX)
 sep_restrict_x_kernel(DevTransfer3 T, const double *__restrict__ fine, double *__restrict__ T1)
 {
   const DevGeom3 &F = T.f, &Cg = T.c;
-  const int i = blockIdx.x * kTrX + threadIdx.x;
-  if (i >= Cg.gx)
+  const int xy = blockIdx.x * kTrX + threadIdx.x;
+  if (xy >= Cg.gx * F.gy)
     return;
-  const int Y = blockIdx.y % F.gy, Z = blockIdx.y / F.gy;
+  const int i = xy % Cg.gx, Y = xy / Cg.gx, Z = blockIdx.y;
   const int q = blockIdx.z, comp = q % 3, bs = (q / 3) % Cg.S, m = q / (3 * Cg.S);
   const long long row = (static_cast<long long>(Z) * F.gy + Y) * F.gx;
   const int nh = T.h_time ? 2 : 1;
@@ -1931,7 +1929,8 @@ launch_zero_constrained3(const DevGeom3 &G, double *x, int nI, cudaStream_t st)
   const long long total = static_cast<long long>(nI) * G.S * G.mv;
   if (total == 0)
     return cudaSuccess;
-  zero_constrained3_kernel<<<grid_for(total), 256, 0, st>>>(G, x, total);
+  const dim3 grid((G.gx * G.gy + 127) / 128, G.gz, nI * G.S * 3);
+  zero_constrained3_kernel<<<grid, 128, 0, st>>>(G, x);
   return cudaGetLastError();
 }
 
@@ -1967,12 +1966,12 @@ launch_prolongate3(const DevTransfer3 &T, const double *coarse, double *fine, in
       double *T1 = work, *T2 = work + static_cast<long long>(nc) * C.S * 3 * p2;
       const int nb = nc * C.S * 3;
       SepDims dz{C.gx, C.gy, C.gz, C.gx, C.gy, F.gz};
-      sep1d_kernel<<<dim3((C.gx + kTrX - 1) / kTrX, C.gy * F.gz, nb), kTrX, 0, st>>>(
+      sep1d_kernel<<<dim3((C.gx * C.gy + kTrX - 1) / kTrX, F.gz, nb), kTrX, 0, st>>>(
         T.pz, 2, coarse, C.isz, C.mv, C.nsc, T1, 3ll * C.S * p1, 3 * p1, p1, dz, C.S);
       SepDims dy{C.gx, C.gy, F.gz, C.gx, F.gy, F.gz};
-      sep1d_kernel<<<dim3((C.gx + kTrX - 1) / kTrX, F.gy * F.gz, nb), kTrX, 0, st>>>(
+      sep1d_kernel<<<dim3((C.gx * F.gy + kTrX - 1) / kTrX, F.gz, nb), kTrX, 0, st>>>(
         T.py, 1, T1, 3ll * C.S * p1, 3 * p1, p1, T2, 3ll * C.S * p2, 3 * p2, p2, dy, C.S);
-      sep_prolong_x_kernel<<<dim3((F.gx + kTrX - 1) / kTrX, F.gy * F.gz, nf * F.S * 3), kTrX, 0, st>>>(T, T2, fine,
+      sep_prolong_x_kernel<<<dim3((F.gx * F.gy + kTrX - 1) / kTrX, F.gz, nf * F.S * 3), kTrX, 0, st>>>(T, T2, fine,
                                                                                                       C.gx);
     }
   else
@@ -1998,12 +1997,12 @@ launch_restrict3(const DevTransfer3 &T, const double *fine, double *coarse, int 
       const long long p1 = static_cast<long long>(F.gz) * F.gy * C.gx, p2 = static_cast<long long>(F.gz) * C.gy * C.gx;
       double *T1 = work, *T2 = work + static_cast<long long>(nc) * C.S * 3 * p1;
       const int nb = nc * C.S * 3;
-      sep_restrict_x_kernel<<<dim3((C.gx + kTrX - 1) / kTrX, F.gy * F.gz, nb), kTrX, 0, st>>>(T, fine, T1);
+      sep_restrict_x_kernel<<<dim3((C.gx * F.gy + kTrX - 1) / kTrX, F.gz, nb), kTrX, 0, st>>>(T, fine, T1);
       SepDims dy{C.gx, F.gy, F.gz, C.gx, C.gy, F.gz};
-      sep1d_kernel<<<dim3((C.gx + kTrX - 1) / kTrX, C.gy * F.gz, nb), kTrX, 0, st>>>(
+      sep1d_kernel<<<dim3((C.gx * C.gy + kTrX - 1) / kTrX, F.gz, nb), kTrX, 0, st>>>(
         T.ry, 1, T1, 3ll * C.S * p1, 3 * p1, p1, T2, 3ll * C.S * p2, 3 * p2, p2, dy, C.S);
       SepDims dz{C.gx, C.gy, F.gz, C.gx, C.gy, C.gz};
-      sep1d_kernel<<<dim3((C.gx + kTrX - 1) / kTrX, C.gy * C.gz, nb), kTrX, 0, st>>>(
+      sep1d_kernel<<<dim3((C.gx * C.gy + kTrX - 1) / kTrX, C.gz, nb), kTrX, 0, st>>>(
         T.rz, 2, T2, 3ll * C.S * p2, 3 * p2, p2, coarse, C.isz, C.mv, C.nsc, dz, C.S);
     }
   else
