@@ -147,6 +147,9 @@ dmma_8x8x4(double (&d)[2], double a, double b)
 #ifndef STMG_SPLIT_MINB
 #define STMG_SPLIT_MINB 1
 #endif
+#ifndef STMG_V176_COLS
+#define STMG_V176_COLS 16
+#endif
 template <int KS, int ROWS = kDRows, int TPW = 1, int COLS = kDCols, int SPLIT = 1>
 __global__ void __launch_bounds__(ROWS / SPLIT / 8 / TPW * 32, SPLIT == 1 ? 1 : STMG_SPLIT_MINB)
 vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ items,
@@ -492,7 +495,7 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
           classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega, group);
       };
       if (rows == 176)
-        go(vanka_dmma_kernel<44, 176, 1, 16, 2>); // 2 CTAs x 88 rows, one 8-row tile per warp
+        go(vanka_dmma_kernel<44, 176, 1, STMG_V176_COLS, 2>); // 2 CTAs x 88 rows, one 8-row tile per warp
       else if (ks <= 8)
         go(vanka_dmma_kernel<8>);
       else if (ks <= 12)
