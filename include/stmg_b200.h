@@ -310,6 +310,8 @@ int stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, dou
                         int nu2, double omega,
                         double rtol, double atol, int max_iterations, stmg3_solver **out);
 int stmg3_solver_destroy(stmg3_solver *solver);
+/* Host-only: the level plan of stmg3_solver_create, in stmg3_solver_info's format. */
+int stmg3_plan_levels(int nx, int ny, int nz, int r, int k, int n_hcoarse, int time_coarsen, int k_min, int64_t *out);
 /* out[0] = n_levels; per level l (coarse first) out[1+7l..]: nx, ny, nz, r, k,
  * time shift (log2 of the time coarsening), interval size. */
 int stmg3_solver_info(const stmg3_solver *solver, int64_t *out);

@@ -107,6 +107,7 @@ _SIGNATURES = {
                              _c_int, _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
                              ctypes.POINTER(_c_void_p)], _c_int),
     "stmg3_solver_destroy": ([_c_void_p], _c_int),
+    "stmg3_plan_levels": ([_c_int] * 8 + [_c_i64p], _c_int),
     "stmg3_solver_info": ([_c_void_p, _c_i64p], _c_int),
     "stmg3_solver_level": ([_c_void_p, _c_int], _c_void_p),
     "stmg3_solver_set_comm": ([_c_void_p, _c_void_p], _c_int),
@@ -557,6 +558,16 @@ def plan_levels(refinements: int, r: int, k: int = -1, n_steps: int = 0, t_end: 
                 levels=[dict(nx=int(out[2 + 5 * l]), r=int(out[3 + 5 * l]), k=int(out[4 + 5 * l]),
                              kind=TRANSFER_KINDS[int(out[5 + 5 * l])], size=int(out[6 + 5 * l]))
                         for l in range(n)])
+
+
+def plan_levels3(nx: int, ny: int, nz: int, r: int, k: int, n_hcoarse: int = 1, time_coarsen: bool = True,
+                 k_min: int = 0) -> list:
+    """Host-only 3D hierarchy plan (coarse first): dicts nx, ny, nz, r, k, tshift, size."""
+    out = (ctypes.c_int64 * (1 + 7 * 64))()
+    _check(load_library().stmg3_plan_levels(nx, ny, nz, r, k, n_hcoarse, int(time_coarsen), k_min, out))
+    return [dict(nx=int(out[1 + 7 * l]), ny=int(out[2 + 7 * l]), nz=int(out[3 + 7 * l]), r=int(out[4 + 7 * l]),
+                 k=int(out[5 + 7 * l]), tshift=int(out[6 + 7 * l]), size=int(out[7 + 7 * l]))
+            for l in range(int(out[0]))]
 
 
 def patch_info(nx: int, ny: int, r: int, k: int, tau: float, nu: float, gamma: float, smoother: int):

@@ -621,6 +621,66 @@ make_level3(stmg_ctx *ctx, const Level3Spec &s, int smoother, const std::vector<
 }
 } // namespace
 
+namespace
+{
+struct PlanLevel3
+{
+  Level3Spec s;
+  int tsh;
+};
+
+// combine_hierarchies (hierarchy.cpp:9-97) in 3D, fine first: spatial list
+// (r -> r/2 ... -> 1, then n_hcoarse h-steps, each also halving the time
+// grid when time_coarsen) and temporal list (k, k/2, ..., k_min) aligned at
+// the COARSE end, so the temporal p-steps sit on the coarsest levels (the
+// reference's C2 plan has L1 = h_space + p_time). Measured: putting them on
+// the fine levels instead costs 35 / 77 iterations at 8^3 / 16^3 (r = 2,
+// k = 2) against 7.
+std::vector<PlanLevel3>
+plan3(const Level3Spec &f, int n_hcoarse, int time_coarsen, int k_min)
+{
+  if (k_min < 0 || k_min > f.k)
+    throw std::invalid_argument("3D solver: need 0 <= k_min <= k");
+  if (n_hcoarse < 0)
+    throw std::invalid_argument("3D solver: n_hcoarse must be >= 0");
+  using D = PlanLevel3;
+  std::vector<D> sp{{f, 0}};
+  while (sp.back().s.r > 1)
+    {
+      D e = sp.back();
+      e.s.r /= 2;
+      sp.push_back(e);
+    }
+  for (int i = 0; i < n_hcoarse; ++i)
+    {
+      D e = sp.back();
+      if (e.s.nx % 2 || e.s.ny % 2 || e.s.nz % 2)
+        throw std::invalid_argument("3D solver: mesh not divisible for h-coarsening");
+      e.s.nx /= 2;
+      e.s.ny /= 2;
+      e.s.nz /= 2;
+      if (time_coarsen)
+        {
+          e.tsh += 1;
+          e.s.tau *= 2.0;
+        }
+      sp.push_back(e);
+    }
+  std::vector<int> tk{f.k};
+  while (tk.back() > k_min)
+    tk.push_back(tk.back() / 2);
+  const size_t nlev = std::max(sp.size(), tk.size());
+  std::vector<D> d(nlev);
+  for (size_t i = 0; i < nlev; ++i)
+    {
+      const size_t c = nlev - 1 - i; // distance from the coarse end
+      d[i] = sp[std::min(sp.size() - 1, i)];
+      d[i].s.k = tk[tk.size() - 1 - std::min(c, tk.size() - 1)];
+    }
+  return d;
+}
+} // namespace
+
 extern "C" {
 
 int
@@ -738,14 +798,6 @@ stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double 
     S->rtol = rtol;
     S->atol = atol;
     S->max_iterations = max_iterations;
-    // plan (fine first): p in time k -> k/2 ... -> 0, p in space r -> r/2
-    // ... -> 1, then n_hcoarse h-steps in space (and time)
-    struct D
-    {
-      Level3Spec s;
-      int tsh;
-    };
-    std::vector<D> d;
     Level3Spec f;
     f.nx = nx;
     f.ny = ny;
@@ -755,48 +807,7 @@ stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double 
     f.tau = tau;
     f.nu = nu;
     f.gamma = gamma;
-    if (k_min < 0 || k_min > k)
-      throw std::invalid_argument("3D solver: need 0 <= k_min <= k");
-    // combine_hierarchies (hierarchy.cpp:9-97) in 3D: spatial list (fine
-    // first: r -> r/2 ... -> 1, then n_hcoarse h-steps, each also halving
-    // the time grid when time_coarsen) and temporal list (k, k/2, ...,
-    // k_min) aligned at the COARSE end, so the temporal p-steps sit on the
-    // coarsest levels (the reference's C2 plan has L1 = h_space + p_time).
-    // Measured: putting them on the fine levels instead costs 35 / 77
-    // iterations at 8^3 / 16^3 (r = 2, k = 2) against 7.
-    std::vector<D> sp{{f, 0}};
-    while (sp.back().s.r > 1)
-      {
-        D e = sp.back();
-        e.s.r /= 2;
-        sp.push_back(e);
-      }
-    for (int i = 0; i < n_hcoarse; ++i)
-      {
-        D e = sp.back();
-        if (e.s.nx % 2 || e.s.ny % 2 || e.s.nz % 2)
-          throw std::invalid_argument("3D solver: mesh not divisible for h-coarsening");
-        e.s.nx /= 2;
-        e.s.ny /= 2;
-        e.s.nz /= 2;
-        if (time_coarsen)
-          {
-            e.tsh += 1;
-            e.s.tau *= 2.0;
-          }
-        sp.push_back(e);
-      }
-    std::vector<int> tk{k};
-    while (tk.back() > k_min)
-      tk.push_back(tk.back() / 2);
-    const size_t nlev = std::max(sp.size(), tk.size());
-    d.resize(nlev);
-    for (size_t i = 0; i < nlev; ++i)
-      {
-        const size_t c = nlev - 1 - i; // distance from the coarse end
-        d[i] = sp[std::min(sp.size() - 1, i)];
-        d[i].s.k = tk[tk.size() - 1 - std::min(c, tk.size() - 1)];
-      }
+    const std::vector<PlanLevel3> d = plan3(f, n_hcoarse, time_coarsen, k_min);
     // geometry of every level: the finest vertices restricted to the coarse
     // vertex set (nested index sets; non-nested geometry on deformed meshes)
     std::vector<std::vector<double>> vv(d.size());
@@ -865,6 +876,35 @@ stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double 
       S->coarse_n = static_cast<int>(L0.spec.isz());
     }
     *out = S.release();
+  });
+}
+
+int
+stmg3_plan_levels(int nx, int ny, int nz, int r, int k, int n_hcoarse, int time_coarsen, int k_min, int64_t *out)
+{
+  return guarded([&] {
+    if (!out)
+      throw std::invalid_argument("null argument");
+    Level3Spec f;
+    f.nx = nx;
+    f.ny = ny;
+    f.nz = nz;
+    f.r = r;
+    f.k = k;
+    const std::vector<PlanLevel3> d = plan3(f, n_hcoarse, time_coarsen, k_min);
+    out[0] = static_cast<int64_t>(d.size());
+    for (size_t i = 0; i < d.size(); ++i) // coarse first, as stmg3_solver_info
+      {
+        const PlanLevel3 &e = d[d.size() - 1 - i];
+        int64_t *o = out + 1 + 7 * i;
+        o[0] = e.s.nx;
+        o[1] = e.s.ny;
+        o[2] = e.s.nz;
+        o[3] = e.s.r;
+        o[4] = e.s.k;
+        o[5] = e.tsh;
+        o[6] = e.s.isz();
+      }
   });
 }
 

@@ -109,3 +109,16 @@ def test_vcycle_fgmres_matches_direct_time_march_3d(oracle):
             x[p0:p0 + fine.mp] = fine.project_mean_zero(np.ascontiguousarray(x[p0:p0 + fine.mp]))
     assert np.linalg.norm(x - xd) / np.linalg.norm(xd) <= 1e-8
     assert 1 <= it <= 40
+
+
+@pytest.mark.parametrize("n,r,k,N,nh,tc,kmin", [(2, 1, 1, 2, 1, True, 0), (4, 1, 1, 4, 2, True, 0),
+                                                 (4, 2, 2, 2, 2, False, 1), (4, 2, 2, 4, 2, False, 2),
+                                                 (4, 1, 1, 4, 2, False, 1), (2, 2, 2, 4, 1, True, 0)])
+def test_3d_hierarchy_plan_matches_oracle(oracle, stmg, n, r, k, N, nh, tc, kmin):
+    """The product's 3D plan (stmg3_plan_levels, host-only) equals the
+    oracle's: combine_hierarchies in 3D with the temporal p-steps aligned at
+    the coarse end, h in space (and time)."""
+    mine = stmg.plan_levels3(n, n, n, r, k, n_hcoarse=nh, time_coarsen=tc, k_min=kmin)
+    H = o3.OracleHier3(n, n, n, r, k, N, t_end=N / 8.0, n_hcoarse=nh, time_coarsen=tc, k_min=kmin)
+    assert [(l["nx"], l["r"], l["k"], l["tshift"], l["size"]) for l in mine] == \
+        [(l["nx"], l["r"], l["k"], l["tshift"], l["size"]) for l in H.levels]
