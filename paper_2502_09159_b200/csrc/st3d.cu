@@ -1188,13 +1188,22 @@ vmult3_gemm_kernel(const Level3Consts P, const double *__restrict__ E, const dou
 #ifndef STMG_V3C_MINB
 #define STMG_V3C_MINB 4
 #endif
+// Doubles per cell slot: 12 x-fields of 27 + 36 pressure partials + 4 PM =
+// 364, padded to 379 (= 11 mod 16). A warp spans 3.5 cells; with this stride
+// the 64-bit accesses of the three line patterns (x pass 3t+o, y pass
+// i+9k+3j, z pass t+9k) need 1944 instead of 2268 modelled wavefronts per
+// block slot (365 = 13 mod 16); the ideal is 1134.
+#ifndef STMG_V3C_CELL
+#define STMG_V3C_CELL 379
+#endif
 template <int S, int MODE>
 __global__ void __launch_bounds__(144, STMG_V3C_MINB)
 vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
                double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
   constexpr int N = 3, NN = 9, NNN = 27, p = 2, NP = 4, CB = 16;
-  constexpr int CELL = 12 * NNN + NP * NN + NP + 1; // 365 (odd): the y groups overwrite x fields 0..8 in place
+  constexpr int CELL = STMG_V3C_CELL; // the y groups overwrite x fields 0..8 in place
+  static_assert(CELL >= 12 * NNN + NP * NN + NP, "cell slot too small");
   extern __shared__ __align__(16) double smc[];
   double *const tab = smc + CB * CELL; // lm[2][3], lc[2][3]
   if (threadIdx.x < 6)
@@ -1519,7 +1528,7 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
     if (P.verts == nullptr && std::getenv("STMG_V3_QUAD") == nullptr)
       {
         constexpr int CB = 16;
-        const size_t smem = sizeof(double) * (CB * (12 * 27 + 4 * 9 + 4 + 1) + 12);
+        const size_t smem = sizeof(double) * (CB * STMG_V3C_CELL + 12);
         const unsigned grid = static_cast<unsigned>((cells + CB - 1) / CB);
         auto gc = [&](auto init, auto kern) {
           init<<<igrid, 128, 0, st>>>(G, x, b, y, total_v);
