@@ -15,6 +15,7 @@
 //  * Scatter: patches are coloured (2x2 colours for cells, 3x3 for vertex
 //    stars) so that one launch never touches a dof twice: read-modify-write
 //    of u with no atomics, deterministic results.
+#include <cstdlib>
 #include "kernels.hpp"
 
 #include <cuda_runtime.h>
@@ -476,7 +477,8 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
 {
   if (n_batches == 0 || n_intervals == 0)
     return cudaSuccess;
-  if (max_nt <= 176)
+  static const bool force_big = std::getenv("STMG_VANKA_BIG") != nullptr; // A/B switch for 128 < n_T <= 176
+  if (max_nt <= 176 && !(force_big && max_nt > kDRows && !item_ptr))
     {
       // 128 rows (16 warps) for 2D patches; 176 rows (22 warps) for 3D Q2 cells (n_T = 170)
       const int rows = max_nt <= kDRows ? kDRows : 176;
