@@ -1899,12 +1899,6 @@ sep_restrict_x_kernel(DevTransfer3 T, const double *__restrict__ fine, double *_
   T1[((static_cast<long long>(m) * Cg.S + bs) * 3 + comp) * plane + (static_cast<long long>(Z) * F.gy + Y) * Cg.gx + i] =
     v;
 }
-
-int
-grid_for(long long total)
-{
-  return static_cast<int>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 148 * 32)));
-}
 } // namespace
 
 bool
