@@ -1188,13 +1188,23 @@ vmult3_gemm_kernel(const Level3Consts P, const double *__restrict__ E, const dou
 #ifndef STMG_V3C_MINB
 #define STMG_V3C_MINB 4
 #endif
-// Doubles per cell slot: 12 x-fields of 27 + 36 pressure partials + 4 PM =
-// 364, padded to 379 (= 11 mod 16). A warp spans 3.5 cells; with this stride
-// the 64-bit accesses of the three line patterns (x pass 3t+o, y pass
-// i+9k+3j, z pass t+9k) need 1944 instead of 2268 modelled wavefronts per
-// block slot (365 = 13 mod 16); the ideal is 1134.
+// Thread map: cell-minor (thread = t * 16 + cell), so a half-warp holds the
+// same line t of 16 cells. With an odd cell stride its 64-bit shared-memory
+// accesses hit 16 distinct bank pairs in every phase (conflict-free), and
+// its global loads / scatters walk 16 neighbouring cells along x. The
+// cell-major map (thread = cell * 9 + t, STMG_V3C_CELLMINOR=0) spans 3.5
+// cells per warp; padding its slot from 365 to 379 doubles (= 11 mod 16)
+// takes a bank model of the three line patterns from 2268 to 1944
+// wavefronts per block slot (ideal 1134).
+#ifndef STMG_V3C_CELLMINOR
+#define STMG_V3C_CELLMINOR 1
+#endif
 #ifndef STMG_V3C_CELL
+#if STMG_V3C_CELLMINOR
+#define STMG_V3C_CELL 365 // 12 x 27 x-fields + 36 pressure partials + 4 PM, made odd
+#else
 #define STMG_V3C_CELL 379
+#endif
 #endif
 template <int S, int MODE>
 __global__ void __launch_bounds__(144, STMG_V3C_MINB)
@@ -1211,7 +1221,11 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
       tab[threadIdx.x] = P.lm[threadIdx.x];
       tab[6 + threadIdx.x] = P.lc[threadIdx.x];
     }
+#if STMG_V3C_CELLMINOR
+  const int t = threadIdx.x / CB, cl = threadIdx.x % CB;
+#else
   const int t = threadIdx.x % NN, cl = threadIdx.x / NN;
+#endif
   const long long gc = static_cast<long long>(blockIdx.x) * CB + cl;
   const bool active = gc < n_cells_total;
   const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
