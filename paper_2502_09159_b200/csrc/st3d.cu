@@ -59,6 +59,9 @@ struct V3
 #ifndef STMG_V3_MAP1_MINB
 #define STMG_V3_MAP1_MINB 3
 #endif
+#ifndef STMG_V3_MAP1_CELLMINOR
+#define STMG_V3_MAP1_CELLMINOR 1
+#endif
 // Forward 1D contraction of a line: o[q] = sum_m M(q, m) in[m] (M = phi /
 // dphi, constant bank, compile-time indices).
 #define V3_FWD(M, in, o)                                                                                             \
@@ -99,8 +102,14 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
         txq[q] = P.xq[q];
       }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if STMG_V3_MAP1_CELLMINOR
+  // MAP 1 cell-minor: a half-warp = one line of CW cells (conflict-free, as MAP 0), fewer registers per thread
+  const int cl = MAP == 0 ? lane % CW : static_cast<int>(threadIdx.x) % CW;             // cell in block
+  const int t = MAP == 0 ? warp * C::LPW + lane / CW : static_cast<int>(threadIdx.x) / CW; // line index
+#else
   const int cl = MAP == 0 ? lane % CW : static_cast<int>(threadIdx.x) / NN;             // cell in block
   const int t = MAP == 0 ? warp * C::LPW + lane / CW : static_cast<int>(threadIdx.x) % NN; // line index
+#endif
   const long long gc = static_cast<long long>(blockIdx.x) * CW + cl;
   const bool active = gc < n_cells_total && t < NN;
   const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
