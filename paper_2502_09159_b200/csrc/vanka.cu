@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include "kernels.hpp"
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace stmg_b200
@@ -151,6 +152,13 @@ dmma_8x8x4(double (&d)[2], double a, double b)
 #ifndef STMG_V176_COLS
 #define STMG_V176_COLS 16
 #endif
+// 176-row split, opt-in: the 2 CTAs of a row split form a cluster and each
+// gathers half of the R rows into both CTAs' tiles (distributed shared
+// memory). No spills, but the two cluster barriers per tile cost more than
+// the halved gather saves (C3: 10.8 vs 13.1 TF/s), so it is off.
+#ifndef STMG_V176_CLUSTER
+#define STMG_V176_CLUSTER 0
+#endif
 template <int KS, int ROWS = kDRows, int TPW = 1, int COLS = kDCols, int SPLIT = 1>
 __global__ void __launch_bounds__(ROWS / SPLIT / 8 / TPW * 32, SPLIT == 1 ? 1 : STMG_SPLIT_MINB)
 vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ items,
@@ -163,12 +171,24 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
   // contraction dimension); warp w owns the TPW 8-row tiles w + j * NW
   constexpr int kDCols = COLS;
   constexpr int OROWS = ROWS / SPLIT;
-  constexpr int kDRows = ROWS, kDThreads = OROWS / 8 / TPW * 32, kDPer = kDRows * kDCols / kDThreads;
+  constexpr bool CL = SPLIT > 1 && STMG_V176_CLUSTER; // cluster of the SPLIT CTAs shares the R gather
+  constexpr int kDRows = ROWS, kDThreads = OROWS / 8 / TPW * 32;
+  constexpr int kDPer = (CL ? OROWS : kDRows) * kDCols / kDThreads; // R rows gathered per thread
   constexpr int kDPerS = OROWS * kDCols / kDThreads;
   constexpr int NW = kDThreads / 32;
   const int row0 = SPLIT > 1 ? static_cast<int>(blockIdx.z) * OROWS : 0;
   extern __shared__ __align__(16) double dsm[];
   double *Rs = dsm;                                                 // kDRows x kDRLd
+  double *Rp = Rs; // the peer CTA's tile (CL)
+  if constexpr (CL)
+    Rp = cooperative_groups::this_cluster().map_shared_rank(Rs, static_cast<int>(blockIdx.z) ^ 1);
+  const int grow0 = CL ? row0 : 0; // first R row this CTA gathers
+  auto bar = [&]() {
+    if constexpr (CL)
+      cooperative_groups::this_cluster().sync();
+    else
+      __syncthreads();
+  };
   double *Zs = Rs + kDRows * kDRLd;                                 // OROWS x kDZLd
   double *w_s = Zs + OROWS * kDZLd;                                 // OROWS
   long long *cb = reinterpret_cast<long long *>(w_s + OROWS);      // [3][2][kDCols] column bases
@@ -213,7 +233,7 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
 #pragma unroll
           for (int q = 0; q < kDPer; ++q)
             {
-              const int i = ibase + q * (kDThreads / kDCols);
+              const int i = grow0 + ibase + q * (kDThreads / kDCols);
               validq[q] = i < nt;
               velq[q] = i < nvel;
               relq[q] = i < nt ? pc.rel[i] : 0;
@@ -262,9 +282,14 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           }
 #pragma unroll
         for (int q = 0; q < kDPer; ++q)
-          Rs[(ibase + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
+          {
+            const int i = (grow0 + ibase + q * (kDThreads / kDCols)) * kDRLd + c;
+            Rs[i] = g[q];
+            if constexpr (CL)
+              Rp[i] = g[q];
+          }
       }
-      __syncthreads();
+      bar();
 
       for (int t = 0; t < ntiles; ++t)
         {
@@ -318,7 +343,7 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
                   }
               }
           column_bases(t + 2);
-          __syncthreads();
+          bar(); // CL: the peer's MMAs are done with its tile before this CTA writes into it
 #pragma unroll
           for (int q = 0; q < kDPerS; ++q)
             {
@@ -329,8 +354,13 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           if (t + 1 < ntiles)
 #pragma unroll
             for (int q = 0; q < kDPer; ++q)
-              Rs[(ibase + q * (kDThreads / kDCols)) * kDRLd + c] = g[q];
-          __syncthreads();
+              {
+                const int i = (grow0 + ibase + q * (kDThreads / kDCols)) * kDRLd + c;
+                Rs[i] = g[q];
+                if constexpr (CL)
+                  Rp[i] = g[q];
+              }
+          bar();
         }
     }
 }
@@ -493,8 +523,26 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       const int ks = (max_nt + 3) / 4;
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem));
-        kern<<<grid, rows == 176 ? 352 : rows * 4, dsmem, stream>>>(
-          classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega, group);
+        if (rows == 176 && STMG_V176_CLUSTER)
+          {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3(352);
+            cfg.dynamicSmemBytes = dsmem;
+            cfg.stream = stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 1;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 2;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, kern, classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz,
+                               n_intervals, omega, group);
+          }
+        else
+          kern<<<grid, rows == 176 ? 352 : rows * 4, dsmem, stream>>>(
+            classes, batches, item_ptr, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega, group);
       };
       if (rows == 176)
         go(vanka_dmma_kernel<44, 176, 1, STMG_V176_COLS, 2>); // 2 CTAs x 88 rows, one 8-row tile per warp
