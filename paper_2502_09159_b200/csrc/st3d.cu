@@ -1205,6 +1205,9 @@ vmult3_gemm_kernel(const Level3Consts P, const double *__restrict__ E, const dou
 // cells per warp; padding its slot from 365 to 379 doubles (= 11 mod 16)
 // takes a bank model of the three line patterns from 2268 to 1944
 // wavefronts per block slot (ideal 1134).
+#ifndef STMG_V3C_CB
+#define STMG_V3C_CB 16 // cells per block (9 threads each); 12 or 14 cells with 6 / 5 blocks per SM spill
+#endif
 #ifndef STMG_V3C_CELLMINOR
 #define STMG_V3C_CELLMINOR 1
 #endif
@@ -1216,11 +1219,11 @@ vmult3_gemm_kernel(const Level3Consts P, const double *__restrict__ E, const dou
 #endif
 #endif
 template <int S, int MODE>
-__global__ void __launch_bounds__(144, STMG_V3C_MINB)
+__global__ void __launch_bounds__(9 * STMG_V3C_CB, STMG_V3C_MINB)
 vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
                double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
 {
-  constexpr int N = 3, NN = 9, NNN = 27, p = 2, NP = 4, CB = 16;
+  constexpr int N = 3, NN = 9, NNN = 27, p = 2, NP = 4, CB = STMG_V3C_CB;
   constexpr int CELL = STMG_V3C_CELL; // the y groups overwrite x fields 0..8 in place
   static_assert(CELL >= 12 * NNN + NP * NN + NP, "cell slot too small");
   extern __shared__ __align__(16) double smc[];
@@ -1550,13 +1553,13 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
   if constexpr (R == 1)
     if (P.verts == nullptr && std::getenv("STMG_V3_QUAD") == nullptr)
       {
-        constexpr int CB = 16;
+        constexpr int CB = STMG_V3C_CB;
         const size_t smem = sizeof(double) * (CB * STMG_V3C_CELL + 12);
         const unsigned grid = static_cast<unsigned>((cells + CB - 1) / CB);
         auto gc = [&](auto init, auto kern) {
           init<<<igrid, 128, 0, st>>>(G, x, b, y, total_v);
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-          kern<<<grid, 144, smem, st>>>(P, x, b, y, xprev0, coupled, cells);
+          kern<<<grid, 9 * CB, smem, st>>>(P, x, b, y, xprev0, coupled, cells);
         };
         switch (mode)
           {
