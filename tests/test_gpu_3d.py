@@ -32,6 +32,10 @@ CASES = [  # nx, ny, nz, r, k, gamma, amp
     (3, 2, 2, 2, 1, 0.0, 0.0),
     (3, 3, 2, 1, 1, 1.0, 0.1),
     (2, 2, 3, 2, 2, 1.0, 0.1),
+    # several 16-cell blocks with a ragged last one, blocks straddling
+    # intervals (cell-minor thread maps of the r = 1 kernels)
+    (5, 4, 3, 1, 1, 1.0, 0.0),
+    (4, 3, 3, 1, 2, 0.5, 0.1),
 ]
 
 
