@@ -278,6 +278,15 @@ def c4_step_leg(stmg, ctx, torch, n_int=8, reps=5):
     return out
 
 
+def vmult3c_fma_per_cell_slot(S, coupled=True):
+    """FMAs of vmult3c_kernel (st3d.cu) per cell and output slot, counted from
+    the kernel: x pass (temporal combination 3*3*(2S+1), x contraction 3*3*12,
+    pressure partials 4*3*4), y pass (3*3*18), z pass (3*3*(9+4)), per line
+    thread x 9 lines, plus the cell's pressure moments (4*S)."""
+    per_line = 3 * 3 * (2 * S + (1 if coupled else 0)) + 108 + 48 + 162 + 117
+    return 9 * per_line + 4 * S
+
+
 def three_d_leg(torch, stmg):
     """BASELINE configs[2] (C3: 32^3 Q2/P1disc, DG(1), 64 intervals: vmult,
     cell-Vanka step, full all-at-once FGMRES + hp-STMG solve) and configs[4]
@@ -288,6 +297,18 @@ def three_d_leg(torch, stmg):
     a = argparse.Namespace(reps=5, c3_cells=32, c3_intervals=64, c3_hcoarse=3, c3_variant="robust", maxit=200,
                            no_solve=False, c5_cells=32, c5_intervals=128, c5_slab=16, c5_variant="robust")
     out = {"C3": bench3d.run_c3(torch, stmg, a)}
+    c3 = out["C3"]
+    hbm, fp64, dmma, src = peaks()
+    cells, S, nI = a.c3_cells ** 3, 2, a.c3_intervals
+    flops = 2.0 * vmult3c_fma_per_cell_slot(S) * cells * S * nI
+    byts = 16.0 * c3["dofs"]
+    c3["vmult_roofline"] = {
+        "kernel": "vmult3c_kernel (C3 vmult, 1D-factor form)", "bound": "fp64",
+        "flops_per_launch": flops, "algorithmic_bytes": byts,
+        "achieved_TFLOPs": flops / (c3["vmult_ms"] * 1e-3) / 1e12,
+        "fp64_frac": flops / (c3["vmult_ms"] * 1e-3) / 1e12 / fp64,
+        "hbm_frac": byts / (c3["vmult_ms"] * 1e-3) / 1e9 / hbm, "peak_source": src}
+    c3["vanka_dmma_frac"] = c3["vanka_update_TFLOPs"] / dmma
     torch.cuda.empty_cache()
     out["C5"] = bench3d.run_c5(torch, stmg, a)
     torch.cuda.empty_cache()
