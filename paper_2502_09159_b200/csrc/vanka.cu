@@ -516,7 +516,9 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       const size_t dsmem = sizeof(double) * (rows * kDRLd + orows * kDZLd + orows) + sizeof(long long) * 6 * kDCols;
       // intervals per block: 16, fewer on small levels so the launch still
       // fills the GPU (a coarse level has only a few batches per colour)
-      int group = kDGroup;
+      // intervals per block: 16 for 2D patches, 4 for the 176-row split (C3: more, shorter blocks balance better)
+      static const int genv = std::getenv("STMG_VGROUP") ? std::atoi(std::getenv("STMG_VGROUP")) : 0;
+      int group = genv > 0 ? genv : (rows == 176 ? 4 : kDGroup);
       while (group > 1 && static_cast<long long>(n_batches) * split * ((n_intervals + group - 1) / group) < 2 * 148)
         group /= 2;
       dim3 grid(n_batches, (n_intervals + group - 1) / group, split);
@@ -567,7 +569,8 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       const int ks = (max_nt + 3) / 4;
       const size_t smem = sizeof(double) * (4 * ks * kBLd) + sizeof(long long) * 2 * kBCols;
       const int tpw = ((max_nt + 7) / 8 + 15) / 16;
-      int group = kBGroup;
+      static const int benv = std::getenv("STMG_BGROUP") ? std::atoi(std::getenv("STMG_BGROUP")) : 0;
+      int group = benv > 0 ? benv : kBGroup;
       while (group > 1 && static_cast<long long>(n_batches) * ((n_intervals + group - 1) / group) < 2 * 148)
         group /= 2;
       dim3 grid(n_batches, (n_intervals + group - 1) / group);
