@@ -132,63 +132,105 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- reference arm
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+def host_cpu():
+    """Host core count as the box reports it (lscpu), for the baselines."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k] = v
+        if "Socket(s)" in info and "Core(s) per socket" in info:
+            info["physical_cores"] = int(info["Socket(s)"]) * int(info["Core(s) per socket"])
+    except Exception:
+        pass
+    return info
+
+
+def cpu_sample():
+    """The one bounded CPU sample both arms time: the C2 discretisation (Q3/P2disc,
+    DG(2), nu = gamma = 1, tau = 1/64) on 64^2 cells, one interval per host
+    thread (the oracle parallelises over intervals with OpenMP, so every
+    thread has an interval), vmult + cell-Vanka step per step."""
+    threads = os.cpu_count() or 1
+    return {"nc": 64, "n_int": max(threads, 1), "threads": threads}
+
+
+def time_oracle(threads, n_int, steps, warmup, nc=64):
+    """DoF/s of the oracle (C++ restatement of the reference, -O3) on one step
+    = all-at-once vmult + one Vanka smoother step over n_int intervals."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_ctypes as oc
 
-    threads = os.cpu_count() or 1
-    nc, n_int = 64, 8  # bounded sample of the C2 discretisation
     lvl = oc.OracleLevel(nc, CONFIG["r"], CONFIG["k"], 1.0 / 64, CONFIG["nu"], CONFIG["gamma"], 0)
     dofs = n_int * lvl.size
     x = oc.seeded(dofs, 1)
     b = oc.seeded(dofs, 2)
     halo = oc.seeded(lvl.n_velocity, 3)
     u = x.copy()
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         lvl.vmult_all(x, n_int, halo, threads)
         u = lvl.smooth_step_all(b, u, CONFIG["omega"], n_int, halo, threads)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(steps):
         lvl.vmult_all(x, n_int, halo, threads)
         u = lvl.smooth_step_all(b, u, CONFIG["omega"], n_int, halo, threads)
-    dt = (time.perf_counter() - t0) / args.steps
-    value = dofs / dt
-    sample = (f"oracle port of the reference (C++ restatement, OpenMP over intervals) on {nc}x{nc} cells, "
-              f"r=2, k=2, {n_int} intervals ({dofs} dofs) per step; per-dof rate of the C2 workload")
+    dt = (time.perf_counter() - t0) / steps
+    return dofs / dt, dt, dofs
+
+
+def _sample_text(smp, threads, n_int, steps):
+    return (f"oracle port of the reference (C++ restatement, -O3, OpenMP over intervals) on {smp['nc']}x{smp['nc']} "
+            f"cells, r=2, k=2, tau=1/64, {n_int} intervals, {threads} thread(s) busy, vmult + Vanka step, "
+            f"{steps} timed steps; per-dof rate of the C2 workload (intervals are independent work)")
+
+
+def arm_config(world, dofs_per_gpu=None, nx=256, N=64):
+    """The workload config, identical in both arms."""
+    return dict(CONFIG, mesh=f"{nx}x{nx}", intervals_per_gpu=N,
+                dofs_per_gpu=dofs_per_gpu if dofs_per_gpu is not None else N * c2_interval_size(nx),
+                parallelism=f"time-slab dp{world}" if world > 1 else "single GPU",
+                l2="inputs 2.4 GB per vector >> 126 MB L2 (no flush needed)")
+
+
+def c2_interval_size(nx, r=2, k=2):
+    g = nx * (r + 1) + 1
+    return (k + 1) * (2 * g * g + nx * nx * (r + 1) * (r + 2) // 2)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    smp = cpu_sample()
+    threads, n_int = smp["threads"], smp["n_int"]
+    value, dt, dofs = time_oracle(threads, n_int, args.steps, args.warmup, smp["nc"])
+    one, _, _ = time_oracle(1, 1, 2, 1, smp["nc"])
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1])",
-            "config": dict(CONFIG, workload=CONFIG["workload"] + " (CPU sample)"),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "config": arm_config(args.gpus, nx=args.nx, N=args.intervals),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(threads, n_int), "kind": "port",
+                             "sample": _sample_text(smp, min(threads, n_int), n_int, args.steps)},
+            "cpu_baseline_1core": {"value": one, "unit": UNIT, "cores": 1, "kind": "port",
+                                   "sample": _sample_text(smp, 1, 1, 2)},
+            "host": host_cpu(),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_quick():
-    """Bounded oracle sample for the cpu_baseline field of our own line."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_ctypes as oc
-
-    threads = os.cpu_count() or 1
-    nc, n_int = 32, 8
-    lvl = oc.OracleLevel(nc, CONFIG["r"], CONFIG["k"], 1.0 / 64, CONFIG["nu"], CONFIG["gamma"], 0)
-    dofs = n_int * lvl.size
-    x, b = oc.seeded(dofs, 1), oc.seeded(dofs, 2)
-    halo = oc.seeded(lvl.n_velocity, 3)
-    lvl.vmult_all(x, n_int, halo, threads)
-    t0 = time.perf_counter()
-    reps = 2
-    u = x
-    for _ in range(reps):
-        lvl.vmult_all(x, n_int, halo, threads)
-        u = lvl.smooth_step_all(b, u, CONFIG["omega"], n_int, halo, threads)
-    dt = (time.perf_counter() - t0) / reps
-    return {"value": dofs / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle (C++ restatement of the reference) on {nc}x{nc} cells, r=2, k=2, {n_int} intervals, "
-                      f"vmult + Vanka step, OpenMP over intervals, {reps} steps"}
+    """The reference arm's sample (same mesh, intervals and threads), fewer
+    steps, for the cpu_baseline field of our own line; plus the 1-core rate."""
+    smp = cpu_sample()
+    threads, n_int = smp["threads"], smp["n_int"]
+    value, _, _ = time_oracle(threads, n_int, 2, 1, smp["nc"])
+    one, _, _ = time_oracle(1, 1, 2, 1, smp["nc"])
+    return ({"value": value, "unit": UNIT, "cores": min(threads, n_int), "kind": "port",
+             "sample": _sample_text(smp, min(threads, n_int), n_int, 2)},
+            {"value": one, "unit": UNIT, "cores": 1, "kind": "port", "sample": _sample_text(smp, 1, 1, 2)})
 
 
 def _consistent_rhs(torch, sol, n_steps, seed):
@@ -440,7 +482,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nx", type=int, default=256)
     ap.add_argument("--intervals", type=int, default=64)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     args = ap.parse_args()
@@ -559,7 +601,8 @@ def main():
         hh.zero_()
         nx_, nb_, nu_, ny_, nh_ = hx.numpy(), hb.numpy(), hu.numpy(), hy.numpy(), hh.numpy()
         halo_arg = nh_ if rank > 0 else None
-        lvl.vmult_host(nx_, ny_, N, halo_arg)
+        lvl.vmult_host(nx_, ny_, N, halo_arg)  # warm-up of both entry points (pinned staging, streams)
+        lvl.smooth_step_host(nb_, nu_, CONFIG["omega"], N, halo_arg, True)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -636,9 +679,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1], torch Philox on device)",
-            "config": dict(CONFIG, mesh=f"{nx}x{nx}", intervals_per_gpu=N, dofs_per_gpu=dofs,
-                           parallelism=f"time-slab dp{world}" if world > 1 else "single GPU",
-                           l2="inputs 2.4 GB per vector >> 126 MB L2 (no flush needed)"),
+            "config": arm_config(world, dofs, nx, N),
             "components": {"vmult_dofs_per_s": world * dofs / (vm_ms * 1e-3),
                            "vanka_step_dofs_per_s": world * dofs / ((rs_ms + vk_ms) * 1e-3)},
             "kernels": kernels, "roofline": roof, "gpu_launches": gpu_launches,
@@ -658,7 +699,8 @@ def main():
             line["3D"] = side(lambda: three_d_leg(torch, stmg))
     if not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline_quick()
+            line["cpu_baseline"], line["cpu_baseline_1core"] = cpu_baseline_quick()
+            line["host"] = host_cpu()
         except Exception as exc:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {exc}"}

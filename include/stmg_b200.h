@@ -50,6 +50,14 @@ const char *stmg_last_error(void);
 /* Library version string, e.g. "stmg_b200 0.1 sm_100a". */
 const char *stmg_version(void);
 
+/* Tuning hooks (process-wide; 0 restores the default heuristic). No
+ * reference counterpart: they fix launch shapes the library otherwise derives
+ * from the level size, so tests can reach every packing of the kernels.
+ *   "vanka_group"     intervals per block of the DMMA item kernels (n_T <= 176)
+ *   "vanka_big_group" intervals per block of the big-patch kernel (n_T > 176)
+ * Unknown keys or values outside [0, 1024]: STMG_EINVAL. */
+int stmg_set_tuning(const char *key, int64_t value);
+
 /* ------------------------------------------------------------ context */
 int stmg_ctx_create(int device, stmg_ctx **out);
 int stmg_ctx_destroy(stmg_ctx *ctx);

@@ -46,6 +46,7 @@ _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _SIGNATURES = {
     "stmg_last_error": ([], ctypes.c_char_p),
     "stmg_version": ([], ctypes.c_char_p),
+    "stmg_set_tuning": ([ctypes.c_char_p, ctypes.c_int64], _c_int),
     "stmg_ctx_create": ([_c_int, ctypes.POINTER(_c_void_p)], _c_int),
     "stmg_ctx_destroy": ([_c_void_p], _c_int),
     "stmg_ctx_set_stream": ([_c_void_p, _c_void_p], _c_int),
@@ -144,21 +145,35 @@ def _check(code: int) -> None:
         raise StmgError(code, load_library().stmg_last_error().decode())
 
 
-def _ptr(t) -> Optional[int]:
-    """Device pointer of a contiguous float64 CUDA tensor (None passes NULL)."""
+def _ptr(t, numel: Optional[int] = None, device: Optional[int] = None, name: str = "tensor") -> Optional[int]:
+    """Device pointer of a contiguous float64 CUDA tensor (None passes NULL).
+
+    ``numel``: minimum element count the C ABI will touch; ``device``: the
+    context's CUDA device. A shorter, mistyped or foreign-device tensor raises
+    instead of letting the kernels read or write past it."""
     if t is None:
         return None
-    if not t.is_cuda or t.dtype.itemsize != 8 or not t.is_contiguous():
-        raise ValueError("stmg_b200 expects contiguous float64 CUDA tensors")
+    import torch
+
+    if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError(f"stmg_b200: {name} must be a contiguous float64 CUDA tensor")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"stmg_b200: {name} lives on cuda:{t.device.index}, the context on cuda:{device}")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"stmg_b200: {name} has {t.numel()} elements, the call needs {numel}")
     return t.data_ptr()
 
 
-def _hptr(a) -> Optional[int]:
+def _hptr(a, numel: Optional[int] = None, name: str = "array") -> Optional[int]:
     """Host pointer of a C-contiguous float64 numpy array (None passes NULL)."""
     if a is None:
         return None
-    if a.dtype.itemsize != 8 or not a.flags["C_CONTIGUOUS"]:
-        raise ValueError("stmg_b200 expects C-contiguous float64 host arrays")
+    import numpy as np
+
+    if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"stmg_b200: {name} must be a C-contiguous float64 host array")
+    if numel is not None and a.size < numel:
+        raise ValueError(f"stmg_b200: {name} has {a.size} elements, the call needs {numel}")
     return a.ctypes.data
 
 
@@ -239,73 +254,94 @@ class Level:
         self.factored = bool(out[8])           # time-diagonalised Vanka inverses in use
         self.factored_matrix_elements = int(out[9])
 
+    # -- argument checks: every vector the C ABI touches is sized here
+    def _v(self, t, n: int, name: str):
+        return _ptr(t, n * self.size, self.ctx.device, name)
+
+    def _halo(self, t, name: str = "x_prev_slot"):
+        return _ptr(t, self.n_velocity, self.ctx.device, name)
+
+    def _hv(self, a, n: int, name: str):
+        return _hptr(a, n * self.size, name)
+
     # -- operator
     def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
-        _check(load_library().stmg_apply_block(self._h, _ptr(x), _ptr(y), n_intervals, int(raw)))
+        _check(load_library().stmg_apply_block(self._h, self._v(x, n_intervals, "x"), self._v(y, n_intervals, "y"),
+                                               n_intervals, int(raw)))
         return y
 
     def apply_block_raw(self, x, y, n_intervals: int = 1):
         return self.apply_block(x, y, n_intervals, raw=True)
 
     def vmult(self, x, y, n_intervals: int = 1, x_prev_slot=None):
-        _check(load_library().stmg_vmult(self._h, _ptr(x), _ptr(y), n_intervals, _ptr(x_prev_slot)))
+        _check(load_library().stmg_vmult(self._h, self._v(x, n_intervals, "x"), self._v(y, n_intervals, "y"),
+                                         n_intervals, self._halo(x_prev_slot)))
         return y
 
     def residual(self, b, x, r, n_intervals: int = 1, x_prev_slot=None, coupled: bool = True):
-        _check(load_library().stmg_residual(self._h, _ptr(b), _ptr(x), _ptr(r), n_intervals, _ptr(x_prev_slot),
+        _check(load_library().stmg_residual(self._h, self._v(b, n_intervals, "b"), self._v(x, n_intervals, "x"),
+                                            self._v(r, n_intervals, "r"), n_intervals, self._halo(x_prev_slot),
                                             int(coupled)))
         return r
 
     def step_health(self, X, n_intervals: int = 1):
         """Saddle-point health per interval (solver.cpp:286-299): [(max_divergence, max_pressure_mean), ...]."""
         out = (ctypes.c_double * (2 * n_intervals))()
-        _check(load_library().stmg_step_health(self._h, _ptr(X), n_intervals, out))
+        _check(load_library().stmg_step_health(self._h, self._v(X, n_intervals, "X"), n_intervals, out))
         return [(out[2 * i], out[2 * i + 1]) for i in range(n_intervals)]
 
     def coupling_rhs(self, v_prev, out):
-        _check(load_library().stmg_coupling_rhs(self._h, _ptr(v_prev), _ptr(out)))
+        _check(load_library().stmg_coupling_rhs(self._h, self._halo(v_prev, "v_prev"), self._v(out, 1, "out")))
         return out
 
     # -- smoother
     def apply_additive(self, residual, out, n_intervals: int = 1):
-        _check(load_library().stmg_apply_additive(self._h, _ptr(residual), _ptr(out), n_intervals))
+        _check(load_library().stmg_apply_additive(self._h, self._v(residual, n_intervals, "residual"),
+                                                  self._v(out, n_intervals, "out"), n_intervals))
         return out
 
     def smooth_step(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False,
                     work=None):
-        _check(load_library().stmg_smooth_step(self._h, _ptr(b), _ptr(u), omega, n_intervals, _ptr(x_prev_slot),
-                                               int(coupled), _ptr(work)))
+        _check(load_library().stmg_smooth_step(self._h, self._v(b, n_intervals, "b"), self._v(u, n_intervals, "u"),
+                                               omega, n_intervals, self._halo(x_prev_slot), int(coupled),
+                                               self._v(work, n_intervals, "work")))
         return u
 
     def vanka_update(self, residual, u, omega: float, n_intervals: int = 1):
-        _check(load_library().stmg_vanka_update(self._h, _ptr(residual), _ptr(u), omega, n_intervals))
+        _check(load_library().stmg_vanka_update(self._h, self._v(residual, n_intervals, "residual"),
+                                                self._v(u, n_intervals, "u"), omega, n_intervals))
         return u
 
     # -- host-buffer (end-to-end) variants
     def assemble_rhs(self, F, t_start: float = 0.0, n_intervals: int = 1, problem: int = PROBLEM_MANUFACTURED):
         """SpaceTimeBlockOperator::assemble_rhs of a built-in force for n_intervals intervals from t_start."""
-        _check(load_library().stmg_assemble_rhs(self._h, problem, t_start, _ptr(F), n_intervals))
+        _check(load_library().stmg_assemble_rhs(self._h, problem, t_start, self._v(F, n_intervals, "F"), n_intervals))
         return F
 
     def interpolate_exact(self, X, t_start: float = 0.0, n_intervals: int = 1, problem: int = PROBLEM_MANUFACTURED):
         """interpolate_exact (harness.cpp:185-239) of the built-in exact solution into X."""
-        _check(load_library().stmg_interpolate_exact(self._h, problem, t_start, _ptr(X), n_intervals))
+        _check(load_library().stmg_interpolate_exact(self._h, problem, t_start, self._v(X, n_intervals, "X"),
+                                                     n_intervals))
         return X
 
     def compute_errors(self, X, t_start: float = 0.0, n_intervals: int = 1,
                        problem: int = PROBLEM_MANUFACTURED) -> dict:
         """compute_errors (harness.cpp:72-183) of a trajectory against the built-in exact solution."""
         out = (ctypes.c_double * 5)()
-        _check(load_library().stmg_compute_errors(self._h, problem, t_start, _ptr(X), n_intervals, out))
+        _check(load_library().stmg_compute_errors(self._h, problem, t_start, self._v(X, n_intervals, "X"),
+                                                  n_intervals, out))
         return dict(e_v_l2=out[0], e_p_l2=out[1], e_v_h1=out[2], e_div=out[3], e_v_linf=out[4])
 
     def vmult_host(self, x, y, n_intervals: int = 1, x_prev_slot=None):
-        _check(load_library().stmg_vmult_host(self._h, _hptr(x), _hptr(y), n_intervals, _hptr(x_prev_slot)))
+        _check(load_library().stmg_vmult_host(self._h, self._hv(x, n_intervals, "x"), self._hv(y, n_intervals, "y"),
+                                              n_intervals, _hptr(x_prev_slot, self.n_velocity, "x_prev_slot")))
         return y
 
     def smooth_step_host(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False):
-        _check(load_library().stmg_smooth_step_host(self._h, _hptr(b), _hptr(u), omega, n_intervals,
-                                                    _hptr(x_prev_slot), int(coupled)))
+        _check(load_library().stmg_smooth_step_host(self._h, self._hv(b, n_intervals, "b"),
+                                                    self._hv(u, n_intervals, "u"), omega, n_intervals,
+                                                    _hptr(x_prev_slot, self.n_velocity, "x_prev_slot"),
+                                                    int(coupled)))
         return u
 
     def __del__(self):
@@ -338,49 +374,57 @@ class Solver:
         self.finest = self.levels[-1]
 
     def restrict_residual(self, l: int, fine, coarse, project_pressure: bool = True):
-        _check(load_library().stmg_restrict_residual(self._h, l, _ptr(fine), _ptr(coarse), int(project_pressure)))
+        _check(load_library().stmg_restrict_residual(self._h, l, self.levels[l]._v(fine, 1, "fine"),
+                                                     self.levels[l - 1]._v(coarse, 1, "coarse"), int(project_pressure)))
         return coarse
 
     def prolongate_correction(self, l: int, coarse, fine, project_pressure: bool = True, accumulate: bool = False):
-        _check(load_library().stmg_prolongate_correction(self._h, l, _ptr(coarse), _ptr(fine),
-                                                         int(project_pressure), int(accumulate)))
+        _check(load_library().stmg_prolongate_correction(self._h, l, self.levels[l - 1]._v(coarse, 1, "coarse"),
+                                                         self.levels[l]._v(fine, 1, "fine"), int(project_pressure),
+                                                         int(accumulate)))
         return fine
 
     def coarse_solve(self, b, x):
-        _check(load_library().stmg_coarse_solve(self._h, _ptr(b), _ptr(x)))
+        c = self.levels[0]
+        _check(load_library().stmg_coarse_solve(self._h, c._v(b, 1, "b"), c._v(x, 1, "x")))
         return x
 
     def vcycle(self, b, x):
-        _check(load_library().stmg_vcycle(self._h, _ptr(b), _ptr(x)))
+        _check(load_library().stmg_vcycle(self._h, self.finest._v(b, 1, "b"), self.finest._v(x, 1, "x")))
         return x
 
     def gmres(self, b, x, history_cap: int = 256):
         it = _c_int(0)
         hist = (ctypes.c_double * history_cap)()
-        code = load_library().stmg_gmres(self._h, _ptr(b), _ptr(x), ctypes.byref(it), hist, history_cap)
+        code = load_library().stmg_gmres(self._h, self.finest._v(b, 1, "b"), self.finest._v(x, 1, "x"),
+                                         ctypes.byref(it), hist, history_cap)
         _check(code)
         return int(it.value), [hist[i] for i in range(min(history_cap, it.value + 1))]
 
     def time_march(self, F, X):
         iters = (ctypes.c_int * self.n_steps)()
-        _check(load_library().stmg_time_march(self._h, _ptr(F), _ptr(X), iters))
+        f = self.finest
+        _check(load_library().stmg_time_march(self._h, f._v(F, self.n_steps, "F"), f._v(X, self.n_steps, "X"), iters))
         return [int(v) for v in iters]
 
     def time_march_problem(self, problem: int, X):
         """time_march of a built-in problem (PROBLEM_MANUFACTURED: force; PROBLEM_CAVITY: lifted lid data)."""
         iters = (ctypes.c_int * self.n_steps)()
-        _check(load_library().stmg_time_march_problem(self._h, problem, _ptr(X), iters))
+        _check(load_library().stmg_time_march_problem(self._h, problem, self.finest._v(X, self.n_steps, "X"), iters))
         return [int(v) for v in iters]
 
     def time_march_ex(self, X, F=None, lifts=None, v_init=None):
         """time_march with load vectors, per-step Dirichlet lift vectors and an initial velocity (all optional)."""
         iters = (ctypes.c_int * self.n_steps)()
-        _check(load_library().stmg_time_march_ex(self._h, _ptr(F), _ptr(lifts), _ptr(v_init), _ptr(X), iters))
+        f, n = self.finest, self.n_steps
+        _check(load_library().stmg_time_march_ex(self._h, f._v(F, n, "F"), f._v(lifts, n, "lifts"),
+                                                 f._halo(v_init, "v_init"), f._v(X, n, "X"), iters))
         return [int(v) for v in iters]
 
     def time_march_host(self, F, X):
         iters = (ctypes.c_int * self.n_steps)()
-        _check(load_library().stmg_time_march_host(self._h, _hptr(F), _hptr(X), iters))
+        f, n = self.finest, self.n_steps
+        _check(load_library().stmg_time_march_host(self._h, f._hv(F, n, "F"), f._hv(X, n, "X"), iters))
         return [int(v) for v in iters]
 
     def set_comm(self, comm) -> None:
@@ -403,15 +447,19 @@ class Solver:
 
     def vcycle_all_at_once(self, b, x, n_intervals: int):
         """One all-at-once V-cycle over n_intervals intervals (Eq. GloSys)."""
-        _check(load_library().stmg_vcycle_all_at_once(self._h, _ptr(b), _ptr(x), n_intervals))
+        f = self.finest
+        _check(load_library().stmg_vcycle_all_at_once(self._h, f._v(b, n_intervals, "b"), f._v(x, n_intervals, "x"),
+                                                      n_intervals))
         return x
 
     def solve_all_at_once(self, F, X, n_intervals: int, v_init=None, history_cap: int = 256):
         """FGMRES + all-at-once hp-STMG on a slab; returns (iterations, residual history)."""
         it = _c_int(0)
         hist = (ctypes.c_double * history_cap)()
-        _check(load_library().stmg_solve_all_at_once(self._h, _ptr(F), _ptr(X), n_intervals, _ptr(v_init),
-                                                      ctypes.byref(it), hist, history_cap))
+        f = self.finest
+        _check(load_library().stmg_solve_all_at_once(self._h, f._v(F, n_intervals, "F"), f._v(X, n_intervals, "X"),
+                                                      n_intervals, f._halo(v_init, "v_init"), ctypes.byref(it), hist,
+                                                      history_cap))
         return int(it.value), [hist[i] for i in range(min(history_cap, it.value + 1))]
 
     def __del__(self):
@@ -432,7 +480,8 @@ class Level3:
             self._h, self._owned = _borrowed, False
         else:
             h = _c_void_p()
-            _check(lib.stmg3_level_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, smoother, _hptr(vertices),
+            _check(lib.stmg3_level_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, smoother,
+                                          _hptr(vertices, 3 * (nx + 1) * (ny + 1) * (nz + 1), "vertices"),
                                           ctypes.byref(h)))
             self._h, self._owned = h, True
         out = (ctypes.c_int64 * 12)()
@@ -440,35 +489,47 @@ class Level3:
         (self.n_slots, self.n_velocity, self.n_pressure, self.size, self.n_scalar, self.gx, self.gy, self.gz,
          self.n_p, self.max_patch, self.n_patch_classes, self.total_matrix_elements) = [int(v) for v in out]
 
+    def _v(self, t, n: int, name: str):
+        return _ptr(t, n * self.size, self.ctx.device, name)
+
+    def _halo(self, t, name: str = "x_prev_slot"):
+        return _ptr(t, self.n_velocity, self.ctx.device, name)
+
     def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
-        _check(load_library().stmg3_apply_block(self._h, _ptr(x), _ptr(y), n_intervals, int(raw)))
+        _check(load_library().stmg3_apply_block(self._h, self._v(x, n_intervals, "x"), self._v(y, n_intervals, "y"),
+                                                n_intervals, int(raw)))
         return y
 
     def vmult(self, x, y, n_intervals: int = 1, x_prev_slot=None):
-        _check(load_library().stmg3_vmult(self._h, _ptr(x), _ptr(y), n_intervals, _ptr(x_prev_slot)))
+        _check(load_library().stmg3_vmult(self._h, self._v(x, n_intervals, "x"), self._v(y, n_intervals, "y"),
+                                          n_intervals, self._halo(x_prev_slot)))
         return y
 
     def residual(self, b, x, r, n_intervals: int = 1, x_prev_slot=None, coupled: bool = True):
-        _check(load_library().stmg3_residual(self._h, _ptr(b), _ptr(x), _ptr(r), n_intervals, _ptr(x_prev_slot),
+        _check(load_library().stmg3_residual(self._h, self._v(b, n_intervals, "b"), self._v(x, n_intervals, "x"),
+                                             self._v(r, n_intervals, "r"), n_intervals, self._halo(x_prev_slot),
                                              int(coupled)))
         return r
 
     def apply_additive(self, residual, out, n_intervals: int = 1):
-        _check(load_library().stmg3_apply_additive(self._h, _ptr(residual), _ptr(out), n_intervals))
+        _check(load_library().stmg3_apply_additive(self._h, self._v(residual, n_intervals, "residual"),
+                                                   self._v(out, n_intervals, "out"), n_intervals))
         return out
 
     def smooth_step(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False,
                     work=None):
-        _check(load_library().stmg3_smooth_step(self._h, _ptr(b), _ptr(u), omega, n_intervals, _ptr(x_prev_slot),
-                                                int(coupled), _ptr(work)))
+        _check(load_library().stmg3_smooth_step(self._h, self._v(b, n_intervals, "b"), self._v(u, n_intervals, "u"),
+                                                omega, n_intervals, self._halo(x_prev_slot), int(coupled),
+                                                self._v(work, n_intervals, "work")))
         return u
 
     def vanka_update(self, residual, u, omega: float, n_intervals: int = 1):
-        _check(load_library().stmg3_vanka_update(self._h, _ptr(residual), _ptr(u), omega, n_intervals))
+        _check(load_library().stmg3_vanka_update(self._h, self._v(residual, n_intervals, "residual"),
+                                                 self._v(u, n_intervals, "u"), omega, n_intervals))
         return u
 
     def project_mean_zero(self, x, n_intervals: int = 1):
-        _check(load_library().stmg3_project_mean_zero(self._h, _ptr(x), n_intervals))
+        _check(load_library().stmg3_project_mean_zero(self._h, self._v(x, n_intervals, "x"), n_intervals))
         return x
 
     def __del__(self):
@@ -489,7 +550,8 @@ class Solver3:
         lib = load_library()
         h = _c_void_p()
         _check(lib.stmg3_solver_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse, int(time_coarsen),
-                                       k_min, int(affine_patches), _hptr(vertices), nu1, nu2, omega, rtol, atol, max_iterations,
+                                       k_min, int(affine_patches),
+                                       _hptr(vertices, 3 * (nx + 1) * (ny + 1) * (nz + 1), "vertices"), nu1, nu2, omega, rtol, atol, max_iterations,
                                        ctypes.byref(h)))
         self._h = h
         out = (ctypes.c_int64 * (1 + 7 * 64))()
@@ -502,19 +564,29 @@ class Solver3:
                        for l in range(self.n_levels)]
         self.finest = self.levels[-1]
 
+    def _n_fine(self, l: int, n_coarse: int) -> int:
+        """Fine intervals of the pair (l, l-1): 2 n_coarse when it coarsens time."""
+        return n_coarse << (self.level_info[l - 1]["tshift"] - self.level_info[l]["tshift"])
+
     def restrict_residual(self, l: int, fine, coarse, n_coarse: int = 1, project_pressure: bool = True):
-        _check(load_library().stmg3_restrict_residual(self._h, l, _ptr(fine), _ptr(coarse), n_coarse,
+        nf = self._n_fine(l, n_coarse)
+        _check(load_library().stmg3_restrict_residual(self._h, l, self.levels[l]._v(fine, nf, "fine"),
+                                                      self.levels[l - 1]._v(coarse, n_coarse, "coarse"), n_coarse,
                                                       int(project_pressure)))
         return coarse
 
     def prolongate_correction(self, l: int, coarse, fine, n_coarse: int = 1, project_pressure: bool = True,
                               accumulate: bool = False):
-        _check(load_library().stmg3_prolongate_correction(self._h, l, _ptr(coarse), _ptr(fine), n_coarse,
+        nf = self._n_fine(l, n_coarse)
+        _check(load_library().stmg3_prolongate_correction(self._h, l, self.levels[l - 1]._v(coarse, n_coarse, "coarse"),
+                                                          self.levels[l]._v(fine, nf, "fine"), n_coarse,
                                                           int(project_pressure), int(accumulate)))
         return fine
 
     def coarse_forward(self, b, x, n_intervals: int):
-        _check(load_library().stmg3_coarse_forward(self._h, _ptr(b), _ptr(x), n_intervals))
+        c = self.levels[0]
+        _check(load_library().stmg3_coarse_forward(self._h, c._v(b, n_intervals, "b"), c._v(x, n_intervals, "x"),
+                                                   n_intervals))
         return x
 
     def set_comm(self, comm) -> None:
@@ -532,14 +604,18 @@ class Solver3:
         _check(lib.stmg3_solver_set_comm(self._h, ctypes.byref(ops)))
 
     def vcycle_all_at_once(self, b, x, n_intervals: int):
-        _check(load_library().stmg3_vcycle_all_at_once(self._h, _ptr(b), _ptr(x), n_intervals))
+        f = self.finest
+        _check(load_library().stmg3_vcycle_all_at_once(self._h, f._v(b, n_intervals, "b"), f._v(x, n_intervals, "x"),
+                                                       n_intervals))
         return x
 
     def solve_all_at_once(self, F, X, n_intervals: int, v_init=None, history_cap: int = 256):
         it = _c_int(0)
         hist = (ctypes.c_double * history_cap)()
-        _check(load_library().stmg3_solve_all_at_once(self._h, _ptr(F), _ptr(X), n_intervals, _ptr(v_init),
-                                                       ctypes.byref(it), hist, history_cap))
+        f = self.finest
+        _check(load_library().stmg3_solve_all_at_once(self._h, f._v(F, n_intervals, "F"), f._v(X, n_intervals, "X"),
+                                                       n_intervals, f._halo(v_init, "v_init"), ctypes.byref(it), hist,
+                                                       history_cap))
         return int(it.value), [hist[i] for i in range(min(history_cap, it.value + 1))]
 
     def __del__(self):

@@ -465,7 +465,8 @@ int
 grid_for(long long n, int threads)
 {
   const long long g = (n + threads - 1) / threads;
-  return static_cast<int>(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+  const long long cap = 16LL * device_sm_count();
+  return static_cast<int>(g < cap ? (g < 1 ? 1 : g) : cap);
 }
 } // namespace
 

@@ -101,6 +101,11 @@ cudaError_t launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *
                                 const double *r, double *u, long long isz, int n_intervals, double omega,
                                 cudaStream_t stream);
 int vanka_cols_per_batch();
+/// Intervals per block of the DMMA / big-patch item kernels (0 = the size
+/// heuristic); the tuning hook behind stmg_set_tuning.
+void set_vanka_group_override(int dmma_group, int big_group);
+/// Multiprocessor count of the current device (cached per device).
+int device_sm_count();
 cudaError_t launch_prolongate(const DevTransfer &T, const double *coarse, double *fine, int n_intervals,
                               int accumulate, cudaStream_t st);
 cudaError_t launch_restrict(const DevTransfer &T, const double *fine, double *coarse, int n_intervals,

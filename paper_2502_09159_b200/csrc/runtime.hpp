@@ -8,7 +8,10 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdarg>
+#include <cstdio>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -54,6 +57,28 @@ guarded(F &&f)
       return STMG_ERUNTIME;
     }
 }
+
+/// NVTX range (profiling: one range per C-ABI call, V-cycle
+/// level and phase, Krylov iteration and time step). nvtx3 is header-only and
+/// costs a null-pointer test when no tool is attached.
+struct NvtxRange
+{
+  explicit NvtxRange(const char *fmt, ...)
+  {
+    char buf[96];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define STMG_NVTX_CAT2(a, b) a##b
+#define STMG_NVTX_CAT(a, b) STMG_NVTX_CAT2(a, b)
+#define STMG_NVTX(...) ::stmg_rt::NvtxRange STMG_NVTX_CAT(nvtx_range_, __LINE__)(__VA_ARGS__)
 
 /// Reallocations of any DevArray: captured CUDA graphs hold raw pointers and
 /// are re-captured when this changes.

@@ -1536,7 +1536,7 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
         const long long ncols = cells * S;
         const size_t smem = sizeof(double) * (kGK * kGBP) + sizeof(long long) * 3 * kGCols +
                             sizeof(int) * (kGCols + 32) + sizeof(double) * (2 * S + 1) * kGCols;
-        const unsigned grid = static_cast<unsigned>(std::min<long long>(2 * 148, (ncols + kGCols - 1) / kGCols));
+        const unsigned grid = static_cast<unsigned>(std::min<long long>(2 * device_sm_count(), (ncols + kGCols - 1) / kGCols));
         auto gg = [&](auto init, auto kern) {
           init<<<igrid, 128, 0, st>>>(G, x, b, y, total_v);
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -324,7 +324,7 @@ build_level(stmg_level &L)
             while (B0 > 1)
               {
                 const long long wx = (nax + P * B0 * mult - 1) / (P * B0 * mult);
-                if ((wx + 1) / 2 * ((nsy + 1) / 2) * ngroups >= 2 * 148)
+                if ((wx + 1) / 2 * ((nsy + 1) / 2) * ngroups >= 2 * stmg_b200::device_sm_count())
                   break;
                 B0 /= 2;
               }
@@ -332,7 +332,7 @@ build_level(stmg_level &L)
           // time-marching set: 32 super-cells per block, fewer on small levels
           // so that a pass still spreads over ~2 blocks per SM (latency)
           const long long per_pass = std::max(1LL, static_cast<long long>(nsx) * nsy / 4);
-          const int B1 = static_cast<int>(std::min(32LL, std::max(1LL, per_pass / 296)));
+          const int B1 = static_cast<int>(std::min(32LL, std::max(1LL, per_pass / (2LL * stmg_b200::device_sm_count()))));
           const int B = set == 0 ? B0 : (set == 2 ? 2 * B0 : B1);
           stmg_level::SuperSet &ss = L.sup[set];
           std::vector<VankaBatch> items;
@@ -672,6 +672,7 @@ struct stmg_solver
   void
   cycle(int l, const double *b_v, double *x_v, int nI = 1, bool aao = false)
   {
+    STMG_NVTX("vcycle L%d (%d intervals)", l, nI);
     if (l == 0)
       {
         if (aao)
@@ -687,6 +688,7 @@ struct stmg_solver
     check(cudaMemsetAsync(x_v, 0, sizeof(double) * isz, ctx->stream), "memset");
     // smoothing step: residual (coupled in all-at-once mode), then Vanka
     const auto smooth = [&](bool first) {
+      STMG_NVTX("L%d smooth", l);
       if (first) // x = 0 on every rank before the first sweep: b - A 0 = b exactly
         L.smooth_step(b_v, x_v, omega, nI, nullptr, 0, S.r.p, true);
       else if (aao)
@@ -707,9 +709,15 @@ struct stmg_solver
     const long long csz = C.level->spec.isz() * nI;
     C.b.resize(csz);
     C.x.resize(csz);
-    restrict_residual(l, S.r.p, C.b.p, project_pressure, nI);
+    {
+      STMG_NVTX("L%d restrict", l);
+      restrict_residual(l, S.r.p, C.b.p, project_pressure, nI);
+    }
     cycle(l - 1, C.b.p, C.x.p, nI, aao);
-    prolongate_correction(l, C.x.p, x_v, project_pressure, true, nI);
+    {
+      STMG_NVTX("L%d prolongate", l);
+      prolongate_correction(l, C.x.p, x_v, project_pressure, true, nI);
+    }
     for (int s = 0; s < nu2; ++s)
       smooth(false);
   }
@@ -874,6 +882,7 @@ struct stmg_solver
         std::vector<double> hcol(m + 2);
         for (; j < m; ++j)
           {
+            STMG_NVTX("fgmres it %d", j);
             DevArray<double> &zj = basis(Z, j, n);
             precondition(V[j]->p, zj.p, nI, aao);
             if (aao)
@@ -1003,6 +1012,7 @@ struct stmg_solver
       }
     for (int step = 0; step < n_steps; ++step)
       {
+        STMG_NVTX("time_march step %d", step);
         const double t_start = step * tau;
         const double *Fn = F ? F + step * n : zero;
         if (problem == STMG_PROBLEM_MANUFACTURED)
@@ -1117,13 +1127,35 @@ stmg_last_error(void)
 const char *
 stmg_version(void)
 {
-  return "stmg_b200 0.1 sm_100a fp64";
+  return "stmg_b200 0.2 sm_100a fp64";
+}
+
+int
+stmg_set_tuning(const char *key, int64_t value)
+{
+  return guarded([&] {
+    STMG_NVTX("stmg_set_tuning");
+    if (!key)
+      throw std::invalid_argument("stmg_set_tuning: null key");
+    static int64_t groups[2] = {0, 0};
+    const std::string k(key);
+    if (value < 0 || value > 1024)
+      throw std::invalid_argument("stmg_set_tuning: value out of range");
+    if (k == "vanka_group")
+      groups[0] = value;
+    else if (k == "vanka_big_group")
+      groups[1] = value;
+    else
+      throw std::invalid_argument("stmg_set_tuning: unknown key " + k);
+    set_vanka_group_override(static_cast<int>(groups[0]), static_cast<int>(groups[1]));
+  });
 }
 
 int
 stmg_ctx_create(int device, stmg_ctx **out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_ctx_create");
     if (!out)
       throw std::invalid_argument("stmg_ctx_create: null out");
     check(cudaSetDevice(device), "cudaSetDevice");
@@ -1144,6 +1176,7 @@ int
 stmg_ctx_set_stream(stmg_ctx *ctx, void *stream)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_ctx_set_stream");
     if (!ctx)
       throw std::invalid_argument("null ctx");
     ctx->stream = static_cast<cudaStream_t>(stream);
@@ -1167,6 +1200,7 @@ stmg_level_create(stmg_ctx *ctx, int nx, int ny, int r, int k, double tau, doubl
                   stmg_level **out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_level_create");
     if (!ctx || !out)
       throw std::invalid_argument("stmg_level_create: null argument");
     if (smoother_kind < -1 || smoother_kind > 1)
@@ -1199,6 +1233,7 @@ int
 stmg_level_sizes(const stmg_level *L, int64_t *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_level_sizes");
     out[0] = L->spec.S();
     out[1] = L->spec.mv();
     out[2] = L->spec.mp();
@@ -1235,6 +1270,7 @@ int
 stmg_coupling_rhs(stmg_level *L, const double *v_prev, double *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_coupling_rhs");
     // raw apply of D*0 - C v_prev on every row, negated: out = C v_prev
     L->vmult(L->zero_vector(1), nullptr, out, 1, v_prev, 1, 2);
     check(launch_scale(L->spec.isz(), -1.0, out, L->ctx->stream), "scale");
@@ -1246,6 +1282,7 @@ int
 stmg_step_health(stmg_level *L, const double *X, int n, double *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_step_health");
     if (n < 1 || !X || !out)
       throw std::invalid_argument("step_health: bad arguments");
     const LevelSpec &s = L->spec;
@@ -1303,6 +1340,7 @@ int
 stmg_apply_additive(stmg_level *L, const double *r, double *out, int n)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_apply_additive");
     check(cudaMemsetAsync(out, 0, sizeof(double) * L->spec.isz() * n, L->ctx->stream), "memset");
     L->vanka(r, out, n, 1.0);
   });
@@ -1319,6 +1357,7 @@ int
 stmg_vanka_update(stmg_level *L, const double *r, double *u, double omega, int n)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_vanka_update");
     if (!(omega > 0.0 && omega <= 1.0))
       throw std::invalid_argument("vanka_update: omega must be in (0, 1]");
     L->vanka(r, u, n, omega);
@@ -1341,6 +1380,7 @@ int
 stmg_vmult_host(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_vmult_host");
     stmg_ctx &C = *L->ctx;
     C.copy_streams();
     const long long isz = L->spec.isz(), mv = L->spec.mv();
@@ -1377,6 +1417,7 @@ stmg_smooth_step_host(stmg_level *L, const double *b, double *u, double omega, i
                       int coupled)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_smooth_step_host");
     if (!(omega > 0.0 && omega <= 1.0))
       throw std::invalid_argument("smooth_step: omega must be in (0, 1]");
     stmg_ctx &C = *L->ctx;
@@ -1426,6 +1467,7 @@ stmg_solver_create(stmg_ctx *ctx, int refinements, int r, int k, int n_steps, do
                    int max_iterations, stmg_solver **out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_solver_create");
     if (!ctx || !out)
       throw std::invalid_argument("stmg_solver_create: null argument");
     if (smoother_kind != STMG_SMOOTHER_CELL && smoother_kind != STMG_SMOOTHER_VERTEX_STAR)
@@ -1486,6 +1528,7 @@ int
 stmg_solver_info(const stmg_solver *s, int64_t *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_solver_info");
     out[0] = static_cast<int64_t>(s->levels.size());
     out[1] = s->n_steps;
     for (size_t l = 0; l < s->levels.size(); ++l)
@@ -1512,6 +1555,7 @@ int
 stmg_restrict_residual(stmg_solver *s, int l, const double *fine, double *coarse, int project_pressure)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_restrict_residual");
     if (l < 1 || l >= static_cast<int>(s->levels.size()))
       throw std::invalid_argument("stmg_restrict_residual: level out of range");
     s->restrict_residual(l, fine, coarse, project_pressure != 0);
@@ -1523,6 +1567,7 @@ stmg_prolongate_correction(stmg_solver *s, int l, const double *coarse, double *
                            int accumulate)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_prolongate_correction");
     if (l < 1 || l >= static_cast<int>(s->levels.size()))
       throw std::invalid_argument("stmg_prolongate_correction: level out of range");
     s->prolongate_correction(l, coarse, fine, project_pressure != 0, accumulate != 0);
@@ -1551,6 +1596,7 @@ int
 stmg_assemble_rhs(stmg_level *L, int problem, double t_start, double *F, int n)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_assemble_rhs");
     if (problem != STMG_PROBLEM_MANUFACTURED)
       throw std::invalid_argument("stmg_assemble_rhs: unknown problem");
     if (n < 0 || !F)
@@ -1566,6 +1612,7 @@ int
 stmg_interpolate_exact(stmg_level *L, int problem, double t_start, double *X, int n)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_interpolate_exact");
     if (problem != STMG_PROBLEM_MANUFACTURED)
       throw std::invalid_argument("stmg_interpolate_exact: unknown problem");
     if (n < 0 || !X)
@@ -1581,6 +1628,7 @@ int
 stmg_compute_errors(stmg_level *L, int problem, double t_start, const double *X, int n, double *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_compute_errors");
     if (problem != STMG_PROBLEM_MANUFACTURED)
       throw std::invalid_argument("stmg_compute_errors: unknown problem");
     if (n < 1 || !X || !out)
@@ -1600,6 +1648,7 @@ int
 stmg_solver_set_comm(stmg_solver *s, const stmg_comm_ops *ops)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_solver_set_comm");
     if (!ops)
       {
         s->has_comm = false;
@@ -1619,6 +1668,7 @@ int
 stmg_vcycle_all_at_once(stmg_solver *s, const double *b, double *x, int n_intervals)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_vcycle_all_at_once");
     if (n_intervals < 1)
       throw std::invalid_argument("stmg_vcycle_all_at_once: need at least one interval");
     s->cycle(static_cast<int>(s->levels.size()) - 1, b, x, n_intervals, true);
@@ -1642,6 +1692,7 @@ int
 stmg_time_march_problem(stmg_solver *s, int problem, double *X, int *iterations)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_time_march_problem");
     if (problem != STMG_PROBLEM_MANUFACTURED && problem != STMG_PROBLEM_CAVITY)
       throw std::invalid_argument("stmg_time_march_problem: unknown problem");
     s->time_march(nullptr, X, iterations, problem);
@@ -1659,6 +1710,7 @@ int
 stmg_time_march_host(stmg_solver *s, const double *F, double *X, int *iterations)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_time_march_host");
     stmg_level &L = s->fine();
     const size_t sz = static_cast<size_t>(L.spec.isz()) * s->n_steps;
     L.host_in.resize(sz);
@@ -1675,6 +1727,7 @@ int
 stmg_plan_levels(int refinements, int r, int k, int n_steps, double t_end, int h_only, int64_t *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_plan_levels");
     HierarchyConfig cfg;
     cfg.refinements = refinements;
     cfg.r = r;
@@ -1702,6 +1755,7 @@ stmg_patch_info(int nx, int ny, int r, int k, double tau, double nu, double gamm
                 double *inverse_out, int class_index)
 {
   return guarded([&] {
+    STMG_NVTX("stmg_patch_info");
     LevelSpec s;
     s.nx = nx;
     s.ny = ny;

@@ -419,6 +419,7 @@ struct stmg3_solver
   void
   cycle(int l, const double *b_v, double *x_v, int nI)
   {
+    STMG_NVTX("vcycle3 L%d (%d intervals)", l, nI);
     if (l == 0)
       {
         coarse_forward(b_v, x_v, nI);
@@ -431,6 +432,7 @@ struct stmg3_solver
     check(cudaMemsetAsync(x_v, 0, sizeof(double) * isz, ctx->stream), "memset");
     for (int s = 0; s < nu1; ++s)
       {
+        STMG_NVTX("L%d pre-smooth", l);
         if (s == 0) // x = 0 on every rank: b - A 0 = b
           L.smooth_step(b_v, x_v, omega, nI, nullptr, 0, S.r.p, true);
         else
@@ -445,11 +447,18 @@ struct stmg3_solver
     const long long csz = C.level->spec.isz() * nc;
     C.b.resize(csz);
     C.x.resize(csz);
-    restrict_residual(l, S.r.p, C.b.p, nc, project_pressure);
+    {
+      STMG_NVTX("L%d restrict", l);
+      restrict_residual(l, S.r.p, C.b.p, nc, project_pressure);
+    }
     cycle(l - 1, C.b.p, C.x.p, nc);
-    prolongate_correction(l, C.x.p, x_v, nc, project_pressure, true);
+    {
+      STMG_NVTX("L%d prolongate", l);
+      prolongate_correction(l, C.x.p, x_v, nc, project_pressure, true);
+    }
     for (int s = 0; s < nu2; ++s)
       {
+        STMG_NVTX("L%d post-smooth", l);
         coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
         L.vanka(S.r.p, x_v, nI, omega);
       }
@@ -516,6 +525,7 @@ struct stmg3_solver
         std::vector<double> hcol(m + 2);
         for (; j < m; ++j)
           {
+            STMG_NVTX("fgmres3 it %d", j);
             DevArray<double> &zj = basis(Z, j, n);
             cycle(top, V[j]->p, zj.p, nI);
             coupled_vmult(top, zj.p, nullptr, w.p, nI, 0);
@@ -688,6 +698,7 @@ stmg3_level_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double t
                    int smoother_kind, const double *vertices, stmg3_level **out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_level_create");
     if (!ctx || !out)
       throw std::invalid_argument("null argument");
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -718,6 +729,7 @@ int
 stmg3_level_sizes(const stmg3_level *L, int64_t *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_level_sizes");
     if (!L || !out)
       throw std::invalid_argument("null argument");
     const Level3Spec &s = L->spec;
@@ -750,6 +762,7 @@ int
 stmg3_apply_additive(stmg3_level *L, const double *r, double *out, int n)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_apply_additive");
     check(cudaMemsetAsync(out, 0, sizeof(double) * L->spec.isz() * n, L->ctx->stream), "memset");
     L->vanka(r, out, n, 1.0);
   });
@@ -766,6 +779,7 @@ int
 stmg3_vanka_update(stmg3_level *L, const double *r, double *u, double omega, int n)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_vanka_update");
     if (!(omega > 0.0 && omega <= 1.0))
       throw std::invalid_argument("vanka_update: omega must be in (0, 1]");
     L->vanka(r, u, n, omega);
@@ -785,6 +799,7 @@ stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double 
                     double rtol, double atol, int max_iterations, stmg3_solver **out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_solver_create");
     if (!ctx || !out)
       throw std::invalid_argument("null argument");
     if (!(omega > 0.0 && omega <= 1.0))
@@ -883,6 +898,7 @@ int
 stmg3_plan_levels(int nx, int ny, int nz, int r, int k, int n_hcoarse, int time_coarsen, int k_min, int64_t *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_plan_levels");
     if (!out)
       throw std::invalid_argument("null argument");
     Level3Spec f;
@@ -919,6 +935,7 @@ int
 stmg3_solver_info(const stmg3_solver *s, int64_t *out)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_solver_info");
     out[0] = static_cast<int64_t>(s->levels.size());
     for (size_t l = 0; l < s->levels.size(); ++l)
       {
@@ -947,6 +964,7 @@ int
 stmg3_solver_set_comm(stmg3_solver *s, const stmg_comm_ops *ops)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_solver_set_comm");
     if (ops)
       {
         if (ops->world < 1 || ops->rank < 0 || ops->rank >= ops->world || !ops->exchange_halo ||
@@ -964,6 +982,7 @@ int
 stmg3_restrict_residual(stmg3_solver *s, int l, const double *fine, double *coarse, int nc, int project)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_restrict_residual");
     if (l < 1 || l >= static_cast<int>(s->levels.size()))
       throw std::invalid_argument("level out of range");
     s->restrict_residual(l, fine, coarse, nc, project != 0);
@@ -975,6 +994,7 @@ stmg3_prolongate_correction(stmg3_solver *s, int l, const double *coarse, double
                             int accumulate)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_prolongate_correction");
     if (l < 1 || l >= static_cast<int>(s->levels.size()))
       throw std::invalid_argument("level out of range");
     s->prolongate_correction(l, coarse, fine, nc, project != 0, accumulate != 0);
@@ -991,6 +1011,7 @@ int
 stmg3_vcycle_all_at_once(stmg3_solver *s, const double *b, double *x, int n)
 {
   return guarded([&] {
+    STMG_NVTX("stmg3_vcycle_all_at_once");
     s->check_slab(n);
     s->cycle(static_cast<int>(s->levels.size()) - 1, b, x, n);
   });

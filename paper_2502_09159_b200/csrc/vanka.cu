@@ -129,9 +129,6 @@ constexpr int kDRows = 128;               // max n_T
 #define STMG_VANKA_COLS 16
 #endif
 constexpr int kDCols = STMG_VANKA_COLS;   // columns per tile
-#ifndef STMG_VANKA176_COLS
-#define STMG_VANKA176_COLS 8 // 176-row variant: 8 columns keep 2 x 44 A-fragments in registers
-#endif
 constexpr int kDRLd = 36;                 // R tile pitch (doubles): conflict-free B-fragment loads
 constexpr int kDZLd = 33;                 // Z tile pitch
 constexpr int kDPer = kDRows * kDCols / kDThreads; // elements per thread per tile (8)
@@ -170,6 +167,7 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
   // computes and scatters OROWS rows but gathers all ROWS rows of R (the
   // contraction dimension); warp w owns the TPW 8-row tiles w + j * NW
   constexpr int kDCols = COLS;
+  static_assert(COLS <= kDZLd && COLS <= kDRLd, "tile columns must fit the R / Z pitches");
   constexpr int OROWS = ROWS / SPLIT;
   constexpr bool CL = SPLIT > 1 && STMG_V176_CLUSTER; // cluster of the SPLIT CTAs shares the R gather
   constexpr int kDRows = ROWS, kDThreads = OROWS / 8 / TPW * 32;
@@ -499,6 +497,39 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 }
 } // namespace
 
+namespace
+{
+// intervals per block of the item kernels: [0] DMMA (128 / 176 rows), [1] big
+// patches; 0 = size heuristic. Initialised from STMG_VGROUP / STMG_BGROUP.
+int g_group_override[2] = {std::getenv("STMG_VGROUP") ? std::atoi(std::getenv("STMG_VGROUP")) : 0,
+                           std::getenv("STMG_BGROUP") ? std::atoi(std::getenv("STMG_BGROUP")) : 0};
+} // namespace
+
+void
+set_vanka_group_override(int dmma_group, int big_group)
+{
+  g_group_override[0] = dmma_group;
+  g_group_override[1] = big_group;
+}
+
+int
+device_sm_count()
+{
+  static int cached[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64)
+    dev = 0;
+  if (cached[dev] == 0)
+    {
+      int n = 0;
+      if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+        n = 148;
+      cached[dev] = n;
+    }
+  return cached[dev];
+}
+
 /// Launch one colour: `n_batches` batches over `n_intervals` intervals.
 cudaError_t
 launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, const int *item_ptr, int n_batches,
@@ -513,14 +544,20 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       // 128 rows (16 warps) for 2D patches; 176 rows (22 warps) for 3D Q2 cells (n_T = 170)
       const int rows = max_nt <= kDRows ? kDRows : 176;
       const int split = rows == 176 ? 2 : 1, orows = rows / split;
-      const size_t dsmem = sizeof(double) * (rows * kDRLd + orows * kDZLd + orows) + sizeof(long long) * 6 * kDCols;
-      // intervals per block: 16, fewer on small levels so the launch still
-      // fills the GPU (a coarse level has only a few batches per colour)
-      // intervals per block: 16 for 2D patches, 4 for the 176-row split (C3: more, shorter blocks balance better)
-      static const int genv = std::getenv("STMG_VGROUP") ? std::atoi(std::getenv("STMG_VGROUP")) : 0;
-      int group = genv > 0 ? genv : (rows == 176 ? 4 : kDGroup);
-      while (group > 1 && static_cast<long long>(n_batches) * split * ((n_intervals + group - 1) / group) < 2 * 148)
-        group /= 2;
+      const int cols = rows == 176 ? STMG_V176_COLS : kDCols; // COLS of the instantiated kernel
+      const size_t dsmem = sizeof(double) * (rows * kDRLd + orows * kDZLd + orows) + sizeof(long long) * 6 * cols;
+      // intervals per block: 16 for 2D patches, 4 for the 176-row split (C3:
+      // more, shorter blocks balance better), fewer on small levels so the
+      // launch still fills the GPU (a coarse level has only a few batches per
+      // colour). A tuning override (stmg_set_tuning) is taken as is.
+      int group = g_group_override[0];
+      if (group <= 0)
+        {
+          group = rows == 176 ? 4 : kDGroup;
+          while (group > 1 &&
+                 static_cast<long long>(n_batches) * split * ((n_intervals + group - 1) / group) < 2 * device_sm_count())
+            group /= 2;
+        }
       dim3 grid(n_batches, (n_intervals + group - 1) / group, split);
       const int ks = (max_nt + 3) / 4;
       auto go = [&](auto kern) {
@@ -569,10 +606,13 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
       const int ks = (max_nt + 3) / 4;
       const size_t smem = sizeof(double) * (4 * ks * kBLd) + sizeof(long long) * 2 * kBCols;
       const int tpw = ((max_nt + 7) / 8 + 15) / 16;
-      static const int benv = std::getenv("STMG_BGROUP") ? std::atoi(std::getenv("STMG_BGROUP")) : 0;
-      int group = benv > 0 ? benv : kBGroup;
-      while (group > 1 && static_cast<long long>(n_batches) * ((n_intervals + group - 1) / group) < 2 * 148)
-        group /= 2;
+      int group = g_group_override[1];
+      if (group <= 0)
+        {
+          group = kBGroup;
+          while (group > 1 && static_cast<long long>(n_batches) * ((n_intervals + group - 1) / group) < 2 * device_sm_count())
+            group /= 2;
+        }
       dim3 grid(n_batches, (n_intervals + group - 1) / group);
       auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -93,3 +93,25 @@ def test_patch_classes_invert_oracle_local_matrices(oracle, stmg, nc, r, k, kind
             assert np.abs(A @ inv @ A - A).max() < 1e-10 * np.abs(A).max()
         else:
             assert best < 1e-9, (i, best)
+
+
+def test_binding_rejects_host_and_mistyped_tensors(stmg):
+    """The binding checks every vector before it reaches the C ABI (no GPU:
+    a CPU tensor is refused as such; sizes are checked on the GPU tier)."""
+    import torch
+
+    with pytest.raises(ValueError, match="CUDA"):
+        stmg._ptr(torch.zeros(4, dtype=torch.float64))
+    with pytest.raises(ValueError, match="float64"):
+        stmg._hptr(np.zeros(4, dtype=np.int64))
+    with pytest.raises(ValueError, match="elements"):
+        stmg._hptr(np.zeros(4), 5)
+    assert stmg._ptr(None) is None
+
+
+def test_tuning_hook_validates_without_gpu(stmg):
+    lib = stmg.load_library()
+    assert lib.stmg_set_tuning(b"vanka_group", 4) == 0
+    assert lib.stmg_set_tuning(b"vanka_group", 0) == 0
+    assert lib.stmg_set_tuning(b"bogus", 1) == 1
+    assert lib.stmg_set_tuning(b"vanka_big_group", 5000) == 1
