@@ -369,6 +369,7 @@ struct PatchFactorization // vanka.hpp:24-39
   LU lu;
   std::unique_ptr<MinNormSolver> cod;
   Vec weights;
+  bool factored = false;
   int size() const { return static_cast<int>(dofs.size()); }
   Vec solve(const Vec &rhs) const { return cod ? cod->solve(rhs) : lu.solve(rhs); }
 };
@@ -376,7 +377,11 @@ struct PatchFactorization // vanka.hpp:24-39
 class VankaSmoother // vanka.hpp:45-89, vanka.cpp
 {
 public:
-  static VankaSmoother build(const SpaceTimeBlockOperator &op, SmootherKind kind);
+  static VankaSmoother build(const SpaceTimeBlockOperator &op, SmootherKind kind, bool factor = true);
+  /// R_T S R_T^T of patch ip (vanka.cpp:92-165) and its factorization
+  /// (vanka.cpp:167-176), for smoothers built with factor == false.
+  Mat local_matrix(const SpaceTimeBlockOperator &op, size_t ip) const;
+  Mat factor_patch(const SpaceTimeBlockOperator &op, size_t ip); // returns R_T S R_T^T
   SmootherKind kind() const { return kind_; }
   const std::vector<PatchFactorization> &patches() const { return patches_; }
   void apply_additive(const BlockVector &residual, BlockVector &out) const;

@@ -120,9 +120,11 @@ oracle_level_create(int nc, int r, int k, double tau, double nu, double gamma, i
     h->ps = std::make_unique<PressureSpace>(*h->mesh, levels - 1, r);
     h->tm = std::make_unique<TemporalMatrices>(temporal_matrices(k, tau));
     h->op = std::make_unique<SpaceTimeBlockOperator>(*h->vs, *h->ps, *h->tm, nu, gamma);
+    // build_smoother: 0 none, 1 full (every patch factored), 2 patch lists and
+    // weights only (patches factored on demand by oracle_smooth_step_rows)
     if (build_smoother)
-      h->sm = std::make_unique<VankaSmoother>(
-        VankaSmoother::build(*h->op, smoother_kind == 1 ? SmootherKind::vertex_star : SmootherKind::cell));
+      h->sm = std::make_unique<VankaSmoother>(VankaSmoother::build(
+        *h->op, smoother_kind == 1 ? SmootherKind::vertex_star : SmootherKind::cell, build_smoother != 2));
     *out = h.release();
   });
 }
@@ -281,6 +283,79 @@ oracle_smooth_step_all(void *hp, const double *b, double *u, double omega, int n
         h->sm->apply_additive(res, corr);
         for (Index i = 0; i < sz; ++i)
           u[n * sz + i] = u_old[n * sz + i] + omega * corr.data[i];
+      }
+  });
+}
+
+/// smooth_step_all (above) evaluated at a subset of rows, for meshes whose
+/// full set of patch factorizations does not fit (BASELINE-size parity):
+/// out[n * nrows + i] = u_new[n][rows[i]]. Only the patches containing a
+/// requested row are factored; they are applied in patch order, so every
+/// requested row receives exactly the additions of the full sweep, in the
+/// same order (vanka.cpp:196-215).
+int
+oracle_smooth_step_rows(void *hp, const double *b, const double *u, double omega, int n_intervals,
+                        const double *x_prev_slot, const long *rows, long nrows, double *out, int threads)
+{
+  return guard([&] {
+    auto *h = static_cast<LevelHandle *>(hp);
+    if (!h->sm)
+      throw std::invalid_argument("no smoother built");
+    if (!(omega > 0.0 && omega <= 1.0))
+      throw std::invalid_argument("smooth_step: omega must be in (0, 1]");
+    const Index sz = h->op->make_vector().size();
+    const Index mv = h->vs->n_dofs();
+    const int ns = h->op->n_slots();
+    std::vector<int> idx(static_cast<size_t>(sz), -1);
+    for (long i = 0; i < nrows; ++i)
+      {
+        if (rows[i] < 0 || rows[i] >= sz)
+          throw std::invalid_argument("oracle_smooth_step_rows: row out of range");
+        idx[rows[i]] = static_cast<int>(i);
+      }
+    auto &patches = h->sm->patches();
+    std::vector<size_t> need;
+    for (size_t ip = 0; ip < patches.size(); ++ip)
+      for (const Index d : patches[ip].dofs)
+        if (idx[d] >= 0)
+          {
+            need.push_back(ip);
+            break;
+          }
+#ifdef _OPENMP
+    if (threads > 0)
+      omp_set_num_threads(threads);
+#pragma omp parallel for schedule(dynamic, 4) if (threads != 1)
+#endif
+    for (long q = 0; q < static_cast<long>(need.size()); ++q)
+      if (!patches[need[q]].factored)
+        h->sm->factor_patch(*h->op, need[q]);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1) if (threads != 1)
+#endif
+    for (int n = 0; n < n_intervals; ++n)
+      {
+        const double *prev = n == 0 ? x_prev_slot : u + (n - 1) * sz + (ns - 1) * mv;
+        Vec au(sz);
+        vmult_interval(*h, u + n * sz, prev, au.data());
+        for (Index i = 0; i < sz; ++i)
+          au[i] = b[n * sz + i] - au[i];
+        std::vector<double> corr(static_cast<size_t>(nrows), 0.0);
+        Vec loc;
+        for (const size_t ip : need)
+          {
+            const auto &patch = patches[ip];
+            const int n_t = patch.size();
+            loc.resize(n_t);
+            for (int i = 0; i < n_t; ++i)
+              loc[i] = au[patch.dofs[i]];
+            loc = patch.solve(loc);
+            for (int i = 0; i < n_t; ++i)
+              if (idx[patch.dofs[i]] >= 0)
+                corr[idx[patch.dofs[i]]] += patch.weights[i] * loc[i];
+          }
+        for (long i = 0; i < nrows; ++i)
+          out[n * nrows + i] = u[n * sz + rows[i]] + omega * corr[i];
       }
   });
 }

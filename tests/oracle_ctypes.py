@@ -44,6 +44,8 @@ def lib():
         L.oracle_vmult_all.argtypes = [_P, _D, _D, ctypes.c_int, _D, ctypes.c_int]
         L.oracle_apply_additive.argtypes = [_P, _D, _D]
         L.oracle_smooth_step_all.argtypes = [_P, _D, _D, ctypes.c_double, ctypes.c_int, _D, ctypes.c_int]
+        L.oracle_smooth_step_rows.argtypes = [_P, _D, _D, ctypes.c_double, ctypes.c_int, _D,
+                                              ctypes.POINTER(ctypes.c_long), ctypes.c_long, _D, ctypes.c_int]
         L.oracle_patch_count.argtypes = [_P]
         L.oracle_patch_count.restype = ctypes.c_long
         L.oracle_patch_size.argtypes = [_P, ctypes.c_long]
@@ -114,6 +116,17 @@ class OracleLevel:
         y = np.zeros_like(x)
         _chk(lib().oracle_vmult_all(self.h, _d(x), _d(y), n, _d(x_prev), threads))
         return y
+
+    def smooth_step_rows(self, b, u, omega, n, rows, x_prev=None, threads=0):
+        """smooth_step_all evaluated at `rows` (indices within one interval) of
+        every interval: shape (n, len(rows)). With build_smoother == 2 only the
+        patches containing a requested row are factored."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        out = np.zeros(n * rows.size)
+        _chk(lib().oracle_smooth_step_rows(self.h, _d(b), _d(u), omega, n, _d(x_prev),
+                                           rows.ctypes.data_as(ctypes.POINTER(ctypes.c_long)), rows.size, _d(out),
+                                           threads))
+        return out.reshape(n, rows.size)
 
     def apply_additive(self, r):
         y = np.zeros(self.size)

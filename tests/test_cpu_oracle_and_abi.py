@@ -115,3 +115,21 @@ def test_tuning_hook_validates_without_gpu(stmg):
     assert lib.stmg_set_tuning(b"vanka_group", 0) == 0
     assert lib.stmg_set_tuning(b"bogus", 1) == 1
     assert lib.stmg_set_tuning(b"vanka_big_group", 5000) == 1
+
+
+@pytest.mark.parametrize("nc,r,k,kind", [(8, 2, 2, 0), (8, 1, 1, 1), (4, 1, 2, 1)])
+def test_oracle_row_subset_smoother_equals_full_sweep(oracle, nc, r, k, kind):
+    """oracle_smooth_step_rows (patches factored on demand, the checker of
+    the BASELINE-size GPU parity tests) returns the full sweep's values,
+    bitwise, at the requested rows."""
+    tau = 1 / 16
+    full = oc.OracleLevel(nc, r, k, tau, 1.0, 1.0, kind)
+    lazy = oc.OracleLevel(nc, r, k, tau, 1.0, 1.0, kind, build_smoother=2)
+    n = 3
+    u = oc.seeded(n * full.size, 21)
+    b = oc.seeded(n * full.size, 22)
+    halo = oc.seeded(full.n_velocity, 23)
+    ref = full.smooth_step_all(b, u, 0.8, n, halo).reshape(n, full.size)
+    rows = np.unique(np.random.default_rng(5).integers(0, full.size, 97))
+    got = lazy.smooth_step_rows(b, u, 0.8, n, rows, halo)
+    assert np.array_equal(got, ref[:, rows])
