@@ -374,8 +374,9 @@ def c3_slab_leg(stmg, torch, dist, world, rank, n_total=64):
     ctx = stmg.Context(torch.cuda.current_device())
     sol = stmg.Solver3(ctx, 32, 32, 32, 1, 1, 1.0 / n_total, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=1,
                        nu1=2, nu2=2, rtol=1e-8)
-    if world > 1:
-        sol.set_comm(timeslab.TorchComm(device=f"cuda:{torch.cuda.current_device()}"))
+    if world > 1:  # the library's C++ NCCL communicator; CGS2: two all-reduces per iteration
+        sol.set_comm(timeslab.nccl_comm())
+        sol.set_krylov(stmg.ORTHO_CGS2)
     f = sol.finest
     F = bench3d.consistent(torch, f, bench3d.seeded(torch, n_local * f.size, 301 + rank), n_local)
     X = torch.zeros_like(F)
@@ -413,8 +414,9 @@ def slab_solve_leg(stmg, ctx, torch, dist, world, rank, n_local=8):
 
     sol = stmg.Solver(ctx, 10, 1, 1, n_steps=n_local, t_end=n_local / 64.0, nu=1.0, gamma=1.0,
                       smoother=stmg.SMOOTHER_VERTEX_STAR, nu1=2, nu2=2, omega=0.8, rtol=1e-8)
-    if world > 1:
-        sol.set_comm(timeslab.TorchComm(device=f"cuda:{torch.cuda.current_device()}"))
+    if world > 1:  # the library's C++ NCCL communicator; CGS2: two all-reduces per iteration
+        sol.set_comm(timeslab.nccl_comm())
+        sol.set_krylov(stmg.ORTHO_CGS2)
     F = _consistent_rhs(torch, sol, n_local, 101 + rank)
     X = torch.zeros_like(F)
     sol.solve_all_at_once(F, X, n_local)  # warm-up: Krylov workspace, coarse tables
@@ -520,6 +522,9 @@ def main():
     halo_u = torch.zeros(mv, dtype=torch.float64, device="cuda")
 
     comm_stream = torch.cuda.Stream() if world > 1 else None
+    if world > 1:  # halo send/recv through the library's NCCL communicator (stmg_comm_nccl_ops)
+        step_comm = timeslab.nccl_comm()
+        step_ops = step_comm.ops()
 
     def coupled(apply, src, halo, dst, *extra):
         """Time-slab application with the halo exchange overlapped: the NCCL
@@ -531,8 +536,10 @@ def main():
             return
         main = torch.cuda.current_stream()
         comm_stream.wait_stream(main)
-        with torch.cuda.stream(comm_stream):
-            h = timeslab.exchange_halo(src, halo, N, isz, mv, S, rank, world)
+        send = src[(N - 1) * isz + (S - 1) * mv:(N - 1) * isz + S * mv]
+        if step_ops.exchange_halo(step_ops.user, send.data_ptr(), halo.data_ptr(), mv, comm_stream.cuda_stream) != 0:
+            raise RuntimeError("halo exchange failed")
+        h = halo if rank > 0 else None
         if N > 1:
             apply(src[isz:], dst[isz:], N - 1, src[(S - 1) * mv:S * mv], *[e[isz:] for e in extra])
         main.wait_stream(comm_stream)

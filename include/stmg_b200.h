@@ -243,6 +243,32 @@ typedef struct stmg_comm_ops {
 } stmg_comm_ops;
 /* Install (ops != NULL, copied) or remove (NULL) the communicator. */
 int stmg_solver_set_comm(stmg_solver *solver, const stmg_comm_ops *ops);
+
+/* Arnoldi orthogonalization of gmres / the all-at-once FGMRES:
+ * STMG_ORTHO_MGS (default) is the reference's modified Gram-Schmidt
+ * (solver.cpp:146-152): j+1 all-reduces in iteration j under a time-slab
+ * partition. STMG_ORTHO_CGS2 is classical Gram-Schmidt applied twice with
+ * batched inner products: two all-reduces per iteration. Same Krylov space;
+ * iteration counts agree within +-1. */
+#define STMG_ORTHO_MGS 0
+#define STMG_ORTHO_CGS2 1
+int stmg_solver_set_krylov(stmg_solver *solver, int orthogonalization);
+
+/* NCCL time-slab communicator inside the library (no caller callbacks in the
+ * per-iteration path): NCCL is loaded at run time (libnccl.so.2), so the
+ * library itself has no link-time NCCL dependency.
+ *  - stmg_comm_nccl_unique_id: rank 0 creates the 128-byte ncclUniqueId, the
+ *    caller broadcasts it (any channel) to every rank;
+ *  - stmg_comm_nccl_create: one communicator per rank on `device`;
+ *  - stmg_comm_nccl_ops: fills an stmg_comm_ops whose callbacks run NCCL
+ *    (send/recv for the halo, all-reduce, all-gather) on the given stream;
+ *    pass it to stmg_solver_set_comm / stmg3_solver_set_comm. The ops stay
+ *    valid until stmg_comm_destroy. */
+typedef struct stmg_comm stmg_comm;
+int stmg_comm_nccl_unique_id(void *unique_id_out /* 128 bytes */);
+int stmg_comm_nccl_create(const void *unique_id, int rank, int world, int device, stmg_comm **out);
+int stmg_comm_nccl_ops(stmg_comm *comm, stmg_comm_ops *ops_out);
+int stmg_comm_destroy(stmg_comm *comm);
 /* One all-at-once V-cycle x = V(b) on the finest level, n_intervals intervals. */
 int stmg_vcycle_all_at_once(stmg_solver *solver, const double *b, double *x, int n_intervals);
 /* Solve A X = F on the slab. v_init (nullable, M^v doubles) is the slot-k
@@ -325,6 +351,7 @@ int stmg3_plan_levels(int nx, int ny, int nz, int r, int k, int n_hcoarse, int t
 int stmg3_solver_info(const stmg3_solver *solver, int64_t *out);
 stmg3_level *stmg3_solver_level(stmg3_solver *solver, int l);
 int stmg3_solver_set_comm(stmg3_solver *solver, const stmg_comm_ops *ops);
+int stmg3_solver_set_krylov(stmg3_solver *solver, int orthogonalization); /* as stmg_solver_set_krylov */
 /* TransferPair::restrict_residual / prolongate_correction (transfer.cpp:102-132)
  * between level l and l-1 on nc coarse intervals (2 nc fine ones when the
  * pair coarsens time). */

@@ -24,6 +24,9 @@ HEADER_PATH = _PKG.parent / "include" / "stmg_b200.h"
 PROBLEM_MANUFACTURED = 0
 PROBLEM_CAVITY = 1
 
+ORTHO_MGS = 0   # modified Gram-Schmidt (the reference's, solver.cpp:146-152)
+ORTHO_CGS2 = 1  # classical Gram-Schmidt twice: two batched all-reduces per iteration
+
 SMOOTHER_NONE = -1
 SMOOTHER_CELL = 0
 SMOOTHER_VERTEX_STAR = 1
@@ -86,6 +89,12 @@ _SIGNATURES = {
     "stmg_interpolate_exact": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int], _c_int),
     "stmg_compute_errors": ([_c_void_p, _c_int, _c_double, _c_void_p, _c_int, ctypes.POINTER(_c_double)], _c_int),
     "stmg_solver_set_comm": ([_c_void_p, _c_void_p], _c_int),
+    "stmg_solver_set_krylov": ([_c_void_p, _c_int], _c_int),
+    "stmg3_solver_set_krylov": ([_c_void_p, _c_int], _c_int),
+    "stmg_comm_nccl_unique_id": ([_c_void_p], _c_int),
+    "stmg_comm_nccl_create": ([_c_void_p, _c_int, _c_int, _c_int, ctypes.POINTER(_c_void_p)], _c_int),
+    "stmg_comm_nccl_ops": ([_c_void_p, _c_void_p], _c_int),
+    "stmg_comm_destroy": ([_c_void_p], _c_int),
     "stmg_vcycle_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
     "stmg_solve_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, ctypes.POINTER(_c_int),
                                 ctypes.POINTER(_c_double), _c_int], _c_int),
@@ -199,6 +208,39 @@ def _guard(fn):
             traceback.print_exception(exc)
             return 1
     return wrapped
+
+
+class NcclComm:
+    """The library's own NCCL time-slab communicator (stmg_comm_nccl_*): halo
+    send/recv, Krylov all-reduces and the coarse all-gather run as NCCL calls
+    inside libstmg_b200, with no Python in the per-iteration path. Rank 0
+    makes the unique id (``NcclComm.unique_id()``); every rank passes the same
+    bytes."""
+
+    def __init__(self, rank: int, world: int, device: int, unique_id: bytes):
+        if len(unique_id) != 128:
+            raise ValueError("NcclComm: the NCCL unique id is 128 bytes")
+        lib = load_library()
+        h = _c_void_p()
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(lib.stmg_comm_nccl_create(ctypes.cast(buf, _c_void_p), rank, world, device, ctypes.byref(h)))
+        self._h, self.rank, self.world, self.device = h, rank, world, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(load_library().stmg_comm_nccl_unique_id(ctypes.cast(buf, _c_void_p)))
+        return buf.raw
+
+    def ops(self) -> "_CommOps":
+        ops = _CommOps()
+        _check(load_library().stmg_comm_nccl_ops(self._h, ctypes.byref(ops)))
+        return ops
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.stmg_comm_destroy(self._h)
+            self._h = None
 
 
 class Context:
@@ -438,12 +480,20 @@ class Solver:
             self._comm = None
             _check(lib.stmg_solver_set_comm(self._h, None))
             return
+        if isinstance(comm, NcclComm):
+            self._comm = comm  # keeps the communicator alive while installed
+            _check(lib.stmg_solver_set_comm(self._h, ctypes.byref(comm.ops())))
+            return
         ops = _CommOps(None, comm.rank, comm.world,
                        _HALO_FN(_guard(lambda u, s, r, n, st: comm.exchange_halo(s, r, n, st))),
                        _REDUCE_FN(_guard(lambda u, b, n, st: comm.allreduce_sum(b, n, st))),
                        _HALO_FN(_guard(lambda u, s, r, n, st: comm.allgather(s, r, n, st))))
         self._comm = ops  # the C side keeps the function pointers: keep them alive
         _check(lib.stmg_solver_set_comm(self._h, ctypes.byref(ops)))
+
+    def set_krylov(self, orthogonalization: int) -> None:
+        """ORTHO_MGS (default, the reference's) or ORTHO_CGS2 (two batched all-reduces per iteration)."""
+        _check(load_library().stmg_solver_set_krylov(self._h, orthogonalization))
 
     def vcycle_all_at_once(self, b, x, n_intervals: int):
         """One all-at-once V-cycle over n_intervals intervals (Eq. GloSys)."""
@@ -596,12 +646,20 @@ class Solver3:
             self._comm = None
             _check(lib.stmg3_solver_set_comm(self._h, None))
             return
+        if isinstance(comm, NcclComm):
+            self._comm = comm
+            _check(lib.stmg3_solver_set_comm(self._h, ctypes.byref(comm.ops())))
+            return
         ops = _CommOps(None, comm.rank, comm.world,
                        _HALO_FN(_guard(lambda u, s, r, n, st: comm.exchange_halo(s, r, n, st))),
                        _REDUCE_FN(_guard(lambda u, b, n, st: comm.allreduce_sum(b, n, st))),
                        _HALO_FN(_guard(lambda u, s, r, n, st: comm.allgather(s, r, n, st))))
         self._comm = ops
         _check(lib.stmg3_solver_set_comm(self._h, ctypes.byref(ops)))
+
+    def set_krylov(self, orthogonalization: int) -> None:
+        """As Solver.set_krylov."""
+        _check(load_library().stmg3_solver_set_krylov(self._h, orthogonalization))
 
     def vcycle_all_at_once(self, b, x, n_intervals: int):
         f = self.finest
@@ -664,6 +722,6 @@ def exported_symbols() -> Sequence[str]:
     return sorted(set(re.findall(r"\b(stmg3?_[a-z_0-9]+)\s*\(", text)))
 
 
-__all__ = ["Context", "Level", "Solver", "Level3", "Solver3", "StmgError", "load_library", "plan_levels", "patch_info",
+__all__ = ["NcclComm", "ORTHO_MGS", "ORTHO_CGS2", "Context", "Level", "Solver", "Level3", "Solver3", "StmgError", "load_library", "plan_levels", "patch_info",
            "exported_symbols", "SMOOTHER_CELL", "SMOOTHER_VERTEX_STAR", "SMOOTHER_NONE", "PROBLEM_MANUFACTURED",
            "PROBLEM_CAVITY"]

@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = BUILD / "libstmg_b200.so"
 
-SOURCES = (["vmult.cu", "vanka.cu", "vanka_tc.cu", "aux_kernels.cu", "problems.cu", "stmg.cu", "setup.cpp", "st3d.cu", "setup3d.cpp", "stmg3d.cu"]
+SOURCES = (["vmult.cu", "vanka.cu", "vanka_tc.cu", "aux_kernels.cu", "problems.cu", "stmg.cu", "setup.cpp", "st3d.cu", "setup3d.cpp", "stmg3d.cu", "comm_nccl.cpp"]
            + [f"vmult_r{r}s{s}.cu" for r in (1, 2, 3, 4) for s in (1, 2, 3, 4, 5)])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
@@ -71,7 +71,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                     raise RuntimeError(f"nvcc failed for {futs[fut]}")
     objs = [str(BUILD / (n + ".o")) for n in SOURCES]
     if force or jobs or not LIB.exists():
-        cmd = [nvcc, *ARCH, *_host_cxx(), "-shared", "-o", str(LIB), *objs, "-lcudart"]
+        cmd = [nvcc, *ARCH, *_host_cxx(), "-shared", "-o", str(LIB), *objs, "-lcudart", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

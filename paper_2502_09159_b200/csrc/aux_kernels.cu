@@ -435,6 +435,73 @@ dot_final_kernel(const double *__restrict__ part, int np, double *__restrict__ o
     *out = s;
 }
 
+// Batched inner products <w, V_i>, i < m (and <w, w> in slot m when
+// with_norm), reading w once per chunk: one pass over the Krylov basis for a
+// classical Gram-Schmidt sweep. Fixed grid and fixed-order reductions, so the
+// result is bitwise reproducible.
+__global__ void __launch_bounds__(kDotThreads)
+multidot_partial_kernel(MultiVec V, int m, int with_norm, const double *__restrict__ w, long long n,
+                        double *__restrict__ part)
+{
+  double s[kMultiMax + 1];
+#pragma unroll
+  for (int i = 0; i <= kMultiMax; ++i)
+    s[i] = 0.0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n; k += stride)
+    {
+      const double wk = w[k];
+#pragma unroll
+      for (int i = 0; i < kMultiMax; ++i)
+        if (i < m)
+          s[i] = fma(wk, V.p[i][k], s[i]);
+      s[kMultiMax] = fma(wk, wk, s[kMultiMax]);
+    }
+  for (int i = 0; i <= m; ++i)
+    {
+      const int slot = i < m ? i : kMultiMax;
+      if (i == m && !with_norm)
+        break;
+      const double t = block_sum<kDotThreads>(s[slot]);
+      if (threadIdx.x == 0)
+        part[static_cast<long long>(i) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kDotThreads)
+multidot_final_kernel(const double *__restrict__ part, int np, double *__restrict__ out)
+{
+  const double *p = part + static_cast<long long>(blockIdx.x) * np;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x)
+    s += p[i];
+  s = block_sum<kDotThreads>(s);
+  if (threadIdx.x == 0)
+    out[blockIdx.x] = s;
+}
+
+// w += sign * sum_i c_i V_i, i < m, c on the device (c_dev) or the host
+// value array (c_host); one read of w and each V_i, one write of w.
+__global__ void
+multi_axpy_kernel(MultiVec V, int m, const double *__restrict__ c_dev, MultiCoef c_host, double sign,
+                  double *__restrict__ w, long long n)
+{
+  __shared__ double c[kMultiMax];
+  if (threadIdx.x < m)
+    c[threadIdx.x] = sign * (c_dev ? c_dev[threadIdx.x] : c_host.c[threadIdx.x]);
+  __syncthreads();
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n; k += stride)
+    {
+      double acc = w[k];
+#pragma unroll
+      for (int i = 0; i < kMultiMax; ++i)
+        if (i < m)
+          acc = fma(c[i], V.p[i][k], acc);
+      w[k] = acc;
+    }
+}
+
 __global__ void
 axpy_kernel(long long n, double alpha, const double *__restrict__ alpha_dev, double sign, const double *__restrict__ x,
             double *__restrict__ y)
@@ -552,6 +619,51 @@ launch_dot(const double *x, const double *y, long long n, double *part, double *
   const int nb = std::min<long long>(dot_partials(), std::max<long long>(1, (n + kDotThreads - 1) / kDotThreads));
   dot_partial_kernel<<<nb, kDotThreads, 0, st>>>(x, y, n, part);
   dot_final_kernel<<<1, kDotThreads, 0, st>>>(part, nb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_multidot(const double *const *V, int m, bool with_norm, const double *w, long long n, double *part,
+                double *out, cudaStream_t st)
+{
+  // out[i] = <w, V_i> (i < m), out[m] = <w, w> if with_norm; chunks of kMultiMax
+  const int nb = std::min<long long>(dot_partials(), std::max<long long>(1, (n + kDotThreads - 1) / kDotThreads));
+  for (int i0 = 0;; i0 += kMultiMax)
+    {
+      const int mm = std::min(kMultiMax, m - i0); // 0 when m == 0 (norm only)
+      const bool last = i0 + kMultiMax >= m;
+      const int wn = last && with_norm ? 1 : 0;
+      MultiVec mv{};
+      for (int i = 0; i < mm; ++i)
+        mv.p[i] = V[i0 + i];
+      if (mm + wn > 0)
+        {
+          multidot_partial_kernel<<<nb, kDotThreads, 0, st>>>(mv, mm, wn, w, n, part);
+          multidot_final_kernel<<<mm + wn, kDotThreads, 0, st>>>(part, nb, out + i0); // norm lands at out[m]
+        }
+      if (last)
+        break;
+    }
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_multi_axpy(const double *const *V, int m, const double *c_dev, const double *c_host, double sign, double *w,
+                  long long n, cudaStream_t st)
+{
+  for (int i0 = 0; i0 < m; i0 += kMultiMax)
+    {
+      MultiVec mv{};
+      MultiCoef mc{};
+      const int mm = std::min(kMultiMax, m - i0);
+      for (int i = 0; i < mm; ++i)
+        {
+          mv.p[i] = V[i0 + i];
+          if (c_host)
+            mc.c[i] = c_host[i0 + i];
+        }
+      multi_axpy_kernel<<<grid_for(n, 256), 256, 0, st>>>(mv, mm, c_dev ? c_dev + i0 : nullptr, mc, sign, w, n);
+    }
   return cudaGetLastError();
 }
 

@@ -136,6 +136,24 @@ cudaError_t launch_errors_manufactured(const DevGeom &G, int r, const ProblemTab
 cudaError_t launch_health(const DevGeom &G, double cell_area, const double *X, const double *Y, double *out,
                           int n_intervals, cudaStream_t st);
 int dot_partials();
+/// Batched Krylov kernels (classical Gram-Schmidt, final update): up to
+/// kMultiMax basis vectors per pass, chunked beyond.
+constexpr int kMultiMax = 16;
+struct MultiVec
+{
+  const double *p[kMultiMax];
+};
+struct MultiCoef
+{
+  double c[kMultiMax];
+};
+/// out[i] = <w, V_i> for i < m; out[m] = <w, w> when with_norm. `part`
+/// holds (kMultiMax + 1) * dot_partials() doubles. Deterministic.
+cudaError_t launch_multidot(const double *const *V, int m, bool with_norm, const double *w, long long n, double *part,
+                            double *out, cudaStream_t st);
+/// w += sign * sum_i c_i V_i with c on the device (c_dev) or host (c_host).
+cudaError_t launch_multi_axpy(const double *const *V, int m, const double *c_dev, const double *c_host, double sign,
+                              double *w, long long n, cudaStream_t st);
 cudaError_t launch_dot(const double *x, const double *y, long long n, double *part, double *out, cudaStream_t st);
 /// y += a x with a = alpha_dev ? sign * (*alpha_dev) : alpha (sign applies to
 /// the device-resident coefficient only).

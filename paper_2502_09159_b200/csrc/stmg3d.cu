@@ -6,6 +6,7 @@
 // time, and FGMRES over a time slab (time-slab partition through
 // stmg_comm_ops, as in 2D).
 #include "../../include/stmg_b200.h"
+#include "krylov.hpp"
 #include "runtime.hpp"
 #include "st3d.hpp"
 
@@ -275,6 +276,7 @@ struct stmg3_solver
   bool project_pressure = true;
   double rtol = 1e-8, atol = 1e-14;
   int max_iterations = 200;
+  int ortho = stmg_krylov::kMGS; // Arnoldi orthogonalization (stmg_solver_set_krylov)
   std::vector<std::unique_ptr<Solver3Level>> levels;
   DevArray<double> cG, cH, cB, cX;
   int coarse_n = 0;
@@ -503,7 +505,7 @@ struct stmg3_solver
     const int top = static_cast<int>(levels.size()) - 1;
     const long long n = L.spec.isz() * nI;
     w.resize(n);
-    part.resize(dot_partials());
+    part.resize(stmg_krylov::part_doubles());
     scal.resize(2 * (max_iterations + 2));
     hist.clear();
     const double norm_b = std::sqrt(dot(b_v, b_v, n, 0));
@@ -529,20 +531,10 @@ struct stmg3_solver
             DevArray<double> &zj = basis(Z, j, n);
             cycle(top, V[j]->p, zj.p, nI);
             coupled_vmult(top, zj.p, nullptr, w.p, nI, 0);
-            for (int i = 0; i <= j; ++i)
-              {
-                check(launch_dot(w.p, V[i]->p, n, part.p, scal.p + i, ctx->stream), "dot");
-                allreduce(scal.p + i, 1);
-                check(launch_axpy(n, 0.0, scal.p + i, -1.0, V[i]->p, w.p, ctx->stream), "axpy");
-                ctx->count(3);
-              }
-            check(launch_dot(w.p, w.p, n, part.p, scal.p + j + 1, ctx->stream), "dot");
-            allreduce(scal.p + j + 1, 1);
-            ctx->count(2);
-            check(cudaMemcpyAsync(hcol.data(), scal.p, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, ctx->stream),
-                  "d2h");
-            check(cudaStreamSynchronize(ctx->stream), "sync");
-            const double h_next = std::sqrt(hcol[j + 1]);
+            // Arnoldi: MGS (the reference's, solver.cpp:146-152) or CGS2
+            // (two batched all-reduces per iteration), krylov.hpp
+            const double h_next = stmg_krylov::orthogonalize(
+              ortho, V, j, w.p, n, part.p, scal.p, hcol, [&](double *buf, int cnt) { allreduce(buf, cnt); }, ctx);
             const bool breakdown = !(h_next > 1e-300);
             auto Hc = [&](int i) -> double & { return H[static_cast<size_t>(j) * (m + 1) + i]; };
             for (int i = 0; i <= j; ++i)
@@ -581,11 +573,7 @@ struct stmg3_solver
               s -= H[static_cast<size_t>(c) * (m + 1) + i] * y[c];
             y[i] = s / H[static_cast<size_t>(i) * (m + 1) + i];
           }
-        for (int i = 0; i < iters; ++i)
-          {
-            check(launch_axpy(n, y[i], nullptr, 1.0, Z[i]->p, x_v, ctx->stream), "axpy");
-            ctx->count();
-          }
+        stmg_krylov::update_solution(Z, y, x_v, n, ctx);
       }
     if (iterations)
       *iterations = iters;
@@ -958,6 +946,18 @@ stmg3_solver_level(stmg3_solver *s, int l)
   if (!s || l < 0 || l >= static_cast<int>(s->levels.size()))
     return nullptr;
   return s->levels[l]->level.get();
+}
+
+int
+stmg3_solver_set_krylov(stmg3_solver *s, int orthogonalization)
+{
+  return guarded([&] {
+    if (!s)
+      throw std::invalid_argument("stmg3_solver_set_krylov: null solver");
+    if (orthogonalization != STMG_ORTHO_MGS && orthogonalization != STMG_ORTHO_CGS2)
+      throw std::invalid_argument("stmg3_solver_set_krylov: unknown orthogonalization");
+    s->ortho = orthogonalization;
+  });
 }
 
 int

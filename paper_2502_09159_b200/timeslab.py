@@ -197,3 +197,29 @@ class LoopbackComm:
             for r, p in enumerate(parts):
                 out[r * n:(r + 1) * n].copy_(p)
         self._sync(stream)
+
+
+def nccl_comm(device: Optional[int] = None, group=None):
+    """The library's C++ NCCL communicator (``NcclComm``) for the ranks of a
+    torch.distributed process group: rank 0 makes the NCCL unique id, the
+    group broadcasts its 128 bytes once, every rank creates its communicator.
+    Afterwards every halo, all-reduce and all-gather of the all-at-once solve
+    is an NCCL call inside libstmg_b200 (no Python per exchange)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import NcclComm
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.cuda.current_device() if device is None else device
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(NcclComm.unique_id()), dtype=torch.uint8))
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        uid_dev = uid.to(f"cuda:{dev}")
+        dist.broadcast(uid_dev, 0, group=group)
+        uid = uid_dev.cpu()
+    else:
+        dist.broadcast(uid, 0, group=group)
+    return NcclComm(rank, world, dev, bytes(uid.numpy().tobytes()))
