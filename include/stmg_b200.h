@@ -317,6 +317,11 @@ int stmg3_level_destroy(stmg3_level *level);
 /* out[0..11] = n_slots, M^v, M^p, interval size, n_scalar, gx, gy, gz, n_p,
  * max patch size n_T, patch classes, sum of n_T^2 over the patches. */
 int stmg3_level_sizes(const stmg3_level *level, int64_t *out);
+/* Vanka patch setup of the level: out[0] seconds, out[1] 1 if the exact
+ * per-cell inverses were built on the GPU (deformed levels: element matrices,
+ * R_T S R_T^T and batched Gauss-Jordan inverses on the device), out[2] 1 if
+ * the undeformed class inverses stand in (affine_patches), out[3] classes. */
+int stmg3_level_patch_info(const stmg3_level *level, double *out);
 /* apply_block / apply_block_raw (st_operator.cpp:397-407) per interval. */
 int stmg3_apply_block(stmg3_level *level, const double *x, double *y, int n_intervals, int raw);
 /* All-at-once operator y_n = D x_n - Z C x_{n-1} (Eq. GloSys, st_operator.cpp:321-421). */

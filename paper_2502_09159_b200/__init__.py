@@ -105,6 +105,7 @@ _SIGNATURES = {
                             _c_int, _c_void_p, ctypes.POINTER(_c_void_p)], _c_int),
     "stmg3_level_destroy": ([_c_void_p], _c_int),
     "stmg3_level_sizes": ([_c_void_p, _c_i64p], _c_int),
+    "stmg3_level_patch_info": ([_c_void_p, ctypes.POINTER(_c_double)], _c_int),
     "stmg3_apply_block": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int], _c_int),
     "stmg3_vmult": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
     "stmg3_residual": ([_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, _c_int], _c_int),
@@ -544,6 +545,13 @@ class Level3:
 
     def _halo(self, t, name: str = "x_prev_slot"):
         return _ptr(t, self.n_velocity, self.ctx.device, name)
+
+    @property
+    def patch_setup(self) -> dict:
+        """Vanka patch setup: seconds, on_gpu (exact per-cell inverses built on the device), affine, classes."""
+        out = (ctypes.c_double * 4)()
+        _check(load_library().stmg3_level_patch_info(self._h, out))
+        return dict(seconds=out[0], on_gpu=bool(out[1]), affine=bool(out[2]), classes=int(out[3]))
 
     def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
         _check(load_library().stmg3_apply_block(self._h, self._v(x, n_intervals, "x"), self._v(y, n_intervals, "y"),

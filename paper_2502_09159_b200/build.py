@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = BUILD / "libstmg_b200.so"
 
-SOURCES = (["vmult.cu", "vanka.cu", "vanka_tc.cu", "aux_kernels.cu", "problems.cu", "stmg.cu", "setup.cpp", "st3d.cu", "setup3d.cpp", "stmg3d.cu", "comm_nccl.cpp"]
+SOURCES = (["vmult.cu", "vanka.cu", "vanka_tc.cu", "aux_kernels.cu", "problems.cu", "stmg.cu", "setup.cpp", "st3d.cu", "setup3d.cpp", "stmg3d.cu", "comm_nccl.cpp", "patch3_gpu.cu"]
            + [f"vmult_r{r}s{s}.cu" for r in (1, 2, 3, 4) for s in (1, 2, 3, 4, 5)])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

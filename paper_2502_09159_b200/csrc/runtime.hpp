@@ -117,6 +117,15 @@ struct DevArray
     g_reallocs.fetch_add(1, std::memory_order_relaxed);
   }
   void
+  release()
+  {
+    if (p)
+      cudaFree(p);
+    p = nullptr;
+    n = 0;
+    g_reallocs.fetch_add(1, std::memory_order_relaxed);
+  }
+  void
   upload(const std::vector<T> &h)
   {
     resize(h.size());

@@ -535,6 +535,69 @@ build_patches3(const Level3Spec &L, const std::vector<double> *verts)
   return ps;
 }
 
+Patch3Layout
+cell_patch_layouts3(const Level3Spec &L)
+{
+  const int N = L.n1(), p = L.p(), np = L.np(), S = L.S();
+  const int gx = L.gx(), gy = L.gy(), gz = L.gz();
+  const long long nsc = L.nsc(), mv = L.mv(), mp = L.mp();
+  std::vector<int> valence(static_cast<size_t>(nsc), 0);
+  for (int cz = 0; cz < L.nz; ++cz)
+    for (int cy = 0; cy < L.ny; ++cy)
+      for (int cx = 0; cx < L.nx; ++cx)
+        for (int k = 0; k < N; ++k)
+          for (int j = 0; j < N; ++j)
+            for (int i = 0; i < N; ++i)
+              valence[(static_cast<size_t>(cz * p + k) * gy + cy * p + j) * gx + cx * p + i]++;
+  auto on_bnd = [&](int X, int Y, int Z) {
+    return X == 0 || Y == 0 || Z == 0 || X == gx - 1 || Y == gy - 1 || Z == gz - 1;
+  };
+  Patch3Layout Lo;
+  const long long nc = L.ncells();
+  Lo.nt.resize(nc);
+  Lo.nvel.resize(nc);
+  Lo.rel_off.resize(nc + 1);
+  Lo.inv_off.resize(nc + 1);
+  Lo.rel_off[0] = Lo.inv_off[0] = 0;
+  std::vector<int> loc;
+  for (int cz = 0; cz < L.nz; ++cz)
+    for (int cy = 0; cy < L.ny; ++cy)
+      for (int cx = 0; cx < L.nx; ++cx)
+        {
+          const long long c = (static_cast<long long>(cz) * L.ny + cy) * L.nx + cx;
+          loc.clear();
+          for (int k = 0; k < N; ++k) // cell_patch: unconstrained nodes, lexicographic
+            for (int j = 0; j < N; ++j)
+              for (int i = 0; i < N; ++i)
+                if (!on_bnd(cx * p + i, cy * p + j, cz * p + k))
+                  loc.push_back((k * N + j) * N + i);
+          const int nl = static_cast<int>(loc.size());
+          for (int a = 0; a < S; ++a)
+            for (int comp = 0; comp < 3; ++comp)
+              for (int t = 0; t < nl; ++t)
+                {
+                  const int i = loc[t] % N, j = (loc[t] / N) % N, k = loc[t] / (N * N);
+                  Lo.rel.push_back(a * mv + comp * nsc + (static_cast<long long>(k) * gy + j) * gx + i);
+                  const long long sn = (static_cast<long long>(cz * p + k) * gy + cy * p + j) * gx + cx * p + i;
+                  Lo.weight.push_back(1.0 / valence[sn]);
+                }
+          for (int a = 0; a < S; ++a)
+            for (int l = 0; l < np; ++l)
+              {
+                Lo.rel.push_back(a * mp + l);
+                Lo.weight.push_back(1.0);
+              }
+          const int n = S * (3 * nl + np);
+          Lo.nt[c] = n;
+          Lo.nvel[c] = S * 3 * nl;
+          Lo.rel_off[c + 1] = Lo.rel_off[c] + n;
+          Lo.inv_off[c + 1] = Lo.inv_off[c] + static_cast<long long>(n) * n;
+          Lo.total_matrix_elements += static_cast<std::uint64_t>(n) * n;
+          Lo.max_nt = std::max(Lo.max_nt, n);
+        }
+  return Lo;
+}
+
 // ================================================================ transfers
 Transfer3Tables
 build_transfer3(const Level3Spec &c, const Level3Spec &f, bool h_time)

@@ -101,6 +101,33 @@ struct Patch3Set
 };
 Patch3Set build_patches3(const Level3Spec &L, const std::vector<double> *verts);
 
+/// Dof layout of every cell patch (one class per cell), without matrices:
+/// the host half of the GPU patch setup (patch3_gpu.cu). rel / weight are
+/// concatenated per cell (rel_off[c] .. rel_off[c] + nt[c]); the inverses go
+/// to inv_off[c] (sum of the previous nt^2).
+struct Patch3Layout
+{
+  std::vector<int> nt, nvel;
+  std::vector<long long> rel_off, inv_off;
+  std::vector<long long> rel;
+  std::vector<double> weight;
+  std::uint64_t total_matrix_elements = 0;
+  int max_nt = 0;
+};
+Patch3Layout cell_patch_layouts3(const Level3Spec &L);
+
+/// GPU setup of the exact per-cell patch inverses (patch3_gpu.cu): element
+/// matrices into E (ncells x elem3_stride(r) doubles), patch matrices and
+/// their in-place Gauss-Jordan inverses into Aall. *status (device) stays 0
+/// on success; 1 = vanishing pivot, 2 = inverted cell, 3 = layout mismatch.
+long long elem3_stride(int r);
+cudaError_t launch_patch3_setup(const Level3Consts &P, int r, int S, double *E, double *Aall, const long long *aoff,
+                                const int *ntv, int max_nt, long long ncells, int *status, cudaStream_t st);
+/// Batched in-place inverse of `count` dense row-major matrices (sizes ntv,
+/// offsets aoff), pivot-free blocked Gauss-Jordan on the FP64 tensor path.
+cudaError_t launch_gj_inverse(double *Aall, const long long *aoff, const int *ntv, int count, int max_nt, int *status,
+                              cudaStream_t st);
+
 /// Transfer between 3D levels: spatial h (1D stencils per direction and
 /// pressure child blocks), spatial p (interpolation + modal embedding), none;
 /// temporal p (E) and/or temporal h (E_left / E_right, PAPER.md Eq. DeftPrRe).

@@ -7,6 +7,8 @@
 // stmg_comm_ops, as in 2D).
 #include "../../include/stmg_b200.h"
 #include "krylov.hpp"
+#include <chrono>
+#include <cstdlib>
 #include "runtime.hpp"
 #include "st3d.hpp"
 
@@ -60,6 +62,12 @@ struct stmg3_level
   // Vanka: classes, colour batches (8 parity colours), anchors
   std::vector<DevArray<long long>> cls_rel;
   std::vector<DevArray<double>> cls_weight, cls_inverse;
+  // exact per-cell patches built on the GPU (deformed levels, patch3_gpu.cu):
+  // concatenated dof offsets, weights and inverses
+  DevArray<long long> rel_all;
+  DevArray<double> weight_all, inv_all;
+  bool gpu_patches = false;
+  double patch_setup_s = 0.0;
   DevArray<DevPatchClass> classes;
   DevArray<VankaBatch> batches;
   DevArray<long long> vel_anchor, pre_anchor;
@@ -187,22 +195,86 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
   // affine_patches: the patch inverses of the undeformed (Cartesian) mesh
   // stand in for the per-cell ones on a deformed mesh (same dof patterns;
   // an approximate local solve)
-  const Patch3Set ps = build_patches3(s, (L.deformed && !affine_patches) ? &L.verts_h : nullptr);
   L.affine_patches = L.deformed && affine_patches;
-  L.n_classes = static_cast<int>(ps.classes.size());
-  L.max_nt = ps.max_nt;
-  L.total_matrix_elements = ps.total_matrix_elements;
-  std::vector<DevPatchClass> dc(ps.classes.size());
-  L.cls_rel.resize(ps.classes.size());
-  L.cls_weight.resize(ps.classes.size());
-  L.cls_inverse.resize(ps.classes.size());
-  for (size_t i = 0; i < ps.classes.size(); ++i)
+  std::vector<int> cell_class;
+  std::vector<DevPatchClass> dc;
+  // Deformed levels with exact patches: one class per cell, set up on the
+  // GPU (element matrices, R_T S R_T^T, batched Gauss-Jordan inverses); the
+  // host path (LU with partial pivoting, setup3d.cpp cell_patch) remains for
+  // 1-cell directions (singular whole-domain patches), a vanishing pivot,
+  // and as the A/B switch STMG_PATCH3_HOST.
+  const bool exact = L.deformed && !affine_patches;
+  bool gpu_done = false;
+  if (exact && s.nx >= 2 && s.ny >= 2 && s.nz >= 2 && (s.r == 1 || s.r == 2) && !std::getenv("STMG_PATCH3_HOST"))
     {
-      const PatchClass &pc = ps.classes[i];
-      L.cls_rel[i].upload(pc.rel);
-      L.cls_weight[i].upload(pc.weight);
-      L.cls_inverse[i].upload(pc.inverse);
-      dc[i] = DevPatchClass{pc.n_t, pc.n_vel, L.cls_rel[i].p, L.cls_weight[i].p, L.cls_inverse[i].p, 0, 0, nullptr};
+      const auto t0 = std::chrono::steady_clock::now();
+      const Patch3Layout lo = cell_patch_layouts3(s);
+      const long long nc = s.ncells();
+      L.rel_all.upload(lo.rel);
+      L.weight_all.upload(lo.weight);
+      L.inv_all.resize(static_cast<size_t>(lo.inv_off.back()));
+      DevArray<long long> aoff;
+      aoff.upload(std::vector<long long>(lo.inv_off.begin(), lo.inv_off.end() - 1));
+      DevArray<int> ntv, st;
+      ntv.upload(lo.nt);
+      st.upload(std::vector<int>{0});
+      {
+        DevArray<double> E;
+        E.resize(static_cast<size_t>(nc) * elem3_stride(s.r));
+        check(launch_patch3_setup(L.consts, s.r, s.S(), E.p, L.inv_all.p, aoff.p, ntv.p, lo.max_nt, nc, st.p,
+                                  L.ctx->stream),
+              "patch3_setup");
+        L.ctx->count(3);
+        check(cudaStreamSynchronize(L.ctx->stream), "patch3_setup");
+      }
+      int status = 0;
+      check(cudaMemcpy(&status, st.p, sizeof(int), cudaMemcpyDeviceToHost), "status");
+      if (status == 2)
+        throw std::runtime_error("3D level: inverted cell");
+      if (status == 0)
+        {
+          cell_class.resize(nc);
+          dc.resize(nc);
+          for (long long c = 0; c < nc; ++c)
+            {
+              cell_class[c] = static_cast<int>(c);
+              dc[c] = DevPatchClass{lo.nt[c], lo.nvel[c], L.rel_all.p + lo.rel_off[c], L.weight_all.p + lo.rel_off[c],
+                                    L.inv_all.p + lo.inv_off[c], 0, 0, nullptr};
+            }
+          L.n_classes = static_cast<int>(nc);
+          L.max_nt = lo.max_nt;
+          L.total_matrix_elements = lo.total_matrix_elements;
+          L.gpu_patches = gpu_done = true;
+        }
+      else
+        {
+          L.inv_all.release();
+          L.rel_all.release();
+          L.weight_all.release();
+        }
+      L.patch_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  if (!gpu_done)
+    {
+      const auto t0 = std::chrono::steady_clock::now();
+      const Patch3Set ps = build_patches3(s, exact ? &L.verts_h : nullptr);
+      L.n_classes = static_cast<int>(ps.classes.size());
+      L.max_nt = ps.max_nt;
+      L.total_matrix_elements = ps.total_matrix_elements;
+      cell_class = ps.cell_class;
+      dc.resize(ps.classes.size());
+      L.cls_rel.resize(ps.classes.size());
+      L.cls_weight.resize(ps.classes.size());
+      L.cls_inverse.resize(ps.classes.size());
+      for (size_t i = 0; i < ps.classes.size(); ++i)
+        {
+          const PatchClass &pc = ps.classes[i];
+          L.cls_rel[i].upload(pc.rel);
+          L.cls_weight[i].upload(pc.weight);
+          L.cls_inverse[i].upload(pc.inverse);
+          dc[i] = DevPatchClass{pc.n_t, pc.n_vel, L.cls_rel[i].p, L.cls_weight[i].p, L.cls_inverse[i].p, 0, 0, nullptr};
+        }
+      L.patch_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
   L.classes.upload(dc);
   // 8 parity colours: cells of one colour share no node, so a launch writes
@@ -214,11 +286,11 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
   for (int col = 0; col < 8; ++col)
     {
       L.colour_first.push_back(static_cast<int>(batches.size()));
-      std::vector<std::vector<long long>> by_class(ps.classes.size());
+      std::vector<std::vector<long long>> by_class(dc.size());
       for (int cz = col >> 2; cz < s.nz; cz += 2)
         for (int cy = (col >> 1) & 1; cy < s.ny; cy += 2)
           for (int cx = col & 1; cx < s.nx; cx += 2)
-            by_class[ps.cell_class[(static_cast<size_t>(cz) * s.ny + cy) * s.nx + cx]].push_back(
+            by_class[cell_class[(static_cast<size_t>(cz) * s.ny + cy) * s.nx + cx]].push_back(
               (static_cast<long long>(cz) * s.ny + cy) * s.nx + cx);
       for (size_t c = 0; c < by_class.size(); ++c)
         for (size_t i = 0; i < by_class[c].size(); i += cols)
@@ -724,6 +796,19 @@ stmg3_level_sizes(const stmg3_level *L, int64_t *out)
     const int64_t v[12] = {s.S(), s.mv(), s.mp(), s.isz(), s.nsc(), s.gx(), s.gy(), s.gz(), s.np(), L->max_nt,
                            L->n_classes, static_cast<int64_t>(L->total_matrix_elements)};
     std::memcpy(out, v, sizeof(v));
+  });
+}
+
+int
+stmg3_level_patch_info(const stmg3_level *L, double *out)
+{
+  return guarded([&] {
+    if (!L || !out)
+      throw std::invalid_argument("stmg3_level_patch_info: null argument");
+    out[0] = L->patch_setup_s;
+    out[1] = L->gpu_patches ? 1.0 : 0.0;
+    out[2] = L->affine_patches ? 1.0 : 0.0;
+    out[3] = static_cast<double>(L->n_classes);
   });
 }
 

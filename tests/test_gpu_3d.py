@@ -307,3 +307,37 @@ def test_3d_status_codes(stmg, ctx):
     with pytest.raises(stmg.StmgError) as e:
         S.solve_all_at_once(F, F.clone(), 3)  # 3 intervals cannot halve in time
     assert e.value.code == 1
+
+
+@pytest.mark.parametrize("nx,ny,nz,r,k", [(2, 2, 2, 1, 1), (3, 2, 2, 2, 2), (2, 3, 2, 1, 2), (2, 2, 3, 2, 1)])
+def test_gpu_patch_setup_matches_host_and_oracle(stmg, ctx, oracle, nx, ny, nz, r, k):
+    """Deformed levels build their exact per-cell patch inverses on the GPU
+    (element matrices, R_T S R_T^T, batched Gauss-Jordan; patch3_gpu.cu):
+    the smoother step equals the host-built one (LU with partial pivoting,
+    STMG_PATCH3_HOST) and the oracle's (vanka.cpp:30-233) to <= 1e-10."""
+    import os
+
+    verts = o3.vertices(nx, ny, nz, 0.1, seed=21)
+    tau = 1.0 / 8
+    gpu = stmg.Level3(ctx, nx, ny, nz, r, k, tau, 1.0, 1.0, stmg.SMOOTHER_CELL, vertices=verts)
+    assert gpu.patch_setup["on_gpu"] and gpu.patch_setup["classes"] == nx * ny * nz
+    os.environ["STMG_PATCH3_HOST"] = "1"
+    try:
+        hst = stmg.Level3(ctx, nx, ny, nz, r, k, tau, 1.0, 1.0, stmg.SMOOTHER_CELL, vertices=verts)
+    finally:
+        del os.environ["STMG_PATCH3_HOST"]
+    assert not hst.patch_setup["on_gpu"]
+    ref = o3.OracleLevel3(nx, ny, nz, r, k, tau, 1.0, 1.0, vertices=verts)
+    rng = np.random.default_rng(22)
+    n = 3
+    u = rng.uniform(-1, 1, n * ref.size)
+    b = rng.uniform(-1, 1, n * ref.size)
+    halo = rng.uniform(-1, 1, ref.mv)
+    ur = ref.smooth_step_all(b, u, 0.8, n, halo)
+    outs = []
+    for lvl in (gpu, hst):
+        ug = _cuda(u)
+        lvl.smooth_step(_cuda(b), ug, 0.8, n, _cuda(halo), coupled=True)
+        outs.append(ug.cpu().numpy())
+        assert _rel(outs[-1], ur) <= 1e-10
+    assert _rel(outs[0], outs[1]) <= 1e-10

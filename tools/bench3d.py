@@ -144,7 +144,9 @@ def run_c5_solve(torch, stmg, args):
     ctx = stmg.Context(0)
     t0 = time.perf_counter()
     sol = stmg.Solver3(ctx, n, n, n, 2, 2, 1.0 / N, 1.0, 1.0, n_hcoarse=4, time_coarsen=False,
-                       k_min=2 if args.c5_variant == "robust" else 0, vertices=verts, affine_patches=True, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
+                       k_min=2 if args.c5_variant == "robust" else 0, vertices=verts,
+                       affine_patches=getattr(args, "c5_patches", "exact") == "affine", nu1=2, nu2=2, rtol=1e-8,
+                       max_iterations=args.maxit)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     f = sol.finest
@@ -167,7 +169,10 @@ def run_c5_solve(torch, stmg, args):
     return {"dofs": N * f.size, "seconds": s, "dofs_per_s": N * f.size / s, "setup_s": setup,
             "fgmres_iterations_per_slab": its, "levels": sol.level_info,
             "partition": f"1 GPU, {nsl} macro steps x {slab} intervals",
-            "smoother": "cell Vanka, undeformed patch inverses (affine_patches)", "variant": args.c5_variant}
+            "smoother": ("cell Vanka, undeformed patch inverses (affine_patches)"
+                         if getattr(args, "c5_patches", "exact") == "affine" else
+                         "cell Vanka, exact per-cell patch inverses (built on the GPU)"),
+            "patch_setup": [l.patch_setup for l in sol.levels[1:]], "variant": args.c5_variant}
 
 
 def run_c5(torch, stmg, args):
@@ -200,6 +205,7 @@ def main():
     ap.add_argument("--maxit", type=int, default=200)
     ap.add_argument("--c5-slab", type=int, default=16)
     ap.add_argument("--c5-variant", default="robust", choices=["robust", "spec"])
+    ap.add_argument("--c5-patches", default="exact", choices=["exact", "affine"])
     args = ap.parse_args()
     import torch
     import paper_2502_09159_b200 as stmg
