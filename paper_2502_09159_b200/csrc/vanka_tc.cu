@@ -20,6 +20,8 @@
 //    block's colour sub-phases, so every red.add lands in a fixed order.
 #include "kernels.hpp"
 
+#include <cstdlib>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace stmg_b200
@@ -48,6 +50,8 @@ constexpr int kTSlot = kTCols * kTLd;
 #endif
 constexpr int kTMaxTiles = STMG_VANKA_MAXTILES; // tiles per block (host falls back beyond)
 constexpr int kTRing = 3; // ring slots of the full/empty mbarrier pipeline (vanka_tc_kernel)
+constexpr size_t kDSmem = sizeof(double) * kTRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * 12) +
+                          8 * sizeof(unsigned long long); // vanka_dfr_kernel
 constexpr size_t kTSmem =
   sizeof(double) * kTRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4)) + 8 * sizeof(unsigned long long);
 
@@ -104,6 +108,14 @@ mbar_wait(unsigned long long *bar, unsigned parity)
                  smem_u32(bar)),
                "r"(parity)
                : "memory");
+}
+
+// fire-and-forget atomic add (atomicAdd may compile to ATOMG with a return
+// register, which serialises a single warp's scatter on the round trips)
+__device__ __forceinline__ void
+red_add(double *addr, double v)
+{
+  asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(addr), "d"(v) : "memory");
 }
 
 __device__ __forceinline__ void
@@ -324,6 +336,222 @@ vanka_tc_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__re
     }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
+
+// ------------------------------------------------------- deferred scatter
+// (anchors and relative offsets may be negative: vertex stars at the domain
+// boundary anchor outside it, so masks use sentinels, not the sign)
+constexpr long long kMaskedCol = -(1LL << 62);
+constexpr int kMaskedRow = -(1 << 30);
+// vanka_tc_kernel with the scatter of tile lt-1 interleaved into the DMMA
+// k-loop of tile lt: each thread's 8 red.adds of the previous tile ride
+// between the first 8 k-steps of the current one, so no warp leaves the
+// tensor pipe for a separate scatter phase (the all-warp kernel runs its
+// gather / scatter in near lockstep across warps, which idles the pipe).
+// Column data is a 64-bit velocity offset (kMaskedCol: masked) plus the
+// 32-bit pressure - velocity distance; class rows become a pointer, a mask
+// and a weight, so the interleaved scatter costs a few integer ops per red.
+template <int KS>
+__global__ void __launch_bounds__(kTThreads, 1)
+vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__restrict__ tiles,
+                 const long long *__restrict__ va, const long long *__restrict__ pa, const int *__restrict__ tile_ptr,
+                 int ng_full, const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals,
+                 double omega)
+{
+  extern __shared__ __align__(16) double ring[];
+  long long *s_colv = reinterpret_cast<long long *>(ring + kTRing * kTSlot);
+  int *s_dp = reinterpret_cast<int *>(s_colv + kTMaxTiles * kTCols);
+  VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_dp + kTMaxTiles * kTCols);
+  unsigned long long *s_bar = reinterpret_cast<unsigned long long *>(s_tile + kTMaxTiles);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = tile_ptr[blockIdx.x], t1 = tile_ptr[blockIdx.x + 1];
+  const int nb = t1 - t0;
+  const int n0 = blockIdx.y * ng_full;
+  const long long base0 = n0 * isz;
+
+  for (int e = tid; e < nb; e += kTThreads)
+    s_tile[e] = tiles[t0 + e];
+  for (int e = tid; e < nb * kTCols; e += kTThreads)
+    {
+      const VankaTile tl = tiles[t0 + e / kTCols];
+      const int j = e % kTCols;
+      const int q = tl.c0 + j, nl = q % ng_full;
+      if (j < tl.ncols && n0 + nl < n_intervals)
+        {
+          const int patch = tl.pfirst + q / ng_full;
+          s_colv[e] = nl * isz + va[patch];
+          s_dp[e] = static_cast<int>(pa[patch] - va[patch]);
+        }
+      else
+        {
+          s_colv[e] = kMaskedCol;
+          s_dp[e] = 0;
+        }
+    }
+  __syncthreads();
+
+  constexpr int QN = kTRows / 32;
+  constexpr int CN = kTCols / (kTThreads / 32);
+  int cls_issue = -1;
+  int relq[QN], pmq[QN]; // relq == kMaskedRow: row beyond the class's patch size
+  auto issue = [&](int lt, int s) {
+    if (lt >= nb)
+      return;
+    const VankaTile tl = s_tile[lt];
+    if (tl.ncols == 0)
+      return;
+    if (tl.cls != cls_issue)
+      {
+        const DevPatchClass pc = classes[tl.cls];
+#pragma unroll
+        for (int q = 0; q < QN; ++q)
+          {
+            const int rw = lane + 32 * q;
+            relq[q] = rw < pc.n_t ? static_cast<int>(pc.rel[rw]) : kMaskedRow;
+            pmq[q] = (rw < pc.n_t && rw >= pc.n_vel) ? -1 : 0;
+          }
+        cls_issue = tl.cls;
+      }
+    double *slot = ring + s * kTSlot + lane;
+#pragma unroll
+    for (int cc = 0; cc < CN; ++cc)
+      {
+        const int col = warp + cc * (kTThreads / 32);
+        const int ci = lt * kTCols + col;
+        const long long cv = s_colv[ci];
+        const bool colok = cv != kMaskedCol;
+        const double *pv = r + (base0 + (colok ? cv : 0));
+        const int dp = s_dp[ci];
+#pragma unroll
+        for (int q = 0; q < QN; ++q)
+          {
+            const bool ok = colok && relq[q] != kMaskedRow;
+            cp_async8z(slot + col * kTLd + 32 * q, pv + (ok ? relq[q] + (dp & pmq[q]) : 0), ok);
+          }
+      }
+  };
+  unsigned long long *full = s_bar, *empty = s_bar + 3, *pdone = s_bar + 6;
+  if (tid == 0)
+    {
+      for (int i = 0; i < 3; ++i)
+        {
+          mbar_init(full + i, kTThreads);
+          mbar_init(empty + i, kTThreads);
+        }
+      mbar_init(pdone + 0, kTThreads);
+      mbar_init(pdone + 1, kTThreads);
+    }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  issue(0, 0);
+  cp_async_mbar_arrive(full + 0);
+  issue(1, 1);
+  cp_async_mbar_arrive(full + 1);
+
+  int loaded = -1, nt_loaded = 0;
+  double afr[KS];
+  const int row = 8 * warp + (lane >> 2);
+  // class row of this thread: u + base0 + rel (pointer), pressure mask
+  double *c_ub = u, *p_ub = u;
+  int c_pm = 0, p_pm = 0;
+  bool c_ok = false;
+  // pending tile (scattered inside the next tile's k-loop)
+  double pacc[kTCols / 8][2];
+  int p_lt = -1;
+  auto scatter_one = [&](int j) {
+    const int ct = j >> 1, b = j & 1;
+    const int ci = p_lt * kTCols + 8 * ct + 2 * (lane & 3) + b;
+    const long long cv = s_colv[ci];
+    if (cv != kMaskedCol)
+      red_add(p_ub + (cv + (s_dp[ci] & p_pm)), pacc[ct][b]);
+  };
+  int prev_phase = -1, transitions = 0;
+  for (int lt = 0; lt < nb; ++lt)
+    {
+      const int slot = lt % 3;
+      mbar_wait(full + slot, (lt / 3) & 1);
+      const VankaTile tl = s_tile[lt];
+      double acc[kTCols / 8][2];
+#pragma unroll
+      for (int ct = 0; ct < kTCols / 8; ++ct)
+        acc[ct][0] = acc[ct][1] = 0.0;
+      if (tl.ncols > 0 && tl.cls != loaded)
+        {
+          const DevPatchClass pc = classes[tl.cls];
+          c_ok = row < pc.n_t;
+          // the valence weight and omega are folded into the inverse's row:
+          // no DMUL per scattered value on the FP64 pipe the DMMAs saturate
+          const double wrow = c_ok ? omega * pc.weight[row] : 0.0;
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk)
+            {
+              const int col = 4 * kk + (lane & 3);
+              afr[kk] = (c_ok && col < pc.n_t) ? wrow * __ldg(pc.inverse + row * pc.n_t + col) : 0.0;
+            }
+          c_pm = (c_ok && row >= pc.n_vel) ? -1 : 0;
+          c_ub = u + (base0 + (c_ok ? pc.rel[row] : 0));
+          nt_loaded = pc.n_t;
+          loaded = tl.cls;
+        }
+      const bool mine = tl.ncols > 0 && 8 * warp < nt_loaded;
+      if (mine)
+        {
+          const double *bbase = ring + slot * kTSlot + (lane >> 2) * kTLd + (lane & 3);
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk)
+            {
+              const double *brow = bbase + 4 * kk;
+              constexpr int kNStep = 8 * kTLd;
+#pragma unroll
+              for (int ct = 0; ct < kTCols / 8; ++ct)
+                dmma(acc[ct], afr[kk], brow[kNStep * ct]);
+              if (kk < 2 * (kTCols / 8) && p_lt >= 0)
+                scatter_one(kk);
+            }
+          if (KS < 2 * (kTCols / 8) && p_lt >= 0)
+#pragma unroll
+            for (int j = KS; j < 2 * (kTCols / 8); ++j)
+              scatter_one(j);
+        }
+      else if (p_lt >= 0)
+#pragma unroll
+        for (int j = 0; j < 2 * (kTCols / 8); ++j)
+          scatter_one(j);
+      mbar_arrive(empty + slot);
+      // the previous tile's scatters are done: a new colour sub-phase may
+      // start scattering only after every thread got here (deterministic order)
+      if (prev_phase >= 0 && tl.phase != prev_phase)
+        {
+          unsigned long long *pd = pdone + (transitions & 1);
+          mbar_arrive(pd);
+          mbar_wait(pd, (transitions >> 1) & 1);
+          ++transitions;
+        }
+      prev_phase = tl.phase;
+      p_lt = (tl.ncols > 0 && c_ok) ? lt : -1;
+#pragma unroll
+      for (int ct = 0; ct < kTCols / 8; ++ct)
+        {
+          pacc[ct][0] = acc[ct][0];
+          pacc[ct][1] = acc[ct][1];
+        }
+      p_ub = c_ub;
+      p_pm = c_pm;
+      if (lt + 2 < nb)
+        {
+          const int ns = (lt + 2) % 3;
+          if (lt >= 1)
+            mbar_wait(empty + ns, ((lt - 1) / 3) & 1);
+          issue(lt + 2, ns);
+          cp_async_mbar_arrive(full + ns);
+        }
+    }
+  if (p_lt >= 0)
+#pragma unroll
+    for (int j = 0; j < 2 * (kTCols / 8); ++j)
+      scatter_one(j);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- factored
 // Time-diagonalised patch solves: A_T^{-1} = (V (x) I) blockdiag(B_b^{-1})
 // (W (x) I) (setup.hpp TemporalEigen). Per tile: stage 1 mixes the slots of
@@ -587,6 +815,34 @@ launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long
     kern<<<grid, kTThreads, kTSmem, stream>>>(classes, tiles, va, pa, tile_ptr, ng_full, r, u, isz, n_intervals,
                                               omega);
   };
+  // deferred-scatter kernel by default (A/B switch STMG_VANKA_KERNEL=tc)
+  static const int variant = [] {
+    const char *e = std::getenv("STMG_VANKA_KERNEL");
+    return (e && std::string(e) == "tc") ? 0 : 1;
+  }();
+  auto gd = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDSmem));
+    kern<<<grid, kTThreads, kDSmem, stream>>>(classes, tiles, va, pa, tile_ptr, ng_full, r, u, isz, n_intervals,
+                                              omega);
+  };
+  if (variant == 1)
+    {
+      if (ks <= 8)
+        gd(vanka_dfr_kernel<8>);
+      else if (ks <= 12)
+        gd(vanka_dfr_kernel<12>);
+      else if (ks <= 16)
+        gd(vanka_dfr_kernel<16>);
+      else if (ks <= 20)
+        gd(vanka_dfr_kernel<20>);
+      else if (ks <= 24)
+        gd(vanka_dfr_kernel<24>);
+      else if (ks <= 29)
+        gd(vanka_dfr_kernel<29>);
+      else
+        gd(vanka_dfr_kernel<32>);
+      return cudaGetLastError();
+    }
   if (ks <= 8)
     go(vanka_tc_kernel<8>);
   else if (ks <= 12)
