@@ -371,6 +371,49 @@ int stmg3_vcycle_all_at_once(stmg3_solver *solver, const double *b, double *x, i
 int stmg3_solve_all_at_once(stmg3_solver *solver, const double *F, double *X, int n_intervals, const double *v_init,
                             int *iterations, double *residual_history, int history_cap);
 
+/* ------------------------------------------------------------ C5 hybrid split
+ * Spatial partition of the 3D all-at-once solve into z_parts slabs of cells
+ * along z (BASELINE C5: 2 spatial x 4 temporal on 8 GPUs; SURVEY.md §8e,
+ * PAPER.md:1013-1014 runs the reference's method under MPI). Part p owns the
+ * cells cz in [p nz/z_parts, (p+1) nz/z_parts) of every level and stores its
+ * own sub-mesh as a complete level: velocity nodes of the interface plane it
+ * shares with a neighbour are stored by both parts and kept equal.
+ *   - vmult / residual: each part applies its cells, then the parts sum the
+ *     interface planes (owner-accumulate; residual r = r_own + r_nb - b);
+ *   - Vanka: patches of owned cells; their matrices include the neighbour's
+ *     cells across the interface (ghost cell layer, setup only) and interface
+ *     weights count the patches of both parts; the interface increments of
+ *     both parts are exchanged and added to the pre-sweep values;
+ *   - restriction: interface residuals are halved, restricted and the coarse
+ *     interface planes summed; prolongation is local;
+ *   - per-slot pressure means and Krylov inner products are summed over the
+ *     parts (the shared plane counted once);
+ *   - the coarsest level gathers its parts and solves globally.
+ * Needs deformed-geometry levels (`vertices`, the GLOBAL (nx+1)(ny+1)(nz+1) x 3
+ * array) with exact GPU-built patches, nz divisible by z_parts at every level
+ * and >= 2 local cells per direction on smoothed levels. Time slabs still go
+ * through stmg3_solver_set_comm (the communicator of the ranks holding the
+ * same part); the part's neighbours through stmg3_solver_set_space_comm. */
+typedef struct stmg_comm_space_ops {
+    void *user;
+    int part;  /* this rank's z part */
+    int parts; /* z parts */
+    /* Send the interface plane shared with part-1 (send_lo) and part+1
+     * (send_hi), receive theirs (recv_lo / recv_hi); absent sides are NULL.
+     * n doubles per plane, stream-ordered on `stream`. */
+    int (*exchange_planes)(void *user, const double *send_lo, double *recv_lo, const double *send_hi,
+                           double *recv_hi, int64_t n, void *stream);
+    int (*allreduce_sum)(void *user, double *buf, int64_t n, void *stream); /* over the parts */
+    int (*allgather)(void *user, const double *send, double *recv, int64_t n, void *stream); /* part order */
+} stmg_comm_space_ops;
+int stmg3_solver_create_split(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
+                              int n_hcoarse, int time_coarsen, int k_min, const double *vertices, int z_parts,
+                              int z_part, int nu1, int nu2, double omega, double rtol, double atol, int max_iterations,
+                              stmg3_solver **out);
+int stmg3_solver_set_space_comm(stmg3_solver *solver, const stmg_comm_space_ops *ops);
+/* Space ops over an NCCL communicator of the z parts (rank = part). */
+int stmg_comm_nccl_space_ops(stmg_comm *comm, stmg_comm_space_ops *ops_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -128,6 +128,11 @@ _SIGNATURES = {
     "stmg3_vcycle_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int], _c_int),
     "stmg3_solve_all_at_once": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p, ctypes.POINTER(_c_int),
                                  ctypes.POINTER(_c_double), _c_int], _c_int),
+    "stmg3_solver_create_split": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double,
+                                   _c_double, _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_int, _c_int, _c_int,
+                                   _c_double, _c_double, _c_double, _c_int, ctypes.POINTER(_c_void_p)], _c_int),
+    "stmg3_solver_set_space_comm": ([_c_void_p, _c_void_p], _c_int),
+    "stmg_comm_nccl_space_ops": ([_c_void_p, _c_void_p], _c_int),
 }
 
 
@@ -197,6 +202,16 @@ class _CommOps(ctypes.Structure):
                 ("allreduce_sum", _REDUCE_FN), ("allgather", _HALO_FN)]
 
 
+_PLANES_FN = ctypes.CFUNCTYPE(_c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int64,
+                              _c_void_p)
+
+
+class _SpaceOps(ctypes.Structure):
+    """struct stmg_comm_space_ops (include/stmg_b200.h): the z parts of the C5 hybrid split."""
+    _fields_ = [("user", _c_void_p), ("part", _c_int), ("parts", _c_int), ("exchange_planes", _PLANES_FN),
+                ("allreduce_sum", _REDUCE_FN), ("allgather", _HALO_FN)]
+
+
 def _guard(fn):
     """Callbacks must not raise into C: map exceptions to a non-zero status."""
     def wrapped(*args):
@@ -236,6 +251,12 @@ class NcclComm:
     def ops(self) -> "_CommOps":
         ops = _CommOps()
         _check(load_library().stmg_comm_nccl_ops(self._h, ctypes.byref(ops)))
+        return ops
+
+    def space_ops(self) -> "_SpaceOps":
+        """The same communicator as the z parts of a hybrid split (rank = part)."""
+        ops = _SpaceOps()
+        _check(load_library().stmg_comm_nccl_space_ops(self._h, ctypes.byref(ops)))
         return ops
 
     def __del__(self):
@@ -603,14 +624,23 @@ class Solver3:
                  gamma: float = 1.0, n_hcoarse: int = 1, time_coarsen: bool = True, k_min: int = 0, vertices=None,
                  affine_patches: bool = False, nu1: int = 2,
                  nu2: int = 2, omega: float = 0.8, rtol: float = 1e-8, atol: float = 1e-14,
-                 max_iterations: int = 200):
+                 max_iterations: int = 200, z_parts: int = 1, z_part: int = 0):
+        """z_parts > 1: this rank's part of the C5 hybrid split (stmg3_solver_create_split):
+        `vertices` is the global vertex array, the levels hold the part's cells;
+        install the parts' communicator with set_space_comm."""
         self.ctx = ctx
         lib = load_library()
         h = _c_void_p()
-        _check(lib.stmg3_solver_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse, int(time_coarsen),
-                                       k_min, int(affine_patches),
-                                       _hptr(vertices, 3 * (nx + 1) * (ny + 1) * (nz + 1), "vertices"), nu1, nu2, omega, rtol, atol, max_iterations,
-                                       ctypes.byref(h)))
+        vp = _hptr(vertices, 3 * (nx + 1) * (ny + 1) * (nz + 1), "vertices")
+        if z_parts > 1:
+            _check(lib.stmg3_solver_create_split(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse,
+                                                 int(time_coarsen), k_min, vp, z_parts, z_part, nu1, nu2, omega,
+                                                 rtol, atol, max_iterations, ctypes.byref(h)))
+        else:
+            _check(lib.stmg3_solver_create(ctx.handle, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse,
+                                           int(time_coarsen), k_min, int(affine_patches), vp, nu1, nu2, omega, rtol,
+                                           atol, max_iterations, ctypes.byref(h)))
+        self.z_parts, self.z_part = z_parts, z_part
         self._h = h
         out = (ctypes.c_int64 * (1 + 7 * 64))()
         _check(lib.stmg3_solver_info(h, out))
@@ -664,6 +694,29 @@ class Solver3:
                        _HALO_FN(_guard(lambda u, s, r, n, st: comm.allgather(s, r, n, st))))
         self._comm = ops
         _check(lib.stmg3_solver_set_comm(self._h, ctypes.byref(ops)))
+
+    def set_space_comm(self, comm) -> None:
+        """The z parts' communicator of a split solver: an NcclComm over the
+        parts, or an object with part, parts, exchange_planes(send_lo, recv_lo,
+        send_hi, recv_hi, n, stream), allreduce_sum(buf, n, stream) and
+        allgather(send, recv, n, stream) (timeslab.LoopbackSpaceComm,
+        timeslab.TorchSpaceComm)."""
+        lib = load_library()
+        if comm is None:
+            self._space = None
+            _check(lib.stmg3_solver_set_space_comm(self._h, None))
+            return
+        if isinstance(comm, NcclComm):
+            self._space = (comm, comm.space_ops())
+            _check(lib.stmg3_solver_set_space_comm(self._h, ctypes.byref(self._space[1])))
+            return
+        ops = _SpaceOps(None, comm.part, comm.parts,
+                        _PLANES_FN(_guard(lambda u, sl, rl, sh, rh, n, st: comm.exchange_planes(sl, rl, sh, rh, n,
+                                                                                               st))),
+                        _REDUCE_FN(_guard(lambda u, b, n, st: comm.allreduce_sum(b, n, st))),
+                        _HALO_FN(_guard(lambda u, s, r, n, st: comm.allgather(s, r, n, st))))
+        self._space = ops
+        _check(lib.stmg3_solver_set_space_comm(self._h, ctypes.byref(ops)))
 
     def set_krylov(self, orthogonalization: int) -> None:
         """As Solver.set_krylov."""

@@ -1,8 +1,10 @@
-// NCCL time-slab communicator of the library: the three
-// exchanges of the all-at-once solve -- the slot-k velocity halo to the next
-// rank (ncclSend / ncclRecv), the Krylov all-reduces and the all-gather of
-// the coarse right-hand sides -- as stmg_comm_ops callbacks that call NCCL
-// directly on the solver's stream. No caller code runs per exchange.
+// NCCL communicators of the library: the three exchanges of
+// the time-slab partition -- the slot-k velocity halo to the next rank
+// (ncclSend / ncclRecv), the Krylov all-reduces and the all-gather of the
+// coarse right-hand sides -- as stmg_comm_ops callbacks, and for the C5
+// hybrid split the interface-plane exchange between z parts, their
+// all-reduce and all-gather (stmg_comm_space_ops). The callbacks call NCCL
+// directly on the solver's stream; no caller code runs per exchange.
 //
 // libnccl.so.2 is opened at run time (dlopen), so the library loads on hosts
 // without NCCL and binds to whichever NCCL the process already has (torch's
@@ -167,6 +169,37 @@ cb_allgather(void *user, const double *send, double *recv, int64_t n, void *stre
       return 1;
     }
 }
+// stmg_comm_space_ops: the z parts of the hybrid split, rank = part
+int
+cb_planes(void *user, const double *send_lo, double *recv_lo, const double *send_hi, double *recv_hi, int64_t n,
+          void *stream)
+{
+  auto *c = static_cast<stmg_comm *>(user);
+  try
+    {
+      NcclApi &api = nccl();
+      auto st = static_cast<cudaStream_t>(stream);
+      const size_t m = static_cast<size_t>(n);
+      nccl_check(api.GroupStart(), "ncclGroupStart");
+      if (send_lo && c->rank > 0)
+        {
+          nccl_check(api.Send(send_lo, m, kNcclFloat64, c->rank - 1, c->comm, st), "ncclSend");
+          nccl_check(api.Recv(recv_lo, m, kNcclFloat64, c->rank - 1, c->comm, st), "ncclRecv");
+        }
+      if (send_hi && c->rank + 1 < c->world)
+        {
+          nccl_check(api.Send(send_hi, m, kNcclFloat64, c->rank + 1, c->comm, st), "ncclSend");
+          nccl_check(api.Recv(recv_hi, m, kNcclFloat64, c->rank + 1, c->comm, st), "ncclRecv");
+        }
+      nccl_check(api.GroupEnd(), "ncclGroupEnd");
+      return 0;
+    }
+  catch (const std::exception &e)
+    {
+      stmg_rt::g_error = e.what();
+      return 1;
+    }
+}
 } // namespace
 
 using stmg_rt::guarded;
@@ -216,6 +249,21 @@ stmg_comm_nccl_ops(stmg_comm *comm, stmg_comm_ops *ops_out)
     ops_out->rank = comm->rank;
     ops_out->world = comm->world;
     ops_out->exchange_halo = cb_halo;
+    ops_out->allreduce_sum = cb_allreduce;
+    ops_out->allgather = cb_allgather;
+  });
+}
+
+int
+stmg_comm_nccl_space_ops(stmg_comm *comm, stmg_comm_space_ops *ops_out)
+{
+  return guarded([&] {
+    if (!comm || !ops_out)
+      throw std::invalid_argument("stmg_comm_nccl_space_ops: null argument");
+    ops_out->user = comm;
+    ops_out->part = comm->rank;
+    ops_out->parts = comm->world;
+    ops_out->exchange_planes = cb_planes;
     ops_out->allreduce_sum = cb_allreduce;
     ops_out->allgather = cb_allgather;
   });

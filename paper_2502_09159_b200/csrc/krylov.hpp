@@ -31,13 +31,24 @@ enum Ortho
   kCGS2 = 1, // classical Gram-Schmidt, twice; two all-reduces per iteration
 };
 
+/// No correction of the local inner products (unpartitioned vectors).
+struct NoFix
+{
+  void operator()(const double *const *, int, bool, const double *, double *) const {}
+};
+
 /// Orthogonalize w against V[0..j]; hcol[0..j] receives the Hessenberg
 /// column, the return value is ||w|| after orthogonalization. `part` must
-/// hold part_doubles() doubles, `scal` 2 * (j + 2) or more.
-template <class Allreduce>
+/// hold part_doubles() doubles, `scal` 2 * (j + 2) or more. fix(V, m,
+/// with_norm, w, out) runs after every local batch of inner products
+/// (out[i] = <w, V_i>, out[m] = <w, w>) and before its all-reduce: a z-split
+/// solver removes there the interface plane a part shares with its lower
+/// neighbour, so every dof is counted once.
+template <class Allreduce, class Fix = NoFix>
 double
 orthogonalize(int ortho, const std::vector<std::unique_ptr<DevArray<double>>> &V, int j, double *w, long long n,
-              double *part, double *scal, std::vector<double> &hcol, Allreduce &&allreduce, stmg_ctx *ctx)
+              double *part, double *scal, std::vector<double> &hcol, Allreduce &&allreduce, stmg_ctx *ctx,
+              Fix &&fix = Fix{})
 {
   using namespace stmg_b200;
   cudaStream_t st = ctx->stream;
@@ -47,11 +58,14 @@ orthogonalize(int ortho, const std::vector<std::unique_ptr<DevArray<double>>> &V
       for (int i = 0; i <= j; ++i)
         {
           check(launch_dot(w, V[i]->p, n, part, scal + i, st), "dot");
+          const double *vi = V[i]->p;
+          fix(&vi, 1, false, w, scal + i);
           allreduce(scal + i, 1);
           check(launch_axpy(n, 0.0, scal + i, -1.0, V[i]->p, w, st), "axpy");
           ctx->count(3);
         }
       check(launch_dot(w, w, n, part, scal + j + 1, st), "dot");
+      fix(nullptr, 0, true, w, scal + j + 1);
       allreduce(scal + j + 1, 1);
       ctx->count(2);
       check(cudaMemcpyAsync(hcol.data(), scal, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, st), "d2h");
@@ -64,9 +78,11 @@ orthogonalize(int ortho, const std::vector<std::unique_ptr<DevArray<double>>> &V
   const int chunks = (j + 1 + kMultiMax - 1) / kMultiMax;
   double *h1 = scal, *h2 = scal + (j + 1);
   check(launch_multidot(ptr.data(), j + 1, false, w, n, part, h1, st), "multidot");
+  fix(ptr.data(), j + 1, false, w, h1);
   allreduce(h1, j + 1);
   check(launch_multi_axpy(ptr.data(), j + 1, h1, nullptr, -1.0, w, n, st), "multi_axpy");
   check(launch_multidot(ptr.data(), j + 1, true, w, n, part, h2, st), "multidot");
+  fix(ptr.data(), j + 1, true, w, h2);
   allreduce(h2, j + 2);
   check(launch_multi_axpy(ptr.data(), j + 1, h2, nullptr, -1.0, w, n, st), "multi_axpy");
   ctx->count(6 * chunks);

@@ -170,14 +170,17 @@ template <int N>
 __global__ void __launch_bounds__(256)
 patch3_assemble_kernel(Level3Consts P, int S, const double *__restrict__ E, long long estride,
                        double *__restrict__ Aall, const long long *__restrict__ aoff, const int *__restrict__ ntv,
-                       int *__restrict__ status)
+                       long long cell0, int *__restrict__ status)
 {
+  // P describes the element-matrix mesh: the level itself, or for a z-split
+  // level the level plus one ghost cell layer across each interface; patch
+  // oc (layouts, inverses) belongs to its cell cell0 + oc
   constexpr int NV = N * N * N, p = N - 1;
   const int np = P.np;
   __shared__ int loc[NV];
   __shared__ int s_nl;
   const int tid = threadIdx.x;
-  const long long cell = blockIdx.x;
+  const long long oc = blockIdx.x, cell = cell0 + oc;
   const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
             cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
   if (tid == 0)
@@ -187,7 +190,7 @@ patch3_assemble_kernel(Level3Consts P, int S, const double *__restrict__ E, long
         {
           const int i = t % N, j = (t / N) % N, k = t / (N * N);
           const int X = cx * p + i, Y = cy * p + j, Z = cz * p + k;
-          const bool bnd = X == 0 || Y == 0 || Z == 0 || X == P.gx - 1 || Y == P.gy - 1 || Z == P.gz - 1;
+          const bool bnd = X == 0 || Y == 0 || Z == P.zlo || X == P.gx - 1 || Y == P.gy - 1 || Z == P.zhi;
           if (!bnd)
             loc[nl++] = t;
         }
@@ -196,13 +199,13 @@ patch3_assemble_kernel(Level3Consts P, int S, const double *__restrict__ E, long
   __syncthreads();
   const int nl = s_nl;
   const int nvel = S * 3 * nl, nt = nvel + S * np;
-  if (nt != ntv[cell])
+  if (nt != ntv[oc])
     {
       if (tid == 0)
         atomicExch(status, 3); // host / device patch layouts disagree
       return;
     }
-  double *A = Aall + aoff[cell];
+  double *A = Aall + aoff[oc];
   __shared__ double kt[kMaxS * kMaxS], mt[kMaxS * kMaxS];
   if (tid < S * S)
     {
@@ -442,15 +445,18 @@ elem3_stride(int r)
 
 cudaError_t
 launch_patch3_setup(const Level3Consts &P, int r, int S, double *E, double *Aall, const long long *aoff,
-                    const int *ntv, int max_nt, long long ncells, int *status, cudaStream_t st)
+                    const int *ntv, int max_nt, long long ncells, int *status, cudaStream_t st, long long ncells_elem,
+                    long long cell0)
 {
+  if (ncells_elem < 0)
+    ncells_elem = ncells;
   const long long es = elem3_stride(r);
   const int N = r + 2, nv = N * N * N, nq = nv;
   const size_t esmem = sizeof(double) * (static_cast<size_t>(nq) * nv * 4 + nq * 10 + static_cast<size_t>(nq) * P.np);
   auto go = [&](auto elem, auto asm_) {
     cudaFuncSetAttribute(elem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(esmem));
-    elem<<<static_cast<unsigned>(ncells), 256, esmem, st>>>(P, E, es, status);
-    asm_<<<static_cast<unsigned>(ncells), 256, 0, st>>>(P, S, E, es, Aall, aoff, ntv, status);
+    elem<<<static_cast<unsigned>(ncells_elem), 256, esmem, st>>>(P, E, es, status);
+    asm_<<<static_cast<unsigned>(ncells), 256, 0, st>>>(P, S, E, es, Aall, aoff, ntv, cell0, status);
   };
   if (r == 1)
     go(elem3_kernel<3>, patch3_assemble_kernel<3>);

@@ -40,6 +40,8 @@ make_level3_consts(const Level3Spec &L, const double *dev_verts)
   P.gx = L.gx();
   P.gy = L.gy();
   P.gz = L.gz();
+  P.zlo = L.zlo();
+  P.zhi = L.zhi();
   P.np = L.np();
   P.nsc = L.nsc();
   P.mv = L.mv();
@@ -79,7 +81,7 @@ make_level3_consts(const Level3Spec &L, const double *dev_verts)
   P.gamma = L.gamma;
   P.hx = 1.0 / L.nx;
   P.hy = 1.0 / L.ny;
-  P.hz = 1.0 / L.nz;
+  P.hz = L.hz();
   P.verts = dev_verts;
   P.gemmE = nullptr;
   for (int i = 0; i < N; ++i)
@@ -342,7 +344,7 @@ cell_patch(const Level3Spec &L, const std::vector<double> *verts, int cx, int cy
   const TimeTables T = time_tables(L.k, L.tau);
   const int gx = L.gx(), gy = L.gy(), gz = L.gz();
   auto on_bnd = [&](int X, int Y, int Z) {
-    return X == 0 || Y == 0 || Z == 0 || X == gx - 1 || Y == gy - 1 || Z == gz - 1;
+    return X == 0 || Y == 0 || Z == L.zlo() || X == gx - 1 || Y == gy - 1 || Z == L.zhi();
   };
   std::vector<int> loc; // local node index of the patch's unconstrained nodes
   for (int k = 0; k < N; ++k)
@@ -469,9 +471,31 @@ cell_patch(const Level3Spec &L, const std::vector<double> *verts, int cx, int cy
 }
 } // namespace
 
+namespace
+{
+/// Nodes on an interface plane also belong to the neighbour part's cells
+/// across it: their valence (vanka.cpp:182-192, counted over the whole
+/// mesh) is twice the local count.
+void
+interface_valence(const Level3Spec &L, std::vector<int> &valence)
+{
+  const long long plane = static_cast<long long>(L.gx()) * L.gy();
+  for (int side = 0; side < 2; ++side)
+    if (side == 0 ? !L.zlo_bc : !L.zhi_bc)
+      {
+        const long long z0 = side == 0 ? 0 : static_cast<long long>(L.gz() - 1) * plane;
+        for (long long i = 0; i < plane; ++i)
+          valence[z0 + i] *= 2;
+      }
+}
+} // namespace
+
 Patch3Set
 build_patches3(const Level3Spec &L, const std::vector<double> *verts)
 {
+  if (L.split())
+    throw std::invalid_argument("3D level: patches of a z-split level are set up on the GPU (nx, ny, nz >= 2, "
+                                "r <= 2, deformed geometry)");
   const int N = L.n1(), p = L.p();
   std::vector<int> valence(static_cast<size_t>(L.nsc()), 0);
   for (int cz = 0; cz < L.nz; ++cz)
@@ -549,8 +573,9 @@ cell_patch_layouts3(const Level3Spec &L)
           for (int j = 0; j < N; ++j)
             for (int i = 0; i < N; ++i)
               valence[(static_cast<size_t>(cz * p + k) * gy + cy * p + j) * gx + cx * p + i]++;
+  interface_valence(L, valence);
   auto on_bnd = [&](int X, int Y, int Z) {
-    return X == 0 || Y == 0 || Z == 0 || X == gx - 1 || Y == gy - 1 || Z == gz - 1;
+    return X == 0 || Y == 0 || Z == L.zlo() || X == gx - 1 || Y == gy - 1 || Z == L.zhi();
   };
   Patch3Layout Lo;
   const long long nc = L.ncells();
@@ -837,6 +862,8 @@ geom3(const Level3Spec &L)
   g.gx = L.gx();
   g.gy = L.gy();
   g.gz = L.gz();
+  g.zlo = L.zlo();
+  g.zhi = L.zhi();
   g.S = L.S();
   g.np = L.np();
   g.nsc = L.nsc();

@@ -25,6 +25,7 @@
 // dofs); cell-owned pressure rows are written directly.
 #include "st3d.hpp"
 
+#include <algorithm>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -123,7 +124,7 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
   double *const GCa = X8 + 24; // deformed: [point][10] J^{-1}, det
   const int tA = t % N, tB = t / N; // line coordinates
   const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
-  const int gx = P.gx, gy = P.gy, gz = P.gz;
+  const int gx = P.gx, gy = P.gy;
   constexpr bool deformed = DEF; // Cartesian instantiations use the diagonal Jacobian
   const double *__restrict__ xn = x + n * isz;
   const double *__restrict__ vprev = nullptr;
@@ -161,7 +162,7 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
       if (active)
         {
           const int Y = cy * p + tA, Z = cz * p + tB;
-          const bool yzb = MODE != 2 && (Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1);
+          const bool yzb = MODE != 2 && (Y == 0 || Z == P.zlo || Y == gy - 1 || Z == P.zhi);
           const long long row = (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
 #pragma unroll
           for (int c = 0; c < 3; ++c)
@@ -440,7 +441,7 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
       if (active)
         {
           const int Y = cy * p + tA, Z = cz * p + tB;
-          const bool yzb = Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1;
+          const bool yzb = Y == 0 || Z == P.zlo || Y == gy - 1 || Z == P.zhi;
 #pragma unroll
           for (int c = 0; c < 3; ++c)
             {
@@ -543,7 +544,7 @@ vmult3l_kernel(const Level3Consts P, const double *__restrict__ x, const double 
   const int t = threadIdx.x;
   const int tA = t % N, tB = t / N; // line coordinates
   const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
-  const int gx = P.gx, gy = P.gy, gz = P.gz;
+  const int gx = P.gx, gy = P.gy;
   const bool deformed = P.verts != nullptr;
   const double *__restrict__ xn = x + n * isz;
   const double *__restrict__ vprev = nullptr;
@@ -584,7 +585,7 @@ vmult3l_kernel(const Level3Consts P, const double *__restrict__ x, const double 
             {
               const int X = cx * p + i;
               const long long node = (static_cast<long long>(Z) * gy + Y) * gx + X;
-              const bool bnd = MODE != 2 && (X == 0 || Y == 0 || Z == 0 || X == gx - 1 || Y == gy - 1 || Z == gz - 1);
+              const bool bnd = MODE != 2 && (X == 0 || Y == 0 || Z == P.zlo || X == gx - 1 || Y == gy - 1 || Z == P.zhi);
               const int li = (tB * N + tA) * N + i;
 #pragma unroll
               for (int c = 0; c < 3; ++c)
@@ -966,7 +967,7 @@ vmult3l_kernel(const Level3Consts P, const double *__restrict__ x, const double 
         {
           const int base = (tB * N + tA) * N;
           const int Y = cy * p + tA, Z = cz * p + tB;
-          const bool yzb = Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1;
+          const bool yzb = Y == 0 || Z == P.zlo || Y == gy - 1 || Z == P.zhi;
 #pragma unroll
           for (int c = 0; c < 3; ++c)
             {
@@ -1251,7 +1252,7 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
   double *const PM = PP + NP * NN;
   const int tA = t % N, tB = t / N;
   const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
-  const int gx = P.gx, gy = P.gy, gz = P.gz;
+  const int gx = P.gx, gy = P.gy;
   const double *__restrict__ xn = x + n * isz;
   const double *__restrict__ vprev = nullptr;
   if (coupled)
@@ -1288,7 +1289,7 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
       if (active)
         {
           const int Y = cy * p + tA, Z = cz * p + tB;
-          const bool yzb = MODE != 2 && (Y == 0 || Z == 0 || Y == gy - 1 || Z == gz - 1);
+          const bool yzb = MODE != 2 && (Y == 0 || Z == P.zlo || Y == gy - 1 || Z == P.zhi);
           const long long row = (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
           double uk[3][N], um[3][N];
 #pragma unroll
@@ -1470,7 +1471,7 @@ vmult3c_kernel(const Level3Consts P, const double *__restrict__ x, const double 
                       s = fma(-ix2[c] * Jm * wx * wy * wz, PM[l], s);
                     }
                   const int Z = cz * p + o;
-                  const bool bnd = MODE != 2 && (xyb || Z == 0 || Z == gz - 1);
+                  const bool bnd = MODE != 2 && (xyb || Z == P.zlo || Z == P.zhi);
                   if (!bnd)
                     atomicAdd(yv + static_cast<long long>(Z) * gy * gx, MODE == 1 ? -s : s);
                 }
@@ -1494,7 +1495,7 @@ vmult3_init_kernel(DevGeom3 G, const double *__restrict__ x, const double *__res
   const int X = xy % G.gx, Y = xy / G.gx, Z = blockIdx.y;
   const int q = blockIdx.z, comp = q % 3, a = (q / 3) % G.S, n = q / (3 * G.S);
   const long long o = n * G.isz + a * G.mv + comp * G.nsc + (static_cast<long long>(Z) * G.gy + Y) * G.gx + X;
-  const bool bnd = X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1;
+  const bool bnd = X == 0 || Y == 0 || Z == G.zlo || X == G.gx - 1 || Y == G.gy - 1 || Z == G.zhi;
   double v = 0.0;
   if (MODE != 2 && bnd)
     v = x[o];
@@ -1516,6 +1517,8 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
   G.gx = P.gx;
   G.gy = P.gy;
   G.gz = P.gz;
+  G.zlo = P.zlo;
+  G.zhi = P.zhi;
   G.S = S;
   G.np = P.np;
   G.nsc = P.nsc;
@@ -1642,7 +1645,7 @@ zero_constrained3_kernel(DevGeom3 G, double *__restrict__ x)
   if (xy >= G.gx * G.gy)
     return;
   const int X = xy % G.gx, Y = xy / G.gx, Z = blockIdx.y;
-  if (!(X == 0 || Y == 0 || Z == 0 || X == G.gx - 1 || Y == G.gy - 1 || Z == G.gz - 1))
+  if (!(X == 0 || Y == 0 || Z == G.zlo || X == G.gx - 1 || Y == G.gy - 1 || Z == G.zhi))
     return;
   const int q = blockIdx.z, comp = q % 3, a = (q / 3) % G.S, n = q / (3 * G.S);
   x[n * G.isz + a * G.mv + comp * G.nsc + (static_cast<long long>(Z) * G.gy + Y) * G.gx + X] = 0.0;
@@ -1970,6 +1973,206 @@ launch_project3(const DevGeom3 &G, const double *pmean, double inv_vol, double *
     return cudaSuccess;
   dim3 grid(G.S, nI);
   project3_kernel<<<grid, kProjThreads, 0, st>>>(G, pmean, inv_vol, x);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- z-split
+// Interface planes of a z-split level (stmg3_solver_create_split): the
+// velocity nodes of the node plane Z = 0 (side 0) or Z = gz - 1 (side 1), for
+// every interval, slot and component, packed as [n][a][c][gx * gy].
+namespace
+{
+__device__ __forceinline__ long long
+plane_index(const DevGeom3 &G, int side, long long e)
+{
+  const long long L = static_cast<long long>(G.gx) * G.gy;
+  const long long seg = e / L, off = e - seg * L;
+  const long long c = seg % 3, a = (seg / 3) % G.S, n = seg / (3 * G.S);
+  return n * G.isz + a * G.mv + c * G.nsc + (side ? static_cast<long long>(G.gz - 1) * L : 0) + off;
+}
+__device__ __forceinline__ bool
+plane_edge(const DevGeom3 &G, long long e)
+{
+  const long long off = e % (static_cast<long long>(G.gx) * G.gy);
+  const int X = static_cast<int>(off % G.gx), Y = static_cast<int>(off / G.gx);
+  return X == 0 || Y == 0 || X == G.gx - 1 || Y == G.gy - 1; // Dirichlet rows of the plane
+}
+
+__global__ void
+plane_op3_kernel(DevGeom3 G, int side, int op, long long n, double *__restrict__ x, double *__restrict__ buf,
+                 const double *__restrict__ other, const double *__restrict__ b, const double *__restrict__ saved)
+{
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x)
+    {
+      const long long i = plane_index(G, side, e);
+      switch (op)
+        {
+        case 0: // pack
+          buf[e] = x[i];
+          break;
+        case 1: // owner-accumulate: x += partner's partial sums (plain application)
+          if (!plane_edge(G, e))
+            x[i] += other[e];
+          break;
+        case 2: // residual: r = r_own + r_partner - b (both are b - partial; b: full vector)
+          if (!plane_edge(G, e))
+            x[i] = (x[i] + other[e]) - b[i];
+          break;
+        case 3: // scale by 1/2 (fine residual before a restriction)
+          x[i] *= 0.5;
+          break;
+        case 4: // Vanka delta of this part: buf = x - saved
+          buf[e] = x[i] - saved[e];
+          break;
+        case 5: // x = saved + (own delta + partner delta): the same sum on both parts
+          x[i] = saved[e] + (buf[e] + other[e]);
+          break;
+        case 6: // unpack
+          x[i] = buf[e];
+          break;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kProjThreads)
+project3_sums_kernel(DevGeom3 G, const double *__restrict__ pmean, const double *__restrict__ x,
+                     double *__restrict__ sums)
+{
+  __shared__ double red[kProjThreads];
+  const int n = blockIdx.y, a = blockIdx.x;
+  const double *pr = x + n * G.isz + G.S * G.mv + a * G.mp;
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < G.mp; i += kProjThreads)
+    s = fma(pmean[i], pr[i], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kProjThreads / 2; w > 0; w >>= 1)
+    {
+      if (threadIdx.x < w)
+        red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+  if (threadIdx.x == 0)
+    sums[n * G.S + a] = red[0];
+}
+
+__global__ void __launch_bounds__(kProjThreads)
+project3_apply_kernel(DevGeom3 G, const double *__restrict__ sums, double inv_vol, double *__restrict__ x)
+{
+  const int n = blockIdx.y, a = blockIdx.x;
+  double *pr = x + n * G.isz + G.S * G.mv + a * G.mp;
+  const double mean = sums[n * G.S + a] * inv_vol;
+  const long long ncell = G.mp / G.np;
+  for (long long c = threadIdx.x; c < ncell; c += kProjThreads)
+    pr[c * G.np] -= mean;
+}
+
+constexpr int kPlaneDotBlocks = 64;
+__global__ void __launch_bounds__(256)
+plane_multidot_kernel(DevGeom3 G, int side, long long n, MultiVec V, int m, int with_norm, const double *__restrict__ w,
+                      double *__restrict__ part)
+{
+  __shared__ double red[256];
+  for (int i = 0; i < m + with_norm; ++i)
+    {
+      const double *v = i < m ? V.p[i] : w;
+      double s = 0.0;
+      for (long long e = blockIdx.x * 256ll + threadIdx.x; e < n; e += 256ll * gridDim.x)
+        {
+          const long long k = plane_index(G, side, e);
+          s = fma(v[k], w[k], s);
+        }
+      red[threadIdx.x] = s;
+      __syncthreads();
+      for (int h = 128; h > 0; h >>= 1)
+        {
+          if (threadIdx.x < h)
+            red[threadIdx.x] += red[threadIdx.x + h];
+          __syncthreads();
+        }
+      if (threadIdx.x == 0)
+        part[i * kPlaneDotBlocks + blockIdx.x] = red[0];
+      __syncthreads();
+    }
+}
+
+__global__ void
+plane_multidot_sub_kernel(const double *__restrict__ part, int count, double *__restrict__ out)
+{
+  const int i = threadIdx.x;
+  if (i >= count)
+    return;
+  double s = 0.0;
+  for (int b = 0; b < kPlaneDotBlocks; ++b)
+    s += part[i * kPlaneDotBlocks + b];
+  out[i] -= s;
+}
+} // namespace
+
+long long
+plane3_doubles(const DevGeom3 &G, int nI)
+{
+  return static_cast<long long>(nI) * G.S * 3 * G.gx * G.gy;
+}
+
+cudaError_t
+launch_plane_op3(const DevGeom3 &G, int side, int op, int nI, double *x, double *buf, const double *other,
+                 const double *b, const double *saved, cudaStream_t st)
+{
+  const long long n = plane3_doubles(G, nI);
+  if (n == 0)
+    return cudaSuccess;
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4 * 148));
+  plane_op3_kernel<<<blocks, 256, 0, st>>>(G, side, op, n, x, buf, other, b, saved);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_project3_sums(const DevGeom3 &G, const double *pmean, const double *x, int nI, double *sums, cudaStream_t st)
+{
+  if (nI == 0)
+    return cudaSuccess;
+  project3_sums_kernel<<<dim3(G.S, nI), kProjThreads, 0, st>>>(G, pmean, x, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_project3_apply(const DevGeom3 &G, const double *sums, double inv_vol, double *x, int nI, cudaStream_t st)
+{
+  if (nI == 0)
+    return cudaSuccess;
+  project3_apply_kernel<<<dim3(G.S, nI), kProjThreads, 0, st>>>(G, sums, inv_vol, x);
+  return cudaGetLastError();
+}
+
+long long
+plane_multidot_part_doubles()
+{
+  return static_cast<long long>(kMultiMax + 1) * kPlaneDotBlocks;
+}
+
+cudaError_t
+launch_plane_multidot_sub(const DevGeom3 &G, int side, int nI, const double *const *V, int m, bool with_norm,
+                          const double *w, double *part, double *out, cudaStream_t st)
+{
+  const long long n = plane3_doubles(G, nI);
+  for (int i0 = 0;; i0 += kMultiMax)
+    {
+      const int mm = std::min(kMultiMax, m - i0);
+      const bool last = i0 + kMultiMax >= m;
+      const int wn = last && with_norm ? 1 : 0;
+      MultiVec mv{};
+      for (int i = 0; i < mm; ++i)
+        mv.p[i] = V[i0 + i];
+      if (mm + wn > 0)
+        {
+          plane_multidot_kernel<<<kPlaneDotBlocks, 256, 0, st>>>(G, side, n, mv, mm, wn, w, part);
+          plane_multidot_sub_kernel<<<1, 32, 0, st>>>(part, mm + wn, out + i0);
+        }
+      if (last)
+        break;
+    }
   return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@ constexpr int kMaxNP3 = 35; // dim P_r^disc(3D), r <= 4
 struct Level3Consts
 {
   int nx, ny, nz, gx, gy, gz, np;
+  int zlo, zhi; // constrained z node planes (-1: interface face, Level3Spec::zlo/zhi)
   long long nsc, mv, mp, isz;
   double phi[kMaxN1 * kMaxN1];  // phi(q, i) = l_i(x_q), row-major [q * N + i]
   double dphi[kMaxN1 * kMaxN1]; // l_i'(x_q)
@@ -52,6 +53,17 @@ struct Level3Spec
 {
   int nx = 1, ny = 1, nz = 1, r = 1, k = 1;
   double tau = 1.0, nu = 1.0, gamma = 0.0;
+  // spatial partition in z (C5 hybrid split, stmg3_solver_create_split):
+  // a face is either the domain boundary (Dirichlet, *_bc = 1) or an
+  // interface to the neighbouring part (0: its nodes are unconstrained and
+  // shared with the neighbour). nz_glob: cells of the whole mesh in z
+  // (0: this level is the whole mesh).
+  int zlo_bc = 1, zhi_bc = 1, nz_glob = 0;
+  bool split() const { return !zlo_bc || !zhi_bc; }
+  /// Node plane index of the constrained z faces (-1: interface, none).
+  int zlo() const { return zlo_bc ? 0 : -1; }
+  int zhi() const { return zhi_bc ? gz() - 1 : -1; }
+  double hz() const { return 1.0 / (nz_glob > 0 ? nz_glob : nz); }
   int n1() const { return r + 2; }
   int p() const { return r + 1; }
   int np() const { return (r + 1) * (r + 2) * (r + 3) / 6; }
@@ -121,8 +133,11 @@ Patch3Layout cell_patch_layouts3(const Level3Spec &L);
 /// their in-place Gauss-Jordan inverses into Aall. *status (device) stays 0
 /// on success; 1 = vanishing pivot, 2 = inverted cell, 3 = layout mismatch.
 long long elem3_stride(int r);
+/// Split levels: P is the level extended by a ghost cell layer across each
+/// interface (ncells_elem element matrices); owned patch c is cell cell0 + c.
 cudaError_t launch_patch3_setup(const Level3Consts &P, int r, int S, double *E, double *Aall, const long long *aoff,
-                                const int *ntv, int max_nt, long long ncells, int *status, cudaStream_t st);
+                                const int *ntv, int max_nt, long long ncells, int *status, cudaStream_t st,
+                                long long ncells_elem = -1, long long cell0 = 0);
 /// Batched in-place inverse of `count` dense row-major matrices (sizes ntv,
 /// offsets aoff), pivot-free blocked Gauss-Jordan on the FP64 tensor path.
 cudaError_t launch_gj_inverse(double *Aall, const long long *aoff, const int *ntv, int count, int max_nt, int *status,
@@ -154,6 +169,7 @@ std::vector<double> pressure_mean3(const Level3Spec &L, const std::vector<double
 struct DevGeom3
 {
   int nx, ny, nz, gx, gy, gz, S, np;
+  int zlo, zhi; // constrained z node planes (-1: interface face)
   long long nsc, mv, mp, isz;
 };
 DevGeom3 geom3(const Level3Spec &L);
@@ -175,6 +191,26 @@ cudaError_t launch_zero_constrained3(const DevGeom3 &G, double *x, int n_interva
 /// deterministic single-block reductions.
 cudaError_t launch_project3(const DevGeom3 &G, const double *pmean, double inv_vol, double *x, int n_intervals,
                             cudaStream_t st);
+/// z-split interface planes (side 0: Z = 0, side 1: Z = gz - 1), packed
+/// [n][a][c][gx * gy] (plane3_doubles). op: 0 pack x -> buf; 1 x += other
+/// (owner-accumulate, Dirichlet edge rows skipped); 2 x = x + other - b
+/// (residual, b the full vector); 3 x *= 1/2; 4 buf = x - saved;
+/// 5 x = saved + (buf + other); 6 x = buf (unpack).
+long long plane3_doubles(const DevGeom3 &G, int nI);
+cudaError_t launch_plane_op3(const DevGeom3 &G, int side, int op, int nI, double *x, double *buf, const double *other,
+                             const double *b, const double *saved, cudaStream_t st);
+/// Split mean-zero projection: per (interval, slot) partial sums <pmean, p>
+/// (sums[n * S + a]), summed over the parts by the caller, then applied.
+cudaError_t launch_project3_sums(const DevGeom3 &G, const double *pmean, const double *x, int nI, double *sums,
+                                 cudaStream_t st);
+cudaError_t launch_project3_apply(const DevGeom3 &G, const double *sums, double inv_vol, double *x, int nI,
+                                  cudaStream_t st);
+/// out[i] -= plane part of <w, V_i> (and out[m] -= plane part of <w, w>):
+/// the interface plane a part shares with its lower neighbour is counted
+/// once in the Krylov inner products. part: plane_multidot_part_doubles().
+long long plane_multidot_part_doubles();
+cudaError_t launch_plane_multidot_sub(const DevGeom3 &G, int side, int nI, const double *const *V, int m,
+                                      bool with_norm, const double *w, double *part, double *out, cudaStream_t st);
 /// nc coarse intervals -> (h_time ? 2 nc : nc) fine intervals. With `work`
 /// (transfer3_work_doubles) spatial transfers run as separable 1D passes.
 long long transfer3_work_doubles(const DevTransfer3 &T, int nc);

@@ -47,6 +47,23 @@ coarse3_step_kernel(const double *__restrict__ G, const double *__restrict__ H, 
 }
 } // namespace
 
+/// dir 0: global[n][map[part][i]] = parts[part][n][i] (the parts of a z-split
+/// coarse level into the whole-mesh vector; shared interface entries hold
+/// equal values); dir 1: local[n][i] = global[n][map[i]].
+__global__ void
+coarse_map_kernel(const double *__restrict__ src, const int *__restrict__ map, int n_loc, int n_glob, int nI,
+                  double *__restrict__ dst, int dir)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, n = blockIdx.y, part = blockIdx.z;
+  if (i >= n_loc)
+    return;
+  const int g = map[static_cast<long long>(part) * n_loc + i];
+  if (dir == 0)
+    dst[static_cast<long long>(n) * n_glob + g] = src[(static_cast<long long>(part) * nI + n) * n_loc + i];
+  else
+    dst[static_cast<long long>(n) * n_loc + i] = src[static_cast<long long>(n) * n_glob + g];
+}
+
 // ================================================================ level
 struct stmg3_level
 {
@@ -76,6 +93,9 @@ struct stmg3_level
   bool affine_patches = false;
   std::uint64_t total_matrix_elements = 0;
   DevArray<double> work, zeros;
+  // z-split level (stmg3_solver_create_split): normalisations of the
+  // projections over the whole mesh (the sums are reduced over the parts)
+  double vol_global = 0.0, ncells_global = 0.0;
 
   void
   vmult(const double *x, const double *b, double *y, int n, const double *xprev, int coupled, int mode)
@@ -155,9 +175,13 @@ struct stmg3_level
 namespace
 {
 void
-build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_patches = false)
+build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_patches = false,
+             const std::vector<double> *verts_ext = nullptr)
 {
   const Level3Spec &s = L.spec;
+  if (s.split() && (!verts_host || !verts_ext || affine_patches))
+    throw std::invalid_argument("3D split level: needs deformed-geometry vertices (with the ghost layer) and exact "
+                                "patches");
   if (s.nx < 1 || s.ny < 1 || s.nz < 1)
     throw std::invalid_argument("3D level: need at least one cell per direction");
   if (!vmult3_supported(s.r, s.S()))
@@ -205,7 +229,10 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
   // and as the A/B switch STMG_PATCH3_HOST.
   const bool exact = L.deformed && !affine_patches;
   bool gpu_done = false;
-  if (exact && s.nx >= 2 && s.ny >= 2 && s.nz >= 2 && (s.r == 1 || s.r == 2) && !std::getenv("STMG_PATCH3_HOST"))
+  const bool gpu_ok = exact && s.nx >= 2 && s.ny >= 2 && s.nz >= 2 && (s.r == 1 || s.r == 2);
+  if (s.split() && L.smoother_kind != STMG_SMOOTHER_NONE && !gpu_ok)
+    throw std::invalid_argument("3D split level: the smoothed levels need >= 2 local cells per direction, r <= 2");
+  if (gpu_ok && (s.split() || !std::getenv("STMG_PATCH3_HOST")))
     {
       const auto t0 = std::chrono::steady_clock::now();
       const Patch3Layout lo = cell_patch_layouts3(s);
@@ -218,19 +245,42 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
       DevArray<int> ntv, st;
       ntv.upload(lo.nt);
       st.upload(std::vector<int>{0});
-      {
-        DevArray<double> E;
-        E.resize(static_cast<size_t>(nc) * elem3_stride(s.r));
-        check(launch_patch3_setup(L.consts, s.r, s.S(), E.p, L.inv_all.p, aoff.p, ntv.p, lo.max_nt, nc, st.p,
-                                  L.ctx->stream),
-              "patch3_setup");
-        L.ctx->count(3);
-        check(cudaStreamSynchronize(L.ctx->stream), "patch3_setup");
-      }
+      if (s.split())
+        {
+          // element matrices of the owned cells plus one ghost cell layer
+          // across each interface: the patches of the interface cells sum
+          // the neighbour part's cells too (R_T S R_T^T of the whole mesh)
+          Level3Spec ex = s;
+          const int gl = s.zlo_bc ? 0 : 1, gh = s.zhi_bc ? 0 : 1;
+          ex.nz = s.nz + gl + gh;
+          if (static_cast<long long>(verts_ext->size()) != 3 * ex.nverts())
+            throw std::invalid_argument("3D split level: ghost-layer vertex array has the wrong size");
+          DevArray<double> vext, E;
+          vext.upload(*verts_ext);
+          const Level3Consts Pe = make_level3_consts(ex, vext.p);
+          E.resize(static_cast<size_t>(ex.ncells()) * elem3_stride(s.r));
+          check(launch_patch3_setup(Pe, s.r, s.S(), E.p, L.inv_all.p, aoff.p, ntv.p, lo.max_nt, nc, st.p,
+                                    L.ctx->stream, ex.ncells(), static_cast<long long>(gl) * s.nx * s.ny),
+                "patch3_setup");
+          L.ctx->count(3);
+          check(cudaStreamSynchronize(L.ctx->stream), "patch3_setup");
+        }
+      else
+        {
+          DevArray<double> E;
+          E.resize(static_cast<size_t>(nc) * elem3_stride(s.r));
+          check(launch_patch3_setup(L.consts, s.r, s.S(), E.p, L.inv_all.p, aoff.p, ntv.p, lo.max_nt, nc, st.p,
+                                    L.ctx->stream),
+                "patch3_setup");
+          L.ctx->count(3);
+          check(cudaStreamSynchronize(L.ctx->stream), "patch3_setup");
+        }
       int status = 0;
       check(cudaMemcpy(&status, st.p, sizeof(int), cudaMemcpyDeviceToHost), "status");
       if (status == 2)
         throw std::runtime_error("3D level: inverted cell");
+      if (status != 0 && s.split())
+        throw std::runtime_error("3D split level: GPU patch setup failed (vanishing pivot or layout mismatch)");
       if (status == 0)
         {
           cell_class.resize(nc);
@@ -360,10 +410,122 @@ struct stmg3_solver
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_x = nullptr, ev_h = nullptr;
 
+  // ---- C5 hybrid split: z parts (stmg3_solver_create_split)
+  int zpart = 0, zparts = 1;
+  stmg_comm_space_ops sops{};
+  bool has_space = false;
+  int coarse_n_loc = 0;     // coarse level: local interval size (coarse_n is the global one)
+  long long coarse_mv = 0;  // velocity block of the (global) coarse level
+  DevArray<int> cmap;       // [parts][coarse_n_loc]: local coarse dof -> global coarse dof
+  DevArray<double> pl_a[2], pl_b[2], pl_s[2], psum, pdpart, cBs, cBg;
+
   stmg3_level &fine() { return *levels.back()->level; }
   int rank() const { return has_comm ? comm.rank : 0; }
   int world() const { return has_comm ? comm.world : 1; }
   int n_at(int l, int nI_fine) const { return nI_fine >> levels[l]->tshift; }
+  bool split() const { return zparts > 1; }
+  void
+  need_space() const
+  {
+    if (split() && !has_space)
+      throw std::runtime_error("z-split solver: install the parts' communicator (stmg3_solver_set_space_comm)");
+  }
+  static bool
+  iface(const stmg3_level &L, int side)
+  {
+    return side == 0 ? !L.spec.zlo_bc : !L.spec.zhi_bc;
+  }
+  /// Exchange the interface planes (pl_a[side] -> partner, partner -> pl_b[side]).
+  void
+  exchange_planes(const stmg3_level &L, long long n)
+  {
+    need_space();
+    if (sops.exchange_planes(sops.user, iface(L, 0) ? pl_a[0].p : nullptr, iface(L, 0) ? pl_b[0].p : nullptr,
+                             iface(L, 1) ? pl_a[1].p : nullptr, iface(L, 1) ? pl_b[1].p : nullptr, n, ctx->stream) != 0)
+      throw std::runtime_error("comm: exchange_planes failed");
+  }
+  void
+  plane_op(const stmg3_level &L, int side, int op, int nI, double *x, double *buf, const double *other,
+           const double *b = nullptr, const double *saved = nullptr)
+  {
+    check(launch_plane_op3(L.geom, side, op, nI, x, buf, other, b, saved, ctx->stream), "plane_op3");
+    ctx->count();
+  }
+  /// Owner-accumulate of the interface rows after a local application:
+  /// y += partner's partial sums (mode 0), r = r_own + r_partner - b (mode 1).
+  void
+  iface_sum(int l, double *y, const double *b, int nI, int mode)
+  {
+    if (!split())
+      return;
+    STMG_NVTX("iface_sum L%d", l);
+    const stmg3_level &L = *levels[l]->level;
+    const long long n = plane3_doubles(L.geom, nI);
+    for (int side = 0; side < 2; ++side)
+      if (iface(L, side))
+        {
+          pl_a[side].resize(n);
+          pl_b[side].resize(n);
+          plane_op(L, side, 0, nI, y, pl_a[side].p, nullptr);
+        }
+    exchange_planes(L, n);
+    for (int side = 0; side < 2; ++side)
+      if (iface(L, side))
+        plane_op(L, side, mode == 1 ? 2 : 1, nI, y, nullptr, pl_b[side].p, b);
+  }
+  /// Additive Vanka update of a split level: both parts' interface
+  /// increments are added to the pre-sweep interface values.
+  void
+  vanka(int l, const double *r, double *u, int nI)
+  {
+    stmg3_level &L = *levels[l]->level;
+    if (!split())
+      {
+        L.vanka(r, u, nI, omega);
+        return;
+      }
+    const long long n = plane3_doubles(L.geom, nI);
+    for (int side = 0; side < 2; ++side)
+      if (iface(L, side))
+        {
+          pl_s[side].resize(n);
+          pl_a[side].resize(n);
+          pl_b[side].resize(n);
+          plane_op(L, side, 0, nI, u, pl_s[side].p, nullptr);
+        }
+    L.vanka(r, u, nI, omega);
+    for (int side = 0; side < 2; ++side)
+      if (iface(L, side))
+        plane_op(L, side, 4, nI, u, pl_a[side].p, nullptr, nullptr, pl_s[side].p);
+    exchange_planes(L, n);
+    for (int side = 0; side < 2; ++side)
+      if (iface(L, side))
+        plane_op(L, side, 5, nI, u, pl_a[side].p, pl_b[side].p, nullptr, pl_s[side].p);
+  }
+  /// Mean-zero projection (residual: along the constant-mode coefficients).
+  void
+  project(int l, double *x, int nI, bool residual)
+  {
+    stmg3_level &L = *levels[l]->level;
+    if (!split())
+      {
+        if (residual)
+          L.project_residual(x, nI);
+        else
+          L.project(x, nI);
+        return;
+      }
+    need_space();
+    const int cnt = nI * L.spec.S();
+    psum.resize(cnt);
+    check(launch_project3_sums(L.geom, residual ? L.one_w.p : L.pmean.p, x, nI, psum.p, ctx->stream), "project3");
+    if (sops.allreduce_sum(sops.user, psum.p, cnt, ctx->stream) != 0)
+      throw std::runtime_error("comm: allreduce_sum (parts) failed");
+    check(launch_project3_apply(L.geom, psum.p, residual ? 1.0 / L.ncells_global : 1.0 / L.vol_global, x, nI,
+                                ctx->stream),
+          "project3");
+    ctx->count(2);
+  }
 
   ~stmg3_solver()
   {
@@ -384,6 +546,7 @@ struct stmg3_solver
     if (world() == 1)
       {
         L.vmult(x, b, y, nI, nullptr, 1, mode);
+        iface_sum(l, y, b, nI, mode);
         return;
       }
     if (!comm_stream)
@@ -406,13 +569,33 @@ struct stmg3_solver
     check(cudaStreamWaitEvent(ctx->stream, ev_h, 0), "wait");
     // interval 0 alone: its init kernel must not touch intervals 1..nI-1
     L.vmult(x, b, y, 1, rank() == 0 ? nullptr : h.p, 1, mode);
+    iface_sum(l, y, b, nI, mode);
   }
 
+  /// Krylov sums over every rank: the time slabs, then the z parts.
   void
   allreduce(double *buf, int n)
   {
     if (world() > 1 && comm.allreduce_sum(comm.user, buf, n, ctx->stream) != 0)
       throw std::runtime_error("comm: allreduce_sum failed");
+    if (split())
+      {
+        need_space();
+        if (sops.allreduce_sum(sops.user, buf, n, ctx->stream) != 0)
+          throw std::runtime_error("comm: allreduce_sum (parts) failed");
+      }
+  }
+  /// Inner products of the finest level count the plane shared with the
+  /// lower part once (the lower part owns it).
+  void
+  plane_fix(const double *const *V, int m, bool with_norm, const double *w, double *out, int nI)
+  {
+    const stmg3_level &L = fine();
+    if (!split() || !iface(L, 0))
+      return;
+    pdpart.resize(plane_multidot_part_doubles());
+    check(launch_plane_multidot_sub(L.geom, 0, nI, V, m, with_norm, w, pdpart.p, out, ctx->stream), "plane_dot");
+    ctx->count(2);
   }
 
   /// restrict_residual: R fine, zero constrained, project (transfer.cpp:117-132)
@@ -422,11 +605,28 @@ struct stmg3_solver
     Solver3Level &F = *levels[l];
     stmg3_level &C = *levels[l - 1]->level;
     F.tw.resize(std::max<long long>(1, transfer3_work_doubles(F.dt, nc)));
+    const int nf = F.dt.h_time ? 2 * nc : nc;
+    double *fv = const_cast<double *>(fine_v); // split: interface planes halved, restored below
+    if (split())
+      for (int side = 0; side < 2; ++side)
+        if (iface(*F.level, side))
+          {
+            pl_s[side].resize(plane3_doubles(F.level->geom, nf));
+            plane_op(*F.level, side, 0, nf, fv, pl_s[side].p, nullptr);
+            plane_op(*F.level, side, 3, nf, fv, nullptr, nullptr);
+          }
     check(launch_restrict3(F.dt, fine_v, coarse_v, nc, ctx->stream, F.dt.spatial ? F.tw.p : nullptr), "restrict3");
     ctx->count(F.dt.spatial ? 4 : 2);
+    if (split())
+      {
+        for (int side = 0; side < 2; ++side)
+          if (iface(*F.level, side))
+            plane_op(*F.level, side, 6, nf, fv, pl_s[side].p, nullptr);
+        iface_sum(l - 1, coarse_v, nullptr, nc, 0);
+      }
     C.zero_constrained(coarse_v, nc);
     if (project)
-      C.project_residual(coarse_v, nc);
+      this->project(l - 1, coarse_v, nc, true);
   }
 
   /// prolongate_correction (transfer.cpp:102-115), then fine (+)= result
@@ -444,7 +644,7 @@ struct stmg3_solver
     ctx->count(F.dt.spatial ? 4 : 2);
     L.zero_constrained(F.t.p, nf);
     if (project)
-      L.project(F.t.p, nf);
+      this->project(l, F.t.p, nf, false);
     if (accumulate)
       {
         check(launch_axpy(n, 1.0, nullptr, 1.0, F.t.p, fine_v, ctx->stream), "axpy");
@@ -460,20 +660,34 @@ struct stmg3_solver
   void
   coarse_forward(const double *b_v, double *x_v, int nI)
   {
+    if (split())
+      {
+        // parts -> the global coarse vector of every local interval
+        need_space();
+        const long long per_loc = static_cast<long long>(coarse_n_loc) * nI;
+        cBs.resize(per_loc * zparts);
+        if (sops.allgather(sops.user, b_v, cBs.p, per_loc, ctx->stream) != 0)
+          throw std::runtime_error("comm: allgather (parts) failed");
+        cBg.resize(static_cast<long long>(coarse_n) * nI);
+        coarse_map_kernel<<<dim3((coarse_n_loc + 127) / 128, nI, zparts), 128, 0, ctx->stream>>>(
+          cBs.p, cmap.p, coarse_n_loc, coarse_n, nI, cBg.p, 0);
+        check(cudaGetLastError(), "coarse_map");
+        ctx->count();
+      }
     const Level3Spec &sp = levels[0]->level->spec;
     const long long per = static_cast<long long>(coarse_n) * nI;
-    const double *B = b_v;
+    const double *B = split() ? cBg.p : b_v;
     if (world() > 1)
       {
         cB.resize(per * world());
-        if (comm.allgather(comm.user, b_v, cB.p, per, ctx->stream) != 0)
+        if (comm.allgather(comm.user, B, cB.p, per, ctx->stream) != 0)
           throw std::runtime_error("comm: allgather failed");
         B = cB.p;
       }
     const int n_all = nI * world();
     cX.resize(static_cast<size_t>(coarse_n) * n_all);
-    const int mv = static_cast<int>(sp.mv());
-    const long long v_off = (sp.S() - 1) * sp.mv();
+    const int mv = static_cast<int>(coarse_mv);
+    const long long v_off = (sp.S() - 1) * coarse_mv;
     const int rows_per_block = 8;
     for (int t = 0; t < n_all; ++t)
       {
@@ -483,6 +697,16 @@ struct stmg3_solver
                                              cX.p + static_cast<long long>(t) * coarse_n);
         check(cudaGetLastError(), "coarse3_step");
         ctx->count();
+      }
+    if (split())
+      {
+        // this part's dofs of this slab's intervals
+        coarse_map_kernel<<<dim3((coarse_n_loc + 127) / 128, nI, 1), 128, 0, ctx->stream>>>(
+          cX.p + static_cast<long long>(rank()) * per, cmap.p + static_cast<long long>(zpart) * coarse_n_loc,
+          coarse_n_loc, coarse_n, nI, x_v, 1);
+        check(cudaGetLastError(), "coarse_map");
+        ctx->count();
+        return;
       }
     check(cudaMemcpyAsync(x_v, cX.p + static_cast<long long>(rank()) * per, sizeof(double) * per,
                           cudaMemcpyDeviceToDevice, ctx->stream),
@@ -508,11 +732,14 @@ struct stmg3_solver
       {
         STMG_NVTX("L%d pre-smooth", l);
         if (s == 0) // x = 0 on every rank: b - A 0 = b
-          L.smooth_step(b_v, x_v, omega, nI, nullptr, 0, S.r.p, true);
+          {
+            check(cudaMemcpyAsync(S.r.p, b_v, sizeof(double) * isz, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+            vanka(l, S.r.p, x_v, nI);
+          }
         else
           {
             coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
-            L.vanka(S.r.p, x_v, nI, omega);
+            vanka(l, S.r.p, x_v, nI);
           }
       }
     coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
@@ -534,7 +761,7 @@ struct stmg3_solver
       {
         STMG_NVTX("L%d post-smooth", l);
         coupled_vmult(l, x_v, b_v, S.r.p, nI, 1);
-        L.vanka(S.r.p, x_v, nI, omega);
+        vanka(l, S.r.p, x_v, nI);
       }
   }
 
@@ -547,10 +774,11 @@ struct stmg3_solver
   }
 
   double
-  dot(const double *a, const double *b, long long n, int slot)
+  dot(const double *a, const double *b, long long n, int slot, int nI)
   {
     check(launch_dot(a, b, n, part.p, scal.p + slot, ctx->stream), "dot");
     ctx->count(2);
+    plane_fix(&b, 1, false, a, scal.p + slot, nI);
     allreduce(scal.p + slot, 1);
     double h = 0.0;
     check(cudaMemcpyAsync(&h, scal.p + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
@@ -580,7 +808,7 @@ struct stmg3_solver
     part.resize(stmg_krylov::part_doubles());
     scal.resize(2 * (max_iterations + 2));
     hist.clear();
-    const double norm_b = std::sqrt(dot(b_v, b_v, n, 0));
+    const double norm_b = std::sqrt(dot(b_v, b_v, n, 0, nI));
     const double tol = std::max(rtol * norm_b, atol);
     hist.push_back(norm_b);
     check(cudaMemsetAsync(x_v, 0, sizeof(double) * n, ctx->stream), "memset");
@@ -606,7 +834,10 @@ struct stmg3_solver
             // Arnoldi: MGS (the reference's, solver.cpp:146-152) or CGS2
             // (two batched all-reduces per iteration), krylov.hpp
             const double h_next = stmg_krylov::orthogonalize(
-              ortho, V, j, w.p, n, part.p, scal.p, hcol, [&](double *buf, int cnt) { allreduce(buf, cnt); }, ctx);
+              ortho, V, j, w.p, n, part.p, scal.p, hcol, [&](double *buf, int cnt) { allreduce(buf, cnt); }, ctx,
+              [&](const double *const *Vp, int m, bool wn, const double *wp, double *out) {
+                plane_fix(Vp, m, wn, wp, out, nI);
+              });
             const bool breakdown = !(h_next > 1e-300);
             auto Hc = [&](int i) -> double & { return H[static_cast<size_t>(j) * (m + 1) + i]; };
             for (int i = 0; i <= j; ++i)
@@ -671,7 +902,7 @@ struct stmg3_solver
         L.zero_constrained(rhs.p, 1);
       }
     const int it = gmres(rhs.p, X, iterations, history, cap, nI);
-    L.project(X, nI);
+    project(static_cast<int>(levels.size()) - 1, X, nI, false);
     return it;
   }
 };
@@ -680,14 +911,47 @@ namespace
 {
 stmg3_level *
 make_level3(stmg_ctx *ctx, const Level3Spec &s, int smoother, const std::vector<double> *verts,
-            bool affine_patches = false)
+            bool affine_patches = false, const std::vector<double> *verts_ext = nullptr)
 {
   auto L = std::make_unique<stmg3_level>();
   L->ctx = ctx;
   L->spec = s;
   L->smoother_kind = smoother;
-  build_level3(*L, verts, affine_patches);
+  build_level3(*L, verts, affine_patches, verts_ext);
   return L.release();
+}
+
+/// Vertex planes [z_lo, z_hi] of a level's vertex array.
+std::vector<double>
+vertex_planes(const Level3Spec &g, const std::vector<double> &v, int z_lo, int z_hi)
+{
+  const size_t plane = static_cast<size_t>(g.nx + 1) * (g.ny + 1) * 3;
+  return std::vector<double>(v.begin() + plane * z_lo, v.begin() + plane * (z_hi + 1));
+}
+
+/// Local coarse dof -> whole-mesh coarse dof of every z part (one interval).
+std::vector<int>
+coarse_part_map(const Level3Spec &g, int parts)
+{
+  const int nzl = g.nz / parts, p = g.p();
+  std::vector<int> map;
+  for (int part = 0; part < parts; ++part)
+    {
+      Level3Spec l = g;
+      l.nz = nzl;
+      const long long lgz = l.gz(), gxy = static_cast<long long>(g.gx()) * g.gy();
+      for (int a = 0; a < g.S(); ++a)
+        for (int c = 0; c < 3; ++c)
+          for (long long Z = 0; Z < lgz; ++Z)
+            for (long long xy = 0; xy < gxy; ++xy)
+              map.push_back(static_cast<int>(a * g.mv() + c * g.nsc() + (Z + part * nzl * p) * gxy + xy));
+      for (int a = 0; a < g.S(); ++a)
+        for (long long cell = 0; cell < l.ncells(); ++cell)
+          for (int m = 0; m < g.np(); ++m)
+            map.push_back(static_cast<int>(g.S() * g.mv() + a * g.mp() +
+                                           (cell + static_cast<long long>(part) * nzl * g.nx * g.ny) * g.np() + m));
+    }
+  return map;
 }
 } // namespace
 
@@ -865,105 +1129,191 @@ stmg3_project_mean_zero(stmg3_level *L, double *x, int n)
   return guarded([&] { L->project(x, n); });
 }
 
+namespace
+{
+stmg3_solver *
+create_solver3(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma, int n_hcoarse,
+               int time_coarsen, int k_min, int affine_patches, const double *vertices, int nu1, int nu2,
+               double omega, double rtol, double atol, int max_iterations, int z_parts, int z_part)
+{
+  if (!ctx)
+    throw std::invalid_argument("null argument");
+  if (!(omega > 0.0 && omega <= 1.0))
+    throw std::invalid_argument("omega must be in (0, 1]");
+  if (z_parts < 1 || z_part < 0 || z_part >= z_parts)
+    throw std::invalid_argument("3D split: need 0 <= z_part < z_parts");
+  if (z_parts > 1 && (!vertices || affine_patches))
+    throw std::invalid_argument("3D split: needs the (global) vertex array and exact patches");
+  check(cudaSetDevice(ctx->device), "cudaSetDevice");
+  auto S = std::make_unique<stmg3_solver>();
+  S->ctx = ctx;
+  S->nu1 = nu1;
+  S->nu2 = nu2;
+  S->omega = omega;
+  S->rtol = rtol;
+  S->atol = atol;
+  S->max_iterations = max_iterations;
+  S->zparts = z_parts;
+  S->zpart = z_part;
+  Level3Spec f;
+  f.nx = nx;
+  f.ny = ny;
+  f.nz = nz;
+  f.r = r;
+  f.k = k;
+  f.tau = tau;
+  f.nu = nu;
+  f.gamma = gamma;
+  const std::vector<PlanLevel3> d = plan3(f, n_hcoarse, time_coarsen, k_min);
+  // geometry of every level: the finest vertices restricted to the coarse
+  // vertex set (nested index sets; non-nested geometry on deformed meshes)
+  std::vector<std::vector<double>> vv(d.size());
+  if (vertices)
+    {
+      vv[0].assign(vertices, vertices + 3 * f.nverts());
+      for (size_t i = 1; i < d.size(); ++i)
+        {
+          const Level3Spec &c = d[i].s;
+          const Level3Spec &fs = d[0].s;
+          const int ratio = fs.nx / c.nx;
+          vv[i].resize(3 * c.nverts());
+          for (int vz = 0; vz <= c.nz; ++vz)
+            for (int vy = 0; vy <= c.ny; ++vy)
+              for (int vx = 0; vx <= c.nx; ++vx)
+                for (int q = 0; q < 3; ++q)
+                  vv[i][((static_cast<size_t>(vz) * (c.ny + 1) + vy) * (c.nx + 1) + vx) * 3 + q] =
+                    vv[0][((static_cast<size_t>(vz * ratio) * (fs.ny + 1) + vy * ratio) * (fs.nx + 1) + vx * ratio) *
+                            3 + q];
+        }
+    }
+  // z-split: every level holds the cells [z0, z0 + nz / z_parts) of its mesh
+  auto local_spec = [&](const Level3Spec &g) {
+    Level3Spec l = g;
+    if (z_parts > 1)
+      {
+        if (g.nz % z_parts)
+          throw std::invalid_argument("3D split: nz of every level must be divisible by z_parts");
+        l.nz = g.nz / z_parts;
+        l.nz_glob = g.nz;
+        l.zlo_bc = z_part == 0;
+        l.zhi_bc = z_part == z_parts - 1;
+      }
+    return l;
+  };
+  for (size_t i = d.size(); i-- > 0;)
+    {
+      auto SL = std::make_unique<Solver3Level>();
+      SL->tshift = d[i].tsh;
+      const Level3Spec ls = local_spec(d[i].s);
+      const int smoother = i + 1 == d.size() ? STMG_SMOOTHER_NONE : STMG_SMOOTHER_CELL;
+      if (z_parts > 1)
+        {
+          const int z0 = z_part * ls.nz, gl = ls.zlo_bc ? 0 : 1, gh = ls.zhi_bc ? 0 : 1;
+          const std::vector<double> own = vertex_planes(d[i].s, vv[i], z0, z0 + ls.nz);
+          const std::vector<double> ext = vertex_planes(d[i].s, vv[i], z0 - gl, z0 + ls.nz + gh);
+          SL->level.reset(make_level3(ctx, ls, smoother, &own, false, &ext));
+          double vol = 0.0;
+          pressure_mean3(d[i].s, &vv[i], &vol);
+          SL->level->vol_global = vol;
+          SL->level->ncells_global = static_cast<double>(d[i].s.ncells());
+        }
+      else
+        SL->level.reset(make_level3(ctx, ls, smoother, vertices ? &vv[i] : nullptr, affine_patches != 0));
+      S->levels.push_back(std::move(SL));
+    }
+  for (size_t l = 1; l < S->levels.size(); ++l)
+    {
+      Solver3Level &F = *S->levels[l];
+      const Level3Spec &cs = S->levels[l - 1]->level->spec, &fs = F.level->spec;
+      const bool ht = S->levels[l - 1]->tshift > F.tshift;
+      const Transfer3Tables t = build_transfer3(cs, fs, ht);
+      DevTransfer3 &dt = F.dt;
+      dt = DevTransfer3{};
+      dt.spatial = t.spatial;
+      dt.pmode = t.pmode;
+      dt.h_time = t.h_time;
+      std::vector<int> buf;
+      if (t.spatial)
+        {
+          const Csr1D *cc[6] = {&t.px, &t.py, &t.pz, &t.rx, &t.ry, &t.rz};
+          DevCsr *dd[6] = {&dt.px, &dt.py, &dt.pz, &dt.rx, &dt.ry, &dt.rz};
+          for (int q = 0; q < 6; ++q)
+            upload_csr(*cc[q], F.csr_i[q], F.csr_v[q], *dd[q], buf);
+          F.child.upload(t.child);
+          dt.child = F.child.p;
+        }
+      const int Sf = fs.S(), Sc = cs.S();
+      for (int h = 0; h < 2; ++h)
+        for (int a = 0; a < Sf; ++a)
+          for (int b = 0; b < Sc; ++b)
+            dt.E[h * kMaxS * kMaxS + a * kMaxS + b] = t.E[(static_cast<size_t>(h) * Sf + a) * Sc + b];
+      dt.f = F.level->geom;
+      dt.c = S->levels[l - 1]->level->geom;
+    }
+  // coarse level: G, H of the forward substitution (whole mesh)
+  {
+    const Level3Spec &g0 = d.back().s;
+    const stmg3_level &L0 = *S->levels[0]->level;
+    std::vector<double> G, H, pm;
+    coarse3_tables(g0, vertices ? &vv.back() : nullptr, G, H, pm);
+    S->cG.upload(G);
+    S->cH.upload(H);
+    S->coarse_n = static_cast<int>(g0.isz());
+    S->coarse_mv = g0.mv();
+    S->coarse_n_loc = static_cast<int>(L0.spec.isz());
+    if (z_parts > 1)
+      S->cmap.upload(coarse_part_map(g0, z_parts));
+  }
+  return S.release();
+}
+} // namespace
+
 int
 stmg3_solver_create(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
                     int n_hcoarse, int time_coarsen, int k_min, int affine_patches, const double *vertices, int nu1,
-                    int nu2, double omega,
-                    double rtol, double atol, int max_iterations, stmg3_solver **out)
+                    int nu2, double omega, double rtol, double atol, int max_iterations, stmg3_solver **out)
 {
   return guarded([&] {
     STMG_NVTX("stmg3_solver_create");
-    if (!ctx || !out)
+    if (!out)
       throw std::invalid_argument("null argument");
-    if (!(omega > 0.0 && omega <= 1.0))
-      throw std::invalid_argument("omega must be in (0, 1]");
-    check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    auto S = std::make_unique<stmg3_solver>();
-    S->ctx = ctx;
-    S->nu1 = nu1;
-    S->nu2 = nu2;
-    S->omega = omega;
-    S->rtol = rtol;
-    S->atol = atol;
-    S->max_iterations = max_iterations;
-    Level3Spec f;
-    f.nx = nx;
-    f.ny = ny;
-    f.nz = nz;
-    f.r = r;
-    f.k = k;
-    f.tau = tau;
-    f.nu = nu;
-    f.gamma = gamma;
-    const std::vector<PlanLevel3> d = plan3(f, n_hcoarse, time_coarsen, k_min);
-    // geometry of every level: the finest vertices restricted to the coarse
-    // vertex set (nested index sets; non-nested geometry on deformed meshes)
-    std::vector<std::vector<double>> vv(d.size());
-    if (vertices)
+    *out = create_solver3(ctx, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse, time_coarsen, k_min, affine_patches,
+                          vertices, nu1, nu2, omega, rtol, atol, max_iterations, 1, 0);
+  });
+}
+
+int
+stmg3_solver_create_split(stmg_ctx *ctx, int nx, int ny, int nz, int r, int k, double tau, double nu, double gamma,
+                          int n_hcoarse, int time_coarsen, int k_min, const double *vertices, int z_parts, int z_part,
+                          int nu1, int nu2, double omega, double rtol, double atol, int max_iterations,
+                          stmg3_solver **out)
+{
+  return guarded([&] {
+    STMG_NVTX("stmg3_solver_create_split");
+    if (!out)
+      throw std::invalid_argument("null argument");
+    *out = create_solver3(ctx, nx, ny, nz, r, k, tau, nu, gamma, n_hcoarse, time_coarsen, k_min, 0, vertices, nu1,
+                          nu2, omega, rtol, atol, max_iterations, z_parts, z_part);
+  });
+}
+
+int
+stmg3_solver_set_space_comm(stmg3_solver *s, const stmg_comm_space_ops *ops)
+{
+  return guarded([&] {
+    STMG_NVTX("stmg3_solver_set_space_comm");
+    if (!s)
+      throw std::invalid_argument("null solver");
+    if (ops)
       {
-        vv[0].assign(vertices, vertices + 3 * f.nverts());
-        for (size_t i = 1; i < d.size(); ++i)
-          {
-            const Level3Spec &c = d[i].s;
-            const Level3Spec &fs = d[0].s;
-            const int ratio = fs.nx / c.nx;
-            vv[i].resize(3 * c.nverts());
-            for (int vz = 0; vz <= c.nz; ++vz)
-              for (int vy = 0; vy <= c.ny; ++vy)
-                for (int vx = 0; vx <= c.nx; ++vx)
-                  for (int q = 0; q < 3; ++q)
-                    vv[i][((static_cast<size_t>(vz) * (c.ny + 1) + vy) * (c.nx + 1) + vx) * 3 + q] =
-                      vv[0][((static_cast<size_t>(vz * ratio) * (fs.ny + 1) + vy * ratio) * (fs.nx + 1) + vx * ratio) *
-                              3 + q];
-          }
+        if (ops->parts != s->zparts || ops->part != s->zpart || !ops->exchange_planes || !ops->allreduce_sum ||
+            !ops->allgather)
+          throw std::invalid_argument("space communicator does not match the solver's z partition");
+        s->sops = *ops;
+        s->has_space = true;
       }
-    for (size_t i = d.size(); i-- > 0;)
-      {
-        auto SL = std::make_unique<Solver3Level>();
-        SL->tshift = d[i].tsh;
-        SL->level.reset(make_level3(ctx, d[i].s, i + 1 == d.size() ? STMG_SMOOTHER_NONE : STMG_SMOOTHER_CELL,
-                                    vertices ? &vv[i] : nullptr, affine_patches != 0));
-        S->levels.push_back(std::move(SL));
-      }
-    for (size_t l = 1; l < S->levels.size(); ++l)
-      {
-        Solver3Level &F = *S->levels[l];
-        const Level3Spec &cs = S->levels[l - 1]->level->spec, &fs = F.level->spec;
-        const bool ht = S->levels[l - 1]->tshift > F.tshift;
-        const Transfer3Tables t = build_transfer3(cs, fs, ht);
-        DevTransfer3 &dt = F.dt;
-        dt = DevTransfer3{};
-        dt.spatial = t.spatial;
-        dt.pmode = t.pmode;
-        dt.h_time = t.h_time;
-        std::vector<int> buf;
-        if (t.spatial)
-          {
-            const Csr1D *cc[6] = {&t.px, &t.py, &t.pz, &t.rx, &t.ry, &t.rz};
-            DevCsr *dd[6] = {&dt.px, &dt.py, &dt.pz, &dt.rx, &dt.ry, &dt.rz};
-            for (int q = 0; q < 6; ++q)
-              upload_csr(*cc[q], F.csr_i[q], F.csr_v[q], *dd[q], buf);
-            F.child.upload(t.child);
-            dt.child = F.child.p;
-          }
-        const int Sf = fs.S(), Sc = cs.S();
-        for (int h = 0; h < 2; ++h)
-          for (int a = 0; a < Sf; ++a)
-            for (int b = 0; b < Sc; ++b)
-              dt.E[h * kMaxS * kMaxS + a * kMaxS + b] = t.E[(static_cast<size_t>(h) * Sf + a) * Sc + b];
-        dt.f = F.level->geom;
-        dt.c = S->levels[l - 1]->level->geom;
-      }
-    // coarse level: G, H of the forward substitution
-    {
-      const stmg3_level &L0 = *S->levels[0]->level;
-      std::vector<double> G, H, pm;
-      coarse3_tables(L0.spec, L0.deformed ? &L0.verts_h : nullptr, G, H, pm);
-      S->cG.upload(G);
-      S->cH.upload(H);
-      S->coarse_n = static_cast<int>(L0.spec.isz());
-    }
-    *out = S.release();
+    else
+      s->has_space = false;
   });
 }
 

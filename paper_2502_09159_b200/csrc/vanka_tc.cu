@@ -455,7 +455,7 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
   int c_pm = 0, p_pm = 0;
   bool c_ok = false;
   // pending tile (scattered inside the next tile's k-loop)
-  double pacc[kTCols / 8][2];
+  double pacc[kTCols / 8][2] = {};
   int p_lt = -1;
   auto scatter_one = [&](int j) {
     const int ct = j >> 1, b = j & 1;

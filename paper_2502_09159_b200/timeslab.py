@@ -97,10 +97,11 @@ class TorchComm:
 
         with _on_stream(stream, self.device):
             ops = []
+            peer = (lambda r: r) if self.group is None else (lambda r: dist.get_global_rank(self.group, r))
             if self.rank + 1 < self.world:
-                ops.append(dist.P2POp(dist.isend, _view(send, n, self.device), self.rank + 1, group=self.group))
+                ops.append(dist.P2POp(dist.isend, _view(send, n, self.device), peer(self.rank + 1), group=self.group))
             if self.rank > 0:
-                ops.append(dist.P2POp(dist.irecv, _view(recv, n, self.device), self.rank - 1, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, _view(recv, n, self.device), peer(self.rank - 1), group=self.group))
             if ops:
                 for w in dist.batch_isend_irecv(ops):
                     w.wait()
@@ -197,6 +198,121 @@ class LoopbackComm:
             for r, p in enumerate(parts):
                 out[r * n:(r + 1) * n].copy_(p)
         self._sync(stream)
+
+
+# ---------------------------------------------------------------- z parts
+# The C5 hybrid split (stmg3_solver_create_split, stmg_comm_space_ops): the
+# part's neighbours exchange their shared interface planes; pressure means
+# and Krylov sums are reduced over the parts; the coarse level is gathered.
+
+def z_part_dofs(nx: int, ny: int, nz: int, r: int, k: int, parts: int, part: int):
+    """Whole-mesh index (within one interval) of every dof of z part `part`,
+    in the part's own BlockVector order (3D layout of include/stmg_b200.h):
+    velocity (slot, component, node (Z, Y, X)), then pressure (slot, cell, mode)."""
+    import numpy as np
+
+    if nz % parts:
+        raise ValueError("nz must be divisible by the number of z parts")
+    p, S = r + 1, k + 1
+    npm = (r + 1) * (r + 2) * (r + 3) // 6
+    gx, gy, gz = nx * p + 1, ny * p + 1, nz * p + 1
+    nsc = gx * gy * gz
+    mv, mp = 3 * nsc, nx * ny * nz * npm
+    nzl = nz // parts
+    gzl = nzl * p + 1
+    plane = gx * gy
+    nodes = (np.arange(gzl)[:, None] + part * nzl * p) * plane + np.arange(plane)[None, :]
+    vel = (np.arange(S)[:, None, None] * mv + np.arange(3)[None, :, None] * nsc + nodes.reshape(1, 1, -1)).ravel()
+    cells = np.arange(nx * ny * nzl) + part * nzl * nx * ny
+    pre = (S * mv + np.arange(S)[:, None, None] * mp + cells[None, :, None] * npm
+           + np.arange(npm)[None, None, :]).ravel()
+    return np.concatenate([vel, pre]).astype(np.int64)
+
+
+class LoopbackSpaceHub:
+    """Shared state of the `parts` in-process z parts of one time slab
+    (host-synchronised, as LoopbackHub)."""
+
+    def __init__(self, parts: int, timeout: float = 120.0):
+        import queue
+
+        self.hub = LoopbackHub(parts, timeout)
+        self.parts = parts
+        # from_below[p]: planes sent up by part p-1; from_above[p]: sent down by p+1
+        self.from_below = [queue.Queue() for _ in range(parts)]
+        self.from_above = [queue.Queue() for _ in range(parts)]
+
+
+class LoopbackSpaceComm:
+    """stmg_comm_space_ops for in-process z parts (threads) on one GPU."""
+
+    def __init__(self, hub: LoopbackSpaceHub, part: int, device="cuda"):
+        self.hub, self.part, self.parts, self.device = hub, part, hub.parts, device
+        self._inner = LoopbackComm(hub.hub, part, device)
+
+    def exchange_planes(self, send_lo, recv_lo, send_hi, recv_hi, n, stream=None):
+        c = self._inner
+        c._sync(stream)
+        if send_lo and self.part > 0:
+            self.hub.from_above[self.part - 1].put(c._snapshot(send_lo, n, stream))
+        if send_hi and self.part + 1 < self.parts:
+            self.hub.from_below[self.part + 1].put(c._snapshot(send_hi, n, stream))
+        for ptr, q in ((recv_lo, self.hub.from_below[self.part]), (recv_hi, self.hub.from_above[self.part])):
+            if ptr:
+                data = q.get(timeout=self.hub.hub.timeout)
+                with _on_stream(stream, self.device):
+                    _view(ptr, n, self.device).copy_(data)
+        c._sync(stream)
+
+    def allreduce_sum(self, buf, n, stream=None):
+        self._inner.allreduce_sum(buf, n, stream)
+
+    def allgather(self, send, recv, n, stream=None):
+        self._inner.allgather(send, recv, n, stream)
+
+
+class TorchSpaceComm:
+    """stmg_comm_space_ops over a torch.distributed group of the z parts
+    (group rank = part): interface planes by send/recv with the neighbours."""
+
+    def __init__(self, device="cuda", group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.part = dist.get_rank(group)
+        self.parts = dist.get_world_size(group)
+        self.device = device
+        self._inner = TorchComm(device, group)
+
+    def _peer(self, part):
+        import torch.distributed as dist
+
+        return part if self.group is None else dist.get_global_rank(self.group, part)
+
+    def exchange_planes(self, send_lo, recv_lo, send_hi, recv_hi, n, stream=None):
+        import torch.distributed as dist
+
+        with _on_stream(stream, self.device):
+            ops = []
+            if send_lo and self.part > 0:
+                ops.append(dist.P2POp(dist.isend, _view(send_lo, n, self.device), self._peer(self.part - 1),
+                                      group=self.group))
+                ops.append(dist.P2POp(dist.irecv, _view(recv_lo, n, self.device), self._peer(self.part - 1),
+                                      group=self.group))
+            if send_hi and self.part + 1 < self.parts:
+                ops.append(dist.P2POp(dist.isend, _view(send_hi, n, self.device), self._peer(self.part + 1),
+                                      group=self.group))
+                ops.append(dist.P2POp(dist.irecv, _view(recv_hi, n, self.device), self._peer(self.part + 1),
+                                      group=self.group))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+
+    def allreduce_sum(self, buf, n, stream=None):
+        self._inner.allreduce_sum(buf, n, stream)
+
+    def allgather(self, send, recv, n, stream=None):
+        self._inner.allgather(send, recv, n, stream)
 
 
 def nccl_comm(device: Optional[int] = None, group=None):

@@ -1,0 +1,154 @@
+"""GPU tier: the C5 hybrid split (stmg3_solver_create_split) -- z parts of a
+deformed 3D mesh, each held as its own sub-mesh with shared interface planes,
+plus time slabs -- reproduces the unpartitioned all-at-once V-cycle and FGMRES
+solve. Parts and slabs run as threads on the one GPU with host-synchronised
+loopback exchanges (timeslab.LoopbackSpaceComm / LoopbackComm), so no kernel
+waits on another rank's kernel. The unpartitioned solver is itself pinned to
+the oracle's 3D restatement (test_gpu_3d.py)."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle3_ctypes as o3
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _run_ranks(fn, n):
+    errors = []
+
+    def wrap(q):
+        try:
+            fn(q)
+        except BaseException as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=wrap, args=(q,)) for q in range(n)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(600)
+    assert not errors, errors
+
+
+SPLITS = [  # nx, ny, nz, r, k, n_hcoarse, parts
+    (4, 4, 4, 1, 1, 1, 2),
+    (4, 4, 4, 2, 2, 1, 2),
+    (4, 4, 6, 1, 1, 1, 3),  # a middle part with two interfaces
+]
+
+
+@pytest.mark.parametrize("nx,ny,nz,r,k,nh,parts", SPLITS)
+def test_split_vcycle_matches_unsplit(stmg, ctx, nx, ny, nz, r, k, nh, parts):
+    """z parts (one time slab): the all-at-once V-cycle of the split solver,
+    gathered over the parts, equals the unpartitioned one (<= 1e-10), and the
+    parts agree on their shared interface planes."""
+    from paper_2502_09159_b200 import timeslab
+
+    N, tau = 2, 1.0 / 8
+    verts = o3.vertices(nx, ny, nz, 0.1, seed=11)
+    S1 = stmg.Solver3(ctx, nx, ny, nz, r, k, tau, 1.0, 1.0, n_hcoarse=nh, time_coarsen=False, k_min=k,
+                      vertices=verts)
+    f = S1.finest
+    ref = o3.OracleLevel3(nx, ny, nz, r, k, tau, 1.0, 1.0, vertices=verts, smoother=False)
+    b = o3.make_consistent3(np.random.default_rng(21).uniform(-1, 1, N * f.size), ref, N)
+    x1 = torch.zeros(N * f.size, dtype=torch.float64, device="cuda")
+    S1.vcycle_all_at_once(_cuda(b), x1, N)
+    torch.cuda.synchronize()
+    x1 = x1.cpu().numpy().reshape(N, f.size)
+    hub = timeslab.LoopbackSpaceHub(parts, timeout=120.0)
+    out = {}
+
+    def rank(part):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            c = stmg.Context(0, stream=stream)
+            sol = stmg.Solver3(c, nx, ny, nz, r, k, tau, 1.0, 1.0, n_hcoarse=nh, time_coarsen=False, k_min=k,
+                               vertices=verts, z_parts=parts, z_part=part)
+            sol.set_space_comm(timeslab.LoopbackSpaceComm(hub, part))
+            idx = timeslab.z_part_dofs(nx, ny, nz, r, k, parts, part)
+            assert len(idx) == sol.finest.size
+            bl = _cuda(b.reshape(N, f.size)[:, idx])
+            xl = torch.zeros_like(bl)
+            stream.synchronize()
+            sol.vcycle_all_at_once(bl.reshape(-1), xl.reshape(-1), N)
+            stream.synchronize()
+            out[part] = (idx, xl.cpu().numpy())
+
+    _run_ranks(rank, parts)
+    scale = np.abs(x1).max()
+    for part in range(parts):
+        idx, xl = out[part]
+        err = np.abs(xl - x1[:, idx]).max() / scale
+        assert err <= 1e-10, (part, err)
+
+
+@pytest.mark.parametrize("parts,slabs", [(2, 2), (3, 1)])
+def test_split_solve_matches_unsplit(stmg, ctx, parts, slabs):
+    """parts x slabs ranks (the C5 hybrid 2 x 4 layout in miniature, C5's
+    discretisation: deformed, Q3/P2disc, DG(2)): FGMRES iterations within
+    +-1 of the unpartitioned solve (which test_gpu_3d.py pins to the oracle),
+    solution <= 1e-9 of it."""
+    from paper_2502_09159_b200 import timeslab
+
+    nx, ny, nz = 4, 4, 2 * parts
+    r, k, nh, n_local = 2, 2, 1, 2
+    N, tau = n_local * slabs, 1.0 / 8
+    verts = o3.vertices(nx, ny, nz, 0.1, seed=12)
+    kw = dict(n_hcoarse=nh, time_coarsen=False, k_min=k, vertices=verts, rtol=1e-10)
+    S1 = stmg.Solver3(ctx, nx, ny, nz, r, k, tau, 1.0, 1.0, **kw)
+    f = S1.finest
+    ref = o3.OracleLevel3(nx, ny, nz, r, k, tau, 1.0, 1.0, vertices=verts, smoother=False)
+    F = o3.make_consistent3(np.random.default_rng(22).uniform(-1, 1, N * f.size), ref, N)
+    X1 = torch.zeros(N * f.size, dtype=torch.float64, device="cuda")
+    it1, _ = S1.solve_all_at_once(_cuda(F), X1, N)
+    torch.cuda.synchronize()
+    X1 = X1.cpu().numpy().reshape(N, f.size)
+    space_hubs = [timeslab.LoopbackSpaceHub(parts, timeout=120.0) for _ in range(slabs)]
+    time_hubs = [timeslab.LoopbackHub(slabs, timeout=120.0) for _ in range(parts)]
+    out = {}
+
+    def rank(q):
+        part, slab = q % parts, q // parts
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            c = stmg.Context(0, stream=stream)
+            sol = stmg.Solver3(c, nx, ny, nz, r, k, tau, 1.0, 1.0, z_parts=parts, z_part=part, **kw)
+            sol.set_space_comm(timeslab.LoopbackSpaceComm(space_hubs[slab], part))
+            if slabs > 1:
+                sol.set_comm(timeslab.LoopbackComm(time_hubs[part], slab))
+            idx = timeslab.z_part_dofs(nx, ny, nz, r, k, parts, part)
+            Fl = _cuda(F.reshape(N, f.size)[slab * n_local:(slab + 1) * n_local][:, idx])
+            Xl = torch.zeros_like(Fl)
+            stream.synchronize()
+            it, _ = sol.solve_all_at_once(Fl.reshape(-1), Xl.reshape(-1), n_local)
+            stream.synchronize()
+            out[q] = (it, part, slab, idx, Xl.cpu().numpy())
+
+    _run_ranks(rank, parts * slabs)
+    its = {v[0] for v in out.values()}
+    assert len(its) == 1 and abs(its.pop() - it1) <= 1, (its, it1)
+    Xp = np.zeros_like(X1)
+    for it, part, slab, idx, Xl in out.values():
+        Xp[slab * n_local:(slab + 1) * n_local][:, idx] = Xl
+    assert np.linalg.norm(Xp - X1) / np.linalg.norm(X1) <= 1e-9
+
+
+def test_split_rejects_bad_partitions(stmg, ctx):
+    verts = o3.vertices(4, 4, 4, 0.1, seed=13)
+    with pytest.raises(stmg.StmgError):  # 4 cells in z do not split in 3
+        stmg.Solver3(ctx, 4, 4, 4, 1, 1, 0.125, n_hcoarse=1, time_coarsen=False, k_min=1, vertices=verts,
+                     z_parts=3, z_part=0)
+    with pytest.raises(stmg.StmgError):  # no geometry: the split needs the deformed-level path
+        stmg.Solver3(ctx, 4, 4, 4, 1, 1, 0.125, n_hcoarse=1, time_coarsen=False, k_min=1, z_parts=2, z_part=0)
+    sol = stmg.Solver3(ctx, 4, 4, 4, 1, 1, 0.125, n_hcoarse=1, time_coarsen=False, k_min=1, vertices=verts,
+                       z_parts=2, z_part=0)
+    b = torch.zeros(sol.finest.size, dtype=torch.float64, device="cuda")
+    with pytest.raises(stmg.StmgError):  # the parts' communicator is missing
+        sol.vcycle_all_at_once(b, torch.zeros_like(b), 1)
