@@ -27,6 +27,8 @@ Extra fields of the JSON line (not the headline; skipped with --no-solve):
   solve.C4_full        (1 GPU) the whole 64-interval C4 system as 8 macro steps
   solve.C3_all_at_once the 64-interval C3 system (32^3, Q2/P1disc, DG(1))
                        split into time slabs over all ranks (NCCL)
+  solve.C5_hybrid      (N >= 2, even) the whole 128-interval C5 system as one
+                       all-at-once solve, hybrid 2 z parts x N/2 time slabs
   C4_step              C4 vmult + vertex-star smoother step over 8 intervals
   3D.C3                (1 GPU) C3: 32^3 Q2/P1disc, DG(1), 64 intervals: vmult,
                        cell-Vanka step, full all-at-once solve (tools/bench3d.py)
@@ -403,6 +405,88 @@ def c3_slab_leg(stmg, torch, dist, world, rank, n_total=64):
     return out
 
 
+def c5_hybrid_leg(stmg, torch, dist, world, rank, n=32, n_total=128, parts=2):
+    """BASELINE configs[4] (C5) as specified: ONE all-at-once FGMRES solve of
+    the whole 128-interval 32^3 deformed Q3/P2disc DG(2) system, hybrid
+    partition of `world` = parts (z) x slabs (time) GPUs (2 x 4 on 8 GPUs;
+    stmg3_solver_create_split). Both communicators are the library's NCCL
+    ones: time slabs among the ranks of one z part, interface planes / part
+    sums among the ranks of one slab. RHS: a hash of the global dof index
+    (so the parts agree on their shared planes), made consistent with the
+    global pressure mean. Hierarchy as the 1-GPU C5 leg (r 2 -> 1, h in space
+    to 2^3, k kept at 2, exact patch inverses built on the GPU). Time = max
+    over ranks."""
+    from paper_2502_09159_b200 import timeslab
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    import bench3d
+
+    slabs = world // parts
+    part, slab = rank % parts, rank // parts
+    n_local = n_total // slabs
+    # every rank creates every group, in the same order
+    tgroups = [dist.new_group([s * parts + p for s in range(slabs)]) for p in range(parts)]
+    sgroups = [dist.new_group([s * parts + p for p in range(parts)]) for s in range(slabs)]
+    ctx = stmg.Context(torch.cuda.current_device())
+    t0 = time.perf_counter()
+    sol = stmg.Solver3(ctx, n, n, n, 2, 2, 1.0 / n_total, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=2,
+                       vertices=bench3d.c5_vertices(n), nu1=2, nu2=2, rtol=1e-8, z_parts=parts, z_part=part)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    if slabs > 1:
+        sol.set_comm(timeslab.nccl_comm(group=tgroups[part]))
+    sol.set_space_comm(timeslab.nccl_comm(group=sgroups[slab]))
+    sol.set_krylov(stmg.ORTHO_CGS2)
+    f = sol.finest
+    idx = torch.from_numpy(timeslab.z_part_dofs(n, n, n, 2, 2, parts, part)).cuda()
+    gn = torch.arange(slab * n_local, (slab + 1) * n_local, device="cuda", dtype=torch.int64)[:, None]
+    h = (idx[None, :] * 2654435761 + gn * 2246822519 + 12345) % 4294967296
+    h = (h ^ (h >> 13)) * 1274126177 % 4294967296
+    F = (h.double() / 4294967296.0 * 2 - 1).reshape(-1).contiguous()
+    del h
+    V = F.view(n_local, f.size)
+    bnd = torch.zeros((f.gz, f.gy, f.gx), dtype=torch.bool, device="cuda")
+    bnd[:, 0] = bnd[:, -1] = True
+    bnd[:, :, 0] = bnd[:, :, -1] = True
+    if part == 0:
+        bnd[0] = True
+    if part == parts - 1:
+        bnd[-1] = True
+    bnd = bnd.reshape(-1)
+    for a in range(f.n_slots):
+        for c in range(3):
+            base = a * f.n_velocity + c * f.n_scalar
+            V[:, base:base + f.n_scalar][:, bnd] = 0.0
+        p0 = f.n_slots * f.n_velocity + a * f.n_pressure
+        P = V[:, p0:p0 + f.n_pressure].view(n_local, -1, f.n_p)
+        m = P[:, :, 0].sum(dim=1).contiguous()
+        dist.all_reduce(m, group=sgroups[slab])
+        P[:, :, 0] -= (m / (n ** 3))[:, None]
+    X = torch.zeros_like(F)
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    it, hist = sol.solve_all_at_once(F, X, n_local)
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) / 1e3
+    t = torch.tensor([sec], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
+    # whole-system dofs: the parts' interface planes are stored twice
+    total = n_total * (f.size * parts - (parts - 1) * f.n_slots * 3 * f.gx * f.gy)
+    out = {"dofs": int(total), "intervals": n_total, "seconds": sec, "dofs_per_s": total / sec,
+           "fgmres_iterations": it, "relative_residual": hist[-1] / hist[0], "setup_s": setup,
+           "levels": sol.n_levels, "smoother": "cell Vanka, exact per-cell patch inverses (built on the GPU)",
+           "partition": f"hybrid {parts} z parts x {slabs} time slabs of {n_local} intervals (one all-at-once solve)",
+           "deviation_from_baseline": "hierarchy substituted: k kept at 2 (BASELINE configs[4]: k 2->1->0), h in "
+                                      "space only, exact coarse forward substitution over all 128 intervals"}
+    del sol, F, X
+    torch.cuda.empty_cache()
+    return out
+
+
 def slab_solve_leg(stmg, ctx, torch, dist, world, rank, n_local=8):
     """All-at-once FGMRES + hp-STMG V(2,2) solve of the C4 discretisation
     (1024^2, Q2/P1, DG(1), tau = 1/64, vertex-star Vanka) partitioned by time
@@ -625,7 +709,7 @@ def main():
         e2e = {"value": world * dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * (3 * dofs + 2 * mv),
                "d2h_bytes_per_step": 8 * 2 * dofs}
 
-    slab = c3slab = None
+    slab = c3slab = c5hyb = None
     if not args.no_solve:
         try:  # a side leg: a failure is reported in the line, never fatal for the headline
             slab = slab_solve_leg(stmg, ctx, torch, dist, world, rank)
@@ -635,6 +719,11 @@ def main():
             c3slab = c3_slab_leg(stmg, torch, dist, world, rank)
         except Exception as exc:
             c3slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        if world > 1 and world % 2 == 0:
+            try:
+                c5hyb = c5_hybrid_leg(stmg, torch, dist, world, rank)
+            except Exception as exc:
+                c5hyb = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank != 0:
         if world > 1:
@@ -700,6 +789,8 @@ def main():
         line["solve"] = side(lambda: solve_legs(stmg, ctx, torch))
         line["solve"]["C4_all_at_once"] = slab
         line["solve"]["C3_all_at_once"] = c3slab
+        if c5hyb is not None:
+            line["solve"]["C5_hybrid"] = c5hyb
         line["C4_step"] = side(lambda: c4_step_leg(stmg, ctx, torch))
         if world == 1:
             line["solve"]["C4_full"] = side(lambda: c4_full_leg(stmg, ctx, torch))

@@ -332,10 +332,11 @@ def nccl_comm(device: Optional[int] = None, group=None):
     if rank == 0:
         uid.copy_(torch.frombuffer(bytearray(NcclComm.unique_id()), dtype=torch.uint8))
     backend = dist.get_backend(group)
+    src = 0 if group is None else dist.get_global_rank(group, 0)  # broadcast takes a global rank
     if backend == "nccl":
         uid_dev = uid.to(f"cuda:{dev}")
-        dist.broadcast(uid_dev, 0, group=group)
+        dist.broadcast(uid_dev, src, group=group)
         uid = uid_dev.cpu()
     else:
-        dist.broadcast(uid, 0, group=group)
+        dist.broadcast(uid, src, group=group)
     return NcclComm(rank, world, dev, bytes(uid.numpy().tobytes()))
