@@ -24,6 +24,7 @@
 #pragma once
 #include "level_consts.cuh"
 
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace stmg_b200
@@ -75,6 +76,18 @@ sign_refl(int i, int k) // C1(N-1-i, N-1-k) = -C1(i, k)
 // cp.async one node row ahead. Warp b stages input slot b with a fixed
 // lane -> node mapping (one address add per copy), so the contractions read
 // shared memory instead of waiting on global loads.
+#ifndef STMG_VM_STAGE_R1
+#define STMG_VM_STAGE_R1 1 // staging of r = 1 plain applications: 0 direct loads, 1 cp.async, 2 bulk copies
+#endif
+#ifndef STMG_VM_STAGE_R1_RESID
+#define STMG_VM_STAGE_R1_RESID 0
+#endif
+#ifndef STMG_VM_STAGE_R2
+#define STMG_VM_STAGE_R2 0
+#endif
+#ifndef STMG_VM_STAGE_R2_RESID
+#define STMG_VM_STAGE_R2_RESID 0
+#endif
 template <int R, int S>
 struct RowStage
 {
@@ -83,20 +96,68 @@ struct RowStage
   static constexpr int NBUF = (2 * S + 2) * VW;  // one node row: S slots x 2 comps + v_prev x 2 comps
   static constexpr int NPRE = S * 32 * NPM;      // pressure of one cell row
   static constexpr size_t kBytes = sizeof(double) * (2 * NBUF + NPRE);
-  // Measured per instantiation (C2 r = 2 and C4 r = 1 on the B200): staging
-  // wins for r = 1 plain applications (C4 vmult 1.66 -> 1.26 ms) and loses
-  // for r = 2 (2.63 -> 2.80 ms) and for residuals (their late b loads stall
-  // in lockstep behind the per-row barriers), which keep direct loads.
+  // bulk-copy (TMA engine, cp.async.bulk) layout: every row padded to VWB
+  // doubles so a 16-byte aligned superset of the strip row fits (the node
+  // grid is odd-sized: rows start at any 8-byte offset)
+  static constexpr int VWB = (VW + 3 + 1) / 2 * 2;
+  static constexpr int NBUFB = (2 * S + 2) * VWB;
+  static constexpr int PB = (32 * NPM + 3 + 1) / 2 * 2;
+  static constexpr int DEPTH = 4; // bulk ring: node rows issued DEPTH - 1 rows ahead
+  static constexpr size_t kBytesBulk =
+    sizeof(double) * (DEPTH * NBUFB + 2 * S * PB) + DEPTH * sizeof(unsigned long long);
+  // Measured per instantiation (C2 r = 2 and C4 r = 1 on the B200): cp.async
+  // staging wins for r = 1 plain applications (C4 vmult 1.66 -> 1.26 ms) and
+  // loses for r = 2 (2.63 -> 2.80 ms) and for residuals (their late b loads
+  // stall in lockstep behind the per-row barriers), which keep direct loads.
   template <bool RESID>
-  static constexpr bool on()
+  __host__ __device__ static constexpr int mode()
   {
 #ifdef STMG_VM_NOSTAGE
-    return false;
+    return 0;
 #else
-    return R == 1 && !RESID;
+    return R == 1 ? (RESID ? STMG_VM_STAGE_R1_RESID : STMG_VM_STAGE_R1)
+                  : (R == 2 ? (RESID ? STMG_VM_STAGE_R2_RESID : STMG_VM_STAGE_R2) : 0);
 #endif
   }
+  template <bool RESID>
+  __host__ __device__ static constexpr bool on()
+  {
+    return mode<RESID>() != 0;
+  }
+  template <bool RESID>
+  static constexpr size_t bytes()
+  {
+    return mode<RESID>() == 2 ? kBytesBulk : (mode<RESID>() == 1 ? kBytes : 0);
+  }
 };
+
+__device__ __forceinline__ unsigned
+vm_smem_u32(const void *p)
+{
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// One bulk copy of the 16-byte aligned superset of src[lo, hi) into the
+// row buffer whose element 0 is global element base_al (16-byte aligned):
+// returns the bytes in flight for the mbarrier's transaction count.
+__device__ __forceinline__ unsigned
+vm_bulk_row(double *row, const double *base_al, const double *lo, const double *hi, unsigned long long *bar)
+{
+  if (hi <= lo)
+    return 0;
+  const double *a = reinterpret_cast<const double *>(reinterpret_cast<uintptr_t>(lo) & ~uintptr_t(15));
+  const double *e = reinterpret_cast<const double *>((reinterpret_cast<uintptr_t>(hi) + 15) & ~uintptr_t(15));
+  const unsigned bytes = static_cast<unsigned>((e - a) * sizeof(double));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                 vm_smem_u32(row + (a - base_al))),
+               "l"(a), "r"(bytes), "r"(vm_smem_u32(bar))
+               : "memory");
+  return bytes;
+}
+__device__ __forceinline__ const double *
+vm_align_down(const double *q)
+{
+  return reinterpret_cast<const double *>(reinterpret_cast<uintptr_t>(q) & ~uintptr_t(15));
+}
 
 __device__ __forceinline__ void
 vm_cp_async8(double *dst, const double *src)
@@ -158,12 +219,84 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
 
   using RS = RowStage<R, S>;
   constexpr bool kStaged = RS::template on<RESID>();
+  constexpr bool kBulk = RS::template mode<RESID>() == 2;
+  constexpr int RW = kBulk ? RS::VWB : RS::VW;  // row pitch of the staging buffers
+  constexpr int NB = kBulk ? RS::NBUFB : RS::NBUF;
+  constexpr int PP = kBulk ? RS::PB : 32 * NPM; // pressure pitch per slot
   extern __shared__ __align__(16) double vm_smem[];
-  double *const pre_s = vm_smem + 2 * RS::NBUF;
+  constexpr int RING = kBulk ? RS::DEPTH : 2;
+  double *const pre_s = vm_smem + RING * NB;
+  unsigned long long *const vm_bar = reinterpret_cast<unsigned long long *>(pre_s + (kBulk ? 2 : 1) * S * PP);
   const int X0 = (blockIdx.x * kStrip - 1) * p; // first node column of the strip
   const int cx0 = blockIdx.x * kStrip - 1;
+  // bulk path: element j of a staged row sits at j + delta, delta = 8-byte
+  // misalignment of the row's first node (the buffer starts 16-byte aligned)
+  auto row_src = [&](int r2, int cyy, int l) -> const double * {
+    const long long rowoff = static_cast<long long>(cyy * p + l) * gx + X0;
+    return r2 < 2 * S ? xn + (r2 >> 1) * mv + (r2 & 1) * nsc + rowoff : vprev + (r2 & 1) * nsc + rowoff;
+  };
+  auto pre_src = [&](int bs, int cyy) -> const double * {
+    return xn + S * mv + bs * mp + (static_cast<long long>(cyy) * P.nx + cx0) * NPM;
+  };
+  auto mis = [](const double *q) -> int { return static_cast<int>((reinterpret_cast<uintptr_t>(q) >> 3) & 1); };
+  if constexpr (kBulk)
+    {
+      if (threadIdx.x == 0)
+        {
+          for (int q = 0; q < RING; ++q)
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(vm_smem_u32(vm_bar + q)));
+          asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+      __syncthreads();
+    }
+  // node row l of cell row cyy (and, for l == 0, its pressure) into buffer
+  // buf by bulk copies: lane q of warp 0 issues copy q (its bytes announced
+  // with expect_tx first), lane 0 arrives once the warp has issued them all
+  auto stage_row_bulk = [&](int cyy, int l, int buf) {
+    if (threadIdx.x >= 32)
+      return;
+    unsigned long long *bar = vm_bar + buf;
+    const int nrows = vprev != nullptr ? 2 * S + 2 : 2 * S;
+    const int q = threadIdx.x;
+    const double *src = nullptr, *lo = nullptr, *hi = nullptr;
+    double *row = nullptr;
+    if (q < nrows)
+      {
+        src = row_src(q, cyy, l);
+        lo = src + max(0, -X0);             // strip-row nodes inside the grid
+        hi = src + min(RS::VW, gx - X0);
+        row = vm_smem + buf * NB + q * RW;
+      }
+    else if (l == 0 && q < nrows + S)
+      {
+        const int bs = q - nrows;
+        src = pre_src(bs, cyy);
+        lo = src + (max(cx0, 0) - cx0) * NPM;
+        hi = src + (min(cx0 + 32, P.nx) - cx0) * NPM;
+        row = pre_s + ((cyy & 1) * S + bs) * PP;
+      }
+    if (src != nullptr && hi > lo)
+      {
+        const double *al = vm_align_down(lo);
+        const double *e = reinterpret_cast<const double *>((reinterpret_cast<uintptr_t>(hi) + 15) & ~uintptr_t(15));
+        const unsigned bytes = static_cast<unsigned>((e - al) * sizeof(double));
+        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;\n" ::"r"(vm_smem_u32(bar)), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       vm_smem_u32(row + (al - vm_align_down(src)))),
+                     "l"(al), "r"(bytes), "r"(vm_smem_u32(bar))
+                     : "memory");
+      }
+    __syncwarp();
+    if (q == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(vm_smem_u32(bar)) : "memory");
+  };
   // gather node row l of cell row cyy (and, for l == 0, its pressure) into buffer buf
   auto stage_row = [&](int cyy, int l, int buf) {
+    if constexpr (kBulk)
+      {
+        stage_row_bulk(cyy, l, buf);
+        return;
+      }
     double *dst = vm_smem + buf * RS::NBUF;
     const long long rowoff = static_cast<long long>(cyy * p + l) * gx + X0;
 #pragma unroll
@@ -196,7 +329,21 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
   auto stage_sync = [&](int cy, int l) {
     if constexpr (kStaged)
       {
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        if constexpr (kBulk)
+          {
+            const int s0 = (cy - cy_first) * N1 + l;
+            asm volatile("{\n .reg .pred p;\n VMW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                         " @!p bra VMW_%=;\n}\n" ::"r"(vm_smem_u32(vm_bar + s0 % RING)),
+                         "r"((s0 / RING) & 1)
+                         : "memory");
+            __syncthreads(); // everybody is past row s0 - 1: its buffer takes row s0 + RING - 1
+            const int s = s0 + RING - 1, cyn = cy_first + s / N1;
+            if (cyn < cy_end)
+              stage_row(cyn, s % N1, s % RING);
+            return;
+          }
+        else
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
         const int s = (cy - cy_first) * N1 + l + 1;
         if (l + 1 < N1)
@@ -207,7 +354,13 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
   };
   if constexpr (kStaged)
     {
-      if (cy_first < cy_end)
+      if constexpr (kBulk)
+        {
+          for (int s = 0; s < RING - 1; ++s)
+            if (cy_first + s / N1 < cy_end)
+              stage_row(cy_first + s / N1, s % N1, s);
+        }
+      else if (cy_first < cy_end)
         stage_row(cy_first, 0, 0);
     }
 
@@ -238,7 +391,8 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
               {
                 const double c = mt[bs];
                 const double *pp = xn + S * mv + bs * mp + cell * NPM;
-                const double *ps = pre_s + (bs * 32 + lane) * NPM;
+                const double *ps = kBulk ? pre_s + ((cy & 1) * S + bs) * PP + mis(pre_src(bs, cy)) + lane * NPM
+                                         : pre_s + (bs * 32 + lane) * NPM;
 #pragma unroll
                 for (int m = 0; m < NPM; ++m)
                   PM[m] = fma(c, kStaged ? ps[m] : __ldg(pp + m), PM[m]);
@@ -290,7 +444,7 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
         {
           if (l > 0)
             stage_sync(cy, l);
-          const double *sb = vm_smem + (((cy - cy_first) * N1 + l) & 1) * RS::NBUF;
+          const double *sb = vm_smem + (((cy - cy_first) * N1 + l) % RING) * NB;
           if (active)
             {
               const int Y = cy * p + l;
@@ -308,10 +462,12 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
 #pragma unroll
                   for (int bs = 0; bs < S; ++bs)
                     {
+                      const int dx = kBulk ? mis(row_src(2 * bs, cy, l)) : 0;
+                      const int dy = kBulk ? mis(row_src(2 * bs + 1, cy, l)) : 0;
                       const double vx =
-                        bnd ? 0.0 : (kStaged ? sb[(bs * 2 + 0) * RS::VW + js] : __ldg(xn + bs * mv + node));
+                        bnd ? 0.0 : (kStaged ? sb[(bs * 2 + 0) * RW + js + dx] : __ldg(xn + bs * mv + node));
                       const double vy =
-                        bnd ? 0.0 : (kStaged ? sb[(bs * 2 + 1) * RS::VW + js] : __ldg(xn + bs * mv + nsc + node));
+                        bnd ? 0.0 : (kStaged ? sb[(bs * 2 + 1) * RW + js + dy] : __ldg(xn + bs * mv + nsc + node));
                       ukx = fma(kt[bs], vx, ukx);
                       umx = fma(mt[bs], vx, umx);
                       uky = fma(kt[bs], vy, uky);
@@ -319,8 +475,10 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
                     }
                   if (vprev != nullptr)
                     {
-                      ukx = fma(-lva, kStaged ? sb[(2 * S + 0) * RS::VW + js] : __ldg(vprev + node), ukx);
-                      uky = fma(-lva, kStaged ? sb[(2 * S + 1) * RS::VW + js] : __ldg(vprev + nsc + node), uky);
+                      const int dx = kBulk ? mis(row_src(2 * S, cy, l)) : 0;
+                      const int dy = kBulk ? mis(row_src(2 * S + 1, cy, l)) : 0;
+                      ukx = fma(-lva, kStaged ? sb[(2 * S + 0) * RW + js + dx] : __ldg(vprev + node), ukx);
+                      uky = fma(-lva, kStaged ? sb[(2 * S + 1) * RW + js + dy] : __ldg(vprev + nsc + node), uky);
                     }
                   UKx[k] = ukx;
                   UMx[k] = umx;
@@ -483,13 +641,13 @@ launch_rs(const LevelConsts &P, const double *x, const double *b, double *y, int
   const int rows = (P.ny + segs - 1) / segs;
   dim3 grid(strips, (P.ny + rows - 1) / rows, n_intervals);
   dim3 block(32 * S);
-  auto go = [&](auto kern, bool staged) {
-    const size_t smem = staged ? RowStage<R, S>::kBytes : 0;
+  auto go = [&](auto kern, size_t smem) {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<grid, block, smem, stream>>>(P, x, b, y, xprev0, rows, coupled);
   };
-  constexpr bool st_plain = RowStage<R, S>::template on<false>(), st_resid = RowStage<R, S>::template on<true>();
+  constexpr size_t st_plain = RowStage<R, S>::template bytes<false>(),
+                   st_resid = RowStage<R, S>::template bytes<true>();
   switch (mode)
     {
       case 0: go(vmult_kernel<R, S, false, false>, st_plain); break;
