@@ -1507,8 +1507,8 @@ vmult3_init_kernel(DevGeom3 G, const double *__restrict__ x, const double *__res
 
 template <int R, int S>
 cudaError_t
-launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, int nI, const double *xprev0,
-           int coupled, int mode, cudaStream_t st)
+launch_rs3_chunk(const Level3Consts &P, const double *x, const double *b, double *y, int nI, const double *xprev0,
+                 int coupled, int mode, cudaStream_t st)
 {
   DevGeom3 G{};
   G.nx = P.nx;
@@ -1634,6 +1634,36 @@ launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, i
         }
     }
   return cudaGetLastError();
+}
+
+/// Intervals per init + scatter pass: the velocity rows the pass's red.adds
+/// hit stay L2-resident between the init kernel and the cell kernel (on
+/// C5's fine level one interval is 66 MB), so y is written to DRAM once
+/// instead of written, re-read and re-written.
+int
+vmult3_chunk(const Level3Consts &P, int S)
+{
+  const long long bytes = static_cast<long long>(S) * P.mv * sizeof(double);
+  return static_cast<int>(std::max<long long>(1, (64ll << 20) / std::max<long long>(1, bytes)));
+}
+
+template <int R, int S>
+cudaError_t
+launch_rs3(const Level3Consts &P, const double *x, const double *b, double *y, int nI, const double *xprev0,
+           int coupled, int mode, cudaStream_t st)
+{
+  const int chunk = vmult3_chunk(P, S);
+  for (int c0 = 0; c0 < nI; c0 += chunk)
+    {
+      const int nc = std::min(chunk, nI - c0);
+      const long long off = static_cast<long long>(c0) * P.isz;
+      const double *xp = c0 == 0 ? xprev0 : x + off - P.isz + (S - 1) * P.mv;
+      const cudaError_t e =
+        launch_rs3_chunk<R, S>(P, x + off, b ? b + off : nullptr, y + off, nc, xp, coupled, mode, st);
+      if (e != cudaSuccess)
+        return e;
+    }
+  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------- aux
@@ -1934,6 +1964,13 @@ bool
 vmult3_supported(int r, int S)
 {
   return r >= 1 && r <= 2 && S >= 1 && S <= 3;
+}
+
+int
+vmult3_launch_count(const Level3Consts &P, int S, int nI)
+{
+  const int chunk = vmult3_chunk(P, S);
+  return 2 * ((nI + chunk - 1) / chunk);
 }
 
 cudaError_t

@@ -186,6 +186,8 @@ struct DevTransfer3
 cudaError_t launch_vmult3(int r, int S, const Level3Consts &P, const double *x, const double *b, double *y,
                           int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t st);
 bool vmult3_supported(int r, int S);
+/// Kernel launches of one launch_vmult3 (an init and a cell pass per L2-sized interval chunk).
+int vmult3_launch_count(const Level3Consts &P, int S, int nI);
 cudaError_t launch_zero_constrained3(const DevGeom3 &G, double *x, int n_intervals, cudaStream_t st);
 /// p -= (<pmean, p> / vol) on the constant mode, per (interval, slot);
 /// deterministic single-block reductions.

@@ -101,7 +101,7 @@ struct stmg3_level
   vmult(const double *x, const double *b, double *y, int n, const double *xprev, int coupled, int mode)
   {
     check(launch_vmult3(spec.r, spec.S(), consts, x, b, y, n, xprev, coupled, mode, ctx->stream), "vmult3");
-    ctx->count(2);
+    ctx->count(vmult3_launch_count(consts, spec.S(), n));
   }
   void
   project(double *x, int n)
