@@ -319,8 +319,10 @@ int stmg3_level_destroy(stmg3_level *level);
 int stmg3_level_sizes(const stmg3_level *level, int64_t *out);
 /* Vanka patch setup of the level: out[0] seconds, out[1] 1 if the exact
  * per-cell inverses were built on the GPU (deformed levels: element matrices,
- * R_T S R_T^T and batched Gauss-Jordan inverses on the device), out[2] 1 if
- * the undeformed class inverses stand in (affine_patches), out[3] classes. */
+ * R_T S R_T^T and batched Gauss-Jordan inverses on the device), 2 if they were
+ * built there in the time-diagonalised form (DG(2): one real and one
+ * complex-pair block per cell), out[2] 1 if the undeformed class inverses
+ * stand in (affine_patches), out[3] classes. */
 int stmg3_level_patch_info(const stmg3_level *level, double *out);
 /* apply_block / apply_block_raw (st_operator.cpp:397-407) per interval. */
 int stmg3_apply_block(stmg3_level *level, const double *x, double *y, int n_intervals, int raw);

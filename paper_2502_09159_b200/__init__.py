@@ -569,10 +569,12 @@ class Level3:
 
     @property
     def patch_setup(self) -> dict:
-        """Vanka patch setup: seconds, on_gpu (exact per-cell inverses built on the device), affine, classes."""
+        """Vanka patch setup: seconds, on_gpu (exact per-cell inverses built on the device),
+        factored (time-diagonalised blocks), affine, classes."""
         out = (ctypes.c_double * 4)()
         _check(load_library().stmg3_level_patch_info(self._h, out))
-        return dict(seconds=out[0], on_gpu=bool(out[1]), affine=bool(out[2]), classes=int(out[3]))
+        return dict(seconds=out[0], on_gpu=out[1] >= 1, factored=out[1] == 2, affine=bool(out[2]),
+                    classes=int(out[3]))
 
     def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
         _check(load_library().stmg3_apply_block(self._h, self._v(x, n_intervals, "x"), self._v(y, n_intervals, "y"),

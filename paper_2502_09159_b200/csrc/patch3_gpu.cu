@@ -287,6 +287,131 @@ patch3_assemble_kernel(Level3Consts P, int S, const double *__restrict__ E, long
     }
 }
 
+// ---------------------------------------------------------------- factored blocks
+// The time-diagonalised patch blocks (st3d.hpp Fac3Params) of every owned
+// cell: B_b = alpha_b M^ + A^ (real eigenvalue) or the 2 x 2 block form of a
+// complex pair, from the same spatial patch matrices as patch3_assemble:
+// M^ (velocity mass per component), A^ = [[A, -B^T], [B, 0]].
+template <int N>
+__global__ void __launch_bounds__(256)
+patch3_fac_assemble_kernel(Level3Consts P, int S, Fac3Params F, const double *__restrict__ E, long long estride,
+                           double *__restrict__ Aall, const long long *__restrict__ aoff,
+                           const int *__restrict__ cell_nt, long long cell0, int *__restrict__ status)
+{
+  constexpr int NV = N * N * N, p = N - 1;
+  const int np = P.np;
+  __shared__ int loc[NV];
+  __shared__ int s_nl;
+  const int tid = threadIdx.x;
+  const long long oc = blockIdx.x, cell = cell0 + oc;
+  const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
+            cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
+  if (tid == 0)
+    {
+      int nl = 0;
+      for (int t = 0; t < NV; ++t)
+        {
+          const int i = t % N, j = (t / N) % N, k = t / (N * N);
+          const int X = cx * p + i, Y = cy * p + j, Z = cz * p + k;
+          const bool bnd = X == 0 || Y == 0 || Z == P.zlo || X == P.gx - 1 || Y == P.gy - 1 || Z == P.zhi;
+          if (!bnd)
+            loc[nl++] = t;
+        }
+      s_nl = nl;
+    }
+  __syncthreads();
+  const int nl = s_nl, nvs = 3 * nl, ns = nvs + np;
+  if (S * ns != cell_nt[oc])
+    {
+      if (tid == 0)
+        atomicExch(status, 3); // host / device patch layouts disagree
+      return;
+    }
+  for (int b = 0; b < F.nb; ++b)
+    {
+      double *A = Aall + aoff[2 * oc + b];
+      const long long m = static_cast<long long>(F.sz[b]) * ns;
+      for (long long e = tid; e < m * m; e += blockDim.x)
+        A[e] = 0.0;
+    }
+  __syncthreads();
+  const long long cstride = 1, ystride = P.nx, zstride = static_cast<long long>(P.nx) * P.ny;
+  auto range = [&](int x, int &lo, int &hi) {
+    lo = x == 0 ? -1 : 0;
+    hi = x == p ? 1 : 0;
+  };
+  for (int pr = tid; pr < nl * nl; pr += blockDim.x)
+    {
+      const int t = pr / nl, u = pr % nl;
+      const int lt = loc[t], lu = loc[u];
+      const int ti = lt % N, tj = (lt / N) % N, tk = lt / (N * N);
+      const int ui = lu % N, uj = (lu / N) % N, uk = lu / (N * N);
+      int lx0, lx1, ly0, ly1, lz0, lz1, a0, a1;
+      range(ti, lx0, lx1);
+      range(ui, a0, a1);
+      lx0 = max(lx0, a0);
+      lx1 = min(lx1, a1);
+      range(tj, ly0, ly1);
+      range(uj, a0, a1);
+      ly0 = max(ly0, a0);
+      ly1 = min(ly1, a1);
+      range(tk, lz0, lz1);
+      range(uk, a0, a1);
+      lz0 = max(lz0, a0);
+      lz1 = min(lz1, a1);
+      double ms = 0.0, as[3][3] = {};
+      for (int dz = lz0; dz <= lz1; ++dz)
+        for (int dy = ly0; dy <= ly1; ++dy)
+          for (int dx = lx0; dx <= lx1; ++dx)
+            {
+              const long long e = cell + dx * cstride + dy * ystride + dz * zstride;
+              const double *Ee = E + e * estride;
+              const int at = ((tk - dz * p) * N + (tj - dy * p)) * N + (ti - dx * p);
+              const int au = ((uk - dz * p) * N + (uj - dy * p)) * N + (ui - dx * p);
+              ms += Ee[at * NV + au];
+              const double *Ea = Ee + NV * NV;
+              for (int c = 0; c < 3; ++c)
+                for (int c2 = 0; c2 < 3; ++c2)
+                  as[c][c2] += Ea[(static_cast<long long>(c) * NV + at) * 3 * NV + c2 * NV + au];
+            }
+      for (int b = 0; b < F.nb; ++b)
+        {
+          const int sz = F.sz[b];
+          const long long m = static_cast<long long>(sz) * ns;
+          double *A = Aall + aoff[2 * oc + b];
+          for (int bi = 0; bi < sz; ++bi)
+            for (int bj = 0; bj < sz; ++bj)
+              {
+                const double cm = bi == bj ? F.alpha[b] : (bi == 0 ? F.beta[b] : -F.beta[b]);
+                const double ca = bi == bj ? 1.0 : 0.0;
+                for (int c = 0; c < 3; ++c)
+                  for (int c2 = 0; c2 < 3; ++c2)
+                    A[static_cast<long long>(bi * nvs + c * nl + t) * m + bj * nvs + c2 * nl + u] =
+                      ca * as[c][c2] + (c == c2 ? cm * ms : 0.0);
+              }
+        }
+    }
+  // B and -B^T: the patch cell's own B (vanka.cpp:124-140), diagonal blocks only
+  const double *Eb = E + cell * estride + 10 * NV * NV;
+  for (int pr = tid; pr < np * 3 * nl; pr += blockDim.x)
+    {
+      const int l = pr / (3 * nl), c = (pr / nl) % 3, u = pr % nl;
+      const double bv = Eb[static_cast<long long>(l) * 3 * NV + c * NV + loc[u]];
+      for (int b = 0; b < F.nb; ++b)
+        {
+          const int sz = F.sz[b];
+          const long long m = static_cast<long long>(sz) * ns;
+          double *A = Aall + aoff[2 * oc + b];
+          for (int bi = 0; bi < sz; ++bi)
+            {
+              const long long vr = bi * nvs + c * nl + u, pc = sz * nvs + bi * np + l;
+              A[vr * m + pc] = -bv;
+              A[pc * m + vr] = bv;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- batched inverse
 constexpr int kGJB = 32;       // pivot block
 constexpr int kGJThreads = 512; // 16 warps
@@ -467,6 +592,36 @@ launch_patch3_setup(const Level3Consts &P, int r, int S, double *E, double *Aall
   const size_t gsmem = sizeof(double) * (kGJB * kGJDLd + static_cast<size_t>(kGJB) * gj_ldr(max_nt));
   cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem));
   gj_inverse_kernel<<<static_cast<unsigned>(ncells), kGJThreads, gsmem, st>>>(Aall, aoff, ntv, status);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_patch3_fac_setup(const Level3Consts &P, int r, int S, const Fac3Params &F, double *E, double *Aall,
+                        const long long *aoff, const int *ntv, const int *cell_nt, int max_m, long long ncells,
+                        int *status, cudaStream_t st, long long ncells_elem, long long cell0)
+{
+  if (ncells_elem < 0)
+    ncells_elem = ncells;
+  if (F.nb < 1 || F.nb > 2)
+    return cudaErrorInvalidValue; // matrices 2c, 2c + 1 per cell
+  const long long es = elem3_stride(r);
+  const int N = r + 2, nv = N * N * N, nq = nv;
+  const size_t esmem = sizeof(double) * (static_cast<size_t>(nq) * nv * 4 + nq * 10 + static_cast<size_t>(nq) * P.np);
+  auto go = [&](auto elem, auto asm_) {
+    cudaFuncSetAttribute(elem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(esmem));
+    elem<<<static_cast<unsigned>(ncells_elem), 256, esmem, st>>>(P, E, es, status);
+    asm_<<<static_cast<unsigned>(ncells), 256, 0, st>>>(P, S, F, E, es, Aall, aoff, cell_nt, cell0, status);
+  };
+  if (r == 1)
+    go(elem3_kernel<3>, patch3_fac_assemble_kernel<3>);
+  else if (r == 2)
+    go(elem3_kernel<4>, patch3_fac_assemble_kernel<4>);
+  else
+    return cudaErrorInvalidValue;
+  // the 1-block case (nb == 1) leaves matrix 2c + 1 empty (size 0)
+  const size_t gsmem = sizeof(double) * (kGJB * kGJDLd + static_cast<size_t>(kGJB) * gj_ldr(max_m));
+  cudaFuncSetAttribute(gj_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gsmem));
+  gj_inverse_kernel<<<static_cast<unsigned>(2 * ncells), kGJThreads, gsmem, st>>>(Aall, aoff, ntv, status);
   return cudaGetLastError();
 }
 

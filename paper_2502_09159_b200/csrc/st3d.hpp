@@ -138,6 +138,28 @@ long long elem3_stride(int r);
 cudaError_t launch_patch3_setup(const Level3Consts &P, int r, int S, double *E, double *Aall, const long long *aoff,
                                 const int *ntv, int max_nt, long long ncells, int *status, cudaStream_t st,
                                 long long ncells_elem = -1, long long cell0 = 0);
+/// Time-diagonalised cell patches (DG(k) with a Kronecker patch matrix
+/// A_T = K_t (x) M^ + M_t (x) A^): A_T^{-1} = (V (x) I) blockdiag(B_b^{-1})
+/// (W (x) I) with M_t^{-1} K_t = V Lambda V^{-1} in real block form, W =
+/// V^{-1} M_t^{-1} (setup.cpp temporal_eigen), B_b = alpha M^ + A^ for a
+/// real eigenvalue, [[alpha M^ + A^, beta M^], [-beta M^, alpha M^ + A^]]
+/// for a pair. Block rows in "factored order": velocity of each coordinate
+/// of the block, then pressure of each (all velocity first: pivot-free
+/// Gauss-Jordan, the velocity block has a positive definite symmetric part).
+struct Fac3Params
+{
+  int S = 0, nb = 0;
+  int c0[kMaxS] = {}, sz[kMaxS] = {};
+  double alpha[kMaxS] = {}, beta[kMaxS] = {};
+  double V[kMaxS * kMaxS] = {}, W[kMaxS * kMaxS] = {}; // row-major S x S
+};
+/// Element matrices (as launch_patch3_setup) and the factored blocks of
+/// every owned cell patch: matrix 2c + b of Aall (offsets aoff, sizes ntv)
+/// is block b of cell c (nb == 2 for DG(2): a real and a pair block).
+cudaError_t launch_patch3_fac_setup(const Level3Consts &P, int r, int S, const Fac3Params &F, double *E, double *Aall,
+                                    const long long *aoff, const int *ntv, const int *cell_nt, int max_m,
+                                    long long ncells, int *status, cudaStream_t st, long long ncells_elem = -1,
+                                    long long cell0 = 0);
 /// Batched in-place inverse of `count` dense row-major matrices (sizes ntv,
 /// offsets aoff), pivot-free blocked Gauss-Jordan on the FP64 tensor path.
 cudaError_t launch_gj_inverse(double *Aall, const long long *aoff, const int *ntv, int count, int max_nt, int *status,
@@ -183,6 +205,14 @@ struct DevTransfer3
   DevGeom3 f, c;
 };
 
+/// Additive Vanka sweep (one colour) with the time-diagonalised cell
+/// inverses: per block one cell patch x <= 16 intervals; gather R, mix the
+/// slots by W, block-diagonal DMMA with the cell's blocks streamed from HBM,
+/// mix by V, weights, scatter (red.add; a colour's patches share no dof).
+cudaError_t launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, int n_batches, int max_nt,
+                                 const long long *vel_anchor, const long long *pre_anchor, const Fac3Params &F,
+                                 const double *r, double *u, long long isz, int n_intervals, double omega,
+                                 cudaStream_t st);
 cudaError_t launch_vmult3(int r, int S, const Level3Consts &P, const double *x, const double *b, double *y,
                           int n_intervals, const double *xprev0, int coupled, int mode, cudaStream_t st);
 bool vmult3_supported(int r, int S);

@@ -82,7 +82,10 @@ struct stmg3_level
   // exact per-cell patches built on the GPU (deformed levels, patch3_gpu.cu):
   // concatenated dof offsets, weights and inverses
   DevArray<long long> rel_all;
-  DevArray<double> weight_all, inv_all;
+  DevArray<double> weight_all, inv_all, fac_all;
+  // time-diagonalised per-cell blocks (DG(2) deformed levels, vanka_big_fac_kernel)
+  bool fac3 = false;
+  Fac3Params fac3p{};
   bool gpu_patches = false;
   double patch_setup_s = 0.0;
   DevArray<DevPatchClass> classes;
@@ -134,9 +137,14 @@ struct stmg3_level
     for (size_t c = 0; c < colour_first.size(); ++c)
       if (colour_count[c] > 0)
         {
-          check(launch_vanka_colour(classes.p, batches.p + colour_first[c], nullptr, colour_count[c], max_nt,
-                                    vel_anchor.p, pre_anchor.p, r, u, spec.isz(), n, omega, ctx->stream),
-                "vanka3");
+          if (fac3)
+            check(launch_vanka_big_fac(classes.p, batches.p + colour_first[c], colour_count[c], max_nt, vel_anchor.p,
+                                       pre_anchor.p, fac3p, r, u, spec.isz(), n, omega, ctx->stream),
+                  "vanka3_fac");
+          else
+            check(launch_vanka_colour(classes.p, batches.p + colour_first[c], nullptr, colour_count[c], max_nt,
+                                      vel_anchor.p, pre_anchor.p, r, u, spec.isz(), n, omega, ctx->stream),
+                  "vanka3");
           ctx->count();
         }
   }
@@ -239,42 +247,91 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
       const long long nc = s.ncells();
       L.rel_all.upload(lo.rel);
       L.weight_all.upload(lo.weight);
-      L.inv_all.resize(static_cast<size_t>(lo.inv_off.back()));
-      DevArray<long long> aoff;
-      aoff.upload(std::vector<long long>(lo.inv_off.begin(), lo.inv_off.end() - 1));
-      DevArray<int> ntv, st;
-      ntv.upload(lo.nt);
+      DevArray<int> ntv, st, cnt;
       st.upload(std::vector<int>{0});
+      // element matrices: the level itself, or for a split level the owned
+      // cells plus one ghost cell layer across each interface (the patches of
+      // the interface cells sum the neighbour part's cells too: R_T S R_T^T
+      // of the whole mesh)
+      Level3Spec ex = s;
+      const int gl = s.zlo_bc ? 0 : 1, gh = s.zhi_bc ? 0 : 1;
+      ex.nz = s.nz + gl + gh;
+      DevArray<double> vext, E;
+      Level3Consts Pe = L.consts;
       if (s.split())
         {
-          // element matrices of the owned cells plus one ghost cell layer
-          // across each interface: the patches of the interface cells sum
-          // the neighbour part's cells too (R_T S R_T^T of the whole mesh)
-          Level3Spec ex = s;
-          const int gl = s.zlo_bc ? 0 : 1, gh = s.zhi_bc ? 0 : 1;
-          ex.nz = s.nz + gl + gh;
           if (static_cast<long long>(verts_ext->size()) != 3 * ex.nverts())
             throw std::invalid_argument("3D split level: ghost-layer vertex array has the wrong size");
-          DevArray<double> vext, E;
           vext.upload(*verts_ext);
-          const Level3Consts Pe = make_level3_consts(ex, vext.p);
-          E.resize(static_cast<size_t>(ex.ncells()) * elem3_stride(s.r));
-          check(launch_patch3_setup(Pe, s.r, s.S(), E.p, L.inv_all.p, aoff.p, ntv.p, lo.max_nt, nc, st.p,
-                                    L.ctx->stream, ex.ncells(), static_cast<long long>(gl) * s.nx * s.ny),
-                "patch3_setup");
-          L.ctx->count(3);
-          check(cudaStreamSynchronize(L.ctx->stream), "patch3_setup");
+          Pe = make_level3_consts(ex, vext.p);
+        }
+      const long long ncells_elem = ex.ncells(), cell0 = static_cast<long long>(gl) * s.nx * s.ny;
+      E.resize(static_cast<size_t>(ncells_elem) * elem3_stride(s.r));
+      // DG(2) (S = 3): time-diagonalised blocks, one real and one pair block
+      // (0.56x the inverse bytes of the dense patch inverse);
+      // A/B switch STMG_VANKA3_DENSE=1
+      Fac3Params F{};
+      bool fac = s.S() == 3 && !std::getenv("STMG_VANKA3_DENSE");
+      if (fac)
+        {
+          const TemporalEigen eg = temporal_eigen(time_tables(s.k, s.tau));
+          fac = eg.ok && !eg.blk_c0.empty() && eg.blk_c0.size() <= 2;
+          if (fac)
+            {
+              F.S = s.S();
+              F.nb = static_cast<int>(eg.blk_c0.size());
+              for (int b = 0; b < F.nb; ++b)
+                {
+                  F.c0[b] = eg.blk_c0[b];
+                  F.sz[b] = eg.blk_sz[b];
+                  F.alpha[b] = eg.alpha[b];
+                  F.beta[b] = eg.beta[b];
+                  fac = fac && F.alpha[b] > 0.0 && (b == 0 ? F.c0[b] == 0 : F.c0[b] == F.c0[b - 1] + F.sz[b - 1]);
+                }
+              for (int i = 0; i < F.S * F.S; ++i)
+                {
+                  F.V[i] = eg.V[i];
+                  F.W[i] = eg.W[i];
+                }
+            }
+        }
+      std::vector<long long> foff;
+      if (fac)
+        {
+          // matrices 2c, 2c + 1: the blocks of cell c (sizes sz_b * n_s)
+          std::vector<int> msz(2 * nc, 0);
+          foff.assign(2 * nc + 1, 0);
+          int max_m = 0;
+          for (long long c = 0; c < nc; ++c)
+            for (int b = 0; b < 2; ++b)
+              {
+                const int m = b < F.nb ? F.sz[b] * (lo.nt[c] / F.S) : 0;
+                msz[2 * c + b] = m;
+                foff[2 * c + b + 1] = foff[2 * c + b] + static_cast<long long>(m) * m;
+                max_m = std::max(max_m, m);
+              }
+          L.fac_all.resize(static_cast<size_t>(foff.back()));
+          DevArray<long long> aoff;
+          aoff.upload(std::vector<long long>(foff.begin(), foff.end() - 1));
+          ntv.upload(msz);
+          cnt.upload(lo.nt);
+          check(launch_patch3_fac_setup(Pe, s.r, s.S(), F, E.p, L.fac_all.p, aoff.p, ntv.p, cnt.p, max_m, nc, st.p,
+                                        L.ctx->stream, ncells_elem, cell0),
+                "patch3_fac_setup");
         }
       else
         {
-          DevArray<double> E;
-          E.resize(static_cast<size_t>(nc) * elem3_stride(s.r));
-          check(launch_patch3_setup(L.consts, s.r, s.S(), E.p, L.inv_all.p, aoff.p, ntv.p, lo.max_nt, nc, st.p,
-                                    L.ctx->stream),
+          L.inv_all.resize(static_cast<size_t>(lo.inv_off.back()));
+          DevArray<long long> aoff;
+          aoff.upload(std::vector<long long>(lo.inv_off.begin(), lo.inv_off.end() - 1));
+          ntv.upload(lo.nt);
+          check(launch_patch3_setup(Pe, s.r, s.S(), E.p, L.inv_all.p, aoff.p, ntv.p, lo.max_nt, nc, st.p,
+                                    L.ctx->stream, ncells_elem, cell0),
                 "patch3_setup");
-          L.ctx->count(3);
-          check(cudaStreamSynchronize(L.ctx->stream), "patch3_setup");
         }
+      L.ctx->count(3);
+      check(cudaStreamSynchronize(L.ctx->stream), "patch3_setup");
+      E.release();
       int status = 0;
       check(cudaMemcpy(&status, st.p, sizeof(int), cudaMemcpyDeviceToHost), "status");
       if (status == 2)
@@ -288,17 +345,23 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
           for (long long c = 0; c < nc; ++c)
             {
               cell_class[c] = static_cast<int>(c);
-              dc[c] = DevPatchClass{lo.nt[c], lo.nvel[c], L.rel_all.p + lo.rel_off[c], L.weight_all.p + lo.rel_off[c],
-                                    L.inv_all.p + lo.inv_off[c], 0, 0, nullptr};
+              dc[c] = fac ? DevPatchClass{lo.nt[c], lo.nvel[c], L.rel_all.p + lo.rel_off[c],
+                                          L.weight_all.p + lo.rel_off[c], nullptr, lo.nt[c] / F.S,
+                                          lo.nvel[c] / F.S, L.fac_all.p + foff[2 * c]}
+                          : DevPatchClass{lo.nt[c], lo.nvel[c], L.rel_all.p + lo.rel_off[c],
+                                          L.weight_all.p + lo.rel_off[c], L.inv_all.p + lo.inv_off[c], 0, 0, nullptr};
             }
           L.n_classes = static_cast<int>(nc);
           L.max_nt = lo.max_nt;
-          L.total_matrix_elements = lo.total_matrix_elements;
+          L.total_matrix_elements = fac ? static_cast<std::uint64_t>(foff.back()) : lo.total_matrix_elements;
           L.gpu_patches = gpu_done = true;
+          L.fac3 = fac;
+          L.fac3p = F;
         }
       else
         {
           L.inv_all.release();
+          L.fac_all.release();
           L.rel_all.release();
           L.weight_all.release();
         }
@@ -1070,7 +1133,7 @@ stmg3_level_patch_info(const stmg3_level *L, double *out)
     if (!L || !out)
       throw std::invalid_argument("stmg3_level_patch_info: null argument");
     out[0] = L->patch_setup_s;
-    out[1] = L->gpu_patches ? 1.0 : 0.0;
+    out[1] = L->gpu_patches ? (L->fac3 ? 2.0 : 1.0) : 0.0;
     out[2] = L->affine_patches ? 1.0 : 0.0;
     out[3] = static_cast<double>(L->n_classes);
   });

@@ -17,6 +17,7 @@
 //    of u with no atomics, deterministic results.
 #include <cstdlib>
 #include "kernels.hpp"
+#include "st3d.hpp"
 
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -495,6 +496,169 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
       __syncthreads();
     }
 }
+
+// ---------------------------------------------------------------- factored big
+// Time-diagonalised cell patches (st3d.hpp Fac3Params; C5: n_T = 606 as one
+// 202-row block for the real eigenvalue of M_t^{-1} K_t and one 404-row block
+// for the complex pair): 0.56x the inverse bytes and DMMA work of the dense
+// 606 x 606 inverse. One block = one cell patch x <= 16 intervals:
+//   gather R (patch order) -> T = (W (x) I) R in factored order (shared
+//   memory) -> Y_b = B_b^{-1} T_b per block, DMMA with the A-fragments
+//   streamed from HBM through an 8-deep register ring (the blocks are used
+//   once per 16 intervals: the kernel is bound by this stream) -> Z = (V (x) I) Y,
+//   valence weights, red.add (the patches of one colour share no dof).
+constexpr int kFCols = 16, kFLd = 20, kFThreads = 512, kFRing = 8;
+
+__global__ void __launch_bounds__(kFThreads, 1)
+vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
+                     const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
+                     const Fac3Params F, const double *__restrict__ r, double *__restrict__ u, long long isz,
+                     int n_intervals, double omega, int group)
+{
+  extern __shared__ __align__(16) double fsm[];
+  const VankaBatch bt = batches[blockIdx.x];
+  const DevPatchClass pc = classes[bt.cls];
+  const int S = F.S, nt = pc.n_t, nvel = pc.n_vel;
+  const int ns = nt / S, nvs = nvel / S, nps = ns - nvs;
+  const int nrow = (nt + 3) / 4 * 4 + 4; // the last block's k-steps read up to 3 rows past nt
+  double *Rs = fsm;                      // nrow x kFLd: R, later Y
+  double *Ts = Rs + nrow * kFLd;         // nrow x kFLd: T
+  long long *cvb = reinterpret_cast<long long *>(Ts + nrow * kFLd);
+  long long *cpb = cvb + kFCols;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = blockIdx.y * group, ng = min(group, n_intervals - n0);
+  int total_rt = 0;
+  for (int b = 0; b < F.nb; ++b)
+    total_rt += (F.sz[b] * ns + 7) / 8;
+  // patch row (slot a, spatial j) and factored row (coordinate i, spatial j)
+  auto prow = [&](int a, int j) { return j < nvs ? a * nvs + j : S * nvs + a * nps + (j - nvs); };
+  auto frow = [&](int i, int j) {
+    int b = 0;
+    while (b + 1 < F.nb && i >= F.c0[b + 1])
+      ++b;
+    const int bi = i - F.c0[b], o = F.c0[b] * ns;
+    return j < nvs ? o + bi * nvs + j : o + F.sz[b] * nvs + bi * nps + (j - nvs);
+  };
+  for (int pi = 0; pi < bt.count; ++pi)
+    {
+      const int patch = bt.first + pi;
+      if (tid < kFCols)
+        {
+          const int n = n0 + tid;
+          cvb[tid] = tid < ng ? n * isz + __ldg(vel_anchor + patch) : 0;
+          cpb[tid] = tid < ng ? n * isz + __ldg(pre_anchor + patch) : 0;
+        }
+      __syncthreads();
+      // gather: column-major walk (consecutive threads -> consecutive patch rows)
+      for (int e = tid; e < nrow * kFCols; e += kFThreads)
+        {
+          const int c = e / nrow, row = e - c * nrow;
+          double v = 0.0;
+          if (row < nt && c < ng)
+            v = __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + __ldg(pc.rel + row));
+          Rs[row * kFLd + c] = v;
+        }
+      __syncthreads();
+      // T = (W (x) I) R
+      for (int e = tid; e < nrow * kFCols; e += kFThreads)
+        {
+          const int j = e / kFCols, c = e - j * kFCols;
+          if (j < ns)
+            {
+              double rb[kMaxS];
+#pragma unroll
+              for (int b = 0; b < kMaxS; ++b)
+                rb[b] = b < S ? Rs[prow(b, j) * kFLd + c] : 0.0;
+              for (int i = 0; i < S; ++i)
+                {
+                  double t = 0.0;
+#pragma unroll
+                  for (int b = 0; b < kMaxS; ++b)
+                    if (b < S)
+                      t = fma(F.W[i * S + b], rb[b], t);
+                  Ts[frow(i, j) * kFLd + c] = t;
+                }
+            }
+          else if (j >= nt / S && j - ns < nrow - nt)
+            Ts[(nt + (j - ns)) * kFLd + c] = 0.0; // padding rows past nt
+        }
+      __syncthreads();
+      // Y_b = B_b^{-1} T_b: warp w takes the row tiles w, w + 16, ... of all blocks
+      for (int g = warp; g < total_rt; g += kFThreads / 32)
+        {
+          int b = 0, lt = g, aoffb = 0;
+          while (lt >= (F.sz[b] * ns + 7) / 8)
+            {
+              lt -= (F.sz[b] * ns + 7) / 8;
+              aoffb += F.sz[b] * ns * F.sz[b] * ns;
+              ++b;
+            }
+          const int K = F.sz[b] * ns, ks = (K + 3) / 4, boff = F.c0[b] * ns;
+          const int row = 8 * lt + (lane >> 2);
+          const double *Ab = pc.fac_inv + aoffb + static_cast<long long>(row < K ? row : 0) * K;
+          auto load_a = [&](int kk) {
+            const int col = 4 * kk + (lane & 3);
+            return (kk < ks && row < K && col < K) ? __ldg(Ab + col) : 0.0;
+          };
+          double ring[kFRing];
+#pragma unroll
+          for (int q = 0; q < kFRing; ++q)
+            ring[q] = load_a(q);
+          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+          const double *bb = Ts + (boff + (lane & 3)) * kFLd + (lane >> 2);
+          for (int kk0 = 0; kk0 < ks; kk0 += kFRing)
+            {
+#pragma unroll
+              for (int q = 0; q < kFRing; ++q)
+                {
+                  const int kk = kk0 + q;
+                  if (kk < ks)
+                    {
+                      const double *brow = bb + 4 * kk * kFLd;
+                      const double b0 = brow[0], b1 = brow[8];
+                      const double a = ring[q];
+                      ring[q] = load_a(kk + kFRing);
+                      dmma_8x8x4(acc[0], a, b0);
+                      dmma_8x8x4(acc[1], a, b1);
+                    }
+                }
+            }
+          if (row < K)
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                Rs[(boff + row) * kFLd + 8 * ct + 2 * (lane & 3) + h] = acc[ct][h];
+        }
+      __syncthreads();
+      // Z = (V (x) I) Y, weights, scatter
+      for (int e = tid; e < ns * kFCols; e += kFThreads)
+        {
+          const int c = e / ns, j = e - c * ns;
+          if (c >= ng)
+            continue;
+          double y[kMaxS];
+#pragma unroll
+          for (int i = 0; i < kMaxS; ++i)
+            y[i] = i < S ? Rs[frow(i, j) * kFLd + c] : 0.0;
+          for (int a = 0; a < S; ++a)
+            {
+              double z = 0.0;
+#pragma unroll
+              for (int i = 0; i < kMaxS; ++i)
+                if (i < S)
+                  z = fma(F.V[a * S + i], y[i], z);
+              const int row = prow(a, j);
+              const double w = omega * __ldg(pc.weight + row);
+              asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(u + (row < nvel ? cvb[c] : cpb[c]) +
+                                                                   __ldg(pc.rel + row)),
+                           "d"(w * z)
+                           : "memory");
+            }
+        }
+      __syncthreads(); // Rs, Ts and the column bases are reused by the next patch
+    }
+}
 } // namespace
 
 namespace
@@ -528,6 +692,25 @@ device_sm_count()
       cached[dev] = n;
     }
   return cached[dev];
+}
+
+cudaError_t
+launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, int n_batches, int max_nt,
+                     const long long *vel_anchor, const long long *pre_anchor, const Fac3Params &F, const double *r,
+                     double *u, long long isz, int n_intervals, double omega, cudaStream_t st)
+{
+  if (n_batches == 0 || n_intervals == 0)
+    return cudaSuccess;
+  const int nrow = (max_nt + 3) / 4 * 4 + 4;
+  const size_t smem = sizeof(double) * 2 * nrow * kFLd + sizeof(long long) * 2 * kFCols;
+  if (smem > 227 * 1024)
+    return cudaErrorInvalidValue;
+  const int group = kFCols;
+  cudaFuncSetAttribute(vanka_big_fac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  dim3 grid(n_batches, (n_intervals + group - 1) / group);
+  vanka_big_fac_kernel<<<grid, kFThreads, smem, st>>>(classes, batches, vel_anchor, pre_anchor, F, r, u, isz,
+                                                       n_intervals, omega, group);
+  return cudaGetLastError();
 }
 
 /// Launch one colour: `n_batches` batches over `n_intervals` intervals.

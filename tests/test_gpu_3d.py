@@ -341,3 +341,33 @@ def test_gpu_patch_setup_matches_host_and_oracle(stmg, ctx, oracle, nx, ny, nz, 
         outs.append(ug.cpu().numpy())
         assert _rel(outs[-1], ur) <= 1e-10
     assert _rel(outs[0], outs[1]) <= 1e-10
+
+
+@pytest.mark.parametrize("nx,ny,nz,r,n", [(4, 4, 4, 2, 20), (3, 4, 2, 1, 5)])
+def test_time_diagonalised_patches_match_dense(stmg, ctx, nx, ny, nz, r, n):
+    """DG(2) deformed levels apply their exact patch inverses in the
+    time-diagonalised form (one real and one pair block per cell,
+    vanka_big_fac_kernel): the smoother step equals the dense-inverse one
+    (STMG_VANKA3_DENSE) to <= 1e-10, with a ragged 16-interval group."""
+    import os
+
+    verts = o3.vertices(nx, ny, nz, 0.1, seed=23)
+    tau = 1.0 / 8
+    fac = stmg.Level3(ctx, nx, ny, nz, r, 2, tau, 1.0, 1.0, stmg.SMOOTHER_CELL, vertices=verts)
+    assert fac.patch_setup["factored"]
+    os.environ["STMG_VANKA3_DENSE"] = "1"
+    try:
+        den = stmg.Level3(ctx, nx, ny, nz, r, 2, tau, 1.0, 1.0, stmg.SMOOTHER_CELL, vertices=verts)
+    finally:
+        del os.environ["STMG_VANKA3_DENSE"]
+    assert den.patch_setup["on_gpu"] and not den.patch_setup["factored"]
+    rng = np.random.default_rng(24)
+    u = rng.uniform(-1, 1, n * fac.size)
+    b = rng.uniform(-1, 1, n * fac.size)
+    halo = rng.uniform(-1, 1, fac.n_velocity)
+    outs = []
+    for lvl in (fac, den):
+        ug = _cuda(u)
+        lvl.smooth_step(_cuda(b), ug, 0.8, n, _cuda(halo), coupled=True)
+        outs.append(ug.cpu().numpy())
+    assert _rel(outs[0], outs[1]) <= 1e-10
