@@ -385,8 +385,8 @@ patch3_fac_assemble_kernel(Level3Consts P, int S, Fac3Params F, const double *__
                 const double cm = bi == bj ? F.alpha[b] : (bi == 0 ? F.beta[b] : -F.beta[b]);
                 const double ca = bi == bj ? 1.0 : 0.0;
                 for (int c = 0; c < 3; ++c)
-                  for (int c2 = 0; c2 < 3; ++c2)
-                    A[static_cast<long long>(bi * nvs + c * nl + t) * m + bj * nvs + c2 * nl + u] =
+                  for (int c2 = 0; c2 < 3; ++c2) // transposed: (row, col) at col * m + row
+                    A[static_cast<long long>(bj * nvs + c2 * nl + u) * m + bi * nvs + c * nl + t] =
                       ca * as[c][c2] + (c == c2 ? cm * ms : 0.0);
               }
         }
@@ -405,8 +405,8 @@ patch3_fac_assemble_kernel(Level3Consts P, int S, Fac3Params F, const double *__
           for (int bi = 0; bi < sz; ++bi)
             {
               const long long vr = bi * nvs + c * nl + u, pc = sz * nvs + bi * np + l;
-              A[vr * m + pc] = -bv;
-              A[pc * m + vr] = bv;
+              A[pc * m + vr] = -bv; // transposed
+              A[vr * m + pc] = bv;
             }
         }
     }

@@ -307,7 +307,8 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
               {
                 const int m = b < F.nb ? F.sz[b] * (lo.nt[c] / F.S) : 0;
                 msz[2 * c + b] = m;
-                foff[2 * c + b + 1] = foff[2 * c + b] + static_cast<long long>(m) * m;
+                // even (16-byte aligned) starts: the apply kernel bulk-copies chunks
+                foff[2 * c + b + 1] = foff[2 * c + b] + (static_cast<long long>(m) * m + 8 + 1) / 2 * 2;
                 max_m = std::max(max_m, m);
               }
           L.fac_all.resize(static_cast<size_t>(foff.back()));

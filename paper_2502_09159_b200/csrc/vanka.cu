@@ -15,6 +15,7 @@
 //  * Scatter: patches are coloured (2x2 colours for cells, 3x3 for vertex
 //    stars) so that one launch never touches a dof twice: read-modify-write
 //    of u with no atomics, deterministic results.
+#include <algorithm>
 #include <cstdlib>
 #include "kernels.hpp"
 #include "st3d.hpp"
@@ -501,36 +502,52 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 // Time-diagonalised cell patches (st3d.hpp Fac3Params; C5: n_T = 606 as one
 // 202-row block for the real eigenvalue of M_t^{-1} K_t and one 404-row block
 // for the complex pair): 0.56x the inverse bytes and DMMA work of the dense
-// 606 x 606 inverse. One block = one cell patch x <= 16 intervals:
-//   gather R (patch order) -> T = (W (x) I) R in factored order (shared
-//   memory) -> Y_b = B_b^{-1} T_b per block, DMMA with the A-fragments
-//   streamed from HBM through an 8-deep register ring (the blocks are used
-//   once per 16 intervals: the kernel is bound by this stream) -> Z = (V (x) I) Y,
-//   valence weights, red.add (the patches of one colour share no dof).
-constexpr int kFCols = 16, kFLd = 20, kFThreads = 512, kFRing = 8;
+// 606 x 606 inverse. One CTA = one cell patch x <= 16 intervals:
+//   gather R (patch order) -> T = (W (x) I) R in factored order -> per block
+//   b, Y_b = B_b^{-1} T_b on the FP64 tensor path -> Z = (V (x) I) Y, valence
+//   weights, red.add (the patches of one colour share no dof).
+// The blocks are stored column-major (patch3_gpu.cu writes them transposed),
+// so 8 consecutive columns of B_b^{-1} -- two DMMA k-steps for every row tile
+// -- are one contiguous run: the TMA engine streams them (cp.async.bulk, one
+// issuing thread) through a 4-slot shared-memory ring with full / empty
+// mbarriers, while the 16 warps run the DMMAs of the slot in front. Each
+// warp keeps the accumulators of its row tiles (tiles w, w + 16, ... of each
+// block) over the whole stream. The blocks are read once per 16 intervals,
+// so the kernel is bound by this stream (HBM).
+constexpr int kFCols = 16, kFLd = 20, kFThreads = 512, kFSlots = 4, kFChunkCols = 8;
+constexpr int kFMaxM = 896;      // largest block (rows = columns)
+constexpr int kFTiles = 4;       // row tiles per warp and block: 16 * 4 * 8 = 512 rows
+constexpr int kFMaxNt = 3 * 202; // C5 fine level; the host checks
+
+__device__ __forceinline__ unsigned
+f_smem(const void *p)
+{
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
 
 __global__ void __launch_bounds__(kFThreads, 1)
 vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
                      const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
                      const Fac3Params F, const double *__restrict__ r, double *__restrict__ u, long long isz,
-                     int n_intervals, double omega, int group)
+                     int n_intervals, double omega, int group, int max_m)
 {
   extern __shared__ __align__(16) double fsm[];
   const VankaBatch bt = batches[blockIdx.x];
   const DevPatchClass pc = classes[bt.cls];
   const int S = F.S, nt = pc.n_t, nvel = pc.n_vel;
   const int ns = nt / S, nvs = nvel / S, nps = ns - nvs;
-  const int nrow = (nt + 3) / 4 * 4 + 4; // the last block's k-steps read up to 3 rows past nt
-  double *Rs = fsm;                      // nrow x kFLd: R, later Y
-  double *Ts = Rs + nrow * kFLd;         // nrow x kFLd: T
-  long long *cvb = reinterpret_cast<long long *>(Ts + nrow * kFLd);
+  const int nrow = (nt + 3) / 4 * 4 + 4;
+  const int slot_d = kFChunkCols * max_m;             // doubles per ring slot
+  const int big = max(nrow * kFLd, kFSlots * slot_d); // R, then the ring, then Y
+  double *Rs = fsm;
+  double *Ts = fsm + big;                             // nrow x kFLd
+  double *s_w = Ts + nrow * kFLd;                     // nt
+  long long *cvb = reinterpret_cast<long long *>(s_w + nrow);
   long long *cpb = cvb + kFCols;
+  unsigned long long *full = reinterpret_cast<unsigned long long *>(cpb + kFCols), *empty = full + kFSlots;
+  int *s_rel = reinterpret_cast<int *>(empty + kFSlots);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = blockIdx.y * group, ng = min(group, n_intervals - n0);
-  int total_rt = 0;
-  for (int b = 0; b < F.nb; ++b)
-    total_rt += (F.sz[b] * ns + 7) / 8;
-  // patch row (slot a, spatial j) and factored row (coordinate i, spatial j)
   auto prow = [&](int a, int j) { return j < nvs ? a * nvs + j : S * nvs + a * nps + (j - nvs); };
   auto frow = [&](int i, int j) {
     int b = 0;
@@ -538,6 +555,41 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
       ++b;
     const int bi = i - F.c0[b], o = F.c0[b] * ns;
     return j < nvs ? o + bi * nvs + j : o + F.sz[b] * nvs + bi * nps + (j - nvs);
+  };
+  // chunk q of the stream: block b, columns [8 kc, 8 kc + 8)
+  int nch[2] = {0, 0}, moff[2] = {0, 0};
+  for (int b = 0; b < F.nb; ++b)
+    {
+      const int m = F.sz[b] * ns;
+      nch[b] = (m + kFChunkCols - 1) / kFChunkCols;
+      moff[b] = b == 0 ? 0 : moff[b - 1] + (F.sz[b - 1] * ns * F.sz[b - 1] * ns + 8 + 1) / 2 * 2;
+    }
+  const int nchunks = nch[0] + nch[1];
+  if (tid == 0)
+    for (int q = 0; q < kFSlots; ++q)
+      {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(f_smem(full + q)));
+        asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(f_smem(empty + q)), "r"(kFThreads));
+      }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  unsigned base[kFSlots] = {}; // uses of each ring slot by earlier patches of this CTA (mbarrier parity)
+  auto issue = [&](int q, int slot) {
+    const int b = q < nch[0] ? 0 : 1, kc = q < nch[0] ? q : q - nch[0];
+    const int m = F.sz[b] * ns, cols = min(kFChunkCols, m - kFChunkCols * kc);
+    const double *src = pc.fac_inv + moff[b] + static_cast<long long>(kFChunkCols * kc) * m;
+    const unsigned bytes = static_cast<unsigned>((cols * m * sizeof(double) + 15) & ~size_t(15));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(f_smem(full + slot)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   f_smem(Rs + slot * slot_d)),
+                 "l"(src), "r"(bytes), "r"(f_smem(full + slot))
+                 : "memory");
+  };
+  auto wait = [&](unsigned long long *bar, unsigned parity) {
+    asm volatile("{\n .reg .pred p;\n FW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra FW_%=;\n}\n" ::"r"(f_smem(bar)),
+                 "r"(parity)
+                 : "memory");
   };
   for (int pi = 0; pi < bt.count; ++pi)
     {
@@ -548,15 +600,18 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
           cvb[tid] = tid < ng ? n * isz + __ldg(vel_anchor + patch) : 0;
           cpb[tid] = tid < ng ? n * isz + __ldg(pre_anchor + patch) : 0;
         }
+      for (int row = tid; row < nt; row += kFThreads)
+        {
+          s_rel[row] = static_cast<int>(__ldg(pc.rel + row));
+          s_w[row] = omega * __ldg(pc.weight + row);
+        }
       __syncthreads();
-      // gather: column-major walk (consecutive threads -> consecutive patch rows)
+      // gather R: column-major walk (consecutive threads -> consecutive patch rows)
       for (int e = tid; e < nrow * kFCols; e += kFThreads)
         {
           const int c = e / nrow, row = e - c * nrow;
-          double v = 0.0;
-          if (row < nt && c < ng)
-            v = __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + __ldg(pc.rel + row));
-          Rs[row * kFLd + c] = v;
+          const bool ok = row < nt && c < ng;
+          Rs[row * kFLd + c] = ok ? __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]) : 0.0;
         }
       __syncthreads();
       // T = (W (x) I) R
@@ -579,57 +634,85 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
                   Ts[frow(i, j) * kFLd + c] = t;
                 }
             }
-          else if (j >= nt / S && j - ns < nrow - nt)
+          else if (j - ns < nrow - nt)
             Ts[(nt + (j - ns)) * kFLd + c] = 0.0; // padding rows past nt
         }
-      __syncthreads();
-      // Y_b = B_b^{-1} T_b: warp w takes the row tiles w, w + 16, ... of all blocks
-      for (int g = warp; g < total_rt; g += kFThreads / 32)
+      __syncthreads(); // R is dead: its space becomes the chunk ring
+      if (tid == 0)
+        for (int q = 0; q < kFSlots && q < nchunks; ++q)
+          issue(q, q);
+      double acc[2][kFTiles][2][2];
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int t = 0; t < kFTiles; ++t)
+          acc[b][t][0][0] = acc[b][t][0][1] = acc[b][t][1][0] = acc[b][t][1][1] = 0.0;
+      for (int q = 0; q < nchunks; ++q)
         {
-          int b = 0, lt = g, aoffb = 0;
-          while (lt >= (F.sz[b] * ns + 7) / 8)
-            {
-              lt -= (F.sz[b] * ns + 7) / 8;
-              aoffb += F.sz[b] * ns * F.sz[b] * ns;
-              ++b;
-            }
-          const int K = F.sz[b] * ns, ks = (K + 3) / 4, boff = F.c0[b] * ns;
-          const int row = 8 * lt + (lane >> 2);
-          const double *Ab = pc.fac_inv + aoffb + static_cast<long long>(row < K ? row : 0) * K;
-          auto load_a = [&](int kk) {
-            const int col = 4 * kk + (lane & 3);
-            return (kk < ks && row < K && col < K) ? __ldg(Ab + col) : 0.0;
-          };
-          double ring[kFRing];
+          const int slot = q % kFSlots;
+          const unsigned use = base[slot] + static_cast<unsigned>(q / kFSlots);
+          wait(full + slot, use & 1);
+          const int b = q < nch[0] ? 0 : 1, kc = q < nch[0] ? q : q - nch[0];
+          const int m = F.sz[b] * ns, boff = F.c0[b] * ns;
+          const double *A = Rs + slot * slot_d; // column j of B_b^{-1} (chunk-local) at j * m
 #pragma unroll
-          for (int q = 0; q < kFRing; ++q)
-            ring[q] = load_a(q);
-          double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-          const double *bb = Ts + (boff + (lane & 3)) * kFLd + (lane >> 2);
-          for (int kk0 = 0; kk0 < ks; kk0 += kFRing)
+          for (int kk = 0; kk < kFChunkCols / 4; ++kk)
             {
+              const int kr = kFChunkCols * kc + 4 * kk + (lane & 3); // column of B^{-1} = row of T_b
+              if (kFChunkCols * kc + 4 * kk >= m)
+                break;
+              const double *brow = Ts + (boff + kr) * kFLd + (lane >> 2);
+              const double b0 = brow[0], b1 = brow[8];
+              const int jl = 4 * kk + (lane & 3);
 #pragma unroll
-              for (int q = 0; q < kFRing; ++q)
+              for (int t = 0; t < kFTiles; ++t)
                 {
-                  const int kk = kk0 + q;
-                  if (kk < ks)
+                  const int row = 8 * (warp + 16 * t) + (lane >> 2);
+                  if (8 * (warp + 16 * t) < m)
                     {
-                      const double *brow = bb + 4 * kk * kFLd;
-                      const double b0 = brow[0], b1 = brow[8];
-                      const double a = ring[q];
-                      ring[q] = load_a(kk + kFRing);
-                      dmma_8x8x4(acc[0], a, b0);
-                      dmma_8x8x4(acc[1], a, b1);
+                      const double a = (row < m && kr < m) ? A[jl * m + row] : 0.0;
+                      if (b == 0)
+                        {
+                          dmma_8x8x4(acc[0][t][0], a, b0);
+                          dmma_8x8x4(acc[0][t][1], a, b1);
+                        }
+                      else
+                        {
+                          dmma_8x8x4(acc[1][t][0], a, b0);
+                          dmma_8x8x4(acc[1][t][1], a, b1);
+                        }
                     }
                 }
             }
-          if (row < K)
-#pragma unroll
-            for (int ct = 0; ct < 2; ++ct)
-#pragma unroll
-              for (int h = 0; h < 2; ++h)
-                Rs[(boff + row) * kFLd + 8 * ct + 2 * (lane & 3) + h] = acc[ct][h];
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(f_smem(empty + slot)) : "memory");
+          if (tid == 0 && q + kFSlots < nchunks)
+            {
+              wait(empty + slot, use & 1);
+              issue(q + kFSlots, slot);
+            }
         }
+#pragma unroll
+      for (int sl = 0; sl < kFSlots; ++sl)
+        base[sl] += nchunks > sl ? static_cast<unsigned>((nchunks - 1 - sl) / kFSlots + 1) : 0u;
+      __syncthreads(); // every chunk was consumed (no copy in flight): Y may overwrite the ring
+      // Y (factored order) into the ring space
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+        if (b < F.nb)
+          {
+            const int m = F.sz[b] * ns, boff = F.c0[b] * ns;
+#pragma unroll
+            for (int t = 0; t < kFTiles; ++t)
+              {
+                const int row = 8 * (warp + 16 * t) + (lane >> 2);
+                if (row < m)
+#pragma unroll
+                  for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                      Rs[(boff + row) * kFLd + 8 * ct + 2 * (lane & 3) + h] = acc[b][t][ct][h];
+              }
+          }
       __syncthreads();
       // Z = (V (x) I) Y, weights, scatter
       for (int e = tid; e < ns * kFCols; e += kFThreads)
@@ -649,14 +732,12 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
                 if (i < S)
                   z = fma(F.V[a * S + i], y[i], z);
               const int row = prow(a, j);
-              const double w = omega * __ldg(pc.weight + row);
-              asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(u + (row < nvel ? cvb[c] : cpb[c]) +
-                                                                   __ldg(pc.rel + row)),
-                           "d"(w * z)
+              asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(u + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]),
+                           "d"(s_w[row] * z)
                            : "memory");
             }
         }
-      __syncthreads(); // Rs, Ts and the column bases are reused by the next patch
+      __syncthreads(); // Rs, Ts and the column data are reused by the next patch
     }
 }
 } // namespace
@@ -702,14 +783,21 @@ launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, in
   if (n_batches == 0 || n_intervals == 0)
     return cudaSuccess;
   const int nrow = (max_nt + 3) / 4 * 4 + 4;
-  const size_t smem = sizeof(double) * 2 * nrow * kFLd + sizeof(long long) * 2 * kFCols;
+  int max_m = 0;
+  for (int b = 0; b < F.nb; ++b)
+    max_m = std::max(max_m, F.sz[b] * (max_nt / F.S));
+  if (F.nb > 2 || max_m > 16 * kFTiles * 8)
+    return cudaErrorInvalidValue; // the host keeps the dense inverses then
+  const size_t big = std::max<size_t>(static_cast<size_t>(nrow) * kFLd, static_cast<size_t>(kFSlots) * kFChunkCols * max_m);
+  const size_t smem = sizeof(double) * (big + static_cast<size_t>(nrow) * kFLd + nrow) + sizeof(long long) * 2 * kFCols +
+                      sizeof(unsigned long long) * 2 * kFSlots + sizeof(int) * nrow;
   if (smem > 227 * 1024)
     return cudaErrorInvalidValue;
   const int group = kFCols;
   cudaFuncSetAttribute(vanka_big_fac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   dim3 grid(n_batches, (n_intervals + group - 1) / group);
   vanka_big_fac_kernel<<<grid, kFThreads, smem, st>>>(classes, batches, vel_anchor, pre_anchor, F, r, u, isz,
-                                                       n_intervals, omega, group);
+                                                       n_intervals, omega, group, max_m);
   return cudaGetLastError();
 }
 
