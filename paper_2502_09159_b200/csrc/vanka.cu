@@ -514,10 +514,11 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 // warp keeps the accumulators of its row tiles (tiles w, w + 16, ... of each
 // block) over the whole stream. The blocks are read once per 16 intervals,
 // so the kernel is bound by this stream (HBM).
+#ifndef STMG_FAC_L2AHEAD
+#define STMG_FAC_L2AHEAD 0 // >0: L2 prefetch of the chunk this far ahead (measured: no gain)
+#endif
 constexpr int kFCols = 16, kFLd = 20, kFThreads = 512, kFSlots = 4, kFChunkCols = 8;
-constexpr int kFMaxM = 896;      // largest block (rows = columns)
 constexpr int kFTiles = 4;       // row tiles per warp and block: 16 * 4 * 8 = 512 rows
-constexpr int kFMaxNt = 3 * 202; // C5 fine level; the host checks
 
 __device__ __forceinline__ unsigned
 f_smem(const void *p)
@@ -525,46 +526,98 @@ f_smem(const void *p)
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
+// One chunk (8 columns of B_b^{-1} = 2 DMMA k-steps) for the NT row tiles a
+// warp owns in block b: all A fragments of a k-step are loaded before its
+// DMMAs (no per-tile branch: NT is uniform per warp and block).
+template <int NT>
+__device__ __forceinline__ void
+fac_chunk(double (&acc)[kFTiles][2][2], const double *__restrict__ A, const double *__restrict__ Ts, int m, int boff,
+          int kc, int warp, int lane)
+{
+#pragma unroll
+  for (int kk = 0; kk < kFChunkCols / 4; ++kk)
+    {
+      if (kFChunkCols * kc + 4 * kk >= m)
+        break;
+      const int kr = kFChunkCols * kc + 4 * kk + (lane & 3); // column of B^{-1} = row of T_b
+      const double *brow = Ts + (boff + kr) * kFLd + (lane >> 2);
+      const double b0 = brow[0], b1 = brow[8];
+      const int jl = 4 * kk + (lane & 3);
+      double a[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        {
+          const int row = 8 * (warp + 16 * t) + (lane >> 2);
+          a[t] = (row < m && kr < m) ? A[jl * m + row] : 0.0;
+        }
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        {
+          dmma_8x8x4(acc[t][0], a[t], b0);
+          dmma_8x8x4(acc[t][1], a[t], b1);
+        }
+    }
+}
+
+__device__ __forceinline__ void
+fac_chunk_n(int nt_w, double (&acc)[kFTiles][2][2], const double *A, const double *Ts, int m, int boff, int kc,
+            int warp, int lane)
+{
+  switch (nt_w)
+    {
+      case 1: fac_chunk<1>(acc, A, Ts, m, boff, kc, warp, lane); break;
+      case 2: fac_chunk<2>(acc, A, Ts, m, boff, kc, warp, lane); break;
+      case 3: fac_chunk<3>(acc, A, Ts, m, boff, kc, warp, lane); break;
+      case 4: fac_chunk<4>(acc, A, Ts, m, boff, kc, warp, lane); break;
+      default: break;
+    }
+}
+
+// Per-patch constants of the stream (the blocks of one cell patch).
+struct FacItem
+{
+  const double *inv; // column-major blocks, block 1 at inv + moff1
+  int nt, nvel, ns, nch0, nch1, moff1;
+};
+
+__device__ __forceinline__ FacItem
+fac_item(const DevPatchClass &pc, const Fac3Params &F)
+{
+  FacItem it;
+  it.inv = pc.fac_inv;
+  it.nt = pc.n_t;
+  it.nvel = pc.n_vel;
+  it.ns = pc.n_t / F.S;
+  const int m0 = F.sz[0] * it.ns, m1 = F.nb > 1 ? F.sz[1] * it.ns : 0;
+  it.nch0 = (m0 + kFChunkCols - 1) / kFChunkCols;
+  it.nch1 = (m1 + kFChunkCols - 1) / kFChunkCols;
+  it.moff1 = (m0 * m0 + 8 + 1) / 2 * 2;
+  return it;
+}
+
+// Persistent: CTA x walks the batches x, x + gridDim.x, ... of the colour.
+// The chunks of all its patches form ONE stream through the ring, so the
+// TMA engine already pulls the next patch's first chunks while the warps
+// write Y, scatter and gather the next patch.
 __global__ void __launch_bounds__(kFThreads, 1)
 vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
-                     const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
+                     int n_batches, const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
                      const Fac3Params F, const double *__restrict__ r, double *__restrict__ u, long long isz,
-                     int n_intervals, double omega, int group, int max_m)
+                     int n_intervals, double omega, int group, int max_m, int max_nt)
 {
   extern __shared__ __align__(16) double fsm[];
-  const VankaBatch bt = batches[blockIdx.x];
-  const DevPatchClass pc = classes[bt.cls];
-  const int S = F.S, nt = pc.n_t, nvel = pc.n_vel;
-  const int ns = nt / S, nvs = nvel / S, nps = ns - nvs;
-  const int nrow = (nt + 3) / 4 * 4 + 4;
-  const int slot_d = kFChunkCols * max_m;             // doubles per ring slot
-  const int big = max(nrow * kFLd, kFSlots * slot_d); // R, then the ring, then Y
-  double *Rs = fsm;
-  double *Ts = fsm + big;                             // nrow x kFLd
-  double *s_w = Ts + nrow * kFLd;                     // nt
-  long long *cvb = reinterpret_cast<long long *>(s_w + nrow);
+  const int S = F.S;
+  const int nrow_max = (max_nt + 3) / 4 * 4 + 4;
+  const int slot_d = kFChunkCols * max_m; // doubles per ring slot
+  double *Rs = fsm;                       // the chunk ring
+  double *Ts = fsm + kFSlots * slot_d;    // nrow x kFLd: T, later Y
+  double *s_w = Ts + nrow_max * kFLd;     // nt
+  long long *cvb = reinterpret_cast<long long *>(s_w + nrow_max);
   long long *cpb = cvb + kFCols;
   unsigned long long *full = reinterpret_cast<unsigned long long *>(cpb + kFCols), *empty = full + kFSlots;
   int *s_rel = reinterpret_cast<int *>(empty + kFSlots);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n0 = blockIdx.y * group, ng = min(group, n_intervals - n0);
-  auto prow = [&](int a, int j) { return j < nvs ? a * nvs + j : S * nvs + a * nps + (j - nvs); };
-  auto frow = [&](int i, int j) {
-    int b = 0;
-    while (b + 1 < F.nb && i >= F.c0[b + 1])
-      ++b;
-    const int bi = i - F.c0[b], o = F.c0[b] * ns;
-    return j < nvs ? o + bi * nvs + j : o + F.sz[b] * nvs + bi * nps + (j - nvs);
-  };
-  // chunk q of the stream: block b, columns [8 kc, 8 kc + 8)
-  int nch[2] = {0, 0}, moff[2] = {0, 0};
-  for (int b = 0; b < F.nb; ++b)
-    {
-      const int m = F.sz[b] * ns;
-      nch[b] = (m + kFChunkCols - 1) / kFChunkCols;
-      moff[b] = b == 0 ? 0 : moff[b - 1] + (F.sz[b - 1] * ns * F.sz[b - 1] * ns + 8 + 1) / 2 * 2;
-    }
-  const int nchunks = nch[0] + nch[1];
   if (tid == 0)
     for (int q = 0; q < kFSlots; ++q)
       {
@@ -572,11 +625,30 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
         asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(f_smem(empty + q)), "r"(kFThreads));
       }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  unsigned base[kFSlots] = {}; // uses of each ring slot by earlier patches of this CTA (mbarrier parity)
-  auto issue = [&](int q, int slot) {
-    const int b = q < nch[0] ? 0 : 1, kc = q < nch[0] ? q : q - nch[0];
-    const int m = F.sz[b] * ns, cols = min(kFChunkCols, m - kFChunkCols * kc);
-    const double *src = pc.fac_inv + moff[b] + static_cast<long long>(kFChunkCols * kc) * m;
+  __syncthreads();
+  auto wait = [&](unsigned long long *bar, unsigned parity) {
+    asm volatile("{\n .reg .pred p;\n FW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra FW_%=;\n}\n" ::"r"(f_smem(bar)),
+                 "r"(parity)
+                 : "memory");
+  };
+  // ---- producer (thread 0): cursor over (batch, patch, chunk) of this CTA
+  int p_bi = blockIdx.x, p_pi = 0, p_q = 0;
+  unsigned p_g = 0; // chunks issued
+  FacItem p_it{};
+  bool p_has = p_bi < n_batches;
+  if (tid == 0 && p_has)
+    p_it = fac_item(classes[batches[p_bi].cls], F);
+  auto issue_next = [&]() {
+    if (!p_has)
+      return;
+    const int slot = p_g % kFSlots;
+    if (p_g >= kFSlots)
+      wait(empty + slot, ((p_g / kFSlots) - 1) & 1); // the consumers released the slot's previous chunk
+    const bool b1 = p_q >= p_it.nch0;
+    const int kc = b1 ? p_q - p_it.nch0 : p_q;
+    const int m = F.sz[b1 ? 1 : 0] * p_it.ns, cols = min(kFChunkCols, m - kFChunkCols * kc);
+    const double *src = p_it.inv + (b1 ? p_it.moff1 : 0) + static_cast<long long>(kFChunkCols * kc) * m;
     const unsigned bytes = static_cast<unsigned>((cols * m * sizeof(double) + 15) & ~size_t(15));
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(f_smem(full + slot)), "r"(bytes)
                  : "memory");
@@ -584,160 +656,169 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
                    f_smem(Rs + slot * slot_d)),
                  "l"(src), "r"(bytes), "r"(f_smem(full + slot))
                  : "memory");
-  };
-  auto wait = [&](unsigned long long *bar, unsigned parity) {
-    asm volatile("{\n .reg .pred p;\n FW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-                 " @!p bra FW_%=;\n}\n" ::"r"(f_smem(bar)),
-                 "r"(parity)
-                 : "memory");
-  };
-  for (int pi = 0; pi < bt.count; ++pi)
+#if STMG_FAC_L2AHEAD > 0
     {
-      const int patch = bt.first + pi;
-      if (tid < kFCols)
+      // the ring holds kFSlots chunks; the chunk STMG_FAC_L2AHEAD further is
+      // pulled into L2 now, so its bulk copy later hits L2
+      const int qa = p_q + STMG_FAC_L2AHEAD;
+      if (qa < p_it.nch0 + p_it.nch1)
         {
-          const int n = n0 + tid;
-          cvb[tid] = tid < ng ? n * isz + __ldg(vel_anchor + patch) : 0;
-          cpb[tid] = tid < ng ? n * isz + __ldg(pre_anchor + patch) : 0;
+          const bool ba = qa >= p_it.nch0;
+          const int kca = ba ? qa - p_it.nch0 : qa;
+          const int ma = F.sz[ba ? 1 : 0] * p_it.ns, colsa = min(kFChunkCols, ma - kFChunkCols * kca);
+          const double *pa = p_it.inv + (ba ? p_it.moff1 : 0) + static_cast<long long>(kFChunkCols * kca) * ma;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(pa),
+                       "r"(static_cast<unsigned>((colsa * ma * sizeof(double)) & ~size_t(15)))
+                       : "memory");
         }
-      for (int row = tid; row < nt; row += kFThreads)
+    }
+#endif
+    ++p_g;
+    if (++p_q == p_it.nch0 + p_it.nch1)
+      {
+        p_q = 0;
+        if (++p_pi == batches[p_bi].count)
+          {
+            p_pi = 0;
+            p_bi += gridDim.x;
+            p_has = p_bi < n_batches;
+          }
+        if (p_has)
+          p_it = fac_item(classes[batches[p_bi].cls], F);
+      }
+  };
+  if (tid == 0)
+    for (int q = 0; q < kFSlots; ++q)
+      issue_next();
+
+  unsigned g = 0; // chunks consumed
+  for (int bi = blockIdx.x; bi < n_batches; bi += gridDim.x)
+    {
+      const VankaBatch bt = batches[bi];
+      const DevPatchClass pc = classes[bt.cls];
+      const FacItem it = fac_item(pc, F);
+      const int nt = it.nt, nvel = it.nvel, ns = it.ns, nvs = nvel / S, nps = ns - nvs;
+      const int nrow = (nt + 3) / 4 * 4 + 4;
+      auto prow = [&](int a, int j) { return j < nvs ? a * nvs + j : S * nvs + a * nps + (j - nvs); };
+      auto frow = [&](int i, int j) {
+        int b = 0;
+        while (b + 1 < F.nb && i >= F.c0[b + 1])
+          ++b;
+        const int bi2 = i - F.c0[b], o = F.c0[b] * ns;
+        return j < nvs ? o + bi2 * nvs + j : o + F.sz[b] * nvs + bi2 * nps + (j - nvs);
+      };
+      const int nchunks = it.nch0 + it.nch1;
+      for (int pi = 0; pi < bt.count; ++pi)
         {
-          s_rel[row] = static_cast<int>(__ldg(pc.rel + row));
-          s_w[row] = omega * __ldg(pc.weight + row);
-        }
-      __syncthreads();
-      // gather R: column-major walk (consecutive threads -> consecutive patch rows)
-      for (int e = tid; e < nrow * kFCols; e += kFThreads)
-        {
-          const int c = e / nrow, row = e - c * nrow;
-          const bool ok = row < nt && c < ng;
-          Rs[row * kFLd + c] = ok ? __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]) : 0.0;
-        }
-      __syncthreads();
-      // T = (W (x) I) R
-      for (int e = tid; e < nrow * kFCols; e += kFThreads)
-        {
-          const int j = e / kFCols, c = e - j * kFCols;
-          if (j < ns)
+          const int patch = bt.first + pi;
+          if (tid < kFCols)
             {
-              double rb[kMaxS];
-#pragma unroll
-              for (int b = 0; b < kMaxS; ++b)
-                rb[b] = b < S ? Rs[prow(b, j) * kFLd + c] : 0.0;
-              for (int i = 0; i < S; ++i)
+              const int n = n0 + tid;
+              cvb[tid] = tid < ng ? n * isz + __ldg(vel_anchor + patch) : 0;
+              cpb[tid] = tid < ng ? n * isz + __ldg(pre_anchor + patch) : 0;
+            }
+          for (int row = tid; row < nt; row += kFThreads)
+            {
+              s_rel[row] = static_cast<int>(__ldg(pc.rel + row));
+              s_w[row] = omega * __ldg(pc.weight + row);
+            }
+          __syncthreads();
+          // T = (W (x) I) R straight from the gather: thread (j, c) loads the S
+          // slot values of spatial dof j in interval column c
+          for (int e = tid; e < nrow * kFCols; e += kFThreads)
+            {
+              const int c = e / nrow, j = e - c * nrow; // consecutive threads: consecutive dofs of a column
+              if (j < ns)
                 {
-                  double t = 0.0;
+                  double rb[kMaxS];
 #pragma unroll
                   for (int b = 0; b < kMaxS; ++b)
-                    if (b < S)
-                      t = fma(F.W[i * S + b], rb[b], t);
-                  Ts[frow(i, j) * kFLd + c] = t;
-                }
-            }
-          else if (j - ns < nrow - nt)
-            Ts[(nt + (j - ns)) * kFLd + c] = 0.0; // padding rows past nt
-        }
-      __syncthreads(); // R is dead: its space becomes the chunk ring
-      if (tid == 0)
-        for (int q = 0; q < kFSlots && q < nchunks; ++q)
-          issue(q, q);
-      double acc[2][kFTiles][2][2];
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
-#pragma unroll
-        for (int t = 0; t < kFTiles; ++t)
-          acc[b][t][0][0] = acc[b][t][0][1] = acc[b][t][1][0] = acc[b][t][1][1] = 0.0;
-      for (int q = 0; q < nchunks; ++q)
-        {
-          const int slot = q % kFSlots;
-          const unsigned use = base[slot] + static_cast<unsigned>(q / kFSlots);
-          wait(full + slot, use & 1);
-          const int b = q < nch[0] ? 0 : 1, kc = q < nch[0] ? q : q - nch[0];
-          const int m = F.sz[b] * ns, boff = F.c0[b] * ns;
-          const double *A = Rs + slot * slot_d; // column j of B_b^{-1} (chunk-local) at j * m
-#pragma unroll
-          for (int kk = 0; kk < kFChunkCols / 4; ++kk)
-            {
-              const int kr = kFChunkCols * kc + 4 * kk + (lane & 3); // column of B^{-1} = row of T_b
-              if (kFChunkCols * kc + 4 * kk >= m)
-                break;
-              const double *brow = Ts + (boff + kr) * kFLd + (lane >> 2);
-              const double b0 = brow[0], b1 = brow[8];
-              const int jl = 4 * kk + (lane & 3);
-#pragma unroll
-              for (int t = 0; t < kFTiles; ++t)
-                {
-                  const int row = 8 * (warp + 16 * t) + (lane >> 2);
-                  if (8 * (warp + 16 * t) < m)
                     {
-                      const double a = (row < m && kr < m) ? A[jl * m + row] : 0.0;
-                      if (b == 0)
-                        {
-                          dmma_8x8x4(acc[0][t][0], a, b0);
-                          dmma_8x8x4(acc[0][t][1], a, b1);
-                        }
-                      else
-                        {
-                          dmma_8x8x4(acc[1][t][0], a, b0);
-                          dmma_8x8x4(acc[1][t][1], a, b1);
-                        }
+                      const int row = b < S ? prow(b, j) : 0;
+                      rb[b] = (b < S && c < ng) ? __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]) : 0.0;
+                    }
+                  for (int i = 0; i < S; ++i)
+                    {
+                      double t = 0.0;
+#pragma unroll
+                      for (int b = 0; b < kMaxS; ++b)
+                        if (b < S)
+                          t = fma(F.W[i * S + b], rb[b], t);
+                      Ts[frow(i, j) * kFLd + c] = t;
                     }
                 }
+              else if (j - ns < nrow - nt)
+                Ts[(nt + (j - ns)) * kFLd + c] = 0.0; // padding rows past nt
             }
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(f_smem(empty + slot)) : "memory");
-          if (tid == 0 && q + kFSlots < nchunks)
-            {
-              wait(empty + slot, use & 1);
-              issue(q + kFSlots, slot);
-            }
-        }
+          __syncthreads();
+          double acc[2][kFTiles][2][2];
 #pragma unroll
-      for (int sl = 0; sl < kFSlots; ++sl)
-        base[sl] += nchunks > sl ? static_cast<unsigned>((nchunks - 1 - sl) / kFSlots + 1) : 0u;
-      __syncthreads(); // every chunk was consumed (no copy in flight): Y may overwrite the ring
-      // Y (factored order) into the ring space
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
-        if (b < F.nb)
-          {
-            const int m = F.sz[b] * ns, boff = F.c0[b] * ns;
+          for (int b = 0; b < 2; ++b)
 #pragma unroll
             for (int t = 0; t < kFTiles; ++t)
-              {
-                const int row = 8 * (warp + 16 * t) + (lane >> 2);
-                if (row < m)
-#pragma unroll
-                  for (int ct = 0; ct < 2; ++ct)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                      Rs[(boff + row) * kFLd + 8 * ct + 2 * (lane & 3) + h] = acc[b][t][ct][h];
-              }
-          }
-      __syncthreads();
-      // Z = (V (x) I) Y, weights, scatter
-      for (int e = tid; e < ns * kFCols; e += kFThreads)
-        {
-          const int c = e / ns, j = e - c * ns;
-          if (c >= ng)
-            continue;
-          double y[kMaxS];
-#pragma unroll
-          for (int i = 0; i < kMaxS; ++i)
-            y[i] = i < S ? Rs[frow(i, j) * kFLd + c] : 0.0;
-          for (int a = 0; a < S; ++a)
+              acc[b][t][0][0] = acc[b][t][0][1] = acc[b][t][1][0] = acc[b][t][1][1] = 0.0;
+          for (int q = 0; q < nchunks; ++q, ++g)
             {
-              double z = 0.0;
+              const int slot = g % kFSlots;
+              wait(full + slot, (g / kFSlots) & 1);
+              const int b = q < it.nch0 ? 0 : 1, kc = q < it.nch0 ? q : q - it.nch0;
+              const int m = F.sz[b] * ns, boff = F.c0[b] * ns, rt = (m + 7) / 8;
+              const int nt_w = warp < rt ? (rt - warp + 15) / 16 : 0; // row tiles of this warp in block b
+              const double *A = Rs + slot * slot_d; // column j of B_b^{-1} (chunk-local) at j * m
+              if (b == 0)
+                fac_chunk_n(nt_w, acc[0], A, Ts, m, boff, kc, warp, lane);
+              else
+                fac_chunk_n(nt_w, acc[1], A, Ts, m, boff, kc, warp, lane);
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(f_smem(empty + slot)) : "memory");
+              if (tid == 0)
+                issue_next(); // refills this slot -- possibly with the next patch's first chunks
+            }
+          __syncthreads(); // every warp is done with T
+          // Y (factored order) into the T space
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            if (b < F.nb)
+              {
+                const int m = F.sz[b] * ns, boff = F.c0[b] * ns;
+#pragma unroll
+                for (int t = 0; t < kFTiles; ++t)
+                  {
+                    const int row = 8 * (warp + 16 * t) + (lane >> 2);
+                    if (row < m)
+#pragma unroll
+                      for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                          Ts[(boff + row) * kFLd + 8 * ct + 2 * (lane & 3) + h] = acc[b][t][ct][h];
+                  }
+              }
+          __syncthreads();
+          // Z = (V (x) I) Y, weights, scatter
+          for (int e = tid; e < ns * kFCols; e += kFThreads)
+            {
+              const int c = e / ns, j = e - c * ns;
+              if (c >= ng)
+                continue;
+              double y[kMaxS];
 #pragma unroll
               for (int i = 0; i < kMaxS; ++i)
-                if (i < S)
-                  z = fma(F.V[a * S + i], y[i], z);
-              const int row = prow(a, j);
-              asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(u + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]),
-                           "d"(s_w[row] * z)
-                           : "memory");
+                y[i] = i < S ? Ts[frow(i, j) * kFLd + c] : 0.0;
+              for (int a = 0; a < S; ++a)
+                {
+                  double z = 0.0;
+#pragma unroll
+                  for (int i = 0; i < kMaxS; ++i)
+                    if (i < S)
+                      z = fma(F.V[a * S + i], y[i], z);
+                  const int row = prow(a, j);
+                  asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(u + (row < nvel ? cvb[c] : cpb[c]) +
+                                                                       s_rel[row]),
+                               "d"(s_w[row] * z)
+                               : "memory");
+                }
             }
+          __syncthreads(); // Ts and the column data are reused by the next patch
         }
-      __syncthreads(); // Rs, Ts and the column data are reused by the next patch
     }
 }
 } // namespace
@@ -788,16 +869,19 @@ launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, in
     max_m = std::max(max_m, F.sz[b] * (max_nt / F.S));
   if (F.nb > 2 || max_m > 16 * kFTiles * 8)
     return cudaErrorInvalidValue; // the host keeps the dense inverses then
-  const size_t big = std::max<size_t>(static_cast<size_t>(nrow) * kFLd, static_cast<size_t>(kFSlots) * kFChunkCols * max_m);
+  const size_t big = static_cast<size_t>(kFSlots) * kFChunkCols * max_m;
   const size_t smem = sizeof(double) * (big + static_cast<size_t>(nrow) * kFLd + nrow) + sizeof(long long) * 2 * kFCols +
                       sizeof(unsigned long long) * 2 * kFSlots + sizeof(int) * nrow;
   if (smem > 227 * 1024)
     return cudaErrorInvalidValue;
   const int group = kFCols;
   cudaFuncSetAttribute(vanka_big_fac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  dim3 grid(n_batches, (n_intervals + group - 1) / group);
-  vanka_big_fac_kernel<<<grid, kFThreads, smem, st>>>(classes, batches, vel_anchor, pre_anchor, F, r, u, isz,
-                                                       n_intervals, omega, group, max_m);
+  // persistent: one CTA per SM walks a strided share of the colour's batches
+  const int ngroups = (n_intervals + group - 1) / group;
+  const int ctas = std::max(1, std::min(n_batches, (device_sm_count() + ngroups - 1) / ngroups));
+  dim3 grid(ctas, ngroups);
+  vanka_big_fac_kernel<<<grid, kFThreads, smem, st>>>(classes, batches, n_batches, vel_anchor, pre_anchor, F, r, u,
+                                                       isz, n_intervals, omega, group, max_m, max_nt);
   return cudaGetLastError();
 }
 
