@@ -144,7 +144,8 @@ def run_c5_solve(torch, stmg, args):
     args.c5_slab intervals (v_init hand-off), FGMRES +
     hp-STMG V(2,2): p in r 2 -> 1, h in space down to 2^3 ("robust": k kept
     at 2; "spec": k 2 -> 1 -> 0 on the coarsest levels), cell Vanka with the
-    undeformed patch inverses (affine_patches)."""
+    exact per-cell patch inverses (default) or the undeformed ones
+    (--c5-patches affine)."""
     n, N, slab = args.c5_cells, args.c5_intervals, args.c5_slab
     verts = c5_vertices(n)
     ctx = stmg.Context(0)
@@ -179,7 +180,8 @@ def run_c5_solve(torch, stmg, args):
             "partition": f"1 GPU, {nsl} macro steps x {slab} intervals",
             "smoother": ("cell Vanka, undeformed patch inverses (affine_patches)"
                          if getattr(args, "c5_patches", "exact") == "affine" else
-                         "cell Vanka, exact per-cell patch inverses (built on the GPU)"),
+                         "cell Vanka, exact per-cell patch inverses built on the GPU, applied in the "
+                         "time-diagonalised form (one real + one complex-pair block per cell)"),
             "patch_setup": [l.patch_setup for l in sol.levels[1:]], "variant": args.c5_variant,
             "deviation_from_baseline": (
                 ("hierarchy substituted: k kept at 2 (BASELINE configs[4]: k 2->1->0), h in space only; " if
