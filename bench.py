@@ -763,7 +763,7 @@ def main():
         roof = {"bound": "hbm", "achieved": kd["GB/s"], "peak": hbm, "unit": "GB/s", "frac": kd["GB/s"] / hbm}
     traffic = None
     try:  # dram__bytes_read+write per launch of this kernel from the committed ncu capture
-        tr = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+        tr = json.loads(sorted((ROOT / "profiles").glob("r*_traffic.json"))[-1].read_text())  # latest round
         per = tr["per_launch_dram_bytes"]
         traffic = per["vmult"] if dom == "vmult" else per["vanka_update_pass"] * tr["launches_per_step"]["vanka_update_pass"]
     except Exception:

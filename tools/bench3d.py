@@ -174,7 +174,27 @@ def run_c5_solve(torch, stmg, args):
     e1.record()
     torch.cuda.synchronize()
     s = e0.elapsed_time(e1) * 1e-3
+    # one fine-level Vanka sweep (8 colour launches) over the slab: the
+    # smoother kernel's own roofline (it streams the patch blocks from HBM)
+    rr = seeded(torch, slab * f.size, 777)
+    uu = torch.zeros_like(rr)
+    sweep_ms = timed(torch, lambda: f.vanka_update(rr, uu, 0.8, slab), 3)
+    blk_bytes = 8.0 * f.total_matrix_elements  # the fine level's stored patch blocks, read once per sweep
+    peak = None
+    try:
+        import json
+        from pathlib import Path
+        peak = float(json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        pass
+    sweep = {"ms": sweep_ms, "intervals": slab, "patch_block_bytes": blk_bytes,
+             "achieved_GBs": blk_bytes / sweep_ms / 1e6,
+             "hbm_frac": (blk_bytes / sweep_ms / 1e6) / peak if peak else None,
+             "kernel": "vanka_big_fac_kernel (time-diagonalised blocks, cp.async.bulk chunk ring)"
+             if f.patch_setup["factored"] else "vanka_big_kernel (dense inverses)"}
+    del rr, uu
     return {"dofs": N * f.size, "seconds": s, "dofs_per_s": N * f.size / s, "setup_s": setup,
+            "fine_vanka_sweep": sweep,
             "device_memory_after_setup_gb": (total - free) / 1e9,
             "fgmres_iterations_per_slab": its, "levels": sol.level_info,
             "partition": f"1 GPU, {nsl} macro steps x {slab} intervals",
