@@ -89,19 +89,20 @@ def test_split_vcycle_matches_unsplit(stmg, ctx, nx, ny, nz, r, k, nh, parts):
         assert err <= 1e-10, (part, err)
 
 
-@pytest.mark.parametrize("parts,slabs", [(2, 2), (3, 1)])
-def test_split_solve_matches_unsplit(stmg, ctx, parts, slabs):
+@pytest.mark.parametrize("parts,slabs,tc,kmin", [(2, 2, False, 2), (3, 1, False, 2), (2, 2, True, 0)])
+def test_split_solve_matches_unsplit(stmg, ctx, parts, slabs, tc, kmin):
     """parts x slabs ranks (the C5 hybrid 2 x 4 layout in miniature, C5's
     discretisation: deformed, Q3/P2disc, DG(2)): FGMRES iterations within
     +-1 of the unpartitioned solve (which test_gpu_3d.py pins to the oracle),
-    solution <= 1e-9 of it."""
+    solution <= 1e-9 of it. The last case also coarsens in time (k 2 -> 0,
+    h in time: the BASELINE C5 plan) through the split transfers."""
     from paper_2502_09159_b200 import timeslab
 
     nx, ny, nz = 4, 4, 2 * parts
     r, k, nh, n_local = 2, 2, 1, 2
     N, tau = n_local * slabs, 1.0 / 8
     verts = o3.vertices(nx, ny, nz, 0.1, seed=12)
-    kw = dict(n_hcoarse=nh, time_coarsen=False, k_min=k, vertices=verts, rtol=1e-10)
+    kw = dict(n_hcoarse=nh, time_coarsen=tc, k_min=kmin, vertices=verts, rtol=1e-10)
     S1 = stmg.Solver3(ctx, nx, ny, nz, r, k, tau, 1.0, 1.0, **kw)
     f = S1.finest
     ref = o3.OracleLevel3(nx, ny, nz, r, k, tau, 1.0, 1.0, vertices=verts, smoother=False)
