@@ -86,6 +86,10 @@ cudaError_t launch_vanka_fac(const DevPatchClass *classes, const VankaTile *tile
                              const long long *pa, const int *tile_ptr, int n_blocks, int ng_full, const FacParams &F,
                              const double *r, double *u, long long isz, int n_intervals, double omega,
                              cudaStream_t stream);
+/// Deferred-scatter DMMA sweep of one colour for 128 < n_T <= 176 (3D Q2 cells), batches of one class.
+cudaError_t launch_vanka_dfr176(const DevPatchClass *classes, const VankaBatch *batches, int n_batches, int max_nt,
+                                const long long *vel_anchor, const long long *pre_anchor, const double *r, double *u,
+                                long long isz, int n_intervals, double omega, int group, cudaStream_t stream);
 int vanka_tc_cols();
 int vanka_tc_max_tiles();
 bool vanka_fac_supported(int S, int nsp); // instantiated (S, n_sp) shapes of vanka_fac_kernel

@@ -894,6 +894,19 @@ launch_vanka_colour(const DevPatchClass *classes, const VankaBatch *batches, con
   if (n_batches == 0 || n_intervals == 0)
     return cudaSuccess;
   static const bool force_big = std::getenv("STMG_VANKA_BIG") != nullptr; // A/B switch for 128 < n_T <= 176
+  static const bool old176 = std::getenv("STMG_VANKA176_OLD") != nullptr;   // A/B switch: the split item kernel
+  if (max_nt > kDRows && max_nt <= 176 && !item_ptr && !force_big && !old176)
+    {
+      // deferred-scatter pipeline (vanka_tc.cu); long blocks keep the ring busy
+      int group = g_group_override[0] > 0 ? g_group_override[0] : 16;
+      while (group > 1 &&
+             static_cast<long long>(n_batches) * 2 * ((n_intervals + group - 1) / group) < 2 * device_sm_count())
+        group /= 2;
+      const cudaError_t e = launch_vanka_dfr176(classes, batches, n_batches, max_nt, vel_anchor, pre_anchor, r, u,
+                                                isz, n_intervals, omega, group, stream);
+      if (e != cudaErrorInvalidValue)
+        return e;
+    }
   if (max_nt <= 176 && !(force_big && max_nt > kDRows && !item_ptr))
     {
       // 128 rows (16 warps) for 2D patches; 176 rows (22 warps) for 3D Q2 cells (n_T = 170)

@@ -552,6 +552,172 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// ------------------------------------------------ 176-row patches (3D Q2)
+// The deferred-scatter pipeline of vanka_dfr_kernel for patches of
+// 128 < n_T <= 176 rows (C3: Q2/P1disc x DG(1) cells, n_T = 170), one colour
+// of same-class batches per launch (3D: 8 parity colours, no dof shared in
+// a launch, so no phase barriers). The 176 rows are split over two CTAs
+// (blockIdx.z) of 11 warps (88 rows each, one 8-row A tile per warp in
+// registers, the valence weight and omega folded in); both CTAs gather the
+// whole R tile (the contraction dimension) into a 3-slot cp.async ring two
+// tiles ahead, and scatter the previous tile's accumulators inside the
+// current tile's DMMA k-loop.
+constexpr int k3Rows = 176, k3Half = 88, k3Warps = 11, k3Threads = 32 * k3Warps, k3KS = k3Rows / 4;
+constexpr int k3Ld = k3Rows + 4; // == 4 mod 16 doubles: conflict-free B fragments
+constexpr int k3Slot = kTCols * k3Ld;
+constexpr int k3MaxCols = 32 * 16; // columns (patch, interval) per block
+
+__global__ void __launch_bounds__(k3Threads, 1)
+vanka_dfr176_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
+                    const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
+                    const double *__restrict__ r, double *__restrict__ u, long long isz, int n_intervals,
+                    double omega, int group)
+{
+  extern __shared__ __align__(16) double ring[];
+  long long *s_colv = reinterpret_cast<long long *>(ring + kTRing * k3Slot);
+  int *s_dp = reinterpret_cast<int *>(s_colv + k3MaxCols);
+  unsigned long long *s_bar = reinterpret_cast<unsigned long long *>(s_dp + k3MaxCols);
+  unsigned long long *full = s_bar, *empty = s_bar + 3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const VankaBatch bt = batches[blockIdx.x];
+  const DevPatchClass pc = classes[bt.cls];
+  const int nt = pc.n_t, nvel = pc.n_vel;
+  const int n0 = blockIdx.y * group, ng = min(group, n_intervals - n0);
+  const int ncols = bt.count * ng, nb = (ncols + kTCols - 1) / kTCols;
+  const int row0 = static_cast<int>(blockIdx.z) * k3Half;
+  for (int e = tid; e < nb * kTCols; e += k3Threads)
+    {
+      if (e < ncols)
+        {
+          const int patch = bt.first + e / ng, nl = e % ng;
+          const long long vb = __ldg(vel_anchor + patch), pb = __ldg(pre_anchor + patch);
+          s_colv[e] = (n0 + nl) * isz + vb;
+          s_dp[e] = static_cast<int>(pb - vb);
+        }
+      else
+        {
+          s_colv[e] = kMaskedCol;
+          s_dp[e] = 0;
+        }
+    }
+  if (tid == 0)
+    for (int i = 0; i < 3; ++i)
+      {
+        mbar_init(full + i, k3Threads);
+        mbar_init(empty + i, k3Threads);
+      }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+
+  // gather: warp w fills columns w, w + 11, w + 22; lane l rows l + 32 q
+  constexpr int QN = (k3Rows + 31) / 32, CN = (kTCols + k3Warps - 1) / k3Warps;
+  int relq[QN], pmq[QN];
+#pragma unroll
+  for (int q = 0; q < QN; ++q)
+    {
+      const int rw = lane + 32 * q;
+      relq[q] = rw < nt ? static_cast<int>(pc.rel[rw]) : kMaskedRow;
+      pmq[q] = (rw < nt && rw >= nvel) ? -1 : 0;
+    }
+  auto issue = [&](int lt, int s) {
+    if (lt < nb)
+      {
+        double *slot = ring + s * k3Slot + lane;
+#pragma unroll
+        for (int cc = 0; cc < CN; ++cc)
+          {
+            const int col = warp + cc * k3Warps;
+            if (col >= kTCols)
+              continue;
+            const int ci = lt * kTCols + col;
+            const long long cv = s_colv[ci];
+            const bool colok = cv != kMaskedCol;
+            const double *pv = r + (colok ? cv : 0);
+            const int dp = s_dp[ci];
+#pragma unroll
+            for (int q = 0; q < QN; ++q)
+              if (lane + 32 * q < k3Ld)
+                {
+                  const bool ok = colok && relq[q] != kMaskedRow;
+                  cp_async8z(slot + col * k3Ld + 32 * q, pv + (ok ? relq[q] + (dp & pmq[q]) : 0), ok);
+                }
+          }
+      }
+    cp_async_mbar_arrive(full + s);
+  };
+  issue(0, 0);
+  issue(1, 1);
+
+  // this warp's 8 rows of the inverse, weight and omega folded in
+  const int row = row0 + 8 * warp + (lane >> 2);
+  const bool c_ok = row < nt;
+  double afr[k3KS];
+  {
+    const double wrow = c_ok ? omega * pc.weight[row] : 0.0;
+#pragma unroll
+    for (int kk = 0; kk < k3KS; ++kk)
+      {
+        const int col = 4 * kk + (lane & 3);
+        afr[kk] = (c_ok && col < nt) ? wrow * __ldg(pc.inverse + row * nt + col) : 0.0;
+      }
+  }
+  const int c_pm = (c_ok && row >= nvel) ? -1 : 0;
+  double *const c_ub = u + (c_ok ? pc.rel[row] : 0);
+  const bool mine = row0 + 8 * warp < nt;
+  double pacc[kTCols / 8][2] = {};
+  int p_lt = -1;
+  auto scatter_one = [&](int j) {
+    const int ct = j >> 1, b = j & 1;
+    const int ci = p_lt * kTCols + 8 * ct + 2 * (lane & 3) + b;
+    const long long cv = s_colv[ci];
+    if (cv != kMaskedCol)
+      red_add(c_ub + (cv + (s_dp[ci] & c_pm)), pacc[ct][b]);
+  };
+  for (int lt = 0; lt < nb; ++lt)
+    {
+      const int slot = lt % 3;
+      mbar_wait(full + slot, (lt / 3) & 1);
+      double acc[kTCols / 8][2];
+#pragma unroll
+      for (int ct = 0; ct < kTCols / 8; ++ct)
+        acc[ct][0] = acc[ct][1] = 0.0;
+      if (mine)
+        {
+          const double *bbase = ring + slot * k3Slot + (lane >> 2) * k3Ld + (lane & 3);
+#pragma unroll
+          for (int kk = 0; kk < k3KS; ++kk)
+            {
+              const double *brow = bbase + 4 * kk;
+#pragma unroll
+              for (int ct = 0; ct < kTCols / 8; ++ct)
+                dmma(acc[ct], afr[kk], brow[8 * k3Ld * ct]);
+              if (kk < 2 * (kTCols / 8) && p_lt >= 0 && c_ok)
+                scatter_one(kk);
+            }
+        }
+      mbar_arrive(empty + slot);
+      p_lt = lt;
+#pragma unroll
+      for (int ct = 0; ct < kTCols / 8; ++ct)
+        {
+          pacc[ct][0] = acc[ct][0];
+          pacc[ct][1] = acc[ct][1];
+        }
+      if (lt + 2 < nb)
+        {
+          const int ns = (lt + 2) % 3;
+          if (lt >= 1)
+            mbar_wait(empty + ns, ((lt - 1) / 3) & 1);
+          issue(lt + 2, ns);
+        }
+    }
+  if (p_lt >= 0 && c_ok && mine)
+#pragma unroll
+    for (int j = 0; j < 2 * (kTCols / 8); ++j)
+      scatter_one(j);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- factored
 // Time-diagonalised patch solves: A_T^{-1} = (V (x) I) blockdiag(B_b^{-1})
 // (W (x) I) (setup.hpp TemporalEigen). Per tile: stage 1 mixes the slots of
@@ -857,6 +1023,23 @@ launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long
     go(vanka_tc_kernel<29>);
   else
     go(vanka_tc_kernel<32>);
+  return cudaGetLastError();
+}
+
+cudaError_t
+launch_vanka_dfr176(const DevPatchClass *classes, const VankaBatch *batches, int n_batches, int max_nt,
+                    const long long *vel_anchor, const long long *pre_anchor, const double *r, double *u,
+                    long long isz, int n_intervals, double omega, int group, cudaStream_t stream)
+{
+  if (n_batches == 0 || n_intervals == 0)
+    return cudaSuccess;
+  if (max_nt > k3Rows || group * vanka_cols_per_batch() > k3MaxCols)
+    return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double) * kTRing * k3Slot + k3MaxCols * 12 + 6 * sizeof(unsigned long long);
+  cudaFuncSetAttribute(vanka_dfr176_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  dim3 grid(n_batches, (n_intervals + group - 1) / group, 2);
+  vanka_dfr176_kernel<<<grid, k3Threads, smem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz,
+                                                          n_intervals, omega, group);
   return cudaGetLastError();
 }
 
