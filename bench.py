@@ -27,7 +27,7 @@ Extra fields of the JSON line (not the headline; skipped with --no-solve):
   solve.C4_full        (1 GPU) the whole 64-interval C4 system as 8 macro steps
   solve.C3_all_at_once the 64-interval C3 system (32^3, Q2/P1disc, DG(1))
                        split into time slabs over all ranks (NCCL)
-  solve.C5_hybrid      (N >= 2, even) the whole 128-interval C5 system as one
+  solve.C5_hybrid      (N >= 4, even) the whole 128-interval C5 system as one
                        all-at-once solve, hybrid 2 z parts x N/2 time slabs
   C4_step              C4 vmult + vertex-star smoother step over 8 intervals
   3D.C3                (1 GPU) C3: 32^3 Q2/P1disc, DG(1), 64 intervals: vmult,
@@ -719,7 +719,7 @@ def main():
             c3slab = c3_slab_leg(stmg, torch, dist, world, rank)
         except Exception as exc:
             c3slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-        if world > 1 and world % 2 == 0:
+        if world >= 4 and world % 2 == 0:  # >= 2 time slabs: <= 64 intervals (~100 GB) per rank
             try:
                 c5hyb = c5_hybrid_leg(stmg, torch, dist, world, rank)
             except Exception as exc:
