@@ -80,8 +80,10 @@ def run_c3(torch, stmg, args):
         out["deviation_from_baseline"] = (
             "hierarchy substituted: k kept at 1 and h-coarsening in space only (to 2^3), exact coarse forward "
             "substitution in time over all intervals. BASELINE configs[2] asks for k 1->0 then h in space AND time "
-            "down to 4^3x8; with the reference's time-block-diagonal cell Vanka that plan is not h-robust "
-            "(42 / 98 FGMRES iterations at 8^3 / 16^3, DESIGN.md 3.4), so the BASELINE plan's solve is unmeasured")
+            "down to 4^3x8; with the reference's cell Vanka that plan is not h-robust: its time h-coarsening costs "
+            "42 / 94 FGMRES iterations at 8^3 / 16^3 (k->0 alone: 15 / 15; damping 0.4-0.8 and a forward "
+            "Gauss-Seidel sweep in time do not help), DESIGN.md 3.4; at 32^3 x 64 its Krylov space does not fit, "
+            "so the full BASELINE plan is unmeasured; solve_k_to_0 measures its k->0 part")
     torch.cuda.synchronize()
     out["setup_s"] = time.perf_counter() - t0
     out["levels"] = sol.level_info
@@ -122,6 +124,26 @@ def run_c3(torch, stmg, args):
         s = e0.elapsed_time(e1) * 1e-3
         out["solve"] = {"seconds": s, "fgmres_iterations": it, "dofs_per_s": dofs / s,
                         "relative_residual": hist[-1] / hist[0]}
+        if not spec:
+            # the part of BASELINE's plan that is h-robust with this smoother:
+            # k 1 -> 0 (temporal p-coarsening) + h in space only; the time
+            # h-coarsening is what breaks robustness
+            del sol
+            torch.cuda.empty_cache()
+            sk = stmg.Solver3(ctx, n, n, n, 1, 1, 1.0 / N, 1.0, 1.0, n_hcoarse=args.c3_hcoarse + 1, time_coarsen=False,
+                              k_min=0, nu1=2, nu2=2, rtol=1e-8, max_iterations=args.maxit)
+            X = torch.zeros_like(F)
+            sk.solve_all_at_once(F, X, N)
+            torch.cuda.synchronize()
+            e0.record()
+            it, hist = sk.solve_all_at_once(F, X, N)
+            e1.record()
+            torch.cuda.synchronize()
+            s = e0.elapsed_time(e1) * 1e-3
+            out["solve_k_to_0"] = {"seconds": s, "fgmres_iterations": it, "dofs_per_s": dofs / s,
+                                   "relative_residual": hist[-1] / hist[0],
+                                   "hierarchy": "k 1 -> 0 on the coarsest level, h in space only to 2^3 "
+                                                "(BASELINE's plan without the time h-coarsening)"}
     return out
 
 
