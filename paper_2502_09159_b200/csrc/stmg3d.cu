@@ -961,8 +961,10 @@ struct stmg3_solver
     check(cudaMemcpyAsync(rhs.p, F, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
     if (v_init && rank() == 0)
       {
-        // F_0 += C v_init (coupling_rhs, constrained rows zero)
+        // F_0 += C v_init (coupling_rhs, constrained rows zero); a z part
+        // sums the coupling's interface rows with its neighbours
         L.vmult(L.zero_vector(1), F, rhs.p, 1, v_init, 1, 1);
+        iface_sum(static_cast<int>(levels.size()) - 1, rhs.p, F, 1, 1);
         L.zero_constrained(rhs.p, 1);
       }
     const int it = gmres(rhs.p, X, iterations, history, cap, nI);

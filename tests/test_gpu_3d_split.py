@@ -141,6 +141,56 @@ def test_split_solve_matches_unsplit(stmg, ctx, parts, slabs, tc, kmin):
     assert np.linalg.norm(Xp - X1) / np.linalg.norm(X1) <= 1e-9
 
 
+def test_split_macro_step_handoff(stmg, ctx):
+    """A slab that continues a previous one (v_init, the slot-k velocity
+    entering its first interval): the split solve adds the jump coupling's
+    interface rows of both parts, equal to the unsplit solve (<= 1e-9)."""
+    from paper_2502_09159_b200 import timeslab
+
+    nx, ny, nz, r, k, parts, N, tau = 4, 4, 4, 1, 1, 2, 2, 1.0 / 8
+    verts = o3.vertices(nx, ny, nz, 0.1, seed=14)
+    kw = dict(n_hcoarse=1, time_coarsen=False, k_min=k, vertices=verts, rtol=1e-10)
+    S1 = stmg.Solver3(ctx, nx, ny, nz, r, k, tau, 1.0, 1.0, **kw)
+    f = S1.finest
+    ref = o3.OracleLevel3(nx, ny, nz, r, k, tau, 1.0, 1.0, vertices=verts, smoother=False)
+    F = o3.make_consistent3(np.random.default_rng(31).uniform(-1, 1, N * f.size), ref, N)
+    vg = np.random.default_rng(32).uniform(-1, 1, f.n_velocity)
+    gz = f.gz
+    bnd = np.zeros((gz, f.gy, f.gx), dtype=bool)
+    bnd[0] = bnd[-1] = True
+    bnd[:, 0] = bnd[:, -1] = True
+    bnd[:, :, 0] = bnd[:, :, -1] = True
+    vg.reshape(3, -1)[:, bnd.reshape(-1)] = 0.0
+    X1 = torch.zeros(N * f.size, dtype=torch.float64, device="cuda")
+    it1, _ = S1.solve_all_at_once(_cuda(F), X1, N, v_init=_cuda(vg))
+    torch.cuda.synchronize()
+    X1 = X1.cpu().numpy().reshape(N, f.size)
+    hub = timeslab.LoopbackSpaceHub(parts, timeout=120.0)
+    out = {}
+
+    def rank(part):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            c = stmg.Context(0, stream=stream)
+            sol = stmg.Solver3(c, nx, ny, nz, r, k, tau, 1.0, 1.0, z_parts=parts, z_part=part, **kw)
+            sol.set_space_comm(timeslab.LoopbackSpaceComm(hub, part))
+            idx = timeslab.z_part_dofs(nx, ny, nz, r, k, parts, part)
+            vidx = idx[:sol.finest.n_velocity]  # slot 0 velocity block: (component, node) order as v_init
+            Fl = _cuda(F.reshape(N, f.size)[:, idx])
+            Xl = torch.zeros_like(Fl)
+            vl = _cuda(vg[vidx])
+            stream.synchronize()
+            it, _ = sol.solve_all_at_once(Fl.reshape(-1), Xl.reshape(-1), N, v_init=vl)
+            stream.synchronize()
+            out[part] = (it, idx, Xl.cpu().numpy())
+
+    _run_ranks(rank, parts)
+    for part in range(parts):
+        it, idx, Xl = out[part]
+        assert abs(it - it1) <= 1
+        assert np.linalg.norm(Xl - X1[:, idx]) / np.linalg.norm(X1[:, idx]) <= 1e-9
+
+
 def test_split_rejects_bad_partitions(stmg, ctx):
     verts = o3.vertices(4, 4, 4, 0.1, seed=13)
     with pytest.raises(stmg.StmgError):  # 4 cells in z do not split in 3
