@@ -129,6 +129,14 @@ int stmg_vanka_update(stmg_level *level, const double *r, double *u, double omeg
 int stmg_vmult_host(stmg_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);
 int stmg_smooth_step_host(stmg_level *level, const double *b, double *u, double omega, int n_intervals,
                           const double *x_prev_slot, int coupled);
+/* Non-blocking variants: enqueue the copies and kernels on the context's
+ * streams and return; the host buffers must stay valid and untouched until
+ * stmg_ctx_synchronize. Consecutive calls overlap (the next call's H2D copies
+ * run while the previous call computes and copies back); a call waits only
+ * for the previous call of the same kind to release its device staging. */
+int stmg_vmult_host_async(stmg_level *level, const double *x, double *y, int n_intervals, const double *x_prev_slot);
+int stmg_smooth_step_host_async(stmg_level *level, const double *b, double *u, double omega, int n_intervals,
+                                const double *x_prev_slot, int coupled);
 
 /* ------------------------------------------------------------ built-in problems
  * The reference's manufactured problem (problems.cpp:13-62): its load vector

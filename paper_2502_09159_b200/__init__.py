@@ -69,6 +69,9 @@ _SIGNATURES = {
     "stmg_vanka_update": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int], _c_int),
     "stmg_vmult_host": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
     "stmg_smooth_step_host": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int], _c_int),
+    "stmg_vmult_host_async": ([_c_void_p, _c_void_p, _c_void_p, _c_int, _c_void_p], _c_int),
+    "stmg_smooth_step_host_async": ([_c_void_p, _c_void_p, _c_void_p, _c_double, _c_int, _c_void_p, _c_int],
+                                    _c_int),
     "stmg_solver_create": ([_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_double, _c_double, _c_double, _c_int,
                             _c_int, _c_int, _c_double, _c_int, _c_double, _c_double, _c_int,
                             ctypes.POINTER(_c_void_p)], _c_int),
@@ -396,16 +399,19 @@ class Level:
                                                   n_intervals, out))
         return dict(e_v_l2=out[0], e_p_l2=out[1], e_v_h1=out[2], e_div=out[3], e_v_linf=out[4])
 
-    def vmult_host(self, x, y, n_intervals: int = 1, x_prev_slot=None):
-        _check(load_library().stmg_vmult_host(self._h, self._hv(x, n_intervals, "x"), self._hv(y, n_intervals, "y"),
-                                              n_intervals, _hptr(x_prev_slot, self.n_velocity, "x_prev_slot")))
+    def vmult_host(self, x, y, n_intervals: int = 1, x_prev_slot=None, blocking: bool = True):
+        """Host (numpy) buffers; blocking=False enqueues only (stmg_vmult_host_async): keep the
+        buffers alive and call ctx.synchronize() before reading y."""
+        fn = load_library().stmg_vmult_host if blocking else load_library().stmg_vmult_host_async
+        _check(fn(self._h, self._hv(x, n_intervals, "x"), self._hv(y, n_intervals, "y"), n_intervals,
+                  _hptr(x_prev_slot, self.n_velocity, "x_prev_slot")))
         return y
 
-    def smooth_step_host(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False):
-        _check(load_library().stmg_smooth_step_host(self._h, self._hv(b, n_intervals, "b"),
-                                                    self._hv(u, n_intervals, "u"), omega, n_intervals,
-                                                    _hptr(x_prev_slot, self.n_velocity, "x_prev_slot"),
-                                                    int(coupled)))
+    def smooth_step_host(self, b, u, omega: float, n_intervals: int = 1, x_prev_slot=None, coupled: bool = False,
+                         blocking: bool = True):
+        fn = load_library().stmg_smooth_step_host if blocking else load_library().stmg_smooth_step_host_async
+        _check(fn(self._h, self._hv(b, n_intervals, "b"), self._hv(u, n_intervals, "u"), omega, n_intervals,
+                  _hptr(x_prev_slot, self.n_velocity, "x_prev_slot"), int(coupled)))
         return u
 
     def __del__(self):

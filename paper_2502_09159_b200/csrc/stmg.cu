@@ -66,6 +66,41 @@ struct stmg_level
   std::uint64_t total_matrix_elements = 0;
   // scratch
   DevArray<double> work, zeros, host_in, host_out, host_prev, proj, err_part, err_out;
+  // host-buffer entry points: staging of stmg_vmult_host (host_in / host_out /
+  // host_prev_v) and stmg_smooth_step_host (host_b / host_u / host_prev), and
+  // per set the events that free its input (kernels done) and output (D2H
+  // done) staging for the next call, so *_async calls can queue back to back
+  DevArray<double> host_b, host_u, host_prev_v;
+  cudaEvent_t ev_in_free[2] = {nullptr, nullptr}, ev_out_free[2] = {nullptr, nullptr};
+  ~stmg_level()
+  {
+    for (cudaEvent_t e : {ev_in_free[0], ev_in_free[1], ev_out_free[0], ev_out_free[1]})
+      if (e)
+        cudaEventDestroy(e);
+  }
+  /// Before a host-buffer call of set k: wait until the previous call of the
+  /// same set released its staging.
+  void
+  host_begin(int k)
+  {
+    if (!ev_in_free[k])
+      {
+        check(cudaEventCreateWithFlags(&ev_in_free[k], cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&ev_out_free[k], cudaEventDisableTiming), "event");
+        check(cudaEventRecord(ev_in_free[k], ctx->stream), "event");
+        check(cudaEventRecord(ev_out_free[k], ctx->d2h), "event");
+      }
+    check(cudaStreamWaitEvent(ctx->h2d, ev_in_free[k], 0), "wait");
+    check(cudaStreamWaitEvent(ctx->stream, ev_out_free[k], 0), "wait");
+  }
+  void
+  host_end(int k, bool sync)
+  {
+    check(cudaEventRecord(ev_in_free[k], ctx->stream), "event");
+    check(cudaEventRecord(ev_out_free[k], ctx->d2h), "event");
+    if (sync)
+      check(cudaStreamSynchronize(ctx->d2h), "sync");
+  }
   // built-in problem tables (problems.cu), built on first use
   ProblemTables ptab{};
   bool ptab_ready = false;
@@ -1173,7 +1208,13 @@ stmg_ctx_set_stream(stmg_ctx *ctx, void *stream)
 int
 stmg_ctx_synchronize(stmg_ctx *ctx)
 {
-  return guarded([&] { check(cudaStreamSynchronize(ctx->stream), "sync"); });
+  return guarded([&] {
+    check(cudaStreamSynchronize(ctx->stream), "sync");
+    if (ctx->h2d) // the host-buffer entry points' copy streams
+      check(cudaStreamSynchronize(ctx->h2d), "sync");
+    if (ctx->d2h)
+      check(cudaStreamSynchronize(ctx->d2h), "sync");
+  });
 }
 
 int64_t
@@ -1363,39 +1404,97 @@ namespace
 constexpr int kHostChunk = STMG_HOST_CHUNK;
 }
 
+namespace
+{
+void
+vmult_host_impl(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot, bool sync)
+{
+  stmg_ctx &C = *L->ctx;
+  C.copy_streams();
+  const long long isz = L->spec.isz(), mv = L->spec.mv();
+  const size_t sz = static_cast<size_t>(isz) * n;
+  L->host_in.resize(sz);
+  L->host_out.resize(sz);
+  L->host_begin(0);
+  const double *prev = nullptr;
+  if (x_prev_slot)
+    {
+      L->host_prev_v.resize(mv);
+      check(cudaMemcpyAsync(L->host_prev_v.p, x_prev_slot, sizeof(double) * mv, cudaMemcpyHostToDevice, C.h2d),
+            "h2d");
+      prev = L->host_prev_v.p;
+    }
+  const int nch = (n + kHostChunk - 1) / kHostChunk;
+  for (int c = 0; c < nch; ++c)
+    {
+      const int i0 = c * kHostChunk, m = std::min(kHostChunk, n - i0);
+      const size_t off = static_cast<size_t>(i0) * isz, len = static_cast<size_t>(m) * isz;
+      check(cudaMemcpyAsync(L->host_in.p + off, x + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
+      check(cudaEventRecord(C.event(2 * c), C.h2d), "event");
+      check(cudaStreamWaitEvent(C.stream, C.event(2 * c), 0), "wait");
+      const double *pc = c == 0 ? prev : L->host_in.p + off - isz + (L->spec.S() - 1) * mv;
+      L->vmult(L->host_in.p + off, nullptr, L->host_out.p + off, m, pc, 1, 0);
+      check(cudaEventRecord(C.event(2 * c + 1), C.stream), "event");
+      check(cudaStreamWaitEvent(C.d2h, C.event(2 * c + 1), 0), "wait");
+      check(cudaMemcpyAsync(y + off, L->host_out.p + off, sizeof(double) * len, cudaMemcpyDeviceToHost, C.d2h), "d2h");
+    }
+  L->host_end(0, sync);
+}
+
+void
+smooth_step_host_impl(stmg_level *L, const double *b, double *u, double omega, int n, const double *x_prev_slot,
+                      int coupled, bool sync)
+{
+  if (!(omega > 0.0 && omega <= 1.0))
+    throw std::invalid_argument("smooth_step: omega must be in (0, 1]");
+  stmg_ctx &C = *L->ctx;
+  C.copy_streams();
+  const long long isz = L->spec.isz(), mv = L->spec.mv();
+  const size_t sz = static_cast<size_t>(isz) * n;
+  L->host_b.resize(sz);
+  L->host_u.resize(sz);
+  L->host_prev.resize(3 * mv); // [0]: x_prev_slot, [1], [2]: ring of pre-update chunk halos
+  L->host_begin(1);
+  const double *prev = nullptr;
+  if (x_prev_slot && coupled)
+    {
+      check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * mv, cudaMemcpyHostToDevice, C.h2d), "h2d");
+      prev = L->host_prev.p;
+    }
+  double *r = L->scratch(std::min(n, kHostChunk));
+  const int nch = (n + kHostChunk - 1) / kHostChunk;
+  for (int c = 0; c < nch; ++c)
+    {
+      const int i0 = c * kHostChunk, m = std::min(kHostChunk, n - i0);
+      const size_t off = static_cast<size_t>(i0) * isz, len = static_cast<size_t>(m) * isz;
+      check(cudaMemcpyAsync(L->host_b.p + off, b + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
+      check(cudaMemcpyAsync(L->host_u.p + off, u + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
+      check(cudaEventRecord(C.event(2 * c), C.h2d), "event");
+      check(cudaStreamWaitEvent(C.stream, C.event(2 * c), 0), "wait");
+      // residual with the pre-update halo of the previous chunk (Jacobi: the
+      // whole step sees the old u, as in VankaSmoother::smooth_step)
+      const double *halo = c == 0 ? prev : L->host_prev.p + (1 + ((c - 1) & 1)) * mv;
+      double *uc = L->host_u.p + off;
+      L->vmult(uc, L->host_b.p + off, r, m, coupled ? halo : nullptr, coupled ? 1 : 0, 1);
+      if (coupled && c + 1 < nch)
+        check(cudaMemcpyAsync(L->host_prev.p + (1 + (c & 1)) * mv, uc + (m - 1) * isz + (L->spec.S() - 1) * mv,
+                              sizeof(double) * mv, cudaMemcpyDeviceToDevice, C.stream),
+              "halo");
+      L->vanka(r, uc, m, omega);
+      check(cudaEventRecord(C.event(2 * c + 1), C.stream), "event");
+      check(cudaStreamWaitEvent(C.d2h, C.event(2 * c + 1), 0), "wait");
+      check(cudaMemcpyAsync(u + off, uc, sizeof(double) * len, cudaMemcpyDeviceToHost, C.d2h), "d2h");
+    }
+  L->host_end(1, sync);
+}
+} // namespace
+
 int
 stmg_vmult_host(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot)
 {
   return guarded([&] {
     STMG_NVTX("stmg_vmult_host");
-    stmg_ctx &C = *L->ctx;
-    C.copy_streams();
-    const long long isz = L->spec.isz(), mv = L->spec.mv();
-    const size_t sz = static_cast<size_t>(isz) * n;
-    L->host_in.resize(sz);
-    L->host_out.resize(sz);
-    const double *prev = nullptr;
-    if (x_prev_slot)
-      {
-        L->host_prev.resize(mv);
-        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * mv, cudaMemcpyHostToDevice, C.h2d), "h2d");
-        prev = L->host_prev.p;
-      }
-    const int nch = (n + kHostChunk - 1) / kHostChunk;
-    for (int c = 0; c < nch; ++c)
-      {
-        const int i0 = c * kHostChunk, m = std::min(kHostChunk, n - i0);
-        const size_t off = static_cast<size_t>(i0) * isz, len = static_cast<size_t>(m) * isz;
-        check(cudaMemcpyAsync(L->host_in.p + off, x + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
-        check(cudaEventRecord(C.event(2 * c), C.h2d), "event");
-        check(cudaStreamWaitEvent(C.stream, C.event(2 * c), 0), "wait");
-        const double *pc = c == 0 ? prev : L->host_in.p + off - isz + (L->spec.S() - 1) * mv;
-        L->vmult(L->host_in.p + off, nullptr, L->host_out.p + off, m, pc, 1, 0);
-        check(cudaEventRecord(C.event(2 * c + 1), C.stream), "event");
-        check(cudaStreamWaitEvent(C.d2h, C.event(2 * c + 1), 0), "wait");
-        check(cudaMemcpyAsync(y + off, L->host_out.p + off, sizeof(double) * len, cudaMemcpyDeviceToHost, C.d2h), "d2h");
-      }
-    check(cudaStreamSynchronize(C.d2h), "sync");
+    vmult_host_impl(L, x, y, n, x_prev_slot, true);
   });
 }
 
@@ -1405,46 +1504,26 @@ stmg_smooth_step_host(stmg_level *L, const double *b, double *u, double omega, i
 {
   return guarded([&] {
     STMG_NVTX("stmg_smooth_step_host");
-    if (!(omega > 0.0 && omega <= 1.0))
-      throw std::invalid_argument("smooth_step: omega must be in (0, 1]");
-    stmg_ctx &C = *L->ctx;
-    C.copy_streams();
-    const long long isz = L->spec.isz(), mv = L->spec.mv();
-    const size_t sz = static_cast<size_t>(isz) * n;
-    L->host_in.resize(sz);   // b
-    L->host_out.resize(sz);  // u
-    L->host_prev.resize(3 * mv); // [0]: x_prev_slot, [1], [2]: ring of pre-update chunk halos
-    const double *prev = nullptr;
-    if (x_prev_slot && coupled)
-      {
-        check(cudaMemcpyAsync(L->host_prev.p, x_prev_slot, sizeof(double) * mv, cudaMemcpyHostToDevice, C.h2d), "h2d");
-        prev = L->host_prev.p;
-      }
-    double *r = L->scratch(std::min(n, kHostChunk));
-    const int nch = (n + kHostChunk - 1) / kHostChunk;
-    for (int c = 0; c < nch; ++c)
-      {
-        const int i0 = c * kHostChunk, m = std::min(kHostChunk, n - i0);
-        const size_t off = static_cast<size_t>(i0) * isz, len = static_cast<size_t>(m) * isz;
-        check(cudaMemcpyAsync(L->host_in.p + off, b + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
-        check(cudaMemcpyAsync(L->host_out.p + off, u + off, sizeof(double) * len, cudaMemcpyHostToDevice, C.h2d), "h2d");
-        check(cudaEventRecord(C.event(2 * c), C.h2d), "event");
-        check(cudaStreamWaitEvent(C.stream, C.event(2 * c), 0), "wait");
-        // residual with the pre-update halo of the previous chunk (Jacobi: the
-        // whole step sees the old u, as in VankaSmoother::smooth_step)
-        const double *halo = c == 0 ? prev : L->host_prev.p + (1 + ((c - 1) & 1)) * mv;
-        double *uc = L->host_out.p + off;
-        L->vmult(uc, L->host_in.p + off, r, m, coupled ? halo : nullptr, coupled ? 1 : 0, 1);
-        if (coupled && c + 1 < nch)
-          check(cudaMemcpyAsync(L->host_prev.p + (1 + (c & 1)) * mv, uc + (m - 1) * isz + (L->spec.S() - 1) * mv,
-                                sizeof(double) * mv, cudaMemcpyDeviceToDevice, C.stream),
-                "halo");
-        L->vanka(r, uc, m, omega);
-        check(cudaEventRecord(C.event(2 * c + 1), C.stream), "event");
-        check(cudaStreamWaitEvent(C.d2h, C.event(2 * c + 1), 0), "wait");
-        check(cudaMemcpyAsync(u + off, uc, sizeof(double) * len, cudaMemcpyDeviceToHost, C.d2h), "d2h");
-      }
-    check(cudaStreamSynchronize(C.d2h), "sync");
+    smooth_step_host_impl(L, b, u, omega, n, x_prev_slot, coupled, true);
+  });
+}
+
+int
+stmg_vmult_host_async(stmg_level *L, const double *x, double *y, int n, const double *x_prev_slot)
+{
+  return guarded([&] {
+    STMG_NVTX("stmg_vmult_host_async");
+    vmult_host_impl(L, x, y, n, x_prev_slot, false);
+  });
+}
+
+int
+stmg_smooth_step_host_async(stmg_level *L, const double *b, double *u, double omega, int n,
+                            const double *x_prev_slot, int coupled)
+{
+  return guarded([&] {
+    STMG_NVTX("stmg_smooth_step_host_async");
+    smooth_step_host_impl(L, b, u, omega, n, x_prev_slot, coupled, false);
   });
 }
 

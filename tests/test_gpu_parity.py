@@ -338,3 +338,27 @@ def test_step_health_matches_oracle(ctx, stmg, nc, r, k):
     sol.time_march(torch.from_numpy(F).cuda(), Xs)
     health = lv.step_health(Xs, 4)
     assert all(m <= 1e-10 for _, m in health)  # pressure projected mean-zero every step
+
+
+def test_host_async_entry_points_queue_back_to_back(ctx, stmg, oracle):
+    """stmg_vmult_host_async / stmg_smooth_step_host_async: several calls
+    enqueued without synchronising (different inputs, multi-chunk) give the
+    blocking results once the context is synchronised."""
+    nc, r, k, n = 16, 2, 2, 9  # 3 chunks of <= 4 intervals
+    lvl = stmg.Level(ctx, nc, nc, r, k, 0.125, 1.0, 1.0, stmg.SMOOTHER_CELL)
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    xs = [pin(oc.seeded(n * lvl.size, 91 + i)) for i in range(2)]
+    bs = [pin(oc.seeded(n * lvl.size, 95 + i)) for i in range(2)]
+    us = [pin(oc.seeded(n * lvl.size, 97 + i)) for i in range(2)]
+    halo = pin(oc.seeded(lvl.n_velocity, 99))
+    want_y = [lvl.vmult_host(x, np.empty_like(x), n, halo) for x in xs]
+    want_u = [lvl.smooth_step_host(b, u.copy(), 0.8, n, halo, True) for b, u in zip(bs, us)]
+    ys = [pin(np.zeros_like(x)) for x in xs]
+    ua = [pin(u.copy()) for u in us]
+    for i in range(2):
+        lvl.vmult_host(xs[i], ys[i], n, halo, blocking=False)
+        lvl.smooth_step_host(bs[i], ua[i], 0.8, n, halo, True, blocking=False)
+    ctx.synchronize()
+    for i in range(2):
+        assert np.array_equal(ys[i], want_y[i])
+        assert np.array_equal(ua[i], want_u[i])
