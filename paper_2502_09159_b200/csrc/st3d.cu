@@ -477,6 +477,506 @@ vmult3_kernel(const Level3Consts P, const double *__restrict__ x, const double *
 #undef V3_FWD
 
 // ---------------------------------------------------------------------------
+// Deformed cells, two blocks per SM (vmult3d_kernel, default for r >= 2 on
+// deformed levels). Same lane = cell map, passes and fields as vmult3_kernel,
+// but phase 3 runs in three thread-local steps on the thread's own z-line
+// (which no other thread touches between the surrounding barriers), with the
+// shared-memory fields as the staging space instead of registers:
+//   3a z-contraction of the four y-pass fields, in place;
+//   3b point loop: geometry, gradients, fluxes, written back in place;
+//   3c transposed z-contraction, in place.
+// No per-point J^{-1}/det cache: the trilinear map is kept as its 8 monomial
+// coefficients per cell (X(xi) = sum_S c_S prod_{i in S} xi_i), so along a
+// z-line each Jacobian column is affine in zeta and costs 2 FMAs per entry.
+// 12 fields per cell (the divergence moments reuse field 9 once the z-flux
+// is consumed): 105 KB per 16-cell block at r = 2, two blocks (16 warps) per
+// SM, against one block (8 warps, 255 registers) for vmult3_kernel.
+template <int R>
+struct V3D
+{
+  static constexpr int N = R + 2, NN = N * N, NNN = N * N * N, p = R + 1;
+  static constexpr int NP = (R + 1) * (R + 2) * (R + 3) / 6;
+  static constexpr int CW = 16, LPW = 2, NWARP = (NN + 1) / 2, THREADS = 32 * NWARP;
+  static constexpr int NF = 12;
+  static constexpr int CELL = NF * NNN + NP + 24 + 1 - (NF * NNN + NP + 24) % 2; // odd
+  static constexpr size_t smem() { return sizeof(double) * (CW * CELL + (R + 1) * N + 2 * N); }
+  static constexpr int MINB = smem() <= 112 * 1024 ? 2 : 1;
+};
+
+/// Exponent d of P_r^disc mode m in 3D, in the order of modes3() (setup3d.cpp,
+/// pdisc.cpp:41-55): degree-major, then descending x, then descending y.
+/// Called with unrolled (constant) m, so it folds to a constant.
+__host__ __device__ constexpr int
+mode3_ex(int r, int m, int d)
+{
+  int i = 0;
+  for (int deg = 0; deg <= r; ++deg)
+    for (int a = deg; a >= 0; --a)
+      for (int b = deg - a; b >= 0; --b, ++i)
+        if (i == m)
+          return d == 0 ? a : (d == 1 ? b : deg - a - b);
+  return 0;
+}
+
+#define V3_FWD(M, in, o)                                                                                             \
+  _Pragma("unroll") for (int q_ = 0; q_ < N; ++q_)                                                                   \
+  {                                                                                                                  \
+    double s_ = 0.0;                                                                                                 \
+    _Pragma("unroll") for (int m_ = 0; m_ < N; ++m_) s_ = fma(P.M[q_ * N + m_], in[m_], s_);                         \
+    o[q_] = s_;                                                                                                      \
+  }
+
+template <int R, int S, int MODE>
+__global__ void __launch_bounds__(V3D<R>::THREADS, V3D<R>::MINB)
+vmult3d_kernel(const Level3Consts P, const double *__restrict__ x, const double *__restrict__ b,
+               double *__restrict__ y, const double *__restrict__ xprev0, int coupled, long long n_cells_total)
+{
+  using C = V3D<R>;
+  constexpr int N = C::N, NN = C::NN, NNN = C::NNN, p = C::p, NP = C::NP, CW = C::CW;
+  extern __shared__ __align__(16) double sm3[];
+  double *const lg = sm3 + CW * C::CELL; // Legendre L_e(x_q) at [e * N + q]
+  double *const tw = lg + (R + 1) * N;
+  double *const txq = tw + N;
+  for (int e = threadIdx.x; e < (R + 1) * N; e += C::THREADS)
+    lg[e] = P.leg[e];
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+    if (threadIdx.x == q)
+      {
+        tw[q] = P.w[q];
+        txq[q] = P.xq[q];
+      }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cl = lane % CW, t = warp * C::LPW + lane / CW; // cell in block, line index
+  const long long gc = static_cast<long long>(blockIdx.x) * CW + cl;
+  const bool active = gc < n_cells_total && t < NN;
+  const long long ncells = static_cast<long long>(P.nx) * P.ny * P.nz;
+  const int n = gc < n_cells_total ? static_cast<int>(gc / ncells) : 0;
+  const long long cell = gc < n_cells_total ? gc - n * ncells : 0;
+  const int cx = static_cast<int>(cell % P.nx), cy = static_cast<int>((cell / P.nx) % P.ny),
+            cz = static_cast<int>(cell / (static_cast<long long>(P.nx) * P.ny));
+  double *const F = sm3 + cl * C::CELL;
+  double *const PM = F + C::NF * NNN;
+  double *const CF = PM + NP; // trilinear map coefficients c_S[d] at CF[3 * S + d]
+  const int tA = t % N, tB = t / N;
+  const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
+  const int gx = P.gx, gy = P.gy;
+  const double *__restrict__ xn = x + n * isz;
+  const double *__restrict__ vprev = nullptr;
+  if (coupled)
+    vprev = n > 0 ? x + (n - 1) * isz + (S - 1) * mv : xprev0;
+  if (active)
+    for (int u = t; u < 24; u += NN)
+    {
+      // c_S[d] = 1/8 sum_v X_v[d] prod_{i in S} s_{v,i}, s_{v,i} = +-1 by vertex bit i
+      const int Sm = u / 3, d = u % 3;
+      double c = 0.0;
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        {
+          const int vx = cx + (v & 1), vy = cy + ((v >> 1) & 1), vz = cz + (v >> 2);
+          const double X = __ldg(P.verts + ((static_cast<long long>(vz) * (P.ny + 1) + vy) * (P.nx + 1) + vx) * 3 + d);
+          c += (__popc(v & Sm) & 1) ? -X : X;
+        }
+      // the sign above is prod_{i in S} s_{v,i} with s = -1 where bit i of v is 0: flip for |S| odd
+      CF[u] = 0.125 * ((__popc(Sm) & 1) ? -c : c);
+    }
+  auto fld = [&](int f) { return F + f * NNN; };
+  const int bx = (tB * N + tA) * N, by = tB * NN + tA, bz = tB * N + tA;
+  __syncthreads();
+
+  for (int a = 0; a < S; ++a)
+    {
+      double kt[S], mt[S], lva = 0.0;
+#pragma unroll
+      for (int aa = 0; aa < S; ++aa)
+        if (a == aa)
+          {
+#pragma unroll
+            for (int bs = 0; bs < S; ++bs)
+              {
+                kt[bs] = P.Kt[aa * S + bs];
+                mt[bs] = P.Mt[aa * S + bs];
+              }
+            lva = P.lv[aa];
+          }
+      // ---- phase 1 (x-lines): gather, temporal combination, x-contraction
+      if (active)
+        {
+          const int Y = cy * p + tA, Z = cz * p + tB;
+          const bool yzb = MODE != 2 && (Y == 0 || Z == P.zlo || Y == gy - 1 || Z == P.zhi);
+          const long long row = (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double uk[N], um[N], o[N];
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  const int X = cx * p + i;
+                  const bool bnd = yzb || (MODE != 2 && (X == 0 || X == gx - 1));
+                  double k_ = 0.0, m_ = 0.0;
+                  if (!bnd)
+#pragma unroll
+                    for (int bs = 0; bs < S; ++bs)
+                      {
+                        const double v = __ldg(xn + bs * mv + c * nsc + row + i);
+                        k_ = fma(kt[bs], v, k_);
+                        m_ = fma(mt[bs], v, m_);
+                      }
+                  if (vprev != nullptr)
+                    k_ = fma(-lva, __ldg(vprev + c * nsc + row + i), k_);
+                  uk[i] = k_;
+                  um[i] = m_;
+                }
+              V3_FWD(phi, uk, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(c)[bx + q] = o[q];
+              V3_FWD(phi, um, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(3 + c)[bx + q] = o[q];
+              V3_FWD(dphi, um, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(6 + c)[bx + q] = o[q];
+            }
+          if (t < NP)
+            {
+              double s = 0.0;
+#pragma unroll
+              for (int bs = 0; bs < S; ++bs)
+                s = fma(mt[bs], __ldg(xn + S * mv + bs * mp + cell * NP + t), s);
+              PM[t] = s;
+            }
+        }
+      __syncthreads();
+      // ---- phase 2 (y-lines, in place): VK; Ax -> AA (phi_y), AD (dphi_y, F[9+c]); Dx -> DA
+      if (active)
+        {
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], o[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(c)[by + m * N];
+              V3_FWD(phi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(c)[by + q * N] = o[q];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(3 + c)[by + m * N];
+              V3_FWD(phi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(3 + c)[by + q * N] = o[q];
+              V3_FWD(dphi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(9 + c)[by + q * N] = o[q];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fld(6 + c)[by + m * N];
+              V3_FWD(phi, in, o)
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                fld(6 + c)[by + q * N] = o[q];
+            }
+        }
+      __syncthreads();
+      // ---- phase 3 (z-lines, thread-local: no barrier between 3a, 3b, 3c)
+      if (active)
+        {
+          // 3a: F[c] -> vk_c, F[6+c] -> g_c0, F[9+c] -> g_c1 (phi_z); F[3+c] -> g_c2 (dphi_z).
+          // Rolled loops: unrolled, ptxas hoists every field's loads and spills.
+#pragma unroll 1
+          for (int f = 0; f < 12; ++f)
+            {
+              double in[N], o[N];
+              double *const fz = fld(f) + bz;
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                in[m] = fz[m * NN];
+              if (f >= 3 && f < 6)
+                {
+                  V3_FWD(dphi, in, o)
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    fz[q * NN] = o[q];
+                }
+              else
+                {
+                  V3_FWD(phi, in, o)
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    fz[q * NN] = o[q];
+                }
+            }
+          // 3b: per Gauss point (vk_c stays in F[c], its weight w det in wdq): Fr_c0 -> F[3+c], Fr_c1 -> F[6+c], Fr_c2 -> F[9+c]
+          const double xi = txq[tA], eta = txq[tB], wxy = tw[tA] * tw[tB];
+          double j0a[3], j0b[3], j1a[3], j1b[3], j2[3]; // J[:,0] = j0a + j0b zeta, J[:,1] = j1a + j1b zeta
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            {
+              j0a[d] = fma(CF[3 * 3 + d], eta, CF[3 * 1 + d]);
+              j0b[d] = fma(CF[3 * 7 + d], eta, CF[3 * 5 + d]);
+              j1a[d] = fma(CF[3 * 3 + d], xi, CF[3 * 2 + d]);
+              j1b[d] = fma(CF[3 * 7 + d], xi, CF[3 * 6 + d]);
+              j2[d] = fma(CF[3 * 7 + d], xi * eta, fma(CF[3 * 6 + d], eta, fma(CF[3 * 5 + d], xi, CF[3 * 4 + d])));
+            }
+          // pressure at the line's Gauss points: p(qz) = sum_e2 L_e2(z_qz) w2[e2],
+          // w2[e2] = sum over modes of z-degree e2 of L_e0(x_tA) L_e1(y_tB) PM[m]
+          double w2[R + 1], lx[R + 1], ly[R + 1];
+#pragma unroll
+          for (int e = 0; e <= R; ++e)
+            {
+              w2[e] = 0.0;
+              lx[e] = lg[e * N + tA];
+              ly[e] = lg[e * N + tB];
+            }
+#pragma unroll
+          for (int m = 0; m < NP; ++m)
+            {
+              double fx = 0.0, fy = 0.0; // selects, not indices: the arrays stay in registers
+#pragma unroll
+              for (int e = 0; e <= R; ++e)
+                {
+                  fx = mode3_ex(R, m, 0) == e ? lx[e] : fx;
+                  fy = mode3_ex(R, m, 1) == e ? ly[e] : fy;
+                }
+              const double v = fx * fy * PM[m];
+#pragma unroll
+              for (int e = 0; e <= R; ++e)
+                w2[e] += mode3_ex(R, m, 2) == e ? v : 0.0;
+            }
+          double qp[N], wdq[N];
+#pragma unroll 1
+          for (int qz = 0; qz < N; ++qz)
+            {
+              const int q = qz * NN + bz;
+              const double ze = P.xq[qz];
+              double J[3][3];
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+                {
+                  J[d][0] = fma(j0b[d], ze, j0a[d]);
+                  J[d][1] = fma(j1b[d], ze, j1a[d]);
+                  J[d][2] = j2[d];
+                }
+              const double a00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+              const double a10 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+              const double a20 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+              const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
+              const double id = 1.0 / det;
+              double Ji[3][3];
+              Ji[0][0] = a00 * id;
+              Ji[1][0] = a10 * id;
+              Ji[2][0] = a20 * id;
+              Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
+              Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
+              Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
+              Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
+              Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
+              Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
+              const double wd = P.w[qz] * wxy * det;
+              double G[3][3];
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                {
+                  const double g0 = fld(6 + c)[q], g1 = fld(9 + c)[q], g2 = fld(3 + c)[q];
+#pragma unroll
+                  for (int d = 0; d < 3; ++d)
+                    G[c][d] = g0 * Ji[0][d] + g1 * Ji[1][d] + g2 * Ji[2][d];
+                }
+              const double div = G[0][0] + G[1][1] + G[2][2];
+              double pq = 0.0;
+#pragma unroll
+              for (int e = 0; e <= R; ++e)
+                pq = fma(P.leg[e * N + qz], w2[e], pq);
+              const double diag = P.gamma * div - pq;
+#pragma unroll
+              for (int i = 0; i < N; ++i) // register-resident: select, no dynamic index
+                if (i == qz)
+                  {
+                    qp[i] = wd * div;
+                    wdq[i] = wd;
+                  }
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                {
+                  double Fp[3];
+#pragma unroll
+                  for (int d = 0; d < 3; ++d)
+                    Fp[d] = wd * (P.nu * G[c][d] + (c == d ? diag : 0.0));
+#pragma unroll
+                  for (int e = 0; e < 3; ++e)
+                    fld(3 * (e + 1) + c)[q] = Fp[0] * Ji[e][0] + Fp[1] * Ji[e][1] + Fp[2] * Ji[e][2];
+                }
+            }
+          // 3c: Sv_c = phi_z^T (w det vk_c) + dphi_z^T Fr_c2 -> F[c]; T0_c = phi_z^T Fr_c0 -> F[3+c];
+          // T1_c = phi_z^T Fr_c1 -> F[6+c]; then QP -> F[9]
+#pragma unroll 1
+          for (int c = 0; c < 3; ++c)
+            {
+              double fv[N], f2[N], o[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  fv[m] = wdq[m] * fld(c)[bz + m * NN];
+                  f2[m] = fld(9 + c)[bz + m * NN];
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s = fma(P.phi[q * N + i], fv[q], s);
+                      s = fma(P.dphi[q * N + i], f2[q], s);
+                    }
+                  o[i] = s;
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                fld(c)[bz + i * NN] = o[i];
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                {
+                  double in[N];
+#pragma unroll
+                  for (int m = 0; m < N; ++m)
+                    in[m] = fld(3 * (e + 1) + c)[bz + m * NN];
+#pragma unroll
+                  for (int i = 0; i < N; ++i)
+                    {
+                      double s = 0.0;
+#pragma unroll
+                      for (int q = 0; q < N; ++q)
+                        s = fma(P.phi[q * N + i], in[q], s);
+                      o[i] = s;
+                    }
+#pragma unroll
+                  for (int i = 0; i < N; ++i)
+                    fld(3 * (e + 1) + c)[bz + i * NN] = o[i];
+                }
+            }
+#pragma unroll
+          for (int i = 0; i < N; ++i)
+            fld(9)[bz + i * NN] = qp[i];
+        }
+      __syncthreads();
+      // ---- phase 4 (y-lines, in place): Ya_c = phi_y^T Sv_c + dphi_y^T T1_c (F[c]),
+      // Yb_c = phi_y^T T0_c (F[3+c]); pressure rows from QP (F[9])
+      if (active)
+        {
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], in2[N], in3[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  in[m] = fld(c)[by + m * N];
+                  in2[m] = fld(6 + c)[by + m * N];
+                  in3[m] = fld(3 + c)[by + m * N];
+                }
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s1 = fma(P.phi[q * N + i], in[q], s1);
+                      s1 = fma(P.dphi[q * N + i], in2[q], s1);
+                      s2 = fma(P.phi[q * N + i], in3[q], s2);
+                    }
+                  fld(c)[by + i * N] = s1;
+                  fld(3 + c)[by + i * N] = s2;
+                }
+            }
+          if (t < NP)
+            {
+              // separable: s = sum_qz L_e2(z) sum_qy L_e1(y) sum_qx L_e0(x) QP
+              const double *qpf = fld(9);
+              int e0 = 0, e1 = 0, e2 = 0;
+#pragma unroll
+              for (int m = 0; m < NP; ++m)
+                if (m == t)
+                  {
+                    e0 = mode3_ex(R, m, 0);
+                    e1 = mode3_ex(R, m, 1);
+                    e2 = mode3_ex(R, m, 2);
+                  }
+              double lxq[N];
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                lxq[q] = lg[e0 * N + q];
+              double s = 0.0;
+#pragma unroll
+              for (int qz = 0; qz < N; ++qz)
+                {
+                  double sy = 0.0;
+#pragma unroll
+                  for (int qy = 0; qy < N; ++qy)
+                    {
+                      double sx = 0.0;
+#pragma unroll
+                      for (int qx = 0; qx < N; ++qx)
+                        sx = fma(lxq[qx], qpf[(qz * N + qy) * N + qx], sx);
+                      sy = fma(lg[e1 * N + qy], sx, sy);
+                    }
+                  s = fma(lg[e2 * N + qz], sy, s);
+                }
+              const long long o = n * isz + S * mv + a * mp + cell * NP + t;
+              y[o] = MODE == 1 ? __ldg(b + o) - s : s;
+            }
+        }
+      __syncthreads();
+      // ---- phase 5 (x-lines): y = phi_x^T Ya + dphi_x^T Yb, scattered from registers
+      if (active)
+        {
+          const int Y = cy * p + tA, Z = cz * p + tB;
+          const bool yzb = Y == 0 || Z == P.zlo || Y == gy - 1 || Z == P.zhi;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            {
+              double in[N], in2[N];
+#pragma unroll
+              for (int m = 0; m < N; ++m)
+                {
+                  in[m] = fld(c)[bx + m];
+                  in2[m] = fld(3 + c)[bx + m];
+                }
+              double *yv = y + n * isz + a * mv + c * nsc + (static_cast<long long>(Z) * gy + Y) * gx + cx * p;
+#pragma unroll
+              for (int i = 0; i < N; ++i)
+                {
+                  double s = 0.0;
+#pragma unroll
+                  for (int q = 0; q < N; ++q)
+                    {
+                      s = fma(P.phi[q * N + i], in[q], s);
+                      s = fma(P.dphi[q * N + i], in2[q], s);
+                    }
+                  const int X = cx * p + i;
+                  const bool bnd = MODE != 2 && (yzb || X == 0 || X == gx - 1);
+                  if (!bnd)
+                    atomicAdd(yv + i, MODE == 1 ? -s : s);
+                }
+            }
+        }
+      // the next slot's phase 1 rewrites only this thread's own x-line of
+      // fields 0..8, which phase 5 alone read: no barrier here
+    }
+}
+#undef V3_FWD
+
+// ---------------------------------------------------------------------------
 // Line-per-thread variant (r = 1): N*N threads per cell, 16 cells per block,
 // 13 in-place fields; every pass reads / writes shared memory. At r = 1 it
 // keeps more warps resident than the lane-per-cell kernel below
@@ -1617,6 +2117,18 @@ launch_rs3_chunk(const Level3Consts &P, const double *x, const double *b, double
       const dim3 block(C::THREADS);
       const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
       const bool def = P.verts != nullptr;
+      if (def && std::getenv("STMG_V3_DEF_OLD") == nullptr)
+        {
+          using D = V3D<R>;
+          const unsigned gridd = static_cast<unsigned>((cells + D::CW - 1) / D::CW);
+          switch (mode)
+            {
+              case 0: go(vmult3_init_kernel<0>, vmult3d_kernel<R, S, 0>, dim3(D::THREADS), gridd, D::smem()); break;
+              case 1: go(vmult3_init_kernel<1>, vmult3d_kernel<R, S, 1>, dim3(D::THREADS), gridd, D::smem()); break;
+              default: go(vmult3_init_kernel<2>, vmult3d_kernel<R, S, 2>, dim3(D::THREADS), gridd, D::smem()); break;
+            }
+          return cudaGetLastError();
+        }
       switch (mode)
         {
           case 0:
