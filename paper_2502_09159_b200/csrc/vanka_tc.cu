@@ -465,6 +465,17 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
       red_add(p_ub + (cv + (s_dp[ci] & p_pm)), pacc[ct][b]);
   };
   int prev_phase = -1, transitions = 0;
+  // split phase barrier: a thread arrives once it scattered the last tile of
+  // a colour sub-phase and waits only right before its first scatter of the
+  // next one (that tile's DMMAs run in between), at most one outstanding
+  int wait_t = -1;
+  auto phase_wait = [&]() {
+    if (wait_t >= 0)
+      {
+        mbar_wait(pdone + (wait_t & 1), (wait_t >> 1) & 1);
+        wait_t = -1;
+      }
+  };
   for (int lt = 0; lt < nb; ++lt)
     {
       const int slot = lt % 3;
@@ -496,6 +507,11 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
       if (mine)
         {
           const double *bbase = ring + slot * kTSlot + (lane >> 2) * kTLd + (lane & 3);
+          // the previous tile's scatters ride in k-steps kS0.. of this tile
+#ifndef STMG_DFR_SC0
+#define STMG_DFR_SC0 4
+#endif
+          constexpr int kSc = 2 * (kTCols / 8), kS0 = KS >= STMG_DFR_SC0 + kSc ? STMG_DFR_SC0 : 0;
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk)
             {
@@ -504,27 +520,31 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
 #pragma unroll
               for (int ct = 0; ct < kTCols / 8; ++ct)
                 dmma(acc[ct], afr[kk], brow[kNStep * ct]);
-              if (kk < 2 * (kTCols / 8) && p_lt >= 0)
-                scatter_one(kk);
+              if (kk == kS0 && p_lt >= 0)
+                phase_wait();
+              if (kk >= kS0 && kk - kS0 < kSc && p_lt >= 0)
+                scatter_one(kk - kS0);
             }
-          if (KS < 2 * (kTCols / 8) && p_lt >= 0)
+          if (KS < kSc && p_lt >= 0)
 #pragma unroll
-            for (int j = KS; j < 2 * (kTCols / 8); ++j)
+            for (int j = KS; j < kSc; ++j)
               scatter_one(j);
         }
       else if (p_lt >= 0)
+        {
+          phase_wait();
 #pragma unroll
-        for (int j = 0; j < 2 * (kTCols / 8); ++j)
-          scatter_one(j);
+          for (int j = 0; j < 2 * (kTCols / 8); ++j)
+            scatter_one(j);
+        }
       mbar_arrive(empty + slot);
       // the previous tile's scatters are done: a new colour sub-phase may
-      // start scattering only after every thread got here (deterministic order)
+      // start scattering only once every thread got here (deterministic order)
       if (prev_phase >= 0 && tl.phase != prev_phase)
         {
-          unsigned long long *pd = pdone + (transitions & 1);
-          mbar_arrive(pd);
-          mbar_wait(pd, (transitions >> 1) & 1);
-          ++transitions;
+          phase_wait();
+          mbar_arrive(pdone + (transitions & 1));
+          wait_t = transitions++;
         }
       prev_phase = tl.phase;
       p_lt = (tl.ncols > 0 && c_ok) ? lt : -1;
@@ -546,9 +566,12 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
         }
     }
   if (p_lt >= 0)
+    {
+      phase_wait();
 #pragma unroll
-    for (int j = 0; j < 2 * (kTCols / 8); ++j)
-      scatter_one(j);
+      for (int j = 0; j < 2 * (kTCols / 8); ++j)
+        scatter_one(j);
+    }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
