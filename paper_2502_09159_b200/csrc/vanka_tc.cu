@@ -50,8 +50,12 @@ constexpr int kTSlot = kTCols * kTLd;
 #endif
 constexpr int kTMaxTiles = STMG_VANKA_MAXTILES; // tiles per block (host falls back beyond)
 constexpr int kTRing = 3; // ring slots of the full/empty mbarrier pipeline (vanka_tc_kernel)
-constexpr size_t kDSmem = sizeof(double) * kTRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * 12) +
-                          8 * sizeof(unsigned long long); // vanka_dfr_kernel
+#ifndef STMG_DFR_RING
+#define STMG_DFR_RING 3 // measured: 4 slots 4.66 vs 4.56 ms (the larger ring takes L1 from the gathers)
+#endif
+constexpr int kDRing = STMG_DFR_RING; // vanka_dfr_kernel: ring slots; tiles gathered kDRing - 1 ahead
+constexpr size_t kDSmem = sizeof(double) * kDRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * 12) +
+                          (2 * kDRing + 2) * sizeof(unsigned long long); // vanka_dfr_kernel
 constexpr size_t kTSmem =
   sizeof(double) * kTRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4)) + 8 * sizeof(unsigned long long);
 
@@ -358,7 +362,7 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
                  double omega)
 {
   extern __shared__ __align__(16) double ring[];
-  long long *s_colv = reinterpret_cast<long long *>(ring + kTRing * kTSlot);
+  long long *s_colv = reinterpret_cast<long long *>(ring + kDRing * kTSlot);
   int *s_dp = reinterpret_cast<int *>(s_colv + kTMaxTiles * kTCols);
   VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_dp + kTMaxTiles * kTCols);
   unsigned long long *s_bar = reinterpret_cast<unsigned long long *>(s_tile + kTMaxTiles);
@@ -429,10 +433,10 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
           }
       }
   };
-  unsigned long long *full = s_bar, *empty = s_bar + 3, *pdone = s_bar + 6;
+  unsigned long long *full = s_bar, *empty = s_bar + kDRing, *pdone = s_bar + 2 * kDRing;
   if (tid == 0)
     {
-      for (int i = 0; i < 3; ++i)
+      for (int i = 0; i < kDRing; ++i)
         {
           mbar_init(full + i, kTThreads);
           mbar_init(empty + i, kTThreads);
@@ -442,10 +446,11 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
     }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
-  issue(0, 0);
-  cp_async_mbar_arrive(full + 0);
-  issue(1, 1);
-  cp_async_mbar_arrive(full + 1);
+  for (int i = 0; i < kDRing - 1; ++i)
+    {
+      issue(i, i);
+      cp_async_mbar_arrive(full + i);
+    }
 
   int loaded = -1, nt_loaded = 0;
   double afr[KS];
@@ -478,8 +483,8 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
   };
   for (int lt = 0; lt < nb; ++lt)
     {
-      const int slot = lt % 3;
-      mbar_wait(full + slot, (lt / 3) & 1);
+      const int slot = lt % kDRing;
+      mbar_wait(full + slot, (lt / kDRing) & 1);
       const VankaTile tl = s_tile[lt];
       double acc[kTCols / 8][2];
 #pragma unroll
@@ -556,12 +561,12 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
         }
       p_ub = c_ub;
       p_pm = c_pm;
-      if (lt + 2 < nb)
+      if (lt + kDRing - 1 < nb)
         {
-          const int ns = (lt + 2) % 3;
+          const int ns = (lt + kDRing - 1) % kDRing;
           if (lt >= 1)
-            mbar_wait(empty + ns, ((lt - 1) / 3) & 1);
-          issue(lt + 2, ns);
+            mbar_wait(empty + ns, ((lt - 1) / kDRing) & 1);
+          issue(lt + kDRing - 1, ns);
           cp_async_mbar_arrive(full + ns);
         }
     }
