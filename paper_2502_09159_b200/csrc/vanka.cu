@@ -517,7 +517,24 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 #ifndef STMG_FAC_L2AHEAD
 #define STMG_FAC_L2AHEAD 0 // >0: L2 prefetch of the chunk this far ahead (measured: no gain)
 #endif
-constexpr int kFCols = 16, kFLd = 20, kFThreads = 512, kFSlots = 4, kFChunkCols = 8;
+#ifndef STMG_FAC_SLOTS
+#define STMG_FAC_SLOTS 4
+#endif
+#ifndef STMG_FAC_SWZ
+#define STMG_FAC_SWZ 0
+#endif
+// T / Y tile: 16 interval columns per row, pitch 20 (conflict-free DMMA
+// B-fragment loads). STMG_FAC_SWZ=1: pitch 16 with the column XORed by 8 on
+// odd rows (also two wavefronts), which frees shared memory for a fifth ring
+// slot: measured 15.98 ms (5 slots) / 16.55 ms (4 slots) against 15.97 ms,
+// so neither the bytes in flight nor the pitch limit the block stream.
+constexpr int kFCols = 16, kFLd = STMG_FAC_SWZ ? 16 : 20, kFThreads = 512, kFSlots = STMG_FAC_SLOTS,
+              kFChunkCols = 8;
+__device__ __forceinline__ int
+tsw(int row, int col)
+{
+  return row * kFLd + (STMG_FAC_SWZ ? (col ^ ((row & 1) << 3)) : col);
+}
 constexpr int kFTiles = 4;       // row tiles per warp and block: 16 * 4 * 8 = 512 rows
 
 __device__ __forceinline__ unsigned
@@ -540,8 +557,7 @@ fac_chunk(double (&acc)[kFTiles][2][2], const double *__restrict__ A, const doub
       if (kFChunkCols * kc + 4 * kk >= m)
         break;
       const int kr = kFChunkCols * kc + 4 * kk + (lane & 3); // column of B^{-1} = row of T_b
-      const double *brow = Ts + (boff + kr) * kFLd + (lane >> 2);
-      const double b0 = brow[0], b1 = brow[8];
+      const double b0 = Ts[tsw(boff + kr, lane >> 2)], b1 = Ts[tsw(boff + kr, (lane >> 2) + 8)];
       const int jl = 4 * kk + (lane & 3);
       double a[NT];
 #pragma unroll
@@ -725,30 +741,48 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
           __syncthreads();
           // T = (W (x) I) R straight from the gather: thread (j, c) loads the S
           // slot values of spatial dof j in interval column c
-          for (int e = tid; e < nrow * kFCols; e += kFThreads)
+#ifndef STMG_FAC_GBATCH
+#define STMG_FAC_GBATCH 4
+#endif
+          // batches of GB elements per thread: all their loads are in flight
+          // before the first W-mix (one latency per batch, not per element)
+          constexpr int GB = STMG_FAC_GBATCH;
+          for (int e0 = tid; e0 < nrow * kFCols; e0 += GB * kFThreads)
             {
-              const int c = e / nrow, j = e - c * nrow; // consecutive threads: consecutive dofs of a column
-              if (j < ns)
+              double rb[GB][kMaxS];
+#pragma unroll
+              for (int u = 0; u < GB; ++u)
                 {
-                  double rb[kMaxS];
+                  const int e = e0 + u * kFThreads;
+                  const int c = e / nrow, j = e - c * nrow; // consecutive threads: consecutive dofs of a column
+                  const bool ld = e < nrow * kFCols && j < ns && c < ng;
 #pragma unroll
                   for (int b = 0; b < kMaxS; ++b)
                     {
-                      const int row = b < S ? prow(b, j) : 0;
-                      rb[b] = (b < S && c < ng) ? __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]) : 0.0;
-                    }
-                  for (int i = 0; i < S; ++i)
-                    {
-                      double t = 0.0;
-#pragma unroll
-                      for (int b = 0; b < kMaxS; ++b)
-                        if (b < S)
-                          t = fma(F.W[i * S + b], rb[b], t);
-                      Ts[frow(i, j) * kFLd + c] = t;
+                      const int row = (ld && b < S) ? prow(b, j) : 0;
+                      rb[u][b] = (ld && b < S) ? __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]) : 0.0;
                     }
                 }
-              else if (j - ns < nrow - nt)
-                Ts[(nt + (j - ns)) * kFLd + c] = 0.0; // padding rows past nt
+#pragma unroll
+              for (int u = 0; u < GB; ++u)
+                {
+                  const int e = e0 + u * kFThreads;
+                  if (e >= nrow * kFCols)
+                    break;
+                  const int c = e / nrow, j = e - c * nrow;
+                  if (j < ns)
+                    for (int i = 0; i < S; ++i)
+                      {
+                        double t = 0.0;
+#pragma unroll
+                        for (int b = 0; b < kMaxS; ++b)
+                          if (b < S)
+                            t = fma(F.W[i * S + b], rb[u][b], t);
+                        Ts[tsw(frow(i, j), c)] = t;
+                      }
+                  else if (j - ns < nrow - nt)
+                    Ts[tsw(nt + (j - ns), c)] = 0.0; // padding rows past nt
+                }
             }
           __syncthreads();
           double acc[2][kFTiles][2][2];
@@ -789,7 +823,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
                       for (int ct = 0; ct < 2; ++ct)
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
-                          Ts[(boff + row) * kFLd + 8 * ct + 2 * (lane & 3) + h] = acc[b][t][ct][h];
+                          Ts[tsw(boff + row, 8 * ct + 2 * (lane & 3) + h)] = acc[b][t][ct][h];
                   }
               }
           __syncthreads();
@@ -802,7 +836,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
               double y[kMaxS];
 #pragma unroll
               for (int i = 0; i < kMaxS; ++i)
-                y[i] = i < S ? Ts[frow(i, j) * kFLd + c] : 0.0;
+                y[i] = i < S ? Ts[tsw(frow(i, j), c)] : 0.0;
               for (int a = 0; a < S; ++a)
                 {
                   double z = 0.0;
