@@ -535,7 +535,7 @@ tsw(int row, int col)
 {
   return row * kFLd + (STMG_FAC_SWZ ? (col ^ ((row & 1) << 3)) : col);
 }
-constexpr int kFTiles = 4;       // row tiles per warp and block: 16 * 4 * 8 = 512 rows
+constexpr int kFTiles = 2; // row tiles per warp and block: n_s <= 16 * 2 * 8 = 256 spatial patch dofs
 
 __device__ __forceinline__ unsigned
 f_smem(const void *p)
@@ -543,29 +543,33 @@ f_smem(const void *p)
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-// One chunk (8 columns of B_b^{-1} = 2 DMMA k-steps) for the NT row tiles a
-// warp owns in block b: all A fragments of a k-step are loaded before its
-// DMMAs (no per-tile branch: NT is uniform per warp and block).
+// T / Y rows: eigen-component i of spatial patch dof j at row i * nsp + j,
+// nsp = n_s rounded up to 8 with zero rows, so the k-steps of a block's last
+// chunk read zeros past n_s and no DMMA operand needs a predicate (the ring
+// slots only ever hold finite inverse entries).
+__device__ __forceinline__ int
+f_nsp(int ns)
+{
+  return (ns + 7) & ~7;
+}
+
+// Real-eigenvalue block: one chunk = 8 columns of B^{-1} (column-major, m
+// rows each); tile t of the warp reads rows abase[t] (lane's column folded
+// in). Rows past n_s read neighbouring ring data and are never written out.
 template <int NT>
 __device__ __forceinline__ void
-fac_chunk(double (&acc)[kFTiles][2][2], const double *__restrict__ A, const double *__restrict__ Ts, int m, int boff,
-          int kc, int warp, int lane)
+fac_real_chunk(double (&acc)[kFTiles][2][2], const double *__restrict__ A, const double *__restrict__ Ts, int m,
+               int trow, const int (&abase)[kFTiles], int lane)
 {
 #pragma unroll
   for (int kk = 0; kk < kFChunkCols / 4; ++kk)
     {
-      if (kFChunkCols * kc + 4 * kk >= m)
-        break;
-      const int kr = kFChunkCols * kc + 4 * kk + (lane & 3); // column of B^{-1} = row of T_b
-      const double b0 = Ts[tsw(boff + kr, lane >> 2)], b1 = Ts[tsw(boff + kr, (lane >> 2) + 8)];
-      const int jl = 4 * kk + (lane & 3);
+      const int kr = trow + 4 * kk + (lane & 3);
+      const double b0 = Ts[tsw(kr, lane >> 2)], b1 = Ts[tsw(kr, (lane >> 2) + 8)];
       double a[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t)
-        {
-          const int row = 8 * (warp + 16 * t) + (lane >> 2);
-          a[t] = (row < m && kr < m) ? A[jl * m + row] : 0.0;
-        }
+        a[t] = A[abase[t] + 4 * kk * m];
 #pragma unroll
       for (int t = 0; t < NT; ++t)
         {
@@ -575,25 +579,57 @@ fac_chunk(double (&acc)[kFTiles][2][2], const double *__restrict__ A, const doub
     }
 }
 
+// Complex-pair block [[X, bM], [-bM, X]] = real form of Z = X - i b M. Its
+// inverse is the real form [[P, -Q], [Q, P]] of Z^{-1} = P + iQ, so the
+// u-columns [P; Q] alone (half the block) give
+//   Y_u = P T_u - Q T_v,   Y_v = Q T_u + P T_v.
+// One chunk = 8 u-columns (2 n_s rows each, stored order); tile t of the warp
+// owns natural row r of both halves: P row at abu[t], Q row at abv[t].
+template <int NT>
 __device__ __forceinline__ void
-fac_chunk_n(int nt_w, double (&acc)[kFTiles][2][2], const double *A, const double *Ts, int m, int boff, int kc,
-            int warp, int lane)
+fac_pair_chunk(double (&acc)[kFTiles][2][2][2], const double *__restrict__ A, const double *__restrict__ Ts, int m1,
+               int tu, int tv, const int (&abu)[kFTiles], const int (&abv)[kFTiles], int lane)
 {
-  switch (nt_w)
+#pragma unroll
+  for (int kk = 0; kk < kFChunkCols / 4; ++kk)
     {
-      case 1: fac_chunk<1>(acc, A, Ts, m, boff, kc, warp, lane); break;
-      case 2: fac_chunk<2>(acc, A, Ts, m, boff, kc, warp, lane); break;
-      case 3: fac_chunk<3>(acc, A, Ts, m, boff, kc, warp, lane); break;
-      case 4: fac_chunk<4>(acc, A, Ts, m, boff, kc, warp, lane); break;
-      default: break;
+      const int kr = 4 * kk + (lane & 3);
+      const double bu0 = Ts[tsw(tu + kr, lane >> 2)], bu1 = Ts[tsw(tu + kr, (lane >> 2) + 8)];
+      const double bv0 = Ts[tsw(tv + kr, lane >> 2)], bv1 = Ts[tsw(tv + kr, (lane >> 2) + 8)];
+      const double nv0 = -bv0, nv1 = -bv1;
+      double au[NT], av[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        {
+          au[t] = A[abu[t] + 4 * kk * m1];
+          av[t] = A[abv[t] + 4 * kk * m1];
+        }
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        {
+          dmma_8x8x4(acc[t][0][0], au[t], bu0);
+          dmma_8x8x4(acc[t][0][1], au[t], bu1);
+          dmma_8x8x4(acc[t][1][0], av[t], bu0);
+          dmma_8x8x4(acc[t][1][1], av[t], bu1);
+        }
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        {
+          dmma_8x8x4(acc[t][0][0], av[t], nv0);
+          dmma_8x8x4(acc[t][0][1], av[t], nv1);
+          dmma_8x8x4(acc[t][1][0], au[t], bv0);
+          dmma_8x8x4(acc[t][1][1], au[t], bv1);
+        }
     }
 }
 
-// Per-patch constants of the stream (the blocks of one cell patch).
+// Per-patch constants of the stream (the blocks of one cell patch). Block b
+// streams nch[b] chunks of kFChunkCols columns, each column m[b] doubles.
 struct FacItem
 {
   const double *inv; // column-major blocks, block 1 at inv + moff1
-  int nt, nvel, ns, nch0, nch1, moff1;
+  int nt, nvel, ns, nvs, moff1;
+  int nch[2], m[2];
 };
 
 __device__ __forceinline__ FacItem
@@ -604,11 +640,23 @@ fac_item(const DevPatchClass &pc, const Fac3Params &F)
   it.nt = pc.n_t;
   it.nvel = pc.n_vel;
   it.ns = pc.n_t / F.S;
-  const int m0 = F.sz[0] * it.ns, m1 = F.nb > 1 ? F.sz[1] * it.ns : 0;
-  it.nch0 = (m0 + kFChunkCols - 1) / kFChunkCols;
-  it.nch1 = (m1 + kFChunkCols - 1) / kFChunkCols;
-  it.moff1 = (m0 * m0 + 8 + 1) / 2 * 2;
+  it.nvs = pc.n_vel / F.S;
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+    {
+      it.m[b] = b < F.nb ? F.sz[b] * it.ns : 0;
+      it.nch[b] = b < F.nb ? (it.ns + kFChunkCols - 1) / kFChunkCols : 0; // pair: the n_s u-columns only
+    }
+  it.moff1 = (it.m[0] * it.m[0] + 8 + 1) / 2 * 2;
   return it;
+}
+
+// Stored row of natural row r (< n_s) of half h of a pair block: the setup
+// (patch3_fac_assemble_kernel) orders a pair block [vel_u, vel_v, p_u, p_v].
+__device__ __forceinline__ int
+fac_pair_row(int h, int r, int nvs, int nps)
+{
+  return r < nvs ? h * nvs + r : 2 * nvs + h * nps + (r - nvs);
 }
 
 // Persistent: CTA x walks the batches x, x + gridDim.x, ... of the colour.
@@ -623,12 +671,12 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
 {
   extern __shared__ __align__(16) double fsm[];
   const int S = F.S;
-  const int nrow_max = (max_nt + 3) / 4 * 4 + 4;
+  const int nrow_max = S * f_nsp(max_nt / S);
   const int slot_d = kFChunkCols * max_m; // doubles per ring slot
   double *Rs = fsm;                       // the chunk ring
   double *Ts = fsm + kFSlots * slot_d;    // nrow x kFLd: T, later Y
   double *s_w = Ts + nrow_max * kFLd;     // nt
-  long long *cvb = reinterpret_cast<long long *>(s_w + nrow_max);
+  long long *cvb = reinterpret_cast<long long *>(s_w + (max_nt + 1) / 2 * 2);
   long long *cpb = cvb + kFCols;
   unsigned long long *full = reinterpret_cast<unsigned long long *>(cpb + kFCols), *empty = full + kFSlots;
   int *s_rel = reinterpret_cast<int *>(empty + kFSlots);
@@ -648,6 +696,12 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
                  "r"(parity)
                  : "memory");
   };
+  auto bulk = [&](double *dst, const double *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   f_smem(dst)),
+                 "l"(src), "r"(bytes), "r"(f_smem(bar))
+                 : "memory");
+  };
   // ---- producer (thread 0): cursor over (batch, patch, chunk) of this CTA
   int p_bi = blockIdx.x, p_pi = 0, p_q = 0;
   unsigned p_g = 0; // chunks issued
@@ -661,36 +715,37 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
     const int slot = p_g % kFSlots;
     if (p_g >= kFSlots)
       wait(empty + slot, ((p_g / kFSlots) - 1) & 1); // the consumers released the slot's previous chunk
-    const bool b1 = p_q >= p_it.nch0;
-    const int kc = b1 ? p_q - p_it.nch0 : p_q;
-    const int m = F.sz[b1 ? 1 : 0] * p_it.ns, cols = min(kFChunkCols, m - kFChunkCols * kc);
-    const double *src = p_it.inv + (b1 ? p_it.moff1 : 0) + static_cast<long long>(kFChunkCols * kc) * m;
-    const unsigned bytes = static_cast<unsigned>((cols * m * sizeof(double) + 15) & ~size_t(15));
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(f_smem(full + slot)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   f_smem(Rs + slot * slot_d)),
-                 "l"(src), "r"(bytes), "r"(f_smem(full + slot))
-                 : "memory");
-#if STMG_FAC_L2AHEAD > 0
-    {
-      // the ring holds kFSlots chunks; the chunk STMG_FAC_L2AHEAD further is
-      // pulled into L2 now, so its bulk copy later hits L2
-      const int qa = p_q + STMG_FAC_L2AHEAD;
-      if (qa < p_it.nch0 + p_it.nch1)
-        {
-          const bool ba = qa >= p_it.nch0;
-          const int kca = ba ? qa - p_it.nch0 : qa;
-          const int ma = F.sz[ba ? 1 : 0] * p_it.ns, colsa = min(kFChunkCols, ma - kFChunkCols * kca);
-          const double *pa = p_it.inv + (ba ? p_it.moff1 : 0) + static_cast<long long>(kFChunkCols * kca) * ma;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(pa),
-                       "r"(static_cast<unsigned>((colsa * ma * sizeof(double)) & ~size_t(15)))
-                       : "memory");
-        }
-    }
-#endif
+    const int b = p_q >= p_it.nch[0] ? 1 : 0;
+    const int kc = b ? p_q - p_it.nch[0] : p_q;
+    const int m = b ? p_it.m[1] : p_it.m[0], k0 = kFChunkCols * kc, k1 = min(k0 + kFChunkCols, p_it.ns);
+    const double *blk = p_it.inv + (b ? p_it.moff1 : 0);
+    double *dst = Rs + slot * slot_d;
+    if ((b ? F.sz[1] : F.sz[0]) == 1)
+      {
+        const unsigned bytes = static_cast<unsigned>(((k1 - k0) * m * sizeof(double) + 15) & ~size_t(15));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(f_smem(full + slot)),
+                     "r"(bytes)
+                     : "memory");
+        bulk(dst, blk + static_cast<long long>(k0) * m, bytes, full + slot);
+      }
+    else
+      {
+        // u-columns k0..k1 of the pair block: velocity columns keep their
+        // index, pressure column nvs + l sits at 2 nvs + l (m = 2 n_s is even:
+        // every column starts 16-byte aligned)
+        const int kv = min(k1, p_it.nvs);
+        const unsigned cb = static_cast<unsigned>(m * sizeof(double));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(f_smem(full + slot)),
+                     "r"((k1 - k0) * cb)
+                     : "memory");
+        if (kv > k0)
+          bulk(dst, blk + static_cast<long long>(k0) * m, (kv - k0) * cb, full + slot);
+        const int kp = max(k0, p_it.nvs);
+        if (k1 > kp)
+          bulk(dst + (kp - k0) * m, blk + static_cast<long long>(kp + p_it.nvs) * m, (k1 - kp) * cb, full + slot);
+      }
     ++p_g;
-    if (++p_q == p_it.nch0 + p_it.nch1)
+    if (++p_q == p_it.nch[0] + p_it.nch[1])
       {
         p_q = 0;
         if (++p_pi == batches[p_bi].count)
@@ -713,17 +768,21 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
       const VankaBatch bt = batches[bi];
       const DevPatchClass pc = classes[bt.cls];
       const FacItem it = fac_item(pc, F);
-      const int nt = it.nt, nvel = it.nvel, ns = it.ns, nvs = nvel / S, nps = ns - nvs;
-      const int nrow = (nt + 3) / 4 * 4 + 4;
+      const int nt = it.nt, nvel = it.nvel, ns = it.ns, nvs = it.nvs, nps = ns - nvs, nsp = f_nsp(ns);
       auto prow = [&](int a, int j) { return j < nvs ? a * nvs + j : S * nvs + a * nps + (j - nvs); };
-      auto frow = [&](int i, int j) {
-        int b = 0;
-        while (b + 1 < F.nb && i >= F.c0[b + 1])
-          ++b;
-        const int bi2 = i - F.c0[b], o = F.c0[b] * ns;
-        return j < nvs ? o + bi2 * nvs + j : o + F.sz[b] * nvs + bi2 * nps + (j - nvs);
-      };
-      const int nchunks = it.nch0 + it.nch1;
+      const int nchunks = it.nch[0] + it.nch[1];
+      // this warp's row tiles (same for every block: all blocks have n_s rows
+      // per half) and their stored rows, lane's chunk column folded in
+      const int rt = (ns + 7) / 8, nt_w = warp < rt ? (rt - warp + 15) / 16 : 0;
+      int abr[kFTiles], abu[kFTiles], abv[kFTiles];
+#pragma unroll
+      for (int t = 0; t < kFTiles; ++t)
+        {
+          const int row = 8 * (warp + 16 * t) + (lane >> 2);
+          abr[t] = (lane & 3) * ns + row;
+          abu[t] = (lane & 3) * (2 * ns) + fac_pair_row(0, row, nvs, nps);
+          abv[t] = (lane & 3) * (2 * ns) + fac_pair_row(1, row, nvs, nps);
+        }
       for (int pi = 0; pi < bt.count; ++pi)
         {
           const int patch = bt.first + pi;
@@ -747,83 +806,101 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
           // batches of GB elements per thread: all their loads are in flight
           // before the first W-mix (one latency per batch, not per element)
           constexpr int GB = STMG_FAC_GBATCH;
-          for (int e0 = tid; e0 < nrow * kFCols; e0 += GB * kFThreads)
+          for (int e0 = tid; e0 < nsp * kFCols; e0 += GB * kFThreads)
             {
               double rb[GB][kMaxS];
 #pragma unroll
-              for (int u = 0; u < GB; ++u)
+              for (int q = 0; q < GB; ++q)
                 {
-                  const int e = e0 + u * kFThreads;
-                  const int c = e / nrow, j = e - c * nrow; // consecutive threads: consecutive dofs of a column
-                  const bool ld = e < nrow * kFCols && j < ns && c < ng;
+                  const int e = e0 + q * kFThreads;
+                  const int c = e / nsp, j = e - c * nsp; // consecutive threads: consecutive dofs of a column
+                  const bool ld = e < nsp * kFCols && j < ns && c < ng;
 #pragma unroll
                   for (int b = 0; b < kMaxS; ++b)
                     {
                       const int row = (ld && b < S) ? prow(b, j) : 0;
-                      rb[u][b] = (ld && b < S) ? __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]) : 0.0;
+                      rb[q][b] = (ld && b < S) ? __ldg(r + (row < nvel ? cvb[c] : cpb[c]) + s_rel[row]) : 0.0;
                     }
                 }
 #pragma unroll
-              for (int u = 0; u < GB; ++u)
+              for (int q = 0; q < GB; ++q)
                 {
-                  const int e = e0 + u * kFThreads;
-                  if (e >= nrow * kFCols)
+                  const int e = e0 + q * kFThreads;
+                  if (e >= nsp * kFCols)
                     break;
-                  const int c = e / nrow, j = e - c * nrow;
-                  if (j < ns)
-                    for (int i = 0; i < S; ++i)
-                      {
-                        double t = 0.0;
+                  const int c = e / nsp, j = e - c * nsp;
+                  for (int i = 0; i < S; ++i)
+                    {
+                      double t = 0.0;
 #pragma unroll
-                        for (int b = 0; b < kMaxS; ++b)
-                          if (b < S)
-                            t = fma(F.W[i * S + b], rb[u][b], t);
-                        Ts[tsw(frow(i, j), c)] = t;
-                      }
-                  else if (j - ns < nrow - nt)
-                    Ts[tsw(nt + (j - ns), c)] = 0.0; // padding rows past nt
+                      for (int b = 0; b < kMaxS; ++b)
+                        if (b < S)
+                          t = fma(F.W[i * S + b], rb[q][b], t);
+                      Ts[tsw(i * nsp + j, c)] = t; // rows j >= n_s: zeros
+                    }
                 }
             }
           __syncthreads();
-          double acc[2][kFTiles][2][2];
+          double accr[kFTiles][2][2], accp[kFTiles][2][2][2];
 #pragma unroll
-          for (int b = 0; b < 2; ++b)
+          for (int t = 0; t < kFTiles; ++t)
 #pragma unroll
-            for (int t = 0; t < kFTiles; ++t)
-              acc[b][t][0][0] = acc[b][t][0][1] = acc[b][t][1][0] = acc[b][t][1][1] = 0.0;
+            for (int h = 0; h < 2; ++h)
+              {
+                accr[t][h][0] = accr[t][h][1] = 0.0;
+                accp[t][0][h][0] = accp[t][0][h][1] = accp[t][1][h][0] = accp[t][1][h][1] = 0.0;
+              }
           for (int q = 0; q < nchunks; ++q, ++g)
             {
               const int slot = g % kFSlots;
               wait(full + slot, (g / kFSlots) & 1);
-              const int b = q < it.nch0 ? 0 : 1, kc = q < it.nch0 ? q : q - it.nch0;
-              const int m = F.sz[b] * ns, boff = F.c0[b] * ns, rt = (m + 7) / 8;
-              const int nt_w = warp < rt ? (rt - warp + 15) / 16 : 0; // row tiles of this warp in block b
-              const double *A = Rs + slot * slot_d; // column j of B_b^{-1} (chunk-local) at j * m
-              if (b == 0)
-                fac_chunk_n(nt_w, acc[0], A, Ts, m, boff, kc, warp, lane);
+              const int b = q < it.nch[0] ? 0 : 1, kc = b ? q - it.nch[0] : q;
+              const int trow = (b ? F.c0[1] : F.c0[0]) * nsp + kFChunkCols * kc; // T row of the chunk's first column
+              const double *A = Rs + slot * slot_d;
+              if ((b ? F.sz[1] : F.sz[0]) == 1)
+                {
+                  if (nt_w == 2)
+                    fac_real_chunk<2>(accr, A, Ts, ns, trow, abr, lane);
+                  else if (nt_w == 1)
+                    fac_real_chunk<1>(accr, A, Ts, ns, trow, abr, lane);
+                }
               else
-                fac_chunk_n(nt_w, acc[1], A, Ts, m, boff, kc, warp, lane);
+                {
+                  if (nt_w == 2)
+                    fac_pair_chunk<2>(accp, A, Ts, 2 * ns, trow, trow + nsp, abu, abv, lane);
+                  else if (nt_w == 1)
+                    fac_pair_chunk<1>(accp, A, Ts, 2 * ns, trow, trow + nsp, abu, abv, lane);
+                }
               asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(f_smem(empty + slot)) : "memory");
               if (tid == 0)
                 issue_next(); // refills this slot -- possibly with the next patch's first chunks
             }
           __syncthreads(); // every warp is done with T
-          // Y (factored order) into the T space
+          // Y into the T rows of its block
 #pragma unroll
           for (int b = 0; b < 2; ++b)
             if (b < F.nb)
               {
-                const int m = F.sz[b] * ns, boff = F.c0[b] * ns;
+                const int t0 = F.c0[b] * nsp;
 #pragma unroll
                 for (int t = 0; t < kFTiles; ++t)
                   {
                     const int row = 8 * (warp + 16 * t) + (lane >> 2);
-                    if (row < m)
+                    if (row < ns)
 #pragma unroll
                       for (int ct = 0; ct < 2; ++ct)
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
-                          Ts[tsw(boff + row, 8 * ct + 2 * (lane & 3) + h)] = acc[b][t][ct][h];
+                          {
+                            const int col = 8 * ct + 2 * (lane & 3) + h;
+                            if (F.sz[b] == 1)
+                              Ts[tsw(t0 + row, col)] = accr[t][ct][h];
+                            else
+                              {
+                                Ts[tsw(t0 + row, col)] = accp[t][0][ct][h];
+                                Ts[tsw(t0 + nsp + row, col)] = accp[t][1][ct][h];
+                              }
+                          }
                   }
               }
           __syncthreads();
@@ -836,7 +913,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
               double y[kMaxS];
 #pragma unroll
               for (int i = 0; i < kMaxS; ++i)
-                y[i] = i < S ? Ts[tsw(frow(i, j), c)] : 0.0;
+                y[i] = i < S ? Ts[tsw(i * nsp + j, c)] : 0.0;
               for (int a = 0; a < S; ++a)
                 {
                   double z = 0.0;
@@ -897,15 +974,20 @@ launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, in
 {
   if (n_batches == 0 || n_intervals == 0)
     return cudaSuccess;
-  const int nrow = (max_nt + 3) / 4 * 4 + 4;
+  const int ns_max = max_nt / F.S, nrow = F.S * ((ns_max + 7) & ~7);
   int max_m = 0;
   for (int b = 0; b < F.nb; ++b)
-    max_m = std::max(max_m, F.sz[b] * (max_nt / F.S));
-  if (F.nb > 2 || max_m > 16 * kFTiles * 8)
+    {
+      if (F.sz[b] < 1 || F.sz[b] > 2)
+        return cudaErrorInvalidValue;
+      max_m = std::max(max_m, F.sz[b] * ns_max);
+    }
+  if (F.nb > 2 || ns_max > 16 * kFTiles * 8 || (F.nb == 2 && F.sz[0] == F.sz[1]))
     return cudaErrorInvalidValue; // the host keeps the dense inverses then
   const size_t big = static_cast<size_t>(kFSlots) * kFChunkCols * max_m;
-  const size_t smem = sizeof(double) * (big + static_cast<size_t>(nrow) * kFLd + nrow) + sizeof(long long) * 2 * kFCols +
-                      sizeof(unsigned long long) * 2 * kFSlots + sizeof(int) * nrow;
+  const size_t smem = sizeof(double) * (big + static_cast<size_t>(nrow) * kFLd + (max_nt + 1) / 2 * 2) +
+                      sizeof(long long) * 2 * kFCols + sizeof(unsigned long long) * 2 * kFSlots +
+                      sizeof(int) * max_nt;
   if (smem > 227 * 1024)
     return cudaErrorInvalidValue;
   const int group = kFCols;

@@ -169,8 +169,14 @@ vm_cp_async8(double *dst, const double *src)
 #ifndef STMG_VM_MINB1
 #define STMG_VM_MINB1 8 // r = 1: 128 registers (C4 residual 1.96 -> 1.50 ms; 96 and 80 registers spill)
 #endif
+#ifndef STMG_VM_MINB2
+#define STMG_VM_MINB2 3 // r = 2: 168 registers, 12 warps per SM
+#endif
+#ifndef STMG_VM_CARRYIN
+#define STMG_VM_CARRYIN 1 // the cell-row carry enters the next row's tile at its start (C2 vmult 2.56 -> 2.51 ms)
+#endif
 template <int R, int S, bool RESID, bool RAW>
-__global__ void __launch_bounds__(32 * S, R == 2 ? 3 : (R == 1 ? STMG_VM_MINB1 : 1))
+__global__ void __launch_bounds__(32 * S, R == 2 ? STMG_VM_MINB2 : (R == 1 ? STMG_VM_MINB1 : 1))
 vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
              double *__restrict__ y, const double *__restrict__ xprev0, int rows_per_seg, int coupled)
 {
@@ -376,6 +382,17 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
 #pragma unroll
       for (int m = 0; m < NPM; ++m)
         Yp[m] = 0.0;
+#if STMG_VM_CARRYIN
+      // the row below's (pre-assembly) top node row enters the bottom node
+      // row here, so the carry is not live during the contractions
+      if (cy > cy_first)
+#pragma unroll
+        for (int i = 0; i < N1; ++i)
+          {
+            Yx[i][0] = carx[i];
+            Yy[i][0] = cary[i];
+          }
+#endif
 
       if (active)
         {
@@ -555,6 +572,14 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
         }
 
       // ---- assemble shared nodes: x across lanes, y through the carry
+#if STMG_VM_CARRYIN
+#pragma unroll
+      for (int i = 0; i < N1; ++i)
+        {
+          carx[i] = Yx[i][N1 - 1];
+          cary[i] = Yy[i][N1 - 1];
+        }
+#endif
 #pragma unroll
       for (int j = 0; j < N1; ++j)
         {
@@ -566,6 +591,7 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
               Yy[0][j] += ly;
             }
         }
+#if !STMG_VM_CARRYIN
       if (cy > cy_first)
 #pragma unroll
         for (int i = 0; i < N1; ++i)
@@ -579,6 +605,7 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
           carx[i] = Yx[i][N1 - 1];
           cary[i] = Yy[i][N1 - 1];
         }
+#endif
 
       // ---- write owned outputs
       if (owner && cy >= cy_begin)
