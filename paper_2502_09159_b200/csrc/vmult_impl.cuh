@@ -102,9 +102,16 @@ struct RowStage
   static constexpr int VWB = (VW + 3 + 1) / 2 * 2;
   static constexpr int NBUFB = (2 * S + 2) * VWB;
   static constexpr int PB = (32 * NPM + 3 + 1) / 2 * 2;
-  static constexpr int DEPTH = 4; // bulk ring: node rows issued DEPTH - 1 rows ahead
+#ifndef STMG_VM_BULK_LAG
+#define STMG_VM_BULK_LAG 0 // 0: block barrier per node row; L >= 1: per-buffer empty mbarriers, refill L rows behind
+#endif
+#ifndef STMG_VM_BULK_DEPTH
+#define STMG_VM_BULK_DEPTH (STMG_VM_BULK_LAG ? 5 : 4)
+#endif
+  static constexpr int DEPTH = STMG_VM_BULK_DEPTH; // bulk ring: node rows issued up to DEPTH - 1 rows ahead
+  static constexpr int LAG = STMG_VM_BULK_LAG;
   static constexpr size_t kBytesBulk =
-    sizeof(double) * (DEPTH * NBUFB + 2 * S * PB) + DEPTH * sizeof(unsigned long long);
+    sizeof(double) * (DEPTH * NBUFB + 2 * S * PB) + 2 * DEPTH * sizeof(unsigned long long);
   // Measured per instantiation (C2 r = 2 and C4 r = 1 on the B200): cp.async
   // staging wins for r = 1 plain applications (C4 vmult 1.66 -> 1.26 ms) and
   // loses for r = 2 (2.63 -> 2.80 ms) and for residuals (their late b loads
@@ -250,7 +257,10 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
       if (threadIdx.x == 0)
         {
           for (int q = 0; q < RING; ++q)
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(vm_smem_u32(vm_bar + q)));
+            {
+              asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(vm_smem_u32(vm_bar + q)));
+              asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(vm_smem_u32(vm_bar + RING + q)), "r"(S));
+            }
           asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
       __syncthreads();
@@ -342,10 +352,37 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
                          " @!p bra VMW_%=;\n}\n" ::"r"(vm_smem_u32(vm_bar + s0 % RING)),
                          "r"((s0 / RING) & 1)
                          : "memory");
-            __syncthreads(); // everybody is past row s0 - 1: its buffer takes row s0 + RING - 1
-            const int s = s0 + RING - 1, cyn = cy_first + s / N1;
-            if (cyn < cy_end)
-              stage_row(cyn, s % N1, s % RING);
+            if constexpr (RS::LAG == 0)
+              {
+                __syncthreads(); // everybody is past row s0 - 1: its buffer takes row s0 + RING - 1
+                const int s = s0 + RING - 1, cyn = cy_first + s / N1;
+                if (cyn < cy_end)
+                  stage_row(cyn, s % N1, s % RING);
+              }
+            else
+              {
+                // no block barrier: a warp releases row s0 - 1 on that buffer's
+                // empty mbarrier (one arrival per warp); the issuing warp refills
+                // the buffer of row s0 - LAG once all warps have released it, so
+                // the warps of a block drift up to LAG rows apart
+                if (s0 > 0)
+                  {
+                    __syncwarp();
+                    if (lane == 0)
+                      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
+                                     vm_smem_u32(vm_bar + RING + (s0 - 1) % RING))
+                                   : "memory");
+                  }
+                const int sr = s0 - RS::LAG, s = sr + RING, cyn = cy_first + s / N1;
+                if (threadIdx.x < 32 && sr >= 0 && cyn < cy_end)
+                  {
+                    asm volatile("{\n .reg .pred p;\n VME_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                                 " @!p bra VME_%=;\n}\n" ::"r"(vm_smem_u32(vm_bar + RING + sr % RING)),
+                                 "r"((sr / RING) & 1)
+                                 : "memory");
+                    stage_row(cyn, s % N1, s % RING);
+                  }
+              }
             return;
           }
         else
@@ -362,7 +399,7 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
     {
       if constexpr (kBulk)
         {
-          for (int s = 0; s < RING - 1; ++s)
+          for (int s = 0; s < (RS::LAG ? RING : RING - 1); ++s)
             if (cy_first + s / N1 < cy_end)
               stage_row(cy_first + s / N1, s % N1, s);
         }
