@@ -182,6 +182,9 @@ vm_cp_async8(double *dst, const double *src)
 #ifndef STMG_VM_CARRYIN
 #define STMG_VM_CARRYIN 1 // the cell-row carry enters the next row's tile at its start (C2 vmult 2.56 -> 2.51 ms)
 #endif
+#ifndef STMG_VM_BINIT
+#define STMG_VM_BINIT 0 // 1: residual tile starts at -b (loads issued with the row's x loads): spills at the 168-register cap, C2 residual 2.96 -> 3.51 ms
+#endif
 template <int R, int S, bool RESID, bool RAW>
 __global__ void __launch_bounds__(32 * S, R == 2 ? STMG_VM_MINB2 : (R == 1 ? STMG_VM_MINB1 : 1))
 vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
@@ -431,6 +434,33 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
           }
 #endif
 
+      if constexpr (RESID && STMG_VM_BINIT)
+        {
+          // r = b - A x as -( -b + A x ): b of the nodes this cell writes enters
+          // the accumulators here, so its loads are in flight with the x loads
+          // of the first node row instead of stalling the write-out
+          if (owner && cy >= cy_begin)
+            {
+              const int ixmax = (cx == P.nx - 1) ? p : p - 1;
+              const int iymax = (cy == P.ny - 1) ? p : p - 1;
+              const long long obase = n * isz + a * mv;
+#pragma unroll
+              for (int j = 0; j < N1; ++j)
+#pragma unroll
+                for (int i = 0; i < N1; ++i)
+                  if (i <= ixmax && j <= iymax)
+                    {
+                      const long long node = static_cast<long long>(cy * p + j) * gx + cx * p + i;
+                      Yx[i][j] -= __ldg(b + obase + node);
+                      Yy[i][j] -= __ldg(b + obase + nsc + node);
+                    }
+              const long long pbase = n * isz + S * mv + a * mp + (static_cast<long long>(cy) * P.nx + cx) * NPM;
+#pragma unroll
+              for (int m = 0; m < NPM; ++m)
+                Yp[m] = -__ldg(b + pbase + m);
+            }
+        }
+
       if (active)
         {
           const long long cell = static_cast<long long>(cy) * P.nx + cx;
@@ -665,9 +695,361 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
                   const int X = cx * p + i;
                   const long long node = static_cast<long long>(Y) * gx + X;
                   double vx = Yx[i][j], vy = Yy[i][j];
+                  if constexpr (RESID && STMG_VM_BINIT)
+                    {
+                      vx = -vx;
+                      vy = -vy;
+                      if (!RAW && (yb || X == 0 || X == gx - 1))
+                        {
+                          vx = __ldg(b + obase + node) - __ldg(x + obase + node);
+                          vy = __ldg(b + obase + nsc + node) - __ldg(x + obase + nsc + node);
+                        }
+                    }
+                  else
+                    {
+                      if (!RAW && (yb || X == 0 || X == gx - 1))
+                        {
+                          // identity rows on constrained velocity dofs (st_operator.cpp:383-394)
+                          vx = __ldg(x + obase + node);
+                          vy = __ldg(x + obase + nsc + node);
+                        }
+                      if (RESID)
+                        {
+                          vx = __ldg(b + obase + node) - vx;
+                          vy = __ldg(b + obase + nsc + node) - vy;
+                        }
+                    }
+                  y[obase + node] = vx;
+                  y[obase + nsc + node] = vy;
+                }
+            }
+          const long long pbase = n * isz + S * mv + a * mp + (static_cast<long long>(cy) * P.nx + cx) * NPM;
+#pragma unroll
+          for (int m = 0; m < NPM; ++m)
+            y[pbase + m] = RESID ? (STMG_VM_BINIT ? -Yp[m] : __ldg(b + pbase + m) - Yp[m]) : Yp[m];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// r = 2 (Q3/P2disc) with a LANE PAIR per cell. The full-tile kernel above
+// holds two 4x4 output tiles per thread and spills at the 168-register cap
+// (ptxas: 184 bytes of stack). Here lane h of a pair owns the output columns
+// i = {0, 1} (h = 0) or {3, 2} (h = 1): lane 1 works on the cell mirrored in
+// x, so by the reflection symmetry of the 1D factors (M1, K1 even; C1 odd;
+// Lm / Lc even or odd by Legendre degree) both lanes use the SAME
+// compile-time coefficients and differ only in the sign sgn = +-1 of the odd
+// ones. A lane loads and time-combines its own two node columns and
+// receives the partner's two with shuffles; the x-contraction and the
+// y-accumulation split cleanly by output column; the divergence rows are
+// summed over a lane's own node columns and completed across the pair once
+// per cell row. Strip = 15 owned cells + 1 halo cell per warp.
+#ifndef STMG_VM_HALF
+#define STMG_VM_HALF 0 // measured on C2: 3.06 ms (160 registers, no spills) vs 2.50 ms full tile: the pair doubles the per-thread overheads (addressing, pressure, shuffles)
+#endif
+#ifndef STMG_VM_HALF_MINB
+#define STMG_VM_HALF_MINB 5
+#endif
+constexpr int kHStrip = 15;
+
+template <int S, bool RESID, bool RAW>
+__global__ void __launch_bounds__(32 * S, STMG_VM_HALF_MINB)
+vmult2h_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
+               double *__restrict__ y, const double *__restrict__ xprev0, int rows_per_seg, int coupled)
+{
+  constexpr int R = 2, N1 = 4, p = 3, NPM = 6, PL = 3, H = 2;
+  const int lane = threadIdx.x & 31;
+  const int a = threadIdx.x >> 5; // output slot
+  const int n = blockIdx.z;       // interval
+  const int c = lane >> 1, h = lane & 1;
+  const int cx = blockIdx.x * kHStrip - 1 + c;
+  const bool active = cx >= 0 && cx < P.nx;
+  const bool owner = c >= 1 && active;
+  const double sgn = h ? -1.0 : 1.0;
+
+  const long long isz = P.isz, mv = P.mv, mp = P.mp, nsc = P.nsc;
+  const int gx = P.gx, gy = P.gy;
+  const double *__restrict__ xn = x + n * isz;
+  const double *__restrict__ vprev = nullptr;
+  if (coupled)
+    vprev = n > 0 ? x + (n - 1) * isz + (S - 1) * mv : xprev0;
+
+  double kt[S], mt[S], lva = 0.0;
+#pragma unroll
+  for (int bs = 0; bs < S; ++bs)
+    kt[bs] = mt[bs] = 0.0;
+#pragma unroll
+  for (int aa = 0; aa < S; ++aa)
+    if (a == aa)
+      {
+#pragma unroll
+        for (int bs = 0; bs < S; ++bs)
+          {
+            kt[bs] = P.KtJ[aa * S + bs];
+            mt[bs] = P.MtJ[aa * S + bs];
+          }
+        lva = P.lvJ[aa];
+      }
+  const double sg_l = sgn * P.sg;
+  // reflection signs of the Legendre moments:
+  // Lc(a, 3-k) = (-1)^(a+1) Lc(a, k), Lm(a, 3-k) = (-1)^a Lm(a, k)
+  const double scx_e = sgn * P.scx, scy_o = sgn * P.scy; // even-degree Lc, odd-degree Lm
+
+  const int cy_begin = blockIdx.y * rows_per_seg;
+  const int cy_end = min(P.ny, cy_begin + rows_per_seg);
+  const int cy_first = max(cy_begin - 1, 0);
+  // own node columns: local kk = 0, 1 are the cell's columns ko[0], ko[1]
+  const int ko0 = h ? 3 : 0, ko1 = h ? 2 : 1;
+
+  double carx[H], cary[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i)
+    carx[i] = cary[i] = 0.0;
+
+  for (int cy = cy_first; cy < cy_end; ++cy)
+    {
+      double Yx[H][N1], Yy[H][N1], Yp[NPM];
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+#pragma unroll
+        for (int j = 0; j < N1; ++j)
+          Yx[i][j] = Yy[i][j] = 0.0;
+#pragma unroll
+      for (int m = 0; m < NPM; ++m)
+        Yp[m] = 0.0;
+      if (cy > cy_first)
+#pragma unroll
+        for (int i = 0; i < H; ++i)
+          {
+            Yx[i][0] = carx[i];
+            Yy[i][0] = cary[i];
+          }
+
+      if (active)
+        {
+          // ---- pressure: PM = sum_b Mt(a,b) p^b (both lanes of the pair), B^T init of the tiles
+          const long long cell = static_cast<long long>(cy) * P.nx + cx;
+          double PM[NPM], PMs[NPM];
+#pragma unroll
+          for (int m = 0; m < NPM; ++m)
+            PM[m] = 0.0;
+#pragma unroll
+          for (int bs = 0; bs < S; ++bs)
+            {
+              const double cc = mt[bs];
+              const double *pp = xn + S * mv + bs * mp + cell * NPM;
+#pragma unroll
+              for (int m = 0; m < NPM; ++m)
+                PM[m] = fma(cc, __ldg(pp + m), PM[m]);
+            }
+#pragma unroll
+          for (int m = 0; m < NPM; ++m)
+            PMs[m] = sgn * PM[m];
+#pragma unroll
+          for (int bb = 0; bb < PL; ++bb)
+            {
+              double Qx[H], Qy[H];
+#pragma unroll
+              for (int i = 0; i < H; ++i)
+                Qx[i] = Qy[i] = 0.0;
+#pragma unroll
+              for (int m = 0; m < NPM; ++m)
+                {
+                  if (pdisc_mode_ay(R, m) != bb)
+                    continue;
+                  const int am = pdisc_mode_ax(R, m);
+                  const double pc = (am & 1) ? PM[m] : PMs[m]; // Lc: even degree is odd under reflection
+                  const double pm = (am & 1) ? PMs[m] : PM[m]; // Lm: odd degree is odd under reflection
+#pragma unroll
+                  for (int i = 0; i < H; ++i)
+                    {
+                      Qx[i] = fma(VM_LC(am, i), pc, Qx[i]);
+                      Qy[i] = fma(VM_LM(am, i), pm, Qy[i]);
+                    }
+                }
+#pragma unroll
+              for (int i = 0; i < H; ++i)
+                {
+                  Qx[i] *= P.scx;
+                  Qy[i] *= P.scy;
+                }
+#pragma unroll
+              for (int i = 0; i < H; ++i)
+#pragma unroll
+                for (int j = 0; j < N1; ++j)
+                  {
+                    Yx[i][j] = fma(-Qx[i], VM_LM(bb, j), Yx[i][j]);
+                    Yy[i][j] = fma(-Qy[i], VM_LC(bb, j), Yy[i][j]);
+                  }
+            }
+        }
+
+      // ---- velocity rows of the cell
+#pragma unroll
+      for (int l = 0; l < N1; ++l)
+        {
+          double UKx[N1], UMx[N1], UKy[N1], UMy[N1];
+#pragma unroll
+          for (int k = 0; k < N1; ++k)
+            UKx[k] = UMx[k] = UKy[k] = UMy[k] = 0.0;
+          if (active)
+            {
+              const int Y = cy * p + l;
+              const bool yb = (Y == 0) || (Y == gy - 1);
+              const long long rowbase = static_cast<long long>(Y) * gx + cx * p;
+#pragma unroll
+              for (int kk = 0; kk < H; ++kk)
+                {
+                  const int k = kk == 0 ? ko0 : ko1;
+                  const int X = cx * p + k;
+                  const bool bnd = !RAW && (yb || X == 0 || X == gx - 1);
+                  const long long node = rowbase + k;
+                  double ukx = 0.0, umx = 0.0, uky = 0.0, umy = 0.0;
+#pragma unroll
+                  for (int bs = 0; bs < S; ++bs)
+                    {
+                      const double vx = bnd ? 0.0 : __ldg(xn + bs * mv + node);
+                      const double vy = bnd ? 0.0 : __ldg(xn + bs * mv + nsc + node);
+                      ukx = fma(kt[bs], vx, ukx);
+                      umx = fma(mt[bs], vx, umx);
+                      uky = fma(kt[bs], vy, uky);
+                      umy = fma(mt[bs], vy, umy);
+                    }
+                  if (vprev != nullptr)
+                    {
+                      ukx = fma(-lva, __ldg(vprev + node), ukx);
+                      uky = fma(-lva, __ldg(vprev + nsc + node), uky);
+                    }
+                  UKx[kk] = ukx;
+                  UMx[kk] = umx;
+                  UKy[kk] = uky;
+                  UMy[kk] = umy;
+                }
+            }
+          // the partner's node columns: its local 1, 0 are this lane's local 2, 3
+          UKx[2] = __shfl_xor_sync(0xffffffffu, UKx[1], 1);
+          UKx[3] = __shfl_xor_sync(0xffffffffu, UKx[0], 1);
+          UMx[2] = __shfl_xor_sync(0xffffffffu, UMx[1], 1);
+          UMx[3] = __shfl_xor_sync(0xffffffffu, UMx[0], 1);
+          UKy[2] = __shfl_xor_sync(0xffffffffu, UKy[1], 1);
+          UKy[3] = __shfl_xor_sync(0xffffffffu, UKy[0], 1);
+          UMy[2] = __shfl_xor_sync(0xffffffffu, UMy[1], 1);
+          UMy[3] = __shfl_xor_sync(0xffffffffu, UMy[0], 1);
+          if (active)
+            {
+              double UMxa[N1], UMyb[N1];
+#pragma unroll
+              for (int k = 0; k < N1; ++k)
+                {
+                  UMxa[k] = P.sax * UMx[k];
+                  UMyb[k] = P.say * UMy[k];
+                }
+#pragma unroll
+              for (int i = 0; i < H; ++i)
+                {
+                  double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0;
+#pragma unroll
+                  for (int k = 0; k < N1; ++k)
+                    {
+                      s0 = fma(VM_M(i, k), UKx[k], s0);
+                      s0 = fma(VM_K(i, k), UMxa[k], s0);
+                      s1 = fma(VM_M(i, k), UMx[k], s1);
+                      s2 = fma(VM_C(i, k), UMy[k], s2);
+                      s3 = fma(VM_M(i, k), UKy[k], s3);
+                      s3 = fma(VM_K(i, k), UMyb[k], s3);
+                      s4 = fma(VM_M(i, k), UMy[k], s4);
+                      s5 = fma(VM_C(k, i), UMx[k], s5);
+                    }
+                  s1 *= P.sbx;
+                  s2 *= sg_l; // C1 is odd under the reflection
+                  s4 *= P.sby;
+                  s5 *= sg_l;
+#pragma unroll
+                  for (int j = 0; j < N1; ++j)
+                    {
+                      double vx = Yx[i][j], vy = Yy[i][j];
+                      vx = fma(VM_M(j, l), s0, vx);
+                      vx = fma(VM_K(j, l), s1, vx);
+                      vx = fma(VM_C(l, j), s2, vx);
+                      vy = fma(VM_M(j, l), s3, vy);
+                      vy = fma(VM_K(j, l), s4, vy);
+                      vy = fma(VM_C(j, l), s5, vy);
+                      Yx[i][j] = vx;
+                      Yy[i][j] = vy;
+                    }
+                }
+              // divergence rows over this lane's own node columns (local 0, 1)
+              double dp[PL], ep[PL];
+#pragma unroll
+              for (int aa = 0; aa < PL; ++aa)
+                {
+                  double s0 = 0, s1 = 0;
+#pragma unroll
+                  for (int k = 0; k < H; ++k)
+                    {
+                      s0 = fma(VM_LC(aa, k), UMx[k], s0);
+                      s1 = fma(VM_LM(aa, k), UMy[k], s1);
+                    }
+                  dp[aa] = s0 * ((aa & 1) ? P.scx : scx_e);
+                  ep[aa] = s1 * ((aa & 1) ? scy_o : P.scy);
+                }
+#pragma unroll
+              for (int m = 0; m < NPM; ++m)
+                {
+                  const int am = pdisc_mode_ax(R, m), bm = pdisc_mode_ay(R, m);
+                  Yp[m] = fma(VM_LM(bm, l), dp[am], Yp[m]);
+                  Yp[m] = fma(VM_LC(bm, l), ep[am], Yp[m]);
+                }
+            }
+        }
+
+      // ---- assemble: pair halves of the divergence, shared nodes in x across cells, y through the carry
+#pragma unroll
+      for (int m = 0; m < NPM; ++m)
+        Yp[m] += __shfl_xor_sync(0xffffffffu, Yp[m], 1);
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+        {
+          carx[i] = Yx[i][N1 - 1];
+          cary[i] = Yy[i][N1 - 1];
+        }
+#pragma unroll
+      for (int j = 0; j < N1; ++j)
+        {
+          // local column 0 is the cell's column 3 on odd lanes, column 0 on even lanes
+          const double lx = __shfl_up_sync(0xffffffffu, Yx[0][j], 1);
+          const double ly = __shfl_up_sync(0xffffffffu, Yy[0][j], 1);
+          if (h == 0 && lane > 0)
+            {
+              Yx[0][j] += lx;
+              Yy[0][j] += ly;
+            }
+        }
+
+      // ---- write owned outputs
+      if (owner && cy >= cy_begin)
+        {
+          const bool lastx = cx == P.nx - 1;
+          const int iymax = (cy == P.ny - 1) ? p : p - 1;
+          const long long obase = n * isz + a * mv;
+#pragma unroll
+          for (int j = 0; j < N1; ++j)
+            {
+              if (j > iymax)
+                continue;
+              const int Y = cy * p + j;
+              const bool yb = (Y == 0) || (Y == gy - 1);
+#pragma unroll
+              for (int i = 0; i < H; ++i)
+                {
+                  // even lane: columns 0, 1; odd lane: column 2, and 3 on the last cell column
+                  if (i == 0 && h == 1 && !lastx)
+                    continue;
+                  const int X = cx * p + (i == 0 ? ko0 : ko1);
+                  const long long node = static_cast<long long>(Y) * gx + X;
+                  double vx = Yx[i][j], vy = Yy[i][j];
                   if (!RAW && (yb || X == 0 || X == gx - 1))
                     {
-                      // identity rows on constrained velocity dofs (st_operator.cpp:383-394)
                       vx = __ldg(x + obase + node);
                       vy = __ldg(x + obase + nsc + node);
                     }
@@ -683,7 +1065,8 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
           const long long pbase = n * isz + S * mv + a * mp + (static_cast<long long>(cy) * P.nx + cx) * NPM;
 #pragma unroll
           for (int m = 0; m < NPM; ++m)
-            y[pbase + m] = RESID ? __ldg(b + pbase + m) - Yp[m] : Yp[m];
+            if ((m < NPM / 2) == (h == 0))
+              y[pbase + m] = RESID ? __ldg(b + pbase + m) - Yp[m] : Yp[m];
         }
     }
 }
@@ -693,7 +1076,8 @@ cudaError_t
 launch_rs(const LevelConsts &P, const double *x, const double *b, double *y, int n_intervals, const double *xprev0,
           int coupled, int mode, cudaStream_t stream)
 {
-  const int strips = (P.nx + kStrip - 1) / kStrip;
+  constexpr bool kHalf = R == 2 && STMG_VM_HALF != 0;
+  const int strips = kHalf ? (P.nx + kHStrip - 1) / kHStrip : (P.nx + kStrip - 1) / kStrip;
   // Row segments: enough blocks to fill 148 SMs several times, >= 8 rows
   // each so the recomputed halo row stays small -- down to 2 rows on small
   // grids, where the march length (latency) matters more than the halo row.
@@ -712,6 +1096,16 @@ launch_rs(const LevelConsts &P, const double *x, const double *b, double *y, int
   };
   constexpr size_t st_plain = RowStage<R, S>::template bytes<false>(),
                    st_resid = RowStage<R, S>::template bytes<true>();
+  if constexpr (kHalf)
+    {
+      switch (mode)
+        {
+          case 0: vmult2h_kernel<S, false, false><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
+          case 1: vmult2h_kernel<S, true, false><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
+          default: vmult2h_kernel<S, false, true><<<grid, block, 0, stream>>>(P, x, b, y, xprev0, rows, coupled); break;
+        }
+      return cudaGetLastError();
+    }
   switch (mode)
     {
       case 0: go(vmult_kernel<R, S, false, false>, st_plain); break;
