@@ -714,27 +714,7 @@ def main():
         e2e = {"value": world * dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * (3 * dofs + 2 * mv),
                "d2h_bytes_per_step": 8 * 2 * dofs}
 
-    slab = c3slab = c5hyb = None
-    if not args.no_solve:
-        try:  # a side leg: a failure is reported in the line, never fatal for the headline
-            slab = slab_solve_leg(stmg, ctx, torch, dist, world, rank)
-        except Exception as exc:
-            slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-        try:
-            c3slab = c3_slab_leg(stmg, torch, dist, world, rank)
-        except Exception as exc:
-            c3slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-        if world >= 4 and world % 2 == 0:  # >= 2 time slabs: <= 64 intervals (~100 GB) per rank
-            try:
-                c5hyb = c5_hybrid_leg(stmg, torch, dist, world, rank)
-            except Exception as exc:
-                c5hyb = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
+    line = None
     hbm, fp64, dmma, peak_src = peaks()
     ncell = nx * nx
     vm_ms = statistics.mean(t_vmult)
@@ -785,6 +765,44 @@ def main():
                            "vanka_step_dofs_per_s": world * dofs / ((rs_ms + vk_ms) * 1e-3)},
             "kernels": kernels, "roofline": roof, "gpu_launches": gpu_launches,
             "clocks": clk.summary(), "e2e": e2e}
+    # ---- collective side legs (every rank takes part). With several ranks they
+    # run under a deadline: a rank that raised while its peers wait in a
+    # collective would otherwise hang the job and lose the headline line.
+    watchdog = None
+    if world > 1 and not args.no_solve:
+        deadline = float(os.environ.get("STMG_BENCH_SIDE_TIMEOUT", "900"))
+
+        def give_up():
+            if rank == 0:
+                line["solve"] = {"error": f"multi-rank side legs exceeded {deadline:.0f} s; headline only"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        watchdog = threading.Timer(deadline, give_up)
+        watchdog.daemon = True
+        watchdog.start()
+    slab = c3slab = c5hyb = None
+    if not args.no_solve:
+        try:  # a side leg: a failure is reported in the line, never fatal for the headline
+            slab = slab_solve_leg(stmg, ctx, torch, dist, world, rank)
+        except Exception as exc:
+            slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        try:
+            c3slab = c3_slab_leg(stmg, torch, dist, world, rank)
+        except Exception as exc:
+            c3slab = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        if world >= 4 and world % 2 == 0:  # >= 2 time slabs: <= 64 intervals (~100 GB) per rank
+            try:
+                c5hyb = c5_hybrid_leg(stmg, torch, dist, world, rank)
+            except Exception as exc:
+                c5hyb = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+    if watchdog is not None:
+        watchdog.cancel()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if not args.no_solve:
         def side(fn):
             try:

@@ -223,12 +223,15 @@ vanka_dmma_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *_
           for (int tw = 0; tw < TPW; ++tw)
             {
               const int arow = row0 + 8 * (warp + tw * NW) + (lane >> 2);
+              // unpredicated clamped loads first (all in flight), mask after
+              const double *ap = pc.inverse + (arow < nt ? arow : 0) * nt;
 #pragma unroll
               for (int kk = 0; kk < KS; ++kk)
-                {
-                  const int col = 4 * kk + (lane & 3);
-                  afr[tw][kk] = (arow < nt && col < nt) ? __ldg(pc.inverse + arow * nt + col) : 0.0;
-                }
+                afr[tw][kk] = __ldg(ap + min(4 * kk + (lane & 3), nt - 1));
+#pragma unroll
+              for (int kk = 0; kk < KS; ++kk)
+                if (!(arow < nt && 4 * kk + (lane & 3) < nt))
+                  afr[tw][kk] = 0.0;
             }
 #pragma unroll
           for (int q = 0; q < kDPer; ++q)

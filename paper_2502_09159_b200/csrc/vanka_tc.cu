@@ -54,7 +54,18 @@ constexpr int kTRing = 3; // ring slots of the full/empty mbarrier pipeline (van
 #define STMG_DFR_RING 3 // measured: 4 slots 4.66 vs 4.56 ms (the larger ring takes L1 from the gathers)
 #endif
 constexpr int kDRing = STMG_DFR_RING; // vanka_dfr_kernel: ring slots; tiles gathered kDRing - 1 ahead
-constexpr size_t kDSmem = sizeof(double) * kDRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * 12) +
+// vanka_dfr_kernel B fragments by 128-bit loads: the rows of an R tile are
+// stored permuted inside every group of 8 (row 8j + 4h + t at 8j + 2t + h), so
+// the B values of lane t for the k-steps 2j and 2j + 1 are adjacent and one
+// LDS.128 feeds two k-steps (half the shared-memory instructions of the DMMA
+// loop); pitch 136 == 8 mod 16 doubles keeps the quarter-warp phases of the
+// 128-bit loads conflict-free.
+#ifndef STMG_DFR_LDS128
+#define STMG_DFR_LDS128 0 // measured: 4.96 vs 4.55 ms on C2 (bv[] costs 8 registers: 132 bytes of spills at the 128-register cap)
+#endif
+constexpr int kDLd = STMG_DFR_LDS128 ? kTRows + 8 : kTLd;
+constexpr int kDSlot = kTCols * kDLd;
+constexpr size_t kDSmem = sizeof(double) * kDRing * kDSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * 12) +
                           (2 * kDRing + 2) * sizeof(unsigned long long); // vanka_dfr_kernel
 constexpr size_t kTSmem =
   sizeof(double) * kTRing * kTSlot + kTMaxTiles * (sizeof(VankaTile) + kTCols * (16 + 4)) + 8 * sizeof(unsigned long long);
@@ -362,7 +373,7 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
                  double omega)
 {
   extern __shared__ __align__(16) double ring[];
-  long long *s_colv = reinterpret_cast<long long *>(ring + kDRing * kTSlot);
+  long long *s_colv = reinterpret_cast<long long *>(ring + kDRing * kDSlot);
   int *s_dp = reinterpret_cast<int *>(s_colv + kTMaxTiles * kTCols);
   VankaTile *s_tile = reinterpret_cast<VankaTile *>(s_dp + kTMaxTiles * kTCols);
   unsigned long long *s_bar = reinterpret_cast<unsigned long long *>(s_tile + kTMaxTiles);
@@ -415,7 +426,11 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
           }
         cls_issue = tl.cls;
       }
-    double *slot = ring + s * kTSlot + lane;
+#if STMG_DFR_LDS128
+    double *slot = ring + s * kDSlot + ((lane & ~7) | ((lane & 3) << 1) | ((lane >> 2) & 1));
+#else
+    double *slot = ring + s * kDSlot + lane;
+#endif
 #pragma unroll
     for (int cc = 0; cc < CN; ++cc)
       {
@@ -429,7 +444,7 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
         for (int q = 0; q < QN; ++q)
           {
             const bool ok = colok && relq[q] != kMaskedRow;
-            cp_async8z(slot + col * kTLd + 32 * q, pv + (ok ? relq[q] + (dp & pmq[q]) : 0), ok);
+            cp_async8z(slot + col * kDLd + 32 * q, pv + (ok ? relq[q] + (dp & pmq[q]) : 0), ok);
           }
       }
   };
@@ -511,20 +526,37 @@ vanka_dfr_kernel(const DevPatchClass *__restrict__ classes, const VankaTile *__r
       const bool mine = tl.ncols > 0 && 8 * warp < nt_loaded;
       if (mine)
         {
-          const double *bbase = ring + slot * kTSlot + (lane >> 2) * kTLd + (lane & 3);
+#if STMG_DFR_LDS128
+          const double *bbase = ring + slot * kDSlot + (lane >> 2) * kDLd + 2 * (lane & 3);
+#else
+          const double *bbase = ring + slot * kDSlot + (lane >> 2) * kDLd + (lane & 3);
+#endif
           // the previous tile's scatters ride in k-steps kS0.. of this tile
 #ifndef STMG_DFR_SC0
 #define STMG_DFR_SC0 4
 #endif
           constexpr int kSc = 2 * (kTCols / 8), kS0 = KS >= STMG_DFR_SC0 + kSc ? STMG_DFR_SC0 : 0;
+#if STMG_DFR_LDS128
+          double2 bv[kTCols / 8];
+#endif
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk)
             {
+              constexpr int kNStep = 8 * kDLd;
+#if STMG_DFR_LDS128
+              if ((kk & 1) == 0)
+#pragma unroll
+                for (int ct = 0; ct < kTCols / 8; ++ct)
+                  bv[ct] = *reinterpret_cast<const double2 *>(bbase + 4 * kk + kNStep * ct);
+#pragma unroll
+              for (int ct = 0; ct < kTCols / 8; ++ct)
+                dmma(acc[ct], afr[kk], (kk & 1) ? bv[ct].y : bv[ct].x);
+#else
               const double *brow = bbase + 4 * kk;
-              constexpr int kNStep = 8 * kTLd;
 #pragma unroll
               for (int ct = 0; ct < kTCols / 8; ++ct)
                 dmma(acc[ct], afr[kk], brow[kNStep * ct]);
+#endif
               if (kk == kS0 && p_lt >= 0)
                 phase_wait();
               if (kk >= kS0 && kk - kS0 < kSc && p_lt >= 0)
@@ -664,7 +696,11 @@ vanka_dfr176_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch 
             const int dp = s_dp[ci];
 #pragma unroll
             for (int q = 0; q < QN; ++q)
-              if (lane + 32 * q < k3Ld)
+              if (lane + 32 * q < k3Ld
+#ifdef STMG_V176_HALFGATHER_DIAG // timing only (wrong results): each CTA gathers its own half of the rows
+                  && (lane + 32 * q) / k3Half == static_cast<int>(blockIdx.z)
+#endif
+              )
                 {
                   const bool ok = colok && relq[q] != kMaskedRow;
                   cp_async8z(slot + col * k3Ld + 32 * q, pv + (ok ? relq[q] + (dp & pmq[q]) : 0), ok);
@@ -682,12 +718,19 @@ vanka_dfr176_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch 
   double afr[k3KS];
   {
     const double wrow = c_ok ? omega * pc.weight[row] : 0.0;
+    // unpredicated loads from clamped addresses, then the mask and the weight:
+    // the predicated form came out of ptxas fully serialised (one L2 round
+    // trip per load, 20 % of this kernel's stall samples in ncu); measured
+    // C3 update 18.7 -> 19.9 TF/s. (In vanka_dfr_kernel the predicated loads
+    // already issue in groups of 7 and this form costs registers: C4 9.73 ->
+    // 9.99 ms, so it keeps them.)
+    const double *arow = pc.inverse + (c_ok ? row : 0) * nt;
 #pragma unroll
     for (int kk = 0; kk < k3KS; ++kk)
-      {
-        const int col = 4 * kk + (lane & 3);
-        afr[kk] = (c_ok && col < nt) ? wrow * __ldg(pc.inverse + row * nt + col) : 0.0;
-      }
+      afr[kk] = __ldg(arow + min(4 * kk + (lane & 3), nt - 1));
+#pragma unroll
+    for (int kk = 0; kk < k3KS; ++kk)
+      afr[kk] = (c_ok && 4 * kk + (lane & 3) < nt) ? wrow * afr[kk] : 0.0;
   }
   const int c_pm = (c_ok && row >= nvel) ? -1 : 0;
   double *const c_ub = u + (c_ok ? pc.rel[row] : 0);
