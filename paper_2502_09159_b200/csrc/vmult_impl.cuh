@@ -182,6 +182,9 @@ vm_cp_async8(double *dst, const double *src)
 #ifndef STMG_VM_CARRYIN
 #define STMG_VM_CARRYIN 1 // the cell-row carry enters the next row's tile at its start (C2 vmult 2.56 -> 2.51 ms)
 #endif
+#ifndef STMG_VM_PF
+#define STMG_VM_PF 0 // 1: L1 prefetch (prefetch.global.L1) of the next node row, one line per lane; 2: also the next cell row's pressure. Measured slower: C2 vmult 2.51 -> 2.81 (1) / 2.96 ms (2)
+#endif
 #ifndef STMG_VM_BINIT
 #define STMG_VM_BINIT 0 // 1: residual tile starts at -b (loads issued with the row's x loads): spills at the 168-register cap, C2 residual 2.96 -> 3.51 ms
 #endif
@@ -529,6 +532,40 @@ vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__
           if (l > 0)
             stage_sync(cy, l);
           const double *sb = vm_smem + (((cy - cy_first) * N1 + l) % RING) * NB;
+          if constexpr (!kStaged && STMG_VM_PF != 0)
+            {
+              // L1 prefetch of the NEXT node row of the strip (all input slots,
+              // both components, the previous interval's velocity), one 128-byte
+              // line per lane: ncu puts a third of the stall samples on the first
+              // use of a row's loads (L2 latency at 11 warps per SM)
+              const int Yn = cy * p + l + 1;
+              constexpr int kLines = (32 * p + 1 + 15) / 16 + 1;
+              if (lane < kLines && Yn < gy && (l < N1 - 1 || cy + 1 < cy_end))
+                {
+                  const int Xc = min(max(X0 + 16 * lane, 0), gx - 1);
+                  const long long off = static_cast<long long>(Yn) * gx + Xc;
+#pragma unroll
+                  for (int bs = 0; bs < S; ++bs)
+                    {
+                      asm volatile("prefetch.global.L1 [%0];\n" ::"l"(xn + bs * mv + off));
+                      asm volatile("prefetch.global.L1 [%0];\n" ::"l"(xn + bs * mv + nsc + off));
+                    }
+                  if (vprev != nullptr)
+                    {
+                      asm volatile("prefetch.global.L1 [%0];\n" ::"l"(vprev + off));
+                      asm volatile("prefetch.global.L1 [%0];\n" ::"l"(vprev + nsc + off));
+                    }
+                }
+              if (STMG_VM_PF > 1 && l == 1 && cy + 1 < cy_end)
+                {
+                  constexpr int kPLines = (32 * NPM + 15) / 16 + 1;
+                  const long long c0 = (static_cast<long long>(cy + 1) * P.nx + max(cx0, 0)) * NPM + 16 * lane;
+                  if (lane < kPLines && c0 < mp)
+#pragma unroll
+                    for (int bs = 0; bs < S; ++bs)
+                      asm volatile("prefetch.global.L1 [%0];\n" ::"l"(xn + S * mv + bs * mp + c0));
+                }
+            }
           if (active)
             {
               const int Y = cy * p + l;
