@@ -1064,18 +1064,31 @@ launch_vanka_tc(const DevPatchClass *classes, const VankaTile *tiles, const long
   };
   if (variant == 1)
     {
-      if (ks <= 8)
+      // exact k-step counts of the cell patches the hierarchies meet
+      // (n_T = 21, 38, 42, 76: Q2/P1 x DG(0), Q3/P2 x DG(0), Q2/P1 x DG(1),
+      // Q3/P2 x DG(1)), so no zero k-steps are multiplied
+      if (ks <= 6)
+        gd(vanka_dfr_kernel<6>);
+      else if (ks <= 8)
         gd(vanka_dfr_kernel<8>);
+      else if (ks <= 10)
+        gd(vanka_dfr_kernel<10>);
+      else if (ks <= 11)
+        gd(vanka_dfr_kernel<11>);
       else if (ks <= 12)
         gd(vanka_dfr_kernel<12>);
       else if (ks <= 16)
         gd(vanka_dfr_kernel<16>);
+      else if (ks <= 19)
+        gd(vanka_dfr_kernel<19>);
       else if (ks <= 20)
         gd(vanka_dfr_kernel<20>);
       else if (ks <= 24)
         gd(vanka_dfr_kernel<24>);
       else if (ks <= 29)
         gd(vanka_dfr_kernel<29>);
+      else if (ks <= 31) // vertex stars of Q2/P1disc x DG(1): n_T = 124
+        gd(vanka_dfr_kernel<31>);
       else
         gd(vanka_dfr_kernel<32>);
       return cudaGetLastError();
