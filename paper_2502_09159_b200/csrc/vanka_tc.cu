@@ -627,6 +627,7 @@ constexpr int k3Ld = k3Rows + 4; // == 4 mod 16 doubles: conflict-free B fragmen
 constexpr int k3Slot = kTCols * k3Ld;
 constexpr int k3MaxCols = 32 * 16; // columns (patch, interval) per block
 
+template <int KS> // k-steps of 4: 43 for n_T <= 172 (C3: n_T = 170), else 44
 __global__ void __launch_bounds__(k3Threads, 1)
 vanka_dfr176_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
                     const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
@@ -715,7 +716,7 @@ vanka_dfr176_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch 
   // this warp's 8 rows of the inverse, weight and omega folded in
   const int row = row0 + 8 * warp + (lane >> 2);
   const bool c_ok = row < nt;
-  double afr[k3KS];
+  double afr[KS];
   {
     const double wrow = c_ok ? omega * pc.weight[row] : 0.0;
     // unpredicated loads from clamped addresses, then the mask and the weight:
@@ -726,10 +727,10 @@ vanka_dfr176_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch 
     // 9.99 ms, so it keeps them.)
     const double *arow = pc.inverse + (c_ok ? row : 0) * nt;
 #pragma unroll
-    for (int kk = 0; kk < k3KS; ++kk)
+    for (int kk = 0; kk < KS; ++kk)
       afr[kk] = __ldg(arow + min(4 * kk + (lane & 3), nt - 1));
 #pragma unroll
-    for (int kk = 0; kk < k3KS; ++kk)
+    for (int kk = 0; kk < KS; ++kk)
       afr[kk] = (c_ok && 4 * kk + (lane & 3) < nt) ? wrow * afr[kk] : 0.0;
   }
   const int c_pm = (c_ok && row >= nvel) ? -1 : 0;
@@ -756,7 +757,7 @@ vanka_dfr176_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch 
         {
           const double *bbase = ring + slot * k3Slot + (lane >> 2) * k3Ld + (lane & 3);
 #pragma unroll
-          for (int kk = 0; kk < k3KS; ++kk)
+          for (int kk = 0; kk < KS; ++kk)
             {
               const double *brow = bbase + 4 * kk;
 #pragma unroll
@@ -1120,10 +1121,16 @@ launch_vanka_dfr176(const DevPatchClass *classes, const VankaBatch *batches, int
   if (max_nt > k3Rows || group * vanka_cols_per_batch() > k3MaxCols)
     return cudaErrorInvalidValue;
   const size_t smem = sizeof(double) * kTRing * k3Slot + k3MaxCols * 12 + 6 * sizeof(unsigned long long);
-  cudaFuncSetAttribute(vanka_dfr176_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   dim3 grid(n_batches, (n_intervals + group - 1) / group, 2);
-  vanka_dfr176_kernel<<<grid, k3Threads, smem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz,
-                                                          n_intervals, omega, group);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, k3Threads, smem, stream>>>(classes, batches, vel_anchor, pre_anchor, r, u, isz, n_intervals, omega,
+                                            group);
+  };
+  if (max_nt <= 4 * (k3KS - 1))
+    go(vanka_dfr176_kernel<k3KS - 1>);
+  else
+    go(vanka_dfr176_kernel<k3KS>);
   return cudaGetLastError();
 }
 
