@@ -188,8 +188,13 @@ vm_cp_async8(double *dst, const double *src)
 #ifndef STMG_VM_BINIT
 #define STMG_VM_BINIT 0 // 1: residual tile starts at -b (loads issued with the row's x loads): spills at the 168-register cap, C2 residual 2.96 -> 3.51 ms
 #endif
+#ifdef STMG_VM_MAXNREG // experiment: an explicit register target instead of the launch bounds
+#define STMG_VM_BOUNDS __maxnreg__(STMG_VM_MAXNREG)
+#else
+#define STMG_VM_BOUNDS __launch_bounds__(32 * S, R == 2 ? STMG_VM_MINB2 : (R == 1 ? STMG_VM_MINB1 : 1))
+#endif
 template <int R, int S, bool RESID, bool RAW>
-__global__ void __launch_bounds__(32 * S, R == 2 ? STMG_VM_MINB2 : (R == 1 ? STMG_VM_MINB1 : 1))
+__global__ void STMG_VM_BOUNDS
 vmult_kernel(const LevelConsts P, const double *__restrict__ x, const double *__restrict__ b,
              double *__restrict__ y, const double *__restrict__ xprev0, int rows_per_seg, int coupled)
 {
