@@ -330,7 +330,11 @@ int stmg3_level_sizes(const stmg3_level *level, int64_t *out);
  * R_T S R_T^T and batched Gauss-Jordan inverses on the device), 2 if they were
  * built there in the time-diagonalised form (DG(2): one real and one
  * complex-pair block per cell), out[2] 1 if the undeformed class inverses
- * stand in (affine_patches), out[3] classes. */
+ * stand in (affine_patches), out[3] classes; for the time-diagonalised form
+ * out[4] = doubles one sweep streams from HBM per interval group (the real
+ * block and the u-columns [P; Q] of the pair block of every patch), out[5] =
+ * its multiply-adds per (patch, interval) column summed over the patches;
+ * both 0 otherwise. out must hold 6 doubles. */
 int stmg3_level_patch_info(const stmg3_level *level, double *out);
 /* apply_block / apply_block_raw (st_operator.cpp:397-407) per interval. */
 int stmg3_apply_block(stmg3_level *level, const double *x, double *y, int n_intervals, int raw);

@@ -577,10 +577,10 @@ class Level3:
     def patch_setup(self) -> dict:
         """Vanka patch setup: seconds, on_gpu (exact per-cell inverses built on the device),
         factored (time-diagonalised blocks), affine, classes."""
-        out = (ctypes.c_double * 4)()
+        out = (ctypes.c_double * 6)()
         _check(load_library().stmg3_level_patch_info(self._h, out))
         return dict(seconds=out[0], on_gpu=out[1] >= 1, factored=out[1] == 2, affine=bool(out[2]),
-                    classes=int(out[3]))
+                    classes=int(out[3]), streamed_elements=int(out[4]), macs_per_column=int(out[5]))
 
     def apply_block(self, x, y, n_intervals: int = 1, raw: bool = False):
         _check(load_library().stmg3_apply_block(self._h, self._v(x, n_intervals, "x"), self._v(y, n_intervals, "y"),

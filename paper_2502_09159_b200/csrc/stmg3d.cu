@@ -95,6 +95,10 @@ struct stmg3_level
   int max_nt = 0, n_classes = 0;
   bool affine_patches = false;
   std::uint64_t total_matrix_elements = 0;
+  // time-diagonalised blocks: doubles the apply kernel streams per sweep (the
+  // real block and the u-columns [P; Q] of the pair block) and its
+  // multiply-adds per (patch, interval) column
+  std::uint64_t fac_streamed_elements = 0, fac_macs = 0;
   DevArray<double> work, zeros;
   // z-split level (stmg3_solver_create_split): normalisations of the
   // projections over the whole mesh (the sums are reduced over the parts)
@@ -296,10 +300,12 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
             }
         }
       std::vector<long long> foff;
+      std::uint64_t fac_streamed = 0, fac_macs = 0;
       if (fac)
         {
           // matrices 2c, 2c + 1: the blocks of cell c (sizes sz_b * n_s)
           std::vector<int> msz(2 * nc, 0);
+          fac_streamed = fac_macs = 0;
           foff.assign(2 * nc + 1, 0);
           int max_m = 0;
           for (long long c = 0; c < nc; ++c)
@@ -307,6 +313,9 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
               {
                 const int m = b < F.nb ? F.sz[b] * (lo.nt[c] / F.S) : 0;
                 msz[2 * c + b] = m;
+                // n_s columns of m rows each: all of a real block, the u-columns of a pair block
+                fac_streamed += static_cast<std::uint64_t>(m) * (lo.nt[c] / F.S);
+                fac_macs += static_cast<std::uint64_t>(m) * m;
                 // even (16-byte aligned) starts: the apply kernel bulk-copies chunks
                 foff[2 * c + b + 1] = foff[2 * c + b] + (static_cast<long long>(m) * m + 8 + 1) / 2 * 2;
                 max_m = std::max(max_m, m);
@@ -358,6 +367,8 @@ build_level3(stmg3_level &L, const std::vector<double> *verts_host, bool affine_
           L.gpu_patches = gpu_done = true;
           L.fac3 = fac;
           L.fac3p = F;
+          L.fac_streamed_elements = fac ? fac_streamed : 0;
+          L.fac_macs = fac ? fac_macs : 0;
         }
       else
         {
@@ -1139,6 +1150,8 @@ stmg3_level_patch_info(const stmg3_level *L, double *out)
     out[1] = L->gpu_patches ? (L->fac3 ? 2.0 : 1.0) : 0.0;
     out[2] = L->affine_patches ? 1.0 : 0.0;
     out[3] = static_cast<double>(L->n_classes);
+    out[4] = static_cast<double>(L->fac_streamed_elements);
+    out[5] = static_cast<double>(L->fac_macs);
   });
 }
 

@@ -201,19 +201,44 @@ def run_c5_solve(torch, stmg, args):
     rr = seeded(torch, slab * f.size, 777)
     uu = torch.zeros_like(rr)
     sweep_ms = timed(torch, lambda: f.vanka_update(rr, uu, 0.8, slab), 3)
-    blk_bytes = 8.0 * f.total_matrix_elements  # the fine level's stored patch blocks, read once per sweep
-    peak = None
+    # Roofline of the sweep. Bytes: what the kernel streams from HBM per sweep
+    # (time-diagonalised form: the real block and the u-columns [P; Q] of the
+    # pair block of every patch, 3 n_s^2 of the 5 n_s^2 stored doubles; dense
+    # form: the whole inverse) plus 24 B per dof (read r, read-modify-write u).
+    # Flops: 2 x multiply-adds per (patch, interval) column x intervals.
+    ps = f.patch_setup
+    stored_bytes = 8.0 * f.total_matrix_elements
+    streamed_bytes = 8.0 * ps["streamed_elements"] if ps["factored"] else stored_bytes
+    macs = ps["macs_per_column"] if ps["factored"] else f.total_matrix_elements
+    groups = (slab + 15) // 16  # the blocks are streamed once per group of <= 16 intervals
+    alg_bytes = streamed_bytes * groups + 24.0 * slab * f.size
+    flops = 2.0 * macs * slab
+    hbm = dmma = None
     try:
         import json
         from pathlib import Path
-        peak = float(json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        root = Path(__file__).resolve().parents[1]
+        hbm = float(json.loads((root / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
     except Exception:
         pass
-    sweep = {"ms": sweep_ms, "intervals": slab, "patch_block_bytes": blk_bytes,
-             "achieved_GBs": blk_bytes / sweep_ms / 1e6,
-             "hbm_frac": (blk_bytes / sweep_ms / 1e6) / peak if peak else None,
+    try:
+        import json
+        from pathlib import Path
+        root = Path(__file__).resolve().parents[1]
+        dmma = float(json.loads((root / "profiles" / "fp64_peaks_r01.json").read_text())["dmma_tflops"])
+    except Exception:
+        pass
+    gbs, tfs = alg_bytes / sweep_ms / 1e6, flops / sweep_ms / 1e9
+    sweep = {"ms": sweep_ms, "intervals": slab, "stored_patch_block_bytes": stored_bytes,
+             "streamed_patch_block_bytes": streamed_bytes * groups, "algorithmic_bytes": alg_bytes,
+             "algorithmic_flops": flops, "achieved_GBs": gbs, "achieved_TFLOPs": tfs,
+             "hbm_frac": gbs / hbm if hbm else None, "dmma_frac": tfs / dmma if dmma else None,
              "kernel": "vanka_big_fac_kernel (time-diagonalised blocks, cp.async.bulk chunk ring)"
-             if f.patch_setup["factored"] else "vanka_big_kernel (dense inverses)"}
+             if ps["factored"] else "vanka_big_kernel (dense inverses)"}
+    if hbm and dmma:
+        t_hbm, t_mma = alg_bytes / (hbm * 1e9), flops / (dmma * 1e12)
+        sweep["bound"] = "tensor" if t_mma >= t_hbm else "hbm"
+        sweep["frac"] = max(t_hbm, t_mma) / (sweep_ms * 1e-3)
     del rr, uu
     return {"dofs": N * f.size, "seconds": s, "dofs_per_s": N * f.size / s, "setup_s": setup,
             "fine_vanka_sweep": sweep,
