@@ -12,7 +12,10 @@ times.
 * the smoother step S(b, u) = u + omega P (b - A u) (vanka.cpp:217-233) is
   linear in (b, u): S(b1 + b2, u1 + u2) = S(b1, u1) + S(b2, u2), <= 1e-10
   (BASELINE's smoother tolerance), and b = A u is a fixed point;
-* the Vanka sweep is bitwise reproducible (2D and the 3D colour sweeps).
+* the Vanka sweep is bitwise reproducible (2D and the 3D colour sweeps);
+* solve round trips: the FGMRES + hp-STMG solutions of C3 (all 64 intervals), of one C4 slab and of
+  one C5 macro step satisfy ||F - A X|| <= 1e-8 ||F|| through the operator; the C3 V-cycle is
+  linear and its restriction is the transpose of its prolongation.
 
 The smoother parts run on the slab sizes the solves use (C4: 8 intervals,
 C5: 16 intervals with the exact per-cell patch blocks, 49 GB).
@@ -118,3 +121,119 @@ def test_full_size_smoother_properties(stmg, ctx, name, dim, nc, r, k, N, kind, 
     ref = us.clone()
     lvl.smooth_step(bs, us, omega, Ns, hs, coupled=True)
     assert _rel(us, ref) <= 1e-10, (name, "fixed point")
+
+
+def _consistent2(sol, F, n):
+    """Constrained velocity rows zero, per-slot pressure mean zero (dof_space.cpp:62-68, 110-119)."""
+    lv = sol.finest
+    gx, gy = lv.grid_x, lv.n_scalar // lv.grid_x
+    Fv = F.view(n, lv.size)
+    r = sol.level_info[-1]["r"]
+    npc = (r + 1) * (r + 2) // 2
+    for a in range(lv.n_slots):
+        for c in range(2):
+            base = a * lv.n_velocity + c * lv.n_scalar
+            g = Fv[:, base: base + lv.n_scalar].view(n, gy, gx)
+            g[:, 0, :] = 0
+            g[:, -1, :] = 0
+            g[:, :, 0] = 0
+            g[:, :, -1] = 0
+        pb = lv.n_slots * lv.n_velocity + a * lv.n_pressure
+        p = Fv[:, pb: pb + lv.n_pressure].view(n, -1, npc)
+        p[:, :, 0] -= p[:, :, 0].mean(dim=1, keepdim=True)
+    return F
+
+
+def _consistent3(lvl, F, n):
+    gx, gy, gz = lvl.gx, lvl.gy, lvl.gz
+    bnd = torch.zeros((gz, gy, gx), dtype=torch.bool, device="cuda")
+    bnd[0] = bnd[-1] = True
+    bnd[:, 0] = bnd[:, -1] = True
+    bnd[:, :, 0] = bnd[:, :, -1] = True
+    bnd = bnd.reshape(-1)
+    V = F.view(n, lvl.size)
+    for a in range(lvl.n_slots):
+        for c in range(3):
+            base = a * lvl.n_velocity + c * lvl.n_scalar
+            V[:, base:base + lvl.n_scalar][:, bnd] = 0.0
+        p0 = lvl.n_slots * lvl.n_velocity + a * lvl.n_pressure
+        P = V[:, p0:p0 + lvl.n_pressure].view(n, -1, lvl.n_p)
+        P[:, :, 0] -= P[:, :, 0].mean(dim=1, keepdim=True)
+    return F
+
+
+def test_full_size_c3_solve_round_trip(stmg, ctx):
+    """BASELINE configs[2] at full size (32^3 x 64 intervals, 1.2e8 dofs), the hierarchy the bench
+    runs: the all-at-once FGMRES + hp-STMG V(2,2) solution put back through the operator gives the
+    load vector (true relative residual <= 1e-8, the solve's tolerance, solver.cpp:110-117); the
+    all-at-once V-cycle is linear; restriction is the transpose of prolongation on the finest pair."""
+    n, N = 32, 64
+    sol = stmg.Solver3(ctx, n, n, n, 1, 1, 1.0 / N, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=1, nu1=2, nu2=2,
+                       rtol=1e-8, max_iterations=60)
+    f = sol.finest
+    F = _consistent3(f, _rand(N * f.size, 21), N)
+    X = torch.zeros_like(F)
+    its, _ = sol.solve_all_at_once(F, X, N)
+    assert 1 <= its <= 12, its  # 8 on the bench
+    R = torch.empty_like(F)
+    f.residual(F, X, R, N, None, coupled=True)
+    assert float(R.norm() / F.norm()) <= 1.05e-8
+    # V-cycle linearity
+    F2 = _consistent3(f, _rand(N * f.size, 22), N)
+    Y1, Y2, Y12 = torch.zeros_like(F), torch.zeros_like(F), torch.zeros_like(F)
+    sol.vcycle_all_at_once(F, Y1, N)
+    sol.vcycle_all_at_once(F2, Y2, N)
+    sol.vcycle_all_at_once(F + F2, Y12, N)
+    assert _rel(Y12, Y1 + Y2) <= 1e-10
+    del Y1, Y2, Y12, R, X
+    # <R f, c> = <f, P c> on the finest level pair (no pressure projection: the bare transfers)
+    L = sol.n_levels - 1
+    c = sol.levels[L - 1]
+    cv = _consistent3(c, _rand(N * c.size, 23), N)  # both transfers zero the constrained rows of their output
+    Rf = torch.zeros_like(cv)
+    sol.restrict_residual(L, F2, Rf, N, project_pressure=False)
+    Pc = torch.zeros_like(F2)
+    sol.prolongate_correction(L, cv, Pc, N, project_pressure=False)
+    lhs, rhs = float(torch.dot(Rf, cv)), float(torch.dot(F2, Pc))
+    assert abs(lhs - rhs) <= 1e-11 * max(abs(lhs), abs(rhs), float(F2.norm() * Pc.norm()) * 1e-3)
+
+
+def test_full_size_c4_slab_solve_round_trip(stmg, ctx):
+    """BASELINE configs[3] mesh (1024^2, Q2/P1disc, DG(1), vertex-star Vanka), one 8-interval
+    all-at-once slab as the bench solves it (1.85e8 dofs): true relative residual <= 1e-8."""
+    slab = 8
+    sol = stmg.Solver(ctx, 10, 1, 1, n_steps=slab, t_end=slab / 64.0, nu=1.0, gamma=1.0,
+                      smoother=stmg.SMOOTHER_VERTEX_STAR, nu1=2, nu2=2, omega=0.8, rtol=1e-8)
+    f = sol.finest
+    F = _consistent2(sol, _rand(slab * f.size, 31), slab)
+    X = torch.zeros_like(F)
+    its, _ = sol.solve_all_at_once(F, X, slab)
+    assert 1 <= its <= 14, its  # 9 on the bench
+    R = torch.empty_like(F)
+    f.residual(F, X, R, slab, None, coupled=True)
+    assert float(R.norm() / F.norm()) <= 1.05e-8
+
+
+def test_full_size_c5_slab_solve_round_trip(stmg, ctx):
+    """BASELINE configs[4] discretisation at full mesh size (32^3 deformed, Q3/P2disc, DG(2)), one
+    16-interval macro step as the bench solves it (1.5e8 dofs, exact per-cell 606-row patch solves
+    in the time-diagonalised form, 49 GB of blocks): true relative residual <= 1e-8."""
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150e9:
+        pytest.skip(f"needs ~120 GB of free device memory, {free / 1e9:.0f} GB free")
+    n, N, slab = 32, 128, 16
+    sol = stmg.Solver3(ctx, n, n, n, 2, 2, 1.0 / N, 1.0, 1.0, n_hcoarse=4, time_coarsen=False, k_min=2,
+                       vertices=_c5_vertices(n), nu1=2, nu2=2, rtol=1e-8, max_iterations=40)
+    f = sol.finest
+    assert f.patch_setup["factored"] and f.patch_setup["on_gpu"]
+    F = _consistent3(f, _rand(slab * f.size, 41), slab)
+    X = torch.zeros_like(F)
+    its, _ = sol.solve_all_at_once(F, X, slab)
+    assert 1 <= its <= 14, its  # 9 on the bench
+    R = torch.empty_like(F)
+    f.residual(F, X, R, slab, None, coupled=True)
+    assert float(R.norm() / F.norm()) <= 1.05e-8
