@@ -521,7 +521,7 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 #define STMG_FAC_L2AHEAD 0 // >0: L2 prefetch of the chunk this far ahead (measured: no gain)
 #endif
 #ifndef STMG_FAC_SLOTS
-#define STMG_FAC_SLOTS 4
+#define STMG_FAC_SLOTS 3 // measured with the producer in warp 15: 2 / 3 / 4 / 5 slots 12.84 / 11.46 / 11.60 / 12.13 ms (the smaller ring leaves L1 to the gather)
 #endif
 #ifndef STMG_FAC_SWZ
 #define STMG_FAC_SWZ 0
