@@ -520,6 +520,9 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 #ifndef STMG_FAC_L2AHEAD
 #define STMG_FAC_L2AHEAD 0 // >0: L2 prefetch of the chunk this far ahead (measured: no gain)
 #endif
+#ifndef STMG_FAC_REGSCATTER
+#define STMG_FAC_REGSCATTER 1
+#endif
 #ifndef STMG_FAC_SLOTS
 #define STMG_FAC_SLOTS 3 // measured with the producer in warp 15: 2 / 3 / 4 / 5 slots 12.84 / 11.46 / 11.60 / 12.13 ms (the smaller ring leaves L1 to the gather)
 #endif
@@ -887,6 +890,58 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
               if (tid == PT)
                 issue_next(); // refills this slot -- possibly with the next patch's first chunks
             }
+#if STMG_FAC_REGSCATTER
+          // Z = (V (x) I) Y, weights and scatter straight from the accumulator
+          // fragments: a thread holds all S eigen-components of its (row, column)
+          // positions (the real block's row j and both halves of the pair
+          // block's row j), so Y never goes through shared memory and no
+          // barrier separates the stream from the scatter
+          {
+            int ir = -1, iu = -1;
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+              if (b < F.nb)
+                {
+                  if (F.sz[b] == 1)
+                    ir = F.c0[b];
+                  else
+                    iu = F.c0[b];
+                }
+#pragma unroll
+            for (int t = 0; t < kFTiles; ++t)
+              {
+                const int j = 8 * (warp + 16 * t) + (lane >> 2);
+                if (t < nt_w && j < ns)
+#pragma unroll
+                  for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                      {
+                        const int col = 8 * ct + 2 * (lane & 3) + h;
+                        if (col >= ng)
+                          continue;
+                        double y[kMaxS];
+#pragma unroll
+                        for (int i = 0; i < kMaxS; ++i)
+                          y[i] = i == ir ? accr[t][ct][h]
+                                         : (i == iu ? accp[t][0][ct][h] : (i == iu + 1 && iu >= 0 ? accp[t][1][ct][h] : 0.0));
+                        for (int a = 0; a < S; ++a)
+                          {
+                            double z = 0.0;
+#pragma unroll
+                            for (int i = 0; i < kMaxS; ++i)
+                              if (i < S)
+                                z = fma(F.V[a * S + i], y[i], z);
+                            const int row = prow(a, j);
+                            asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(u + (row < nvel ? cvb[col] : cpb[col]) +
+                                                                                 s_rel[row]),
+                                         "d"(s_w[row] * z)
+                                         : "memory");
+                          }
+                      }
+              }
+          }
+#else
           __syncthreads(); // every warp is done with T
           // Y into the T rows of its block
 #pragma unroll
@@ -940,6 +995,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
                                : "memory");
                 }
             }
+#endif
           __syncthreads(); // Ts and the column data are reused by the next patch
         }
     }
