@@ -361,6 +361,14 @@ def test_time_diagonalised_patches_match_dense(stmg, ctx, nx, ny, nz, r, n):
     finally:
         del os.environ["STMG_VANKA3_DENSE"]
     assert den.patch_setup["on_gpu"] and not den.patch_setup["factored"]
+    # the roofline bookkeeping of the bench: per patch of n_T = 3 n_s rows the factored form stores
+    # 5 n_s^2 doubles (+ alignment), streams 3 n_s^2 per sweep and does 5 n_s^2 multiply-adds per column
+    # (dense: n_T^2 = 9 n_s^2 of each); summed over the patches sum(n_T^2) = den.total_matrix_elements
+    sum_nt2 = den.total_matrix_elements
+    ps = fac.patch_setup
+    assert ps["streamed_elements"] * 3 == sum_nt2 and ps["macs_per_column"] * 9 == sum_nt2 * 5
+    assert sum_nt2 * 5 // 9 <= fac.total_matrix_elements <= sum_nt2 * 5 // 9 + 20 * nx * ny * nz
+    assert den.patch_setup["streamed_elements"] == 0
     rng = np.random.default_rng(24)
     u = rng.uniform(-1, 1, n * fac.size)
     b = rng.uniform(-1, 1, n * fac.size)
