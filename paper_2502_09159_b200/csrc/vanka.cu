@@ -523,6 +523,9 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 #ifndef STMG_FAC_REGSCATTER
 #define STMG_FAC_REGSCATTER 1
 #endif
+#ifndef STMG_FAC_CHUNKCOLS
+#define STMG_FAC_CHUNKCOLS 8 // u-columns of a pair block per ring slot (a multiple of 4)
+#endif
 #ifndef STMG_FAC_SLOTS
 #define STMG_FAC_SLOTS 3 // measured with the producer in warp 15: 2 / 3 / 4 / 5 slots 12.84 / 11.46 / 11.60 / 12.13 ms (the smaller ring leaves L1 to the gather)
 #endif
@@ -535,7 +538,14 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 // slot: measured 15.98 ms (5 slots) / 16.55 ms (4 slots) against 15.97 ms,
 // so neither the bytes in flight nor the pitch limit the block stream.
 constexpr int kFCols = 16, kFLd = STMG_FAC_SWZ ? 16 : 20, kFThreads = 512, kFSlots = STMG_FAC_SLOTS,
-              kFChunkCols = 8;
+              kFChunkCols = STMG_FAC_CHUNKCOLS;
+#ifndef STMG_FAC_REALCOLS
+#define STMG_FAC_REALCOLS (2 * STMG_FAC_CHUNKCOLS)
+#endif
+// a real-eigenvalue block has half the rows of a pair block: its chunks take
+// twice the columns, so both fill a ring slot and the real block needs half
+// the hand-offs (its chunks carry only 8 DMMAs per warp and 8 columns)
+constexpr int kFRealCols = STMG_FAC_REALCOLS;
 __device__ __forceinline__ int
 tsw(int row, int col)
 {
@@ -553,10 +563,10 @@ f_smem(const void *p)
 // nsp = n_s rounded up to 8 with zero rows, so the k-steps of a block's last
 // chunk read zeros past n_s and no DMMA operand needs a predicate (the ring
 // slots only ever hold finite inverse entries).
-__device__ __forceinline__ int
+__host__ __device__ __forceinline__ int
 f_nsp(int ns)
 {
-  return (ns + 7) & ~7;
+  return (ns + kFRealCols - 1) / kFRealCols * kFRealCols; // a real block's last chunk spans kFRealCols T rows
 }
 
 // Real-eigenvalue block: one chunk = 8 columns of B^{-1} (column-major, m
@@ -568,7 +578,7 @@ fac_real_chunk(double (&acc)[kFTiles][2][2], const double *__restrict__ A, const
                int trow, const int (&abase)[kFTiles], int lane)
 {
 #pragma unroll
-  for (int kk = 0; kk < kFChunkCols / 4; ++kk)
+  for (int kk = 0; kk < kFRealCols / 4; ++kk)
     {
       const int kr = trow + 4 * kk + (lane & 3);
       const double b0 = Ts[tsw(kr, lane >> 2)], b1 = Ts[tsw(kr, (lane >> 2) + 8)];
@@ -651,7 +661,8 @@ fac_item(const DevPatchClass &pc, const Fac3Params &F)
   for (int b = 0; b < 2; ++b)
     {
       it.m[b] = b < F.nb ? F.sz[b] * it.ns : 0;
-      it.nch[b] = b < F.nb ? (it.ns + kFChunkCols - 1) / kFChunkCols : 0; // pair: the n_s u-columns only
+      const int cc = F.sz[b] == 1 ? kFRealCols : kFChunkCols;
+      it.nch[b] = b < F.nb ? (it.ns + cc - 1) / cc : 0; // pair: the n_s u-columns only
     }
   it.moff1 = (it.m[0] * it.m[0] + 8 + 1) / 2 * 2;
   return it;
@@ -678,7 +689,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
   extern __shared__ __align__(16) double fsm[];
   const int S = F.S;
   const int nrow_max = S * f_nsp(max_nt / S);
-  const int slot_d = kFChunkCols * max_m; // doubles per ring slot
+  const int slot_d = max(kFChunkCols * max_m, kFRealCols * (max_nt / S)); // doubles per ring slot
   double *Rs = fsm;                       // the chunk ring
   double *Ts = fsm + kFSlots * slot_d;    // nrow x kFLd: T, later Y
   double *s_w = Ts + nrow_max * kFLd;     // nt
@@ -732,7 +743,8 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
       wait(empty + slot, ((p_g / kFSlots) - 1) & 1); // the consumers released the slot's previous chunk
     const int b = p_q >= p_it.nch[0] ? 1 : 0;
     const int kc = b ? p_q - p_it.nch[0] : p_q;
-    const int m = b ? p_it.m[1] : p_it.m[0], k0 = kFChunkCols * kc, k1 = min(k0 + kFChunkCols, p_it.ns);
+    const int ccols = (b ? F.sz[1] : F.sz[0]) == 1 ? kFRealCols : kFChunkCols;
+    const int m = b ? p_it.m[1] : p_it.m[0], k0 = ccols * kc, k1 = min(k0 + ccols, p_it.ns);
     const double *blk = p_it.inv + (b ? p_it.moff1 : 0);
     double *dst = Rs + slot * slot_d;
     if ((b ? F.sz[1] : F.sz[0]) == 1)
@@ -870,7 +882,8 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
               const int slot = g % kFSlots;
               wait(full + slot, (g / kFSlots) & 1);
               const int b = q < it.nch[0] ? 0 : 1, kc = b ? q - it.nch[0] : q;
-              const int trow = (b ? F.c0[1] : F.c0[0]) * nsp + kFChunkCols * kc; // T row of the chunk's first column
+              const int trow = (b ? F.c0[1] : F.c0[0]) * nsp +
+                               ((b ? F.sz[1] : F.sz[0]) == 1 ? kFRealCols : kFChunkCols) * kc; // T row of the chunk's first column
               const double *A = Rs + slot * slot_d;
               if ((b ? F.sz[1] : F.sz[0]) == 1)
                 {
@@ -1042,7 +1055,7 @@ launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, in
 {
   if (n_batches == 0 || n_intervals == 0)
     return cudaSuccess;
-  const int ns_max = max_nt / F.S, nrow = F.S * ((ns_max + 7) & ~7);
+  const int ns_max = max_nt / F.S, nrow = F.S * f_nsp(ns_max);
   int max_m = 0;
   for (int b = 0; b < F.nb; ++b)
     {
@@ -1052,7 +1065,7 @@ launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, in
     }
   if (F.nb > 2 || ns_max > 16 * kFTiles * 8 || (F.nb == 2 && F.sz[0] == F.sz[1]))
     return cudaErrorInvalidValue; // the host keeps the dense inverses then
-  const size_t big = static_cast<size_t>(kFSlots) * kFChunkCols * max_m;
+  const size_t big = static_cast<size_t>(kFSlots) * std::max(kFChunkCols * max_m, kFRealCols * ns_max);
   const size_t smem = sizeof(double) * (big + static_cast<size_t>(nrow) * kFLd + (max_nt + 1) / 2 * 2) +
                       sizeof(long long) * 2 * kFCols + sizeof(unsigned long long) * 2 * kFSlots +
                       sizeof(int) * max_nt;
