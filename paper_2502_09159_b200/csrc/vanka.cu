@@ -523,6 +523,9 @@ vanka_big_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__
 #ifndef STMG_FAC_REGSCATTER
 #define STMG_FAC_REGSCATTER 1
 #endif
+#ifndef STMG_FAC_WARP_ARRIVE
+#define STMG_FAC_WARP_ARRIVE 1
+#endif
 #ifndef STMG_FAC_CHUNKCOLS
 #define STMG_FAC_CHUNKCOLS 8 // u-columns of a pair block per ring slot (a multiple of 4)
 #endif
@@ -703,7 +706,8 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
     for (int q = 0; q < kFSlots; ++q)
       {
         asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(f_smem(full + q)));
-        asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(f_smem(empty + q)), "r"(kFThreads));
+        asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(f_smem(empty + q)),
+                     "r"(STMG_FAC_WARP_ARRIVE ? kFThreads / 32 : kFThreads));
       }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
@@ -899,7 +903,12 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
                   else if (nt_w == 1)
                     fac_pair_chunk<1>(accp, A, Ts, 2 * ns, trow, trow + nsp, abu, abv, lane);
                 }
-              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(f_smem(empty + slot)) : "memory");
+#if STMG_FAC_WARP_ARRIVE
+              // one arrival per warp (its lanes' reads of the slot are ordered before it by the warp barrier)
+              __syncwarp();
+              if (lane == 0)
+#endif
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(f_smem(empty + slot)) : "memory");
               if (tid == PT)
                 issue_next(); // refills this slot -- possibly with the next patch's first chunks
             }
