@@ -683,13 +683,15 @@ fac_pair_row(int h, int r, int nvs, int nps)
 // The chunks of all its patches form ONE stream through the ring, so the
 // TMA engine already pulls the next patch's first chunks while the warps
 // write Y, scatter and gather the next patch.
-__global__ void __launch_bounds__(kFThreads, 1)
+template <int NW> // warps per CTA: 16 (one CTA per SM) or, for patches of <= 128 spatial dofs, 8 (two per SM)
+__global__ void __launch_bounds__(NW * 32, 16 / NW)
 vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch *__restrict__ batches,
                      int n_batches, const long long *__restrict__ vel_anchor, const long long *__restrict__ pre_anchor,
                      const Fac3Params F, const double *__restrict__ r, double *__restrict__ u, long long isz,
                      int n_intervals, double omega, int group, int max_m, int max_nt)
 {
   extern __shared__ __align__(16) double fsm[];
+  constexpr int NTH = NW * 32;
   const int S = F.S;
   const int nrow_max = S * f_nsp(max_nt / S);
   const int slot_d = max(kFChunkCols * max_m, kFRealCols * (max_nt / S)); // doubles per ring slot
@@ -707,7 +709,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
       {
         asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(f_smem(full + q)));
         asm volatile("mbarrier.init.shared.b64 [%0], %1;\n" ::"r"(f_smem(empty + q)),
-                     "r"(STMG_FAC_WARP_ARRIVE ? kFThreads / 32 : kFThreads));
+                     "r"(STMG_FAC_WARP_ARRIVE ? NTH / 32 : NTH));
       }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
@@ -730,7 +732,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
   // sub-partition, the producer itself was the last to get there: C5 fine
   // sweep 12.3 -> 11.9 ms)
 #ifndef STMG_FAC_PROD
-#define STMG_FAC_PROD (kFThreads - 32)
+#define STMG_FAC_PROD (NTH - 32)
 #endif
   constexpr int PT = STMG_FAC_PROD;
   int p_bi = blockIdx.x, p_pi = 0, p_q = 0;
@@ -804,12 +806,12 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
       const int nchunks = it.nch[0] + it.nch[1];
       // this warp's row tiles (same for every block: all blocks have n_s rows
       // per half) and their stored rows, lane's chunk column folded in
-      const int rt = (ns + 7) / 8, nt_w = warp < rt ? (rt - warp + 15) / 16 : 0;
+      const int rt = (ns + 7) / 8, nt_w = warp < rt ? (rt - warp + NW - 1) / NW : 0;
       int abr[kFTiles], abu[kFTiles], abv[kFTiles];
 #pragma unroll
       for (int t = 0; t < kFTiles; ++t)
         {
-          const int row = 8 * (warp + 16 * t) + (lane >> 2);
+          const int row = 8 * (warp + NW * t) + (lane >> 2);
           abr[t] = (lane & 3) * ns + row;
           abu[t] = (lane & 3) * (2 * ns) + fac_pair_row(0, row, nvs, nps);
           abv[t] = (lane & 3) * (2 * ns) + fac_pair_row(1, row, nvs, nps);
@@ -823,7 +825,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
               cvb[tid] = tid < ng ? n * isz + __ldg(vel_anchor + patch) : 0;
               cpb[tid] = tid < ng ? n * isz + __ldg(pre_anchor + patch) : 0;
             }
-          for (int row = tid; row < nt; row += kFThreads)
+          for (int row = tid; row < nt; row += NTH)
             {
               s_rel[row] = static_cast<int>(__ldg(pc.rel + row));
               s_w[row] = omega * __ldg(pc.weight + row);
@@ -837,13 +839,13 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
           // batches of GB elements per thread: all their loads are in flight
           // before the first W-mix (one latency per batch, not per element)
           constexpr int GB = STMG_FAC_GBATCH;
-          for (int e0 = tid; e0 < nsp * kFCols; e0 += GB * kFThreads)
+          for (int e0 = tid; e0 < nsp * kFCols; e0 += GB * NTH)
             {
               double rb[GB][kMaxS];
 #pragma unroll
               for (int q = 0; q < GB; ++q)
                 {
-                  const int e = e0 + q * kFThreads;
+                  const int e = e0 + q * NTH;
                   const int c = e / nsp, j = e - c * nsp; // consecutive threads: consecutive dofs of a column
                   const bool ld = e < nsp * kFCols && j < ns && c < ng;
 #pragma unroll
@@ -856,7 +858,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
 #pragma unroll
               for (int q = 0; q < GB; ++q)
                 {
-                  const int e = e0 + q * kFThreads;
+                  const int e = e0 + q * NTH;
                   if (e >= nsp * kFCols)
                     break;
                   const int c = e / nsp, j = e - c * nsp;
@@ -932,7 +934,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
 #pragma unroll
             for (int t = 0; t < kFTiles; ++t)
               {
-                const int j = 8 * (warp + 16 * t) + (lane >> 2);
+                const int j = 8 * (warp + NW * t) + (lane >> 2);
                 if (t < nt_w && j < ns)
 #pragma unroll
                   for (int ct = 0; ct < 2; ++ct)
@@ -974,7 +976,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
 #pragma unroll
                 for (int t = 0; t < kFTiles; ++t)
                   {
-                    const int row = 8 * (warp + 16 * t) + (lane >> 2);
+                    const int row = 8 * (warp + NW * t) + (lane >> 2);
                     if (row < ns)
 #pragma unroll
                       for (int ct = 0; ct < 2; ++ct)
@@ -994,7 +996,7 @@ vanka_big_fac_kernel(const DevPatchClass *__restrict__ classes, const VankaBatch
               }
           __syncthreads();
           // Z = (V (x) I) Y, weights, scatter
-          for (int e = tid; e < ns * kFCols; e += kFThreads)
+          for (int e = tid; e < ns * kFCols; e += NTH)
             {
               const int c = e / ns, j = e - c * ns;
               if (c >= ng)
@@ -1081,13 +1083,31 @@ launch_vanka_big_fac(const DevPatchClass *classes, const VankaBatch *batches, in
   if (smem > 227 * 1024)
     return cudaErrorInvalidValue;
   const int group = kFCols;
-  cudaFuncSetAttribute(vanka_big_fac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  // persistent: one CTA per SM walks a strided share of the colour's batches
+  // persistent: the CTAs walk a strided share of the colour's batches. Patches of <= 128 spatial dofs
+  // (the r = 1 levels of the C5 hierarchy) run as two 8-warp CTAs per SM when their shared memory
+  // allows it, so one CTA's gather / scatter and barriers overlap the other's stream
+#ifndef STMG_FAC_SMALL_CTAS
+#define STMG_FAC_SMALL_CTAS 1
+#endif
   const int ngroups = (n_intervals + group - 1) / group;
-  const int ctas = std::max(1, std::min(n_batches, (device_sm_count() + ngroups - 1) / ngroups));
+  const bool small = STMG_FAC_SMALL_CTAS && ns_max <= 8 * kFTiles * 8 && smem <= 110 * 1024 &&
+                     static_cast<long long>(n_batches) * ngroups > device_sm_count(); // else the 16-warp CTAs are faster per patch
+  const int per_sm = small ? 2 : 1;
+  const int ctas = std::max(1, std::min(n_batches, (per_sm * device_sm_count() + ngroups - 1) / ngroups));
   dim3 grid(ctas, ngroups);
-  vanka_big_fac_kernel<<<grid, kFThreads, smem, st>>>(classes, batches, n_batches, vel_anchor, pre_anchor, F, r, u,
+  if (small)
+    {
+      cudaFuncSetAttribute(vanka_big_fac_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      vanka_big_fac_kernel<8><<<grid, 256, smem, st>>>(classes, batches, n_batches, vel_anchor, pre_anchor, F, r, u,
                                                        isz, n_intervals, omega, group, max_m, max_nt);
+    }
+  else
+    {
+      cudaFuncSetAttribute(vanka_big_fac_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      vanka_big_fac_kernel<16><<<grid, kFThreads, smem, st>>>(classes, batches, n_batches, vel_anchor, pre_anchor, F,
+                                                               r, u, isz, n_intervals, omega, group, max_m, max_nt);
+    }
   return cudaGetLastError();
 }
 
