@@ -500,7 +500,10 @@ struct V3D
   static constexpr int NF = 12;
   static constexpr int CELL = NF * NNN + NP + 24 + 1 - (NF * NNN + NP + 24) % 2; // odd
   static constexpr size_t smem() { return sizeof(double) * (CW * CELL + (R + 1) * N + 2 * N); }
-  static constexpr int MINB = smem() <= 112 * 1024 ? 2 : 1;
+#ifndef STMG_V3D_MINB_R1
+#define STMG_V3D_MINB_R1 3 // 2 / 3 / 4 blocks per SM: 2.66 / 2.39 / 2.46 ms (4 spills)
+#endif
+  static constexpr int MINB = R == 1 ? STMG_V3D_MINB_R1 : (smem() <= 112 * 1024 ? 2 : 1);
 };
 
 /// Exponent d of P_r^disc mode m in 3D, in the order of modes3() (setup3d.cpp,
@@ -2081,6 +2084,19 @@ launch_rs3_chunk(const Level3Consts &P, const double *x, const double *b, double
         const dim3 block(C::THREADS);
         const unsigned grid = static_cast<unsigned>((cells + C::CW - 1) / C::CW);
         const bool def = P.verts != nullptr;
+        if (def && std::getenv("STMG_V3_R1_DEF_OLD") == nullptr)
+          { // the r >= 2 deformed kernel (no J^-1 cache, thread-local z-lines) also on deformed r = 1 levels,
+            // three blocks per SM: 32^3 x 16 intervals, DG(2): residual 3.00 -> 2.39 ms
+            using D = V3D<R>;
+            const unsigned gridd = static_cast<unsigned>((cells + D::CW - 1) / D::CW);
+            switch (mode)
+              {
+                case 0: go(vmult3_init_kernel<0>, vmult3d_kernel<R, S, 0>, dim3(D::THREADS), gridd, D::smem()); break;
+                case 1: go(vmult3_init_kernel<1>, vmult3d_kernel<R, S, 1>, dim3(D::THREADS), gridd, D::smem()); break;
+                default: go(vmult3_init_kernel<2>, vmult3d_kernel<R, S, 2>, dim3(D::THREADS), gridd, D::smem()); break;
+              }
+            return cudaGetLastError();
+          }
         switch (mode)
           {
             case 0:
